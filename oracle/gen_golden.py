@@ -1,0 +1,236 @@
+"""TEST INFRASTRUCTURE ONLY — regenerate the golden fixtures in tests/golden/.
+
+Every fixture is an OUTPUT OF THE UNMODIFIED REFERENCE (oracle/_ref/
+libspectree_ref.so, compiled from /root/reference/proj/src by oracle/Makefile)
+on seeded inputs. The fixtures travel with the repo so the GPU box (which has
+no /root/reference) can check the CUDA path against the reference itself.
+
+    python oracle/gen_golden.py          # needs /root/reference (this container)
+
+Fixtures:
+  tree_kats.npz      merge / dfs_chains / verify known-answer tests lifted from
+                     proj/tests/token_tree_test.cpp:41-266 and
+                     proj/tests/python/test_smoke.py:17-27, as reference outputs
+  tree_random.npz    200 random merges + verify walks (numpy-seeded inputs)
+  weights_toy.npz    init_random_weights (proj/src/transformer.cpp:71-114) for a
+                     toy config: full f64 tensor stream
+  decode_c1.npz      C1: 2 layers, d=256, 4 heads, V=258,
+                     128-token prompt, 16-node tree -> per-node f64 logits + tokens
+  decode_toy.npz     toy-config trees (transformer_test.cpp toy_config) incl.
+                     the paper tree and a no-causal-fix negative control
+  engine_toy.npz     run_incremental / run_speculative (perfect speculator)
+                     sequences + LLM step counts (acceptance criterion #4 shape)
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+from oracle.oracle import Reference, build  # noqa: E402
+
+GOLDEN = os.path.join(os.path.dirname(HERE), "tests", "golden")
+
+# (layers, heads, d_model, vocab, max_positions, ffn_mult)
+TOY = (2, 2, 16, 32, 64, 4)          # proj/tests/transformer_test.cpp:15-23
+C1 = (2, 4, 256, 258, 256, 4)        # BASELINE.json configs[0]; SURVEY.md §8(d)
+
+
+def _ragged(seqs):
+    lens = np.array([len(s) for s in seqs], np.int32)
+    flat = np.array([t for s in seqs for t in s], np.int32)
+    return flat, lens
+
+
+def tree_kats(R):
+    cases = {
+        "merge6": [[2, 3, 4, 5], [2, 3, 8, 9]],
+        "linear": [[7, 1, 1]],
+        "paper": [[2, 3, 4, 5], [2, 3, 6, 7], [2, 3, 8, 9]],
+        "chain4": [[4, 4, 4, 4, 4]],
+        "walk": [[0, 1, 3], [0, 2]],
+        "mismatch": [[0, 1], [0, 2]],
+        "rootonly": [[5]],
+    }
+    outputs = {
+        "merge6": [3, 4, 5, 1, 0, 0],   # test_smoke.py:26-27 -> [3, 4, 5, 1]
+        "walk": [1, 3, 7, 0],           # token_tree_test.cpp:218-228 -> [1, 3, 7]
+        "mismatch": [9, 0, 0],          # token_tree_test.cpp:229-233 -> [9]
+        "rootonly": [9],                # token_tree_test.cpp:205-209 -> [9]
+    }
+    out = {}
+    for name, seqs in cases.items():
+        flat, lens = _ragged(seqs)
+        tok, par, dep = R.merge(seqs)
+        out[f"{name}_flat"], out[f"{name}_lens"] = flat, lens
+        out[f"{name}_tok"], out[f"{name}_par"], out[f"{name}_dep"] = tok, par, dep
+        chains = R.dfs_chains(seqs)
+        out[f"{name}_chain_ids"] = np.array([i for c in chains for i in c], np.int32)
+        out[f"{name}_chain_lens"] = np.array([len(c) for c in chains], np.int32)
+        if name in outputs:
+            out[f"{name}_outputs"] = np.array(outputs[name], np.int32)
+            out[f"{name}_verified"] = R.verify(seqs, outputs[name])
+    # error KATs (token_tree_test.cpp:72-88): codes from the reference
+    errs = {}
+    for name, seqs, mx in [("root_mismatch", [[1, 2], [3, 4]], 64),
+                           ("too_large", [[1, 2, 3, 4, 5]], 3),
+                           ("empty_seq", [[1, 2], []], 64)]:
+        try:
+            R.merge(seqs, mx)
+            errs[name] = "ok"
+        except Exception as e:  # OracleError
+            errs[name] = e.code
+    out["error_names"] = np.array(list(errs.keys()))
+    out["error_codes"] = np.array(list(errs.values()))
+    return out
+
+
+def tree_random(R, n_cases=200, seed=1234):
+    rng = np.random.default_rng(seed)
+    flats, lens_all, nseq, toks, pars, deps, nn, outs, vers, vlen = ([] for _ in range(10))
+    for _ in range(n_cases):
+        vocab = int(rng.integers(3, 9))
+        k = int(rng.integers(1, 7))
+        root = int(rng.integers(0, vocab))
+        seqs = [[root] + rng.integers(0, vocab, int(rng.integers(0, 6))).tolist() for _ in range(k)]
+        tok, par, dep = R.merge(seqs, 1024)
+        o = rng.integers(0, vocab, len(tok)).astype(np.int32)
+        ver = R.verify(seqs, o, 1024)
+        f, l = _ragged(seqs)
+        flats.append(f); lens_all.append(l); nseq.append(k)
+        toks.append(tok); pars.append(par); deps.append(dep); nn.append(len(tok))
+        outs.append(o); vers.append(ver); vlen.append(len(ver))
+    cat = lambda xs: np.concatenate(xs).astype(np.int32)  # noqa: E731
+    return dict(flat=cat(flats), lens=cat(lens_all), nseq=np.array(nseq, np.int32),
+                tok=cat(toks), par=cat(pars), dep=cat(deps), n_nodes=np.array(nn, np.int32),
+                outputs=cat(outs), verified=cat(vers), n_verified=np.array(vlen, np.int32))
+
+
+def attention_tree(R, seed=99):
+    """Reference attention() (transformer.cpp:160-216) with an explicit tree mask:
+    rows [0,P) are the committed prefix (causal among themselves), rows
+    [P,P+n) the tree nodes, each seeing the whole prefix plus its ancestors.
+    Pins the restated masked tree attention (restate.c) to the reference's own
+    softmax/PV arithmetic."""
+    rng = np.random.default_rng(seed)
+    out = {}
+    seqs = [[2, 3, 4, 5], [2, 3, 6, 7], [2, 3, 8, 9, 1], [2, 7]]
+    tok, par, dep = R.merge(seqs)
+    n = len(tok)
+    P, d, heads = 6, 16, 2
+    l = P + n
+    mask = np.full((l, l), -1e30)
+    for j in range(P):
+        mask[j, : j + 1] = 0.0
+    for u in range(n):
+        mask[P + u, :P] = 0.0
+        v = u
+        while v >= 0:
+            mask[P + u, P + v] = 0.0
+            v = par[v]
+    x = rng.uniform(-1, 1, (l, d))
+    ws = [rng.uniform(-0.5, 0.5, (d, d)) for _ in range(3)]
+    wo = np.eye(d)
+    o = R.attention(x, ws[0], ws[1], ws[2], wo, heads, mask)
+    out.update(x=x, wq=ws[0], wk=ws[1], wv=ws[2], par=par, P=np.array(P), heads=np.array(heads),
+               mask=mask, out=o)
+    return out
+
+
+def random_tree_seqs(rng, root, vocab, n_seqs, max_extra):
+    return [[root] + rng.integers(0, vocab, int(rng.integers(0, max_extra + 1))).tolist()
+            for _ in range(n_seqs)]
+
+
+def exact_size_tree(R, rng, root, vocab, T, width, depth):
+    """W root-to-leaf paths, resampled until the merge has exactly T nodes."""
+    while True:
+        seqs = [[root] + rng.integers(0, vocab, depth).tolist() for _ in range(width)]
+        tok, _, _ = R.merge(seqs, 1 << 20)
+        if len(tok) == T:
+            return seqs
+        if len(tok) > T:
+            # drop tokens from the last path until the size fits
+            while len(tok) > T and len(seqs[-1]) > 1:
+                seqs[-1] = seqs[-1][:-1]
+                tok, _, _ = R.merge(seqs, 1 << 20)
+            if len(tok) == T:
+                return seqs
+
+
+def decode_fixture(R, cfg, seed, prompt, seqs, max_nodes=64, apply_fix=True):
+    logits, toks = R.tree_decode(cfg, seed, prompt, seqs, max_nodes, apply_fix)
+    tok, par, dep = R.merge(seqs, max_nodes)
+    return logits, toks, tok, par, dep
+
+
+def main():
+    build(ref=True)
+    R = Reference()
+    os.makedirs(GOLDEN, exist_ok=True)
+
+    np.savez_compressed(os.path.join(GOLDEN, "tree_kats.npz"), **tree_kats(R))
+    np.savez_compressed(os.path.join(GOLDEN, "tree_random.npz"), **tree_random(R))
+
+    np.savez_compressed(os.path.join(GOLDEN, "attention_tree.npz"), **attention_tree(R))
+
+    w = R.init_weights(TOY, 42)
+    np.savez_compressed(os.path.join(GOLDEN, "weights_toy.npz"), cfg=np.array(TOY), seed=42,
+                        weights=w)
+
+    # C1: 128-token prompt (root = prompt[-1], prefix_len 128), exactly 16 nodes.
+    rng = np.random.default_rng(2305)
+    prompt = rng.integers(0, C1[3], 128).astype(np.int32)
+    seqs = exact_size_tree(R, rng, int(prompt[-1]), C1[3], 16, 4, 4)
+    logits, toks, tok, par, dep = decode_fixture(R, C1, 42, prompt, seqs)
+    fl, ln = _ragged(seqs)
+    np.savez_compressed(os.path.join(GOLDEN, "decode_c1.npz"), cfg=np.array(C1), seed=42,
+                        prompt=prompt, flat=fl, lens=ln, tok=tok, par=par, dep=dep,
+                        logits=logits, tokens=toks)
+
+    # Toy trees: paper tree (transformer_test.cpp:359-375), random trees, and the
+    # no-causal-fix negative control (transformer_test.cpp:300-315 analogue).
+    rng = np.random.default_rng(47)
+    toy = {}
+    cases = [("paper", np.array([3, 1, 2], np.int32),
+              [[2, 3, 4, 5], [2, 3, 6, 7], [2, 3, 8, 9]], True),
+             ("linear", np.array([6, 2, 9], np.int32), [[9, 4, 8, 1]], True)]
+    for i in range(8):
+        prompt = rng.integers(0, TOY[3], int(rng.integers(3, 9))).astype(np.int32)
+        cases.append((f"rand{i}", prompt,
+                      random_tree_seqs(rng, int(prompt[-1]), TOY[3], 4, 4), True))
+    cases.append(("nofix", np.array([3, 1, 2], np.int32), [[2, 3, 4, 5], [2, 3, 6, 7]], False))
+    names = []
+    for name, prompt, seqs, fix in cases:
+        seed = 51
+        logits, toks, tok, par, dep = decode_fixture(R, TOY, seed, prompt, seqs, 64, fix)
+        fl, ln = _ragged(seqs)
+        toy.update({f"{name}_prompt": prompt, f"{name}_flat": fl, f"{name}_lens": ln,
+                    f"{name}_tok": tok, f"{name}_par": par, f"{name}_dep": dep,
+                    f"{name}_logits": logits, f"{name}_tokens": toks,
+                    f"{name}_fix": np.array(int(fix))})
+        names.append(name)
+    toy["names"] = np.array(names)
+    toy["cfg"] = np.array(TOY)
+    toy["seed"] = np.array(51)
+    np.savez_compressed(os.path.join(GOLDEN, "decode_toy.npz"), **toy)
+
+    # Engine: acceptance #4 shape (perfect speculator, b=1, d=4) on a toy model.
+    ecfg = (2, 2, 32, 64, 256, 4)   # acceptance_test.cpp:220
+    eng = {"cfg": np.array(ecfg), "seed": np.array(31)}
+    prompt = np.array([5, 9, 2, 7, 4], np.int32)
+    inc, inc_steps = R.run_incremental(ecfg, 31, prompt, 100)
+    spec, spec_steps = R.run_speculative_self(ecfg, 31, prompt, 100, 1, 4)
+    eng.update(prompt=prompt, incremental=inc, incremental_steps=np.array(inc_steps),
+               speculative=spec, speculative_steps=np.array(spec_steps))
+    np.savez_compressed(os.path.join(GOLDEN, "engine_toy.npz"), **eng)
+    print("golden fixtures written to", GOLDEN)
+    for f in sorted(os.listdir(GOLDEN)):
+        print(f"  {f}: {os.path.getsize(os.path.join(GOLDEN, f))} bytes")
+
+
+if __name__ == "__main__":
+    main()
