@@ -1,0 +1,159 @@
+/* spectree_capi.h — the C-ABI of the B200-native token-tree verification path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes,
+ * no torch or C++ types. The C++ headers in include/spectree/ (same
+ * declarations as the reference's proj/include/spectree/*.hpp) sit on top of
+ * it, and so do the Python ctypes bindings (paper_2305_09781_b200/_capi.py).
+ *
+ * Conventions
+ *   - Status: 0 = ok, otherwise 1 + spectree::Errc
+ *     (reference proj/include/spectree/error.hpp:8-25); st_last_error_message()
+ *     returns a thread-local description of the last failure.
+ *   - All tensor pointers are DEVICE pointers, caller-owned; no allocation
+ *     happens inside a launch (workspaces are caller-provided). Launches are
+ *     ordered on the given cudaStream_t (passed as void*; NULL = legacy stream).
+ *   - No CPU fallback: on a machine without a CUDA device every compute entry
+ *     point fails with ST_ERR_NO_DEVICE.
+ *   - Layouts:
+ *       q, o        [B][T][H][D]          tree-node queries / outputs
+ *       k/v cache   [B][Hkv][Lmax][D]     per layer; rows [0,P[b]) committed,
+ *                                         rows [P[b], P[b]+n[b]) = tree scratch
+ *                                         indexed by preorder node id
+ *       mask        [B][T][W] uint64      bit v of mask[b][u]: tree row v is an
+ *                                         ancestor-or-self of node u
+ *       logits      [B][T][V] float32
+ *       parent,tok  [B][T] int32          preorder (parent[u] < u, root = 0)
+ */
+#ifndef SPECTREE_CAPI_H
+#define SPECTREE_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ST_ABI_VERSION 1
+
+typedef int st_status;
+
+/* 1 + spectree::Errc (reference error.hpp:8-25), plus ABI-only codes >= 100. */
+enum {
+    ST_OK = 0,
+    ST_ERR_EMPTY_INPUT = 1,
+    ST_ERR_ROOT_MISMATCH = 2,
+    ST_ERR_UNKNOWN_NODE = 3,
+    ST_ERR_MISSING_OUTPUT = 4,
+    ST_ERR_TREE_TOO_LARGE = 5,
+    ST_ERR_TREE_TOO_DEEP = 6,
+    ST_ERR_SHAPE_MISMATCH = 7,
+    ST_ERR_PROMPT_TOO_LONG = 8,
+    ST_ERR_CACHE_GAP = 9,
+    ST_ERR_CHAIN_NOT_LINKED = 10,
+    ST_ERR_EMPTY_CONTEXT = 11,
+    ST_ERR_INVALID_ARGUMENT = 16,
+    ST_ERR_NO_DEVICE = 100,
+    ST_ERR_CUDA = 101,
+    ST_ERR_UNSUPPORTED = 102,
+};
+
+typedef enum { ST_F16 = 0, ST_BF16 = 1, ST_F32 = 2, ST_F64 = 3 } st_dtype;
+
+int st_abi_version(void);
+const char* st_last_error_message(void);
+/* Number of visible CUDA devices (0 on a CPU-only host; never fails). */
+int st_device_count(void);
+
+/* ------------------------------------------------------------------ K1 ---
+ * Tree attention: for every (request b, head h, node u < n[b]):
+ *   o[b][u][h] = softmax_{r in R(b,u)} (q[b][u][h] . k[b][h/G][r] * scale) . v[b][h/G][r]
+ *   R(b,u) = [0, P[b]) U { P[b]+v : bit v of mask[b][u] }
+ * Replaces the per-chain loop of reference transformer.cpp:394-446 over
+ * chain_attention_step_impl's attention core (transformer.cpp:270-299) with
+ * one masked pass. Masked rows contribute exactly +0 (transformer.hpp:13-16).
+ * Rows u >= n[b] of o are not written. lse (optional) = natural-log
+ * log-sum-exp [B][H][T] in float32. */
+typedef struct {
+    st_dtype dtype;           /* q/k/v/o element type */
+    int B, T, H, Hkv, D;      /* T = max nodes per request (row stride of q/o/mask) */
+    int W;                    /* mask words per node, >= ceil(T/64) */
+    int64_t Lmax;             /* cache rows per (b, kv head) */
+    const void* q;
+    const void* k_cache;
+    const void* v_cache;
+    const uint64_t* mask;
+    const int32_t* prefix_len; /* [B] committed rows P[b] (device) */
+    const int32_t* n_nodes;    /* [B] tree nodes n[b] <= T (device) */
+    void* o;
+    float* lse;                /* optional, NULL allowed */
+    double scale;              /* usually 1/sqrt(D) */
+    void* workspace;           /* st_tree_attention_workspace_size() bytes, zeroed once */
+    size_t workspace_bytes;
+    int force_path;            /* 0 auto, 1 CUDA-core, 2 tcgen05 tensor-core */
+} st_attn_args;
+
+size_t st_tree_attention_workspace_size(const st_attn_args* a);
+st_status st_tree_attention(const st_attn_args* a, void* stream);
+/* Which kernel `auto` picks for these args: 1 CUDA-core, 2 tcgen05. */
+int st_tree_attention_path(const st_attn_args* a);
+
+/* ------------------------------------------------------------------ K2 ---
+ * Append: write the tree nodes' K/V rows into the cache scratch region
+ *   cache[b][h][P[b] + u] = new[b][u][h]     for u < n[b]
+ * (the reference writes chain rows straight into cache positions,
+ * transformer.cpp:265-268). k_new/v_new: [B][T][Hkv][D]. */
+st_status st_kv_append(st_dtype dtype, int B, int T, int Hkv, int D, int64_t Lmax,
+                       const void* k_new, const void* v_new, const int32_t* prefix_len,
+                       const int32_t* n_nodes, void* k_cache, void* v_cache, void* stream);
+
+/* Compact: keep the accepted root-to-node path, in place, for n_layers layers
+ * (cache pointer of layer l = base + l * layer_stride elements):
+ *   cache[b][h][P[b] + k] = cache[b][h][P[b] + ids[b][k]]   for k < n_keep[b]
+ * then (if new_prefix_len != NULL) new_prefix_len[b] = P[b] + n_keep[b].
+ * Replaces the post-verify re-decode of reference engine.cpp:123-129. ids is
+ * [B][ids_stride], strictly increasing with ids[b][0] == 0 (the root). */
+st_status st_kv_compact(st_dtype dtype, int B, int Hkv, int D, int64_t Lmax, int n_layers,
+                        int64_t layer_stride, const int32_t* ids, int ids_stride,
+                        const int32_t* n_keep, const int32_t* prefix_len,
+                        int32_t* new_prefix_len, void* k_cache, void* v_cache, void* stream);
+
+/* ------------------------------------------------------------------ K3 ---
+ * Greedy verification: per-node argmax over logits (lowest id wins ties,
+ * reference transformer.cpp:116-122) then the Alg.-2 walk (reference
+ * token_tree.cpp:153-175). Outputs per request b:
+ *   argmax[b][u]            greedy LLM output of node u            (optional)
+ *   verified[b][0..len)     accepted tokens + bonus token
+ *   ids[b][0..len)          accepted node ids, root first (input to st_kv_compact)
+ *   len[b]
+ * Optional engine step semantics (reference engine.cpp:110-121): if budget
+ * != NULL, truncate to budget[b] tokens; then cut after the first `eos`
+ * (eos < 0 disables). The truncated length is what st_kv_compact keeps.
+ * verified/ids have row stride T+1. workspace: st_verify_workspace_size(). */
+size_t st_verify_workspace_size(int B, int T);
+st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32_t* tokens,
+                           const int32_t* parent, const int32_t* n_nodes,
+                           const int32_t* budget, int32_t eos, int32_t* argmax,
+                           int32_t* verified, int32_t* ids, int32_t* len, void* workspace,
+                           void* stream);
+
+/* ------------------------------------------------------------------ K4 ---
+ * Stochastic multi-step speculative sampling (SpecInfer MSS; NOT in the
+ * reference — contract in DESIGN.md §5). q[b][v][:] is the draft
+ * distribution of the SSM that proposed node v (row 0 unused). uniforms
+ * [B][n_uniforms] in [0,1), consumed strictly in order. */
+st_status st_verify_mss(const float* logits, const float* q, int B, int T, int V,
+                        const int32_t* tokens, const int32_t* parent, const int32_t* n_nodes,
+                        float temperature, const float* uniforms, int n_uniforms,
+                        int32_t* verified, int32_t* ids, int32_t* len, void* stream);
+
+/* --------------------------------------------------------- tree packing ---
+ * Device-side ancestor bitmask build: mask[b][u] = mask[b][parent[u]] | bit(u)
+ * (reference TokenTree::ancestors, token_tree.cpp:130-139, as a bitset). */
+st_status st_build_masks(const int32_t* parent, const int32_t* n_nodes, int B, int T, int W,
+                         uint64_t* mask, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECTREE_CAPI_H */

@@ -1,0 +1,208 @@
+"""ctypes binding of the C-ABI (include/spectree_capi.h) over torch tensors.
+
+torch is only plumbing here (device memory and streams); every computation
+goes through ``libspectree_b200.so``. There is no CPU fallback: if the library
+or a CUDA device is missing, calls raise ``SpectreeError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspectree_b200.so")
+
+# 1 + spectree::Errc (reference proj/include/spectree/error.hpp:8-25)
+ERRC = ["empty_input", "root_mismatch", "unknown_node", "missing_output", "tree_too_large",
+        "tree_too_deep", "shape_mismatch", "prompt_too_long", "cache_gap", "chain_not_linked",
+        "empty_context", "incomplete_profile", "bad_magic", "crc_mismatch", "io_error",
+        "invalid_argument"]
+EXTRA = {100: "no_device", 101: "cuda_error", 102: "unsupported"}
+
+DTYPES = {torch.float16: 0, torch.bfloat16: 1, torch.float32: 2, torch.float64: 3}
+
+
+class SpectreeError(RuntimeError):
+    """Mirror of spectree::Error: carries the Errc name in ``.code``."""
+
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        self.code = ERRC[status - 1] if 0 < status <= len(ERRC) else EXTRA.get(status, str(status))
+        super().__init__(f"[{self.code}] {msg}")
+
+
+class AttnArgs(C.Structure):
+    _fields_ = [("dtype", C.c_int), ("B", C.c_int), ("T", C.c_int), ("H", C.c_int),
+                ("Hkv", C.c_int), ("D", C.c_int), ("W", C.c_int), ("Lmax", C.c_int64),
+                ("q", C.c_void_p), ("k_cache", C.c_void_p), ("v_cache", C.c_void_p),
+                ("mask", C.c_void_p), ("prefix_len", C.c_void_p), ("n_nodes", C.c_void_p),
+                ("o", C.c_void_p), ("lse", C.c_void_p), ("scale", C.c_double),
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
+                ("force_path", C.c_int)]
+
+
+_lib = None
+
+# every exported symbol and its signature (restype, argtypes)
+_V, _I, _I64, _Z, _D, _F = C.c_void_p, C.c_int, C.c_int64, C.c_size_t, C.c_double, C.c_float
+SIGNATURES = {
+    "st_abi_version": (_I, []),
+    "st_last_error_message": (C.c_char_p, []),
+    "st_device_count": (_I, []),
+    "st_tree_attention_workspace_size": (_Z, [C.POINTER(AttnArgs)]),
+    "st_tree_attention": (_I, [C.POINTER(AttnArgs), _V]),
+    "st_tree_attention_path": (_I, [C.POINTER(AttnArgs)]),
+    "st_kv_append": (_I, [_I, _I, _I, _I, _I, _I64, _V, _V, _V, _V, _V, _V, _V]),
+    "st_kv_compact": (_I, [_I, _I, _I, _I, _I64, _I, _I64, _V, _I, _V, _V, _V, _V, _V, _V]),
+    "st_verify_workspace_size": (_Z, [_I, _I]),
+    "st_verify_greedy": (_I, [_V, _I, _I, _I, _V, _V, _V, _V, C.c_int32, _V, _V, _V, _V, _V, _V]),
+    "st_verify_mss": (_I, [_V, _V, _I, _I, _I, _V, _V, _V, _F, _V, _I, _V, _V, _V, _V]),
+    "st_build_masks": (_I, [_V, _V, _I, _I, _I, _V, _V]),
+    "st_tree_merge": (_I, [_V, _V, _I, _I, _V, _V, _V, _I, C.POINTER(_I)]),
+}
+
+
+def lib():
+    """Load libspectree_b200.so (fails loudly: no fallback exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise SpectreeError(102, f"{_LIB_PATH} missing: run __graft_entry__.build()")
+        L = C.CDLL(_LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            if hasattr(L, name):
+                fn = getattr(L, name)
+                fn.restype, fn.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != 0:
+        raise SpectreeError(status, lib().st_last_error_message().decode())
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+# ------------------------------------------------------------------ K1 ----
+def attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, lse=None, scale=None,
+              workspace=None, force_path=0):
+    B, T, H, D = q.shape
+    Hkv, Lmax = k_cache.shape[1], k_cache.shape[2]
+    a = AttnArgs()
+    a.dtype = DTYPES[q.dtype]
+    a.B, a.T, a.H, a.Hkv, a.D, a.W, a.Lmax = B, T, H, Hkv, D, mask.shape[-1], Lmax
+    a.q, a.k_cache, a.v_cache = q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr()
+    a.mask, a.prefix_len, a.n_nodes = mask.data_ptr(), prefix_len.data_ptr(), n_nodes.data_ptr()
+    a.o = out.data_ptr()
+    a.lse = lse.data_ptr() if lse is not None else None
+    a.scale = float(scale if scale is not None else D ** -0.5)
+    a.workspace = workspace.data_ptr() if workspace is not None else None
+    a.workspace_bytes = workspace.numel() if workspace is not None else 0
+    a.force_path = force_path
+    return a
+
+
+def tree_attention_workspace(q, k_cache, v_cache, mask, prefix_len, n_nodes, force_path=0):
+    out = torch.empty_like(q)
+    a = attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, force_path=force_path)
+    n = lib().st_tree_attention_workspace_size(C.byref(a))
+    return torch.zeros(max(int(n), 1), dtype=torch.uint8, device=q.device)
+
+
+def tree_attention_path(q, k_cache, v_cache, mask, prefix_len, n_nodes, force_path=0):
+    out = torch.empty_like(q)
+    a = attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, force_path=force_path)
+    return int(lib().st_tree_attention_path(C.byref(a)))
+
+
+def tree_attention(q, k_cache, v_cache, mask, prefix_len, n_nodes, out=None, lse=None,
+                   scale=None, workspace=None, force_path=0, stream=None):
+    """K1 through st_tree_attention. Shapes: q [B,T,H,D]; caches [B,Hkv,Lmax,D];
+    mask [B,T,W] int64 (uint64 bits); prefix_len/n_nodes [B] int32 (device)."""
+    if out is None:
+        out = torch.empty_like(q)
+    if workspace is None:
+        workspace = tree_attention_workspace(q, k_cache, v_cache, mask, prefix_len, n_nodes,
+                                             force_path)
+    a = attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, lse, scale, workspace,
+                  force_path)
+    check(lib().st_tree_attention(C.byref(a), _stream(stream)))
+    return out
+
+
+# ------------------------------------------------------------------ K2 ----
+def kv_append(k_new, v_new, prefix_len, n_nodes, k_cache, v_cache, stream=None):
+    B, T, Hkv, D = k_new.shape
+    check(lib().st_kv_append(DTYPES[k_new.dtype], B, T, Hkv, D, k_cache.shape[-2], _ptr(k_new),
+                             _ptr(v_new), _ptr(prefix_len), _ptr(n_nodes), _ptr(k_cache),
+                             _ptr(v_cache), _stream(stream)))
+
+
+def kv_compact(ids, n_keep, prefix_len, k_cache, v_cache, new_prefix_len=None, stream=None):
+    """k_cache/v_cache: [L,B,Hkv,Lmax,D] (layer-major) or [B,Hkv,Lmax,D]."""
+    if k_cache.dim() == 4:
+        n_layers, layer_stride = 1, k_cache.numel()
+        B, Hkv, Lmax, D = k_cache.shape
+    else:
+        n_layers = k_cache.shape[0]
+        layer_stride = k_cache[0].numel()
+        B, Hkv, Lmax, D = k_cache.shape[1:]
+    check(lib().st_kv_compact(DTYPES[k_cache.dtype], B, Hkv, D, Lmax, n_layers, layer_stride,
+                              _ptr(ids), ids.shape[-1], _ptr(n_keep), _ptr(prefix_len),
+                              _ptr(new_prefix_len), _ptr(k_cache), _ptr(v_cache),
+                              _stream(stream)))
+
+
+# ------------------------------------------------------------------ K3 ----
+def verify_workspace(B, T, device="cuda"):
+    n = lib().st_verify_workspace_size(B, T)
+    return torch.zeros(int(n), dtype=torch.uint8, device=device)
+
+
+def verify_greedy(logits, tokens, parent, n_nodes, budget=None, eos=-1, workspace=None,
+                  stream=None, want_argmax=True):
+    B, T, V = logits.shape
+    dev = logits.device
+    argmax = torch.empty((B, T), dtype=torch.int32, device=dev) if want_argmax else None
+    verified = torch.full((B, T + 1), -1, dtype=torch.int32, device=dev)
+    ids = torch.full((B, T + 1), -1, dtype=torch.int32, device=dev)
+    length = torch.zeros(B, dtype=torch.int32, device=dev)
+    if workspace is None:
+        workspace = verify_workspace(B, T, dev)
+    check(lib().st_verify_greedy(_ptr(logits), B, T, V, _ptr(tokens), _ptr(parent), _ptr(n_nodes),
+                                 _ptr(budget), int(eos), _ptr(argmax), _ptr(verified), _ptr(ids),
+                                 _ptr(length), _ptr(workspace), _stream(stream)))
+    return argmax, verified, ids, length
+
+
+# ------------------------------------------------------------------ K4 ----
+def verify_mss(logits, q, tokens, parent, n_nodes, temperature, uniforms, stream=None):
+    B, T, V = logits.shape
+    dev = logits.device
+    verified = torch.full((B, T + 1), -1, dtype=torch.int32, device=dev)
+    ids = torch.full((B, T + 1), -1, dtype=torch.int32, device=dev)
+    length = torch.zeros(B, dtype=torch.int32, device=dev)
+    check(lib().st_verify_mss(_ptr(logits), _ptr(q), B, T, V, _ptr(tokens), _ptr(parent),
+                              _ptr(n_nodes), float(temperature), _ptr(uniforms),
+                              uniforms.shape[-1], _ptr(verified), _ptr(ids), _ptr(length),
+                              _stream(stream)))
+    return verified, ids, length
+
+
+# ---------------------------------------------------------------- masks ----
+def build_masks(parent, n_nodes, W=None, stream=None):
+    B, T = parent.shape
+    W = W or (T + 63) // 64
+    mask = torch.zeros((B, T, W), dtype=torch.int64, device=parent.device)
+    check(lib().st_build_masks(_ptr(parent), _ptr(n_nodes), B, T, W, _ptr(mask), _stream(stream)))
+    return mask

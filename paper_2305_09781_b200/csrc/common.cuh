@@ -1,0 +1,81 @@
+// Shared helpers for the sm_100a kernels and the C-ABI layer.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "spectree_capi.h"
+
+namespace st {
+
+// Thread-local last error (st_last_error_message).
+void set_error(const std::string& msg);
+const std::string& last_error();
+
+// Returns ST_ERR_NO_DEVICE when no CUDA device is visible (no CPU fallback).
+st_status require_device();
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+#define ST_CHECK_ARG(cond, code, msg)                      \
+    do {                                                   \
+        if (!(cond)) {                                     \
+            ::st::set_error(std::string(__func__) + ": " + (msg)); \
+            return (code);                                 \
+        }                                                  \
+    } while (0)
+
+#define ST_CUDA_TRY(expr)                                                            \
+    do {                                                                             \
+        cudaError_t _e = (expr);                                                     \
+        if (_e != cudaSuccess) {                                                     \
+            ::st::set_error(std::string(__func__) + ": " #expr ": " + cudaGetErrorString(_e)); \
+            return ST_ERR_CUDA;                                                      \
+        }                                                                            \
+    } while (0)
+
+#define ST_LAUNCH_CHECK() ST_CUDA_TRY(cudaGetLastError())
+
+inline size_t dtype_size(st_dtype t) {
+    switch (t) {
+        case ST_F16: return 2;
+        case ST_BF16: return 2;
+        case ST_F32: return 4;
+        case ST_F64: return 8;
+    }
+    return 0;
+}
+
+// ----------------------------------------------------------- conversions ---
+template <class T> struct acc_of { using type = float; };
+template <> struct acc_of<double> { using type = double; };
+
+template <class A> __device__ __forceinline__ A to_acc(__half x) { return (A)__half2float(x); }
+template <class A> __device__ __forceinline__ A to_acc(__nv_bfloat16 x) { return (A)__bfloat162float(x); }
+template <class A> __device__ __forceinline__ A to_acc(float x) { return (A)x; }
+template <class A> __device__ __forceinline__ A to_acc(double x) { return (A)x; }
+
+template <class T> __device__ __forceinline__ T from_acc(float x);
+template <> __device__ __forceinline__ __half from_acc<__half>(float x) { return __float2half_rn(x); }
+template <> __device__ __forceinline__ __nv_bfloat16 from_acc<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+template <> __device__ __forceinline__ float from_acc<float>(float x) { return x; }
+template <> __device__ __forceinline__ double from_acc<double>(float x) { return (double)x; }
+template <class T> __device__ __forceinline__ T from_acc_d(double x);
+template <> __device__ __forceinline__ double from_acc_d<double>(double x) { return x; }
+
+}  // namespace st
+
+// Dispatch an st_dtype onto a C++ element type.
+#define ST_DISPATCH_DTYPE(DT, T, ...)                      \
+    switch (DT) {                                          \
+        case ST_F16: { using T = __half; __VA_ARGS__; break; }        \
+        case ST_BF16: { using T = __nv_bfloat16; __VA_ARGS__; break; } \
+        case ST_F32: { using T = float; __VA_ARGS__; break; }         \
+        case ST_F64: { using T = double; __VA_ARGS__; break; }        \
+        default: ::st::set_error("unknown dtype"); return ST_ERR_INVALID_ARGUMENT; \
+    }

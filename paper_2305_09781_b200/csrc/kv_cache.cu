@@ -1,0 +1,137 @@
+// K2: KV-cache append of the tree nodes' K/V and in-place compaction of the
+// accepted root-to-node path.
+//
+// Reference behaviour being replaced:
+//   * chain rows are written straight into cache positions base+i
+//     (proj/src/transformer.cpp:265-268), siblings overwriting each other;
+//   * after verify, run_speculative re-decodes every accepted token one at a
+//     time to repair the cache (proj/src/engine.cpp:123-129).
+// Here the tree's rows live at [P, P+n) indexed by preorder node id, and after
+// verification the accepted rows (root + matched path) are moved to
+// [P, P+n_keep) — one pass over 2*(n_keep)*Hkv*D elements per layer instead of
+// n_keep full forward passes.
+//
+// In-place safety: ids are strictly increasing with
+// ids[k] >= k, so copying row ids[k] -> k in increasing k never overwrites a
+// source that a LATER copy still needs; the kernel therefore walks k
+// sequentially (one barrier per row) while all threads of the block copy the
+// row's Hkv*D elements in parallel with 16-byte vectors.
+#include "common.cuh"
+
+namespace st {
+namespace {
+
+// One block per (b, u) tree row: copies Hkv rows of D elements for K and V.
+template <class V>
+__global__ void kv_append_kernel(const char* __restrict__ k_new, const char* __restrict__ v_new,
+                                 const int32_t* __restrict__ prefix_len,
+                                 const int32_t* __restrict__ n_nodes, char* __restrict__ k_cache,
+                                 char* __restrict__ v_cache, int T, int Hkv, int64_t row_bytes,
+                                 int64_t Lmax) {
+    const int b = blockIdx.y, u = blockIdx.x;
+    if (u >= n_nodes[b]) return;
+    const int64_t P = prefix_len[b];
+    const int64_t nvec = row_bytes / (int64_t)sizeof(V);
+    for (int64_t i = threadIdx.x; i < (int64_t)Hkv * nvec; i += blockDim.x) {
+        const int h = (int)(i / nvec);
+        const int64_t e = i % nvec;
+        const int64_t src = (((int64_t)b * T + u) * Hkv + h) * row_bytes;
+        const int64_t dst = (((int64_t)b * Hkv + h) * Lmax + P + u) * row_bytes;
+        reinterpret_cast<V*>(k_cache + dst)[e] = reinterpret_cast<const V*>(k_new + src)[e];
+        reinterpret_cast<V*>(v_cache + dst)[e] = reinterpret_cast<const V*>(v_new + src)[e];
+    }
+}
+
+// One block per (layer, b): rows k = 1..n_keep-1 copied sequentially.
+template <class V>
+__global__ void kv_compact_kernel(const int32_t* __restrict__ ids, int ids_stride,
+                                  const int32_t* __restrict__ n_keep,
+                                  const int32_t* __restrict__ prefix_len,
+                                  int32_t* __restrict__ new_prefix_len, char* k_cache,
+                                  char* v_cache, int Hkv, int64_t row_bytes, int64_t Lmax,
+                                  int64_t layer_stride_bytes) {
+    const int b = blockIdx.x, layer = blockIdx.y;
+    const int keep = n_keep[b];
+    const int64_t P = prefix_len[b];
+    const int32_t* idb = ids + (int64_t)b * ids_stride;
+    char* kl = k_cache + layer * layer_stride_bytes;
+    char* vl = v_cache + layer * layer_stride_bytes;
+    const int64_t nvec = row_bytes / (int64_t)sizeof(V);
+    for (int k = 1; k < keep; ++k) {
+        const int src_row = idb[k];
+        if (src_row != k) {
+            for (int64_t i = threadIdx.x; i < (int64_t)Hkv * nvec; i += blockDim.x) {
+                const int h = (int)(i / nvec);
+                const int64_t e = i % nvec;
+                const int64_t base = ((int64_t)b * Hkv + h) * Lmax;
+                const int64_t s = (base + P + src_row) * row_bytes;
+                const int64_t d = (base + P + k) * row_bytes;
+                reinterpret_cast<V*>(kl + d)[e] = reinterpret_cast<const V*>(kl + s)[e];
+                reinterpret_cast<V*>(vl + d)[e] = reinterpret_cast<const V*>(vl + s)[e];
+            }
+        }
+        __syncthreads();
+    }
+    if (new_prefix_len && layer == 0 && threadIdx.x == 0) new_prefix_len[b] = (int32_t)(P + keep);
+}
+
+}  // namespace
+}  // namespace st
+
+extern "C" {
+
+st_status st_kv_append(st_dtype dtype, int B, int T, int Hkv, int D, int64_t Lmax,
+                       const void* k_new, const void* v_new, const int32_t* prefix_len,
+                       const int32_t* n_nodes, void* k_cache, void* v_cache, void* stream) {
+    if (st_status e = st::require_device()) return e;
+    ST_CHECK_ARG(B >= 0 && T >= 1 && Hkv >= 1 && D >= 1 && Lmax >= T, ST_ERR_SHAPE_MISMATCH,
+                 "bad shape");
+    ST_CHECK_ARG(st::dtype_size(dtype) != 0, ST_ERR_INVALID_ARGUMENT, "bad dtype");
+    if (B == 0) return ST_OK;
+    ST_CHECK_ARG(k_new && v_new && prefix_len && n_nodes && k_cache && v_cache,
+                 ST_ERR_INVALID_ARGUMENT, "null pointer");
+    const int64_t row_bytes = (int64_t)D * st::dtype_size(dtype);
+    const dim3 grid(T, B);
+    auto s = st::as_stream(stream);
+    if (row_bytes % 16 == 0)
+        st::kv_append_kernel<int4><<<grid, 128, 0, s>>>((const char*)k_new, (const char*)v_new,
+                                                        prefix_len, n_nodes, (char*)k_cache,
+                                                        (char*)v_cache, T, Hkv, row_bytes, Lmax);
+    else
+        st::kv_append_kernel<char><<<grid, 128, 0, s>>>((const char*)k_new, (const char*)v_new,
+                                                        prefix_len, n_nodes, (char*)k_cache,
+                                                        (char*)v_cache, T, Hkv, row_bytes, Lmax);
+    ST_LAUNCH_CHECK();
+    return ST_OK;
+}
+
+st_status st_kv_compact(st_dtype dtype, int B, int Hkv, int D, int64_t Lmax, int n_layers,
+                        int64_t layer_stride, const int32_t* ids, int ids_stride,
+                        const int32_t* n_keep, const int32_t* prefix_len,
+                        int32_t* new_prefix_len, void* k_cache, void* v_cache, void* stream) {
+    if (st_status e = st::require_device()) return e;
+    ST_CHECK_ARG(B >= 0 && Hkv >= 1 && D >= 1 && n_layers >= 1 && ids_stride >= 1,
+                 ST_ERR_SHAPE_MISMATCH, "bad shape");
+    ST_CHECK_ARG(st::dtype_size(dtype) != 0, ST_ERR_INVALID_ARGUMENT, "bad dtype");
+    if (B == 0) return ST_OK;
+    ST_CHECK_ARG(ids && n_keep && prefix_len && k_cache && v_cache, ST_ERR_INVALID_ARGUMENT,
+                 "null pointer");
+    const int64_t es = (int64_t)st::dtype_size(dtype);
+    const int64_t row_bytes = (int64_t)D * es;
+    const dim3 grid(B, n_layers);
+    auto s = st::as_stream(stream);
+    if (row_bytes % 16 == 0)
+        st::kv_compact_kernel<int4><<<grid, 256, 0, s>>>(ids, ids_stride, n_keep, prefix_len,
+                                                         new_prefix_len, (char*)k_cache,
+                                                         (char*)v_cache, Hkv, row_bytes, Lmax,
+                                                         layer_stride * es);
+    else
+        st::kv_compact_kernel<char><<<grid, 256, 0, s>>>(ids, ids_stride, n_keep, prefix_len,
+                                                         new_prefix_len, (char*)k_cache,
+                                                         (char*)v_cache, Hkv, row_bytes, Lmax,
+                                                         layer_stride * es);
+    ST_LAUNCH_CHECK();
+    return ST_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+// K1 dispatcher: st_tree_attention (C-ABI) -> CUDA-core or tcgen05 kernel.
+//
+// Dispatch rule (north star: tensor cores "only where GQA head-grouping x
+// tree width makes them dense enough to pay"): half-precision inputs with
+// D == 128 and (H/Hkv) * T >= 16 go to the tcgen05 kernel; everything else
+// (f32/f64 parity runs, tiny trees) to the CUDA-core kernel.
+#include "common.cuh"
+#include "tree_attn.h"
+
+namespace {
+
+st_status validate(const st_attn_args* a) {
+    ST_CHECK_ARG(a != nullptr, ST_ERR_INVALID_ARGUMENT, "null args");
+    ST_CHECK_ARG(a->B >= 0 && a->T >= 1 && a->H >= 1 && a->Hkv >= 1 && a->D >= 1,
+                 ST_ERR_SHAPE_MISMATCH, "bad shape");
+    ST_CHECK_ARG(a->H % a->Hkv == 0, ST_ERR_SHAPE_MISMATCH, "H must be a multiple of Hkv");
+    ST_CHECK_ARG(a->W * 64 >= a->T, ST_ERR_SHAPE_MISMATCH, "mask words W < ceil(T/64)");
+    ST_CHECK_ARG(a->Lmax >= a->T, ST_ERR_SHAPE_MISMATCH, "cache rows Lmax < T");
+    ST_CHECK_ARG(a->B == 0 || (a->q && a->k_cache && a->v_cache && a->mask && a->prefix_len &&
+                               a->n_nodes && a->o),
+                 ST_ERR_INVALID_ARGUMENT, "null tensor pointer");
+    return ST_OK;
+}
+
+int choose_path(const st_attn_args* a) {
+    if (a->force_path == 1 || a->force_path == 2) return a->force_path;
+    const bool dense = (int64_t)(a->H / a->Hkv) * a->T >= 16;
+    return (dense && st::tree_attention_tc_supported(a)) ? 2 : 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+int st_tree_attention_path(const st_attn_args* a) {
+    if (validate(a) != ST_OK) return 0;
+    return choose_path(a);
+}
+
+size_t st_tree_attention_workspace_size(const st_attn_args* a) {
+    if (validate(a) != ST_OK) return 0;
+    return choose_path(a) == 2 ? st::tree_attention_tc_workspace(a) : 0;
+}
+
+st_status st_tree_attention(const st_attn_args* a, void* stream) {
+    if (st_status e = st::require_device()) return e;
+    if (st_status e = validate(a)) return e;
+    if (a->B == 0) return ST_OK;
+    const int path = choose_path(a);
+    if (path == 2) {
+        if (!st::tree_attention_tc_supported(a)) {
+            st::set_error("st_tree_attention: tcgen05 path needs f16/bf16, D == 128, G*T <= 128");
+            return ST_ERR_UNSUPPORTED;
+        }
+        const size_t need = st::tree_attention_tc_workspace(a);
+        if (a->workspace_bytes < need || (need && !a->workspace)) {
+            st::set_error("st_tree_attention: workspace too small");
+            return ST_ERR_INVALID_ARGUMENT;
+        }
+        return st::tree_attention_tc(a, st::as_stream(stream));
+    }
+    return st::tree_attention_cc(a, st::as_stream(stream));
+}
+
+}  // extern "C"
