@@ -1,12 +1,621 @@
-// K1 tcgen05 path — placeholder until the tensor-core kernel lands.
+// K1, tcgen05 instantiation: masked one-pass tree attention on the sm_100a
+// 5th-gen tensor cores (f16 / bf16 in, fp32 accumulate), head dim 128.
+//
+// What it computes is exactly K1 of the C-ABI (include/spectree_capi.h): for
+// every (request b, head h, tree node u) a softmax over the committed KV rows
+// [0, P[b]) plus the tree rows P[b]+v whose bit v is set in mask[b][u] — the
+// reference's per-chain loop (proj/src/transformer.cpp:394-446 over the
+// attention core :270-299) collapsed into one masked pass.
+//
+// Design:
+//   * Persistent, stream-K scheduled: grid = #SMs, one CTA per SM. The
+//     concatenation over (b, h) of each pair's 128-row KV tiles is cut into
+//     #SMs equal contiguous ranges, so every SM streams the same number of
+//     bytes whatever the per-request lengths are. A pair split across CTAs
+//     leaves partial (O, m, l) rows in the workspace and the last CTA to finish
+//     that pair merges them in fixed CTA order (deterministic; no atomics in
+//     any reduction, the ticket only elects the merger).
+//   * Warp roles (192 threads): warps 0-3 softmax/epilogue (thread r <-> query
+//     row r <-> TMEM lane r), warp 4 TMA producer, warp 5 MMA issuer.
+//   * TMA (SWIZZLE_128B) streams K and V tiles [128 rows x 128 d] through two
+//     2-stage rings; Q [128 x 128] (rows >= T zero-filled by TMA) once per pair.
+//   * S = Q K^T on tcgen05 (M=128, N=128, K=16 x 8) into a double-buffered TMEM
+//     S; softmax reads it with tcgen05.ld, applies the tree mask only on tiles
+//     that reach the tree region, writes P (bf16/f16) to smem in the UMMA
+//     K-major SW128 layout; O += P V on tcgen05 (V read MN-major) into TMEM.
+//   * Online softmax with lazy rescaling: the running max is only moved (and O
+//     in TMEM rescaled) when it grows by more than 2^8, so P stays <= 256.
+//   * Masked rows are exact zeros in P, so they contribute +0 (reference
+//     transformer.hpp:13-16) and outputs do not depend on non-ancestor rows.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cfloat>
+#include <mutex>
+#include <type_traits>
+#include <unordered_map>
+
 #include "common.cuh"
+#include "sm100.cuh"
 #include "tree_attn.h"
 
 namespace st {
-bool tree_attention_tc_supported(const st_attn_args*) { return false; }
-size_t tree_attention_tc_workspace(const st_attn_args*) { return 0; }
-st_status tree_attention_tc(const st_attn_args*, cudaStream_t) {
-    set_error("tcgen05 path not built");
-    return ST_ERR_UNSUPPORTED;
+namespace {
+
+using namespace sm100;
+
+constexpr int BM = 128;            // query rows per pair (tree nodes, padded)
+constexpr int BN = 128;            // KV rows per tile
+constexpr int HD = 128;            // head dim
+constexpr int KSTAGES = 2, VSTAGES = 2;
+constexpr uint32_t ATOM_BYTES = 128 * 128;          // 128 rows x 64 elems x 2 B
+constexpr uint32_t TILE_BYTES = 2 * ATOM_BYTES;     // 32 KB
+constexpr int NUM_THREADS = 192;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t TM_O = 256;                       // S0 at 0, S1 at 128, O at 256
+constexpr int SLOT_FLOATS = BM * HD + 2 * BM;        // partial O rows + m + l
+constexpr float kLazyThreshLog2 = 8.0f;
+
+// dynamic smem layout (offsets from a 1024-aligned base)
+constexpr uint32_t OFF_Q = 0;
+constexpr uint32_t OFF_K = OFF_Q + TILE_BYTES;
+constexpr uint32_t OFF_V = OFF_K + KSTAGES * TILE_BYTES;
+constexpr uint32_t OFF_P = OFF_V + VSTAGES * TILE_BYTES;
+constexpr uint32_t OFF_BAR = OFF_P + TILE_BYTES;
+constexpr uint32_t SMEM_BYTES = OFF_BAR + 256 + 1024;  // + barriers + alignment slack
+
+struct TcParams {
+    const int32_t* prefix_len;
+    const int32_t* n_nodes;
+    const uint64_t* mask;
+    void* o;
+    float* lse;
+    float* partial;      // [gridDim.x * 2][SLOT_FLOATS]
+    unsigned* tickets;   // [B * H]
+    int B, T, H, W;
+    float c_log2;        // scale * log2(e)
+    float scale;
+};
+
+struct Seg {
+    int b, h, lo, hi, ntiles;
+    long long pair_start;
+};
+
+__device__ __forceinline__ int ntiles_of(const TcParams& p, int b) {
+    const int n = __ldg(p.n_nodes + b);
+    return n > 0 ? (__ldg(p.prefix_len + b) + n + BN - 1) / BN : 0;
 }
+
+__device__ long long total_tiles(const TcParams& p) {
+    long long t = 0;
+    for (int b = 0; b < p.B; ++b) t += (long long)p.H * ntiles_of(p, b);
+    return t;
+}
+
+// Segment starting at global tile t (t < t_end) of this CTA's range.
+__device__ Seg find_seg(const TcParams& p, long long t, long long t_end) {
+    long long base = 0;
+    Seg s{};
+    for (int b = 0; b < p.B; ++b) {
+        const int nt = ntiles_of(p, b);
+        const long long span = (long long)p.H * nt;
+        if (t < base + span) {
+            const long long off = t - base;
+            s.b = b;
+            s.h = (int)(off / nt);
+            s.lo = (int)(off % nt);
+            s.ntiles = nt;
+            s.pair_start = base + (long long)s.h * nt;
+            const long long hi = s.lo + (t_end - t);
+            s.hi = (int)(hi < nt ? hi : nt);
+            return s;
+        }
+        base += span;
+    }
+    s.b = -1;
+    return s;
+}
+
+__device__ __forceinline__ long long range_start(long long c, long long total, long long G) {
+    return c * total / G;
+}
+__device__ __forceinline__ long long cta_of(long long t, long long total, long long G) {
+    return ((t + 1) * G + total - 1) / total - 1;
+}
+
+template <class T> struct pk2;
+template <> struct pk2<__half> {
+    static __device__ __forceinline__ uint32_t pack(float a, float b) {
+        __half2 h = __floats2half2_rn(a, b);
+        return *reinterpret_cast<uint32_t*>(&h);
+    }
+};
+template <> struct pk2<__nv_bfloat16> {
+    static __device__ __forceinline__ uint32_t pack(float a, float b) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+        return *reinterpret_cast<uint32_t*>(&h);
+    }
+};
+
+template <class T>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_v, const TcParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint8_t* sm_q = smem + OFF_Q;
+    uint8_t* sm_k = smem + OFF_K;
+    uint8_t* sm_v = smem + OFF_V;
+    uint8_t* sm_p = smem + OFF_P;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* q_full = bars + 0;
+    uint64_t* q_empty = bars + 1;
+    uint64_t* k_full = bars + 2;              // [KSTAGES]
+    uint64_t* k_empty = k_full + KSTAGES;     // [KSTAGES]
+    uint64_t* v_full = k_empty + KSTAGES;     // [VSTAGES]
+    uint64_t* v_empty = v_full + VSTAGES;     // [VSTAGES]
+    uint64_t* s_full = v_empty + VSTAGES;     // [2]
+    uint64_t* s_empty = s_full + 2;           // [2]
+    uint64_t* p_full = s_empty + 2;
+    uint64_t* pv_done = p_full + 1;
+    uint64_t* o_empty = pv_done + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
+    __shared__ int merge_flag;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
+        for (int i = 0; i < KSTAGES; ++i) { mbar_init(k_full + i, 1); mbar_init(k_empty + i, 1); }
+        for (int i = 0; i < VSTAGES; ++i) { mbar_init(v_full + i, 1); mbar_init(v_empty + i, 1); }
+        for (int i = 0; i < 2; ++i) { mbar_init(s_full + i, 1); mbar_init(s_empty + i, 128); }
+        mbar_init(p_full, 128);
+        mbar_init(pv_done, 1);
+        mbar_init(o_empty, 128);
+        fence_barrier_init();
+    }
+    if (warp == 4 && lane == 0) {
+        prefetch_tmap(&tm_q);
+        prefetch_tmap(&tm_k);
+        prefetch_tmap(&tm_v);
+    }
+    if (warp == 5) tmem_alloc<TMEM_COLS>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const long long G = gridDim.x;
+    const long long total = total_tiles(p);
+    const long long t_begin = range_start(blockIdx.x, total, G);
+    const long long t_end = range_start(blockIdx.x + 1, total, G);
+
+    if (warp == 4) {
+        // ============================ TMA producer ============================
+        if (lane == 0) {
+            uint32_t qc = 0, kc = 0, vc = 0;
+            for (long long t = t_begin; t < t_end;) {
+                const Seg s = find_seg(p, t, t_end);
+                mbar_wait(q_empty, (qc & 1) ^ 1);
+                mbar_arrive_expect_tx(q_full, TILE_BYTES);
+                tma_load_4d(sm_q, &tm_q, q_full, 0, s.h, 0, s.b);
+                tma_load_4d(sm_q + ATOM_BYTES, &tm_q, q_full, 64, s.h, 0, s.b);
+                ++qc;
+                const int bh = s.b * p.H + s.h;
+                for (int j = s.lo; j < s.hi; ++j) {
+                    {
+                        const uint32_t st = kc % KSTAGES, ph = (kc / KSTAGES) & 1;
+                        mbar_wait(k_empty + st, ph ^ 1);
+                        mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
+                        uint8_t* dst = sm_k + st * TILE_BYTES;
+                        tma_load_3d(dst, &tm_k, k_full + st, 0, j * BN, bh);
+                        tma_load_3d(dst + ATOM_BYTES, &tm_k, k_full + st, 64, j * BN, bh);
+                        ++kc;
+                    }
+                    {
+                        const uint32_t st = vc % VSTAGES, ph = (vc / VSTAGES) & 1;
+                        mbar_wait(v_empty + st, ph ^ 1);
+                        mbar_arrive_expect_tx(v_full + st, TILE_BYTES);
+                        uint8_t* dst = sm_v + st * TILE_BYTES;
+                        tma_load_3d(dst, &tm_v, v_full + st, 0, j * BN, bh);
+                        tma_load_3d(dst + ATOM_BYTES, &tm_v, v_full + st, 64, j * BN, bh);
+                        ++vc;
+                    }
+                }
+                t += s.hi - s.lo;
+            }
+        }
+    } else if (warp == 5) {
+        // ============================ MMA issuer ==============================
+        if (lane == 0) {
+            constexpr uint32_t fmt = std::is_same<T, __half>::value ? 0u : 1u;
+            constexpr uint32_t idS = idesc_f16(fmt, BM, BN, 0, 0);   // Q K^T: both K-major
+            constexpr uint32_t idPV = idesc_f16(fmt, BM, HD, 0, 1);  // P V: V is MN-major
+            const uint32_t q_base = smem_u32(sm_q), k_base = smem_u32(sm_k);
+            const uint32_t v_base = smem_u32(sm_v), p_base = smem_u32(sm_p);
+            uint32_t qc = 0, kc = 0, vc = 0, sc = 0, pc = 0, segc = 0;
+            auto issue_pv = [&](int i_local) {
+                mbar_wait(p_full, pc & 1);
+                const uint32_t st = vc % VSTAGES;
+                mbar_wait(v_full + st, (vc / VSTAGES) & 1);
+                if (i_local == 0) mbar_wait(o_empty, (segc & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t vb = v_base + st * TILE_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < BN / 16; ++kk) {
+                    const uint64_t a = smem_desc(p_base + (kk >> 2) * ATOM_BYTES + (kk & 3) * 32, 16, 1024);
+                    const uint64_t b = smem_desc(vb + kk * 2048, ATOM_BYTES, 1024);
+                    umma_f16_ss(tmem + TM_O, a, b, idPV, (i_local > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit(pv_done);
+                umma_commit(v_empty + st);
+                ++vc;
+                ++pc;
+            };
+            for (long long t = t_begin; t < t_end;) {
+                const Seg s = find_seg(p, t, t_end);
+                const int ntl = s.hi - s.lo;
+                mbar_wait(q_full, qc & 1);
+                ++qc;
+                for (int i = 0; i < ntl; ++i) {
+                    const uint32_t st = kc % KSTAGES;
+                    mbar_wait(k_full + st, (kc / KSTAGES) & 1);
+                    const uint32_t sb = sc & 1;
+                    mbar_wait(s_empty + sb, ((sc >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                    const uint32_t kb = k_base + st * TILE_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < HD / 16; ++kk) {
+                        const uint32_t off = (kk >> 2) * ATOM_BYTES + (kk & 3) * 32;
+                        umma_f16_ss(tmem + sb * BN, smem_desc(q_base + off, 16, 1024),
+                                    smem_desc(kb + off, 16, 1024), idS, kk > 0 ? 1u : 0u);
+                    }
+                    umma_commit(s_full + sb);
+                    umma_commit(k_empty + st);
+                    if (i == ntl - 1) umma_commit(q_empty);
+                    ++kc;
+                    ++sc;
+                    if (i > 0) issue_pv(i - 1);
+                }
+                issue_pv(ntl - 1);
+                ++segc;
+                t += ntl;
+            }
+        }
+    } else {
+        // ===================== softmax + epilogue (warps 0-3) ==================
+        const int r = threadIdx.x;  // query row == TMEM lane
+        const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+        const float c = p.c_log2;
+        const float thresh_raw = kLazyThreshLog2 / c;
+        uint32_t sc = 0, pvc = 0;
+        for (long long t = t_begin; t < t_end;) {
+            const Seg s = find_seg(p, t, t_end);
+            const int ntl = s.hi - s.lo;
+            const int n = __ldg(p.n_nodes + s.b);
+            const int P = __ldg(p.prefix_len + s.b);
+            const bool valid = r < n;
+            uint64_t mw0 = 0, mw1 = 0;
+            if (valid) {
+                const uint64_t* mr = p.mask + ((long long)s.b * p.T + r) * p.W;
+                mw0 = __ldg(mr);
+                if (p.W > 1) mw1 = __ldg(mr + 1);
+            }
+            float m = -INFINITY, l = 0.f;
+            for (int i = 0; i < ntl; ++i) {
+                const int j = s.lo + i;
+                const uint32_t sb = sc & 1;
+                mbar_wait(s_full + sb, (sc >> 1) & 1);
+                tc_fence_after();
+                float sv[BN];
+#pragma unroll
+                for (int ch = 0; ch < BN / 32; ++ch) {
+                    uint32_t raw[32];
+                    tmem_ld_32x32b_x32(lane_addr + sb * BN + ch * 32, raw);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) sv[ch * 32 + k] = __uint_as_float(raw[k]);
+                }
+                tc_fence_before();
+                mbar_arrive(s_empty + sb);
+                ++sc;
+
+                const int row0 = j * BN;
+                if (row0 + BN > P) {  // tile reaches the tree (or past it): apply the mask
+#pragma unroll
+                    for (int k = 0; k < BN; ++k) {
+                        const int ra = row0 + k;
+                        bool vis = ra < P;
+                        if (!vis) {
+                            const int v = ra - P;
+                            vis = v < n && (((v < 64 ? mw0 : mw1) >> (v & 63)) & 1ull);
+                        }
+                        if (!vis) sv[k] = -INFINITY;
+                    }
+                }
+                float mx = -INFINITY;
+#pragma unroll
+                for (int k = 0; k < BN; ++k) mx = fmaxf(mx, sv[k]);
+                const float m_new = fmaxf(m, mx);
+
+                // P buffer free and O stable once the previous P.V retired
+                if (i > 0) {
+                    mbar_wait(pv_done, pvc & 1);
+                    ++pvc;
+                    tc_fence_after();
+                }
+                float alpha = 1.f;
+                bool rescale = false;
+                if (m == -INFINITY) {
+                    m = m_new;  // nothing with nonzero weight accumulated yet
+                } else if (m_new - m > thresh_raw) {
+                    alpha = ex2((m - m_new) * c);
+                    l *= alpha;
+                    m = m_new;
+                    rescale = true;
+                }
+                if (__any_sync(0xffffffffu, rescale && valid)) {
+#pragma unroll
+                    for (int ch = 0; ch < HD / 32; ++ch) {
+                        uint32_t raw[32];
+                        tmem_ld_32x32b_x32(lane_addr + TM_O + ch * 32, raw);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int k = 0; k < 32; ++k)
+                            raw[k] = __float_as_uint(__uint_as_float(raw[k]) * alpha);
+                        tmem_st_32x32b_x32(lane_addr + TM_O + ch * 32, raw);
+                    }
+                    tmem_st_wait();
+                }
+                const float base = (m == -INFINITY) ? 0.f : m * c;
+                float lsum = 0.f;
+                uint8_t* prow = sm_p + r * 128;
+#pragma unroll
+                for (int ch = 0; ch < BN / 8; ++ch) {
+                    uint32_t w4[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float p0 = ex2(fmaf(sv[ch * 8 + 2 * k], c, -base));
+                        const float p1 = ex2(fmaf(sv[ch * 8 + 2 * k + 1], c, -base));
+                        lsum += p0 + p1;
+                        w4[k] = pk2<T>::pack(p0, p1);
+                    }
+                    const uint32_t atom = ch >> 3, cin = ch & 7;
+                    *reinterpret_cast<uint4*>(prow + atom * ATOM_BYTES + ((cin ^ (r & 7)) << 4)) =
+                        make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                }
+                l += lsum;
+                fence_proxy_async_smem();
+                tc_fence_before();
+                mbar_arrive(p_full);
+            }
+
+            // ---- segment epilogue: O row from TMEM ----
+            mbar_wait(pv_done, pvc & 1);
+            ++pvc;
+            tc_fence_after();
+            float ov[HD];
+#pragma unroll
+            for (int ch = 0; ch < HD / 32; ++ch) {
+                uint32_t raw[32];
+                tmem_ld_32x32b_x32(lane_addr + TM_O + ch * 32, raw);
+                tmem_ld_wait();
+#pragma unroll
+                for (int k = 0; k < 32; ++k) ov[ch * 32 + k] = __uint_as_float(raw[k]);
+            }
+            tc_fence_before();
+            mbar_arrive(o_empty);
+
+            const bool full = (s.lo == 0 && s.hi == s.ntiles);
+            if (full) {
+                if (valid) {
+                    const float inv = 1.f / l;
+                    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(p.o) +
+                                                          (((long long)s.b * p.T + r) * p.H + s.h) * HD);
+#pragma unroll
+                    for (int ch = 0; ch < HD / 8; ++ch) {
+                        uint32_t w4[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            w4[k] = pk2<T>::pack(ov[ch * 8 + 2 * k] * inv, ov[ch * 8 + 2 * k + 1] * inv);
+                        dst[ch] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                    }
+                    if (p.lse)
+                        p.lse[((long long)s.b * p.H + s.h) * p.T + r] = m * p.scale + __logf(l);
+                }
+            } else {
+                // partial piece -> workspace slot, last finisher of the pair merges
+                const long long my_start = range_start(blockIdx.x, total, G);
+                const int slot = (t == my_start) ? 0 : 1;
+                float* sp = p.partial + ((long long)blockIdx.x * 2 + slot) * SLOT_FLOATS;
+                if (valid) {
+                    float4* po = reinterpret_cast<float4*>(sp + r * HD);
+#pragma unroll
+                    for (int k = 0; k < HD / 4; ++k)
+                        po[k] = make_float4(ov[4 * k], ov[4 * k + 1], ov[4 * k + 2], ov[4 * k + 3]);
+                    sp[BM * HD + r] = m;
+                    sp[BM * HD + BM + r] = l;
+                }
+                __threadfence();
+                named_bar_sync(1, 128);
+                const long long pair_end = s.pair_start + s.ntiles;
+                const long long c_first = cta_of(s.pair_start, total, G);
+                const long long c_last = cta_of(pair_end - 1, total, G);
+                if (r == 0) {
+                    const unsigned old = atomicAdd(p.tickets + s.b * p.H + s.h, 1u);
+                    merge_flag = (old == (unsigned)(c_last - c_first));
+                }
+                named_bar_sync(1, 128);
+                if (merge_flag) {
+                    __threadfence();
+                    if (valid) {
+                        float M = -INFINITY;
+                        for (long long cc = c_first; cc <= c_last; ++cc) {
+                            const long long rs = range_start(cc, total, G);
+                            const int sl = (s.pair_start > rs) ? 1 : 0;
+                            const float* q = p.partial + (cc * 2 + sl) * SLOT_FLOATS;
+                            M = fmaxf(M, __ldcg(q + BM * HD + r));
+                        }
+                        float acc[HD];
+#pragma unroll
+                        for (int k = 0; k < HD; ++k) acc[k] = 0.f;
+                        float L = 0.f;
+                        for (long long cc = c_first; cc <= c_last; ++cc) {
+                            const long long rs = range_start(cc, total, G);
+                            const int sl = (s.pair_start > rs) ? 1 : 0;
+                            const float* q = p.partial + (cc * 2 + sl) * SLOT_FLOATS;
+                            const float mk = __ldcg(q + BM * HD + r);
+                            if (mk == -INFINITY) continue;
+                            const float w = ex2((mk - M) * c);
+                            L += w * __ldcg(q + BM * HD + BM + r);
+                            const float4* qo = reinterpret_cast<const float4*>(q + r * HD);
+#pragma unroll
+                            for (int k = 0; k < HD / 4; ++k) {
+                                const float4 x = __ldcg(qo + k);
+                                acc[4 * k] += w * x.x;
+                                acc[4 * k + 1] += w * x.y;
+                                acc[4 * k + 2] += w * x.z;
+                                acc[4 * k + 3] += w * x.w;
+                            }
+                        }
+                        const float inv = 1.f / L;
+                        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(p.o) +
+                                                              (((long long)s.b * p.T + r) * p.H + s.h) * HD);
+#pragma unroll
+                        for (int ch = 0; ch < HD / 8; ++ch) {
+                            uint32_t w4[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                w4[k] = pk2<T>::pack(acc[ch * 8 + 2 * k] * inv, acc[ch * 8 + 2 * k + 1] * inv);
+                            dst[ch] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                        }
+                        if (p.lse)
+                            p.lse[((long long)s.b * p.H + s.h) * p.T + r] = M * p.scale + __logf(L);
+                    }
+                    if (r == 0) p.tickets[s.b * p.H + s.h] = 0u;
+                }
+            }
+            t += ntl;
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 5) tmem_dealloc<TMEM_COLS>(tmem);
+}
+
+// ------------------------------------------------------------------ host --
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+int num_sms() {
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cache[dev]) cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev);
+    return cache[dev];
+}
+
+bool encode(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* ptr, const uint64_t* dims,
+            const uint64_t* strides_bytes, const uint32_t* box) {
+    auto fn = get_encode();
+    if (!fn) return false;
+    uint32_t es[4] = {1, 1, 1, 1};
+    return fn(m, dt, rank, const_cast<void*>(ptr), dims, strides_bytes, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+bool tree_attention_tc_supported(const st_attn_args* a) {
+    auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    return (a->dtype == ST_F16 || a->dtype == ST_BF16) && a->D == HD && a->H == a->Hkv &&
+           a->T <= BM && a->W <= 2 && a->Lmax < (1ll << 31) && al(a->q) && al(a->k_cache) &&
+           al(a->v_cache) && al(a->o) && (int64_t)a->B * a->H < (1ll << 31);
+}
+
+size_t tree_attention_tc_workspace(const st_attn_args* a) {
+    return align_up((size_t)num_sms() * 2 * SLOT_FLOATS * sizeof(float), 256) +
+           (size_t)a->B * a->H * sizeof(unsigned);
+}
+
+st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
+    const CUtensorMapDataType dt =
+        a->dtype == ST_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    CUtensorMap tq, tk, tv;
+    {
+        const uint64_t dims[4] = {(uint64_t)HD, (uint64_t)a->H, (uint64_t)a->T, (uint64_t)a->B};
+        const uint64_t strides[3] = {HD * 2ull, (uint64_t)a->H * HD * 2, (uint64_t)a->T * a->H * HD * 2};
+        const uint32_t box[4] = {64, 1, BM, 1};
+        if (!encode(&tq, dt, 4, a->q, dims, strides, box)) {
+            set_error("st_tree_attention: cuTensorMapEncodeTiled(q) failed");
+            return ST_ERR_CUDA;
+        }
+    }
+    {
+        const uint64_t dims[3] = {(uint64_t)HD, (uint64_t)a->Lmax, (uint64_t)a->B * a->Hkv};
+        const uint64_t strides[2] = {HD * 2ull, (uint64_t)a->Lmax * HD * 2};
+        const uint32_t box[3] = {64, BN, 1};
+        if (!encode(&tk, dt, 3, a->k_cache, dims, strides, box) ||
+            !encode(&tv, dt, 3, a->v_cache, dims, strides, box)) {
+            set_error("st_tree_attention: cuTensorMapEncodeTiled(kv) failed");
+            return ST_ERR_CUDA;
+        }
+    }
+    const int G = num_sms();
+    TcParams prm;
+    prm.prefix_len = a->prefix_len;
+    prm.n_nodes = a->n_nodes;
+    prm.mask = a->mask;
+    prm.o = a->o;
+    prm.lse = a->lse;
+    prm.partial = reinterpret_cast<float*>(a->workspace);
+    prm.tickets = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(a->workspace) +
+                                              align_up((size_t)G * 2 * SLOT_FLOATS * sizeof(float), 256));
+    prm.B = a->B;
+    prm.T = a->T;
+    prm.H = a->H;
+    prm.W = a->W;
+    prm.scale = (float)a->scale;
+    prm.c_log2 = (float)(a->scale * 1.4426950408889634);
+    if (a->dtype == ST_F16) {
+        static bool attr = false;
+        if (!attr) {
+            ST_CUDA_TRY(cudaFuncSetAttribute(tree_attn_tc_kernel<__half>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+            attr = true;
+        }
+        tree_attn_tc_kernel<__half><<<G, NUM_THREADS, SMEM_BYTES, stream>>>(tq, tk, tv, prm);
+    } else {
+        static bool attr = false;
+        if (!attr) {
+            ST_CUDA_TRY(cudaFuncSetAttribute(tree_attn_tc_kernel<__nv_bfloat16>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+            attr = true;
+        }
+        tree_attn_tc_kernel<__nv_bfloat16><<<G, NUM_THREADS, SMEM_BYTES, stream>>>(tq, tk, tv, prm);
+    }
+    ST_LAUNCH_CHECK();
+    return ST_OK;
+}
+
 }  // namespace st

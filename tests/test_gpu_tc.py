@@ -1,0 +1,117 @@
+"""Parity of the tcgen05 tree-attention kernel (K1, f16/bf16, D=128).
+
+Checked against the f64 CPU restatement on the same (rounded) inputs with the
+north-star tolerance: max-abs 2e-3. Shapes exercise the stream-K split
+(pairs cut across CTAs and merged), tiles straddling the prefix/tree border,
+ragged node counts, and the 128-node maximum.
+"""
+import numpy as np
+import pytest
+import torch
+
+from tests.test_gpu_kernels import check_k1, make_batch, run_k1
+from tests.treegen import pack, width_depth_seqs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def capi():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2305_09781_b200 import _capi
+    return _capi
+
+
+@pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
+@pytest.mark.parametrize("B,H,P_range", [(3, 2, (1, 60)), (4, 8, (100, 700)), (2, 3, (1000, 1300)),
+                                         (9, 16, (0, 300))])
+def test_tc_matches_oracle(capi, restatement, dtype, B, H, P_range):
+    rng = np.random.default_rng(B * 100 + H)
+    bt = make_batch(restatement, rng, B, H, H, 128, dtype=dtype, P_range=P_range)
+    out, lse = run_k1(capi, bt, dtype, force_path=2, lse=True)
+    check_k1(restatement, bt, out, dtype, lse)
+
+
+def _dummy(bt, dtype):
+    dev = "cuda"
+    q = torch.zeros(bt["q"].shape, dtype=dtype, device=dev)
+    kc = torch.zeros(bt["kc"].shape, dtype=dtype, device=dev)
+    mask = torch.zeros(bt["mask"].shape, dtype=torch.int64, device=dev)
+    P = torch.tensor(bt["P"], device=dev)
+    n = torch.tensor(bt["n"], device=dev)
+    return q, kc, kc, mask, P, n
+
+
+@pytest.mark.parametrize("T,width,depth", [(16, 4, 4), (64, 8, 8), (128, 16, 8), (61, 9, 8)])
+def test_tc_tree_widths(capi, restatement, T, width, depth):
+    rng = np.random.default_rng(T)
+    trees = []
+    for _ in range(3):
+        while True:
+            t = restatement.merge(width_depth_seqs(rng, 5, 32000, width, depth), 4096)
+            if len(t[0]) <= T:
+                break
+        trees.append(t)
+    bt = make_batch(restatement, rng, 3, 4, 4, 128, trees=trees, T=T, P_range=(50, 400),
+                    dtype=torch.float16)
+    out, lse = run_k1(capi, bt, torch.float16, force_path=2, lse=True)
+    check_k1(restatement, bt, out, torch.float16, lse)
+
+
+def test_tc_bitwise_deterministic_and_non_ancestor_invariant(capi, restatement):
+    rng = np.random.default_rng(4)
+    trees = [restatement.merge([[9, 3, 5, 6], [9, 3, 7, 8]])] * 2
+    bt = make_batch(restatement, rng, 2, 32, 32, 128, trees=trees, P_range=(900, 900),
+                    dtype=torch.float16)
+    a, _ = run_k1(capi, bt, torch.float16, force_path=2)
+    b, _ = run_k1(capi, bt, torch.float16, force_path=2)
+    assert torch.equal(a, b)
+    P = int(bt["P"][0])
+    bt["kc"][:, :, P + 4:P + 6] += 3.0
+    bt["vc"][:, :, P + 4:P + 6] -= 2.0
+    c, _ = run_k1(capi, bt, torch.float16, force_path=2)
+    assert torch.equal(a[:, :4], c[:, :4])
+
+
+def test_tc_c2_shape_sampled_heads(capi, restatement):
+    """C2 (B=8, T=64, L=2048, H=32, D=128, f16): full launch, checked on a
+    sample of (b, h) pairs with a vectorised f64 reference."""
+    rng = np.random.default_rng(2)
+    B, T, H, D, L = 8, 64, 32, 128, 2048
+    trees = []
+    while len(trees) < B:
+        t = restatement.merge(width_depth_seqs(rng, 1, 32000, 8, 8), 4096)
+        if len(t[0]) <= T:
+            trees.append(t)
+    tok, par, dep, n = pack(trees, T)
+    dev = "cuda"
+    Lmax = L + T
+    P = np.full(B, L, np.int32)
+    q = torch.rand(B, T, H, D, device=dev, dtype=torch.float16) * 2 - 1
+    kc = torch.rand(B, H, Lmax, D, device=dev, dtype=torch.float16) * 2 - 1
+    vc = torch.rand(B, H, Lmax, D, device=dev, dtype=torch.float16) * 2 - 1
+    from tests.treegen import masks
+    m = masks(restatement, par, n, 1)
+    mask = torch.tensor(m.view(np.int64), device=dev)
+    out = capi.tree_attention(q, kc, vc, mask, torch.tensor(P, device=dev),
+                              torch.tensor(n, device=dev), force_path=2)
+    torch.cuda.synchronize()
+    worst = 0.0
+    for (b, h) in [(0, 0), (3, 17), (7, 31), (5, 8)]:
+        qq = q[b, :, h].double().cpu().numpy()
+        kk = kc[b, h].double().cpu().numpy()
+        vv = vc[b, h].double().cpu().numpy()
+        s = qq @ kk[: L + n[b]].T / np.sqrt(D)
+        vis = np.ones_like(s, dtype=bool)
+        for u in range(T):
+            for v in range(n[b]):
+                vis[u, L + v] = bool((int(m[b, u, 0]) >> v) & 1) if u < n[b] else False
+        s = np.where(vis, s, -np.inf)
+        s -= s.max(axis=1, keepdims=True)
+        pr = np.exp(s)
+        pr /= pr.sum(axis=1, keepdims=True)
+        ref = pr @ vv[: L + n[b]]
+        got = out[b, : n[b], h].double().cpu().numpy()
+        worst = max(worst, np.abs(got - ref[: n[b]]).max())
+    assert worst <= 2e-3, worst
