@@ -137,6 +137,13 @@ st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32
                            int32_t* verified, int32_t* ids, int32_t* len, void* workspace,
                            void* stream);
 
+/* The walk alone, given per-node LLM outputs [B][T] (what the reference's
+ * verify() consumes, token_tree.cpp:153-175); same outputs as st_verify_greedy. */
+st_status st_verify_outputs(const int32_t* outputs, int B, int T, const int32_t* tokens,
+                            const int32_t* parent, const int32_t* n_nodes,
+                            const int32_t* budget, int32_t eos, int32_t* verified,
+                            int32_t* ids, int32_t* len, void* stream);
+
 /* ------------------------------------------------------------------ K4 ---
  * Stochastic multi-step speculative sampling (SpecInfer MSS; NOT in the
  * reference — contract in DESIGN.md §5). q[b][v][:] is the draft
@@ -146,6 +153,15 @@ st_status st_verify_mss(const float* logits, const float* q, int B, int T, int V
                         const int32_t* tokens, const int32_t* parent, const int32_t* n_nodes,
                         float temperature, const float* uniforms, int n_uniforms,
                         int32_t* verified, int32_t* ids, int32_t* len, void* stream);
+
+/* ------------------------------------------------------------ host tree ---
+ * TokenTree::merge_sequences of the host C++ library (drop-in for reference
+ * token_tree.cpp:42-102): sequences given flattened (flat, lens[nseq]);
+ * writes preorder tok/parent/depth (cap entries) and *n_out. Host-only: needs
+ * no GPU. Returns tree_too_large / root_mismatch / empty_input like the
+ * reference; ST_ERR_INVALID_ARGUMENT if cap is too small. */
+st_status st_tree_merge(const int32_t* flat, const int32_t* lens, int nseq, int max_nodes,
+                        int32_t* tok, int32_t* parent, int32_t* depth, int cap, int* n_out);
 
 /* --------------------------------------------------------- tree packing ---
  * Device-side ancestor bitmask build: mask[b][u] = mask[b][parent[u]] | bit(u)

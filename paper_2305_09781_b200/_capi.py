@@ -57,6 +57,7 @@ SIGNATURES = {
     "st_kv_compact": (_I, [_I, _I, _I, _I, _I64, _I, _I64, _V, _I, _V, _V, _V, _V, _V, _V]),
     "st_verify_workspace_size": (_Z, [_I, _I]),
     "st_verify_greedy": (_I, [_V, _I, _I, _I, _V, _V, _V, _V, C.c_int32, _V, _V, _V, _V, _V, _V]),
+    "st_verify_outputs": (_I, [_V, _I, _I, _V, _V, _V, _V, C.c_int32, _V, _V, _V, _V]),
     "st_verify_mss": (_I, [_V, _V, _I, _I, _I, _V, _V, _V, _F, _V, _I, _V, _V, _V, _V]),
     "st_build_masks": (_I, [_V, _V, _I, _I, _I, _V, _V]),
     "st_tree_merge": (_I, [_V, _V, _I, _I, _V, _V, _V, _I, C.POINTER(_I)]),

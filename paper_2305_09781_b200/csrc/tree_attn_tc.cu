@@ -445,8 +445,12 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 const long long c_first = cta_of(s.pair_start, total, G);
                 const long long c_last = cta_of(pair_end - 1, total, G);
                 if (r == 0) {
+                    // CTAs with an empty range (total < #SMs) contribute no piece
+                    unsigned pieces = 0;
+                    for (long long cc = c_first; cc <= c_last; ++cc)
+                        pieces += range_start(cc + 1, total, G) > range_start(cc, total, G);
                     const unsigned old = atomicAdd(p.tickets + s.b * p.H + s.h, 1u);
-                    merge_flag = (old == (unsigned)(c_last - c_first));
+                    merge_flag = (old == pieces - 1);
                 }
                 named_bar_sync(1, 128);
                 if (merge_flag) {
@@ -455,6 +459,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         float M = -INFINITY;
                         for (long long cc = c_first; cc <= c_last; ++cc) {
                             const long long rs = range_start(cc, total, G);
+                            if (range_start(cc + 1, total, G) == rs) continue;  // empty range
                             const int sl = (s.pair_start > rs) ? 1 : 0;
                             const float* q = p.partial + (cc * 2 + sl) * SLOT_FLOATS;
                             M = fmaxf(M, __ldcg(q + BM * HD + r));
@@ -465,6 +470,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         float L = 0.f;
                         for (long long cc = c_first; cc <= c_last; ++cc) {
                             const long long rs = range_start(cc, total, G);
+                            if (range_start(cc + 1, total, G) == rs) continue;  // empty range
                             const int sl = (s.pair_start > rs) ? 1 : 0;
                             const float* q = p.partial + (cc * 2 + sl) * SLOT_FLOATS;
                             const float mk = __ldcg(q + BM * HD + r);

@@ -38,6 +38,60 @@ __device__ __forceinline__ bool beats(float av, int ai, float bv, int bi) {
 
 __device__ __forceinline__ float sanitize(float x) { return x != x ? -INFINITY : x; }
 
+// Alg.-2 walk (reference token_tree.cpp:153-175) + engine truncation
+// (engine.cpp:110-121) for request b, executed by one full warp. `outs` holds
+// the per-node LLM outputs [B][T]; read through L2 when written by other CTAs.
+__device__ void walk_warp(const int32_t* outs, const int32_t* __restrict__ tokens,
+                          const int32_t* __restrict__ parent, int n, int T, int b,
+                          const int32_t* __restrict__ budget, int32_t eos,
+                          int32_t* __restrict__ verified, int32_t* __restrict__ ids,
+                          int32_t* __restrict__ len, int lane, bool coherent) {
+    const int32_t* tok = tokens + (int64_t)b * T;
+    const int32_t* par = parent + (int64_t)b * T;
+    const int32_t* am = outs + (int64_t)b * T;
+    int32_t* vrow = verified + (int64_t)b * (T + 1);
+    int32_t* irow = ids + (int64_t)b * (T + 1);
+    int cur = 0, m = 0;
+    if (lane == 0) irow[0] = 0;
+    for (;;) {
+        const int32_t want = coherent ? __ldcg(am + cur) : am[cur];
+        int next = -1;
+        for (int v0 = cur + 1; v0 < n && next < 0; v0 += 32) {
+            const int v = v0 + lane;
+            const bool hit = v < n && par[v] == cur && tok[v] == want;
+            const unsigned bal = __ballot_sync(0xffffffffu, hit);
+            if (bal) next = v0 + __ffs(bal) - 1;
+        }
+        if (next < 0) break;
+        cur = next;
+        if (lane == 0) {
+            vrow[m] = want;
+            irow[m + 1] = cur;
+        }
+        ++m;
+    }
+    if (lane == 0) {
+        vrow[m] = coherent ? __ldcg(am + cur) : am[cur];  // bonus token
+        int L = m + 1;
+        if (budget && L > budget[b]) L = budget[b] > 0 ? budget[b] : 0;
+        if (eos >= 0) {
+            for (int k = 0; k < L; ++k)
+                if (vrow[k] == eos) { L = k + 1; break; }
+        }
+        len[b] = L;
+    }
+}
+
+__global__ void walk_kernel(const int32_t* __restrict__ outs, int T,
+                            const int32_t* __restrict__ tokens, const int32_t* __restrict__ parent,
+                            const int32_t* __restrict__ n_nodes, const int32_t* __restrict__ budget,
+                            int32_t eos, int32_t* __restrict__ verified, int32_t* __restrict__ ids,
+                            int32_t* __restrict__ len) {
+    const int b = blockIdx.x;
+    walk_warp(outs, tokens, parent, n_nodes[b], T, b, budget, eos, verified, ids, len,
+              threadIdx.x & 31, false);
+}
+
 __global__ void __launch_bounds__(kThreads)
 greedy_verify_kernel(const float* __restrict__ logits, int T, int V,
                      const int32_t* __restrict__ tokens, const int32_t* __restrict__ parent,
@@ -115,41 +169,8 @@ greedy_verify_kernel(const float* __restrict__ logits, int T, int V,
 
     // ---- Alg.-2 walk by the last block of request b (one warp) ----
     __threadfence();
-    const int32_t* tok = tokens + (int64_t)b * T;
-    const int32_t* par = parent + (int64_t)b * T;
-    const int32_t* am = argmax_ws + (int64_t)b * T;
-    int32_t* vrow = verified + (int64_t)b * (T + 1);
-    int32_t* irow = ids + (int64_t)b * (T + 1);
-    int cur = 0, m = 0;
-    if (lane == 0) irow[0] = 0;
-    for (;;) {
-        const int32_t want = __ldcg(am + cur);
-        int next = -1;
-        for (int v0 = cur + 1; v0 < n && next < 0; v0 += 32) {
-            const int v = v0 + lane;
-            const bool hit = v < n && par[v] == cur && tok[v] == want;
-            const unsigned bal = __ballot_sync(0xffffffffu, hit);
-            if (bal) next = v0 + __ffs(bal) - 1;
-        }
-        if (next < 0) break;
-        cur = next;
-        if (lane == 0) {
-            vrow[m] = want;
-            irow[m + 1] = cur;
-        }
-        ++m;
-    }
-    if (lane == 0) {
-        vrow[m] = __ldcg(am + cur);  // bonus token
-        int L = m + 1;
-        if (budget && L > budget[b]) L = budget[b] > 0 ? budget[b] : 0;
-        if (eos >= 0) {
-            for (int k = 0; k < L; ++k)
-                if (vrow[k] == eos) { L = k + 1; break; }
-        }
-        len[b] = L;
-        tickets[b] = 0;  // reusable workspace
-    }
+    walk_warp(argmax_ws, tokens, parent, n, T, b, budget, eos, verified, ids, len, lane, true);
+    if (lane == 0) tickets[b] = 0;  // reusable workspace
 }
 
 __global__ void build_masks_kernel(const int32_t* __restrict__ parent,
@@ -200,6 +221,21 @@ st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32
     st::greedy_verify_kernel<<<grid, st::kThreads, 0, st::as_stream(stream)>>>(
         logits, T, V, tokens, parent, n_nodes, budget, eos, argmax, scratch, verified, ids, len,
         tickets);
+    ST_LAUNCH_CHECK();
+    return ST_OK;
+}
+
+st_status st_verify_outputs(const int32_t* outputs, int B, int T, const int32_t* tokens,
+                            const int32_t* parent, const int32_t* n_nodes, const int32_t* budget,
+                            int32_t eos, int32_t* verified, int32_t* ids, int32_t* len,
+                            void* stream) {
+    if (st_status e = st::require_device()) return e;
+    ST_CHECK_ARG(B >= 0 && T >= 1, ST_ERR_SHAPE_MISMATCH, "bad shape");
+    if (B == 0) return ST_OK;
+    ST_CHECK_ARG(outputs && tokens && parent && n_nodes && verified && ids && len,
+                 ST_ERR_INVALID_ARGUMENT, "null pointer");
+    st::walk_kernel<<<B, 32, 0, st::as_stream(stream)>>>(outputs, T, tokens, parent, n_nodes,
+                                                         budget, eos, verified, ids, len);
     ST_LAUNCH_CHECK();
     return ST_OK;
 }
