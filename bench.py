@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark of the token-tree verification hot path (BASELINE.json metric:
+"tree-verify tokens/s & KV HBM GB/s vs roofline at 1/2/4/8 B200; CPU ref
+baseline").
+
+Workload (config C2, BASELINE.json configs[1]): LLaMA-7B-shape attention layer,
+fp16, batch 8 requests per GPU, 64-node token tree each, 2048 committed KV rows,
+H = 32 heads x D = 128, greedy verification over a 32000-token vocabulary.
+
+One step = one pass of the hot path over the batch:
+  K2 append of the tree's K/V into the cache scratch rows
+  -> ancestor bitmasks built on device
+  -> K1 tree attention (tcgen05)                       [dominant kernel]
+  -> K3 greedy verify (vocab argmax + accepted-path walk)
+  -> K2 in-place compaction of the accepted path
+  (+ N>1: NCCL all-gather of the accepted tokens — the DP exchange step)
+
+value  = tree tokens verified per second over all ranks (B*T*N / step time),
+         inputs resident in HBM, CUDA-event timed, max over ranks.
+e2e    = same metric through the C-ABI with HOST buffers: every step copies
+         Q, the tree's K/V and the tree topology from pinned host memory and
+         reads the accepted tokens back (logits stay device-resident: in the
+         full model they come from the on-device LM head).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# C2
+B, T, H, D, L, V = 8, 64, 32, 128, 2048, 32000
+WIDTH, DEPTH = 8, 8            # 8 root-to-leaf paths, trimmed to exactly 64 nodes
+LAUNCHES_PER_STEP = 5          # append, masks, K1, K3, compact
+METRIC = "tree-verify tokens/s"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def c2_trees(make_tree, seed, vocab, n_req=B, nodes=T):
+    """W paths of depth ceil((T-1)/W) with uniform tokens, trimmed to exactly T nodes."""
+    rng = np.random.default_rng(seed)
+    trees = []
+    for _ in range(n_req):
+        root = int(rng.integers(0, vocab))
+        while True:
+            seqs = [[root] + rng.integers(0, vocab, DEPTH).tolist() for _ in range(WIDTH)]
+            t = make_tree(seqs)
+            # trim trailing tokens of the last paths until exactly `nodes`
+            i = len(seqs) - 1
+            while t.size > nodes and i >= 0:
+                if len(seqs[i]) > 1:
+                    seqs[i] = seqs[i][:-1]
+                else:
+                    i -= 1
+                t = make_tree(seqs)
+            if t.size == nodes:
+                trees.append((t, seqs))
+                break
+    return trees
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------- reference arm ---
+def reference_sample(n_threads, steps, warmup, full_tree):
+    """The reference's own tree_parallel_decode (oracle/_ref, compiled from the
+    unmodified reference sources) at the C2 layer shape on host cores.
+    Reference recipe at LLaMA-7B attention shape: 1 layer, d=4096, 32 heads,
+    V=258, ffn_mult=1; KV injected, one request per thread."""
+    from oracle.oracle import Reference, available_reference
+    if not available_reference():
+        return None
+    R = Reference()
+
+    class _T:
+        def __init__(self, seqs):
+            self.size = len(R.merge(seqs, 1 << 20)[0])
+
+    trees = c2_trees(lambda s: _T(s), 7, 258, n_req=1)
+    seqs = trees[0][1]
+    if not full_tree:   # bounded sample: root + the first root-to-leaf path (9 nodes)
+        seqs = [seqs[0]]
+    nodes = len(R.merge(seqs, 1 << 20)[0])
+    cfg = (1, H, H * D, 258, L + T + 2, 1)
+    times = []
+    for i in range(warmup + steps):
+        t = R.bench_tree_decode(cfg, 42, n_threads, L + 1, seqs, 1 << 20, n_threads)
+        if i >= warmup:
+            times.append(t)
+    sec = statistics.median(times)
+    return dict(value=n_threads * nodes / sec, seconds=sec, nodes=nodes, requests=n_threads,
+                kind="reference")
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    nt = cpu_threads()
+    res = reference_sample(nt, args.steps, args.warmup, full_tree=False)
+    cfg = {"workload": "C2 reference CPU path: tree_parallel_decode (f64) at the LLaMA-7B "
+                       "attention-layer shape, KV 2048, 1 layer, V=258, ffn_mult=1",
+           "B": B, "T": T, "L": L, "H": H, "D": D}
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs "
+                          "/root/reference at build time)"}))
+        return
+    sample = (f"{res['requests']} requests x {res['nodes']}-node sample (root + one 8-deep path "
+              f"of a C2 tree) per step, one request per host thread")
+    line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": res["seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": res["value"], "unit": UNIT, "cores": nt,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# -------------------------------------------------------------- clocks ----
+class ClockSampler:
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        for line in open(self.f.name):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------ our arm ------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_09781_b200 import _capi
+    from paper_2305_09781_b200.tree import TokenTree, TreeBatch
+
+    rank, world, local = dist_env()
+    assert world == args.gpus or "RANK" not in os.environ, "--gpus must match WORLD_SIZE"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- synthetic inputs of the C2 shape (per rank: B requests) ----
+    trees = c2_trees(lambda s: TokenTree.merge_sequences(s, 1 << 20), 1000 + rank, V)
+    batch = TreeBatch([t for t, _ in trees], T)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    Lmax = L + T
+    kc = (torch.rand(B, H, Lmax, D, device=dev, generator=g) * 2 - 1).half()
+    vc = (torch.rand(B, H, Lmax, D, device=dev, generator=g) * 2 - 1).half()
+    q = (torch.rand(B, T, H, D, device=dev, generator=g) * 2 - 1).half()
+    knew = (torch.rand(B, T, H, D, device=dev, generator=g) * 2 - 1).half()
+    vnew = (torch.rand(B, T, H, D, device=dev, generator=g) * 2 - 1).half()
+    logits = torch.randn(B, T, V, device=dev, generator=g)
+    # planted acceptance: each node's argmax is its first child's token w.p. 0.7
+    rng = np.random.default_rng(77 + rank)
+    for b in range(B):
+        for u in range(batch.n_nodes[b]):
+            kids = np.nonzero(batch.parents[b] == u)[0]
+            if kids.size and rng.random() < 0.7:
+                logits[b, u, int(batch.tokens[b, kids[0]])] = 50.0
+    tok = torch.tensor(batch.tokens, device=dev)
+    par = torch.tensor(batch.parents, device=dev)
+    nn = torch.tensor(batch.n_nodes, device=dev)
+    P = torch.full((B,), L, dtype=torch.int32, device=dev)
+    out = torch.empty_like(q)
+    ws_attn = _capi.tree_attention_workspace(q, kc, vc, torch.zeros(B, T, 1, dtype=torch.int64,
+                                                                    device=dev), P, nn)
+    ws_ver = _capi.verify_workspace(B, T, dev)
+    mask = torch.zeros(B, T, 1, dtype=torch.int64, device=dev)
+    path = _capi.tree_attention_path(q, kc, vc, mask, P, nn)
+    gathered = torch.zeros(world * B * (T + 2), dtype=torch.int32, device=dev)
+
+    k1_events = []
+
+    def step(time_k1=False):
+        _capi.kv_append(knew, vnew, P, nn, kc, vc)
+        m = _capi.build_masks(par, nn)
+        if time_k1:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+        _capi.tree_attention(q, kc, vc, m, P, nn, out=out, workspace=ws_attn)
+        if time_k1:
+            e1.record()
+            k1_events.append((e0, e1))
+        _, ver, ids, ln = _capi.verify_greedy(logits, tok, par, nn, workspace=ws_ver,
+                                              want_argmax=False)
+        _capi.kv_compact(ids, ln, P, kc, vc)
+        if world > 1:
+            mine = torch.cat([ver.flatten(), ln])
+            dist.all_gather_into_tensor(gathered[: world * mine.numel()], mine)
+        return ver, ln
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        ver, ln = step()
+    barrier()
+    accepted = int(ln.sum().item())
+
+    clocks = ClockSampler(local)
+    barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        step(time_k1=True)
+    t1.record()
+    barrier()
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    k1_ms = statistics.mean(a.elapsed_time(b) for a, b in k1_events)
+    if world > 1:
+        tt = torch.tensor([ms, k1_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, k1_ms = tt.tolist()
+    ms_step = ms / args.steps
+    value = B * T * world / (ms_step / 1e3)
+
+    # ---- e2e: C-ABI calls with host buffers, copies inside the timed region ----
+    h_q = q.cpu().pin_memory()
+    h_k = knew.cpu().pin_memory()
+    h_v = vnew.cpu().pin_memory()
+    h_topo = torch.tensor(np.concatenate([batch.tokens.ravel(), batch.parents.ravel(),
+                                          batch.n_nodes]), dtype=torch.int32).pin_memory()
+    d_topo = torch.empty_like(h_topo, device=dev)
+    h_out = torch.empty(B * (T + 1) + B, dtype=torch.int32).pin_memory()
+    h2d = (h_q.numel() * 2 + h_k.numel() * 2 + h_v.numel() * 2 + h_topo.numel() * 4)
+    d2h = h_out.numel() * 4
+
+    def e2e_step():
+        q.copy_(h_q, non_blocking=True)
+        knew.copy_(h_k, non_blocking=True)
+        vnew.copy_(h_v, non_blocking=True)
+        d_topo.copy_(h_topo, non_blocking=True)
+        ver, ln = step()
+        h_out[: B * (T + 1)].copy_(ver.flatten(), non_blocking=True)
+        h_out[B * (T + 1):].copy_(ln, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(3):
+        e2e_step()
+    barrier()
+    w0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    barrier()
+    e2e_ms = (time.perf_counter() - w0) * 1e3
+    if world > 1:
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = tt.item()
+    e2e_value = B * T * world / (e2e_ms / args.steps / 1e3)
+
+    # ---- roofline of the dominant kernel (K1) ----
+    s = 2
+    bytes_k1 = s * (2 * B * L * H * D + B * T * H * D + 2 * B * T * H * D + B * T * H * D) + 8 * B * T
+    achieved = bytes_k1 / (k1_ms / 1e3) / 1e9
+    peaks = {}
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        peaks = json.load(open(pk))
+    peak = peaks.get("hbm_gbs", 6650.0)
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        nt = cpu_threads()
+        try:
+            res = reference_sample(min(B, nt), 1, 0, full_tree=True)
+        except Exception as e:  # noqa: BLE001
+            res = None
+            print(f"cpu baseline failed: {e}", file=sys.stderr)
+        if res is not None:
+            cpu = {"value": res["value"], "unit": UNIT, "cores": min(B, nt), "kind": "reference",
+                   "sample": f"{res['requests']} C2 requests (full {res['nodes']}-node tree, KV "
+                             f"2048) through the reference tree_parallel_decode, f64, 1 layer "
+                             f"d=4096 H=32 V=258 ffn_mult=1, one request per thread; "
+                             f"{res['seconds']:.1f} s"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+        "config": {"workload": "C2: LLaMA-7B-shape attention layer, fp16, batch 8/GPU, 64-node "
+                               "tree, KV 2048, greedy verify (V=32000)",
+                   "B_per_gpu": B, "T": T, "L": L, "H": H, "D": D, "V": V,
+                   "parallelism": f"dp{world} (requests partitioned)",
+                   "l2": "inputs larger than L2: 268 MB KV + 65.5 MB logits per step",
+                   "k1_path": "tcgen05" if path == 2 else "cuda-core"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "K1 tree attention", "bytes_per_launch": bytes_k1,
+                     "us_per_launch": k1_ms * 1e3,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+        "clocks": clk,
+        "verified_tokens_per_step": accepted,
+        "verified_tokens_per_s": accepted * world / (ms_step / 1e3),
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,10 +1,218 @@
-// K4 placeholder (multi-step speculative sampling lands in a later commit).
+// K4: stochastic multi-step speculative sampling (MSS) — SpecInfer's
+// stochastic verification, which the reference does NOT implement
+// (SPEC.md:8, :100). Contract: DESIGN.md §5 / SURVEY.md Appendix B; the fp32
+// CPU oracle oracle/restate_mss.c fixes every rounding step, and this kernel
+// reproduces it bit for bit given the same host-supplied uniforms:
+//
+//   u = root
+//   loop: p = softmax(z[u] / tau)
+//         for each child v of u (ascending id): r = U[k++]
+//             accept if r * q_v[t_v] <= p[t_v]      -> emit t_v, u = v, continue loop
+//             else p = norm(max(p - q_v, 0))        (residual renormalisation)
+//         emit inverse-CDF sample of p with r = U[k++]; stop
+//
+// One 256-thread block per request keeps the working distribution p[V] in
+// shared memory. Every vocabulary reduction uses the fixed order of the
+// contract: thread t owns the contiguous chunk [t*CH, (t+1)*CH) and sums it
+// sequentially, warps combine their 32 chunk sums with an xor butterfly and
+// the 8 warp sums are added in order; the exponential is the contract's
+// exp_spec (fma Horner polynomial + exact power-of-two scaling); all fp32
+// operations use explicit _rn intrinsics so nothing is contracted.
+#include <cfloat>
+
 #include "common.cuh"
 
-extern "C" st_status st_verify_mss(const float*, const float*, int, int, int, const int32_t*,
-                                   const int32_t*, const int32_t*, float, const float*, int,
-                                   int32_t*, int32_t*, int32_t*, void*) {
+namespace st {
+namespace {
+
+constexpr int NT = 256;
+
+__device__ __forceinline__ float exp_spec(float x) {
+    if (!(x > -104.0f)) return 0.0f;
+    const float t = __fmul_rn(x, 1.44269504f);
+    const float nf = rintf(t);
+    const float f = __fsub_rn(t, nf);
+    float p = 1.54035304e-4f;
+    p = __fmaf_rn(p, f, 1.33335581e-3f);
+    p = __fmaf_rn(p, f, 9.61812911e-3f);
+    p = __fmaf_rn(p, f, 5.55041087e-2f);
+    p = __fmaf_rn(p, f, 2.40226507e-1f);
+    p = __fmaf_rn(p, f, 6.93147182e-1f);
+    p = __fmaf_rn(p, f, 1.0f);
+    const int n = (int)nf;
+    if (n >= -126) return __fmul_rn(p, __uint_as_float((uint32_t)(n + 127) << 23));
+    return __fmul_rn(__fmul_rn(p, __uint_as_float((uint32_t)(n + 227) << 23)),
+                     __uint_as_float((uint32_t)27 << 23));
+}
+
+// Combine per-thread chunk partials in the contract order; result broadcast.
+__device__ float combine_spec(float part, float* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part = __fadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+    __syncthreads();
+    if (lane == 0) red[warp] = part;
+    __syncthreads();
+    float tot = red[0];
+#pragma unroll
+    for (int w = 1; w < NT / 32; ++w) tot = __fadd_rn(tot, red[w]);
+    return tot;
+}
+
+__device__ float block_max(float v, float* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    float m = red[0];
+#pragma unroll
+    for (int w = 1; w < NT / 32; ++w) m = fmaxf(m, red[w]);
+    return m;
+}
+
+__global__ void __launch_bounds__(NT)
+mss_kernel(const float* __restrict__ logits, const float* __restrict__ q, int T, int V,
+           const int32_t* __restrict__ tokens, const int32_t* __restrict__ parent,
+           const int32_t* __restrict__ n_nodes, float temperature,
+           const float* __restrict__ uniforms, int n_uniforms, int32_t* __restrict__ verified,
+           int32_t* __restrict__ ids, int32_t* __restrict__ len) {
+    extern __shared__ float p[];  // [V]
+    __shared__ float red[NT / 32];
+    __shared__ float cum[NT], csum[NT];
+    __shared__ int sh_pick;
+    const int b = blockIdx.x, tid = threadIdx.x;
+    const int n = n_nodes[b];
+    const int CH = (V + NT - 1) / NT;
+    const int c0 = tid * CH, c1 = min(V, c0 + CH);
+    const int32_t* tok = tokens + (int64_t)b * T;
+    const int32_t* par = parent + (int64_t)b * T;
+    const float* U = uniforms + (int64_t)b * n_uniforms;
+    int32_t* vrow = verified + (int64_t)b * (T + 1);
+    int32_t* irow = ids + (int64_t)b * (T + 1);
+    const float inv_tau = __fdiv_rn(1.0f, temperature);
+    int u = 0, k = 0, m = 0;
+    if (tid == 0) irow[0] = 0;
+
+    for (;;) {
+        __syncthreads();  // every reader of the previous p is done
+        // ---- p = softmax(z[u] / tau) in the contract's arithmetic ----
+        const float* z = logits + ((int64_t)b * T + u) * V;
+        float mx = -INFINITY;
+        for (int i = tid; i < V; i += NT) {
+            const float zi = z[i];
+            p[i] = zi;
+            mx = fmaxf(mx, zi);
+        }
+        mx = block_max(mx, red);
+        for (int i = tid; i < V; i += NT) p[i] = exp_spec(__fmul_rn(__fsub_rn(p[i], mx), inv_tau));
+        __syncthreads();
+        float a = 0.0f;
+        for (int i = c0; i < c1; ++i) a = __fadd_rn(a, p[i]);
+        const float S = combine_spec(a, red);
+        for (int i = tid; i < V; i += NT) p[i] = __fdiv_rn(p[i], S);
+        __syncthreads();
+
+        // ---- children of u in ascending id order ----
+        int next = -1;
+        for (int v = u + 1; v < n; ++v) {
+            if (par[v] != u) continue;
+            const float r = U[k++];
+            const int32_t t = tok[v];
+            const float* qv = q + ((int64_t)b * T + v) * V;
+            if (__fmul_rn(r, qv[t]) <= p[t]) {
+                next = v;
+                break;
+            }
+            float s2 = 0.0f;
+            for (int i = c0; i < c1; ++i) s2 = __fadd_rn(s2, fmaxf(__fsub_rn(p[i], qv[i]), 0.0f));
+            const float S2 = combine_spec(s2, red);
+            if (S2 > 0.0f) {
+                for (int i = c0; i < c1; ++i)
+                    p[i] = __fdiv_rn(fmaxf(__fsub_rn(p[i], qv[i]), 0.0f), S2);
+            }
+            __syncthreads();
+        }
+        if (next >= 0) {
+            if (tid == 0) {
+                vrow[m] = tok[next];
+                irow[m + 1] = next;
+            }
+            ++m;
+            u = next;
+            continue;
+        }
+
+        // ---- inverse-CDF sample of p ----
+        const float r = U[k++];
+        float c = 0.0f;
+        for (int i = c0; i < c1; ++i) c = __fadd_rn(c, p[i]);
+        csum[tid] = c;
+        __syncthreads();
+        if (tid == 0) {
+            float run = 0.0f;
+            for (int t = 0; t < NT; ++t) {
+                run = __fadd_rn(run, csum[t]);
+                cum[t] = run;
+            }
+            const float target = __fmul_rn(r, cum[NT - 1]);
+            int tc = -1;
+            for (int t = 0; t < NT; ++t)
+                if (cum[t] > target) { tc = t; break; }
+            if (tc < 0)
+                for (int t = NT - 1; t >= 0; --t)
+                    if (csum[t] > 0.0f) { tc = t; break; }
+            int pick = 0;
+            if (tc >= 0) {
+                float acc = tc > 0 ? cum[tc - 1] : 0.0f;
+                int last_pos = -1;
+                pick = -1;
+                for (int i = tc * CH; i < min(V, (tc + 1) * CH); ++i) {
+                    acc = __fadd_rn(acc, p[i]);
+                    if (p[i] > 0.0f) last_pos = i;
+                    if (acc > target) { pick = i; break; }
+                }
+                if (pick < 0) pick = last_pos >= 0 ? last_pos : tc * CH;
+            }
+            sh_pick = pick;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            vrow[m] = sh_pick;
+            len[b] = m + 1;
+        }
+        break;
+    }
+}
+
+}  // namespace
+}  // namespace st
+
+extern "C" st_status st_verify_mss(const float* logits, const float* q, int B, int T, int V,
+                                   const int32_t* tokens, const int32_t* parent,
+                                   const int32_t* n_nodes, float temperature,
+                                   const float* uniforms, int n_uniforms, int32_t* verified,
+                                   int32_t* ids, int32_t* len, void* stream) {
     if (st_status e = st::require_device()) return e;
-    st::set_error("st_verify_mss: not built yet");
-    return ST_ERR_UNSUPPORTED;
+    ST_CHECK_ARG(B >= 0 && T >= 1 && V >= 1, ST_ERR_SHAPE_MISMATCH, "bad shape");
+    ST_CHECK_ARG(temperature > 0.0f, ST_ERR_INVALID_ARGUMENT, "temperature must be > 0");
+    ST_CHECK_ARG(n_uniforms >= T + 1, ST_ERR_INVALID_ARGUMENT,
+                 "need n_uniforms >= T + 1 (one per visited child plus the final sample)");
+    if (B == 0) return ST_OK;
+    ST_CHECK_ARG(logits && q && tokens && parent && n_nodes && uniforms && verified && ids && len,
+                 ST_ERR_INVALID_ARGUMENT, "null pointer");
+    const size_t smem = (size_t)V * sizeof(float);
+    ST_CHECK_ARG(smem <= 200 * 1024, ST_ERR_UNSUPPORTED, "vocabulary too large for K4 (V <= 51200)");
+    static size_t attr_set = 0;
+    if (smem > 48 * 1024 && smem > attr_set) {
+        ST_CUDA_TRY(cudaFuncSetAttribute(st::mss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+        attr_set = smem;
+    }
+    st::mss_kernel<<<B, st::NT, smem, st::as_stream(stream)>>>(logits, q, T, V, tokens, parent,
+                                                               n_nodes, temperature, uniforms,
+                                                               n_uniforms, verified, ids, len);
+    ST_LAUNCH_CHECK();
+    return ST_OK;
 }

@@ -10,7 +10,7 @@ import pytest
 import torch
 
 from tests.test_gpu_kernels import check_k1, make_batch, run_k1
-from tests.treegen import pack, width_depth_seqs
+from tests.treegen import expansion_seqs, pack, width_depth_seqs
 
 pytestmark = pytest.mark.gpu
 
@@ -43,15 +43,17 @@ def _dummy(bt, dtype):
     return q, kc, kc, mask, P, n
 
 
-@pytest.mark.parametrize("T,width,depth", [(16, 4, 4), (64, 8, 8), (128, 16, 8), (61, 9, 8)])
+@pytest.mark.parametrize("T,width,depth", [(16, 4, 3), (64, 9, 7), (128, 16, 7), (61, 0, 0)])
 def test_tc_tree_widths(capi, restatement, T, width, depth):
     rng = np.random.default_rng(T)
     trees = []
     for _ in range(3):
-        while True:
-            t = restatement.merge(width_depth_seqs(rng, 5, 32000, width, depth), 4096)
-            if len(t[0]) <= T:
-                break
+        if width == 0:   # C4: merged tree of 3 SSMs, expansion <1,1,3,1,1,1,1,1>
+            seqs = expansion_seqs(rng, 5, 32000, 3, [1, 1, 3, 1, 1, 1, 1, 1])
+        else:
+            seqs = width_depth_seqs(rng, 5, 32000, width, depth)
+        t = restatement.merge(seqs, 4096)
+        assert len(t[0]) <= T
         trees.append(t)
     bt = make_batch(restatement, rng, 3, 4, 4, 128, trees=trees, T=T, P_range=(50, 400),
                     dtype=torch.float16)

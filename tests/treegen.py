@@ -32,3 +32,17 @@ def masks(restatement, par, n, W):
     for b in range(B):
         out[b, : n[b]] = restatement.ancestor_masks(par[b, : n[b]], W)
     return out
+
+
+def expansion_seqs(rng, root, vocab, n_ssm, expansion):
+    """SpecInfer expansion trees: each SSM keeps the
+    top-e_i children per frontier node at depth i (here: random tokens); the
+    SSMs' root-to-leaf paths are returned for merge_sequences. With
+    expansion <1,1,3,1,1,1,1,1> and 3 SSMs this gives the 61-node C4 tree."""
+    seqs = []
+    for _ in range(n_ssm):
+        frontier = [[root]]
+        for e in expansion:
+            frontier = [p + [int(t)] for p in frontier for t in rng.integers(0, vocab, e)]
+        seqs.extend(frontier)
+    return seqs

@@ -1,0 +1,17 @@
+#!/bin/bash
+# One GPU session: parity tests, smoke, bench, ncu launch list + full K1 capture.
+# Usage (from repo root, under gpurun): bash tools/gpu_round.sh <tag>
+TAG=${1:-r}
+OUT=gpurun_out
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $OUT/$TAG.gpu.txt
+timeout 600 python -m pytest tests -m gpu -q --timeout 180 > $OUT/$TAG.pytest.txt 2>&1; echo "pytest rc=$?" >> $OUT/$TAG.pytest.txt
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/$TAG.smoke.txt 2>&1
+timeout 300 python bench.py > $OUT/$TAG.bench.json 2> $OUT/$TAG.bench.err
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -s 40 -c 60 --csv \
+    --log-file $OUT/$TAG.launches.csv python bench.py --steps 8 --warmup 3 --no-cpu-baseline \
+    > /dev/null 2> $OUT/$TAG.ncu1.err
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:tree_attn_tc -s 3 -c 1 \
+    -o $OUT/$TAG.k1 -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
+    > /dev/null 2> $OUT/$TAG.ncu2.err
+ls -la $OUT
