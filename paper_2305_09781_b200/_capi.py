@@ -171,13 +171,17 @@ def verify_workspace(B, T, device="cuda"):
 
 
 def verify_greedy(logits, tokens, parent, n_nodes, budget=None, eos=-1, workspace=None,
-                  stream=None, want_argmax=True):
+                  stream=None, want_argmax=True, out=None):
+    """out: optional preallocated (verified [B,T+1], ids [B,T+1], len [B]) int32."""
     B, T, V = logits.shape
     dev = logits.device
     argmax = torch.empty((B, T), dtype=torch.int32, device=dev) if want_argmax else None
-    verified = torch.full((B, T + 1), -1, dtype=torch.int32, device=dev)
-    ids = torch.full((B, T + 1), -1, dtype=torch.int32, device=dev)
-    length = torch.zeros(B, dtype=torch.int32, device=dev)
+    if out is None:
+        verified = torch.full((B, T + 1), -1, dtype=torch.int32, device=dev)
+        ids = torch.full((B, T + 1), -1, dtype=torch.int32, device=dev)
+        length = torch.zeros(B, dtype=torch.int32, device=dev)
+    else:
+        verified, ids, length = out
     if workspace is None:
         workspace = verify_workspace(B, T, dev)
     check(lib().st_verify_greedy(_ptr(logits), B, T, V, _ptr(tokens), _ptr(parent), _ptr(n_nodes),
@@ -201,9 +205,10 @@ def verify_mss(logits, q, tokens, parent, n_nodes, temperature, uniforms, stream
 
 
 # ---------------------------------------------------------------- masks ----
-def build_masks(parent, n_nodes, W=None, stream=None):
+def build_masks(parent, n_nodes, W=None, stream=None, out=None):
     B, T = parent.shape
     W = W or (T + 63) // 64
-    mask = torch.zeros((B, T, W), dtype=torch.int64, device=parent.device)
+    mask = out if out is not None else torch.empty((B, T, W), dtype=torch.int64,
+                                                   device=parent.device)
     check(lib().st_build_masks(_ptr(parent), _ptr(n_nodes), B, T, W, _ptr(mask), _stream(stream)))
     return mask

@@ -44,25 +44,31 @@ namespace {
 
 using namespace sm100;
 
-constexpr int BM = 128;            // query rows per pair (tree nodes, padded)
 constexpr int BN = 128;            // KV rows per tile
 constexpr int HD = 128;            // head dim
-constexpr int KSTAGES = 2, VSTAGES = 2;
-constexpr uint32_t ATOM_BYTES = 128 * 128;          // 128 rows x 64 elems x 2 B
-constexpr uint32_t TILE_BYTES = 2 * ATOM_BYTES;     // 32 KB
-constexpr int NUM_THREADS = 192;
+constexpr uint32_t KV_ATOM = 128 * 128;             // 128 rows x 64 elems x 2 B
+constexpr uint32_t TILE_BYTES = 2 * KV_ATOM;        // 32 KB K or V tile
+constexpr int NUM_THREADS = 224;                     // 4 softmax + K-TMA + V-TMA + MMA warps
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t TM_O = 256;                       // S0 at 0, S1 at 128, O at 256
-constexpr int SLOT_FLOATS = BM * HD + 2 * BM;        // partial O rows + m + l
+constexpr int SLOT_FLOATS = 128 * HD + 2 * 128;      // partial O rows + m + l
 constexpr float kLazyThreshLog2 = 8.0f;
 
-// dynamic smem layout (offsets from a 1024-aligned base)
-constexpr uint32_t OFF_Q = 0;
-constexpr uint32_t OFF_K = OFF_Q + TILE_BYTES;
-constexpr uint32_t OFF_V = OFF_K + KSTAGES * TILE_BYTES;
-constexpr uint32_t OFF_P = OFF_V + VSTAGES * TILE_BYTES;
-constexpr uint32_t OFF_BAR = OFF_P + TILE_BYTES;
-constexpr uint32_t SMEM_BYTES = OFF_BAR + 256 + 1024;  // + barriers + alignment slack
+// Per-M configuration: M = 64 query rows (T <= 64) or 128 (T <= 128).
+template <int M> struct Cfg {
+    static constexpr int RPW = M / 4;                       // rows per softmax warp
+    static constexpr uint32_t A_ATOM = M * 128;             // M rows x 64 elems x 2 B
+    static constexpr uint32_t A_BYTES = 2 * A_ATOM;         // Q or one P buffer
+    static constexpr int KSTAGES = 2;
+    static constexpr int VSTAGES = M == 64 ? 3 : 2;
+    static constexpr uint32_t OFF_Q = 0;
+    static constexpr uint32_t OFF_P = OFF_Q + A_BYTES;      // 2 P buffers
+    static constexpr uint32_t OFF_K = OFF_P + 2 * A_BYTES;
+    static constexpr uint32_t OFF_V = OFF_K + KSTAGES * TILE_BYTES;
+    static constexpr uint32_t OFF_BAR = OFF_V + VSTAGES * TILE_BYTES;
+    static constexpr uint32_t SMEM_BYTES = OFF_BAR + 256 + 1024;
+    static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+};
 
 struct TcParams {
     const int32_t* prefix_len;
@@ -139,28 +145,43 @@ template <> struct pk2<__nv_bfloat16> {
 };
 
 template <class T>
+__device__ __forceinline__ void store_row(T* dst_row, const float* v, float scale) {
+    uint4* dst = reinterpret_cast<uint4*>(dst_row);
+#pragma unroll
+    for (int ch = 0; ch < HD / 8; ++ch) {
+        uint32_t w4[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            w4[k] = pk2<T>::pack(v[ch * 8 + 2 * k] * scale, v[ch * 8 + 2 * k + 1] * scale);
+        dst[ch] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    }
+}
+
+template <class T, int M>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const TcParams p) {
+    using C = Cfg<M>;
+    constexpr int KS = C::KSTAGES, VS = C::VSTAGES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    uint8_t* sm_q = smem + OFF_Q;
-    uint8_t* sm_k = smem + OFF_K;
-    uint8_t* sm_v = smem + OFF_V;
-    uint8_t* sm_p = smem + OFF_P;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint8_t* sm_q = smem + C::OFF_Q;
+    uint8_t* sm_p = smem + C::OFF_P;
+    uint8_t* sm_k = smem + C::OFF_K;
+    uint8_t* sm_v = smem + C::OFF_V;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
     uint64_t* q_full = bars + 0;
     uint64_t* q_empty = bars + 1;
-    uint64_t* k_full = bars + 2;              // [KSTAGES]
-    uint64_t* k_empty = k_full + KSTAGES;     // [KSTAGES]
-    uint64_t* v_full = k_empty + KSTAGES;     // [VSTAGES]
-    uint64_t* v_empty = v_full + VSTAGES;     // [VSTAGES]
-    uint64_t* s_full = v_empty + VSTAGES;     // [2]
-    uint64_t* s_empty = s_full + 2;           // [2]
-    uint64_t* p_full = s_empty + 2;
-    uint64_t* pv_done = p_full + 1;
-    uint64_t* o_empty = pv_done + 1;
+    uint64_t* k_full = bars + 2;         // [KS]
+    uint64_t* k_empty = k_full + KS;     // [KS]
+    uint64_t* v_full = k_empty + KS;     // [VS]
+    uint64_t* v_empty = v_full + VS;     // [VS]
+    uint64_t* s_full = v_empty + VS;     // [2]
+    uint64_t* s_empty = s_full + 2;      // [2]
+    uint64_t* p_full = s_empty + 2;      // [2]
+    uint64_t* pv_done = p_full + 2;      // [2]
+    uint64_t* o_empty = pv_done + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
     __shared__ int merge_flag;
 
@@ -169,20 +190,23 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (threadIdx.x == 0) {
         mbar_init(q_full, 1);
         mbar_init(q_empty, 1);
-        for (int i = 0; i < KSTAGES; ++i) { mbar_init(k_full + i, 1); mbar_init(k_empty + i, 1); }
-        for (int i = 0; i < VSTAGES; ++i) { mbar_init(v_full + i, 1); mbar_init(v_empty + i, 1); }
-        for (int i = 0; i < 2; ++i) { mbar_init(s_full + i, 1); mbar_init(s_empty + i, 128); }
-        mbar_init(p_full, 128);
-        mbar_init(pv_done, 1);
+        for (int i = 0; i < KS; ++i) { mbar_init(k_full + i, 1); mbar_init(k_empty + i, 1); }
+        for (int i = 0; i < VS; ++i) { mbar_init(v_full + i, 1); mbar_init(v_empty + i, 1); }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(s_full + i, 1);
+            mbar_init(s_empty + i, 128);
+            mbar_init(p_full + i, 128);
+            mbar_init(pv_done + i, 1);
+        }
         mbar_init(o_empty, 128);
         fence_barrier_init();
     }
     if (warp == 4 && lane == 0) {
         prefetch_tmap(&tm_q);
         prefetch_tmap(&tm_k);
-        prefetch_tmap(&tm_v);
     }
-    if (warp == 5) tmem_alloc<TMEM_COLS>(tmem_slot);
+    if (warp == 5 && lane == 0) prefetch_tmap(&tm_v);
+    if (warp == 6) tmem_alloc<TMEM_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -194,63 +218,71 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     const long long t_end = range_start(blockIdx.x + 1, total, G);
 
     if (warp == 4) {
-        // ============================ TMA producer ============================
+        // ======================= TMA producer: Q and K =========================
         if (lane == 0) {
-            uint32_t qc = 0, kc = 0, vc = 0;
+            uint32_t qc = 0, kc = 0;
             for (long long t = t_begin; t < t_end;) {
                 const Seg s = find_seg(p, t, t_end);
                 mbar_wait(q_empty, (qc & 1) ^ 1);
-                mbar_arrive_expect_tx(q_full, TILE_BYTES);
+                mbar_arrive_expect_tx(q_full, C::A_BYTES);
                 tma_load_4d(sm_q, &tm_q, q_full, 0, s.h, 0, s.b);
-                tma_load_4d(sm_q + ATOM_BYTES, &tm_q, q_full, 64, s.h, 0, s.b);
+                tma_load_4d(sm_q + C::A_ATOM, &tm_q, q_full, 64, s.h, 0, s.b);
                 ++qc;
                 const int bh = s.b * p.H + s.h;
-                for (int j = s.lo; j < s.hi; ++j) {
-                    {
-                        const uint32_t st = kc % KSTAGES, ph = (kc / KSTAGES) & 1;
-                        mbar_wait(k_empty + st, ph ^ 1);
-                        mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
-                        uint8_t* dst = sm_k + st * TILE_BYTES;
-                        tma_load_3d(dst, &tm_k, k_full + st, 0, j * BN, bh);
-                        tma_load_3d(dst + ATOM_BYTES, &tm_k, k_full + st, 64, j * BN, bh);
-                        ++kc;
-                    }
-                    {
-                        const uint32_t st = vc % VSTAGES, ph = (vc / VSTAGES) & 1;
-                        mbar_wait(v_empty + st, ph ^ 1);
-                        mbar_arrive_expect_tx(v_full + st, TILE_BYTES);
-                        uint8_t* dst = sm_v + st * TILE_BYTES;
-                        tma_load_3d(dst, &tm_v, v_full + st, 0, j * BN, bh);
-                        tma_load_3d(dst + ATOM_BYTES, &tm_v, v_full + st, 64, j * BN, bh);
-                        ++vc;
-                    }
+                for (int j = s.lo; j < s.hi; ++j, ++kc) {
+                    const uint32_t st = kc % KS, ph = (kc / KS) & 1;
+                    mbar_wait(k_empty + st, ph ^ 1);
+                    mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
+                    uint8_t* dst = sm_k + st * TILE_BYTES;
+                    tma_load_3d(dst, &tm_k, k_full + st, 0, j * BN, bh);
+                    tma_load_3d(dst + KV_ATOM, &tm_k, k_full + st, 64, j * BN, bh);
                 }
                 t += s.hi - s.lo;
             }
         }
     } else if (warp == 5) {
+        // =========================== TMA producer: V ============================
+        if (lane == 0) {
+            uint32_t vc = 0;
+            for (long long t = t_begin; t < t_end;) {
+                const Seg s = find_seg(p, t, t_end);
+                const int bh = s.b * p.H + s.h;
+                for (int j = s.lo; j < s.hi; ++j, ++vc) {
+                    const uint32_t st = vc % VS, ph = (vc / VS) & 1;
+                    mbar_wait(v_empty + st, ph ^ 1);
+                    mbar_arrive_expect_tx(v_full + st, TILE_BYTES);
+                    uint8_t* dst = sm_v + st * TILE_BYTES;
+                    tma_load_3d(dst, &tm_v, v_full + st, 0, j * BN, bh);
+                    tma_load_3d(dst + KV_ATOM, &tm_v, v_full + st, 64, j * BN, bh);
+                }
+                t += s.hi - s.lo;
+            }
+        }
+    } else if (warp == 6) {
         // ============================ MMA issuer ==============================
         if (lane == 0) {
             constexpr uint32_t fmt = std::is_same<T, __half>::value ? 0u : 1u;
-            constexpr uint32_t idS = idesc_f16(fmt, BM, BN, 0, 0);   // Q K^T: both K-major
-            constexpr uint32_t idPV = idesc_f16(fmt, BM, HD, 0, 1);  // P V: V is MN-major
+            constexpr uint32_t idS = idesc_f16(fmt, M, BN, 0, 0);   // Q K^T: both K-major
+            constexpr uint32_t idPV = idesc_f16(fmt, M, HD, 0, 1);  // P V: V is MN-major
             const uint32_t q_base = smem_u32(sm_q), k_base = smem_u32(sm_k);
             const uint32_t v_base = smem_u32(sm_v), p_base = smem_u32(sm_p);
             uint32_t qc = 0, kc = 0, vc = 0, sc = 0, pc = 0, segc = 0;
             auto issue_pv = [&](int i_local) {
-                mbar_wait(p_full, pc & 1);
-                const uint32_t st = vc % VSTAGES;
-                mbar_wait(v_full + st, (vc / VSTAGES) & 1);
+                const uint32_t pb = pc & 1;
+                mbar_wait(p_full + pb, (pc >> 1) & 1);
+                const uint32_t st = vc % VS;
+                mbar_wait(v_full + st, (vc / VS) & 1);
                 if (i_local == 0) mbar_wait(o_empty, (segc & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t vb = v_base + st * TILE_BYTES;
+                const uint32_t pbase = p_base + pb * C::A_BYTES;
 #pragma unroll
                 for (int kk = 0; kk < BN / 16; ++kk) {
-                    const uint64_t a = smem_desc(p_base + (kk >> 2) * ATOM_BYTES + (kk & 3) * 32, 16, 1024);
-                    const uint64_t b = smem_desc(vb + kk * 2048, ATOM_BYTES, 1024);
+                    const uint64_t a = smem_desc(pbase + (kk >> 2) * C::A_ATOM + (kk & 3) * 32, 16, 1024);
+                    const uint64_t b = smem_desc(vb + kk * 2048, KV_ATOM, 1024);
                     umma_f16_ss(tmem + TM_O, a, b, idPV, (i_local > 0 || kk > 0) ? 1u : 0u);
                 }
-                umma_commit(pv_done);
+                umma_commit(pv_done + pb);
                 umma_commit(v_empty + st);
                 ++vc;
                 ++pc;
@@ -261,17 +293,18 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 mbar_wait(q_full, qc & 1);
                 ++qc;
                 for (int i = 0; i < ntl; ++i) {
-                    const uint32_t st = kc % KSTAGES;
-                    mbar_wait(k_full + st, (kc / KSTAGES) & 1);
+                    const uint32_t st = kc % KS;
+                    mbar_wait(k_full + st, (kc / KS) & 1);
                     const uint32_t sb = sc & 1;
                     mbar_wait(s_empty + sb, ((sc >> 1) & 1) ^ 1);
                     tc_fence_after();
                     const uint32_t kb = k_base + st * TILE_BYTES;
 #pragma unroll
                     for (int kk = 0; kk < HD / 16; ++kk) {
-                        const uint32_t off = (kk >> 2) * ATOM_BYTES + (kk & 3) * 32;
-                        umma_f16_ss(tmem + sb * BN, smem_desc(q_base + off, 16, 1024),
-                                    smem_desc(kb + off, 16, 1024), idS, kk > 0 ? 1u : 0u);
+                        umma_f16_ss(tmem + sb * BN,
+                                    smem_desc(q_base + (kk >> 2) * C::A_ATOM + (kk & 3) * 32, 16, 1024),
+                                    smem_desc(kb + (kk >> 2) * KV_ATOM + (kk & 3) * 32, 16, 1024),
+                                    idS, kk > 0 ? 1u : 0u);
                     }
                     umma_commit(s_full + sb);
                     umma_commit(k_empty + st);
@@ -287,17 +320,21 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
     } else {
         // ===================== softmax + epilogue (warps 0-3) ==================
-        const int r = threadIdx.x;  // query row == TMEM lane
+        // TMEM lane 32*warp + lane holds query row warp*RPW + lane (lane < RPW),
+        // for both the M=128 (full) and M=64 (half-subpartition) layouts.
+        const bool row_lane = lane < C::RPW;
+        const int r = warp * C::RPW + (row_lane ? lane : 0);
         const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
         const float c = p.c_log2;
         const float thresh_raw = kLazyThreshLog2 / c;
-        uint32_t sc = 0, pvc = 0;
+        uint32_t sc = 0, pc = 0;
         for (long long t = t_begin; t < t_end;) {
             const Seg s = find_seg(p, t, t_end);
             const int ntl = s.hi - s.lo;
             const int n = __ldg(p.n_nodes + s.b);
             const int P = __ldg(p.prefix_len + s.b);
-            const bool valid = r < n;
+            const bool valid = row_lane && r < n;
+            const bool warp_live = __any_sync(0xffffffffu, valid);
             uint64_t mw0 = 0, mw1 = 0;
             if (valid) {
                 const uint64_t* mr = p.mask + ((long long)s.b * p.T + r) * p.W;
@@ -308,143 +345,142 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             for (int i = 0; i < ntl; ++i) {
                 const int j = s.lo + i;
                 const uint32_t sb = sc & 1;
-                mbar_wait(s_full + sb, (sc >> 1) & 1);
-                tc_fence_after();
-                float sv[BN];
-#pragma unroll
-                for (int ch = 0; ch < BN / 32; ++ch) {
-                    uint32_t raw[32];
-                    tmem_ld_32x32b_x32(lane_addr + sb * BN + ch * 32, raw);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int k = 0; k < 32; ++k) sv[ch * 32 + k] = __uint_as_float(raw[k]);
-                }
-                tc_fence_before();
-                mbar_arrive(s_empty + sb);
-                ++sc;
-
-                const int row0 = j * BN;
-                if (row0 + BN > P) {  // tile reaches the tree (or past it): apply the mask
-#pragma unroll
-                    for (int k = 0; k < BN; ++k) {
-                        const int ra = row0 + k;
-                        bool vis = ra < P;
-                        if (!vis) {
-                            const int v = ra - P;
-                            vis = v < n && (((v < 64 ? mw0 : mw1) >> (v & 63)) & 1ull);
-                        }
-                        if (!vis) sv[k] = -INFINITY;
-                    }
-                }
-                float mx = -INFINITY;
-#pragma unroll
-                for (int k = 0; k < BN; ++k) mx = fmaxf(mx, sv[k]);
-                const float m_new = fmaxf(m, mx);
-
-                // P buffer free and O stable once the previous P.V retired
-                if (i > 0) {
-                    mbar_wait(pv_done, pvc & 1);
-                    ++pvc;
+                const uint32_t pb = pc & 1;
+                if (warp_live) {
+                    float sv[BN];
+                    mbar_wait(s_full + sb, (sc >> 1) & 1);
                     tc_fence_after();
-                }
-                float alpha = 1.f;
-                bool rescale = false;
-                if (m == -INFINITY) {
-                    m = m_new;  // nothing with nonzero weight accumulated yet
-                } else if (m_new - m > thresh_raw) {
-                    alpha = ex2((m - m_new) * c);
-                    l *= alpha;
-                    m = m_new;
-                    rescale = true;
-                }
-                if (__any_sync(0xffffffffu, rescale && valid)) {
 #pragma unroll
-                    for (int ch = 0; ch < HD / 32; ++ch) {
+                    for (int ch = 0; ch < BN / 32; ++ch) {
                         uint32_t raw[32];
-                        tmem_ld_32x32b_x32(lane_addr + TM_O + ch * 32, raw);
+                        tmem_ld_32x32b_x32(lane_addr + sb * BN + ch * 32, raw);
                         tmem_ld_wait();
 #pragma unroll
-                        for (int k = 0; k < 32; ++k)
-                            raw[k] = __float_as_uint(__uint_as_float(raw[k]) * alpha);
-                        tmem_st_32x32b_x32(lane_addr + TM_O + ch * 32, raw);
+                        for (int k = 0; k < 32; ++k) sv[ch * 32 + k] = __uint_as_float(raw[k]);
                     }
-                    tmem_st_wait();
-                }
-                const float base = (m == -INFINITY) ? 0.f : m * c;
-                float lsum = 0.f;
-                uint8_t* prow = sm_p + r * 128;
+                    tc_fence_before();
+                    mbar_arrive(s_empty + sb);
+                    const int row0 = j * BN;
+                    if (row0 + BN > P) {  // tile reaches the tree (or past it): apply the mask
 #pragma unroll
-                for (int ch = 0; ch < BN / 8; ++ch) {
-                    uint32_t w4[4];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const float p0 = ex2(fmaf(sv[ch * 8 + 2 * k], c, -base));
-                        const float p1 = ex2(fmaf(sv[ch * 8 + 2 * k + 1], c, -base));
-                        lsum += p0 + p1;
-                        w4[k] = pk2<T>::pack(p0, p1);
+                        for (int k = 0; k < BN; ++k) {
+                            const int ra = row0 + k;
+                            bool vis = ra < P;
+                            if (!vis) {
+                                const int v = ra - P;
+                                vis = v < n && (((v < 64 ? mw0 : mw1) >> (v & 63)) & 1ull);
+                            }
+                            if (!vis) sv[k] = -INFINITY;
+                        }
                     }
-                    const uint32_t atom = ch >> 3, cin = ch & 7;
-                    *reinterpret_cast<uint4*>(prow + atom * ATOM_BYTES + ((cin ^ (r & 7)) << 4)) =
-                        make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                    float mx = -INFINITY;
+#pragma unroll
+                    for (int k = 0; k < BN; ++k) mx = fmaxf(mx, sv[k]);
+                    const float m_new = fmaxf(m, mx);
+
+                    // P buffer pb was last read by P.V number pc-2
+                    mbar_wait(pv_done + pb, ((pc >> 1) & 1) ^ 1);
+                    float alpha = 1.f;
+                    bool rescale = false;
+                    if (m == -INFINITY) {
+                        m = m_new;  // nothing with nonzero weight accumulated yet
+                    } else if (m_new - m > thresh_raw) {
+                        alpha = ex2((m - m_new) * c);
+                        l *= alpha;
+                        m = m_new;
+                        rescale = true;
+                    }
+                    if (__any_sync(0xffffffffu, rescale && valid)) {
+                        // O must be stable: wait for P.V number pc-1 (this segment, i > 0)
+                        const uint32_t q1 = pc - 1;
+                        mbar_wait(pv_done + (q1 & 1), (q1 >> 1) & 1);
+                        tc_fence_after();
+#pragma unroll
+                        for (int ch = 0; ch < HD / 32; ++ch) {
+                            uint32_t raw[32];
+                            tmem_ld_32x32b_x32(lane_addr + TM_O + ch * 32, raw);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int k = 0; k < 32; ++k)
+                                raw[k] = __float_as_uint(__uint_as_float(raw[k]) * alpha);
+                            tmem_st_32x32b_x32(lane_addr + TM_O + ch * 32, raw);
+                        }
+                        tmem_st_wait();
+                    }
+                    const float base = (m == -INFINITY) ? 0.f : m * c;
+                    float lsum = 0.f;
+                    uint8_t* prow = sm_p + pb * C::A_BYTES + r * 128;
+#pragma unroll
+                    for (int ch = 0; ch < BN / 8; ++ch) {
+                        uint32_t w4[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const float p0 = ex2(fmaf(sv[ch * 8 + 2 * k], c, -base));
+                            const float p1 = ex2(fmaf(sv[ch * 8 + 2 * k + 1], c, -base));
+                            lsum += p0 + p1;
+                            w4[k] = pk2<T>::pack(p0, p1);
+                        }
+                        const uint32_t atom = ch >> 3, cin = ch & 7;
+                        if (row_lane)
+                            *reinterpret_cast<uint4*>(prow + atom * C::A_ATOM + ((cin ^ (r & 7)) << 4)) =
+                                make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                    }
+                    l += lsum;
+                    fence_proxy_async_smem();
+                    tc_fence_before();
+                } else {
+                    mbar_arrive(s_empty + sb);
                 }
-                l += lsum;
-                fence_proxy_async_smem();
-                tc_fence_before();
-                mbar_arrive(p_full);
+                ++sc;
+                mbar_arrive(p_full + pb);
+                ++pc;
             }
 
             // ---- segment epilogue: O row from TMEM ----
-            mbar_wait(pv_done, pvc & 1);
-            ++pvc;
-            tc_fence_after();
-            float ov[HD];
-#pragma unroll
-            for (int ch = 0; ch < HD / 32; ++ch) {
-                uint32_t raw[32];
-                tmem_ld_32x32b_x32(lane_addr + TM_O + ch * 32, raw);
-                tmem_ld_wait();
-#pragma unroll
-                for (int k = 0; k < 32; ++k) ov[ch * 32 + k] = __uint_as_float(raw[k]);
-            }
-            tc_fence_before();
-            mbar_arrive(o_empty);
-
             const bool full = (s.lo == 0 && s.hi == s.ntiles);
-            if (full) {
+            const int slot = (t == t_begin) ? 0 : 1;
+            float* sp = p.partial + ((long long)blockIdx.x * 2 + slot) * SLOT_FLOATS;
+            T* out_row = reinterpret_cast<T*>(p.o) + (((long long)s.b * p.T + r) * p.H + s.h) * HD;
+            if (warp_live) {
+                const uint32_t q1 = pc - 1;
+                mbar_wait(pv_done + (q1 & 1), (q1 >> 1) & 1);
+                tc_fence_after();
+                float ov[HD];
+#pragma unroll
+                for (int ch = 0; ch < HD / 32; ++ch) {
+                    uint32_t raw[32];
+                    tmem_ld_32x32b_x32(lane_addr + TM_O + ch * 32, raw);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) ov[ch * 32 + k] = __uint_as_float(raw[k]);
+                }
+                tc_fence_before();
+                mbar_arrive(o_empty);
                 if (valid) {
-                    const float inv = 1.f / l;
-                    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(p.o) +
-                                                          (((long long)s.b * p.T + r) * p.H + s.h) * HD);
+                    if (full) {
+                        store_row<T>(out_row, ov, 1.f / l);
+                        if (p.lse) p.lse[((long long)s.b * p.H + s.h) * p.T + r] = m * p.scale + __logf(l);
+                    } else {
+                        float4* po = reinterpret_cast<float4*>(sp + r * HD);
 #pragma unroll
-                    for (int ch = 0; ch < HD / 8; ++ch) {
-                        uint32_t w4[4];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            w4[k] = pk2<T>::pack(ov[ch * 8 + 2 * k] * inv, ov[ch * 8 + 2 * k + 1] * inv);
-                        dst[ch] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                        for (int k = 0; k < HD / 4; ++k)
+                            po[k] = make_float4(ov[4 * k], ov[4 * k + 1], ov[4 * k + 2], ov[4 * k + 3]);
+                        sp[128 * HD + r] = m;
+                        sp[128 * HD + 128 + r] = l;
                     }
-                    if (p.lse)
-                        p.lse[((long long)s.b * p.H + s.h) * p.T + r] = m * p.scale + __logf(l);
                 }
             } else {
-                // partial piece -> workspace slot, last finisher of the pair merges
-                const long long my_start = range_start(blockIdx.x, total, G);
-                const int slot = (t == my_start) ? 0 : 1;
-                float* sp = p.partial + ((long long)blockIdx.x * 2 + slot) * SLOT_FLOATS;
-                if (valid) {
-                    float4* po = reinterpret_cast<float4*>(sp + r * HD);
-#pragma unroll
-                    for (int k = 0; k < HD / 4; ++k)
-                        po[k] = make_float4(ov[4 * k], ov[4 * k + 1], ov[4 * k + 2], ov[4 * k + 3]);
-                    sp[BM * HD + r] = m;
-                    sp[BM * HD + BM + r] = l;
-                }
+                mbar_arrive(o_empty);
+            }
+
+            if (!full) {
+                // partial piece written above; the last finisher of the pair merges
                 __threadfence();
                 named_bar_sync(1, 128);
                 const long long pair_end = s.pair_start + s.ntiles;
                 const long long c_first = cta_of(s.pair_start, total, G);
                 const long long c_last = cta_of(pair_end - 1, total, G);
-                if (r == 0) {
+                if (threadIdx.x == 0) {
                     // CTAs with an empty range (total < #SMs) contribute no piece
                     unsigned pieces = 0;
                     for (long long cc = c_first; cc <= c_last; ++cc)
@@ -456,13 +492,13 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 if (merge_flag) {
                     __threadfence();
                     if (valid) {
-                        float M = -INFINITY;
+                        float M_ = -INFINITY;
                         for (long long cc = c_first; cc <= c_last; ++cc) {
                             const long long rs = range_start(cc, total, G);
                             if (range_start(cc + 1, total, G) == rs) continue;  // empty range
                             const int sl = (s.pair_start > rs) ? 1 : 0;
                             const float* q = p.partial + (cc * 2 + sl) * SLOT_FLOATS;
-                            M = fmaxf(M, __ldcg(q + BM * HD + r));
+                            M_ = fmaxf(M_, __ldcg(q + 128 * HD + r));
                         }
                         float acc[HD];
 #pragma unroll
@@ -470,13 +506,13 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         float L = 0.f;
                         for (long long cc = c_first; cc <= c_last; ++cc) {
                             const long long rs = range_start(cc, total, G);
-                            if (range_start(cc + 1, total, G) == rs) continue;  // empty range
+                            if (range_start(cc + 1, total, G) == rs) continue;
                             const int sl = (s.pair_start > rs) ? 1 : 0;
                             const float* q = p.partial + (cc * 2 + sl) * SLOT_FLOATS;
-                            const float mk = __ldcg(q + BM * HD + r);
+                            const float mk = __ldcg(q + 128 * HD + r);
                             if (mk == -INFINITY) continue;
-                            const float w = ex2((mk - M) * c);
-                            L += w * __ldcg(q + BM * HD + BM + r);
+                            const float w = ex2((mk - M_) * c);
+                            L += w * __ldcg(q + 128 * HD + 128 + r);
                             const float4* qo = reinterpret_cast<const float4*>(q + r * HD);
 #pragma unroll
                             for (int k = 0; k < HD / 4; ++k) {
@@ -487,21 +523,11 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                                 acc[4 * k + 3] += w * x.w;
                             }
                         }
-                        const float inv = 1.f / L;
-                        uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<T*>(p.o) +
-                                                              (((long long)s.b * p.T + r) * p.H + s.h) * HD);
-#pragma unroll
-                        for (int ch = 0; ch < HD / 8; ++ch) {
-                            uint32_t w4[4];
-#pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                w4[k] = pk2<T>::pack(acc[ch * 8 + 2 * k] * inv, acc[ch * 8 + 2 * k + 1] * inv);
-                            dst[ch] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-                        }
+                        store_row<T>(out_row, acc, 1.f / L);
                         if (p.lse)
-                            p.lse[((long long)s.b * p.H + s.h) * p.T + r] = M * p.scale + __logf(L);
+                            p.lse[((long long)s.b * p.H + s.h) * p.T + r] = M_ * p.scale + __logf(L);
                     }
-                    if (r == 0) p.tickets[s.b * p.H + s.h] = 0u;
+                    if (threadIdx.x == 0) p.tickets[s.b * p.H + s.h] = 0u;
                 }
             }
             t += ntl;
@@ -511,7 +537,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 5) tmem_dealloc<TMEM_COLS>(tmem);
+    if (warp == 6) tmem_dealloc<TMEM_COLS>(tmem);
 }
 
 // ------------------------------------------------------------------ host --
@@ -555,7 +581,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 bool tree_attention_tc_supported(const st_attn_args* a) {
     auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
     return (a->dtype == ST_F16 || a->dtype == ST_BF16) && a->D == HD && a->H == a->Hkv &&
-           a->T <= BM && a->W <= 2 && a->Lmax < (1ll << 31) && al(a->q) && al(a->k_cache) &&
+           a->T <= 128 && a->W <= 2 && a->Lmax < (1ll << 31) && al(a->q) && al(a->k_cache) &&
            al(a->v_cache) && al(a->o) && (int64_t)a->B * a->H < (1ll << 31);
 }
 
@@ -564,6 +590,18 @@ size_t tree_attention_tc_workspace(const st_attn_args* a) {
            (size_t)a->B * a->H * sizeof(unsigned);
 }
 
+#define ST_TRY_LAUNCH_TC(TT, MM)                                                                \
+    do {                                                                                        \
+        static bool attr = false;                                                               \
+        if (!attr) {                                                                            \
+            ST_CUDA_TRY(cudaFuncSetAttribute(tree_attn_tc_kernel<TT, MM>,                       \
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                             Cfg<MM>::SMEM_BYTES));                             \
+            attr = true;                                                                        \
+        }                                                                                       \
+        tree_attn_tc_kernel<TT, MM><<<G, NUM_THREADS, Cfg<MM>::SMEM_BYTES, stream>>>(tq, tk, tv, prm); \
+    } while (0)
+
 st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     const CUtensorMapDataType dt =
         a->dtype == ST_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
@@ -571,7 +609,7 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     {
         const uint64_t dims[4] = {(uint64_t)HD, (uint64_t)a->H, (uint64_t)a->T, (uint64_t)a->B};
         const uint64_t strides[3] = {HD * 2ull, (uint64_t)a->H * HD * 2, (uint64_t)a->T * a->H * HD * 2};
-        const uint32_t box[4] = {64, 1, BM, 1};
+        const uint32_t box[4] = {64, 1, (uint32_t)(a->T <= 64 ? 64 : 128), 1};
         if (!encode(&tq, dt, 4, a->q, dims, strides, box)) {
             set_error("st_tree_attention: cuTensorMapEncodeTiled(q) failed");
             return ST_ERR_CUDA;
@@ -603,22 +641,11 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     prm.W = a->W;
     prm.scale = (float)a->scale;
     prm.c_log2 = (float)(a->scale * 1.4426950408889634);
+    const bool m64 = a->T <= 64;
     if (a->dtype == ST_F16) {
-        static bool attr = false;
-        if (!attr) {
-            ST_CUDA_TRY(cudaFuncSetAttribute(tree_attn_tc_kernel<__half>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-            attr = true;
-        }
-        tree_attn_tc_kernel<__half><<<G, NUM_THREADS, SMEM_BYTES, stream>>>(tq, tk, tv, prm);
+        if (m64) { ST_TRY_LAUNCH_TC(__half, 64); } else { ST_TRY_LAUNCH_TC(__half, 128); }
     } else {
-        static bool attr = false;
-        if (!attr) {
-            ST_CUDA_TRY(cudaFuncSetAttribute(tree_attn_tc_kernel<__nv_bfloat16>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-            attr = true;
-        }
-        tree_attn_tc_kernel<__nv_bfloat16><<<G, NUM_THREADS, SMEM_BYTES, stream>>>(tq, tk, tv, prm);
+        if (m64) { ST_TRY_LAUNCH_TC(__nv_bfloat16, 64); } else { ST_TRY_LAUNCH_TC(__nv_bfloat16, 128); }
     }
     ST_LAUNCH_CHECK();
     return ST_OK;

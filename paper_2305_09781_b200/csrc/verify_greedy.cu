@@ -173,25 +173,26 @@ greedy_verify_kernel(const float* __restrict__ logits, int T, int V,
     if (lane == 0) tickets[b] = 0;  // reusable workspace
 }
 
+// One thread per (request, node): walk the parent chain (depth <= T) and set
+// the ancestor-or-self bits; no inter-thread dependency, one launch per batch.
 __global__ void build_masks_kernel(const int32_t* __restrict__ parent,
                                    const int32_t* __restrict__ n_nodes, int T, int W,
                                    uint64_t* __restrict__ mask) {
-    // one warp per request; lane w owns mask word w (W <= 32 words = 2048 nodes)
-    const int b = blockIdx.x, w = threadIdx.x;
+    const int b = blockIdx.y;
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= T) return;
     const int n = n_nodes[b];
     const int32_t* par = parent + (int64_t)b * T;
-    uint64_t* mb = mask + (int64_t)b * T * W;
-    for (int u = 0; u < T; ++u) {
-        uint64_t word = 0;
-        if (u < n) {
-            const int p = par[u];
-            if (p >= 0 && w < W) word = mb[(int64_t)p * W + w];
-            if (w == (u >> 6)) word |= 1ull << (u & 63);
-        }
-        __syncwarp();
-        if (w < W) mb[(int64_t)u * W + w] = word;
-        __syncwarp();
+    uint64_t* mu = mask + ((int64_t)b * T + u) * W;
+    uint64_t w[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) w[i] = 0;
+    if (u < n) {
+        for (int v = u; v >= 0; v = par[v]) w[v >> 6] |= 1ull << (v & 63);
     }
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+        if (i < W) mu[i] = w[i];
 }
 
 }  // namespace
@@ -247,7 +248,8 @@ st_status st_build_masks(const int32_t* parent, const int32_t* n_nodes, int B, i
                  "bad shape (need ceil(T/64) <= W <= 32)");
     if (B == 0) return ST_OK;
     ST_CHECK_ARG(parent && n_nodes && mask, ST_ERR_INVALID_ARGUMENT, "null pointer");
-    st::build_masks_kernel<<<B, 32, 0, st::as_stream(stream)>>>(parent, n_nodes, T, W, mask);
+    const dim3 grid((T + 127) / 128, B);
+    st::build_masks_kernel<<<grid, 128, 0, st::as_stream(stream)>>>(parent, n_nodes, T, W, mask);
     ST_LAUNCH_CHECK();
     return ST_OK;
 }

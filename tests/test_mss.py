@@ -32,7 +32,7 @@ def make_case(restatement, rng, V, width=3, depth=4, n_req=1, peaked=3.0):
             q[b, v] *= 0.3
             q[b, v, tok[b, v]] += 0.7
             if rng.random() < 0.5:
-                logits[b, par[b, v], tok[b, v]] += 4.0
+                logits[b, par[b, v], tok[b, v]] += 6.0 * peaked
     return tok, par, n, logits, q
 
 
