@@ -2,7 +2,7 @@
  *
  * This is the drop-in boundary: plain pointers and sizes,
  * no torch or C++ types. The C++ headers in include/spectree/ (same
- * declarations as the reference's proj/include/spectree/*.hpp) sit on top of
+ * declarations as the reference's proj/include/spectree headers) sit on top of
  * it, and so do the Python ctypes bindings (paper_2305_09781_b200/_capi.py).
  *
  * Conventions

@@ -227,6 +227,12 @@ def main():
     eng.update(prompt=prompt, incremental=inc, incremental_steps=np.array(inc_steps),
                speculative=spec, speculative_steps=np.array(spec_steps))
     np.savez_compressed(os.path.join(GOLDEN, "engine_toy.npz"), **eng)
+    # plain-text copy for the C++ engine parity test (tests/cpp/engine_parity_test.cpp)
+    with open(os.path.join(GOLDEN, "engine_toy.txt"), "w") as f:
+        f.write(" ".join(map(str, ecfg)) + " 31\n")
+        f.write(f"{len(prompt)} " + " ".join(map(str, prompt.tolist())) + "\n")
+        f.write(f"{len(inc)} " + " ".join(map(str, inc.tolist())) + "\n")
+        f.write(f"{inc_steps} {spec_steps}\n")
     print("golden fixtures written to", GOLDEN)
     for f in sorted(os.listdir(GOLDEN)):
         print(f"  {f}: {os.path.getsize(os.path.join(GOLDEN, f))} bytes")

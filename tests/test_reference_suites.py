@@ -1,0 +1,28 @@
+"""The reference's OWN C++ unit suites (proj/tests/token_tree_test.cpp and
+proj/tests/transformer_test.cpp, compiled unchanged by tests/cpp/Makefile
+against include/spectree + libspectree_b200.so) and our engine parity test,
+run on the GPU. Tolerances are the reference's own (tokens exact, logits
+<= 1e-9, bitwise where the reference asserts bitwise)."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "build", "reftests")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["token_tree_test", "transformer_test", "engine_parity_test"])
+def test_suite(name):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    path = os.path.join(BIN, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not built (tests/cpp/Makefile needs /root/reference at build time)")
+    r = subprocess.run([path], capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:])
+    assert r.returncode == 0, r.stdout[-6000:] + r.stderr[-2000:]
+    assert "failed: 0" in r.stdout
