@@ -31,6 +31,8 @@
 #include <cudaTypedefs.h>
 
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <type_traits>
 #include <unordered_map>
@@ -81,7 +83,14 @@ struct TcParams {
     int B, T, H, W;
     float c_log2;        // scale * log2(e)
     float scale;
+    unsigned long long* trace;  // optional pipeline trace of CTA 0 (ST_K1_TRACE)
 };
+
+#define K1_TRACE(slot, idx)                                                       \
+    do {                                                                          \
+        if (p.trace && blockIdx.x == 0 && (idx) < 64)                             \
+            p.trace[(slot) * 64 + (idx)] = clock64();                             \
+    } while (0)
 
 struct Seg {
     int b, h, lo, hi, ntiles;
@@ -232,6 +241,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 for (int j = s.lo; j < s.hi; ++j, ++kc) {
                     const uint32_t st = kc % KS, ph = (kc / KS) & 1;
                     mbar_wait(k_empty + st, ph ^ 1);
+                    K1_TRACE(0, kc);
                     mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
                     uint8_t* dst = sm_k + st * TILE_BYTES;
                     tma_load_3d(dst, &tm_k, k_full + st, 0, j * BN, bh);
@@ -250,6 +260,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 for (int j = s.lo; j < s.hi; ++j, ++vc) {
                     const uint32_t st = vc % VS, ph = (vc / VS) & 1;
                     mbar_wait(v_empty + st, ph ^ 1);
+                    K1_TRACE(1, vc);
                     mbar_arrive_expect_tx(v_full + st, TILE_BYTES);
                     uint8_t* dst = sm_v + st * TILE_BYTES;
                     tma_load_3d(dst, &tm_v, v_full + st, 0, j * BN, bh);
@@ -272,6 +283,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 mbar_wait(p_full + pb, (pc >> 1) & 1);
                 const uint32_t st = vc % VS;
                 mbar_wait(v_full + st, (vc / VS) & 1);
+                K1_TRACE(7, vc);
                 if (i_local == 0) mbar_wait(o_empty, (segc & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t vb = v_base + st * TILE_BYTES;
@@ -282,6 +294,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     const uint64_t b = smem_desc(vb + kk * 2048, KV_ATOM, 1024);
                     umma_f16_ss(tmem + TM_O, a, b, idPV, (i_local > 0 || kk > 0) ? 1u : 0u);
                 }
+                K1_TRACE(3, pc);
                 umma_commit(pv_done + pb);
                 umma_commit(v_empty + st);
                 ++vc;
@@ -295,6 +308,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 for (int i = 0; i < ntl; ++i) {
                     const uint32_t st = kc % KS;
                     mbar_wait(k_full + st, (kc / KS) & 1);
+                    K1_TRACE(6, kc);
                     const uint32_t sb = sc & 1;
                     mbar_wait(s_empty + sb, ((sc >> 1) & 1) ^ 1);
                     tc_fence_after();
@@ -306,6 +320,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                                     smem_desc(kb + (kk >> 2) * KV_ATOM + (kk & 3) * 32, 16, 1024),
                                     idS, kk > 0 ? 1u : 0u);
                     }
+                    K1_TRACE(2, sc);
                     umma_commit(s_full + sb);
                     umma_commit(k_empty + st);
                     if (i == ntl - 1) umma_commit(q_empty);
@@ -349,6 +364,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 if (warp_live) {
                     float sv[BN];
                     mbar_wait(s_full + sb, (sc >> 1) & 1);
+                    if (threadIdx.x == 0) K1_TRACE(4, sc);
                     tc_fence_after();
 #pragma unroll
                     for (int ch = 0; ch < BN / 32; ++ch) {
@@ -429,9 +445,14 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     fence_proxy_async_smem();
                     tc_fence_before();
                 } else {
+                    // rows all padding: no TMEM traffic or math, but the same
+                    // waits as live warps so every arrival lands in its own phase
+                    mbar_wait(s_full + sb, (sc >> 1) & 1);
                     mbar_arrive(s_empty + sb);
+                    mbar_wait(pv_done + pb, ((pc >> 1) & 1) ^ 1);
                 }
                 ++sc;
+                if (threadIdx.x == 0) K1_TRACE(5, pc);
                 mbar_arrive(p_full + pb);
                 ++pc;
             }
@@ -470,6 +491,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     }
                 }
             } else {
+                const uint32_t q1 = pc - 1;
+                mbar_wait(pv_done + (q1 & 1), (q1 >> 1) & 1);
                 mbar_arrive(o_empty);
             }
 
@@ -641,6 +664,13 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     prm.W = a->W;
     prm.scale = (float)a->scale;
     prm.c_log2 = (float)(a->scale * 1.4426950408889634);
+    prm.trace = nullptr;
+    static unsigned long long* trace_buf = nullptr;
+    if (getenv("ST_K1_TRACE")) {
+        if (!trace_buf) cudaMalloc(&trace_buf, 8 * 64 * sizeof(unsigned long long));
+        cudaMemsetAsync(trace_buf, 0, 8 * 64 * sizeof(unsigned long long), stream);
+        prm.trace = trace_buf;
+    }
     const bool m64 = a->T <= 64;
     if (a->dtype == ST_F16) {
         if (m64) { ST_TRY_LAUNCH_TC(__half, 64); } else { ST_TRY_LAUNCH_TC(__half, 128); }
@@ -648,6 +678,18 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
         if (m64) { ST_TRY_LAUNCH_TC(__nv_bfloat16, 64); } else { ST_TRY_LAUNCH_TC(__nv_bfloat16, 128); }
     }
     ST_LAUNCH_CHECK();
+    if (prm.trace) {  // diagnostic only: dump CTA 0's pipeline timestamps
+        unsigned long long h[8 * 64];
+        cudaMemcpyAsync(h, prm.trace, sizeof h, cudaMemcpyDeviceToHost, stream);
+        cudaStreamSynchronize(stream);
+        if (FILE* f = fopen(getenv("ST_K1_TRACE"), "a")) {
+            for (int r = 0; r < 8; ++r) {
+                for (int i = 0; i < 64; ++i) fprintf(f, "%llu ", h[r * 64 + i]);
+                fprintf(f, "\n");
+            }
+            fclose(f);
+        }
+    }
     return ST_OK;
 }
 

@@ -5,7 +5,7 @@ TAG=${1:-r}
 OUT=gpurun_out
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $OUT/$TAG.gpu.txt
-timeout 600 python -m pytest tests -m gpu -q --timeout 180 > $OUT/$TAG.pytest.txt 2>&1; echo "pytest rc=$?" >> $OUT/$TAG.pytest.txt
+timeout 900 python -m pytest tests -m gpu -q --timeout 240 --timeout-method=thread > $OUT/$TAG.pytest.txt 2>&1; echo "pytest rc=$?" >> $OUT/$TAG.pytest.txt
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/$TAG.smoke.txt 2>&1
 timeout 300 python bench.py > $OUT/$TAG.bench.json 2> $OUT/$TAG.bench.err
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -s 40 -c 60 --csv \

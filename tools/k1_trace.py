@@ -1,0 +1,35 @@
+"""Diagnostic: run K1 at the C2 shape with ST_K1_TRACE set and print CTA 0's
+per-tile pipeline timeline (cycles relative to the first K load)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/k1_trace.txt"
+os.environ["ST_K1_TRACE"] = out
+if os.path.exists(out):
+    os.remove(out)
+from paper_2305_09781_b200 import _capi  # noqa: E402
+
+B, T, H, D, L = 8, 64, 32, 128, 2048
+dev = "cuda"
+q = torch.randn(B, T, H, D, device=dev).half()
+kc = torch.randn(B, H, L + T, D, device=dev).half()
+vc = torch.randn(B, H, L + T, D, device=dev).half()
+par = torch.tensor([[-1] + [0] * (T - 1)] * B, dtype=torch.int32, device=dev)
+n = torch.full((B,), T, dtype=torch.int32, device=dev)
+P = torch.full((B,), L, dtype=torch.int32, device=dev)
+mask = _capi.build_masks(par, n)
+ws = _capi.tree_attention_workspace(q, kc, vc, mask, P, n)
+for _ in range(3):
+    _capi.tree_attention(q, kc, vc, mask, P, n, workspace=ws)
+torch.cuda.synchronize()
+rows = [list(map(int, l.split())) for l in open(out)][-8:]
+t = np.array(rows, dtype=np.int64)
+t0 = t[0][t[0] > 0].min()
+names = ["K issue", "V issue", "S issue", "PV issue", "S ready(smx)", "P done(smx)", "K full(mma)", "V full(mma)"]
+print("tile " + " ".join(f"{x:>12s}" for x in names))
+for i in range(30):
+    print(f"{i:4d} " + " ".join(f"{(t[r][i] - t0) if t[r][i] else -1:12d}" for r in range(8)))
