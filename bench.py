@@ -199,6 +199,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2305_09781_b200 import _capi
+    from paper_2305_09781_b200.dist import gather_accepted
     from paper_2305_09781_b200.tree import TokenTree, TreeBatch
 
     rank, world, local = dist_env()
@@ -258,9 +259,8 @@ def main():
         _, ver, ids, ln = _capi.verify_greedy(logits, tok, par, nn, workspace=ws_ver,
                                               want_argmax=False, out=vout)
         _capi.kv_compact(ids, ln, P, kc, vc)
-        if world > 1:
-            mine = torch.cat([ver.flatten(), ln])
-            dist.all_gather_into_tensor(gathered[: world * mine.numel()], mine)
+        if world > 1:   # DP exchange: every rank sees every request's accepted tokens
+            gather_accepted(ver, ln, world, out=gathered)
         return ver, ln
 
     def barrier():

@@ -11,10 +11,11 @@
 //   * engine step (proj/src/engine.cpp:110-121): budget truncation, then the
 //     EOS cut.
 //
-// Work split: one 256-thread block per (request, node) streams that node's
-// logits row once (HBM-bound: 4*V bytes per node, float4 loads, 8 in flight
-// per thread); the last block of a request to finish (atomic ticket, reset by
-// the walker so the workspace is reusable) runs the walk with one warp:
+// Work split: kSplit 256-thread blocks per (request, node) stream slices of
+// that node's logits row once (HBM-bound: 4*V bytes per node, float4 loads)
+// and fold their best (value, lowest index) into one 64-bit order-preserving
+// key with atomicMax (order-independent, hence deterministic); the last block
+// of a request (atomic ticket, reset with the keys for reuse) runs the walk:
 // children of u are the ids v > u with parent[v] == u, scanned 32 at a time
 // with a ballot.
 #include <cfloat>
@@ -25,18 +26,6 @@ namespace st {
 namespace {
 
 constexpr int kThreads = 256;
-
-struct ArgBest {
-    float v;
-    int i;
-};
-
-// a "beats" b under first-index-of-max ordering (NaN already mapped to -inf).
-__device__ __forceinline__ bool beats(float av, int ai, float bv, int bi) {
-    return av > bv || (av == bv && ai < bi);
-}
-
-__device__ __forceinline__ float sanitize(float x) { return x != x ? -INFINITY : x; }
 
 // Alg.-2 walk (reference token_tree.cpp:153-175) + engine truncation
 // (engine.cpp:110-121) for request b, executed by one full warp. `outs` holds
@@ -92,85 +81,98 @@ __global__ void walk_kernel(const int32_t* __restrict__ outs, int T,
               threadIdx.x & 31, false);
 }
 
+// Order-preserving 64-bit key: high word = orderable float bits, low word =
+// ~index, so an unsigned max picks the largest value and, among equal values,
+// the LOWEST index (reference tie rule). NaN maps to -inf (never wins); a NaN
+// at index 0 gets the maximal key (the reference never replaces index 0).
+__device__ __forceinline__ unsigned long long arg_key(float v, int i) {
+    if (v != v) {
+        if (i == 0) return ~0ull;
+        v = -INFINITY;
+    }
+    uint32_t u = __float_as_uint(v);
+    u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    return ((unsigned long long)u << 32) | (uint32_t)(~(uint32_t)i);
+}
+__device__ __forceinline__ int key_index(unsigned long long k) {
+    return k == ~0ull ? 0 : (int)(~(uint32_t)(k & 0xffffffffu));
+}
+
+constexpr int kSplit = 4;   // blocks per logits row
+
 __global__ void __launch_bounds__(kThreads)
 greedy_verify_kernel(const float* __restrict__ logits, int T, int V,
                      const int32_t* __restrict__ tokens, const int32_t* __restrict__ parent,
                      const int32_t* __restrict__ n_nodes, const int32_t* __restrict__ budget,
-                     int32_t eos, int32_t* __restrict__ argmax_out, int32_t* argmax_ws,
-                     int32_t* __restrict__ verified, int32_t* __restrict__ ids,
+                     int32_t eos, int32_t* __restrict__ argmax_out, unsigned long long* keys,
+                     int32_t* argmax_ws, int32_t* __restrict__ verified, int32_t* __restrict__ ids,
                      int32_t* __restrict__ len, unsigned* tickets) {
-    const int u = blockIdx.x, b = blockIdx.y;
+    const int part = blockIdx.x, u = blockIdx.y, b = blockIdx.z;
     const int n = n_nodes[b];
     if (u >= n) return;
     const float* row = logits + ((int64_t)b * T + u) * V;
-
-    // ---- argmax over the row (first index of the maximum) ----
-    float bv = -INFINITY;
-    int bi = 0x7fffffff;
-    const bool aligned = ((reinterpret_cast<uintptr_t>(row) & 15) == 0);
-    int i0 = 0;
-    if (aligned) {
+    // this block's slice of the row, in float4 units when the row is aligned
+    const bool vec = ((reinterpret_cast<uintptr_t>(row) & 15) == 0) && (V % 4 == 0);
+    unsigned long long best = 0;
+    if (vec) {
         const int nv = V >> 2;
+        const int per = (nv + kSplit - 1) / kSplit;
+        const int lo = part * per, hi = min(nv, lo + per);
         const float4* r4 = reinterpret_cast<const float4*>(row);
-        constexpr int U = 8;
-        for (int base = threadIdx.x; base < nv; base += kThreads * U) {
+        constexpr int U = 4;
+        for (int base = lo + threadIdx.x; base < hi; base += kThreads * U) {
             float4 x[U];
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 const int j = base + k * kThreads;
-                x[k] = j < nv ? __ldg(r4 + j) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+                x[k] = j < hi ? __ldcs(r4 + j) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
             }
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 const int j = (base + k * kThreads) * 4;
-                if (j < V) {
-                    const float e0 = sanitize(x[k].x), e1 = sanitize(x[k].y), e2 = sanitize(x[k].z),
-                                e3 = sanitize(x[k].w);
-                    if (beats(e0, j, bv, bi)) { bv = e0; bi = j; }
-                    if (beats(e1, j + 1, bv, bi)) { bv = e1; bi = j + 1; }
-                    if (beats(e2, j + 2, bv, bi)) { bv = e2; bi = j + 2; }
-                    if (beats(e3, j + 3, bv, bi)) { bv = e3; bi = j + 3; }
+                if (j < hi * 4) {
+                    best = max(best, arg_key(x[k].x, j));
+                    best = max(best, arg_key(x[k].y, j + 1));
+                    best = max(best, arg_key(x[k].z, j + 2));
+                    best = max(best, arg_key(x[k].w, j + 3));
                 }
             }
         }
-        i0 = nv * 4;
-    }
-    for (int j = i0 + threadIdx.x; j < V; j += kThreads) {
-        const float e = sanitize(row[j]);
-        if (beats(e, j, bv, bi)) { bv = e; bi = j; }
+    } else {
+        const int per = (V + kSplit - 1) / kSplit;
+        const int lo = part * per, hi = min(V, lo + per);
+        for (int j = lo + threadIdx.x; j < hi; j += kThreads) best = max(best, arg_key(row[j], j));
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (beats(ov, oi, bv, bi)) { bv = ov; bi = oi; }
-    }
-    __shared__ ArgBest red[kThreads / 32];
+    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    __shared__ unsigned long long red[kThreads / 32];
     __shared__ bool is_last;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) red[warp] = {bv, bi};
+    if (lane == 0) red[warp] = best;
     __syncthreads();
     if (threadIdx.x == 0) {
-        ArgBest best = red[0];
-        for (int w = 1; w < kThreads / 32; ++w)
-            if (beats(red[w].v, red[w].i, best.v, best.i)) best = red[w];
-        // reference rule: a NaN at index 0 is never replaced.
-        const float x0 = row[0];
-        int arg = (x0 != x0) ? 0 : best.i;
-        if (arg == 0x7fffffff) arg = 0;  // all entries NaN-mapped: index 0
-        argmax_ws[(int64_t)b * T + u] = arg;
-        if (argmax_out) argmax_out[(int64_t)b * T + u] = arg;
+        for (int w = 1; w < kThreads / 32; ++w) best = max(best, red[w]);
+        atomicMax(keys + (int64_t)b * T + u, best);
         __threadfence();
         const unsigned t = atomicAdd(&tickets[b], 1u);
-        is_last = (t == (unsigned)n - 1);
+        is_last = (t == (unsigned)n * kSplit - 1);
     }
     __syncthreads();
     if (!is_last || warp != 0) return;
 
-    // ---- Alg.-2 walk by the last block of request b (one warp) ----
+    // ---- last block of request b: resolve argmax, walk, reset workspace ----
     __threadfence();
+    int32_t* am = argmax_ws + (int64_t)b * T;
+    for (int v = lane; v < n; v += 32) {
+        unsigned long long* kp = keys + (int64_t)b * T + v;
+        const int a = key_index(atomicExch(kp, 0ull));  // read + reset for reuse
+        am[v] = a;
+        if (argmax_out) argmax_out[(int64_t)b * T + v] = a;
+    }
+    __syncwarp();
+    __threadfence_block();
     walk_warp(argmax_ws, tokens, parent, n, T, b, budget, eos, verified, ids, len, lane, true);
-    if (lane == 0) tickets[b] = 0;  // reusable workspace
+    if (lane == 0) tickets[b] = 0;
 }
 
 // One thread per (request, node): walk the parent chain (depth <= T) and set
@@ -201,8 +203,8 @@ __global__ void build_masks_kernel(const int32_t* __restrict__ parent,
 extern "C" {
 
 size_t st_verify_workspace_size(int B, int T) {
-    // tickets [B] + argmax scratch [B][T]
-    return (size_t)B * sizeof(unsigned) + (size_t)B * T * sizeof(int32_t) + 256;
+    // keys [B][T] u64 | tickets [B] | argmax scratch [B][T]   (zeroed once by the caller)
+    return (size_t)B * T * 8 + (size_t)B * sizeof(unsigned) + (size_t)B * T * sizeof(int32_t) + 512;
 }
 
 st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32_t* tokens,
@@ -215,13 +217,16 @@ st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32
     ST_CHECK_ARG(logits && tokens && parent && n_nodes && verified && ids && len && workspace,
                  ST_ERR_INVALID_ARGUMENT, "null pointer");
     ST_CHECK_ARG(B <= 65535 && T <= 2147483647, ST_ERR_SHAPE_MISMATCH, "too many requests");
-    unsigned* tickets = reinterpret_cast<unsigned*>(workspace);
+    ST_CHECK_ARG((reinterpret_cast<uintptr_t>(workspace) & 7) == 0, ST_ERR_INVALID_ARGUMENT,
+                 "workspace must be 8-byte aligned");
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(workspace);
+    unsigned* tickets = reinterpret_cast<unsigned*>(keys + (size_t)B * T);
     int32_t* scratch = reinterpret_cast<int32_t*>(
         (reinterpret_cast<uintptr_t>(tickets + B) + 15) & ~uintptr_t(15));
-    const dim3 grid(T, B);
+    const dim3 grid(st::kSplit, T, B);
     st::greedy_verify_kernel<<<grid, st::kThreads, 0, st::as_stream(stream)>>>(
-        logits, T, V, tokens, parent, n_nodes, budget, eos, argmax, scratch, verified, ids, len,
-        tickets);
+        logits, T, V, tokens, parent, n_nodes, budget, eos, argmax, keys, scratch, verified, ids,
+        len, tickets);
     ST_LAUNCH_CHECK();
     return ST_OK;
 }
