@@ -376,6 +376,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     }
                     tc_fence_before();
                     mbar_arrive(s_empty + sb);
+                    if (threadIdx.x == 0) K1_TRACE(8, sc);
                     const int row0 = j * BN;
                     if (row0 + BN > P) {  // tile reaches the tree (or past it): apply the mask
 #pragma unroll
@@ -393,9 +394,11 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 #pragma unroll
                     for (int k = 0; k < BN; ++k) mx = fmaxf(mx, sv[k]);
                     const float m_new = fmaxf(m, mx);
+                    if (threadIdx.x == 0) K1_TRACE(9, sc);
 
                     // P buffer pb was last read by P.V number pc-2
                     mbar_wait(pv_done + pb, ((pc >> 1) & 1) ^ 1);
+                    if (threadIdx.x == 0) K1_TRACE(10, sc);
                     float alpha = 1.f;
                     bool rescale = false;
                     if (m == -INFINITY) {
@@ -423,6 +426,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         }
                         tmem_st_wait();
                     }
+                    if (threadIdx.x == 0) K1_TRACE(11, sc);
                     const float base = (m == -INFINITY) ? 0.f : m * c;
                     float lsum = 0.f;
                     uint8_t* prow = sm_p + pb * C::A_BYTES + r * 128;
@@ -667,8 +671,8 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     prm.trace = nullptr;
     static unsigned long long* trace_buf = nullptr;
     if (getenv("ST_K1_TRACE")) {
-        if (!trace_buf) cudaMalloc(&trace_buf, 8 * 64 * sizeof(unsigned long long));
-        cudaMemsetAsync(trace_buf, 0, 8 * 64 * sizeof(unsigned long long), stream);
+        if (!trace_buf) cudaMalloc(&trace_buf, 12 * 64 * sizeof(unsigned long long));
+        cudaMemsetAsync(trace_buf, 0, 12 * 64 * sizeof(unsigned long long), stream);
         prm.trace = trace_buf;
     }
     const bool m64 = a->T <= 64;
@@ -679,11 +683,11 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     }
     ST_LAUNCH_CHECK();
     if (prm.trace) {  // diagnostic only: dump CTA 0's pipeline timestamps
-        unsigned long long h[8 * 64];
+        unsigned long long h[12 * 64];
         cudaMemcpyAsync(h, prm.trace, sizeof h, cudaMemcpyDeviceToHost, stream);
         cudaStreamSynchronize(stream);
         if (FILE* f = fopen(getenv("ST_K1_TRACE"), "a")) {
-            for (int r = 0; r < 8; ++r) {
+            for (int r = 0; r < 12; ++r) {
                 for (int i = 0; i < 64; ++i) fprintf(f, "%llu ", h[r * 64 + i]);
                 fprintf(f, "\n");
             }

@@ -26,10 +26,10 @@ ws = _capi.tree_attention_workspace(q, kc, vc, mask, P, n)
 for _ in range(3):
     _capi.tree_attention(q, kc, vc, mask, P, n, workspace=ws)
 torch.cuda.synchronize()
-rows = [list(map(int, l.split())) for l in open(out)][-8:]
+rows = [list(map(int, l.split())) for l in open(out)][-12:]
 t = np.array(rows, dtype=np.int64)
 t0 = t[0][t[0] > 0].min()
-names = ["K issue", "V issue", "S issue", "PV issue", "S ready(smx)", "P done(smx)", "K full(mma)", "V full(mma)"]
+names = ["K issue", "V issue", "S issue", "PV issue", "S ready", "P done", "K full(mma)", "V full(mma)", "S loaded", "masked+max", "pv wait done", "rescaled"]
 print("tile " + " ".join(f"{x:>12s}" for x in names))
 for i in range(30):
-    print(f"{i:4d} " + " ".join(f"{(t[r][i] - t0) if t[r][i] else -1:12d}" for r in range(8)))
+    print(f"{i:4d} " + " ".join(f"{(t[r][i] - t0) if t[r][i] else -1:12d}" for r in range(12)))
