@@ -51,20 +51,22 @@ constexpr int HD = 128;            // head dim
 constexpr uint32_t KV_ATOM = 128 * 128;             // 128 rows x 64 elems x 2 B
 constexpr uint32_t TILE_BYTES = 2 * KV_ATOM;        // 32 KB K or V tile
 constexpr int NUM_THREADS = 224;                     // 4 softmax + K-TMA + V-TMA + MMA warps
-constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t TM_O = 256;                       // S0 at 0, S1 at 128, O at 256
 constexpr int SLOT_FLOATS = 128 * HD + 2 * 128;      // partial O rows + m + l
 constexpr float kLazyThreshLog2 = 8.0f;
 
 // Per-M configuration: M = 64 query rows (T <= 64) or 128 (T <= 128).
 template <int M> struct Cfg {
-    static constexpr int RPW = M / 4;                       // rows per softmax warp
+    static constexpr int SPLIT = M == 64 ? 2 : 1;           // threads per query row
     static constexpr uint32_t A_ATOM = M * 128;             // M rows x 64 elems x 2 B
     static constexpr uint32_t A_BYTES = 2 * A_ATOM;         // Q or one P buffer
+    static constexpr int QSTAGES = M == 64 ? 2 : 1;
     static constexpr int KSTAGES = 2;
     static constexpr int VSTAGES = M == 64 ? 3 : 2;
+    static constexpr uint32_t S_COLS = BN / SPLIT;          // TMEM columns per S buffer
+    static constexpr uint32_t O_COL = 2 * S_COLS;           // O accumulator column
+    static constexpr uint32_t TMEM_COLS = M == 64 ? 256 : 512;
     static constexpr uint32_t OFF_Q = 0;
-    static constexpr uint32_t OFF_P = OFF_Q + A_BYTES;      // 2 P buffers
+    static constexpr uint32_t OFF_P = OFF_Q + QSTAGES * A_BYTES;  // 2 P buffers
     static constexpr uint32_t OFF_K = OFF_P + 2 * A_BYTES;
     static constexpr uint32_t OFF_V = OFF_K + KSTAGES * TILE_BYTES;
     static constexpr uint32_t OFF_BAR = OFF_V + VSTAGES * TILE_BYTES;
@@ -153,11 +155,11 @@ template <> struct pk2<__nv_bfloat16> {
     }
 };
 
-template <class T>
+template <class T, int NCOL>
 __device__ __forceinline__ void store_row(T* dst_row, const float* v, float scale) {
     uint4* dst = reinterpret_cast<uint4*>(dst_row);
 #pragma unroll
-    for (int ch = 0; ch < HD / 8; ++ch) {
+    for (int ch = 0; ch < NCOL / 8; ++ch) {
         uint32_t w4[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k)
@@ -171,7 +173,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const TcParams p) {
     using C = Cfg<M>;
-    constexpr int KS = C::KSTAGES, VS = C::VSTAGES;
+    constexpr int KS = C::KSTAGES, VS = C::VSTAGES, QS = C::QSTAGES;
+    constexpr int SPLIT = C::SPLIT;          // threads per query row (2 for M=64)
+    constexpr int COLS = BN / SPLIT;         // S columns per thread per tile
+    constexpr int DCOLS = HD / SPLIT;        // O columns per thread
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -180,9 +185,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     uint8_t* sm_k = smem + C::OFF_K;
     uint8_t* sm_v = smem + C::OFF_V;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-    uint64_t* q_full = bars + 0;
-    uint64_t* q_empty = bars + 1;
-    uint64_t* k_full = bars + 2;         // [KS]
+    uint64_t* q_full = bars;             // [QS]
+    uint64_t* q_empty = q_full + QS;     // [QS]
+    uint64_t* k_full = q_empty + QS;     // [KS]
     uint64_t* k_empty = k_full + KS;     // [KS]
     uint64_t* v_full = k_empty + KS;     // [VS]
     uint64_t* v_empty = v_full + VS;     // [VS]
@@ -197,8 +202,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
-        mbar_init(q_full, 1);
-        mbar_init(q_empty, 1);
+        for (int i = 0; i < QS; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
         for (int i = 0; i < KS; ++i) { mbar_init(k_full + i, 1); mbar_init(k_empty + i, 1); }
         for (int i = 0; i < VS; ++i) { mbar_init(v_full + i, 1); mbar_init(v_empty + i, 1); }
         for (int i = 0; i < 2; ++i) {
@@ -215,7 +219,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         prefetch_tmap(&tm_k);
     }
     if (warp == 5 && lane == 0) prefetch_tmap(&tm_v);
-    if (warp == 6) tmem_alloc<TMEM_COLS>(tmem_slot);
+    if (warp == 6) tmem_alloc<C::TMEM_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -232,10 +236,11 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             uint32_t qc = 0, kc = 0;
             for (long long t = t_begin; t < t_end;) {
                 const Seg s = find_seg(p, t, t_end);
-                mbar_wait(q_empty, (qc & 1) ^ 1);
-                mbar_arrive_expect_tx(q_full, C::A_BYTES);
-                tma_load_4d(sm_q, &tm_q, q_full, 0, s.h, 0, s.b);
-                tma_load_4d(sm_q + C::A_ATOM, &tm_q, q_full, 64, s.h, 0, s.b);
+                const uint32_t qb = qc % QS;
+                mbar_wait(q_empty + qb, ((qc / QS) & 1) ^ 1);
+                mbar_arrive_expect_tx(q_full + qb, C::A_BYTES);
+                tma_load_4d(sm_q + qb * C::A_BYTES, &tm_q, q_full + qb, 0, s.h, 0, s.b);
+                tma_load_4d(sm_q + qb * C::A_BYTES + C::A_ATOM, &tm_q, q_full + qb, 64, s.h, 0, s.b);
                 ++qc;
                 const int bh = s.b * p.H + s.h;
                 for (int j = s.lo; j < s.hi; ++j, ++kc) {
@@ -271,11 +276,18 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
     } else if (warp == 6) {
         // ============================ MMA issuer ==============================
+        // M=128: S = Q K^T (N=128) and O += P V (N=128), one accumulator each.
+        // M=64 : every product is split into two N=64 MMAs whose accumulators
+        //        land in TMEM lanes 0-15 and 16-31 of each subpartition (the
+        //        interleaved M=64 layout), so all 32 softmax lanes hold data:
+        //        S kv-rows 0-63 | 64-127 and O d 0-63 | 64-127.
         if (lane == 0) {
             constexpr uint32_t fmt = std::is_same<T, __half>::value ? 0u : 1u;
-            constexpr uint32_t idS = idesc_f16(fmt, M, BN, 0, 0);   // Q K^T: both K-major
-            constexpr uint32_t idPV = idesc_f16(fmt, M, HD, 0, 1);  // P V: V is MN-major
-            const uint32_t q_base = smem_u32(sm_q), k_base = smem_u32(sm_k);
+            constexpr uint32_t NS = BN / SPLIT, NO = HD / SPLIT;
+            constexpr uint32_t idS = idesc_f16(fmt, M, NS, 0, 0);   // Q K^T: both K-major
+            constexpr uint32_t idPV = idesc_f16(fmt, M, NO, 0, 1);  // P V: V is MN-major
+            constexpr uint32_t HI_LANES = 16u << 16;                // lane offset of the 2nd half
+            const uint32_t q_base0 = smem_u32(sm_q), k_base = smem_u32(sm_k);
             const uint32_t v_base = smem_u32(sm_v), p_base = smem_u32(sm_p);
             uint32_t qc = 0, kc = 0, vc = 0, sc = 0, pc = 0, segc = 0;
             auto issue_pv = [&](int i_local) {
@@ -291,8 +303,14 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 #pragma unroll
                 for (int kk = 0; kk < BN / 16; ++kk) {
                     const uint64_t a = smem_desc(pbase + (kk >> 2) * C::A_ATOM + (kk & 3) * 32, 16, 1024);
-                    const uint64_t b = smem_desc(vb + kk * 2048, KV_ATOM, 1024);
-                    umma_f16_ss(tmem + TM_O, a, b, idPV, (i_local > 0 || kk > 0) ? 1u : 0u);
+                    const uint32_t acc = (i_local > 0 || kk > 0) ? 1u : 0u;
+                    if constexpr (SPLIT == 1) {
+                        umma_f16_ss(tmem + C::O_COL, a, smem_desc(vb + kk * 2048, KV_ATOM, 1024), idPV, acc);
+                    } else {
+                        umma_f16_ss(tmem + C::O_COL, a, smem_desc(vb + kk * 2048, KV_ATOM, 1024), idPV, acc);
+                        umma_f16_ss(tmem + HI_LANES + C::O_COL, a,
+                                    smem_desc(vb + KV_ATOM + kk * 2048, KV_ATOM, 1024), idPV, acc);
+                    }
                 }
                 K1_TRACE(3, pc);
                 umma_commit(pv_done + pb);
@@ -303,8 +321,10 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             for (long long t = t_begin; t < t_end;) {
                 const Seg s = find_seg(p, t, t_end);
                 const int ntl = s.hi - s.lo;
-                mbar_wait(q_full, qc & 1);
+                const uint32_t qb = qc % QS;
+                mbar_wait(q_full + qb, (qc / QS) & 1);
                 ++qc;
+                const uint32_t q_base = q_base0 + qb * C::A_BYTES;
                 for (int i = 0; i < ntl; ++i) {
                     const uint32_t st = kc % KS;
                     mbar_wait(k_full + st, (kc / KS) & 1);
@@ -313,17 +333,25 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     mbar_wait(s_empty + sb, ((sc >> 1) & 1) ^ 1);
                     tc_fence_after();
                     const uint32_t kb = k_base + st * TILE_BYTES;
+                    const uint32_t scol = sb * C::S_COLS;
 #pragma unroll
                     for (int kk = 0; kk < HD / 16; ++kk) {
-                        umma_f16_ss(tmem + sb * BN,
-                                    smem_desc(q_base + (kk >> 2) * C::A_ATOM + (kk & 3) * 32, 16, 1024),
-                                    smem_desc(kb + (kk >> 2) * KV_ATOM + (kk & 3) * 32, 16, 1024),
-                                    idS, kk > 0 ? 1u : 0u);
+                        const uint32_t off = (kk >> 2) * C::A_ATOM + (kk & 3) * 32;
+                        const uint32_t koff = (kk >> 2) * KV_ATOM + (kk & 3) * 32;
+                        const uint64_t a = smem_desc(q_base + off, 16, 1024);
+                        const uint32_t acc = kk > 0 ? 1u : 0u;
+                        if constexpr (SPLIT == 1) {
+                            umma_f16_ss(tmem + scol, a, smem_desc(kb + koff, 16, 1024), idS, acc);
+                        } else {  // kv rows 0-63 -> lanes 0-15, kv rows 64-127 -> lanes 16-31
+                            umma_f16_ss(tmem + scol, a, smem_desc(kb + koff, 16, 1024), idS, acc);
+                            umma_f16_ss(tmem + HI_LANES + scol, a,
+                                        smem_desc(kb + koff + 64 * 128, 16, 1024), idS, acc);
+                        }
                     }
                     K1_TRACE(2, sc);
                     umma_commit(s_full + sb);
                     umma_commit(k_empty + st);
-                    if (i == ntl - 1) umma_commit(q_empty);
+                    if (i == ntl - 1) umma_commit(q_empty + qb);
                     ++kc;
                     ++sc;
                     if (i > 0) issue_pv(i - 1);
@@ -335,10 +363,12 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
     } else {
         // ===================== softmax + epilogue (warps 0-3) ==================
-        // TMEM lane 32*warp + lane holds query row warp*RPW + lane (lane < RPW),
-        // for both the M=128 (full) and M=64 (half-subpartition) layouts.
-        const bool row_lane = lane < C::RPW;
-        const int r = warp * C::RPW + (row_lane ? lane : 0);
+        // Thread (warp w, lane t) reads TMEM lane 32w+t. M=128: query row
+        // 32w+t, all 128 kv columns / all 128 d. M=64: row 16w+(t&15) and the
+        // half h = t>>4 of the kv columns (S) and of d (O); the two halves of a
+        // row exchange max / sum with one shuffle.
+        const int half = SPLIT == 2 ? (lane >> 4) : 0;
+        const int r = SPLIT == 2 ? warp * 16 + (lane & 15) : warp * 32 + lane;
         const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
         const float c = p.c_log2;
         const float thresh_raw = kLazyThreshLog2 / c;
@@ -348,7 +378,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             const int ntl = s.hi - s.lo;
             const int n = __ldg(p.n_nodes + s.b);
             const int P = __ldg(p.prefix_len + s.b);
-            const bool valid = row_lane && r < n;
+            const bool valid = r < n;
             const bool warp_live = __any_sync(0xffffffffu, valid);
             uint64_t mw0 = 0, mw1 = 0;
             if (valid) {
@@ -356,20 +386,20 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 mw0 = __ldg(mr);
                 if (p.W > 1) mw1 = __ldg(mr + 1);
             }
-            float m = -INFINITY, l = 0.f;
+            float m = -INFINITY, l = 0.f;   // l: this thread's share of the row sum
             for (int i = 0; i < ntl; ++i) {
                 const int j = s.lo + i;
                 const uint32_t sb = sc & 1;
                 const uint32_t pb = pc & 1;
+                mbar_wait(s_full + sb, (sc >> 1) & 1);
                 if (warp_live) {
-                    float sv[BN];
-                    mbar_wait(s_full + sb, (sc >> 1) & 1);
-                    if (threadIdx.x == 0) K1_TRACE(4, sc);
+                    float sv[COLS];
                     tc_fence_after();
+                    if (threadIdx.x == 0) K1_TRACE(4, sc);
 #pragma unroll
-                    for (int ch = 0; ch < BN / 32; ++ch) {
+                    for (int ch = 0; ch < COLS / 32; ++ch) {
                         uint32_t raw[32];
-                        tmem_ld_32x32b_x32(lane_addr + sb * BN + ch * 32, raw);
+                        tmem_ld_32x32b_x32(lane_addr + sb * C::S_COLS + ch * 32, raw);
                         tmem_ld_wait();
 #pragma unroll
                         for (int k = 0; k < 32; ++k) sv[ch * 32 + k] = __uint_as_float(raw[k]);
@@ -377,22 +407,37 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     tc_fence_before();
                     mbar_arrive(s_empty + sb);
                     if (threadIdx.x == 0) K1_TRACE(8, sc);
-                    const int row0 = j * BN;
-                    if (row0 + BN > P) {  // tile reaches the tree (or past it): apply the mask
+                    // ---- tree mask: one visibility word per 32 columns ----
+                    if (j * BN + BN > P) {
 #pragma unroll
-                        for (int k = 0; k < BN; ++k) {
-                            const int ra = row0 + k;
-                            bool vis = ra < P;
-                            if (!vis) {
-                                const int v = ra - P;
-                                vis = v < n && (((v < 64 ? mw0 : mw1) >> (v & 63)) & 1ull);
+                        for (int wd = 0; wd < COLS / 32; ++wd) {
+                            const int a = j * BN + half * COLS + wd * 32;  // first kv row of the word
+                            const int pre = P - a;
+                            uint32_t vis = pre >= 32 ? 0xffffffffu : (pre <= 0 ? 0u : ((1u << pre) - 1u));
+                            const int o = a - P;                          // tree index of bit 0
+                            if (o > -32 && o < n) {
+                                uint64_t win;
+                                if (o < 0) win = mw0 << (-o);
+                                else if (o == 0) win = mw0;
+                                else if (o < 64) win = (mw0 >> o) | (mw1 << (64 - o));
+                                else win = mw1 >> (o - 64);
+                                vis |= (uint32_t)win;
                             }
-                            if (!vis) sv[k] = -INFINITY;
+#pragma unroll
+                            for (int k = 0; k < 32; ++k)
+                                if (!((vis >> k) & 1u)) sv[wd * 32 + k] = -INFINITY;
                         }
                     }
-                    float mx = -INFINITY;
+                    float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                    for (int k = 0; k < BN; ++k) mx = fmaxf(mx, sv[k]);
+                    for (int k = 0; k < COLS; k += 4) {
+                        mq[0] = fmaxf(mq[0], sv[k]);
+                        mq[1] = fmaxf(mq[1], sv[k + 1]);
+                        mq[2] = fmaxf(mq[2], sv[k + 2]);
+                        mq[3] = fmaxf(mq[3], sv[k + 3]);
+                    }
+                    float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+                    if constexpr (SPLIT == 2) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
                     const float m_new = fmaxf(m, mx);
                     if (threadIdx.x == 0) K1_TRACE(9, sc);
 
@@ -415,43 +460,43 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         mbar_wait(pv_done + (q1 & 1), (q1 >> 1) & 1);
                         tc_fence_after();
 #pragma unroll
-                        for (int ch = 0; ch < HD / 32; ++ch) {
+                        for (int ch = 0; ch < DCOLS / 32; ++ch) {
                             uint32_t raw[32];
-                            tmem_ld_32x32b_x32(lane_addr + TM_O + ch * 32, raw);
+                            tmem_ld_32x32b_x32(lane_addr + C::O_COL + ch * 32, raw);
                             tmem_ld_wait();
 #pragma unroll
                             for (int k = 0; k < 32; ++k)
                                 raw[k] = __float_as_uint(__uint_as_float(raw[k]) * alpha);
-                            tmem_st_32x32b_x32(lane_addr + TM_O + ch * 32, raw);
+                            tmem_st_32x32b_x32(lane_addr + C::O_COL + ch * 32, raw);
                         }
                         tmem_st_wait();
                     }
                     if (threadIdx.x == 0) K1_TRACE(11, sc);
                     const float base = (m == -INFINITY) ? 0.f : m * c;
-                    float lsum = 0.f;
+                    float ls[4] = {0.f, 0.f, 0.f, 0.f};
                     uint8_t* prow = sm_p + pb * C::A_BYTES + r * 128;
 #pragma unroll
-                    for (int ch = 0; ch < BN / 8; ++ch) {
+                    for (int ch = 0; ch < COLS / 8; ++ch) {
                         uint32_t w4[4];
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
                             const float p0 = ex2(fmaf(sv[ch * 8 + 2 * k], c, -base));
                             const float p1 = ex2(fmaf(sv[ch * 8 + 2 * k + 1], c, -base));
-                            lsum += p0 + p1;
+                            ls[k] += p0 + p1;
                             w4[k] = pk2<T>::pack(p0, p1);
                         }
-                        const uint32_t atom = ch >> 3, cin = ch & 7;
-                        if (row_lane)
-                            *reinterpret_cast<uint4*>(prow + atom * C::A_ATOM + ((cin ^ (r & 7)) << 4)) =
-                                make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                        // 16-byte chunk cc of the row's 128 kv columns; atom = cc / 8
+                        const uint32_t cc = half * (COLS / 8) + ch;
+                        const uint32_t atom = cc >> 3, cin = cc & 7;
+                        *reinterpret_cast<uint4*>(prow + atom * C::A_ATOM + ((cin ^ (r & 7)) << 4)) =
+                            make_uint4(w4[0], w4[1], w4[2], w4[3]);
                     }
-                    l += lsum;
+                    l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
                     fence_proxy_async_smem();
                     tc_fence_before();
                 } else {
                     // rows all padding: no TMEM traffic or math, but the same
                     // waits as live warps so every arrival lands in its own phase
-                    mbar_wait(s_full + sb, (sc >> 1) & 1);
                     mbar_arrive(s_empty + sb);
                     mbar_wait(pv_done + pb, ((pc >> 1) & 1) ^ 1);
                 }
@@ -461,20 +506,23 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 ++pc;
             }
 
-            // ---- segment epilogue: O row from TMEM ----
+            // ---- segment epilogue: this thread's O columns from TMEM ----
             const bool full = (s.lo == 0 && s.hi == s.ntiles);
             const int slot = (t == t_begin) ? 0 : 1;
             float* sp = p.partial + ((long long)blockIdx.x * 2 + slot) * SLOT_FLOATS;
-            T* out_row = reinterpret_cast<T*>(p.o) + (((long long)s.b * p.T + r) * p.H + s.h) * HD;
+            const int d0 = half * DCOLS;
+            T* out_row = reinterpret_cast<T*>(p.o) + (((long long)s.b * p.T + r) * p.H + s.h) * HD + d0;
+            const uint32_t q1 = pc - 1;
+            mbar_wait(pv_done + (q1 & 1), (q1 >> 1) & 1);
+            float l_row = l;
+            if constexpr (SPLIT == 2) l_row += __shfl_xor_sync(0xffffffffu, l, 16);
             if (warp_live) {
-                const uint32_t q1 = pc - 1;
-                mbar_wait(pv_done + (q1 & 1), (q1 >> 1) & 1);
                 tc_fence_after();
-                float ov[HD];
+                float ov[DCOLS];
 #pragma unroll
-                for (int ch = 0; ch < HD / 32; ++ch) {
+                for (int ch = 0; ch < DCOLS / 32; ++ch) {
                     uint32_t raw[32];
-                    tmem_ld_32x32b_x32(lane_addr + TM_O + ch * 32, raw);
+                    tmem_ld_32x32b_x32(lane_addr + C::O_COL + ch * 32, raw);
                     tmem_ld_wait();
 #pragma unroll
                     for (int k = 0; k < 32; ++k) ov[ch * 32 + k] = __uint_as_float(raw[k]);
@@ -483,20 +531,21 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 mbar_arrive(o_empty);
                 if (valid) {
                     if (full) {
-                        store_row<T>(out_row, ov, 1.f / l);
-                        if (p.lse) p.lse[((long long)s.b * p.H + s.h) * p.T + r] = m * p.scale + __logf(l);
+                        store_row<T, DCOLS>(out_row, ov, 1.f / l_row);
+                        if (p.lse && half == 0)
+                            p.lse[((long long)s.b * p.H + s.h) * p.T + r] = m * p.scale + __logf(l_row);
                     } else {
-                        float4* po = reinterpret_cast<float4*>(sp + r * HD);
+                        float4* po = reinterpret_cast<float4*>(sp + r * HD + d0);
 #pragma unroll
-                        for (int k = 0; k < HD / 4; ++k)
+                        for (int k = 0; k < DCOLS / 4; ++k)
                             po[k] = make_float4(ov[4 * k], ov[4 * k + 1], ov[4 * k + 2], ov[4 * k + 3]);
-                        sp[128 * HD + r] = m;
-                        sp[128 * HD + 128 + r] = l;
+                        if (half == 0) {
+                            sp[128 * HD + r] = m;
+                            sp[128 * HD + 128 + r] = l_row;
+                        }
                     }
                 }
             } else {
-                const uint32_t q1 = pc - 1;
-                mbar_wait(pv_done + (q1 & 1), (q1 >> 1) & 1);
                 mbar_arrive(o_empty);
             }
 
@@ -527,9 +576,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             const float* q = p.partial + (cc * 2 + sl) * SLOT_FLOATS;
                             M_ = fmaxf(M_, __ldcg(q + 128 * HD + r));
                         }
-                        float acc[HD];
+                        float acc[DCOLS];
 #pragma unroll
-                        for (int k = 0; k < HD; ++k) acc[k] = 0.f;
+                        for (int k = 0; k < DCOLS; ++k) acc[k] = 0.f;
                         float L = 0.f;
                         for (long long cc = c_first; cc <= c_last; ++cc) {
                             const long long rs = range_start(cc, total, G);
@@ -540,9 +589,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             if (mk == -INFINITY) continue;
                             const float w = ex2((mk - M_) * c);
                             L += w * __ldcg(q + 128 * HD + 128 + r);
-                            const float4* qo = reinterpret_cast<const float4*>(q + r * HD);
+                            const float4* qo = reinterpret_cast<const float4*>(q + r * HD + d0);
 #pragma unroll
-                            for (int k = 0; k < HD / 4; ++k) {
+                            for (int k = 0; k < DCOLS / 4; ++k) {
                                 const float4 x = __ldcg(qo + k);
                                 acc[4 * k] += w * x.x;
                                 acc[4 * k + 1] += w * x.y;
@@ -550,8 +599,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                                 acc[4 * k + 3] += w * x.w;
                             }
                         }
-                        store_row<T>(out_row, acc, 1.f / L);
-                        if (p.lse)
+                        store_row<T, DCOLS>(out_row, acc, 1.f / L);
+                        if (p.lse && half == 0)
                             p.lse[((long long)s.b * p.H + s.h) * p.T + r] = M_ * p.scale + __logf(L);
                     }
                     if (threadIdx.x == 0) p.tickets[s.b * p.H + s.h] = 0u;
@@ -564,7 +613,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 6) tmem_dealloc<TMEM_COLS>(tmem);
+    if (warp == 6) tmem_dealloc<C::TMEM_COLS>(tmem);
 }
 
 // ------------------------------------------------------------------ host --
