@@ -229,6 +229,12 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     const long long total = total_tiles(p);
     const long long t_begin = range_start(blockIdx.x, total, G);
     const long long t_end = range_start(blockIdx.x + 1, total, G);
+    if (p.trace && threadIdx.x == 0) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
+        p.trace[12 * 64 + 4 * blockIdx.x] = gt;
+        p.trace[12 * 64 + 4 * blockIdx.x + 2] = (unsigned long long)(t_end - t_begin);
+    }
 
     if (warp == 4) {
         // ======================= TMA producer: Q and K =========================
@@ -613,6 +619,11 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (p.trace && threadIdx.x == 0) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
+        p.trace[12 * 64 + 4 * blockIdx.x + 1] = gt;
+    }
     if (warp == 6) tmem_dealloc<C::TMEM_COLS>(tmem);
 }
 
@@ -720,8 +731,8 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     prm.trace = nullptr;
     static unsigned long long* trace_buf = nullptr;
     if (getenv("ST_K1_TRACE")) {
-        if (!trace_buf) cudaMalloc(&trace_buf, 12 * 64 * sizeof(unsigned long long));
-        cudaMemsetAsync(trace_buf, 0, 12 * 64 * sizeof(unsigned long long), stream);
+        if (!trace_buf) cudaMalloc(&trace_buf, (12 * 64 + 4 * 1024) * sizeof(unsigned long long));
+        cudaMemsetAsync(trace_buf, 0, (12 * 64 + 4 * 1024) * sizeof(unsigned long long), stream);
         prm.trace = trace_buf;
     }
     const bool m64 = a->T <= 64;
@@ -732,7 +743,7 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     }
     ST_LAUNCH_CHECK();
     if (prm.trace) {  // diagnostic only: dump CTA 0's pipeline timestamps
-        unsigned long long h[12 * 64];
+        static unsigned long long h[12 * 64 + 4 * 1024];
         cudaMemcpyAsync(h, prm.trace, sizeof h, cudaMemcpyDeviceToHost, stream);
         cudaStreamSynchronize(stream);
         if (FILE* f = fopen(getenv("ST_K1_TRACE"), "a")) {
@@ -740,6 +751,8 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
                 for (int i = 0; i < 64; ++i) fprintf(f, "%llu ", h[r * 64 + i]);
                 fprintf(f, "\n");
             }
+            for (int i = 0; i < 4 * G; ++i) fprintf(f, "%llu ", h[12 * 64 + i]);
+            fprintf(f, "\n");
             fclose(f);
         }
     }

@@ -26,10 +26,24 @@ ws = _capi.tree_attention_workspace(q, kc, vc, mask, P, n)
 for _ in range(3):
     _capi.tree_attention(q, kc, vc, mask, P, n, workspace=ws)
 torch.cuda.synchronize()
-rows = [list(map(int, l.split())) for l in open(out)][-12:]
+lines = [list(map(int, l.split())) for l in open(out)]
+rows = lines[-13:-1]
+cta = np.array(lines[-1], dtype=np.int64).reshape(-1, 4)
 t = np.array(rows, dtype=np.int64)
 t0 = t[0][t[0] > 0].min()
 names = ["K issue", "V issue", "S issue", "PV issue", "S ready", "P done", "K full(mma)", "V full(mma)", "S loaded", "masked+max", "pv wait done", "rescaled"]
 print("tile " + " ".join(f"{x:>12s}" for x in names))
 for i in range(30):
     print(f"{i:4d} " + " ".join(f"{(t[r][i] - t0) if t[r][i] else -1:12d}" for r in range(12)))
+
+st, en, nt = cta[:, 0], cta[:, 1], cta[:, 2]
+t0g = st.min()
+print("\nper-CTA (us): start min/median/max %.2f %.2f %.2f | end min/median/max %.2f %.2f %.2f" % (
+    (st.min() - t0g) / 1e3, (np.median(st) - t0g) / 1e3, (st.max() - t0g) / 1e3,
+    (en.min() - t0g) / 1e3, (np.median(en) - t0g) / 1e3, (en.max() - t0g) / 1e3))
+dur = (en - st) / 1e3
+order = np.argsort(dur)
+print("slowest CTAs:", [(int(i), round(float(dur[i]), 1), int(nt[i])) for i in order[-8:]])
+print("fastest CTAs:", [(int(i), round(float(dur[i]), 1), int(nt[i])) for i in order[:5]])
+hist = np.histogram(dur, bins=8)
+print("duration histogram:", hist[0].tolist(), [round(float(x), 1) for x in hist[1]])
