@@ -81,12 +81,21 @@ struct TcParams {
     void* o;
     float* lse;
     float* partial;      // [gridDim.x * 2][SLOT_FLOATS]
-    unsigned* tickets;   // [B * H]
+    unsigned* tickets;   // [B * H] (unused since the combine kernel; kept for layout)
     int B, T, H, W;
     float c_log2;        // scale * log2(e)
     float scale;
     unsigned long long* trace;  // optional pipeline trace of CTA 0 (ST_K1_TRACE)
 };
+
+#define K1_GT(k)                                                                  \
+    do {                                                                          \
+        if (p.trace) {                                                            \
+            unsigned long long gt_;                                               \
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt_));               \
+            p.trace[12 * 64 + 8 * blockIdx.x + (k)] = gt_;                        \
+        }                                                                         \
+    } while (0)
 
 #define K1_TRACE(slot, idx)                                                       \
     do {                                                                          \
@@ -197,7 +206,6 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     uint64_t* pv_done = p_full + 2;      // [2]
     uint64_t* o_empty = pv_done + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
-    __shared__ int merge_flag;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -232,8 +240,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (p.trace && threadIdx.x == 0) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
-        p.trace[12 * 64 + 4 * blockIdx.x] = gt;
-        p.trace[12 * 64 + 4 * blockIdx.x + 2] = (unsigned long long)(t_end - t_begin);
+        p.trace[12 * 64 + 8 * blockIdx.x] = gt;
+        p.trace[12 * 64 + 8 * blockIdx.x + 2] = (unsigned long long)(t_end - t_begin);
     }
 
     if (warp == 4) {
@@ -520,6 +528,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             T* out_row = reinterpret_cast<T*>(p.o) + (((long long)s.b * p.T + r) * p.H + s.h) * HD + d0;
             const uint32_t q1 = pc - 1;
             mbar_wait(pv_done + (q1 & 1), (q1 >> 1) & 1);
+            if (threadIdx.x == 0) K1_GT(3);
             float l_row = l;
             if constexpr (SPLIT == 2) l_row += __shfl_xor_sync(0xffffffffu, l, 16);
             if (warp_live) {
@@ -555,63 +564,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 mbar_arrive(o_empty);
             }
 
-            if (!full) {
-                // partial piece written above; the last finisher of the pair merges
-                __threadfence();
-                named_bar_sync(1, 128);
-                const long long pair_end = s.pair_start + s.ntiles;
-                const long long c_first = cta_of(s.pair_start, total, G);
-                const long long c_last = cta_of(pair_end - 1, total, G);
-                if (threadIdx.x == 0) {
-                    // CTAs with an empty range (total < #SMs) contribute no piece
-                    unsigned pieces = 0;
-                    for (long long cc = c_first; cc <= c_last; ++cc)
-                        pieces += range_start(cc + 1, total, G) > range_start(cc, total, G);
-                    const unsigned old = atomicAdd(p.tickets + s.b * p.H + s.h, 1u);
-                    merge_flag = (old == pieces - 1);
-                }
-                named_bar_sync(1, 128);
-                if (merge_flag) {
-                    __threadfence();
-                    if (valid) {
-                        float M_ = -INFINITY;
-                        for (long long cc = c_first; cc <= c_last; ++cc) {
-                            const long long rs = range_start(cc, total, G);
-                            if (range_start(cc + 1, total, G) == rs) continue;  // empty range
-                            const int sl = (s.pair_start > rs) ? 1 : 0;
-                            const float* q = p.partial + (cc * 2 + sl) * SLOT_FLOATS;
-                            M_ = fmaxf(M_, __ldcg(q + 128 * HD + r));
-                        }
-                        float acc[DCOLS];
-#pragma unroll
-                        for (int k = 0; k < DCOLS; ++k) acc[k] = 0.f;
-                        float L = 0.f;
-                        for (long long cc = c_first; cc <= c_last; ++cc) {
-                            const long long rs = range_start(cc, total, G);
-                            if (range_start(cc + 1, total, G) == rs) continue;
-                            const int sl = (s.pair_start > rs) ? 1 : 0;
-                            const float* q = p.partial + (cc * 2 + sl) * SLOT_FLOATS;
-                            const float mk = __ldcg(q + 128 * HD + r);
-                            if (mk == -INFINITY) continue;
-                            const float w = ex2((mk - M_) * c);
-                            L += w * __ldcg(q + 128 * HD + 128 + r);
-                            const float4* qo = reinterpret_cast<const float4*>(q + r * HD + d0);
-#pragma unroll
-                            for (int k = 0; k < DCOLS / 4; ++k) {
-                                const float4 x = __ldcg(qo + k);
-                                acc[4 * k] += w * x.x;
-                                acc[4 * k + 1] += w * x.y;
-                                acc[4 * k + 2] += w * x.z;
-                                acc[4 * k + 3] += w * x.w;
-                            }
-                        }
-                        store_row<T, DCOLS>(out_row, acc, 1.f / L);
-                        if (p.lse && half == 0)
-                            p.lse[((long long)s.b * p.H + s.h) * p.T + r] = M_ * p.scale + __logf(L);
-                    }
-                    if (threadIdx.x == 0) p.tickets[s.b * p.H + s.h] = 0u;
-                }
-            }
+            if (threadIdx.x == 0) K1_GT(4);
+            // split pairs: the partial (O, m, l) pieces are merged by combine_kernel
             t += ntl;
         }
     }
@@ -622,9 +576,73 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (p.trace && threadIdx.x == 0) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
-        p.trace[12 * 64 + 4 * blockIdx.x + 1] = gt;
+        p.trace[12 * 64 + 8 * blockIdx.x + 1] = gt;
     }
     if (warp == 6) tmem_dealloc<C::TMEM_COLS>(tmem);
+}
+
+// Merge of the partial pieces of pairs that the stream-K schedule split over
+// several CTAs: one block per (b, h) pair (unsplit pairs exit at once); thread
+// (row, d-quarter) reads the <= few pieces' (m, l) and O rows and writes the
+// normalised output. Fixed piece order -> deterministic.
+template <class T>
+__global__ void __launch_bounds__(128)
+combine_kernel(const TcParams p, int G) {
+    const int bh = blockIdx.x;
+    const int b = bh / p.H, h = bh % p.H;
+    const int n = __ldg(p.n_nodes + b);
+    if (n == 0) return;
+    long long total = 0, pair_start = -1;
+    int nt = 0;
+    for (int bb = 0; bb < p.B; ++bb) {
+        const int t_ = ntiles_of(p, bb);
+        if (bb == b) {
+            nt = t_;
+            pair_start = total + (long long)h * t_;
+        }
+        total += (long long)p.H * t_;
+    }
+    const long long c_first = cta_of(pair_start, total, G);
+    const long long c_last = cta_of(pair_start + nt - 1, total, G);
+    if (c_first == c_last) return;  // written directly by the attention kernel
+    constexpr int MAXP = 16;
+    int slots[MAXP];
+    int np = 0;
+    for (long long cc = c_first; cc <= c_last && np < MAXP; ++cc) {
+        const long long rs = range_start(cc, total, G);
+        if (range_start(cc + 1, total, G) == rs) continue;  // empty range: no piece
+        slots[np++] = (int)(cc * 2 + ((pair_start > rs) ? 1 : 0));
+    }
+    const float c = p.c_log2;
+    // thread -> (row r, 32-column quarter q); loop rows in strides of 32
+    const int q = threadIdx.x & 3;
+    for (int r = threadIdx.x >> 2; r < n; r += 32) {
+        float M_ = -INFINITY;
+        for (int k = 0; k < np; ++k)
+            M_ = fmaxf(M_, __ldg(p.partial + (long long)slots[k] * SLOT_FLOATS + 128 * HD + r));
+        float acc[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) acc[k] = 0.f;
+        float L = 0.f;
+        for (int k = 0; k < np; ++k) {
+            const float* piece = p.partial + (long long)slots[k] * SLOT_FLOATS;
+            const float mk = __ldg(piece + 128 * HD + r);
+            const float w = mk == -INFINITY ? 0.f : ex2((mk - M_) * c);
+            L += w * __ldg(piece + 128 * HD + 128 + r);
+            const float4* src = reinterpret_cast<const float4*>(piece + r * HD + q * 32);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const float4 x = __ldg(src + e);
+                acc[4 * e] += w * x.x;
+                acc[4 * e + 1] += w * x.y;
+                acc[4 * e + 2] += w * x.z;
+                acc[4 * e + 3] += w * x.w;
+            }
+        }
+        T* out_row = reinterpret_cast<T*>(p.o) + (((long long)b * p.T + r) * p.H + h) * HD + q * 32;
+        store_row<T, 32>(out_row, acc, 1.f / L);
+        if (p.lse && q == 0) p.lse[((long long)b * p.H + h) * p.T + r] = M_ * p.scale + __logf(L);
+    }
 }
 
 // ------------------------------------------------------------------ host --
@@ -687,6 +705,7 @@ size_t tree_attention_tc_workspace(const st_attn_args* a) {
             attr = true;                                                                        \
         }                                                                                       \
         tree_attn_tc_kernel<TT, MM><<<G, NUM_THREADS, Cfg<MM>::SMEM_BYTES, stream>>>(tq, tk, tv, prm); \
+        combine_kernel<TT><<<a->B * a->H, 128, 0, stream>>>(prm, G);                          \
     } while (0)
 
 st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
@@ -731,8 +750,8 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     prm.trace = nullptr;
     static unsigned long long* trace_buf = nullptr;
     if (getenv("ST_K1_TRACE")) {
-        if (!trace_buf) cudaMalloc(&trace_buf, (12 * 64 + 4 * 1024) * sizeof(unsigned long long));
-        cudaMemsetAsync(trace_buf, 0, (12 * 64 + 4 * 1024) * sizeof(unsigned long long), stream);
+        if (!trace_buf) cudaMalloc(&trace_buf, (12 * 64 + 8 * 1024) * sizeof(unsigned long long));
+        cudaMemsetAsync(trace_buf, 0, (12 * 64 + 8 * 1024) * sizeof(unsigned long long), stream);
         prm.trace = trace_buf;
     }
     const bool m64 = a->T <= 64;
@@ -743,7 +762,7 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     }
     ST_LAUNCH_CHECK();
     if (prm.trace) {  // diagnostic only: dump CTA 0's pipeline timestamps
-        static unsigned long long h[12 * 64 + 4 * 1024];
+        static unsigned long long h[12 * 64 + 8 * 1024];
         cudaMemcpyAsync(h, prm.trace, sizeof h, cudaMemcpyDeviceToHost, stream);
         cudaStreamSynchronize(stream);
         if (FILE* f = fopen(getenv("ST_K1_TRACE"), "a")) {
@@ -751,7 +770,7 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
                 for (int i = 0; i < 64; ++i) fprintf(f, "%llu ", h[r * 64 + i]);
                 fprintf(f, "\n");
             }
-            for (int i = 0; i < 4 * G; ++i) fprintf(f, "%llu ", h[12 * 64 + i]);
+            for (int i = 0; i < 8 * G; ++i) fprintf(f, "%llu ", h[12 * 64 + i]);
             fprintf(f, "\n");
             fclose(f);
         }

@@ -28,7 +28,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 lines = [list(map(int, l.split())) for l in open(out)]
 rows = lines[-13:-1]
-cta = np.array(lines[-1], dtype=np.int64).reshape(-1, 4)
+cta = np.array(lines[-1], dtype=np.int64).reshape(-1, 8)
 t = np.array(rows, dtype=np.int64)
 t0 = t[0][t[0] > 0].min()
 names = ["K issue", "V issue", "S issue", "PV issue", "S ready", "P done", "K full(mma)", "V full(mma)", "S loaded", "masked+max", "pv wait done", "rescaled"]
@@ -47,3 +47,9 @@ print("slowest CTAs:", [(int(i), round(float(dur[i]), 1), int(nt[i])) for i in o
 print("fastest CTAs:", [(int(i), round(float(dur[i]), 1), int(nt[i])) for i in order[:5]])
 hist = np.histogram(dur, bins=8)
 print("duration histogram:", hist[0].tolist(), [round(float(x), 1) for x in hist[1]])
+
+rel = lambda k: (cta[:, k] - cta[:, 0]) / 1e3  # noqa: E731
+for k, name in [(3, "last PV done"), (4, "O read+written"), (5, "partial fenced"), (6, "ticket"), (7, "merge done"), (1, "CTA end")]:
+    v = rel(k)
+    ok = cta[:, k] > 0
+    print(f"{name:16s} (us after CTA start): median {np.median(v[ok]) if ok.any() else -1:7.2f}  max {v[ok].max() if ok.any() else -1:7.2f}  n={ok.sum()}")
