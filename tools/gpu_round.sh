@@ -15,3 +15,4 @@ timeout 400 ncu --set full --clock-control none --import-source on -k regex:tree
     -o $OUT/$TAG.k1 -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
     > /dev/null 2> $OUT/$TAG.ncu2.err
 ls -la $OUT
+timeout 600 python tools/sweep_c5.py --out gpurun_out/$TAG.c5_sweep.json > gpurun_out/$TAG.c5_sweep.txt 2>&1
