@@ -59,15 +59,16 @@ template <int M> struct Cfg {
     static constexpr int SPLIT = M == 64 ? 2 : 1;           // threads per query row
     static constexpr uint32_t A_ATOM = M * 128;             // M rows x 64 elems x 2 B
     static constexpr uint32_t A_BYTES = 2 * A_ATOM;         // Q or one P buffer
-    static constexpr int QSTAGES = M == 64 ? 2 : 1;
-    static constexpr int KSTAGES = 2;
+    static constexpr int QSTAGES = 1;
+    static constexpr int PBUF = M == 64 ? 1 : 2;             // P buffers in smem
+    static constexpr int KSTAGES = M == 64 ? 3 : 2;
     static constexpr int VSTAGES = M == 64 ? 3 : 2;
     static constexpr uint32_t S_COLS = BN / SPLIT;          // TMEM columns per S buffer
     static constexpr uint32_t O_COL = 2 * S_COLS;           // O accumulator column
     static constexpr uint32_t TMEM_COLS = M == 64 ? 256 : 512;
     static constexpr uint32_t OFF_Q = 0;
-    static constexpr uint32_t OFF_P = OFF_Q + QSTAGES * A_BYTES;  // 2 P buffers
-    static constexpr uint32_t OFF_K = OFF_P + 2 * A_BYTES;
+    static constexpr uint32_t OFF_P = OFF_Q + QSTAGES * A_BYTES;
+    static constexpr uint32_t OFF_K = OFF_P + PBUF * A_BYTES;
     static constexpr uint32_t OFF_V = OFF_K + KSTAGES * TILE_BYTES;
     static constexpr uint32_t OFF_BAR = OFF_V + VSTAGES * TILE_BYTES;
     static constexpr uint32_t SMEM_BYTES = OFF_BAR + 256 + 1024;
@@ -313,7 +314,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 if (i_local == 0) mbar_wait(o_empty, (segc & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t vb = v_base + st * TILE_BYTES;
-                const uint32_t pbase = p_base + pb * C::A_BYTES;
+                const uint32_t pbase = p_base + (pc % C::PBUF) * C::A_BYTES;
 #pragma unroll
                 for (int kk = 0; kk < BN / 16; ++kk) {
                     const uint64_t a = smem_desc(pbase + (kk >> 2) * C::A_ATOM + (kk & 3) * 32, 16, 1024);
@@ -455,9 +456,6 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     const float m_new = fmaxf(m, mx);
                     if (threadIdx.x == 0) K1_TRACE(9, sc);
 
-                    // P buffer pb was last read by P.V number pc-2
-                    mbar_wait(pv_done + pb, ((pc >> 1) & 1) ^ 1);
-                    if (threadIdx.x == 0) K1_TRACE(10, sc);
                     float alpha = 1.f;
                     bool rescale = false;
                     if (m == -INFINITY) {
@@ -486,24 +484,32 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         tmem_st_wait();
                     }
                     if (threadIdx.x == 0) K1_TRACE(11, sc);
+                    // exps into packed registers first, so the wait for the P
+                    // buffer below overlaps the MUFU work
                     const float base = (m == -INFINITY) ? 0.f : m * c;
                     float ls[4] = {0.f, 0.f, 0.f, 0.f};
-                    uint8_t* prow = sm_p + pb * C::A_BYTES + r * 128;
+                    uint32_t pk[COLS / 2];
+#pragma unroll
+                    for (int k = 0; k < COLS / 2; ++k) {
+                        const float p0 = ex2(fmaf(sv[2 * k], c, -base));
+                        const float p1 = ex2(fmaf(sv[2 * k + 1], c, -base));
+                        ls[k & 3] += p0 + p1;
+                        pk[k] = pk2<T>::pack(p0, p1);
+                    }
+                    // P buffer (pc % PBUF) was last read by P.V number pc-PBUF
+                    if (pc >= (uint32_t)C::PBUF) {
+                        const uint32_t q2 = pc - C::PBUF;
+                        mbar_wait(pv_done + (q2 & 1), (q2 >> 1) & 1);
+                    }
+                    if (threadIdx.x == 0) K1_TRACE(10, sc);
+                    uint8_t* prow = sm_p + (pc % C::PBUF) * C::A_BYTES + r * 128;
 #pragma unroll
                     for (int ch = 0; ch < COLS / 8; ++ch) {
-                        uint32_t w4[4];
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const float p0 = ex2(fmaf(sv[ch * 8 + 2 * k], c, -base));
-                            const float p1 = ex2(fmaf(sv[ch * 8 + 2 * k + 1], c, -base));
-                            ls[k] += p0 + p1;
-                            w4[k] = pk2<T>::pack(p0, p1);
-                        }
                         // 16-byte chunk cc of the row's 128 kv columns; atom = cc / 8
                         const uint32_t cc = half * (COLS / 8) + ch;
                         const uint32_t atom = cc >> 3, cin = cc & 7;
                         *reinterpret_cast<uint4*>(prow + atom * C::A_ATOM + ((cin ^ (r & 7)) << 4)) =
-                            make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                            make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
                     }
                     l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
                     fence_proxy_async_smem();
@@ -512,7 +518,10 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     // rows all padding: no TMEM traffic or math, but the same
                     // waits as live warps so every arrival lands in its own phase
                     mbar_arrive(s_empty + sb);
-                    mbar_wait(pv_done + pb, ((pc >> 1) & 1) ^ 1);
+                    if (pc >= (uint32_t)C::PBUF) {
+                        const uint32_t q2 = pc - C::PBUF;
+                        mbar_wait(pv_done + (q2 & 1), (q2 >> 1) & 1);
+                    }
                 }
                 ++sc;
                 if (threadIdx.x == 0) K1_TRACE(5, pc);
@@ -582,66 +591,97 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 }
 
 // Merge of the partial pieces of pairs that the stream-K schedule split over
-// several CTAs: one block per (b, h) pair (unsplit pairs exit at once); thread
-// (row, d-quarter) reads the <= few pieces' (m, l) and O rows and writes the
-// normalised output. Fixed piece order -> deterministic.
+// several CTAs. One block per (b, h) pair: the schedule arithmetic is done
+// once per block (unsplit pairs exit at once); then warp w handles rows
+// w, w+4, ...; lane l owns d columns [4l, 4l+4). All loads of a row (every
+// piece's m, l and O float4) are issued before any use, so a row costs one
+// L2 round trip. Fixed piece order -> deterministic.
 template <class T>
 __global__ void __launch_bounds__(128)
 combine_kernel(const TcParams p, int G) {
+    constexpr int MAXP = 4;   // a pair spans <= 4 CTAs unless ranges are < 1/3 pair
+    __shared__ int s_slots[16];
+    __shared__ int s_np;
     const int bh = blockIdx.x;
     const int b = bh / p.H, h = bh % p.H;
-    const int n = __ldg(p.n_nodes + b);
-    if (n == 0) return;
-    long long total = 0, pair_start = -1;
-    int nt = 0;
-    for (int bb = 0; bb < p.B; ++bb) {
-        const int t_ = ntiles_of(p, bb);
-        if (bb == b) {
-            nt = t_;
-            pair_start = total + (long long)h * t_;
+    if (threadIdx.x == 0) {
+        long long total = 0, pair_start = -1;
+        int nt = 0;
+        for (int bb = 0; bb < p.B; ++bb) {
+            const int t_ = ntiles_of(p, bb);
+            if (bb == b) {
+                nt = t_;
+                pair_start = total + (long long)h * t_;
+            }
+            total += (long long)p.H * t_;
         }
-        total += (long long)p.H * t_;
+        int np = 0;
+        if (nt > 0) {
+            const long long c_first = cta_of(pair_start, total, G);
+            const long long c_last = cta_of(pair_start + nt - 1, total, G);
+            if (c_first != c_last)
+                for (long long cc = c_first; cc <= c_last && np < 16; ++cc) {
+                    const long long rs = range_start(cc, total, G);
+                    if (range_start(cc + 1, total, G) == rs) continue;  // empty range
+                    s_slots[np++] = (int)(cc * 2 + ((pair_start > rs) ? 1 : 0));
+                }
+        }
+        s_np = np;
     }
-    const long long c_first = cta_of(pair_start, total, G);
-    const long long c_last = cta_of(pair_start + nt - 1, total, G);
-    if (c_first == c_last) return;  // written directly by the attention kernel
-    constexpr int MAXP = 16;
-    int slots[MAXP];
-    int np = 0;
-    for (long long cc = c_first; cc <= c_last && np < MAXP; ++cc) {
-        const long long rs = range_start(cc, total, G);
-        if (range_start(cc + 1, total, G) == rs) continue;  // empty range: no piece
-        slots[np++] = (int)(cc * 2 + ((pair_start > rs) ? 1 : 0));
-    }
+    __syncthreads();
+    const int np = s_np;
+    if (np == 0) return;  // written directly by the attention kernel
+    const int n = __ldg(p.n_nodes + b);
     const float c = p.c_log2;
-    // thread -> (row r, 32-column quarter q); loop rows in strides of 32
-    const int q = threadIdx.x & 3;
-    for (int r = threadIdx.x >> 2; r < n; r += 32) {
-        float M_ = -INFINITY;
-        for (int k = 0; k < np; ++k)
-            M_ = fmaxf(M_, __ldg(p.partial + (long long)slots[k] * SLOT_FLOATS + 128 * HD + r));
-        float acc[32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int r = warp; r < n; r += 4) {
+        float mk[MAXP], lk[MAXP];
+        float4 ok[MAXP];
 #pragma unroll
-        for (int k = 0; k < 32; ++k) acc[k] = 0.f;
-        float L = 0.f;
-        for (int k = 0; k < np; ++k) {
-            const float* piece = p.partial + (long long)slots[k] * SLOT_FLOATS;
-            const float mk = __ldg(piece + 128 * HD + r);
-            const float w = mk == -INFINITY ? 0.f : ex2((mk - M_) * c);
-            L += w * __ldg(piece + 128 * HD + 128 + r);
-            const float4* src = reinterpret_cast<const float4*>(piece + r * HD + q * 32);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const float4 x = __ldg(src + e);
-                acc[4 * e] += w * x.x;
-                acc[4 * e + 1] += w * x.y;
-                acc[4 * e + 2] += w * x.z;
-                acc[4 * e + 3] += w * x.w;
+        for (int k = 0; k < MAXP; ++k) {
+            if (k < np) {
+                const float* piece = p.partial + (long long)s_slots[k] * SLOT_FLOATS;
+                mk[k] = __ldcg(piece + 128 * HD + r);
+                lk[k] = __ldcg(piece + 128 * HD + 128 + r);
+                ok[k] = __ldcg(reinterpret_cast<const float4*>(piece + r * HD) + lane);
             }
         }
-        T* out_row = reinterpret_cast<T*>(p.o) + (((long long)b * p.T + r) * p.H + h) * HD + q * 32;
-        store_row<T, 32>(out_row, acc, 1.f / L);
-        if (p.lse && q == 0) p.lse[((long long)b * p.H + h) * p.T + r] = M_ * p.scale + __logf(L);
+        float M_ = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < MAXP; ++k)
+            if (k < np) M_ = fmaxf(M_, mk[k]);
+        float L = 0.f;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < MAXP; ++k) {
+            if (k < np && mk[k] != -INFINITY) {
+                const float w = ex2((mk[k] - M_) * c);
+                L += w * lk[k];
+                acc.x += w * ok[k].x;
+                acc.y += w * ok[k].y;
+                acc.z += w * ok[k].z;
+                acc.w += w * ok[k].w;
+            }
+        }
+        for (int k = MAXP; k < np; ++k) {  // rare: more pieces than registers
+            const float* piece = p.partial + (long long)s_slots[k] * SLOT_FLOATS;
+            const float m2 = __ldcg(piece + 128 * HD + r);
+            if (m2 == -INFINITY) continue;
+            float Mn = fmaxf(M_, m2);
+            const float sc0 = ex2((M_ - Mn) * c), w = ex2((m2 - Mn) * c);
+            const float4 o2 = __ldcg(reinterpret_cast<const float4*>(piece + r * HD) + lane);
+            L = L * sc0 + w * __ldcg(piece + 128 * HD + 128 + r);
+            acc.x = acc.x * sc0 + w * o2.x;
+            acc.y = acc.y * sc0 + w * o2.y;
+            acc.z = acc.z * sc0 + w * o2.z;
+            acc.w = acc.w * sc0 + w * o2.w;
+            M_ = Mn;
+        }
+        const float inv = 1.f / L;
+        T* out = reinterpret_cast<T*>(p.o) + (((long long)b * p.T + r) * p.H + h) * HD + 4 * lane;
+        const uint2 v = make_uint2(pk2<T>::pack(acc.x * inv, acc.y * inv), pk2<T>::pack(acc.z * inv, acc.w * inv));
+        *reinterpret_cast<uint2*>(out) = v;
+        if (p.lse && lane == 0) p.lse[((long long)b * p.H + h) * p.T + r] = M_ * p.scale + __logf(L);
     }
 }
 
