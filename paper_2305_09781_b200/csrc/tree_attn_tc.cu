@@ -59,9 +59,9 @@ template <int M> struct Cfg {
     static constexpr int SPLIT = M == 64 ? 2 : 1;           // threads per query row
     static constexpr uint32_t A_ATOM = M * 128;             // M rows x 64 elems x 2 B
     static constexpr uint32_t A_BYTES = 2 * A_ATOM;         // Q or one P buffer
-    static constexpr int QSTAGES = 1;
-    static constexpr int PBUF = M == 64 ? 1 : 2;             // P buffers in smem
-    static constexpr int KSTAGES = M == 64 ? 3 : 2;
+    static constexpr int QSTAGES = M == 64 ? 2 : 1;          // next pair's Q prefetched
+    static constexpr int PBUF = 2;                            // P buffers in smem
+    static constexpr int KSTAGES = 2;
     static constexpr int VSTAGES = M == 64 ? 3 : 2;
     static constexpr uint32_t S_COLS = BN / SPLIT;          // TMEM columns per S buffer
     static constexpr uint32_t O_COL = 2 * S_COLS;           // O accumulator column
@@ -597,13 +597,16 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 // piece's m, l and O float4) are issued before any use, so a row costs one
 // L2 round trip. Fixed piece order -> deterministic.
 template <class T>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(512)
 combine_kernel(const TcParams p, int G) {
-    constexpr int MAXP = 4;   // a pair spans <= 4 CTAs unless ranges are < 1/3 pair
+    constexpr int MAXP = 4;   // pieces held in registers (more are folded in a slow loop)
+    constexpr int RPW = 4;    // rows per warp, all in flight together
     __shared__ int s_slots[16];
     __shared__ int s_np;
     const int bh = blockIdx.x;
     const int b = bh / p.H, h = bh % p.H;
+    // PDL: everything above is independent of the attention kernel's output
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 0) {
         long long total = 0, pair_start = -1;
         int nt = 0;
@@ -634,54 +637,64 @@ combine_kernel(const TcParams p, int G) {
     const int n = __ldg(p.n_nodes + b);
     const float c = p.c_log2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int r = warp; r < n; r += 4) {
-        float mk[MAXP], lk[MAXP];
-        float4 ok[MAXP];
+    const int nw = blockDim.x >> 5;
+    for (int r0 = warp; r0 < n; r0 += nw * RPW) {
+        float mk[RPW][MAXP], lk[RPW][MAXP];
+        float4 ok[RPW][MAXP];
 #pragma unroll
-        for (int k = 0; k < MAXP; ++k) {
-            if (k < np) {
+        for (int i = 0; i < RPW; ++i) {
+            const int r = r0 + i * nw;
+#pragma unroll
+            for (int k = 0; k < MAXP; ++k) {
+                if (k < np && r < n) {
+                    const float* piece = p.partial + (long long)s_slots[k] * SLOT_FLOATS;
+                    mk[i][k] = __ldcg(piece + 128 * HD + r);
+                    lk[i][k] = __ldcg(piece + 128 * HD + 128 + r);
+                    ok[i][k] = __ldcg(reinterpret_cast<const float4*>(piece + r * HD) + lane);
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            const int r = r0 + i * nw;
+            if (r >= n) break;
+            float M_ = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < MAXP; ++k)
+                if (k < np) M_ = fmaxf(M_, mk[i][k]);
+            float L = 0.f;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < MAXP; ++k) {
+                if (k < np && mk[i][k] != -INFINITY) {
+                    const float w = ex2((mk[i][k] - M_) * c);
+                    L += w * lk[i][k];
+                    acc.x += w * ok[i][k].x;
+                    acc.y += w * ok[i][k].y;
+                    acc.z += w * ok[i][k].z;
+                    acc.w += w * ok[i][k].w;
+                }
+            }
+            for (int k = MAXP; k < np; ++k) {  // rare: more pieces than registers
                 const float* piece = p.partial + (long long)s_slots[k] * SLOT_FLOATS;
-                mk[k] = __ldcg(piece + 128 * HD + r);
-                lk[k] = __ldcg(piece + 128 * HD + 128 + r);
-                ok[k] = __ldcg(reinterpret_cast<const float4*>(piece + r * HD) + lane);
+                const float m2 = __ldcg(piece + 128 * HD + r);
+                if (m2 == -INFINITY) continue;
+                const float Mn = fmaxf(M_, m2);
+                const float sc0 = ex2((M_ - Mn) * c), w = ex2((m2 - Mn) * c);
+                const float4 o2 = __ldcg(reinterpret_cast<const float4*>(piece + r * HD) + lane);
+                L = L * sc0 + w * __ldcg(piece + 128 * HD + 128 + r);
+                acc.x = acc.x * sc0 + w * o2.x;
+                acc.y = acc.y * sc0 + w * o2.y;
+                acc.z = acc.z * sc0 + w * o2.z;
+                acc.w = acc.w * sc0 + w * o2.w;
+                M_ = Mn;
             }
+            const float inv = 1.f / L;
+            T* out = reinterpret_cast<T*>(p.o) + (((long long)b * p.T + r) * p.H + h) * HD + 4 * lane;
+            *reinterpret_cast<uint2*>(out) =
+                make_uint2(pk2<T>::pack(acc.x * inv, acc.y * inv), pk2<T>::pack(acc.z * inv, acc.w * inv));
+            if (p.lse && lane == 0) p.lse[((long long)b * p.H + h) * p.T + r] = M_ * p.scale + __logf(L);
         }
-        float M_ = -INFINITY;
-#pragma unroll
-        for (int k = 0; k < MAXP; ++k)
-            if (k < np) M_ = fmaxf(M_, mk[k]);
-        float L = 0.f;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int k = 0; k < MAXP; ++k) {
-            if (k < np && mk[k] != -INFINITY) {
-                const float w = ex2((mk[k] - M_) * c);
-                L += w * lk[k];
-                acc.x += w * ok[k].x;
-                acc.y += w * ok[k].y;
-                acc.z += w * ok[k].z;
-                acc.w += w * ok[k].w;
-            }
-        }
-        for (int k = MAXP; k < np; ++k) {  // rare: more pieces than registers
-            const float* piece = p.partial + (long long)s_slots[k] * SLOT_FLOATS;
-            const float m2 = __ldcg(piece + 128 * HD + r);
-            if (m2 == -INFINITY) continue;
-            float Mn = fmaxf(M_, m2);
-            const float sc0 = ex2((M_ - Mn) * c), w = ex2((m2 - Mn) * c);
-            const float4 o2 = __ldcg(reinterpret_cast<const float4*>(piece + r * HD) + lane);
-            L = L * sc0 + w * __ldcg(piece + 128 * HD + 128 + r);
-            acc.x = acc.x * sc0 + w * o2.x;
-            acc.y = acc.y * sc0 + w * o2.y;
-            acc.z = acc.z * sc0 + w * o2.z;
-            acc.w = acc.w * sc0 + w * o2.w;
-            M_ = Mn;
-        }
-        const float inv = 1.f / L;
-        T* out = reinterpret_cast<T*>(p.o) + (((long long)b * p.T + r) * p.H + h) * HD + 4 * lane;
-        const uint2 v = make_uint2(pk2<T>::pack(acc.x * inv, acc.y * inv), pk2<T>::pack(acc.z * inv, acc.w * inv));
-        *reinterpret_cast<uint2*>(out) = v;
-        if (p.lse && lane == 0) p.lse[((long long)b * p.H + h) * p.T + r] = M_ * p.scale + __logf(L);
     }
 }
 
@@ -735,6 +748,23 @@ size_t tree_attention_tc_workspace(const st_attn_args* a) {
            (size_t)a->B * a->H * sizeof(unsigned);
 }
 
+// combine_kernel with programmatic dependent launch: it is scheduled while the
+// attention kernel drains and blocks in griddepcontrol.wait until it ends.
+template <class TT>
+void launch_combine(const TcParams& prm, int G, int blocks, cudaStream_t stream) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, combine_kernel<TT>, prm, G);
+}
+
 #define ST_TRY_LAUNCH_TC(TT, MM)                                                                \
     do {                                                                                        \
         static bool attr = false;                                                               \
@@ -745,7 +775,7 @@ size_t tree_attention_tc_workspace(const st_attn_args* a) {
             attr = true;                                                                        \
         }                                                                                       \
         tree_attn_tc_kernel<TT, MM><<<G, NUM_THREADS, Cfg<MM>::SMEM_BYTES, stream>>>(tq, tk, tv, prm); \
-        combine_kernel<TT><<<a->B * a->H, 128, 0, stream>>>(prm, G);                          \
+        launch_combine<TT>(prm, G, a->B * a->H, stream);                                        \
     } while (0)
 
 st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {

@@ -28,39 +28,69 @@ namespace {
 constexpr int kThreads = 256;
 
 // Alg.-2 walk (reference token_tree.cpp:153-175) + engine truncation
-// (engine.cpp:110-121) for request b, executed by one full warp. `outs` holds
-// the per-node LLM outputs [B][T]; read through L2 when written by other CTAs.
+// (engine.cpp:110-121) for request b, executed by one full warp.
+// `outs` holds the per-node LLM outputs [B][T] (read through L2 when written by
+// other CTAs). The tree is staged in shared memory and every node's matching
+// child is found in parallel first (children have unique tokens, so at most one
+// matches), which turns the walk into a short pointer chase in smem instead of
+// a chain of dependent global loads per level.
+constexpr int kWalkMax = 1024;   // nodes staged in smem; larger trees walk from global
+
 __device__ void walk_warp(const int32_t* outs, const int32_t* __restrict__ tokens,
                           const int32_t* __restrict__ parent, int n, int T, int b,
                           const int32_t* __restrict__ budget, int32_t eos,
                           int32_t* __restrict__ verified, int32_t* __restrict__ ids,
-                          int32_t* __restrict__ len, int lane, bool coherent) {
+                          int32_t* __restrict__ len, int lane, bool coherent, int* s_out,
+                          int* s_next) {
     const int32_t* tok = tokens + (int64_t)b * T;
     const int32_t* par = parent + (int64_t)b * T;
     const int32_t* am = outs + (int64_t)b * T;
     int32_t* vrow = verified + (int64_t)b * (T + 1);
     int32_t* irow = ids + (int64_t)b * (T + 1);
-    int cur = 0, m = 0;
-    if (lane == 0) irow[0] = 0;
-    for (;;) {
-        const int32_t want = coherent ? __ldcg(am + cur) : am[cur];
-        int next = -1;
-        for (int v0 = cur + 1; v0 < n && next < 0; v0 += 32) {
-            const int v = v0 + lane;
-            const bool hit = v < n && par[v] == cur && tok[v] == want;
-            const unsigned bal = __ballot_sync(0xffffffffu, hit);
-            if (bal) next = v0 + __ffs(bal) - 1;
+    int m = 0, cur = 0;
+    if (n <= kWalkMax) {
+        for (int v = lane; v < n; v += 32) {
+            s_out[v] = coherent ? __ldcg(am + v) : am[v];
+            s_next[v] = -1;
         }
-        if (next < 0) break;
-        cur = next;
+        __syncwarp();
+        for (int v = 1 + lane; v < n; v += 32) {
+            const int u = par[v];
+            if (tok[v] == s_out[u]) s_next[u] = v;
+        }
+        __syncwarp();
         if (lane == 0) {
-            vrow[m] = want;
-            irow[m + 1] = cur;
+            irow[0] = 0;
+            for (int nx = s_next[0]; nx >= 0; nx = s_next[cur]) {
+                vrow[m] = s_out[cur];
+                irow[m + 1] = nx;
+                cur = nx;
+                ++m;
+            }
+            vrow[m] = s_out[cur];  // bonus token
         }
-        ++m;
+    } else {
+        if (lane == 0) irow[0] = 0;
+        for (;;) {
+            const int32_t want = coherent ? __ldcg(am + cur) : am[cur];
+            int next = -1;
+            for (int v0 = cur + 1; v0 < n && next < 0; v0 += 32) {
+                const int v = v0 + lane;
+                const bool hit = v < n && par[v] == cur && tok[v] == want;
+                const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                if (bal) next = v0 + __ffs(bal) - 1;
+            }
+            if (next < 0) break;
+            cur = next;
+            if (lane == 0) {
+                vrow[m] = want;
+                irow[m + 1] = cur;
+            }
+            ++m;
+        }
+        if (lane == 0) vrow[m] = coherent ? __ldcg(am + cur) : am[cur];  // bonus token
     }
     if (lane == 0) {
-        vrow[m] = coherent ? __ldcg(am + cur) : am[cur];  // bonus token
         int L = m + 1;
         if (budget && L > budget[b]) L = budget[b] > 0 ? budget[b] : 0;
         if (eos >= 0) {
@@ -76,9 +106,10 @@ __global__ void walk_kernel(const int32_t* __restrict__ outs, int T,
                             const int32_t* __restrict__ n_nodes, const int32_t* __restrict__ budget,
                             int32_t eos, int32_t* __restrict__ verified, int32_t* __restrict__ ids,
                             int32_t* __restrict__ len) {
+    __shared__ int s_out[kWalkMax], s_next[kWalkMax];
     const int b = blockIdx.x;
     walk_warp(outs, tokens, parent, n_nodes[b], T, b, budget, eos, verified, ids, len,
-              threadIdx.x & 31, false);
+              threadIdx.x & 31, false, s_out, s_next);
 }
 
 // Order-preserving 64-bit key: high word = orderable float bits, low word =
@@ -171,7 +202,9 @@ greedy_verify_kernel(const float* __restrict__ logits, int T, int V,
     }
     __syncwarp();
     __threadfence_block();
-    walk_warp(argmax_ws, tokens, parent, n, T, b, budget, eos, verified, ids, len, lane, true);
+    __shared__ int s_out[kWalkMax], s_next[kWalkMax];
+    walk_warp(argmax_ws, tokens, parent, n, T, b, budget, eos, verified, ids, len, lane, true,
+              s_out, s_next);
     if (lane == 0) tickets[b] = 0;
 }
 
