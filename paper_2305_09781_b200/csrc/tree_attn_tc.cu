@@ -82,7 +82,7 @@ struct TcParams {
     void* o;
     float* lse;
     float* partial;      // [gridDim.x * 2][SLOT_FLOATS]
-    unsigned* tickets;   // [B * H] (unused since the combine kernel; kept for layout)
+    long long* sched;    // [gridDim.x + 1][4]: range start, last pair start, last pair tiles
     int B, T, H, W;
     float c_log2;        // scale * log2(e)
     float scale;
@@ -238,6 +238,19 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     const long long total = total_tiles(p);
     const long long t_begin = range_start(blockIdx.x, total, G);
     const long long t_end = range_start(blockIdx.x + 1, total, G);
+    if (threadIdx.x == 0) {  // schedule table for combine_kernel
+        long long* e = p.sched + 4 * blockIdx.x;
+        e[0] = t_begin;
+        if (t_end > t_begin) {
+            const Seg last = find_seg(p, t_end - 1, t_end);
+            e[1] = last.pair_start;
+            e[2] = last.ntiles;
+        } else {
+            e[1] = -1;
+            e[2] = 0;
+        }
+        if (blockIdx.x == gridDim.x - 1) p.sched[4 * gridDim.x] = t_end;  // == total
+    }
     if (p.trace && threadIdx.x == 0) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
@@ -596,44 +609,47 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 // w, w+4, ...; lane l owns d columns [4l, 4l+4). All loads of a row (every
 // piece's m, l and O float4) are issued before any use, so a row costs one
 // L2 round trip. Fixed piece order -> deterministic.
+// Merge of the partial pieces of pairs that the stream-K schedule split over
+// several CTAs. Block c handles the pair that starts in CTA c's range and
+// continues past it (at most one per CTA), read from the schedule table the
+// attention kernel published: its pieces are CTA c's last segment (slot 0 if
+// that segment is c's whole range, else slot 1) and the first segment (slot 0)
+// of each following non-empty CTA until the pair ends. Warp w merges rows w,
+// w+8, ...; lane l owns d columns [4l, 4l+4); all loads of a row group are
+// issued before use. Fixed piece order -> deterministic.
 template <class T>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(256)
 combine_kernel(const TcParams p, int G) {
     constexpr int MAXP = 4;   // pieces held in registers (more are folded in a slow loop)
-    constexpr int RPW = 4;    // rows per warp, all in flight together
-    __shared__ int s_slots[16];
-    __shared__ int s_np;
-    const int bh = blockIdx.x;
-    const int b = bh / p.H, h = bh % p.H;
-    // PDL: everything above is independent of the attention kernel's output
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (threadIdx.x == 0) {
-        long long total = 0, pair_start = -1;
-        int nt = 0;
-        for (int bb = 0; bb < p.B; ++bb) {
-            const int t_ = ntiles_of(p, bb);
-            if (bb == b) {
-                nt = t_;
-                pair_start = total + (long long)h * t_;
-            }
-            total += (long long)p.H * t_;
-        }
-        int np = 0;
-        if (nt > 0) {
-            const long long c_first = cta_of(pair_start, total, G);
-            const long long c_last = cta_of(pair_start + nt - 1, total, G);
-            if (c_first != c_last)
-                for (long long cc = c_first; cc <= c_last && np < 16; ++cc) {
-                    const long long rs = range_start(cc, total, G);
-                    if (range_start(cc + 1, total, G) == rs) continue;  // empty range
-                    s_slots[np++] = (int)(cc * 2 + ((pair_start > rs) ? 1 : 0));
-                }
-        }
-        s_np = np;
+    constexpr int RPW = 4;    // rows per warp in flight together
+    const int cta = blockIdx.x;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: wait for the attention kernel
+    const long long* tab = p.sched;
+    const long long rs = __ldcg(tab + 4 * cta), re = __ldcg(tab + 4 * (cta + 1));
+    const long long ps = __ldcg(tab + 4 * cta + 1), nt = __ldcg(tab + 4 * cta + 2);
+    if (re <= rs || ps < rs || ps + nt <= re) return;  // empty / pair not started here / not split
+    const long long pend = ps + nt;
+    int slots[16];
+    int np = 0;
+    slots[np++] = cta * 2 + (ps == rs ? 0 : 1);
+    for (int cc = cta + 1; cc < G && np < 16; ++cc) {
+        const long long r0 = __ldcg(tab + 4 * cc), r1 = __ldcg(tab + 4 * (cc + 1));
+        if (r0 >= pend) break;
+        if (r1 > r0) slots[np++] = cc * 2;  // non-empty CTA: its first segment
     }
-    __syncthreads();
-    const int np = s_np;
-    if (np == 0) return;  // written directly by the attention kernel
+    // (b, h) of the pair from its start tile: pairs are laid out request-major
+    long long base = 0;
+    int b = 0, h = 0;
+    for (int bb = 0; bb < p.B; ++bb) {
+        const int t_ = ntiles_of(p, bb);
+        const long long span = (long long)p.H * t_;
+        if (ps < base + span) {
+            b = bb;
+            h = (int)((ps - base) / t_);
+            break;
+        }
+        base += span;
+    }
     const int n = __ldg(p.n_nodes + b);
     const float c = p.c_log2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -647,7 +663,7 @@ combine_kernel(const TcParams p, int G) {
 #pragma unroll
             for (int k = 0; k < MAXP; ++k) {
                 if (k < np && r < n) {
-                    const float* piece = p.partial + (long long)s_slots[k] * SLOT_FLOATS;
+                    const float* piece = p.partial + (long long)slots[k] * SLOT_FLOATS;
                     mk[i][k] = __ldcg(piece + 128 * HD + r);
                     lk[i][k] = __ldcg(piece + 128 * HD + 128 + r);
                     ok[i][k] = __ldcg(reinterpret_cast<const float4*>(piece + r * HD) + lane);
@@ -676,7 +692,7 @@ combine_kernel(const TcParams p, int G) {
                 }
             }
             for (int k = MAXP; k < np; ++k) {  // rare: more pieces than registers
-                const float* piece = p.partial + (long long)s_slots[k] * SLOT_FLOATS;
+                const float* piece = p.partial + (long long)slots[k] * SLOT_FLOATS;
                 const float m2 = __ldcg(piece + 128 * HD + r);
                 if (m2 == -INFINITY) continue;
                 const float Mn = fmaxf(M_, m2);
@@ -745,7 +761,7 @@ bool tree_attention_tc_supported(const st_attn_args* a) {
 
 size_t tree_attention_tc_workspace(const st_attn_args* a) {
     return align_up((size_t)num_sms() * 2 * SLOT_FLOATS * sizeof(float), 256) +
-           (size_t)a->B * a->H * sizeof(unsigned);
+           (size_t)(num_sms() + 1) * 4 * sizeof(long long);
 }
 
 // combine_kernel with programmatic dependent launch: it is scheduled while the
@@ -754,7 +770,7 @@ template <class TT>
 void launch_combine(const TcParams& prm, int G, int blocks, cudaStream_t stream) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(blocks);
-    cfg.blockDim = dim3(512);
+    cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -775,7 +791,7 @@ void launch_combine(const TcParams& prm, int G, int blocks, cudaStream_t stream)
             attr = true;                                                                        \
         }                                                                                       \
         tree_attn_tc_kernel<TT, MM><<<G, NUM_THREADS, Cfg<MM>::SMEM_BYTES, stream>>>(tq, tk, tv, prm); \
-        launch_combine<TT>(prm, G, a->B * a->H, stream);                                        \
+        launch_combine<TT>(prm, G, G, stream);                                                  \
     } while (0)
 
 st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
@@ -809,8 +825,8 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     prm.o = a->o;
     prm.lse = a->lse;
     prm.partial = reinterpret_cast<float*>(a->workspace);
-    prm.tickets = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(a->workspace) +
-                                              align_up((size_t)G * 2 * SLOT_FLOATS * sizeof(float), 256));
+    prm.sched = reinterpret_cast<long long*>(reinterpret_cast<uint8_t*>(a->workspace) +
+                                             align_up((size_t)G * 2 * SLOT_FLOATS * sizeof(float), 256));
     prm.B = a->B;
     prm.T = a->T;
     prm.H = a->H;
