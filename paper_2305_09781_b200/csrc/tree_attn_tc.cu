@@ -83,6 +83,7 @@ struct TcParams {
     float* lse;
     float* partial;      // [gridDim.x * 2][SLOT_FLOATS]
     long long* sched;    // [gridDim.x + 1][4]: range start, last pair start, last pair tiles
+    unsigned* tickets;   // [B * H] pieces finished per split pair (reset by the merger)
     int B, T, H, W;
     float c_log2;        // scale * log2(e)
     float scale;
@@ -178,6 +179,96 @@ __device__ __forceinline__ void store_row(T* dst_row, const float* v, float scal
     }
 }
 
+// Merge of a split pair's pieces by its last finisher: thread (row r, half)
+// combines its DCOLS output columns. Every piece's (m, l) and O chunk is loaded
+// before any use (the pieces sit in L2), so the merge costs one round trip.
+// Piece slots come from the schedule table: CTA c_first contributes its last
+// segment (slot 0 iff that segment is its whole range), later non-empty CTAs
+// their first segment (slot 0). Fixed piece order -> deterministic.
+template <class T, int DCOLS>
+__device__ __noinline__ void merge_pieces(const TcParams& p, const Seg& s, long long c_first,
+                                             long long c_last, int r, int half, bool valid) {
+    constexpr int MAXP = 2;
+    if (!valid) return;
+    int slots[8];
+    int np = 0;
+    for (long long cc = c_first; cc <= c_last && np < 8; ++cc) {
+        const long long rs = __ldcg(p.sched + 4 * cc), re = __ldcg(p.sched + 4 * (cc + 1));
+        if (re <= rs) continue;  // empty range: no piece
+        slots[np++] = (int)(cc * 2 + ((cc == c_first && s.pair_start > rs) ? 1 : 0));
+    }
+    const float c = p.c_log2;
+    float mk[MAXP], lk[MAXP];
+#pragma unroll
+    for (int k = 0; k < MAXP; ++k) {
+        if (k < np) {
+            const float* piece = p.partial + (long long)slots[k] * SLOT_FLOATS;
+            mk[k] = __ldcg(piece + 128 * HD + r);
+            lk[k] = __ldcg(piece + 128 * HD + 128 + r);
+        }
+    }
+    float M_ = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < MAXP; ++k)
+        if (k < np) M_ = fmaxf(M_, mk[k]);
+    for (int k = MAXP; k < np; ++k)
+        M_ = fmaxf(M_, __ldcg(p.partial + (long long)slots[k] * SLOT_FLOATS + 128 * HD + r));
+    float wk[8];
+    float L = 0.f;
+    for (int k = 0; k < np; ++k) {
+        const float m_k = k < MAXP ? mk[k] : __ldcg(p.partial + (long long)slots[k] * SLOT_FLOATS + 128 * HD + r);
+        const float l_k = k < MAXP ? lk[k] : __ldcg(p.partial + (long long)slots[k] * SLOT_FLOATS + 128 * HD + 128 + r);
+        wk[k] = m_k == -INFINITY ? 0.f : ex2((m_k - M_) * c);
+        L += wk[k] * l_k;
+    }
+    const float inv = 1.f / L;
+    T* out_base = reinterpret_cast<T*>(p.o) + (((long long)s.b * p.T + r) * p.H + s.h) * HD;
+    // 32 output columns at a time: both pieces' chunks in flight together
+#pragma unroll 1
+    for (int d0 = half * DCOLS; d0 < (half + 1) * DCOLS; d0 += 32) {
+        float acc[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) acc[e] = 0.f;
+        float4 ok[MAXP][8];
+#pragma unroll
+        for (int k = 0; k < MAXP; ++k)
+            if (k < np) {
+                const float4* src = reinterpret_cast<const float4*>(
+                    p.partial + (long long)slots[k] * SLOT_FLOATS + r * HD + d0);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) ok[k][e] = __ldcg(src + e);
+            }
+#pragma unroll
+        for (int k = 0; k < MAXP; ++k) {
+            if (k < np) {
+                const float w = wk[k];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    acc[4 * e] += w * ok[k][e].x;
+                    acc[4 * e + 1] += w * ok[k][e].y;
+                    acc[4 * e + 2] += w * ok[k][e].z;
+                    acc[4 * e + 3] += w * ok[k][e].w;
+                }
+            }
+        }
+        for (int k = MAXP; k < np; ++k) {  // pairs spanning more CTAs
+            const float w = wk[k];
+            const float4* src = reinterpret_cast<const float4*>(
+                p.partial + (long long)slots[k] * SLOT_FLOATS + r * HD + d0);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const float4 x = __ldcg(src + e);
+                acc[4 * e] += w * x.x;
+                acc[4 * e + 1] += w * x.y;
+                acc[4 * e + 2] += w * x.z;
+                acc[4 * e + 3] += w * x.w;
+            }
+        }
+        store_row<T, 32>(out_base + d0, acc, inv);
+    }
+    if (p.lse && half == 0) p.lse[((long long)s.b * p.H + s.h) * p.T + r] = M_ * p.scale + __logf(L);
+}
+
 template <class T, int M>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -207,6 +298,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     uint64_t* pv_done = p_full + 2;      // [2]
     uint64_t* o_empty = pv_done + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
+    __shared__ int s_merge;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -587,7 +679,31 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             }
 
             if (threadIdx.x == 0) K1_GT(4);
-            // split pairs: the partial (O, m, l) pieces are merged by combine_kernel
+            if (!full) {
+                // Split pair: this piece is in the workspace. The LAST piece to
+                // finish merges (a ticket elects it; nobody waits). With the
+                // stream-K ranges that is almost always the CTA whose range ends
+                // in the pair, at the end of its range.
+                __threadfence();
+                named_bar_sync(1, 128);
+                const long long pair_end = s.pair_start + s.ntiles;
+                const long long c_first = cta_of(s.pair_start, total, G);
+                const long long c_last = cta_of(pair_end - 1, total, G);
+                if (threadIdx.x == 0) {
+                    unsigned pieces = 0;
+                    for (long long cc = c_first; cc <= c_last; ++cc)
+                        pieces += __ldcg(p.sched + 4 * (cc + 1)) > __ldcg(p.sched + 4 * cc);
+                    const unsigned old = atomicAdd(p.tickets + s.b * p.H + s.h, 1u);
+                    s_merge = (old == pieces - 1);
+                }
+                named_bar_sync(1, 128);
+                if (s_merge) {
+                    __threadfence();
+                    merge_pieces<T, DCOLS>(p, s, c_first, c_last, r, half, valid);
+                    if (threadIdx.x == 0) p.tickets[s.b * p.H + s.h] = 0u;
+                }
+                if (threadIdx.x == 0) K1_GT(7);
+            }
             t += ntl;
         }
     }
@@ -761,7 +877,8 @@ bool tree_attention_tc_supported(const st_attn_args* a) {
 
 size_t tree_attention_tc_workspace(const st_attn_args* a) {
     return align_up((size_t)num_sms() * 2 * SLOT_FLOATS * sizeof(float), 256) +
-           (size_t)(num_sms() + 1) * 4 * sizeof(long long);
+           align_up((size_t)(num_sms() + 1) * 4 * sizeof(long long), 256) +
+           (size_t)a->B * a->H * sizeof(unsigned);
 }
 
 // combine_kernel with programmatic dependent launch: it is scheduled while the
@@ -791,7 +908,6 @@ void launch_combine(const TcParams& prm, int G, int blocks, cudaStream_t stream)
             attr = true;                                                                        \
         }                                                                                       \
         tree_attn_tc_kernel<TT, MM><<<G, NUM_THREADS, Cfg<MM>::SMEM_BYTES, stream>>>(tq, tk, tv, prm); \
-        launch_combine<TT>(prm, G, G, stream);                                                  \
     } while (0)
 
 st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
@@ -827,6 +943,8 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     prm.partial = reinterpret_cast<float*>(a->workspace);
     prm.sched = reinterpret_cast<long long*>(reinterpret_cast<uint8_t*>(a->workspace) +
                                              align_up((size_t)G * 2 * SLOT_FLOATS * sizeof(float), 256));
+    prm.tickets = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(prm.sched) +
+                                              align_up((size_t)(G + 1) * 4 * sizeof(long long), 256));
     prm.B = a->B;
     prm.T = a->T;
     prm.H = a->H;
