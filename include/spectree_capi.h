@@ -118,6 +118,12 @@ st_status st_kv_compact(st_dtype dtype, int B, int Hkv, int D, int64_t Lmax, int
                         const int32_t* n_keep, const int32_t* prefix_len,
                         int32_t* new_prefix_len, void* k_cache, void* v_cache, void* stream);
 
+/* Head-sharded attention (C4): reorder an all-gathered
+ * [world][B][T][Hl][D] (rank r's K1 output for heads r*Hl..r*Hl+Hl-1) into
+ * [B][T][world*Hl][D]. */
+st_status st_heads_gather_layout(st_dtype dtype, int world, int B, int T, int Hl, int D,
+                                 const void* gathered, void* out, void* stream);
+
 /* ------------------------------------------------------------------ K3 ---
  * Greedy verification: per-node argmax over logits (lowest id wins ties,
  * reference transformer.cpp:116-122) then the Alg.-2 walk (reference

@@ -55,6 +55,7 @@ SIGNATURES = {
     "st_tree_attention_path": (_I, [C.POINTER(AttnArgs)]),
     "st_kv_append": (_I, [_I, _I, _I, _I, _I, _I64, _V, _V, _V, _V, _V, _V, _V]),
     "st_kv_compact": (_I, [_I, _I, _I, _I, _I64, _I, _I64, _V, _I, _V, _V, _V, _V, _V, _V]),
+    "st_heads_gather_layout": (_I, [_I, _I, _I, _I, _I, _I, _V, _V, _V]),
     "st_verify_workspace_size": (_Z, [_I, _I]),
     "st_verify_greedy": (_I, [_V, _I, _I, _I, _V, _V, _V, _V, C.c_int32, _V, _V, _V, _V, _V, _V]),
     "st_verify_outputs": (_I, [_V, _I, _I, _V, _V, _V, _V, C.c_int32, _V, _V, _V, _V]),
@@ -162,6 +163,17 @@ def kv_compact(ids, n_keep, prefix_len, k_cache, v_cache, new_prefix_len=None, s
                               _ptr(ids), ids.shape[-1], _ptr(n_keep), _ptr(prefix_len),
                               _ptr(new_prefix_len), _ptr(k_cache), _ptr(v_cache),
                               _stream(stream)))
+
+
+def heads_gather_layout(gathered, world, out=None, stream=None):
+    """[world, B, T, Hl, D] -> [B, T, world*Hl, D] (C4 head-sharded outputs)."""
+    W, B, T, Hl, D = gathered.shape
+    assert W == world
+    if out is None:
+        out = torch.empty((B, T, world * Hl, D), dtype=gathered.dtype, device=gathered.device)
+    check(lib().st_heads_gather_layout(DTYPES[gathered.dtype], world, B, T, Hl, D, _ptr(gathered),
+                                       _ptr(out), _stream(stream)))
+    return out
 
 
 # ------------------------------------------------------------------ K3 ----

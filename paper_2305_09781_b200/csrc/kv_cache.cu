@@ -16,6 +16,8 @@
 // source that a LATER copy still needs; the kernel therefore walks k
 // sequentially (one barrier per row) while all threads of the block copy the
 // row's Hkv*D elements in parallel with 16-byte vectors.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace st {
@@ -135,3 +137,45 @@ st_status st_kv_compact(st_dtype dtype, int B, int Hkv, int D, int64_t Lmax, int
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------------
+// Head-sharded attention (C4): every rank computes K1 for its Hl heads and the
+// ranks all-gather their [B][T][Hl][D] outputs (NCCL, contiguous per rank);
+// this reorders the gathered [world][B][T][Hl][D] into [B][T][world*Hl][D]
+// (the row layout the output projection consumes). 16-byte vector copies.
+namespace st {
+namespace {
+__global__ void heads_layout_kernel(const int4* __restrict__ src, int4* __restrict__ dst,
+                                    int world, int BT, int row_vecs /* Hl*D*s/16 */) {
+    const int64_t total = (int64_t)world * BT * row_vecs;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int e = (int)(i % row_vecs);
+        const int64_t rest = i / row_vecs;
+        const int bt = (int)(rest % BT);
+        const int r = (int)(rest / BT);
+        dst[((int64_t)bt * world + r) * row_vecs + e] = src[i];
+    }
+}
+}  // namespace
+}  // namespace st
+
+extern "C" st_status st_heads_gather_layout(st_dtype dtype, int world, int B, int T, int Hl, int D,
+                                            const void* gathered, void* out, void* stream) {
+    if (st_status e = st::require_device()) return e;
+    ST_CHECK_ARG(world >= 1 && B >= 0 && T >= 1 && Hl >= 1 && D >= 1, ST_ERR_SHAPE_MISMATCH,
+                 "bad shape");
+    const int64_t row_bytes = (int64_t)Hl * D * st::dtype_size(dtype);
+    ST_CHECK_ARG(row_bytes % 16 == 0 && st::dtype_size(dtype) != 0, ST_ERR_SHAPE_MISMATCH,
+                 "Hl*D*sizeof(dtype) must be a multiple of 16 bytes");
+    if (B == 0) return ST_OK;
+    ST_CHECK_ARG(gathered && out && gathered != out, ST_ERR_INVALID_ARGUMENT,
+                 "null or aliased pointer");
+    const int row_vecs = (int)(row_bytes / 16);
+    const int64_t total = (int64_t)world * B * T * row_vecs;
+    const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    st::heads_layout_kernel<<<blocks, 256, 0, st::as_stream(stream)>>>(
+        (const int4*)gathered, (int4*)out, world, B * T, row_vecs);
+    ST_LAUNCH_CHECK();
+    return ST_OK;
+}

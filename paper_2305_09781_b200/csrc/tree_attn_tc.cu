@@ -83,7 +83,6 @@ struct TcParams {
     float* lse;
     float* partial;      // [gridDim.x * 2][SLOT_FLOATS]
     long long* sched;    // [gridDim.x + 1][4]: range start, last pair start, last pair tiles
-    unsigned* tickets;   // [B * H] pieces finished per split pair (reset by the merger)
     int B, T, H, W;
     float c_log2;        // scale * log2(e)
     float scale;
@@ -179,96 +178,6 @@ __device__ __forceinline__ void store_row(T* dst_row, const float* v, float scal
     }
 }
 
-// Merge of a split pair's pieces by its last finisher: thread (row r, half)
-// combines its DCOLS output columns. Every piece's (m, l) and O chunk is loaded
-// before any use (the pieces sit in L2), so the merge costs one round trip.
-// Piece slots come from the schedule table: CTA c_first contributes its last
-// segment (slot 0 iff that segment is its whole range), later non-empty CTAs
-// their first segment (slot 0). Fixed piece order -> deterministic.
-template <class T, int DCOLS>
-__device__ __noinline__ void merge_pieces(const TcParams& p, const Seg& s, long long c_first,
-                                             long long c_last, int r, int half, bool valid) {
-    constexpr int MAXP = 2;
-    if (!valid) return;
-    int slots[8];
-    int np = 0;
-    for (long long cc = c_first; cc <= c_last && np < 8; ++cc) {
-        const long long rs = __ldcg(p.sched + 4 * cc), re = __ldcg(p.sched + 4 * (cc + 1));
-        if (re <= rs) continue;  // empty range: no piece
-        slots[np++] = (int)(cc * 2 + ((cc == c_first && s.pair_start > rs) ? 1 : 0));
-    }
-    const float c = p.c_log2;
-    float mk[MAXP], lk[MAXP];
-#pragma unroll
-    for (int k = 0; k < MAXP; ++k) {
-        if (k < np) {
-            const float* piece = p.partial + (long long)slots[k] * SLOT_FLOATS;
-            mk[k] = __ldcg(piece + 128 * HD + r);
-            lk[k] = __ldcg(piece + 128 * HD + 128 + r);
-        }
-    }
-    float M_ = -INFINITY;
-#pragma unroll
-    for (int k = 0; k < MAXP; ++k)
-        if (k < np) M_ = fmaxf(M_, mk[k]);
-    for (int k = MAXP; k < np; ++k)
-        M_ = fmaxf(M_, __ldcg(p.partial + (long long)slots[k] * SLOT_FLOATS + 128 * HD + r));
-    float wk[8];
-    float L = 0.f;
-    for (int k = 0; k < np; ++k) {
-        const float m_k = k < MAXP ? mk[k] : __ldcg(p.partial + (long long)slots[k] * SLOT_FLOATS + 128 * HD + r);
-        const float l_k = k < MAXP ? lk[k] : __ldcg(p.partial + (long long)slots[k] * SLOT_FLOATS + 128 * HD + 128 + r);
-        wk[k] = m_k == -INFINITY ? 0.f : ex2((m_k - M_) * c);
-        L += wk[k] * l_k;
-    }
-    const float inv = 1.f / L;
-    T* out_base = reinterpret_cast<T*>(p.o) + (((long long)s.b * p.T + r) * p.H + s.h) * HD;
-    // 32 output columns at a time: both pieces' chunks in flight together
-#pragma unroll 1
-    for (int d0 = half * DCOLS; d0 < (half + 1) * DCOLS; d0 += 32) {
-        float acc[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) acc[e] = 0.f;
-        float4 ok[MAXP][8];
-#pragma unroll
-        for (int k = 0; k < MAXP; ++k)
-            if (k < np) {
-                const float4* src = reinterpret_cast<const float4*>(
-                    p.partial + (long long)slots[k] * SLOT_FLOATS + r * HD + d0);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) ok[k][e] = __ldcg(src + e);
-            }
-#pragma unroll
-        for (int k = 0; k < MAXP; ++k) {
-            if (k < np) {
-                const float w = wk[k];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    acc[4 * e] += w * ok[k][e].x;
-                    acc[4 * e + 1] += w * ok[k][e].y;
-                    acc[4 * e + 2] += w * ok[k][e].z;
-                    acc[4 * e + 3] += w * ok[k][e].w;
-                }
-            }
-        }
-        for (int k = MAXP; k < np; ++k) {  // pairs spanning more CTAs
-            const float w = wk[k];
-            const float4* src = reinterpret_cast<const float4*>(
-                p.partial + (long long)slots[k] * SLOT_FLOATS + r * HD + d0);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const float4 x = __ldcg(src + e);
-                acc[4 * e] += w * x.x;
-                acc[4 * e + 1] += w * x.y;
-                acc[4 * e + 2] += w * x.z;
-                acc[4 * e + 3] += w * x.w;
-            }
-        }
-        store_row<T, 32>(out_base + d0, acc, inv);
-    }
-    if (p.lse && half == 0) p.lse[((long long)s.b * p.H + s.h) * p.T + r] = M_ * p.scale + __logf(L);
-}
-
 template <class T, int M>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -298,7 +207,6 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     uint64_t* pv_done = p_full + 2;      // [2]
     uint64_t* o_empty = pv_done + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
-    __shared__ int s_merge;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -337,6 +245,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             const Seg last = find_seg(p, t_end - 1, t_end);
             e[1] = last.pair_start;
             e[2] = last.ntiles;
+            e[3] = (long long)last.b * p.H + last.h;
         } else {
             e[1] = -1;
             e[2] = 0;
@@ -679,31 +588,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             }
 
             if (threadIdx.x == 0) K1_GT(4);
-            if (!full) {
-                // Split pair: this piece is in the workspace. The LAST piece to
-                // finish merges (a ticket elects it; nobody waits). With the
-                // stream-K ranges that is almost always the CTA whose range ends
-                // in the pair, at the end of its range.
-                __threadfence();
-                named_bar_sync(1, 128);
-                const long long pair_end = s.pair_start + s.ntiles;
-                const long long c_first = cta_of(s.pair_start, total, G);
-                const long long c_last = cta_of(pair_end - 1, total, G);
-                if (threadIdx.x == 0) {
-                    unsigned pieces = 0;
-                    for (long long cc = c_first; cc <= c_last; ++cc)
-                        pieces += __ldcg(p.sched + 4 * (cc + 1)) > __ldcg(p.sched + 4 * cc);
-                    const unsigned old = atomicAdd(p.tickets + s.b * p.H + s.h, 1u);
-                    s_merge = (old == pieces - 1);
-                }
-                named_bar_sync(1, 128);
-                if (s_merge) {
-                    __threadfence();
-                    merge_pieces<T, DCOLS>(p, s, c_first, c_last, r, half, valid);
-                    if (threadIdx.x == 0) p.tickets[s.b * p.H + s.h] = 0u;
-                }
-                if (threadIdx.x == 0) K1_GT(7);
-            }
+            // split pairs: the partial (O, m, l) pieces are merged by combine_kernel
             t += ntl;
         }
     }
@@ -736,35 +621,27 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 template <class T>
 __global__ void __launch_bounds__(256)
 combine_kernel(const TcParams p, int G) {
-    constexpr int MAXP = 4;   // pieces held in registers (more are folded in a slow loop)
-    constexpr int RPW = 4;    // rows per warp in flight together
+    constexpr int MAXP = 4;   // pieces held in registers; more are merged online
+    constexpr int RPW = 2;    // rows per warp in flight together
     const int cta = blockIdx.x;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: wait for the attention kernel
     const long long* tab = p.sched;
     const long long rs = __ldcg(tab + 4 * cta), re = __ldcg(tab + 4 * (cta + 1));
     const long long ps = __ldcg(tab + 4 * cta + 1), nt = __ldcg(tab + 4 * cta + 2);
     if (re <= rs || ps < rs || ps + nt <= re) return;  // empty / pair not started here / not split
+    const int bh = (int)__ldcg(tab + 4 * cta + 3);
+    const int b = bh / p.H, h = bh % p.H;
     const long long pend = ps + nt;
-    int slots[16];
+    // first MAXP pieces: this CTA's last segment, then the first segment of each
+    // following non-empty CTA; `next_cta` continues the list for the online tail
+    int slots[MAXP];
     int np = 0;
     slots[np++] = cta * 2 + (ps == rs ? 0 : 1);
-    for (int cc = cta + 1; cc < G && np < 16; ++cc) {
-        const long long r0 = __ldcg(tab + 4 * cc), r1 = __ldcg(tab + 4 * (cc + 1));
+    int next_cta = cta + 1;
+    for (; next_cta < G && np < MAXP; ++next_cta) {
+        const long long r0 = __ldcg(tab + 4 * next_cta), r1 = __ldcg(tab + 4 * (next_cta + 1));
         if (r0 >= pend) break;
-        if (r1 > r0) slots[np++] = cc * 2;  // non-empty CTA: its first segment
-    }
-    // (b, h) of the pair from its start tile: pairs are laid out request-major
-    long long base = 0;
-    int b = 0, h = 0;
-    for (int bb = 0; bb < p.B; ++bb) {
-        const int t_ = ntiles_of(p, bb);
-        const long long span = (long long)p.H * t_;
-        if (ps < base + span) {
-            b = bb;
-            h = (int)((ps - base) / t_);
-            break;
-        }
-        base += span;
+        if (r1 > r0) slots[np++] = next_cta * 2;
     }
     const int n = __ldg(p.n_nodes + b);
     const float c = p.c_log2;
@@ -807,12 +684,17 @@ combine_kernel(const TcParams p, int G) {
                     acc.w += w * ok[i][k].w;
                 }
             }
-            for (int k = MAXP; k < np; ++k) {  // rare: more pieces than registers
-                const float* piece = p.partial + (long long)slots[k] * SLOT_FLOATS;
+            // pairs spanning more than MAXP CTAs: online merge of the rest
+            for (int cc = next_cta; cc < G; ++cc) {
+                const long long q0 = __ldcg(tab + 4 * cc), q1 = __ldcg(tab + 4 * (cc + 1));
+                if (q0 >= pend) break;
+                if (q1 <= q0) continue;
+                const float* piece = p.partial + (long long)(cc * 2) * SLOT_FLOATS;
                 const float m2 = __ldcg(piece + 128 * HD + r);
                 if (m2 == -INFINITY) continue;
                 const float Mn = fmaxf(M_, m2);
-                const float sc0 = ex2((M_ - Mn) * c), w = ex2((m2 - Mn) * c);
+                const float sc0 = M_ == -INFINITY ? 0.f : ex2((M_ - Mn) * c);
+                const float w = ex2((m2 - Mn) * c);
                 const float4 o2 = __ldcg(reinterpret_cast<const float4*>(piece + r * HD) + lane);
                 L = L * sc0 + w * __ldcg(piece + 128 * HD + 128 + r);
                 acc.x = acc.x * sc0 + w * o2.x;
@@ -877,8 +759,7 @@ bool tree_attention_tc_supported(const st_attn_args* a) {
 
 size_t tree_attention_tc_workspace(const st_attn_args* a) {
     return align_up((size_t)num_sms() * 2 * SLOT_FLOATS * sizeof(float), 256) +
-           align_up((size_t)(num_sms() + 1) * 4 * sizeof(long long), 256) +
-           (size_t)a->B * a->H * sizeof(unsigned);
+           (size_t)(num_sms() + 1) * 4 * sizeof(long long);
 }
 
 // combine_kernel with programmatic dependent launch: it is scheduled while the
@@ -908,6 +789,7 @@ void launch_combine(const TcParams& prm, int G, int blocks, cudaStream_t stream)
             attr = true;                                                                        \
         }                                                                                       \
         tree_attn_tc_kernel<TT, MM><<<G, NUM_THREADS, Cfg<MM>::SMEM_BYTES, stream>>>(tq, tk, tv, prm); \
+        launch_combine<TT>(prm, G, G, stream);                                                  \
     } while (0)
 
 st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
@@ -943,8 +825,6 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     prm.partial = reinterpret_cast<float*>(a->workspace);
     prm.sched = reinterpret_cast<long long*>(reinterpret_cast<uint8_t*>(a->workspace) +
                                              align_up((size_t)G * 2 * SLOT_FLOATS * sizeof(float), 256));
-    prm.tickets = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(prm.sched) +
-                                              align_up((size_t)(G + 1) * 4 * sizeof(long long), 256));
     prm.B = a->B;
     prm.T = a->T;
     prm.H = a->H;

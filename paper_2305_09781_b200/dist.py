@@ -42,3 +42,29 @@ def gather_accepted(verified: torch.Tensor, lengths: torch.Tensor, world: int,
     ver = parts[:, : B * T1].reshape(world * B, T1)
     ln = parts[:, B * T1:].reshape(world * B)
     return ver, ln
+
+
+def head_shard(n_heads: int, world: int, rank: int) -> tuple[int, int]:
+    """Heads [h0, h1) owned by `rank` for head-sharded attention (C4). The
+    Q/K/V projections are column-sharded the same way, so each rank's KV cache
+    holds only its heads and K1 runs unchanged on H = n_heads / world."""
+    if n_heads % world:
+        raise ValueError(f"{n_heads} heads do not split over {world} ranks")
+    per = n_heads // world
+    return rank * per, (rank + 1) * per
+
+
+def gather_head_outputs(o_local: torch.Tensor, world: int, gathered: torch.Tensor | None = None,
+                        out: torch.Tensor | None = None):
+    """All-gather every rank's K1 output [B, T, Hl, D] (NCCL, one contiguous
+    chunk per rank) and lay it out as [B, T, world*Hl, D] with the CUDA layout
+    kernel (st_heads_gather_layout)."""
+    from . import _capi
+    B, T, Hl, D = o_local.shape
+    if gathered is None:
+        gathered = torch.empty((world, B, T, Hl, D), dtype=o_local.dtype, device=o_local.device)
+    if world > 1:
+        dist.all_gather_into_tensor(gathered.view(-1), o_local.contiguous().view(-1))
+    else:
+        gathered[0].copy_(o_local)
+    return _capi.heads_gather_layout(gathered, world, out=out)

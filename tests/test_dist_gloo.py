@@ -86,3 +86,42 @@ def test_two_rank_gather_equals_single_process():
     ref_ver, ref_ln = _verify_shard(R, tok, par, n, logits, 0, len(n))
     np.testing.assert_array_equal(got_ln, ref_ln)
     np.testing.assert_array_equal(got_ver, ref_ver)
+
+
+def _head_worker(rank, world, port, q):
+    """C4 plumbing: each rank owns heads head_shard(H, world, rank), computes its
+    slice of a (toy, CPU) attention output, and all-gathers; the gathered chunks
+    re-laid out [B,T,world*Hl,D] must equal the unsharded result."""
+    from paper_2305_09781_b200.dist import head_shard
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = torch.Generator().manual_seed(0)
+    B, T, H, D = 2, 5, 8, 16
+    full = torch.randn(B, T, H, D, generator=g)
+    h0, h1 = head_shard(H, world, rank)
+    mine = full[:, :, h0:h1].contiguous()
+    gathered = torch.empty(world * mine.numel())
+    dist.all_gather_into_tensor(gathered, mine.view(-1))
+    out = gathered.view(world, B, T, h1 - h0, D).permute(1, 2, 0, 3, 4).reshape(B, T, H, D)
+    if rank == 0:
+        q.put(bool(torch.equal(out, full)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_head_sharded_gather_layout_two_ranks():
+    from paper_2305_09781_b200.dist import head_shard
+    assert head_shard(64, 8, 3) == (24, 32)
+    with pytest.raises(ValueError):
+        head_shard(10, 4, 0)
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_head_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    assert q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0

@@ -241,3 +241,12 @@ def test_library_fails_loudly_without_device_path(capi):
         capi.build_masks(torch.zeros((1, 100), dtype=torch.int32, device="cuda"),
                          torch.ones(1, dtype=torch.int32, device="cuda"), W=1)
     assert e.value.code == "shape_mismatch"
+
+
+def test_heads_gather_layout(capi):
+    """C4: [world,B,T,Hl,D] -> [B,T,world*Hl,D] equals a torch permute."""
+    g = torch.randn(4, 3, 7, 8, 128, device="cuda").half()
+    out = capi.heads_gather_layout(g, 4)
+    torch.cuda.synchronize()
+    ref = g.permute(1, 2, 0, 3, 4).reshape(3, 7, 32, 128)
+    assert torch.equal(out, ref)

@@ -1,0 +1,89 @@
+"""C4 (BASELINE.json configs[3]): LLaMA-65B-shape attention with heads sharded
+over 8 B200s — the per-rank slice on one GPU: K1 over this rank's 8 of 64
+heads (B=8, KV 2048, merged tree of 3 SSMs with expansion <1,1,3,1,1,1,1,1> =
+61 nodes), then the head-output layout kernel on a (1-rank) gathered buffer.
+The NCCL all-gather itself needs 8 GPUs; its bytes are reported, not timed.
+
+  python tools/c4_slice.py [--out profiles/c4_slice.json]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2305_09781_b200 import _capi  # noqa: E402
+from paper_2305_09781_b200.dist import head_shard  # noqa: E402
+from paper_2305_09781_b200.tree import TokenTree, TreeBatch  # noqa: E402
+
+B, H_TOTAL, WORLD, D, L = 8, 64, 8, 128, 2048
+EXPANSION = [1, 1, 3, 1, 1, 1, 1, 1]
+
+
+def c4_tree(rng, root):
+    seqs = []
+    for _ in range(3):  # 3 SSMs
+        frontier = [[root]]
+        for e in EXPANSION:
+            frontier = [p + [int(t)] for p in frontier for t in rng.integers(0, 32000, e)]
+        seqs.extend(frontier)
+    return TokenTree.merge_sequences(seqs, 1 << 20)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "c4_slice.json"))
+    ap.add_argument("--iters", type=int, default=20)
+    args = ap.parse_args()
+    rng = np.random.default_rng(65)
+    tb = TreeBatch([c4_tree(rng, int(rng.integers(0, 32000))) for _ in range(B)])
+    T = tb.T
+    h0, h1 = head_shard(H_TOTAL, WORLD, 0)
+    Hl = h1 - h0
+    dev = "cuda"
+    q = torch.empty(B, T, Hl, D, dtype=torch.float16, device=dev).uniform_(-1, 1)
+    kc = torch.empty(B, Hl, L + T, D, dtype=torch.float16, device=dev).uniform_(-1, 1)
+    vc = torch.empty(B, Hl, L + T, D, dtype=torch.float16, device=dev).uniform_(-1, 1)
+    par = torch.tensor(tb.parents, device=dev)
+    n = torch.tensor(tb.n_nodes, device=dev)
+    P = torch.full((B,), L, dtype=torch.int32, device=dev)
+    mask = _capi.build_masks(par, n)
+    out = torch.empty_like(q)
+    ws = _capi.tree_attention_workspace(q, kc, vc, mask, P, n)
+    gathered = torch.empty((WORLD, B, T, Hl, D), dtype=torch.float16, device=dev)
+    full = torch.empty((B, T, H_TOTAL, D), dtype=torch.float16, device=dev)
+    for _ in range(3):
+        _capi.tree_attention(q, kc, vc, mask, P, n, out=out, workspace=ws)
+        _capi.heads_gather_layout(gathered, WORLD, out=full)
+    torch.cuda.synchronize()
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    e[0].record()
+    for _ in range(args.iters):
+        _capi.tree_attention(q, kc, vc, mask, P, n, out=out, workspace=ws)
+    e[1].record()
+    for _ in range(args.iters):
+        _capi.heads_gather_layout(gathered, WORLD, out=full)
+    e[2].record()
+    torch.cuda.synchronize()
+    k1_us = e[0].elapsed_time(e[1]) * 1e3 / args.iters
+    lay_us = e[1].elapsed_time(e[2]) * 1e3 / args.iters
+    W = (T + 63) // 64
+    byts = 2 * (2 * B * L * Hl * D + 4 * B * T * Hl * D) + 8 * B * T * W
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    res = {"config": "C4 per-rank slice: 65B shape, 8 of 64 heads, B=8, T=%d, KV %d, fp16" % (T, L),
+           "tree_nodes": tb.n_nodes.tolist(), "k1_us": k1_us, "k1_bytes": byts,
+           "k1_gbs": byts / (k1_us * 1e-6) / 1e9, "k1_frac": byts / (k1_us * 1e-6) / 1e9 / peak,
+           "layout_us": lay_us, "allgather_bytes_per_rank_out": B * T * Hl * D * 2,
+           "allgather_bytes_per_rank_in": (WORLD - 1) * B * T * Hl * D * 2}
+    print(json.dumps(res, indent=1))
+    json.dump(res, open(args.out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
