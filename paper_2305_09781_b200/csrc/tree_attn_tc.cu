@@ -619,10 +619,10 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 // w+8, ...; lane l owns d columns [4l, 4l+4); all loads of a row group are
 // issued before use. Fixed piece order -> deterministic.
 template <class T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 1)
 combine_kernel(const TcParams p, int G) {
-    constexpr int MAXP = 4;   // pieces held in registers; more are merged online
-    constexpr int RPW = 2;    // rows per warp in flight together
+    constexpr int MAXP = 2;   // pieces held in registers; more are merged online
+    constexpr int RPW = 8;    // rows per warp in flight together (8 warps x 8 = 64 rows/pass)
     const int cta = blockIdx.x;
     asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: wait for the attention kernel
     const long long* tab = p.sched;

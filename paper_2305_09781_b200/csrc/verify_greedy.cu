@@ -14,8 +14,8 @@
 // Work split: kSplit 256-thread blocks per (request, node) stream slices of
 // that node's logits row once (HBM-bound: 4*V bytes per node, float4 loads)
 // and fold their best (value, lowest index) into one 64-bit order-preserving
-// key with atomicMax (order-independent, hence deterministic); the last block
-// of a request (atomic ticket, reset with the keys for reuse) runs the walk:
+// key with atomicMax (order-independent, hence deterministic); a second,
+// PDL-launched kernel (one warp per request) resolves the keys and walks:
 // children of u are the ids v > u with parent[v] == u, scanned 32 at a time
 // with a ballot.
 #include <cfloat>
@@ -130,19 +130,17 @@ __device__ __forceinline__ int key_index(unsigned long long k) {
 }
 
 constexpr int kSplit = 4;   // blocks per logits row
+constexpr int kUnroll = 8;  // float4 loads in flight per thread (a 4000-float slice in one batch)
 
+// Phase 1: stream every live node's logits once; kSplit blocks per row each
+// reduce their slice to one order-preserving key and fold it in with
+// atomicMax (order-independent -> deterministic). No fences or tickets.
 __global__ void __launch_bounds__(kThreads)
-greedy_verify_kernel(const float* __restrict__ logits, int T, int V,
-                     const int32_t* __restrict__ tokens, const int32_t* __restrict__ parent,
-                     const int32_t* __restrict__ n_nodes, const int32_t* __restrict__ budget,
-                     int32_t eos, int32_t* __restrict__ argmax_out, unsigned long long* keys,
-                     int32_t* argmax_ws, int32_t* __restrict__ verified, int32_t* __restrict__ ids,
-                     int32_t* __restrict__ len, unsigned* tickets) {
+greedy_argmax_kernel(const float* __restrict__ logits, int T, int V,
+                     const int32_t* __restrict__ n_nodes, unsigned long long* keys) {
     const int part = blockIdx.x, u = blockIdx.y, b = blockIdx.z;
-    const int n = n_nodes[b];
-    if (u >= n) return;
+    if (u >= n_nodes[b]) return;
     const float* row = logits + ((int64_t)b * T + u) * V;
-    // this block's slice of the row, in float4 units when the row is aligned
     const bool vec = ((reinterpret_cast<uintptr_t>(row) & 15) == 0) && (V % 4 == 0);
     unsigned long long best = 0;
     if (vec) {
@@ -150,16 +148,15 @@ greedy_verify_kernel(const float* __restrict__ logits, int T, int V,
         const int per = (nv + kSplit - 1) / kSplit;
         const int lo = part * per, hi = min(nv, lo + per);
         const float4* r4 = reinterpret_cast<const float4*>(row);
-        constexpr int U = 4;
-        for (int base = lo + threadIdx.x; base < hi; base += kThreads * U) {
-            float4 x[U];
+        for (int base = lo + threadIdx.x; base < hi; base += kThreads * kUnroll) {
+            float4 x[kUnroll];
 #pragma unroll
-            for (int k = 0; k < U; ++k) {
+            for (int k = 0; k < kUnroll; ++k) {
                 const int j = base + k * kThreads;
                 x[k] = j < hi ? __ldcs(r4 + j) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
             }
 #pragma unroll
-            for (int k = 0; k < U; ++k) {
+            for (int k = 0; k < kUnroll; ++k) {
                 const int j = (base + k * kThreads) * 4;
                 if (j < hi * 4) {
                     best = max(best, arg_key(x[k].x, j));
@@ -177,35 +174,40 @@ greedy_verify_kernel(const float* __restrict__ logits, int T, int V,
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
     __shared__ unsigned long long red[kThreads / 32];
-    __shared__ bool is_last;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) red[warp] = best;
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < kThreads / 32; ++w) best = max(best, red[w]);
         atomicMax(keys + (int64_t)b * T + u, best);
-        __threadfence();
-        const unsigned t = atomicAdd(&tickets[b], 1u);
-        is_last = (t == (unsigned)n * kSplit - 1);
     }
-    __syncthreads();
-    if (!is_last || warp != 0) return;
+    // let the dependent walk kernel get scheduled while the stream drains
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
-    // ---- last block of request b: resolve argmax, walk, reset workspace ----
-    __threadfence();
+// Phase 2 (launched with programmatic dependent launch): one warp per request
+// resolves the argmax keys (resetting them for the next call), then walks.
+__global__ void __launch_bounds__(32)
+greedy_walk_kernel(int T, const int32_t* __restrict__ tokens, const int32_t* __restrict__ parent,
+                   const int32_t* __restrict__ n_nodes, const int32_t* __restrict__ budget,
+                   int32_t eos, int32_t* __restrict__ argmax_out, unsigned long long* keys,
+                   int32_t* argmax_ws, int32_t* __restrict__ verified, int32_t* __restrict__ ids,
+                   int32_t* __restrict__ len) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    __shared__ int s_out[kWalkMax], s_next[kWalkMax];
+    const int b = blockIdx.x, lane = threadIdx.x;
+    const int n = n_nodes[b];
     int32_t* am = argmax_ws + (int64_t)b * T;
     for (int v = lane; v < n; v += 32) {
         unsigned long long* kp = keys + (int64_t)b * T + v;
-        const int a = key_index(atomicExch(kp, 0ull));  // read + reset for reuse
+        const int a = key_index(*kp);
+        *kp = 0ull;  // reset for the next call
         am[v] = a;
         if (argmax_out) argmax_out[(int64_t)b * T + v] = a;
     }
     __syncwarp();
-    __threadfence_block();
-    __shared__ int s_out[kWalkMax], s_next[kWalkMax];
-    walk_warp(argmax_ws, tokens, parent, n, T, b, budget, eos, verified, ids, len, lane, true,
+    walk_warp(argmax_ws, tokens, parent, n, T, b, budget, eos, verified, ids, len, lane, false,
               s_out, s_next);
-    if (lane == 0) tickets[b] = 0;
 }
 
 // One thread per (request, node): walk the parent chain (depth <= T) and set
@@ -257,9 +259,20 @@ st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32
     int32_t* scratch = reinterpret_cast<int32_t*>(
         (reinterpret_cast<uintptr_t>(tickets + B) + 15) & ~uintptr_t(15));
     const dim3 grid(st::kSplit, T, B);
-    st::greedy_verify_kernel<<<grid, st::kThreads, 0, st::as_stream(stream)>>>(
-        logits, T, V, tokens, parent, n_nodes, budget, eos, argmax, keys, scratch, verified, ids,
-        len, tickets);
+    auto strm = st::as_stream(stream);
+    st::greedy_argmax_kernel<<<grid, st::kThreads, 0, strm>>>(logits, T, V, n_nodes, keys);
+    ST_LAUNCH_CHECK();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(B);
+    cfg.blockDim = dim3(32);
+    cfg.stream = strm;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ST_CUDA_TRY(cudaLaunchKernelEx(&cfg, st::greedy_walk_kernel, T, tokens, parent, n_nodes, budget,
+                                   eos, argmax, keys, scratch, verified, ids, len));
     ST_LAUNCH_CHECK();
     return ST_OK;
 }
