@@ -169,6 +169,30 @@ st_status st_verify_mss(const float* logits, const float* q, int B, int T, int V
 st_status st_tree_merge(const int32_t* flat, const int32_t* lens, int nseq, int max_nodes,
                         int32_t* tok, int32_t* parent, int32_t* depth, int cap, int* n_out);
 
+/* ------------------------------------------------- device decoder model ---
+ * The reference's pre-LN decoder (proj/include/spectree/transformer.hpp:18-57)
+ * resident on the device in f16/bf16 for the full-stack path (C3): weights are
+ * generated on the GPU from UniformStream(seed) in the serialized order of
+ * init_random_weights (reference transformer.cpp:71-114). st_model_tree_forward
+ * runs every tree row of a batch through all layers (GEMMs over B*T rows; K2
+ * append + K1 tree attention per layer) and writes f32 logits [B][T][V].
+ * KV caches: [num_layers][B][H][Lmax][D]; row u of request b is written at
+ * P[b]+u and sees rows [0,P[b]) plus its mask. */
+typedef struct st_model st_model;
+typedef struct {
+    int num_layers, num_heads, d_model, vocab_size, max_positions, ffn_mult;
+} st_model_config;
+st_status st_model_create(const st_model_config* cfg, uint64_t seed, st_dtype dtype,
+                          st_model** out);
+void st_model_destroy(st_model* m);
+size_t st_model_param_count(const st_model* m);
+size_t st_model_workspace_size(const st_model* m, int B, int T);
+st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens,
+                                const int32_t* positions, const uint64_t* mask, int W,
+                                const int32_t* prefix_len, const int32_t* n_nodes, void* k_cache,
+                                void* v_cache, int64_t Lmax, float* logits, void* workspace,
+                                size_t workspace_bytes, void* stream);
+
 /* --------------------------------------------------------- tree packing ---
  * Device-side ancestor bitmask build: mask[b][u] = mask[b][parent[u]] | bit(u)
  * (reference TokenTree::ancestors, token_tree.cpp:130-139, as a bitset). */

@@ -61,6 +61,11 @@ SIGNATURES = {
     "st_verify_outputs": (_I, [_V, _I, _I, _V, _V, _V, _V, C.c_int32, _V, _V, _V, _V]),
     "st_verify_mss": (_I, [_V, _V, _I, _I, _I, _V, _V, _V, _F, _V, _I, _V, _V, _V, _V]),
     "st_build_masks": (_I, [_V, _V, _I, _I, _I, _V, _V]),
+    "st_model_create": (_I, [_V, C.c_uint64, _I, _V]),
+    "st_model_destroy": (None, [_V]),
+    "st_model_param_count": (_Z, [_V]),
+    "st_model_workspace_size": (_Z, [_V, _I, _I]),
+    "st_model_tree_forward": (_I, [_V, _I, _I, _V, _V, _V, _I, _V, _V, _V, _V, _I64, _V, _V, _Z, _V]),
     "st_tree_merge": (_I, [_V, _V, _I, _I, _V, _V, _V, _I, C.POINTER(_I)]),
 }
 
@@ -224,3 +229,54 @@ def build_masks(parent, n_nodes, W=None, stream=None, out=None):
                                                    device=parent.device)
     check(lib().st_build_masks(_ptr(parent), _ptr(n_nodes), B, T, W, _ptr(mask), _stream(stream)))
     return mask
+
+
+# ------------------------------------------------------ device model ----
+class ModelConfig(C.Structure):
+    _fields_ = [("num_layers", C.c_int), ("num_heads", C.c_int), ("d_model", C.c_int),
+                ("vocab_size", C.c_int), ("max_positions", C.c_int), ("ffn_mult", C.c_int)]
+
+
+class DeviceModel:
+    """The reference decoder resident on the GPU (f16/bf16), weights generated
+    on device from UniformStream(seed) — st_model_* of the C-ABI."""
+
+    def __init__(self, num_layers, num_heads, d_model, vocab_size, max_positions, ffn_mult=4,
+                 seed=42, dtype=torch.float16):
+        self.cfg = ModelConfig(num_layers, num_heads, d_model, vocab_size, max_positions, ffn_mult)
+        self.dtype = dtype
+        h = C.c_void_p()
+        check(lib().st_model_create(C.byref(self.cfg), seed, DTYPES[dtype], C.byref(h)))
+        self.handle = h
+        self._ws = None
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib().st_model_destroy(self.handle)
+            self.handle = None
+
+    @property
+    def param_count(self):
+        return int(lib().st_model_param_count(self.handle))
+
+    def new_cache(self, B, Lmax, device="cuda"):
+        c = self.cfg
+        shape = (c.num_layers, B, c.num_heads, Lmax, c.d_model // c.num_heads)
+        return (torch.zeros(shape, dtype=self.dtype, device=device),
+                torch.zeros(shape, dtype=self.dtype, device=device))
+
+    def tree_forward(self, tokens, positions, mask, prefix_len, n_nodes, k_cache, v_cache,
+                     logits=None, stream=None):
+        B, T = tokens.shape
+        if logits is None:
+            logits = torch.empty((B, T, self.cfg.vocab_size), dtype=torch.float32,
+                                 device=tokens.device)
+        need = int(lib().st_model_workspace_size(self.handle, B, T))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.zeros(need, dtype=torch.uint8, device=tokens.device)
+        check(lib().st_model_tree_forward(self.handle, B, T, _ptr(tokens), _ptr(positions),
+                                          _ptr(mask), mask.shape[-1], _ptr(prefix_len),
+                                          _ptr(n_nodes), _ptr(k_cache), _ptr(v_cache),
+                                          k_cache.shape[-2], _ptr(logits), _ptr(self._ws),
+                                          self._ws.numel(), _stream(stream)))
+        return logits

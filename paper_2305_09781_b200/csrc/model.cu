@@ -1,0 +1,322 @@
+// Device-resident half-precision decoder (the reference recipe at LLaMA
+// shapes: "batched around-path GEMMs" for the C3 full
+// stack). The reference runs one f64 matvec per tree node per matrix
+// (proj/src/transformer.cpp:262-319); here every projection is ONE GEMM over
+// all B*T tree rows of the batch (cuBLAS — plain library GEMMs, fp32
+// accumulate), and the verification hot path in between is ours: K2 append of
+// the rows' K/V into the per-layer cache, K1 masked tree attention.
+//
+// Weights follow init_random_weights exactly (proj/src/transformer.cpp:71-114):
+// every tensor is drawn from ONE UniformStream(seed) in the serialized order
+// (tok, pos, per layer [ln1 g,b, wq, wk, wv, wo, ln2 g,b, w1, w2], lnf g,b,
+// W_out), U(-0.08, 0.08) — generated on the device (value i is a pure function
+// of (seed, i)) and rounded to the model dtype.
+#include <cublas_v2.h>
+
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+
+struct st_model {
+    st_model_config cfg;
+    st_dtype dtype;
+    void* buf = nullptr;
+    size_t elems = 0;
+    cublasHandle_t blas = nullptr;
+    // element offsets into buf
+    size_t tok, pos, lnf_g, lnf_b, wout;
+    struct Layer {
+        size_t ln1_g, ln1_b, wq, wk, wv, wo, ln2_g, ln2_b, w1, w2;
+    };
+    std::vector<Layer> layers;
+};
+
+namespace st {
+namespace {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// UniformStream(seed) value number `index` (0-based): reference rng.hpp:17-28.
+__device__ __forceinline__ double uniform_at(uint64_t seed, uint64_t index, double lo, double hi) {
+    const uint64_t z = mix64(seed + (index + 1) * 0x9e3779b97f4a7c15ULL);
+    return lo + (hi - lo) * ((double)(z >> 11) * 0x1.0p-53);
+}
+
+template <class T>
+__global__ void gen_weights_kernel(T* dst, int64_t n, uint64_t seed, uint64_t stream_offset) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = from_acc<T>((float)uniform_at(seed, stream_offset + i, -0.08, 0.08));
+}
+
+template <class T>
+__global__ void embed_kernel(const T* __restrict__ tok_emb, const T* __restrict__ pos_emb,
+                             const int32_t* __restrict__ tokens, const int32_t* __restrict__ pos,
+                             int d, T* __restrict__ x) {
+    const int i = blockIdx.x;
+    const T* te = tok_emb + (int64_t)tokens[i] * d;
+    const T* pe = pos_emb + (int64_t)pos[i] * d;
+    for (int c = threadIdx.x; c < d; c += blockDim.x)
+        x[(int64_t)i * d + c] = from_acc<T>(to_acc<float>(te[c]) + to_acc<float>(pe[c]));
+}
+
+__device__ float block_sum(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = v;
+    __syncthreads();
+    float s = 0.f;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[k];
+    return s;
+}
+
+// LayerNorm (eps 1e-5, two-pass mean/variance; reference transformer.cpp:48-65), fp32 math.
+template <class T>
+__global__ void layernorm_kernel(const T* __restrict__ x, const T* __restrict__ g,
+                                 const T* __restrict__ b, int d, T* __restrict__ out) {
+    __shared__ float red[32];
+    const T* xr = x + (int64_t)blockIdx.x * d;
+    T* orow = out + (int64_t)blockIdx.x * d;
+    float s = 0.f;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) s += to_acc<float>(xr[c]);
+    const float mean = block_sum(s, red) / d;
+    float v = 0.f;
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+        const float z = to_acc<float>(xr[c]) - mean;
+        v += z * z;
+    }
+    const float inv = rsqrtf(block_sum(v, red) / d + 1e-5f);
+    for (int c = threadIdx.x; c < d; c += blockDim.x)
+        orow[c] = from_acc<T>(to_acc<float>(g[c]) * (to_acc<float>(xr[c]) - mean) * inv +
+                              to_acc<float>(b[c]));
+}
+
+template <class T>
+__global__ void gelu_kernel(T* __restrict__ x, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float v = to_acc<float>(x[i]);
+        x[i] = from_acc<T>(0.5f * v * (1.f + erff(v * 0.70710678118654752f)));
+    }
+}
+
+cudaDataType_t cuda_type(st_dtype t) { return t == ST_F16 ? CUDA_R_16F : CUDA_R_16BF; }
+
+// Row-major C[M][N] (+)= A[M][K] * W[K][N]  (column-major view: C^T = W^T A^T)
+st_status gemm(st_model* m, const void* A, size_t w_off, void* C, cudaDataType_t ctype, int M, int N,
+               int K, bool accumulate, cudaStream_t s) {
+    const float alpha = 1.f, beta = accumulate ? 1.f : 0.f;
+    const size_t es = dtype_size(m->dtype);
+    const void* W = static_cast<const char*>(m->buf) + w_off * es;
+    cublasSetStream(m->blas, s);
+    const cublasStatus_t st =
+        cublasGemmEx(m->blas, CUBLAS_OP_N, CUBLAS_OP_N, N, M, K, &alpha, W, cuda_type(m->dtype), N,
+                     A, cuda_type(m->dtype), K, &beta, C, ctype, N, CUBLAS_COMPUTE_32F,
+                     CUBLAS_GEMM_DEFAULT);
+    if (st != CUBLAS_STATUS_SUCCESS) {
+        set_error("cublasGemmEx failed: status " + std::to_string((int)st));
+        return ST_ERR_CUDA;
+    }
+    return ST_OK;
+}
+
+template <class T>
+const T* wptr(const st_model* m, size_t off) {
+    return static_cast<const T*>(m->buf) + off;
+}
+
+}  // namespace
+}  // namespace st
+
+extern "C" {
+
+st_status st_model_create(const st_model_config* cfg, uint64_t seed, st_dtype dtype,
+                          st_model** out) {
+    if (st_status e = st::require_device()) return e;
+    ST_CHECK_ARG(cfg && out, ST_ERR_INVALID_ARGUMENT, "null pointer");
+    ST_CHECK_ARG(dtype == ST_F16 || dtype == ST_BF16, ST_ERR_UNSUPPORTED,
+                 "device model supports f16/bf16 (the f64 parity model is the C++ API)");
+    const auto& c = *cfg;
+    ST_CHECK_ARG(c.num_layers >= 1 && c.num_heads >= 1 && c.d_model >= 1 && c.vocab_size >= 2 &&
+                     c.max_positions >= 1 && c.ffn_mult >= 1 && c.d_model % c.num_heads == 0,
+                 ST_ERR_SHAPE_MISMATCH, "bad model config");
+    auto* m = new st_model;
+    m->cfg = c;
+    m->dtype = dtype;
+    const size_t d = c.d_model, F = (size_t)c.ffn_mult * d, V = c.vocab_size;
+    size_t at = 0;
+    auto take = [&](size_t n) {
+        const size_t o = at;
+        at += n;
+        return o;
+    };
+    m->tok = take(V * d);
+    m->pos = take((size_t)c.max_positions * d);
+    for (int l = 0; l < c.num_layers; ++l) {
+        st_model::Layer L;
+        L.ln1_g = take(d);
+        L.ln1_b = take(d);
+        L.wq = take(d * d);
+        L.wk = take(d * d);
+        L.wv = take(d * d);
+        L.wo = take(d * d);
+        L.ln2_g = take(d);
+        L.ln2_b = take(d);
+        L.w1 = take(d * F);
+        L.w2 = take(F * d);
+        m->layers.push_back(L);
+    }
+    m->lnf_g = take(d);
+    m->lnf_b = take(d);
+    m->wout = take(d * V);
+    m->elems = at;
+    if (cudaMalloc(&m->buf, at * st::dtype_size(dtype)) != cudaSuccess) {
+        cudaGetLastError();
+        delete m;
+        st::set_error("st_model_create: out of device memory");
+        return ST_ERR_CUDA;
+    }
+    // the whole parameter vector IS the stream: element i = UniformStream(seed) value i
+    const unsigned blocks = 148 * 8;
+    if (dtype == ST_F16)
+        st::gen_weights_kernel<__half><<<blocks, 256>>>((__half*)m->buf, (int64_t)at, seed, 0);
+    else
+        st::gen_weights_kernel<__nv_bfloat16><<<blocks, 256>>>((__nv_bfloat16*)m->buf, (int64_t)at,
+                                                               seed, 0);
+    if (cudaDeviceSynchronize() != cudaSuccess || cublasCreate(&m->blas) != CUBLAS_STATUS_SUCCESS) {
+        cudaGetLastError();
+        cudaFree(m->buf);
+        delete m;
+        st::set_error("st_model_create: init failed");
+        return ST_ERR_CUDA;
+    }
+    *out = m;
+    return ST_OK;
+}
+
+void st_model_destroy(st_model* m) {
+    if (!m) return;
+    if (m->blas) cublasDestroy(m->blas);
+    if (m->buf) cudaFree(m->buf);
+    delete m;
+}
+
+size_t st_model_param_count(const st_model* m) { return m ? m->elems : 0; }
+
+size_t st_model_workspace_size(const st_model* m, int B, int T) {
+    if (!m) return 0;
+    const size_t rows = (size_t)B * T, d = m->cfg.d_model, F = (size_t)m->cfg.ffn_mult * d;
+    st_attn_args a{};
+    a.dtype = m->dtype;
+    a.B = B;
+    a.T = T;
+    a.H = m->cfg.num_heads;
+    a.Hkv = m->cfg.num_heads;
+    a.D = (int)(d / m->cfg.num_heads);
+    a.W = (T + 63) / 64;
+    a.Lmax = T;
+    const size_t es = st::dtype_size(m->dtype);
+    return rows * (6 * d + F) * es + st_tree_attention_workspace_size(&a) + 8 * 256;
+}
+
+st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens,
+                                const int32_t* positions, const uint64_t* mask, int W,
+                                const int32_t* prefix_len, const int32_t* n_nodes, void* k_cache,
+                                void* v_cache, int64_t Lmax, float* logits, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+    if (st_status e = st::require_device()) return e;
+    ST_CHECK_ARG(m && tokens && positions && mask && prefix_len && n_nodes && k_cache && v_cache &&
+                     logits && workspace,
+                 ST_ERR_INVALID_ARGUMENT, "null pointer");
+    ST_CHECK_ARG(B >= 1 && T >= 1 && W * 64 >= T && Lmax >= T, ST_ERR_SHAPE_MISMATCH, "bad shape");
+    ST_CHECK_ARG(workspace_bytes >= st_model_workspace_size(m, B, T), ST_ERR_INVALID_ARGUMENT,
+                 "workspace too small");
+    const auto& c = m->cfg;
+    const int rows = B * T, d = c.d_model, H = c.num_heads, Dh = d / H, F = c.ffn_mult * d;
+    const size_t es = st::dtype_size(m->dtype);
+    cudaStream_t s = st::as_stream(stream);
+    char* ws = static_cast<char*>(workspace);
+    auto take = [&](size_t bytes) {
+        char* p = ws;
+        ws += (bytes + 255) & ~size_t(255);
+        return (void*)p;
+    };
+    void* x = take((size_t)rows * d * es);
+    void* h = take((size_t)rows * d * es);
+    void* q = take((size_t)rows * d * es);
+    void* kn = take((size_t)rows * d * es);
+    void* vn = take((size_t)rows * d * es);
+    void* o = take((size_t)rows * d * es);
+    void* f = take((size_t)rows * F * es);
+    st_attn_args a{};
+    a.dtype = m->dtype;
+    a.B = B;
+    a.T = T;
+    a.H = H;
+    a.Hkv = H;
+    a.D = Dh;
+    a.W = W;
+    a.Lmax = Lmax;
+    a.mask = mask;
+    a.prefix_len = prefix_len;
+    a.n_nodes = n_nodes;
+    a.scale = 1.0 / std::sqrt((double)Dh);
+    a.workspace = ws;
+    a.workspace_bytes = st_tree_attention_workspace_size(&a);
+    const size_t layer_elems = (size_t)B * H * Lmax * Dh;
+    const cudaDataType_t ht = st::cuda_type(m->dtype);
+
+#define ST_M_DISPATCH(...)                                                   \
+    if (m->dtype == ST_F16) {                                                \
+        using T = __half;                                                    \
+        __VA_ARGS__;                                                         \
+    } else {                                                                 \
+        using T = __nv_bfloat16;                                             \
+        __VA_ARGS__;                                                         \
+    }
+    ST_M_DISPATCH(st::embed_kernel<T><<<rows, 256, 0, s>>>(st::wptr<T>(m, m->tok),
+                                                           st::wptr<T>(m, m->pos), tokens,
+                                                           positions, d, (T*)x));
+    ST_LAUNCH_CHECK();
+    for (int l = 0; l < c.num_layers; ++l) {
+        const auto& L = m->layers[l];
+        void* kc = static_cast<char*>(k_cache) + (size_t)l * layer_elems * es;
+        void* vc = static_cast<char*>(v_cache) + (size_t)l * layer_elems * es;
+        ST_M_DISPATCH(st::layernorm_kernel<T><<<rows, 256, 0, s>>>(
+            (const T*)x, st::wptr<T>(m, L.ln1_g), st::wptr<T>(m, L.ln1_b), d, (T*)h));
+        ST_LAUNCH_CHECK();
+        if (st_status e = st::gemm(m, h, L.wq, q, ht, rows, d, d, false, s)) return e;
+        if (st_status e = st::gemm(m, h, L.wk, kn, ht, rows, d, d, false, s)) return e;
+        if (st_status e = st::gemm(m, h, L.wv, vn, ht, rows, d, d, false, s)) return e;
+        if (st_status e = st_kv_append(m->dtype, B, T, H, Dh, Lmax, kn, vn, prefix_len, n_nodes, kc,
+                                       vc, stream))
+            return e;
+        a.q = q;
+        a.k_cache = kc;
+        a.v_cache = vc;
+        a.o = o;
+        if (st_status e = st_tree_attention(&a, stream)) return e;
+        if (st_status e = st::gemm(m, o, L.wo, x, ht, rows, d, d, true, s)) return e;
+        ST_M_DISPATCH(st::layernorm_kernel<T><<<rows, 256, 0, s>>>(
+            (const T*)x, st::wptr<T>(m, L.ln2_g), st::wptr<T>(m, L.ln2_b), d, (T*)h));
+        ST_LAUNCH_CHECK();
+        if (st_status e = st::gemm(m, h, L.w1, f, ht, rows, F, d, false, s)) return e;
+        ST_M_DISPATCH(st::gelu_kernel<T><<<148 * 8, 256, 0, s>>>((T*)f, (int64_t)rows * F));
+        ST_LAUNCH_CHECK();
+        if (st_status e = st::gemm(m, f, L.w2, x, ht, rows, d, F, true, s)) return e;
+    }
+    ST_M_DISPATCH(st::layernorm_kernel<T><<<rows, 256, 0, s>>>(
+        (const T*)x, st::wptr<T>(m, m->lnf_g), st::wptr<T>(m, m->lnf_b), d, (T*)h));
+    ST_LAUNCH_CHECK();
+#undef ST_M_DISPATCH
+    return st::gemm(m, h, m->wout, logits, CUDA_R_32F, rows, c.vocab_size, d, false, s);
+}
+
+}  // extern "C"
