@@ -16,6 +16,10 @@ st_status validate(const st_attn_args* a) {
     ST_CHECK_ARG(a->H % a->Hkv == 0, ST_ERR_SHAPE_MISMATCH, "H must be a multiple of Hkv");
     ST_CHECK_ARG(a->W * 64 >= a->T, ST_ERR_SHAPE_MISMATCH, "mask words W < ceil(T/64)");
     ST_CHECK_ARG(a->Lmax >= a->T, ST_ERR_SHAPE_MISMATCH, "cache rows Lmax < T");
+    return ST_OK;
+}
+
+st_status validate_ptrs(const st_attn_args* a) {
     ST_CHECK_ARG(a->B == 0 || (a->q && a->k_cache && a->v_cache && a->mask && a->prefix_len &&
                                a->n_nodes && a->o),
                  ST_ERR_INVALID_ARGUMENT, "null tensor pointer");
@@ -45,6 +49,7 @@ size_t st_tree_attention_workspace_size(const st_attn_args* a) {
 st_status st_tree_attention(const st_attn_args* a, void* stream) {
     if (st_status e = st::require_device()) return e;
     if (st_status e = validate(a)) return e;
+    if (st_status e = validate_ptrs(a)) return e;
     if (a->B == 0) return ST_OK;
     const int path = choose_path(a);
     if (path == 2) {

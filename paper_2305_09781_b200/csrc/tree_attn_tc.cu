@@ -144,6 +144,45 @@ __device__ Seg find_seg(const TcParams& p, long long t, long long t_end) {
     return s;
 }
 
+// CTA work ranges over the pair-major tile sequence. Stream-K (equal tile
+// counts; pairs may be split, leaving partial pieces for combine_kernel) unless
+// every pair has the same tile count and whole-pair ranges cost at most
+// kAlignedSlack tiles more than perfect balance — then CTA c takes pairs
+// [c*Np/G, (c+1)*Np/G) and no pair is split (no partials, no merge).
+constexpr long long kAlignedSlack = 6;
+
+struct Sched {
+    long long total;
+    long long np;   // pairs with tiles
+    int nt;         // tiles per pair when uniform
+    bool aligned;
+};
+
+__device__ Sched make_sched(const TcParams& p, long long G) {
+    Sched s{0, 0, 0, false};
+    int lo = 1 << 30, hi = 0;
+    for (int b = 0; b < p.B; ++b) {
+        const int nt = ntiles_of(p, b);
+        if (nt > 0) {
+            lo = min(lo, nt);
+            hi = max(hi, nt);
+            s.np += p.H;
+        }
+        s.total += (long long)p.H * nt;
+    }
+    if (s.np > 0 && lo == hi) {
+        s.nt = lo;
+        const long long aligned_span = (s.np + G - 1) / G * s.nt;
+        const long long streamk_span = (s.total + G - 1) / G;
+        s.aligned = aligned_span <= streamk_span + kAlignedSlack;
+    }
+    return s;
+}
+
+__device__ __forceinline__ long long range_start(long long c, const Sched& s, long long G) {
+    return s.aligned ? (c * s.np / G) * s.nt : c * s.total / G;
+}
+
 __device__ __forceinline__ long long range_start(long long c, long long total, long long G) {
     return c * total / G;
 }
@@ -235,9 +274,10 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     const uint32_t tmem = *tmem_slot;
 
     const long long G = gridDim.x;
-    const long long total = total_tiles(p);
-    const long long t_begin = range_start(blockIdx.x, total, G);
-    const long long t_end = range_start(blockIdx.x + 1, total, G);
+    const Sched sched = make_sched(p, G);
+    const long long total = sched.total;
+    const long long t_begin = range_start(blockIdx.x, sched, G);
+    const long long t_end = range_start(blockIdx.x + 1, sched, G);
     if (threadIdx.x == 0) {  // schedule table for combine_kernel
         long long* e = p.sched + 4 * blockIdx.x;
         e[0] = t_begin;
