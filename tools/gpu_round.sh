@@ -16,3 +16,5 @@ timeout 400 ncu --set full --clock-control none --import-source on -k regex:tree
     > /dev/null 2> $OUT/$TAG.ncu2.err
 ls -la $OUT
 timeout 600 python tools/sweep_c5.py --out gpurun_out/$TAG.c5_sweep.json > gpurun_out/$TAG.c5_sweep.txt 2>&1
+timeout 900 python bench.py --config c3 --steps 5 --warmup 2 > $OUT/$TAG.c3.json 2> $OUT/$TAG.c3.err
+timeout 120 python tools/c4_slice.py --out $OUT/$TAG.c4.json > $OUT/$TAG.c4.txt 2>&1
