@@ -8,23 +8,29 @@
 // attention core :270-299) collapsed into one masked pass.
 //
 // Design:
-//   * Persistent, stream-K scheduled: grid = #SMs, one CTA per SM. The
-//     concatenation over (b, h) of each pair's 128-row KV tiles is cut into
-//     #SMs equal contiguous ranges, so every SM streams the same number of
-//     bytes whatever the per-request lengths are. A pair split across CTAs
-//     leaves partial (O, m, l) rows in the workspace and the last CTA to finish
-//     that pair merges them in fixed CTA order (deterministic; no atomics in
-//     any reduction, the ticket only elects the merger).
-//   * Warp roles (192 threads): warps 0-3 softmax/epilogue (thread r <-> query
-//     row r <-> TMEM lane r), warp 4 TMA producer, warp 5 MMA issuer.
-//   * TMA (SWIZZLE_128B) streams K and V tiles [128 rows x 128 d] through two
-//     2-stage rings; Q [128 x 128] (rows >= T zero-filled by TMA) once per pair.
-//   * S = Q K^T on tcgen05 (M=128, N=128, K=16 x 8) into a double-buffered TMEM
-//     S; softmax reads it with tcgen05.ld, applies the tree mask only on tiles
-//     that reach the tree region, writes P (bf16/f16) to smem in the UMMA
-//     K-major SW128 layout; O += P V on tcgen05 (V read MN-major) into TMEM.
-//   * Online softmax with lazy rescaling: the running max is only moved (and O
-//     in TMEM rescaled) when it grows by more than 2^8, so P stays <= 256.
+//   * Persistent, one CTA per SM, over the pair-major sequence of every (b, h)
+//     pair's 128-row KV tiles. Ranges are either whole pairs (when all pairs
+//     have the same tile count and that balances within kAlignedSlack tiles)
+//     or stream-K (equal tile counts per CTA; a pair cut by a range boundary
+//     leaves partial (O, m, l) pieces that combine_kernel — launched with PDL —
+//     merges in fixed order: deterministic, no atomics in any reduction).
+//   * Warp roles (224 threads): warps 0-3 softmax/epilogue, warp 4 TMA producer
+//     for Q and K, warp 5 TMA producer for V, warp 6 MMA issuer (one lane).
+//   * TMA (SWIZZLE_128B) streams K and V tiles [128 rows x 128 d]: K ring 2,
+//     V ring 3 (M=64) / 2 (M=128); Q (rows >= T zero-filled by TMA) double-
+//     buffered for M=64 so the next pair's Q is in smem before its first S.
+//   * S = Q K^T and O += P V on tcgen05 (kind::f16, fp32 accumulate in TMEM).
+//     M=128 (T <= 128): one N=128 MMA per K=16 step; each softmax thread owns a
+//     query row. M=64 (T <= 64): every product is split into two N=64 MMAs
+//     whose accumulators land in TMEM lanes 0-15 and 16-31 of each subpartition,
+//     so all 32 lanes of a softmax warp hold data (half a row each: half the
+//     MUFU work per thread).
+//   * Softmax: tcgen05.ld of S (double-buffered in TMEM), the tree mask applied
+//     only on tiles that reach the tree rows (one 32-bit visibility word per 32
+//     columns), ex2 with lazy rescaling (the running max moves only when it
+//     grows by > 2^8; O is then rescaled in TMEM), P staged in registers and
+//     stored (f16/bf16) to a double-buffered smem tile in the UMMA K-major
+//     SW128 layout; V read MN-major by the P.V MMA.
 //   * Masked rows are exact zeros in P, so they contribute +0 (reference
 //     transformer.hpp:13-16) and outputs do not depend on non-ancestor rows.
 #include <cuda.h>
@@ -114,12 +120,6 @@ __device__ __forceinline__ int ntiles_of(const TcParams& p, int b) {
     return n > 0 ? (__ldg(p.prefix_len + b) + n + BN - 1) / BN : 0;
 }
 
-__device__ long long total_tiles(const TcParams& p) {
-    long long t = 0;
-    for (int b = 0; b < p.B; ++b) t += (long long)p.H * ntiles_of(p, b);
-    return t;
-}
-
 // Segment starting at global tile t (t < t_end) of this CTA's range.
 __device__ Seg find_seg(const TcParams& p, long long t, long long t_end) {
     long long base = 0;
@@ -181,13 +181,6 @@ __device__ Sched make_sched(const TcParams& p, long long G) {
 
 __device__ __forceinline__ long long range_start(long long c, const Sched& s, long long G) {
     return s.aligned ? (c * s.np / G) * s.nt : c * s.total / G;
-}
-
-__device__ __forceinline__ long long range_start(long long c, long long total, long long G) {
-    return c * total / G;
-}
-__device__ __forceinline__ long long cta_of(long long t, long long total, long long G) {
-    return ((t + 1) * G + total - 1) / total - 1;
 }
 
 template <class T> struct pk2;
