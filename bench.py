@@ -43,7 +43,7 @@ sys.path.insert(0, ROOT)
 # C2
 B, T, H, D, L, V = 8, 64, 32, 128, 2048, 32000
 WIDTH, DEPTH = 8, 8            # 8 root-to-leaf paths, trimmed to exactly 64 nodes
-LAUNCHES_PER_STEP = 5          # append, masks, K1, K3, compact
+LAUNCHES_PER_STEP = 7          # append, masks, K1, K1 combine, K3 argmax, K3 walk, compact
 METRIC = "tree-verify tokens/s"
 UNIT = "tokens/s"
 
@@ -66,6 +66,33 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+_ORIG_AFFINITY: set = set()
+
+
+def bind_to_gpu_numa(local):
+    """Pin this process to the host CPUs local to the GPU (sysfs local_cpulist),
+    so pinned staging buffers are allocated on the GPU's NUMA node — what a
+    serving deployment does. Returns the CPU count bound to (None if unknown)."""
+    import torch
+    try:
+        pr = torch.cuda.get_device_properties(local)
+        bus = "%04x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+        with open(f"/sys/bus/pci/devices/{bus}/local_cpulist") as f:
+            spec = f.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        cpus &= os.sched_getaffinity(0)
+        if cpus:
+            _ORIG_AFFINITY.update(os.sched_getaffinity(0))
+            os.sched_setaffinity(0, cpus)
+            return len(cpus)
+    except (OSError, ValueError, AttributeError):
+        pass
+    return None
 
 
 def c2_trees(make_tree, seed, vocab, n_req=B, nodes=T):
@@ -211,6 +238,7 @@ def main():
     assert world == args.gpus or "RANK" not in os.environ, "--gpus must match WORLD_SIZE"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    numa_cpus = bind_to_gpu_numa(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
@@ -284,13 +312,18 @@ def main():
     torch.cuda.current_stream().wait_stream(side)
     barrier()
     graphs = {}
-    for name, fn in (("pre", pre), ("k1", k1), ("post", post)):
+    for name, fn in (("pre", pre), ("k1", k1), ("post", post), ("full", lambda *a: eager(a))):
         g_ = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_):
             fn(*resident)
         graphs[name] = g_
 
     def step(time_k1=False):
+        if not time_k1:   # the whole step as one graph
+            graphs["full"].replay()
+            if world > 1:
+                gather_accepted(vout[0], vout[2], world, out=gathered)
+            return vout[0], vout[2]
         graphs["pre"].replay()
         if time_k1:
             e0 = torch.cuda.Event(enable_timing=True)
@@ -322,9 +355,13 @@ def main():
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
     for _ in range(args.steps):
-        step(time_k1=True)
+        step()
     t1.record()
     barrier()
+    # K1's own duration: the same K steps again, split into pre / K1 / post
+    # graphs with events around K1 (+ its combine) on the launching stream
+    for _ in range(args.steps):
+        step(time_k1=True)
     for _ in range(200):        # keep sampling a little past the timed region
         step()
     barrier()
@@ -442,6 +479,8 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
+        if _ORIG_AFFINITY:   # the CPU baseline gets every host core again
+            os.sched_setaffinity(0, _ORIG_AFFINITY)
         nt = cpu_threads()
         try:
             res = reference_sample(min(B, nt), 1, 0, full_tree=True)
@@ -464,6 +503,9 @@ def main():
                    "B_per_gpu": B, "T": T, "L": L, "H": H, "D": D, "V": V,
                    "parallelism": f"dp{world} (requests partitioned)",
                    "l2": "inputs larger than L2: 268 MB KV + 65.5 MB logits per step",
+                   "timing": "value: K replays of one CUDA graph holding the whole step; "
+                             "roofline: CUDA events around K1 (+ combine) in K more steps "
+                             "replayed as pre / K1 / post graphs",
                    "k1_path": "tcgen05" if path == 2 else "cuda-core"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
@@ -472,7 +514,9 @@ def main():
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
+                "h2d_gbs_implied": h2d / (e2e_ms / args.steps / 1e3) / 1e9,
+                "host_numa_cpus": numa_cpus},
         "gpu_launches": LAUNCHES_PER_STEP * args.steps,
         "clocks": clk,
         "verified_tokens_per_step": accepted,

@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "spectree_capi.h"
 
@@ -49,6 +50,34 @@ inline size_t dtype_size(st_dtype t) {
         case ST_F64: return 8;
     }
     return 0;
+}
+
+// ------------------------------------------- programmatic dependent launch ---
+// Every path kernel is launched with programmatic stream serialization: its
+// grid may be scheduled while the previous kernel on the stream drains, runs
+// its prologue (barrier init, TMEM alloc, tensor-map prefetch — nothing that
+// reads another kernel's output) and then blocks in pdl_wait() until that
+// kernel has completed and its writes are visible. Because every kernel waits
+// before it exits, completion stays transitive along the stream.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t stream, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // ----------------------------------------------------------- conversions ---

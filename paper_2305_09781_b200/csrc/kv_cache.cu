@@ -24,23 +24,48 @@ namespace st {
 namespace {
 
 // One block per (b, u) tree row: copies Hkv rows of D elements for K and V.
+// The node's Hkv*D source elements are contiguous; each thread keeps kUnroll
+// K and V vectors in flight before storing them (the copy is latency-bound
+// otherwise: one 16 B load per thread per round trip).
+constexpr int kAppendThreads = 128;
+constexpr int kAppendUnroll = 4;
+
 template <class V>
-__global__ void kv_append_kernel(const char* __restrict__ k_new, const char* __restrict__ v_new,
-                                 const int32_t* __restrict__ prefix_len,
-                                 const int32_t* __restrict__ n_nodes, char* __restrict__ k_cache,
-                                 char* __restrict__ v_cache, int T, int Hkv, int64_t row_bytes,
-                                 int64_t Lmax) {
+__global__ void __launch_bounds__(kAppendThreads)
+kv_append_kernel(const char* __restrict__ k_new, const char* __restrict__ v_new,
+                 const int32_t* __restrict__ prefix_len, const int32_t* __restrict__ n_nodes,
+                 char* __restrict__ k_cache, char* __restrict__ v_cache, int T, int Hkv,
+                 int row_vecs, int64_t Lmax) {
+    pdl_wait();
+    pdl_trigger();
     const int b = blockIdx.y, u = blockIdx.x;
     if (u >= n_nodes[b]) return;
     const int64_t P = prefix_len[b];
-    const int64_t nvec = row_bytes / (int64_t)sizeof(V);
-    for (int64_t i = threadIdx.x; i < (int64_t)Hkv * nvec; i += blockDim.x) {
-        const int h = (int)(i / nvec);
-        const int64_t e = i % nvec;
-        const int64_t src = (((int64_t)b * T + u) * Hkv + h) * row_bytes;
-        const int64_t dst = (((int64_t)b * Hkv + h) * Lmax + P + u) * row_bytes;
-        reinterpret_cast<V*>(k_cache + dst)[e] = reinterpret_cast<const V*>(k_new + src)[e];
-        reinterpret_cast<V*>(v_cache + dst)[e] = reinterpret_cast<const V*>(v_new + src)[e];
+    const int total = Hkv * row_vecs;
+    const V* ks = reinterpret_cast<const V*>(k_new) + ((int64_t)b * T + u) * total;
+    const V* vs = reinterpret_cast<const V*>(v_new) + ((int64_t)b * T + u) * total;
+    V* kd = reinterpret_cast<V*>(k_cache) + ((int64_t)b * Hkv * Lmax + P + u) * row_vecs;
+    V* vd = reinterpret_cast<V*>(v_cache) + ((int64_t)b * Hkv * Lmax + P + u) * row_vecs;
+    const int64_t head_stride = Lmax * row_vecs;  // vectors between heads in the cache
+    for (int i0 = threadIdx.x; i0 < total; i0 += kAppendThreads * kAppendUnroll) {
+        V kx[kAppendUnroll], vx[kAppendUnroll];
+#pragma unroll
+        for (int r = 0; r < kAppendUnroll; ++r) {
+            const int i = i0 + r * kAppendThreads;
+            if (i < total) {
+                kx[r] = ks[i];
+                vx[r] = vs[i];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kAppendUnroll; ++r) {
+            const int i = i0 + r * kAppendThreads;
+            if (i < total) {
+                const int h = i / row_vecs, e = i - h * row_vecs;
+                kd[h * head_stride + e] = kx[r];
+                vd[h * head_stride + e] = vx[r];
+            }
+        }
     }
 }
 
@@ -52,6 +77,8 @@ __global__ void kv_compact_kernel(const int32_t* __restrict__ ids, int ids_strid
                                   int32_t* __restrict__ new_prefix_len, char* k_cache,
                                   char* v_cache, int Hkv, int64_t row_bytes, int64_t Lmax,
                                   int64_t layer_stride_bytes) {
+    pdl_wait();
+    pdl_trigger();
     const int b = blockIdx.x, layer = blockIdx.y;
     const int keep = n_keep[b];
     const int64_t P = prefix_len[b];
@@ -95,14 +122,12 @@ st_status st_kv_append(st_dtype dtype, int B, int T, int Hkv, int D, int64_t Lma
     const int64_t row_bytes = (int64_t)D * st::dtype_size(dtype);
     const dim3 grid(T, B);
     auto s = st::as_stream(stream);
-    if (row_bytes % 16 == 0)
-        st::kv_append_kernel<int4><<<grid, 128, 0, s>>>((const char*)k_new, (const char*)v_new,
-                                                        prefix_len, n_nodes, (char*)k_cache,
-                                                        (char*)v_cache, T, Hkv, row_bytes, Lmax);
-    else
-        st::kv_append_kernel<char><<<grid, 128, 0, s>>>((const char*)k_new, (const char*)v_new,
-                                                        prefix_len, n_nodes, (char*)k_cache,
-                                                        (char*)v_cache, T, Hkv, row_bytes, Lmax);
+    const bool vec = row_bytes % 16 == 0;
+    ST_CUDA_TRY(st::launch_pdl(vec ? st::kv_append_kernel<int4> : st::kv_append_kernel<char>, grid,
+                               dim3(st::kAppendThreads), 0, s, (const char*)k_new,
+                               (const char*)v_new, prefix_len, n_nodes, (char*)k_cache,
+                               (char*)v_cache, T, Hkv, (int)(vec ? row_bytes / 16 : row_bytes),
+                               Lmax));
     ST_LAUNCH_CHECK();
     return ST_OK;
 }
@@ -122,16 +147,11 @@ st_status st_kv_compact(st_dtype dtype, int B, int Hkv, int D, int64_t Lmax, int
     const int64_t row_bytes = (int64_t)D * es;
     const dim3 grid(B, n_layers);
     auto s = st::as_stream(stream);
-    if (row_bytes % 16 == 0)
-        st::kv_compact_kernel<int4><<<grid, 256, 0, s>>>(ids, ids_stride, n_keep, prefix_len,
-                                                         new_prefix_len, (char*)k_cache,
-                                                         (char*)v_cache, Hkv, row_bytes, Lmax,
-                                                         layer_stride * es);
-    else
-        st::kv_compact_kernel<char><<<grid, 256, 0, s>>>(ids, ids_stride, n_keep, prefix_len,
-                                                         new_prefix_len, (char*)k_cache,
-                                                         (char*)v_cache, Hkv, row_bytes, Lmax,
-                                                         layer_stride * es);
+    ST_CUDA_TRY(st::launch_pdl(row_bytes % 16 == 0 ? st::kv_compact_kernel<int4>
+                                                    : st::kv_compact_kernel<char>,
+                               grid, dim3(256), 0, s, ids, ids_stride, n_keep, prefix_len,
+                               new_prefix_len, (char*)k_cache, (char*)v_cache, Hkv, row_bytes,
+                               Lmax, layer_stride * es));
     ST_LAUNCH_CHECK();
     return ST_OK;
 }

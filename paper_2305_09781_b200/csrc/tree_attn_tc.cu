@@ -59,6 +59,10 @@ constexpr uint32_t TILE_BYTES = 2 * KV_ATOM;        // 32 KB K or V tile
 constexpr int NUM_THREADS = 224;                     // 4 softmax + K-TMA + V-TMA + MMA warps
 constexpr int SLOT_FLOATS = 128 * HD + 2 * 128;      // partial O rows + m + l
 constexpr float kLazyThreshLog2 = 8.0f;
+// Batches of up to kTabB requests get their cumulative tile counts staged in
+// shared memory once per CTA (one parallel round of global loads); larger
+// batches walk the lengths in global memory.
+constexpr int kTabB = 128;
 
 // Per-M configuration: M = 64 query rows (T <= 64) or 128 (T <= 128).
 template <int M> struct Cfg {
@@ -77,7 +81,8 @@ template <int M> struct Cfg {
     static constexpr uint32_t OFF_K = OFF_P + PBUF * A_BYTES;
     static constexpr uint32_t OFF_V = OFF_K + KSTAGES * TILE_BYTES;
     static constexpr uint32_t OFF_BAR = OFF_V + VSTAGES * TILE_BYTES;
-    static constexpr uint32_t SMEM_BYTES = OFF_BAR + 256 + 1024;
+    static constexpr uint32_t OFF_TAB = OFF_BAR + 256;     // per-request tile table
+    static constexpr uint32_t SMEM_BYTES = OFF_TAB + (kTabB + 4) * 4 + 1024;
     static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
@@ -93,14 +98,17 @@ struct TcParams {
     float c_log2;        // scale * log2(e)
     float scale;
     unsigned long long* trace;  // optional pipeline trace of CTA 0 (ST_K1_TRACE)
+    int aligned_slack;          // whole-pair schedule allowed within this many tiles of stream-K
 };
+
+constexpr int kTraceCta = 12;  // per-CTA globaltimer/clock slots of the ST_K1_TRACE dump
 
 #define K1_GT(k)                                                                  \
     do {                                                                          \
         if (p.trace) {                                                            \
             unsigned long long gt_;                                               \
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt_));               \
-            p.trace[12 * 64 + 8 * blockIdx.x + (k)] = gt_;                        \
+            p.trace[12 * 64 + kTraceCta * blockIdx.x + (k)] = gt_;                        \
         }                                                                         \
     } while (0)
 
@@ -120,10 +128,30 @@ __device__ __forceinline__ int ntiles_of(const TcParams& p, int b) {
     return n > 0 ? (__ldg(p.prefix_len + b) + n + BN - 1) / BN : 0;
 }
 
-// Segment starting at global tile t (t < t_end) of this CTA's range.
-__device__ Seg find_seg(const TcParams& p, long long t, long long t_end) {
-    long long base = 0;
+// Segment starting at global tile t (t < t_end) of this CTA's range. `cum`
+// (shared memory, or null): cum[b] = tiles of requests < b, cum[kTabB+1..3] =
+// requests with tiles, min and max tiles per request.
+__device__ Seg find_seg(const TcParams& p, const int* cum, long long t, long long t_end) {
     Seg s{};
+    if (cum) {
+        int lo = 0, hi = p.B;  // largest b with H*cum[b] <= t (skips empty requests)
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if ((long long)p.H * cum[mid] <= t) lo = mid; else hi = mid;
+        }
+        const int nt = cum[lo + 1] - cum[lo];
+        const long long base = (long long)p.H * cum[lo];
+        const long long off = t - base;
+        s.b = lo;
+        s.h = (int)(off / nt);
+        s.lo = (int)(off % nt);
+        s.ntiles = nt;
+        s.pair_start = base + (long long)s.h * nt;
+        const long long h2 = s.lo + (t_end - t);
+        s.hi = (int)(h2 < nt ? h2 : nt);
+        return s;
+    }
+    long long base = 0;
     for (int b = 0; b < p.B; ++b) {
         const int nt = ntiles_of(p, b);
         const long long span = (long long)p.H * nt;
@@ -158,10 +186,16 @@ struct Sched {
     bool aligned;
 };
 
-__device__ Sched make_sched(const TcParams& p, long long G) {
+__device__ Sched make_sched(const TcParams& p, const int* cum, long long G) {
     Sched s{0, 0, 0, false};
     int lo = 1 << 30, hi = 0;
-    for (int b = 0; b < p.B; ++b) {
+    if (cum) {
+        s.total = (long long)p.H * cum[p.B];
+        s.np = (long long)p.H * cum[kTabB + 1];
+        lo = cum[kTabB + 2];
+        hi = cum[kTabB + 3];
+    }
+    for (int b = 0; b < (cum ? 0 : p.B); ++b) {
         const int nt = ntiles_of(p, b);
         if (nt > 0) {
             lo = min(lo, nt);
@@ -174,7 +208,7 @@ __device__ Sched make_sched(const TcParams& p, long long G) {
         s.nt = lo;
         const long long aligned_span = (s.np + G - 1) / G * s.nt;
         const long long streamk_span = (s.total + G - 1) / G;
-        s.aligned = aligned_span <= streamk_span + kAlignedSlack;
+        s.aligned = aligned_span <= streamk_span + p.aligned_slack;
     }
     return s;
 }
@@ -241,6 +275,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) K1_GT(8);
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < QS; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
@@ -265,9 +300,49 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // Everything above touches no other kernel's output; from here on the
+    // lengths, masks, Q and the KV cache are read.
+    pdl_wait();
+    int* cum = p.B <= kTabB ? reinterpret_cast<int*>(smem + C::OFF_TAB) : nullptr;
+    if (cum && warp == 0) {
+        int v[kTabB / 32];
+#pragma unroll
+        for (int c = 0; c < kTabB / 32; ++c) {  // all loads in flight together
+            const int b = c * 32 + lane;
+            v[c] = b < p.B ? ntiles_of(p, b) : 0;
+        }
+        int carry = 0, cnt = 0, mn = 1 << 30, mx = 0;
+#pragma unroll
+        for (int c = 0; c < kTabB / 32; ++c) {
+            int x = v[c];
+            cnt += __popc(__ballot_sync(0xffffffffu, x > 0));
+            mn = min(mn, x > 0 ? x : 1 << 30);
+            mx = max(mx, x);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            cum[c * 32 + lane + 1] = carry + x;
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) {
+            cum[0] = 0;
+            cum[kTabB + 1] = cnt;
+            cum[kTabB + 2] = mn;
+            cum[kTabB + 3] = mx;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) K1_GT(9);
 
     const long long G = gridDim.x;
-    const Sched sched = make_sched(p, G);
+    const Sched sched = make_sched(p, cum, G);
     const long long total = sched.total;
     const long long t_begin = range_start(blockIdx.x, sched, G);
     const long long t_end = range_start(blockIdx.x + 1, sched, G);
@@ -275,7 +350,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         long long* e = p.sched + 4 * blockIdx.x;
         e[0] = t_begin;
         if (t_end > t_begin) {
-            const Seg last = find_seg(p, t_end - 1, t_end);
+            const Seg last = find_seg(p, cum, t_end - 1, t_end);
             e[1] = last.pair_start;
             e[2] = last.ntiles;
             e[3] = (long long)last.b * p.H + last.h;
@@ -288,8 +363,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (p.trace && threadIdx.x == 0) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
-        p.trace[12 * 64 + 8 * blockIdx.x] = gt;
-        p.trace[12 * 64 + 8 * blockIdx.x + 2] = (unsigned long long)(t_end - t_begin);
+        p.trace[12 * 64 + kTraceCta * blockIdx.x] = gt;
+        p.trace[12 * 64 + kTraceCta * blockIdx.x + 2] = (unsigned long long)(t_end - t_begin);
+        p.trace[12 * 64 + kTraceCta * blockIdx.x + 6] = clock64();
     }
 
     if (warp == 4) {
@@ -297,7 +373,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         if (lane == 0) {
             uint32_t qc = 0, kc = 0;
             for (long long t = t_begin; t < t_end;) {
-                const Seg s = find_seg(p, t, t_end);
+                const Seg s = find_seg(p, cum, t, t_end);
                 const uint32_t qb = qc % QS;
                 mbar_wait(q_empty + qb, ((qc / QS) & 1) ^ 1);
                 mbar_arrive_expect_tx(q_full + qb, C::A_BYTES);
@@ -309,6 +385,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     const uint32_t st = kc % KS, ph = (kc / KS) & 1;
                     mbar_wait(k_empty + st, ph ^ 1);
                     K1_TRACE(0, kc);
+                    if (kc == 0) K1_GT(5);
                     mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
                     uint8_t* dst = sm_k + st * TILE_BYTES;
                     tma_load_3d(dst, &tm_k, k_full + st, 0, j * BN, bh);
@@ -322,7 +399,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         if (lane == 0) {
             uint32_t vc = 0;
             for (long long t = t_begin; t < t_end;) {
-                const Seg s = find_seg(p, t, t_end);
+                const Seg s = find_seg(p, cum, t, t_end);
                 const int bh = s.b * p.H + s.h;
                 for (int j = s.lo; j < s.hi; ++j, ++vc) {
                     const uint32_t st = vc % VS, ph = (vc / VS) & 1;
@@ -343,85 +420,87 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         //        land in TMEM lanes 0-15 and 16-31 of each subpartition (the
         //        interleaved M=64 layout), so all 32 softmax lanes hold data:
         //        S kv-rows 0-63 | 64-127 and O d 0-63 | 64-127.
-        if (lane == 0) {
-            constexpr uint32_t fmt = std::is_same<T, __half>::value ? 0u : 1u;
-            constexpr uint32_t NS = BN / SPLIT, NO = HD / SPLIT;
-            constexpr uint32_t idS = idesc_f16(fmt, M, NS, 0, 0);   // Q K^T: both K-major
-            constexpr uint32_t idPV = idesc_f16(fmt, M, NO, 0, 1);  // P V: V is MN-major
-            constexpr uint32_t HI_LANES = 16u << 16;                // lane offset of the 2nd half
-            const uint32_t q_base0 = smem_u32(sm_q), k_base = smem_u32(sm_k);
-            const uint32_t v_base = smem_u32(sm_v), p_base = smem_u32(sm_p);
-            uint32_t qc = 0, kc = 0, vc = 0, sc = 0, pc = 0, segc = 0;
-            auto issue_pv = [&](int i_local) {
-                const uint32_t pb = pc & 1;
-                mbar_wait(p_full + pb, (pc >> 1) & 1);
-                const uint32_t st = vc % VS;
-                mbar_wait(v_full + st, (vc / VS) & 1);
-                K1_TRACE(7, vc);
-                if (i_local == 0) mbar_wait(o_empty, (segc & 1) ^ 1);
-                tc_fence_after();
-                const uint32_t vb = v_base + st * TILE_BYTES;
-                const uint32_t pbase = p_base + (pc % C::PBUF) * C::A_BYTES;
+        // The whole warp runs this loop (uniform control flow); MMAs and
+        // commits are issued by one elected lane inside the asm.
+        constexpr uint32_t fmt = std::is_same<T, __half>::value ? 0u : 1u;
+        constexpr uint32_t NS = BN / SPLIT, NO = HD / SPLIT;
+        constexpr uint32_t idS = idesc_f16(fmt, M, NS, 0, 0);   // Q K^T: both K-major
+        constexpr uint32_t idPV = idesc_f16(fmt, M, NO, 0, 1);  // P V: V is MN-major
+        constexpr uint32_t HI_LANES = 16u << 16;                // lane offset of the 2nd half
+        const uint32_t q_base0 = smem_u32(sm_q), k_base = smem_u32(sm_k);
+        const uint32_t v_base = smem_u32(sm_v), p_base = smem_u32(sm_p);
+        uint32_t qc = 0, kc = 0, vc = 0, sc = 0, pc = 0, segc = 0;
+        auto issue_pv = [&](int i_local) {
+            const uint32_t pb = pc & 1;
+            mbar_wait(p_full + pb, (pc >> 1) & 1);
+            const uint32_t st = vc % VS;
+            mbar_wait(v_full + st, (vc / VS) & 1);
+            K1_TRACE(7, vc);
+            if (i_local == 0) mbar_wait(o_empty, (segc & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t vb = v_base + st * TILE_BYTES;
+            const uint64_t pd = smem_desc(p_base + (pc % C::PBUF) * C::A_BYTES, 16, 1024);
+            const uint64_t vd = smem_desc(vb, KV_ATOM, 1024);
 #pragma unroll
-                for (int kk = 0; kk < BN / 16; ++kk) {
-                    const uint64_t a = smem_desc(pbase + (kk >> 2) * C::A_ATOM + (kk & 3) * 32, 16, 1024);
-                    const uint32_t acc = (i_local > 0 || kk > 0) ? 1u : 0u;
-                    if constexpr (SPLIT == 1) {
-                        umma_f16_ss(tmem + C::O_COL, a, smem_desc(vb + kk * 2048, KV_ATOM, 1024), idPV, acc);
-                    } else {
-                        umma_f16_ss(tmem + C::O_COL, a, smem_desc(vb + kk * 2048, KV_ATOM, 1024), idPV, acc);
-                        umma_f16_ss(tmem + HI_LANES + C::O_COL, a,
-                                    smem_desc(vb + KV_ATOM + kk * 2048, KV_ATOM, 1024), idPV, acc);
-                    }
+            for (int kk = 0; kk < BN / 16; ++kk) {
+                const uint64_t a = pd + (((kk >> 2) * C::A_ATOM + (kk & 3) * 32) >> 4);
+                const uint32_t acc = (i_local > 0 || kk > 0) ? 1u : 0u;
+                if constexpr (SPLIT == 1) {
+                    umma_f16_ss_warp(tmem + C::O_COL, a, vd + ((kk * 2048) >> 4), idPV, acc);
+                } else {
+                    umma_f16_ss_warp(tmem + C::O_COL, a, vd + ((kk * 2048) >> 4), idPV, acc);
+                    umma_f16_ss_warp(tmem + HI_LANES + C::O_COL, a,
+                                     vd + ((KV_ATOM + kk * 2048) >> 4), idPV, acc);
                 }
-                K1_TRACE(3, pc);
-                umma_commit(pv_done + pb);
-                umma_commit(v_empty + st);
-                ++vc;
-                ++pc;
-            };
-            for (long long t = t_begin; t < t_end;) {
-                const Seg s = find_seg(p, t, t_end);
-                const int ntl = s.hi - s.lo;
-                const uint32_t qb = qc % QS;
-                mbar_wait(q_full + qb, (qc / QS) & 1);
-                ++qc;
-                const uint32_t q_base = q_base0 + qb * C::A_BYTES;
-                for (int i = 0; i < ntl; ++i) {
-                    const uint32_t st = kc % KS;
-                    mbar_wait(k_full + st, (kc / KS) & 1);
-                    K1_TRACE(6, kc);
-                    const uint32_t sb = sc & 1;
-                    mbar_wait(s_empty + sb, ((sc >> 1) & 1) ^ 1);
-                    tc_fence_after();
-                    const uint32_t kb = k_base + st * TILE_BYTES;
-                    const uint32_t scol = sb * C::S_COLS;
-#pragma unroll
-                    for (int kk = 0; kk < HD / 16; ++kk) {
-                        const uint32_t off = (kk >> 2) * C::A_ATOM + (kk & 3) * 32;
-                        const uint32_t koff = (kk >> 2) * KV_ATOM + (kk & 3) * 32;
-                        const uint64_t a = smem_desc(q_base + off, 16, 1024);
-                        const uint32_t acc = kk > 0 ? 1u : 0u;
-                        if constexpr (SPLIT == 1) {
-                            umma_f16_ss(tmem + scol, a, smem_desc(kb + koff, 16, 1024), idS, acc);
-                        } else {  // kv rows 0-63 -> lanes 0-15, kv rows 64-127 -> lanes 16-31
-                            umma_f16_ss(tmem + scol, a, smem_desc(kb + koff, 16, 1024), idS, acc);
-                            umma_f16_ss(tmem + HI_LANES + scol, a,
-                                        smem_desc(kb + koff + 64 * 128, 16, 1024), idS, acc);
-                        }
-                    }
-                    K1_TRACE(2, sc);
-                    umma_commit(s_full + sb);
-                    umma_commit(k_empty + st);
-                    if (i == ntl - 1) umma_commit(q_empty + qb);
-                    ++kc;
-                    ++sc;
-                    if (i > 0) issue_pv(i - 1);
-                }
-                issue_pv(ntl - 1);
-                ++segc;
-                t += ntl;
             }
+            K1_TRACE(3, pc);
+            umma_commit_warp(pv_done + pb);
+            umma_commit_warp(v_empty + st);
+            ++vc;
+            ++pc;
+        };
+        for (long long t = t_begin; t < t_end;) {
+            const Seg s = find_seg(p, cum, t, t_end);
+            const int ntl = s.hi - s.lo;
+            const uint32_t qb = qc % QS;
+            mbar_wait(q_full + qb, (qc / QS) & 1);
+            ++qc;
+            const uint32_t q_base = q_base0 + qb * C::A_BYTES;
+            for (int i = 0; i < ntl; ++i) {
+                const uint32_t st = kc % KS;
+                mbar_wait(k_full + st, (kc / KS) & 1);
+                K1_TRACE(6, kc);
+                const uint32_t sb = sc & 1;
+                mbar_wait(s_empty + sb, ((sc >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t kb = k_base + st * TILE_BYTES;
+                const uint32_t scol = sb * C::S_COLS;
+                const uint64_t qd = smem_desc(q_base, 16, 1024), kd = smem_desc(kb, 16, 1024);
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * C::A_ATOM + (kk & 3) * 32;
+                    const uint32_t koff = (kk >> 2) * KV_ATOM + (kk & 3) * 32;
+                    const uint64_t a = qd + (off >> 4);
+                    const uint32_t acc = kk > 0 ? 1u : 0u;
+                    if constexpr (SPLIT == 1) {
+                        umma_f16_ss_warp(tmem + scol, a, kd + (koff >> 4), idS, acc);
+                    } else {  // kv rows 0-63 -> lanes 0-15, kv rows 64-127 -> lanes 16-31
+                        umma_f16_ss_warp(tmem + scol, a, kd + (koff >> 4), idS, acc);
+                        umma_f16_ss_warp(tmem + HI_LANES + scol, a,
+                                         kd + ((koff + 64 * 128) >> 4), idS, acc);
+                    }
+                }
+                K1_TRACE(2, sc);
+                umma_commit_warp(s_full + sb);
+                umma_commit_warp(k_empty + st);
+                if (i == ntl - 1) umma_commit_warp(q_empty + qb);
+                ++kc;
+                ++sc;
+                if (i > 0) issue_pv(i - 1);
+            }
+            issue_pv(ntl - 1);
+            ++segc;
+            t += ntl;
         }
     } else {
         // ===================== softmax + epilogue (warps 0-3) ==================
@@ -436,7 +515,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         const float thresh_raw = kLazyThreshLog2 / c;
         uint32_t sc = 0, pc = 0;
         for (long long t = t_begin; t < t_end;) {
-            const Seg s = find_seg(p, t, t_end);
+            const Seg s = find_seg(p, cum, t, t_end);
             const int ntl = s.hi - s.lo;
             const int n = __ldg(p.n_nodes + s.b);
             const int P = __ldg(p.prefix_len + s.b);
@@ -632,7 +711,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (p.trace && threadIdx.x == 0) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
-        p.trace[12 * 64 + 8 * blockIdx.x + 1] = gt;
+        p.trace[12 * 64 + kTraceCta * blockIdx.x + 1] = gt;
+        p.trace[12 * 64 + kTraceCta * blockIdx.x + 7] = clock64();
     }
     if (warp == 6) tmem_dealloc<C::TMEM_COLS>(tmem);
 }
@@ -657,7 +737,8 @@ combine_kernel(const TcParams p, int G) {
     constexpr int MAXP = 2;   // pieces held in registers; more are merged online
     constexpr int RPW = 8;    // rows per warp in flight together (8 warps x 8 = 64 rows/pass)
     const int cta = blockIdx.x;
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: wait for the attention kernel
+    pdl_wait();  // the attention kernel's pieces and schedule table
+    pdl_trigger();
     const long long* tab = p.sched;
     const long long rs = __ldcg(tab + 4 * cta), re = __ldcg(tab + 4 * (cta + 1));
     const long long ps = __ldcg(tab + 4 * cta + 1), nt = __ldcg(tab + 4 * cta + 2);
@@ -795,23 +876,9 @@ size_t tree_attention_tc_workspace(const st_attn_args* a) {
            (size_t)(num_sms() + 1) * 4 * sizeof(long long);
 }
 
-// combine_kernel with programmatic dependent launch: it is scheduled while the
-// attention kernel drains and blocks in griddepcontrol.wait until it ends.
-template <class TT>
-void launch_combine(const TcParams& prm, int G, int blocks, cudaStream_t stream) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(blocks);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, combine_kernel<TT>, prm, G);
-}
-
+// K1 and combine_kernel are both launched with programmatic dependent launch
+// (common.cuh): K1's prologue overlaps the previous kernel's tail, and the
+// combine is scheduled while K1 drains, blocking in pdl_wait() until it ends.
 #define ST_TRY_LAUNCH_TC(TT, MM)                                                                \
     do {                                                                                        \
         static bool attr = false;                                                               \
@@ -821,8 +888,9 @@ void launch_combine(const TcParams& prm, int G, int blocks, cudaStream_t stream)
                                              Cfg<MM>::SMEM_BYTES));                             \
             attr = true;                                                                        \
         }                                                                                       \
-        tree_attn_tc_kernel<TT, MM><<<G, NUM_THREADS, Cfg<MM>::SMEM_BYTES, stream>>>(tq, tk, tv, prm); \
-        launch_combine<TT>(prm, G, G, stream);                                                  \
+        ST_CUDA_TRY(launch_pdl(tree_attn_tc_kernel<TT, MM>, dim3(G), dim3(NUM_THREADS),          \
+                               Cfg<MM>::SMEM_BYTES, stream, tq, tk, tv, prm));                  \
+        ST_CUDA_TRY(launch_pdl(combine_kernel<TT>, dim3(G), dim3(256), 0, stream, prm, G));     \
     } while (0)
 
 st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
@@ -865,10 +933,13 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     prm.scale = (float)a->scale;
     prm.c_log2 = (float)(a->scale * 1.4426950408889634);
     prm.trace = nullptr;
+    // diagnostic override of the whole-pair schedule threshold (ST_K1_SLACK=-1: always stream-K)
+    static const int slack_env = getenv("ST_K1_SLACK") ? atoi(getenv("ST_K1_SLACK")) : (int)kAlignedSlack;
+    prm.aligned_slack = slack_env;
     static unsigned long long* trace_buf = nullptr;
     if (getenv("ST_K1_TRACE")) {
-        if (!trace_buf) cudaMalloc(&trace_buf, (12 * 64 + 8 * 1024) * sizeof(unsigned long long));
-        cudaMemsetAsync(trace_buf, 0, (12 * 64 + 8 * 1024) * sizeof(unsigned long long), stream);
+        if (!trace_buf) cudaMalloc(&trace_buf, (12 * 64 + kTraceCta * 1024) * sizeof(unsigned long long));
+        cudaMemsetAsync(trace_buf, 0, (12 * 64 + kTraceCta * 1024) * sizeof(unsigned long long), stream);
         prm.trace = trace_buf;
     }
     const bool m64 = a->T <= 64;
@@ -879,7 +950,7 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     }
     ST_LAUNCH_CHECK();
     if (prm.trace) {  // diagnostic only: dump CTA 0's pipeline timestamps
-        static unsigned long long h[12 * 64 + 8 * 1024];
+        static unsigned long long h[12 * 64 + kTraceCta * 1024];
         cudaMemcpyAsync(h, prm.trace, sizeof h, cudaMemcpyDeviceToHost, stream);
         cudaStreamSynchronize(stream);
         if (FILE* f = fopen(getenv("ST_K1_TRACE"), "a")) {
@@ -887,7 +958,7 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
                 for (int i = 0; i < 64; ++i) fprintf(f, "%llu ", h[r * 64 + i]);
                 fprintf(f, "\n");
             }
-            for (int i = 0; i < 8 * G; ++i) fprintf(f, "%llu ", h[12 * 64 + i]);
+            for (int i = 0; i < kTraceCta * G; ++i) fprintf(f, "%llu ", h[12 * 64 + i]);
             fprintf(f, "\n");
             fclose(f);
         }

@@ -18,6 +18,7 @@
 // PDL-launched kernel (one warp per request) resolves the keys and walks:
 // children of u are the ids v > u with parent[v] == u, scanned 32 at a time
 // with a ballot.
+#include <algorithm>
 #include <cfloat>
 
 #include "common.cuh"
@@ -138,6 +139,8 @@ constexpr int kUnroll = 8;  // float4 loads in flight per thread (a 4000-float s
 __global__ void __launch_bounds__(kThreads)
 greedy_argmax_kernel(const float* __restrict__ logits, int T, int V,
                      const int32_t* __restrict__ n_nodes, unsigned long long* keys) {
+    pdl_wait();
+    pdl_trigger();  // let the walk kernel get scheduled while the rows stream
     const int part = blockIdx.x, u = blockIdx.y, b = blockIdx.z;
     if (u >= n_nodes[b]) return;
     const float* row = logits + ((int64_t)b * T + u) * V;
@@ -181,8 +184,6 @@ greedy_argmax_kernel(const float* __restrict__ logits, int T, int V,
         for (int w = 1; w < kThreads / 32; ++w) best = max(best, red[w]);
         atomicMax(keys + (int64_t)b * T + u, best);
     }
-    // let the dependent walk kernel get scheduled while the stream drains
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // Phase 2 (launched with programmatic dependent launch): one warp per request
@@ -193,7 +194,8 @@ greedy_walk_kernel(int T, const int32_t* __restrict__ tokens, const int32_t* __r
                    int32_t eos, int32_t* __restrict__ argmax_out, unsigned long long* keys,
                    int32_t* argmax_ws, int32_t* __restrict__ verified, int32_t* __restrict__ ids,
                    int32_t* __restrict__ len) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    pdl_wait();
+    pdl_trigger();
     __shared__ int s_out[kWalkMax], s_next[kWalkMax];
     const int b = blockIdx.x, lane = threadIdx.x;
     const int n = n_nodes[b];
@@ -210,26 +212,43 @@ greedy_walk_kernel(int T, const int32_t* __restrict__ tokens, const int32_t* __r
               s_out, s_next);
 }
 
-// One thread per (request, node): walk the parent chain (depth <= T) and set
-// the ancestor-or-self bits; no inter-thread dependency, one launch per batch.
+// One thread per (request, node). The request's parent row is staged in
+// shared memory first; the walk up the parent chain (ids strictly decrease)
+// then emits the ancestor-or-self bits word by word, high word first, so no
+// per-thread word array is needed (nothing spills to local memory).
 __global__ void build_masks_kernel(const int32_t* __restrict__ parent,
                                    const int32_t* __restrict__ n_nodes, int T, int W,
                                    uint64_t* __restrict__ mask) {
+    extern __shared__ int s_par[];
+    pdl_wait();
+    pdl_trigger();
     const int b = blockIdx.y;
     const int u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= T) return;
     const int n = n_nodes[b];
+    const int upto = min(n, (int)((blockIdx.x + 1) * blockDim.x));  // nodes this block needs
     const int32_t* par = parent + (int64_t)b * T;
+    for (int v = threadIdx.x; v < upto; v += blockDim.x) s_par[v] = par[v];
+    __syncthreads();
+    if (u >= T) return;
     uint64_t* mu = mask + ((int64_t)b * T + u) * W;
-    uint64_t w[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) w[i] = 0;
+    int wi = W - 1;
     if (u < n) {
-        for (int v = u; v >= 0; v = par[v]) w[v >> 6] |= 1ull << (v & 63);
+        uint64_t acc = 0;
+        for (int v = u; v >= 0;) {
+            const int vw = v >> 6;
+            while (wi > vw) {
+                mu[wi] = acc;
+                acc = 0;
+                --wi;
+            }
+            acc |= 1ull << (v & 63);
+            const int pv = s_par[v];
+            v = pv < v ? pv : -1;  // preorder: parent id < child id (stop on malformed input)
+        }
+        mu[wi] = acc;
+        --wi;
     }
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-        if (i < W) mu[i] = w[i];
+    for (; wi >= 0; --wi) mu[wi] = 0;
 }
 
 }  // namespace
@@ -260,19 +279,12 @@ st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32
         (reinterpret_cast<uintptr_t>(tickets + B) + 15) & ~uintptr_t(15));
     const dim3 grid(st::kSplit, T, B);
     auto strm = st::as_stream(stream);
-    st::greedy_argmax_kernel<<<grid, st::kThreads, 0, strm>>>(logits, T, V, n_nodes, keys);
+    ST_CUDA_TRY(st::launch_pdl(st::greedy_argmax_kernel, grid, dim3(st::kThreads), 0, strm, logits,
+                               T, V, n_nodes, keys));
     ST_LAUNCH_CHECK();
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(B);
-    cfg.blockDim = dim3(32);
-    cfg.stream = strm;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    ST_CUDA_TRY(cudaLaunchKernelEx(&cfg, st::greedy_walk_kernel, T, tokens, parent, n_nodes, budget,
-                                   eos, argmax, keys, scratch, verified, ids, len));
+    ST_CUDA_TRY(st::launch_pdl(st::greedy_walk_kernel, dim3(B), dim3(32), 0, strm, T, tokens,
+                               parent, n_nodes, budget, eos, argmax, keys, scratch, verified, ids,
+                               len));
     ST_LAUNCH_CHECK();
     return ST_OK;
 }
@@ -300,7 +312,9 @@ st_status st_build_masks(const int32_t* parent, const int32_t* n_nodes, int B, i
     if (B == 0) return ST_OK;
     ST_CHECK_ARG(parent && n_nodes && mask, ST_ERR_INVALID_ARGUMENT, "null pointer");
     const dim3 grid((T + 127) / 128, B);
-    st::build_masks_kernel<<<grid, 128, 0, st::as_stream(stream)>>>(parent, n_nodes, T, W, mask);
+    const size_t smem = (size_t)std::min(T, 128 * (int)grid.x) * sizeof(int32_t);
+    ST_CUDA_TRY(st::launch_pdl(st::build_masks_kernel, grid, dim3(128), smem, st::as_stream(stream),
+                               parent, n_nodes, T, W, mask));
     ST_LAUNCH_CHECK();
     return ST_OK;
 }

@@ -33,6 +33,22 @@ def test_tc_matches_oracle(capi, restatement, dtype, B, H, P_range):
     check_k1(restatement, bt, out, dtype, lse)
 
 
+@pytest.mark.parametrize("B,empty", [(40, (0, 7, 39)), (136, (5,))])
+def test_tc_batch_table_and_empty_requests(capi, restatement, B, empty):
+    """B <= 128 uses the shared-memory tile table (binary search over the
+    cumulative tile counts), B = 136 the global-memory walk; requests with no
+    tree nodes own no tiles and must be skipped by both."""
+    rng = np.random.default_rng(B)
+    bt = make_batch(restatement, rng, B, 2, 2, 128, dtype=torch.float16, P_range=(0, 300))
+    for b in empty:
+        bt["n"][b] = 0
+    out, _ = run_k1(capi, bt, torch.float16, force_path=2)
+    keep = [b for b in range(B) if b not in empty]
+    sub = {k: (v[keep] if isinstance(v, np.ndarray) and v.shape[:1] == (B,) else v)
+           for k, v in bt.items()}
+    check_k1(restatement, sub, out[keep], torch.float16)
+
+
 def _dummy(bt, dtype):
     dev = "cuda"
     q = torch.zeros(bt["q"].shape, dtype=dtype, device=dev)

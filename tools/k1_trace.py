@@ -28,7 +28,7 @@ for _ in range(3):
 torch.cuda.synchronize()
 lines = [list(map(int, l.split())) for l in open(out)]
 rows = lines[-13:-1]
-cta = np.array(lines[-1], dtype=np.int64).reshape(-1, 8)
+cta = np.array(lines[-1], dtype=np.int64).reshape(-1, 12)
 t = np.array(rows, dtype=np.int64)
 t0 = t[0][t[0] > 0].min()
 names = ["K issue", "V issue", "S issue", "PV issue", "S ready", "P done", "K full(mma)", "V full(mma)", "S loaded", "masked+max", "pv wait done", "rescaled"]
@@ -49,7 +49,16 @@ hist = np.histogram(dur, bins=8)
 print("duration histogram:", hist[0].tolist(), [round(float(x), 1) for x in hist[1]])
 
 rel = lambda k: (cta[:, k] - cta[:, 0]) / 1e3  # noqa: E731
-for k, name in [(3, "last PV done"), (4, "O read+written"), (5, "partial fenced"), (6, "ticket"), (7, "merge done"), (1, "CTA end")]:
+mhz = (cta[:, 7] - cta[:, 6]) / (cta[:, 1] - cta[:, 0]) * 1e3
+print("SM clock from clock64/globaltimer (MHz): median %.0f min %.0f max %.0f" % (np.median(mhz), mhz.min(), mhz.max()))
+for k, name in [(8, "kernel entry"), (9, "setup done"), (5, "first K issue"), (3, "last PV done"), (4, "O read+written"), (1, "CTA end")]:
     v = rel(k)
     ok = cta[:, k] > 0
-    print(f"{name:16s} (us after CTA start): median {np.median(v[ok]) if ok.any() else -1:7.2f}  max {v[ok].max() if ok.any() else -1:7.2f}  n={ok.sum()}")
+    if k == 8:
+        v = -v
+    print(f"{name:16s} (us after CTA start; entry: before): median {np.median(v[ok]) if ok.any() else -1:7.2f}  max {v[ok].max() if ok.any() else -1:7.2f}  n={ok.sum()}")
+ent = cta[:, 8]
+e0 = ent.min()
+print("kernel entry spread (us): %.2f ; whole kernel entry->last end (us): %.2f" % ((ent.max() - e0) / 1e3, (cta[:, 1].max() - e0) / 1e3))
+per_tile = (cta[:, 3] - cta[:, 5]) / np.maximum(nt - 1, 1) / 1e3
+print("per-tile (us, first K issue -> last PV done): median %.3f min %.3f max %.3f" % (np.median(per_tile), per_tile.min(), per_tile.max()))
