@@ -70,15 +70,13 @@ template <int M> struct Cfg {
     static constexpr uint32_t A_ATOM = M * 128;             // M rows x 64 elems x 2 B
     static constexpr uint32_t A_BYTES = 2 * A_ATOM;         // Q or one P buffer
     static constexpr int QSTAGES = M == 64 ? 2 : 1;          // next pair's Q prefetched
-    static constexpr int PBUF = 2;                            // P buffers in smem
-    static constexpr int KSTAGES = 2;
-    static constexpr int VSTAGES = M == 64 ? 3 : 2;
+    static constexpr int KSTAGES = 3;
+    static constexpr int VSTAGES = 3;
     static constexpr uint32_t S_COLS = BN / SPLIT;          // TMEM columns per S buffer
     static constexpr uint32_t O_COL = 2 * S_COLS;           // O accumulator column
     static constexpr uint32_t TMEM_COLS = M == 64 ? 256 : 512;
     static constexpr uint32_t OFF_Q = 0;
-    static constexpr uint32_t OFF_P = OFF_Q + QSTAGES * A_BYTES;
-    static constexpr uint32_t OFF_K = OFF_P + PBUF * A_BYTES;
+    static constexpr uint32_t OFF_K = OFF_Q + QSTAGES * A_BYTES;
     static constexpr uint32_t OFF_V = OFF_K + KSTAGES * TILE_BYTES;
     static constexpr uint32_t OFF_BAR = OFF_V + VSTAGES * TILE_BYTES;
     static constexpr uint32_t OFF_TAB = OFF_BAR + 256;     // per-request tile table
@@ -257,7 +255,6 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     uint8_t* sm_q = smem + C::OFF_Q;
-    uint8_t* sm_p = smem + C::OFF_P;
     uint8_t* sm_k = smem + C::OFF_K;
     uint8_t* sm_v = smem + C::OFF_V;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -268,8 +265,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     uint64_t* v_full = k_empty + KS;     // [VS]
     uint64_t* v_empty = v_full + VS;     // [VS]
     uint64_t* s_full = v_empty + VS;     // [2]
-    uint64_t* s_empty = s_full + 2;      // [2]
-    uint64_t* p_full = s_empty + 2;      // [2]
+    uint64_t* p_full = s_full + 2;       // [2]
     uint64_t* pv_done = p_full + 2;      // [2]
     uint64_t* o_empty = pv_done + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
@@ -283,7 +279,6 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         for (int i = 0; i < VS; ++i) { mbar_init(v_full + i, 1); mbar_init(v_empty + i, 1); }
         for (int i = 0; i < 2; ++i) {
             mbar_init(s_full + i, 1);
-            mbar_init(s_empty + i, 128);
             mbar_init(p_full + i, 128);
             mbar_init(pv_done + i, 1);
         }
@@ -428,7 +423,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         constexpr uint32_t idPV = idesc_f16(fmt, M, NO, 0, 1);  // P V: V is MN-major
         constexpr uint32_t HI_LANES = 16u << 16;                // lane offset of the 2nd half
         const uint32_t q_base0 = smem_u32(sm_q), k_base = smem_u32(sm_k);
-        const uint32_t v_base = smem_u32(sm_v), p_base = smem_u32(sm_p);
+        const uint32_t v_base = smem_u32(sm_v);
         uint32_t qc = 0, kc = 0, vc = 0, sc = 0, pc = 0, segc = 0;
         auto issue_pv = [&](int i_local) {
             const uint32_t pb = pc & 1;
@@ -439,17 +434,19 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             if (i_local == 0) mbar_wait(o_empty, (segc & 1) ^ 1);
             tc_fence_after();
             const uint32_t vb = v_base + st * TILE_BYTES;
-            const uint64_t pd = smem_desc(p_base + (pc % C::PBUF) * C::A_BYTES, 16, 1024);
             const uint64_t vd = smem_desc(vb, KV_ATOM, 1024);
+            // P of this tile sits in TMEM over its S buffer (K-major, 2 elements
+            // per column: K=16 per MMA = 8 columns). For M=64 each half-lane
+            // group holds the full P rows, matching its O accumulator's lanes.
+            const uint32_t pt = tmem + pb * C::S_COLS;
 #pragma unroll
             for (int kk = 0; kk < BN / 16; ++kk) {
-                const uint64_t a = pd + (((kk >> 2) * C::A_ATOM + (kk & 3) * 32) >> 4);
                 const uint32_t acc = (i_local > 0 || kk > 0) ? 1u : 0u;
                 if constexpr (SPLIT == 1) {
-                    umma_f16_ss_warp(tmem + C::O_COL, a, vd + ((kk * 2048) >> 4), idPV, acc);
+                    umma_f16_ts_warp(tmem + C::O_COL, pt + kk * 8, vd + ((kk * 2048) >> 4), idPV, acc);
                 } else {
-                    umma_f16_ss_warp(tmem + C::O_COL, a, vd + ((kk * 2048) >> 4), idPV, acc);
-                    umma_f16_ss_warp(tmem + HI_LANES + C::O_COL, a,
+                    umma_f16_ts_warp(tmem + C::O_COL, pt + kk * 8, vd + ((kk * 2048) >> 4), idPV, acc);
+                    umma_f16_ts_warp(tmem + HI_LANES + C::O_COL, pt + HI_LANES + kk * 8,
                                      vd + ((KV_ATOM + kk * 2048) >> 4), idPV, acc);
                 }
             }
@@ -470,8 +467,10 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 const uint32_t st = kc % KS;
                 mbar_wait(k_full + st, (kc / KS) & 1);
                 K1_TRACE(6, kc);
+                // S buffer sb last held P of tile sc-2, read by the P.V MMA
+                // issued before this one: tcgen05 MMAs of one thread execute in
+                // issue order, so no barrier is needed before overwriting it.
                 const uint32_t sb = sc & 1;
-                mbar_wait(s_empty + sb, ((sc >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t kb = k_base + st * TILE_BYTES;
                 const uint32_t scol = sb * C::S_COLS;
@@ -545,8 +544,6 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 #pragma unroll
                         for (int k = 0; k < 32; ++k) sv[ch * 32 + k] = __uint_as_float(raw[k]);
                     }
-                    tc_fence_before();
-                    mbar_arrive(s_empty + sb);
                     if (threadIdx.x == 0) K1_TRACE(8, sc);
                     // ---- tree mask: one visibility word per 32 columns ----
                     if (j * BN + BN > P) {
@@ -610,8 +607,6 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         tmem_st_wait();
                     }
                     if (threadIdx.x == 0) K1_TRACE(11, sc);
-                    // exps into packed registers first, so the wait for the P
-                    // buffer below overlaps the MUFU work
                     const float base = (m == -INFINITY) ? 0.f : m * c;
                     float ls[4] = {0.f, 0.f, 0.f, 0.f};
                     uint32_t pk[COLS / 2];
@@ -622,33 +617,31 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         ls[k & 3] += p0 + p1;
                         pk[k] = pk2<T>::pack(p0, p1);
                     }
-                    // P buffer (pc % PBUF) was last read by P.V number pc-PBUF
-                    if (pc >= (uint32_t)C::PBUF) {
-                        const uint32_t q2 = pc - C::PBUF;
-                        mbar_wait(pv_done + (q2 & 1), (q2 >> 1) & 1);
-                    }
-                    if (threadIdx.x == 0) K1_TRACE(10, sc);
-                    uint8_t* prow = sm_p + (pc % C::PBUF) * C::A_BYTES + r * 128;
+                    // P (f16/bf16) into TMEM over this tile's S columns: 64
+                    // columns per row (2 elements each). M=64: the two lanes of a
+                    // row swap halves so both hold the full row (the P.V MMA of
+                    // each half-lane group reads A from its own lanes).
+                    const uint32_t pt = lane_addr + sb * C::S_COLS;
+                    if constexpr (SPLIT == 2) {
+                        uint32_t lo[32], hi[32];
 #pragma unroll
-                    for (int ch = 0; ch < COLS / 8; ++ch) {
-                        // 16-byte chunk cc of the row's 128 kv columns; atom = cc / 8
-                        const uint32_t cc = half * (COLS / 8) + ch;
-                        const uint32_t atom = cc >> 3, cin = cc & 7;
-                        *reinterpret_cast<uint4*>(prow + atom * C::A_ATOM + ((cin ^ (r & 7)) << 4)) =
-                            make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+                        for (int k = 0; k < 32; ++k) {
+                            const uint32_t o = __shfl_xor_sync(0xffffffffu, pk[k], 16);
+                            lo[k] = half ? o : pk[k];
+                            hi[k] = half ? pk[k] : o;
+                        }
+                        tmem_st_32x32b_x32(pt, lo);
+                        tmem_st_32x32b_x32(pt + 32, hi);
+                    } else {
+                        tmem_st_32x32b_x32(pt, *reinterpret_cast<const uint32_t(*)[32]>(pk));
+                        tmem_st_32x32b_x32(pt + 32, *reinterpret_cast<const uint32_t(*)[32]>(pk + 32));
                     }
+                    tmem_st_wait();
+                    if (threadIdx.x == 0) K1_TRACE(10, sc);
                     l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-                    fence_proxy_async_smem();
                     tc_fence_before();
-                } else {
-                    // rows all padding: no TMEM traffic or math, but the same
-                    // waits as live warps so every arrival lands in its own phase
-                    mbar_arrive(s_empty + sb);
-                    if (pc >= (uint32_t)C::PBUF) {
-                        const uint32_t q2 = pc - C::PBUF;
-                        mbar_wait(pv_done + (q2 & 1), (q2 >> 1) & 1);
-                    }
                 }
+                // (rows all padding: no TMEM traffic or math, only the arrival)
                 ++sc;
                 if (threadIdx.x == 0) K1_TRACE(5, pc);
                 mbar_arrive(p_full + pb);

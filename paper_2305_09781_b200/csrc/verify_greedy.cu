@@ -151,6 +151,12 @@ greedy_argmax_kernel(const float* __restrict__ logits, int T, int V,
         const int per = (nv + kSplit - 1) / kSplit;
         const int lo = part * per, hi = min(nv, lo + per);
         const float4* r4 = reinterpret_cast<const float4*>(row);
+        // this thread's elements in increasing index order with the reference's
+        // strict '>' (NaN never wins, ties keep the lower index); the 64-bit key
+        // is formed once per thread. Starts at the thread's first index so an
+        // all -inf/NaN slice reports its lowest index, as arg_key would.
+        float bv = -INFINITY;
+        int bi = lo + (int)threadIdx.x < hi ? (lo + (int)threadIdx.x) * 4 : -1;
         for (int base = lo + threadIdx.x; base < hi; base += kThreads * kUnroll) {
             float4 x[kUnroll];
 #pragma unroll
@@ -161,14 +167,14 @@ greedy_argmax_kernel(const float* __restrict__ logits, int T, int V,
 #pragma unroll
             for (int k = 0; k < kUnroll; ++k) {
                 const int j = (base + k * kThreads) * 4;
-                if (j < hi * 4) {
-                    best = max(best, arg_key(x[k].x, j));
-                    best = max(best, arg_key(x[k].y, j + 1));
-                    best = max(best, arg_key(x[k].z, j + 2));
-                    best = max(best, arg_key(x[k].w, j + 3));
-                }
+                if (x[k].x > bv) { bv = x[k].x; bi = j; }
+                if (x[k].y > bv) { bv = x[k].y; bi = j + 1; }
+                if (x[k].z > bv) { bv = x[k].z; bi = j + 2; }
+                if (x[k].w > bv) { bv = x[k].w; bi = j + 3; }
             }
         }
+        if (bi >= 0) best = arg_key(bv, bi);
+        if (lo == 0 && threadIdx.x == 0 && row[0] != row[0]) best = ~0ull;  // NaN at index 0
     } else {
         const int per = (V + kSplit - 1) / kSplit;
         const int lo = part * per, hi = min(V, lo + per);

@@ -224,14 +224,21 @@ def test_k3_tie_and_nan_rules(capi, restatement):
     (argmax_token, reference transformer.cpp:116-122)."""
     tok, par, dep = restatement.merge([[0, 1], [0, 2]])
     T, V = len(tok), 4100
-    logits = np.zeros((4, T, V), np.float32)
+    logits = np.zeros((8, T, V), np.float32)
     logits[0, :, 7] = logits[0, :, 3000] = 5.0       # tie -> 7
     logits[1, :, 1] = np.nan
     logits[1, :, 2] = 1.0                            # NaN skipped -> 2
     logits[2, :, 0] = np.nan
     logits[2, :, 5] = 9.0                            # NaN at 0 -> 0
     logits[3, :, :] = -np.inf                        # all -inf -> 0
-    tok4, par4, _, n4 = pack([(tok, par, dep)] * 4)
+    logits[4, :, :] = np.nan                         # -inf at 0, NaN elsewhere but one
+    logits[4, :, 0] = -np.inf
+    logits[4, :, 3999] = -5.0                        # -> 3999 (last slice)
+    logits[5, :, [2050, 2051, 4099]] = 2.0           # tie inside one float4 -> 2050
+    logits[6, :, :] = -np.inf
+    logits[6, :, 4000] = np.nan                      # -> 0
+    logits[7] = np.random.default_rng(3).standard_normal((T, V)).astype(np.float32)
+    tok4, par4, _, n4 = pack([(tok, par, dep)] * 8)
     _verify_case(capi, restatement, logits, tok4, par4, n4)
 
 
