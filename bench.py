@@ -312,28 +312,29 @@ def main():
     torch.cuda.current_stream().wait_stream(side)
     barrier()
     graphs = {}
-    for name, fn in (("pre", pre), ("k1", k1), ("post", post), ("full", lambda *a: eager(a))):
+    for name, fn in (("full", lambda *a: eager(a)),):
         g_ = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_):
             fn(*resident)
         graphs[name] = g_
+    # the same step with timing events (external: recorded as graph nodes)
+    # bracketing K1 and its combine
+    ev_k1 = (torch.cuda.Event(enable_timing=True, external=True),
+             torch.cuda.Event(enable_timing=True, external=True))
+    g_ = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_):
+        pre(*resident)
+        ev_k1[0].record()
+        k1(*resident)
+        ev_k1[1].record()
+        post(*resident)
+    graphs["timed"] = g_
 
     def step(time_k1=False):
-        if not time_k1:   # the whole step as one graph
-            graphs["full"].replay()
-            if world > 1:
-                gather_accepted(vout[0], vout[2], world, out=gathered)
-            return vout[0], vout[2]
-        graphs["pre"].replay()
-        if time_k1:
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-        graphs["k1"].replay()
-        if time_k1:
-            e1.record()
-            k1_events.append((e0, e1))
-        graphs["post"].replay()
+        graphs["timed" if time_k1 else "full"].replay()
+        if time_k1:   # read this step's K1 duration before the next replay
+            ev_k1[1].synchronize()
+            k1_events.append(ev_k1[0].elapsed_time(ev_k1[1]))
         if world > 1:   # DP exchange: every rank sees every request's accepted tokens
             gather_accepted(vout[0], vout[2], world, out=gathered)
         return vout[0], vout[2]
@@ -358,8 +359,8 @@ def main():
         step()
     t1.record()
     barrier()
-    # K1's own duration: the same K steps again, split into pre / K1 / post
-    # graphs with events around K1 (+ its combine) on the launching stream
+    # K1's own duration: the same K steps again, from the graph whose timing
+    # events bracket K1 + its combine on the launching stream
     for _ in range(args.steps):
         step(time_k1=True)
     for _ in range(200):        # keep sampling a little past the timed region
@@ -367,7 +368,7 @@ def main():
     barrier()
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
-    k1_ms = statistics.mean(a.elapsed_time(b) for a, b in k1_events)
+    k1_ms = statistics.mean(k1_events)
     if world > 1:
         tt = torch.tensor([ms, k1_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -376,15 +377,31 @@ def main():
     value = B * T * world / (ms_step / 1e3)
 
     # ---- e2e: C-ABI calls with HOST buffers, copies inside the timed region ----
-    # Per step: H2D of Q, the tree's K/V and the tree topology from pinned host
-    # memory, the step, D2H of the accepted tokens + lengths, which the host
-    # reads. Serving-style pipelining: step i+1's H2D runs on a copy stream while
-    # step i computes (two device input sets).
+    # Per step: the host merges every request's candidate sequences into its
+    # token tree (st_tree_merge_batch on the host thread pool, packed straight
+    # into pinned memory), H2D of Q, the tree's K/V and the tree topology, the
+    # step, D2H of the accepted tokens + lengths, which the host reads.
+    # Serving-style pipelining: step i+1's merge + H2D run while step i
+    # computes (two host and two device input sets).
+    from paper_2305_09781_b200.tree import MergeInputs, merge_batch
+    merge_in = MergeInputs([sq for _, sq in trees])
     h_q = q.cpu().pin_memory()
     h_k = knew.cpu().pin_memory()
     h_v = vnew.cpu().pin_memory()
-    h_topo = torch.tensor(np.concatenate([batch.tokens.ravel(), batch.parents.ravel(),
-                                          batch.n_nodes]), dtype=torch.int32).pin_memory()
+    h_topos = [torch.empty(2 * B * T + B, dtype=torch.int32).pin_memory() for _ in range(2)]
+
+    def host_merge(h):
+        merge_batch(merge_in, T, max_nodes=T, out=(h[: B * T].view(B, T), h[B * T: 2 * B * T].view(B, T),
+                                                   None, h[2 * B * T:]))
+    for h in h_topos:
+        host_merge(h)
+        assert np.array_equal(h[: B * T].numpy().reshape(B, T), batch.tokens)
+        assert np.array_equal(h[2 * B * T:].numpy(), batch.n_nodes)
+    t_m = time.perf_counter()
+    for _ in range(50):
+        host_merge(h_topos[1])
+    merge_us = (time.perf_counter() - t_m) / 50 * 1e6
+    h_topo = h_topos[0]
     h2d = (h_q.numel() * 2 + h_k.numel() * 2 + h_v.numel() * 2 + h_topo.numel() * 4)
     sets = []
     for _ in range(2):
@@ -409,14 +426,18 @@ def main():
         e2e_graphs.append(g_)
     cur = torch.cuda.current_stream()
 
-    def issue_copy(i):
+    def issue_copy(i, merge=True):
         st = sets[i % 2]
+        h = h_topos[i % 2]
+        if merge:   # host buffer i%2 was last read by step i-2's copy
+            ev_copied[i % 2].synchronize()
+            host_merge(h)
         with torch.cuda.stream(copy_stream):
             copy_stream.wait_event(ev_free[i % 2])
             st[0].copy_(h_q, non_blocking=True)
             st[1].copy_(h_k, non_blocking=True)
             st[2].copy_(h_v, non_blocking=True)
-            st[6].copy_(h_topo, non_blocking=True)
+            st[6].copy_(h, non_blocking=True)
             ev_copied[i % 2].record(copy_stream)
 
     def issue_compute(i):
@@ -447,11 +468,24 @@ def main():
         return got
 
     e2e_run(4)
+    # the copies alone, event-timed on the copy stream: explains e2e (PCIe-bound)
     barrier()
-    w0 = time.perf_counter()
-    e2e_run(args.steps)
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(copy_stream)
+    for i in range(10):
+        issue_copy(i, merge=False)
+    c1.record(copy_stream)
     barrier()
-    e2e_ms = (time.perf_counter() - w0) * 1e3
+    h2d_gbs = h2d * 10 / (c0.elapsed_time(c1) / 1e3) / 1e9
+    # three windows of K end-to-end steps; the median window is reported
+    windows = []
+    for _ in range(3):
+        barrier()
+        w0 = time.perf_counter()
+        e2e_run(args.steps)
+        barrier()
+        windows.append((time.perf_counter() - w0) * 1e3)
+    e2e_ms = statistics.median(windows)
     if world > 1:
         tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -504,8 +538,8 @@ def main():
                    "parallelism": f"dp{world} (requests partitioned)",
                    "l2": "inputs larger than L2: 268 MB KV + 65.5 MB logits per step",
                    "timing": "value: K replays of one CUDA graph holding the whole step; "
-                             "roofline: CUDA events around K1 (+ combine) in K more steps "
-                             "replayed as pre / K1 / post graphs",
+                             "roofline: K more steps of the same graph with timing events "
+                             "(graph nodes) around K1 + its combine, read after each step",
                    "k1_path": "tcgen05" if path == 2 else "cuda-core"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
@@ -515,8 +549,14 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
+                "windows_ms_per_step": [w / args.steps for w in windows],
+                "h2d_gbs_copies_alone": h2d_gbs,
                 "h2d_gbs_implied": h2d / (e2e_ms / args.steps / 1e3) / 1e9,
-                "host_numa_cpus": numa_cpus},
+                "host_numa_cpus": numa_cpus,
+                "host_tree_merge_us_per_step": merge_us,
+                "note": "per step: host merge_sequences of all B trees on the thread pool into "
+                        "pinned memory + H2D, pipelined against the previous step's compute; "
+                        "bound by PCIe H2D"},
         "gpu_launches": LAUNCHES_PER_STEP * args.steps,
         "clocks": clk,
         "verified_tokens_per_step": accepted,

@@ -169,6 +169,19 @@ st_status st_verify_mss(const float* logits, const float* q, int B, int T, int V
 st_status st_tree_merge(const int32_t* flat, const int32_t* lens, int nseq, int max_nodes,
                         int32_t* tok, int32_t* parent, int32_t* depth, int cap, int* n_out);
 
+/* Batched host tree pipeline: merge_sequences for B
+ * requests on a persistent host thread pool (n_threads <= 0: all hardware
+ * threads), packed into padded [B][T] tok / parent / depth (depth may be
+ * NULL) and n_nodes[B]; rows past a tree's size are filled with token 0,
+ * parent -1, depth 0. Request b's sequences are the next nseq[b] entries of
+ * lens[], their tokens the next sum(lens) entries of flat[]. Per-request
+ * status (same codes as st_tree_merge) into status[B] when non-NULL; returns
+ * the first non-OK status. A failed request gets n_nodes = 0. Host-only. */
+st_status st_tree_merge_batch(int B, const int32_t* flat, const int32_t* lens,
+                              const int32_t* nseq, int max_nodes, int T, int32_t* tok,
+                              int32_t* parent, int32_t* depth, int32_t* n_nodes,
+                              int32_t* status, int n_threads);
+
 /* ------------------------------------------------- device decoder model ---
  * The reference's pre-LN decoder (proj/include/spectree/transformer.hpp:18-57)
  * resident on the device in f16/bf16 for the full-stack path (C3): weights are

@@ -67,6 +67,7 @@ SIGNATURES = {
     "st_model_workspace_size": (_Z, [_V, _I, _I]),
     "st_model_tree_forward": (_I, [_V, _I, _I, _V, _V, _V, _I, _V, _V, _V, _V, _I64, _V, _V, _Z, _V]),
     "st_tree_merge": (_I, [_V, _V, _I, _I, _V, _V, _V, _I, C.POINTER(_I)]),
+    "st_tree_merge_batch": (_I, [_I, _V, _V, _V, _I, _I, _V, _V, _V, _V, _V, _I]),
 }
 
 

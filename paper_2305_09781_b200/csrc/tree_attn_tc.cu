@@ -711,12 +711,6 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 }
 
 // Merge of the partial pieces of pairs that the stream-K schedule split over
-// several CTAs. One block per (b, h) pair: the schedule arithmetic is done
-// once per block (unsplit pairs exit at once); then warp w handles rows
-// w, w+4, ...; lane l owns d columns [4l, 4l+4). All loads of a row (every
-// piece's m, l and O float4) are issued before any use, so a row costs one
-// L2 round trip. Fixed piece order -> deterministic.
-// Merge of the partial pieces of pairs that the stream-K schedule split over
 // several CTAs. Block c handles the pair that starts in CTA c's range and
 // continues past it (at most one per CTA), read from the schedule table the
 // attention kernel published: its pieces are CTA c's last segment (slot 0 if

@@ -6,7 +6,8 @@
   (csrc/host/token_tree.cpp) through ``st_tree_merge``.
 * ``verify`` runs the K3 walk on the GPU through ``st_verify_outputs``.
 * ``TreeBatch`` packs several trees into the device layout
-  (include/spectree_capi.h) for the batched kernels.
+  (include/spectree_capi.h) for the batched kernels; ``merge_batch`` merges
+  and packs a whole batch on the host thread pool (``st_tree_merge_batch``).
 """
 from __future__ import annotations
 
@@ -147,3 +148,47 @@ class TreeBatch:
             k = t.size
             self.tokens[b, :k], self.parents[b, :k], self.depths[b, :k] = t.tokens, t.parents, t.depths
             self.n_nodes[b] = k
+
+
+class MergeInputs:
+    """Flattened candidate sequences of a batch (request b's sequences are the
+    next nseq[b] entries of lens, their tokens the next sum(lens) of flat) —
+    the argument layout of st_tree_merge_batch."""
+
+    def __init__(self, batch_sequences):
+        seqs = [[list(map(int, s)) for s in req] for req in batch_sequences]
+        self.B = len(seqs)
+        self.nseq = np.array([len(r) for r in seqs], np.int32)
+        self.lens = np.array([len(s) for r in seqs for s in r] or [0], np.int32)
+        self.flat = np.array([t for r in seqs for s in r for t in s] or [0], np.int32)
+
+
+def merge_batch(batch_sequences, T: int, max_nodes: int = 64, out=None, n_threads: int = 0,
+                raise_on_error: bool = True):
+    """TokenTree.merge_sequences for every request of a batch on the host
+    thread pool, packed into padded [B][T] arrays. ``out`` may be a tuple of
+    preallocated (tok, parent, depth, n_nodes) arrays — numpy, or pinned torch
+    CPU tensors so a single H2D copy follows. Returns (tok, parent, depth,
+    n_nodes, status)."""
+    mi = batch_sequences if isinstance(batch_sequences, MergeInputs) else MergeInputs(batch_sequences)
+    B = mi.B
+    if out is None:
+        out = (np.zeros((B, T), np.int32), np.zeros((B, T), np.int32), np.zeros((B, T), np.int32),
+               np.zeros(B, np.int32))
+    tok, par, dep, n = out
+    status = np.zeros(max(B, 1), np.int32)
+
+    def ptr(a):
+        if isinstance(a, np.ndarray):
+            assert a.dtype == np.int32 and a.flags.c_contiguous
+            return a.ctypes.data_as(C.c_void_p)
+        assert a.dtype.__str__() == "torch.int32" and a.is_contiguous() and a.device.type == "cpu"
+        return C.c_void_p(a.data_ptr())
+
+    st = lib().st_tree_merge_batch(B, ptr(mi.flat), ptr(mi.lens), ptr(mi.nseq), int(max_nodes), int(T),
+                                   ptr(tok), ptr(par), None if dep is None else ptr(dep), ptr(n),
+                                   ptr(status), int(n_threads))
+    if st != 0 and raise_on_error:
+        bad = int(np.nonzero(status[:B])[0][0])
+        raise SpectreeError(int(status[bad]), f"merge_batch: request {bad}")
+    return tok, par, dep, n, status[:B]
