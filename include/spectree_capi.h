@@ -160,6 +160,31 @@ st_status st_verify_mss(const float* logits, const float* q, int B, int T, int V
                         float temperature, const float* uniforms, int n_uniforms,
                         int32_t* verified, int32_t* ids, int32_t* len, void* stream);
 
+/* ---------------------------------------- head-sharded K1 (C4, §8(e)) ---
+ * K1 over this rank's H heads (heads [rank*H, (rank+1)*H) of world*H) with
+ * the all-gather fused into the epilogue: every output row (b, u, local head
+ * h) is stored straight into each rank's full-head buffer out[k]
+ * ([B][T][world*H][D], k = 0..world-1, peer-mapped device pointers such as
+ * symmetric-memory buffers) at head rank*H + h — over NVLink, overlapped with
+ * the attention kernel — instead of an NCCL all-gather + relayout afterwards.
+ * a->o is ignored; a->lse (local heads) is still written when non-NULL.
+ * Completion is published with st_peer_signal and consumed with
+ * st_peer_wait. Needs the tcgen05 path. */
+typedef struct {
+    int world, rank;
+    void* const* out;   /* DEVICE array [world] of device pointers */
+} st_peer_out;
+st_status st_tree_attention_allgather(const st_attn_args* a, const st_peer_out* po, void* stream);
+
+/* Stream-ordered after this rank's peer writes: a system-scope release store
+ * of `epoch` into slot `rank` of every rank's signal array (signals: DEVICE
+ * array [world] of peer-mapped uint32_t[world]). */
+st_status st_peer_signal(uint32_t* const* signals, int world, int rank, uint32_t epoch,
+                         void* stream);
+/* Holds the stream until every slot of this rank's signal array has reached
+ * `epoch` (wrap-around compare); traps after ~10 s instead of hanging. */
+st_status st_peer_wait(const uint32_t* my_signals, int world, uint32_t epoch, void* stream);
+
 /* ------------------------------------------------------------ host tree ---
  * TokenTree::merge_sequences of the host C++ library (drop-in for reference
  * token_tree.cpp:42-102): sequences given flattened (flat, lens[nseq]);

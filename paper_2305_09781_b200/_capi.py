@@ -32,6 +32,10 @@ class SpectreeError(RuntimeError):
         super().__init__(f"[{self.code}] {msg}")
 
 
+class PeerOut(C.Structure):
+    _fields_ = [("world", C.c_int), ("rank", C.c_int), ("out", C.c_void_p)]
+
+
 class AttnArgs(C.Structure):
     _fields_ = [("dtype", C.c_int), ("B", C.c_int), ("T", C.c_int), ("H", C.c_int),
                 ("Hkv", C.c_int), ("D", C.c_int), ("W", C.c_int), ("Lmax", C.c_int64),
@@ -68,6 +72,9 @@ SIGNATURES = {
     "st_model_tree_forward": (_I, [_V, _I, _I, _V, _V, _V, _I, _V, _V, _V, _V, _I64, _V, _V, _Z, _V]),
     "st_tree_merge": (_I, [_V, _V, _I, _I, _V, _V, _V, _I, C.POINTER(_I)]),
     "st_tree_merge_batch": (_I, [_I, _V, _V, _V, _I, _I, _V, _V, _V, _V, _V, _I]),
+    "st_tree_attention_allgather": (_I, [C.POINTER(AttnArgs), C.POINTER(PeerOut), _V]),
+    "st_peer_signal": (_I, [_V, _I, _I, C.c_uint32, _V]),
+    "st_peer_wait": (_I, [_V, _I, C.c_uint32, _V]),
 }
 
 
@@ -111,7 +118,7 @@ def attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, lse=None, sca
     a.B, a.T, a.H, a.Hkv, a.D, a.W, a.Lmax = B, T, H, Hkv, D, mask.shape[-1], Lmax
     a.q, a.k_cache, a.v_cache = q.data_ptr(), k_cache.data_ptr(), v_cache.data_ptr()
     a.mask, a.prefix_len, a.n_nodes = mask.data_ptr(), prefix_len.data_ptr(), n_nodes.data_ptr()
-    a.o = out.data_ptr()
+    a.o = out.data_ptr() if out is not None else None
     a.lse = lse.data_ptr() if lse is not None else None
     a.scale = float(scale if scale is not None else D ** -0.5)
     a.workspace = workspace.data_ptr() if workspace is not None else None
@@ -146,6 +153,33 @@ def tree_attention(q, k_cache, v_cache, mask, prefix_len, n_nodes, out=None, lse
                   force_path)
     check(lib().st_tree_attention(C.byref(a), _stream(stream)))
     return out
+
+
+def tree_attention_allgather(q, k_cache, v_cache, mask, prefix_len, n_nodes, out_ptrs, world,
+                             rank, lse=None, scale=None, workspace=None, stream=None):
+    """Head-sharded K1 with the all-gather fused into the epilogue
+    (st_tree_attention_allgather): this rank's heads q [B,T,H,D] are written
+    into every rank's [B,T,world*H,D] buffer; out_ptrs is a device int64
+    tensor [world] of (peer-mapped) buffer addresses."""
+    assert out_ptrs.dtype == torch.int64 and out_ptrs.is_cuda and out_ptrs.numel() == world
+    if workspace is None:
+        workspace = tree_attention_workspace(q, k_cache, v_cache, mask, prefix_len, n_nodes)
+    a = attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, None, lse, scale, workspace, 0)
+    po = PeerOut(int(world), int(rank), out_ptrs.data_ptr())
+    check(lib().st_tree_attention_allgather(C.byref(a), C.byref(po), _stream(stream)))
+
+
+def peer_signal(signal_ptrs, world, rank, epoch, stream=None):
+    """Publish `epoch` into slot `rank` of every rank's signal array
+    (signal_ptrs: device int64 tensor [world] of peer-mapped uint32[world])."""
+    check(lib().st_peer_signal(C.c_void_p(signal_ptrs.data_ptr()), int(world), int(rank),
+                               int(epoch) & 0xFFFFFFFF, _stream(stream)))
+
+
+def peer_wait(my_signals, world, epoch, stream=None):
+    """Hold the stream until every slot of my_signals (int32 [world]) reached epoch."""
+    check(lib().st_peer_wait(_ptr(my_signals), int(world), int(epoch) & 0xFFFFFFFF,
+                             _stream(stream)))
 
 
 # ------------------------------------------------------------------ K2 ----

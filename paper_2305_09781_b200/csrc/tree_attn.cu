@@ -67,4 +67,27 @@ st_status st_tree_attention(const st_attn_args* a, void* stream) {
     return st::tree_attention_cc(a, st::as_stream(stream));
 }
 
+st_status st_tree_attention_allgather(const st_attn_args* a, const st_peer_out* po,
+                                      void* stream) {
+    if (st_status e = st::require_device()) return e;
+    if (st_status e = validate(a)) return e;
+    ST_CHECK_ARG(po && po->out && po->world >= 1 && po->rank >= 0 && po->rank < po->world,
+                 ST_ERR_INVALID_ARGUMENT, "bad st_peer_out");
+    ST_CHECK_ARG(a->B == 0 || (a->q && a->k_cache && a->v_cache && a->mask && a->prefix_len &&
+                               a->n_nodes),
+                 ST_ERR_INVALID_ARGUMENT, "null tensor pointer");
+    if (a->B == 0) return ST_OK;
+    if (choose_path(a) != 2 || !st::tree_attention_tc_supported(a)) {
+        st::set_error("st_tree_attention_allgather: needs the tcgen05 path (f16/bf16, D == 128, "
+                      "(H/Hkv)*T >= 16)");
+        return ST_ERR_UNSUPPORTED;
+    }
+    const size_t need = st::tree_attention_tc_workspace(a);
+    if (a->workspace_bytes < need || (need && !a->workspace)) {
+        st::set_error("st_tree_attention_allgather: workspace too small");
+        return ST_ERR_INVALID_ARGUMENT;
+    }
+    return st::tree_attention_tc(a, st::as_stream(stream), po);
+}
+
 }  // extern "C"

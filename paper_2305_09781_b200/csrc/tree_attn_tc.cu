@@ -97,6 +97,10 @@ struct TcParams {
     float scale;
     unsigned long long* trace;  // optional pipeline trace of CTA 0 (ST_K1_TRACE)
     int aligned_slack;          // whole-pair schedule allowed within this many tiles of stream-K
+    // head-sharded output (st_tree_attention_allgather): rows go to every rank's
+    // [B][T][H_out][D] buffer at head head_offset + h; null -> o with H_out = H
+    void* const* o_peers;
+    int world, head_offset, H_out;
 };
 
 constexpr int kTraceCta = 12;  // per-CTA globaltimer/clock slots of the ST_K1_TRACE dump
@@ -653,7 +657,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             const int slot = (t == t_begin) ? 0 : 1;
             float* sp = p.partial + ((long long)blockIdx.x * 2 + slot) * SLOT_FLOATS;
             const int d0 = half * DCOLS;
-            T* out_row = reinterpret_cast<T*>(p.o) + (((long long)s.b * p.T + r) * p.H + s.h) * HD + d0;
+            const long long orow = (((long long)s.b * p.T + r) * p.H_out + p.head_offset + s.h) * HD + d0;
             const uint32_t q1 = pc - 1;
             mbar_wait(pv_done + (q1 & 1), (q1 >> 1) & 1);
             if (threadIdx.x == 0) K1_GT(3);
@@ -674,7 +678,12 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 mbar_arrive(o_empty);
                 if (valid) {
                     if (full) {
-                        store_row<T, DCOLS>(out_row, ov, 1.f / l_row);
+                        if (p.o_peers) {  // fused all-gather: this row into every rank's buffer
+                            for (int k = 0; k < p.world; ++k)
+                                store_row<T, DCOLS>(reinterpret_cast<T*>(p.o_peers[k]) + orow, ov, 1.f / l_row);
+                        } else {
+                            store_row<T, DCOLS>(reinterpret_cast<T*>(p.o) + orow, ov, 1.f / l_row);
+                        }
                         if (p.lse && half == 0)
                             p.lse[((long long)s.b * p.H + s.h) * p.T + r] = m * p.scale + __logf(l_row);
                     } else {
@@ -805,9 +814,15 @@ combine_kernel(const TcParams p, int G) {
                 M_ = Mn;
             }
             const float inv = 1.f / L;
-            T* out = reinterpret_cast<T*>(p.o) + (((long long)b * p.T + r) * p.H + h) * HD + 4 * lane;
-            *reinterpret_cast<uint2*>(out) =
+            const long long orow = (((long long)b * p.T + r) * p.H_out + p.head_offset + h) * HD + 4 * lane;
+            const uint2 val =
                 make_uint2(pk2<T>::pack(acc.x * inv, acc.y * inv), pk2<T>::pack(acc.z * inv, acc.w * inv));
+            if (p.o_peers) {
+                for (int k = 0; k < p.world; ++k)
+                    *reinterpret_cast<uint2*>(reinterpret_cast<T*>(p.o_peers[k]) + orow) = val;
+            } else {
+                *reinterpret_cast<uint2*>(reinterpret_cast<T*>(p.o) + orow) = val;
+            }
             if (p.lse && lane == 0) p.lse[((long long)b * p.H + h) * p.T + r] = M_ * p.scale + __logf(L);
         }
     }
@@ -880,7 +895,7 @@ size_t tree_attention_tc_workspace(const st_attn_args* a) {
         ST_CUDA_TRY(launch_pdl(combine_kernel<TT>, dim3(G), dim3(256), 0, stream, prm, G));     \
     } while (0)
 
-st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
+st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st_peer_out* po) {
     const CUtensorMapDataType dt =
         a->dtype == ST_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     CUtensorMap tq, tk, tv;
@@ -919,6 +934,10 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream) {
     prm.W = a->W;
     prm.scale = (float)a->scale;
     prm.c_log2 = (float)(a->scale * 1.4426950408889634);
+    prm.o_peers = po ? po->out : nullptr;
+    prm.world = po ? po->world : 1;
+    prm.head_offset = po ? po->rank * a->H : 0;
+    prm.H_out = po ? po->world * a->H : a->H;
     prm.trace = nullptr;
     // diagnostic override of the whole-pair schedule threshold (ST_K1_SLACK=-1: always stream-K)
     static const int slack_env = getenv("ST_K1_SLACK") ? atoi(getenv("ST_K1_SLACK")) : (int)kAlignedSlack;

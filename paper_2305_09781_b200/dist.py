@@ -68,3 +68,64 @@ def gather_head_outputs(o_local: torch.Tensor, world: int, gathered: torch.Tenso
     else:
         gathered[0].copy_(o_local)
     return _capi.heads_gather_layout(gathered, world, out=out)
+
+
+class PeerHeadGather:
+    """Head-sharded attention with the all-gather fused into K1 (C4).
+
+    Every rank owns one symmetric-memory allocation holding two full-head
+    output slots [2][B, T, world*Hl, D] and two signal arrays uint32[2][world].
+    ``attention`` runs K1 over this rank's heads with st_tree_attention_allgather
+    (its epilogue stores each output row into every rank's slot over NVLink)
+    and then publishes the call's epoch with st_peer_signal; ``wait`` holds the
+    stream until every rank's epoch has arrived and returns the gathered
+    [B, T, world*Hl, D] slot. Slots alternate by epoch: a rank that has
+    received epoch e from every peer knows each peer has finished reading slot
+    (e-1)%2, so rank r's epoch e+1 writes into it are safe.
+
+    ``buffers`` / ``signals`` (lists of per-"rank" tensors on one device) make
+    a single-process simulation of ``world`` ranks possible for tests.
+    """
+
+    def __init__(self, B, T, Hl, D, dtype, device, world, rank, group=None,
+                 buffers=None, signals=None):
+        self.world, self.rank, self.epoch = world, rank, 0
+        shape = (2, B, T, world * Hl, D)
+        esz = torch.empty((), dtype=dtype).element_size()
+        obytes = 2 * B * T * world * Hl * D * esz
+        if buffers is None:
+            import torch.distributed._symmetric_memory as symm
+            raw = symm.empty(obytes + 2 * world * 4, dtype=torch.uint8, device=device)
+            raw[obytes:].zero_()
+            hdl = symm.rendezvous(raw, group or dist.group.WORLD)
+            bases = list(hdl.buffer_ptrs)
+            self.out = raw[:obytes].view(dtype).view(shape)
+            self.signal = raw[obytes:].view(torch.int32).view(2, world)
+            out_bases, sig_bases = bases, [b + obytes for b in bases]
+            dist.barrier(group)   # every signal array is zeroed before anyone signals
+        else:
+            self.out = buffers[rank].view(shape)
+            self.signal = signals[rank].view(2, world)
+            out_bases = [t.data_ptr() for t in buffers]
+            sig_bases = [t.data_ptr() for t in signals]
+        slot = B * T * world * Hl * D * esz
+        self._out_ptrs = [torch.tensor([b + s * slot for b in out_bases], dtype=torch.int64,
+                                       device=device) for s in range(2)]
+        self._sig_ptrs = [torch.tensor([b + s * world * 4 for b in sig_bases], dtype=torch.int64,
+                                       device=device) for s in range(2)]
+
+    def attention(self, q, k_cache, v_cache, mask, prefix_len, n_nodes, workspace=None,
+                  stream=None):
+        from . import _capi
+        self.epoch += 1
+        s = self.epoch % 2
+        _capi.tree_attention_allgather(q, k_cache, v_cache, mask, prefix_len, n_nodes,
+                                       self._out_ptrs[s], self.world, self.rank,
+                                       workspace=workspace, stream=stream)
+        _capi.peer_signal(self._sig_ptrs[s], self.world, self.rank, self.epoch, stream=stream)
+
+    def wait(self, stream=None):
+        from . import _capi
+        s = self.epoch % 2
+        _capi.peer_wait(self.signal[s], self.world, self.epoch, stream=stream)
+        return self.out[s]

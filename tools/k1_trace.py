@@ -1,5 +1,6 @@
-"""Diagnostic: run K1 at the C2 shape with ST_K1_TRACE set and print CTA 0's
-per-tile pipeline timeline (cycles relative to the first K load)."""
+"""Diagnostic: run K1 (default: the C2 shape; --B/--T/--H/--L to change) with
+ST_K1_TRACE set and print CTA 0's per-tile pipeline timeline (cycles relative
+to the first K load) and per-CTA globaltimer summaries."""
 import os
 import sys
 
@@ -7,13 +8,22 @@ import numpy as np
 import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/k1_trace.txt"
+import argparse
+
+ap = argparse.ArgumentParser()
+ap.add_argument("out", nargs="?", default="gpurun_out/k1_trace.txt")
+ap.add_argument("--B", type=int, default=8)
+ap.add_argument("--T", type=int, default=64)
+ap.add_argument("--H", type=int, default=32)
+ap.add_argument("--L", type=int, default=2048)
+args = ap.parse_args()
+out = args.out
 os.environ["ST_K1_TRACE"] = out
 if os.path.exists(out):
     os.remove(out)
 from paper_2305_09781_b200 import _capi  # noqa: E402
 
-B, T, H, D, L = 8, 64, 32, 128, 2048
+B, T, H, D, L = args.B, args.T, args.H, 128, args.L
 dev = "cuda"
 q = torch.randn(B, T, H, D, device=dev).half()
 kc = torch.randn(B, H, L + T, D, device=dev).half()
