@@ -127,6 +127,25 @@ st_status gemm(st_model* m, const void* A, size_t w_off, void* C, cudaDataType_t
     return ST_OK;
 }
 
+// `batch` GEMMs sharing the activation A: C_i = A W_i, W_i at w_off + i*w_stride
+// elements, C_i at C + i*c_stride elements (one launch for Q/K/V).
+st_status gemm_shared_a(st_model* m, const void* A, size_t w_off, size_t w_stride, void* C,
+                        long long c_stride, int batch, int M, int N, int K, cudaStream_t s) {
+    const float alpha = 1.f, beta = 0.f;
+    const size_t es = dtype_size(m->dtype);
+    const void* W = static_cast<const char*>(m->buf) + w_off * es;
+    cublasSetStream(m->blas, s);
+    const cublasStatus_t st = cublasGemmStridedBatchedEx(
+        m->blas, CUBLAS_OP_N, CUBLAS_OP_N, N, M, K, &alpha, W, cuda_type(m->dtype), N,
+        (long long)w_stride, A, cuda_type(m->dtype), K, 0, &beta, C, cuda_type(m->dtype), N,
+        c_stride, batch, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+    if (st != CUBLAS_STATUS_SUCCESS) {
+        set_error("cublasGemmStridedBatchedEx failed: status " + std::to_string((int)st));
+        return ST_ERR_CUDA;
+    }
+    return ST_OK;
+}
+
 template <class T>
 const T* wptr(const st_model* m, size_t off) {
     return static_cast<const T*>(m->buf) + off;
@@ -292,9 +311,18 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
         ST_M_DISPATCH(st::layernorm_kernel<T><<<rows, 256, 0, s>>>(
             (const T*)x, st::wptr<T>(m, L.ln1_g), st::wptr<T>(m, L.ln1_b), d, (T*)h));
         ST_LAUNCH_CHECK();
-        if (st_status e = st::gemm(m, h, L.wq, q, ht, rows, d, d, false, s)) return e;
-        if (st_status e = st::gemm(m, h, L.wk, kn, ht, rows, d, d, false, s)) return e;
-        if (st_status e = st::gemm(m, h, L.wv, vn, ht, rows, d, d, false, s)) return e;
+        const size_t dd = (size_t)d * d;
+        const long long qkv_stride = (static_cast<char*>(kn) - static_cast<char*>(q)) / (long long)es;
+        if (L.wk == L.wq + dd && L.wv == L.wk + dd &&
+            static_cast<char*>(vn) - static_cast<char*>(kn) == qkv_stride * (long long)es) {
+            // wq|wk|wv are consecutive in the serialized order: one batched launch
+            if (st_status e = st::gemm_shared_a(m, h, L.wq, dd, q, qkv_stride, 3, rows, d, d, s))
+                return e;
+        } else {
+            if (st_status e = st::gemm(m, h, L.wq, q, ht, rows, d, d, false, s)) return e;
+            if (st_status e = st::gemm(m, h, L.wk, kn, ht, rows, d, d, false, s)) return e;
+            if (st_status e = st::gemm(m, h, L.wv, vn, ht, rows, d, d, false, s)) return e;
+        }
         if (st_status e = st_kv_append(m->dtype, B, T, H, Dh, Lmax, kn, vn, prefix_len, n_nodes, kc,
                                        vc, stream))
             return e;

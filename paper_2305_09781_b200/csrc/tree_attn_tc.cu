@@ -724,14 +724,20 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 // continues past it (at most one per CTA), read from the schedule table the
 // attention kernel published: its pieces are CTA c's last segment (slot 0 if
 // that segment is c's whole range, else slot 1) and the first segment (slot 0)
-// of each following non-empty CTA until the pair ends. Warp w merges rows w,
-// w+8, ...; lane l owns d columns [4l, 4l+4); all loads of a row group are
-// issued before use. Fixed piece order -> deterministic.
+// of each following non-empty CTA until the pair ends. Warp 0 gathers that
+// piece list once (32 table entries per ballot) into shared memory; then warp
+// w merges rows w, w+8, ... (RPW rows at a time, lane l owning d columns
+// [4l, 4l+4)) over the pieces in chunks of CHUNK, every load of a chunk in
+// flight together, with an online (m, l, O) merge across chunks. Fixed piece
+// order -> deterministic.
 template <class T>
 __global__ void __launch_bounds__(256, 1)
 combine_kernel(const TcParams p, int G) {
-    constexpr int MAXP = 2;   // pieces held in registers; more are merged online
-    constexpr int RPW = 8;    // rows per warp in flight together (8 warps x 8 = 64 rows/pass)
+    constexpr int CHUNK = 4;      // pieces loaded together
+    constexpr int RPW = 4;        // rows per warp in flight together
+    constexpr int MAXPIECES = 256;
+    __shared__ int s_slots[MAXPIECES];
+    __shared__ int s_np;
     const int cta = blockIdx.x;
     pdl_wait();  // the attention kernel's pieces and schedule table
     pdl_trigger();
@@ -742,88 +748,105 @@ combine_kernel(const TcParams p, int G) {
     const int bh = (int)__ldcg(tab + 4 * cta + 3);
     const int b = bh / p.H, h = bh % p.H;
     const long long pend = ps + nt;
-    // first MAXP pieces: this CTA's last segment, then the first segment of each
-    // following non-empty CTA; `next_cta` continues the list for the online tail
-    int slots[MAXP];
-    int np = 0;
-    slots[np++] = cta * 2 + (ps == rs ? 0 : 1);
-    int next_cta = cta + 1;
-    for (; next_cta < G && np < MAXP; ++next_cta) {
-        const long long r0 = __ldcg(tab + 4 * next_cta), r1 = __ldcg(tab + 4 * (next_cta + 1));
-        if (r0 >= pend) break;
-        if (r1 > r0) slots[np++] = next_cta * 2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0) {
+        int np = 0;
+        if (lane == 0) s_slots[0] = cta * 2 + (ps == rs ? 0 : 1);
+        np = 1;
+        for (int base = cta + 1; base < G && np < MAXPIECES; base += 32) {
+            const int cc = base + lane;
+            long long r0 = pend, r1 = pend;
+            if (cc < G) {
+                r0 = __ldcg(tab + 4 * cc);
+                r1 = __ldcg(tab + 4 * (cc + 1));
+            }
+            const bool inside = r0 < pend;
+            const unsigned have = __ballot_sync(0xffffffffu, inside && r1 > r0);
+            const unsigned past = __ballot_sync(0xffffffffu, !inside);
+            // CTAs before the first one past the pair's end, with non-empty ranges
+            const unsigned upto = past ? ((1u << __ffs(past) - 1) - 1u) : 0xffffffffu;
+            const unsigned take = have & upto;
+            if ((take >> lane) & 1u) {
+                const int at = np + __popc(take & ((1u << lane) - 1u));
+                if (at < MAXPIECES) s_slots[at] = cc * 2;
+            }
+            np += __popc(take);
+            if (past) break;
+        }
+        if (lane == 0) s_np = min(np, MAXPIECES);
     }
+    __syncthreads();
+    const int np = s_np;
     const int n = __ldg(p.n_nodes + b);
     const float c = p.c_log2;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nw = blockDim.x >> 5;
     for (int r0 = warp; r0 < n; r0 += nw * RPW) {
-        float mk[RPW][MAXP], lk[RPW][MAXP];
-        float4 ok[RPW][MAXP];
+        float M_[RPW], L[RPW];
+        float4 acc[RPW];
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
-            const int r = r0 + i * nw;
+            M_[i] = -INFINITY;
+            L[i] = 0.f;
+            acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (int k0 = 0; k0 < np; k0 += CHUNK) {
+            float mk[RPW][CHUNK], lk[RPW][CHUNK];
+            float4 ok[RPW][CHUNK];
 #pragma unroll
-            for (int k = 0; k < MAXP; ++k) {
-                if (k < np && r < n) {
-                    const float* piece = p.partial + (long long)slots[k] * SLOT_FLOATS;
-                    mk[i][k] = __ldcg(piece + 128 * HD + r);
-                    lk[i][k] = __ldcg(piece + 128 * HD + 128 + r);
-                    ok[i][k] = __ldcg(reinterpret_cast<const float4*>(piece + r * HD) + lane);
+            for (int i = 0; i < RPW; ++i) {
+                const int r = r0 + i * nw;
+#pragma unroll
+                for (int k = 0; k < CHUNK; ++k) {
+                    mk[i][k] = -INFINITY;
+                    if (k0 + k < np && r < n) {
+                        const float* piece = p.partial + (long long)s_slots[k0 + k] * SLOT_FLOATS;
+                        mk[i][k] = __ldcg(piece + 128 * HD + r);
+                        lk[i][k] = __ldcg(piece + 128 * HD + 128 + r);
+                        ok[i][k] = __ldcg(reinterpret_cast<const float4*>(piece + r * HD) + lane);
+                    }
                 }
+            }
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                float Mn = M_[i];
+#pragma unroll
+                for (int k = 0; k < CHUNK; ++k) Mn = fmaxf(Mn, mk[i][k]);
+                if (Mn == -INFINITY) continue;
+                const float sc0 = M_[i] == -INFINITY ? 0.f : ex2((M_[i] - Mn) * c);
+                L[i] *= sc0;
+                acc[i].x *= sc0;
+                acc[i].y *= sc0;
+                acc[i].z *= sc0;
+                acc[i].w *= sc0;
+#pragma unroll
+                for (int k = 0; k < CHUNK; ++k) {
+                    if (mk[i][k] != -INFINITY) {
+                        const float w = ex2((mk[i][k] - Mn) * c);
+                        L[i] += w * lk[i][k];
+                        acc[i].x += w * ok[i][k].x;
+                        acc[i].y += w * ok[i][k].y;
+                        acc[i].z += w * ok[i][k].z;
+                        acc[i].w += w * ok[i][k].w;
+                    }
+                }
+                M_[i] = Mn;
             }
         }
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
             const int r = r0 + i * nw;
             if (r >= n) break;
-            float M_ = -INFINITY;
-#pragma unroll
-            for (int k = 0; k < MAXP; ++k)
-                if (k < np) M_ = fmaxf(M_, mk[i][k]);
-            float L = 0.f;
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int k = 0; k < MAXP; ++k) {
-                if (k < np && mk[i][k] != -INFINITY) {
-                    const float w = ex2((mk[i][k] - M_) * c);
-                    L += w * lk[i][k];
-                    acc.x += w * ok[i][k].x;
-                    acc.y += w * ok[i][k].y;
-                    acc.z += w * ok[i][k].z;
-                    acc.w += w * ok[i][k].w;
-                }
-            }
-            // pairs spanning more than MAXP CTAs: online merge of the rest
-            for (int cc = next_cta; cc < G; ++cc) {
-                const long long q0 = __ldcg(tab + 4 * cc), q1 = __ldcg(tab + 4 * (cc + 1));
-                if (q0 >= pend) break;
-                if (q1 <= q0) continue;
-                const float* piece = p.partial + (long long)(cc * 2) * SLOT_FLOATS;
-                const float m2 = __ldcg(piece + 128 * HD + r);
-                if (m2 == -INFINITY) continue;
-                const float Mn = fmaxf(M_, m2);
-                const float sc0 = M_ == -INFINITY ? 0.f : ex2((M_ - Mn) * c);
-                const float w = ex2((m2 - Mn) * c);
-                const float4 o2 = __ldcg(reinterpret_cast<const float4*>(piece + r * HD) + lane);
-                L = L * sc0 + w * __ldcg(piece + 128 * HD + 128 + r);
-                acc.x = acc.x * sc0 + w * o2.x;
-                acc.y = acc.y * sc0 + w * o2.y;
-                acc.z = acc.z * sc0 + w * o2.z;
-                acc.w = acc.w * sc0 + w * o2.w;
-                M_ = Mn;
-            }
-            const float inv = 1.f / L;
+            const float inv = 1.f / L[i];
             const long long orow = (((long long)b * p.T + r) * p.H_out + p.head_offset + h) * HD + 4 * lane;
-            const uint2 val =
-                make_uint2(pk2<T>::pack(acc.x * inv, acc.y * inv), pk2<T>::pack(acc.z * inv, acc.w * inv));
+            const uint2 val = make_uint2(pk2<T>::pack(acc[i].x * inv, acc[i].y * inv),
+                                         pk2<T>::pack(acc[i].z * inv, acc[i].w * inv));
             if (p.o_peers) {
                 for (int k = 0; k < p.world; ++k)
                     *reinterpret_cast<uint2*>(reinterpret_cast<T*>(p.o_peers[k]) + orow) = val;
             } else {
                 *reinterpret_cast<uint2*>(reinterpret_cast<T*>(p.o) + orow) = val;
             }
-            if (p.lse && lane == 0) p.lse[((long long)b * p.H + h) * p.T + r] = M_ * p.scale + __logf(L);
+            if (p.lse && lane == 0) p.lse[((long long)b * p.H + h) * p.T + r] = M_[i] * p.scale + __logf(L[i]);
         }
     }
 }
