@@ -107,6 +107,135 @@ __global__ void gelu_kernel(T* __restrict__ x, int64_t n) {
     }
 }
 
+// 8 half-precision values <-> one 16-byte vector
+template <class T> __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
+    const T* h = reinterpret_cast<const T*>(&u);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) f[k] = to_acc<float>(h[k]);
+}
+template <class T> __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+    uint4 u;
+    T* h = reinterpret_cast<T*>(&u);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) h[k] = from_acc<T>(f[k]);
+    return u;
+}
+
+// LayerNorm with the row held in registers: 128 threads per row, 16-byte
+// accesses, the reference's two passes (mean, then variance of x - mean) as
+// two 4-warp reductions over registers (d % 8 == 0, d <= 8 * 128 * LN_MAXC).
+constexpr int LN_THREADS = 128, LN_MAXC = 8;
+__device__ __forceinline__ float ln_block_sum(float v, float* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5;
+    __syncthreads();  // red[] reuse across the two passes
+    if ((threadIdx.x & 31) == 0) red[w] = v;
+    __syncthreads();
+    return (red[0] + red[1]) + (red[2] + red[3]);
+}
+template <class T, int NC>
+__global__ void __launch_bounds__(LN_THREADS)
+layernorm_vec_kernel(const T* __restrict__ x, const T* __restrict__ g, const T* __restrict__ b,
+                     int d, T* __restrict__ out) {
+    __shared__ float red[LN_THREADS / 32];
+    const int nv = d >> 3;
+    const uint4* xr = reinterpret_cast<const uint4*>(x + (int64_t)blockIdx.x * d);
+    float v[NC][8];
+    uint4 gq[NC], bq[NC];   // gamma / beta chunks, loaded with the row (no extra round trip)
+    const uint4* gr = reinterpret_cast<const uint4*>(g);
+    const uint4* br = reinterpret_cast<const uint4*>(b);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const int j = c * LN_THREADS + threadIdx.x;
+        if (j < nv) {
+            gq[c] = __ldg(gr + j);
+            bq[c] = __ldg(br + j);
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const int j = c * LN_THREADS + threadIdx.x;
+        if (j < nv) {
+            unpack8<T>(xr[j], v[c]);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s += v[c][k];
+        }
+    }
+    const float mean = ln_block_sum(s, red) / d;
+    float q = 0.f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        if (c * LN_THREADS + (int)threadIdx.x < nv) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const float z = v[c][k] - mean;
+                q += z * z;
+            }
+        }
+    }
+    const float inv = rsqrtf(ln_block_sum(q, red) / d + 1e-5f);
+    uint4* orow = reinterpret_cast<uint4*>(out + (int64_t)blockIdx.x * d);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const int j = c * LN_THREADS + threadIdx.x;
+        if (j < nv) {
+            float gg[8], bb[8], o[8];
+            unpack8<T>(gq[c], gg);
+            unpack8<T>(bq[c], bb);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] = gg[k] * (v[c][k] - mean) * inv + bb[k];
+            orow[j] = pack8<T>(o);
+        }
+    }
+}
+
+// GELU (erf form, reference transformer.cpp:67): 0.5 v (1 + erf(v / sqrt 2)).
+// 1 + erf(x) via Abramowitz & Stegun 7.1.26 (|erf error| <= 1.5e-7, far below
+// the f16/bf16 output resolution), evaluated as erfc(|x|) = poly(t) e^{-x^2}
+// for x < 0 so the small values of the negative tail keep their relative
+// accuracy (no 1 - erf cancellation). Branch-free: 2 MUFU ops + 7 FMAs
+// instead of erff's branchy evaluation.
+__device__ __forceinline__ float gelu_f(float v) {
+    const float x = v * 0.70710678118654752f;
+    const float a = fabsf(x);
+    const float t = __frcp_rn(fmaf(0.3275911f, a, 1.f));
+    float y = fmaf(1.061405429f, t, -1.453152027f);
+    y = fmaf(y, t, 1.421413741f);
+    y = fmaf(y, t, -0.284496736f);
+    y = fmaf(y, t, 0.254829592f);
+    y *= t * __expf(-a * a);          // erfc(|x|)
+    const float one_plus_erf = x >= 0.f ? 2.f - y : y;
+    return 0.5f * v * one_plus_erf;
+}
+
+// GELU in place, 8 values per 16-byte access; each thread keeps GELU_ILP
+// independent loads in flight before its stores (in place, so the compiler
+// cannot hoist the next load over the previous store by itself).
+constexpr int GELU_ILP = 4;
+template <class T>
+__global__ void gelu_vec_kernel(uint4* __restrict__ x, int64_t n8) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n8;
+         i0 += stride * GELU_ILP) {
+        uint4 u[GELU_ILP];
+#pragma unroll
+        for (int r = 0; r < GELU_ILP; ++r)
+            if (i0 + r * stride < n8) u[r] = x[i0 + r * stride];
+#pragma unroll
+        for (int r = 0; r < GELU_ILP; ++r) {
+            if (i0 + r * stride < n8) {
+                float f[8];
+                unpack8<T>(u[r], f);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) f[k] = gelu_f(f[k]);
+                x[i0 + r * stride] = pack8<T>(f);
+            }
+        }
+    }
+}
+
 cudaDataType_t cuda_type(st_dtype t) { return t == ST_F16 ? CUDA_R_16F : CUDA_R_16BF; }
 
 // Row-major C[M][N] (+)= A[M][K] * W[K][N]  (column-major view: C^T = W^T A^T)
@@ -304,13 +433,30 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
                                                            st::wptr<T>(m, m->pos), tokens,
                                                            positions, d, (T*)x));
     ST_LAUNCH_CHECK();
+    auto aligned16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+    // LayerNorm of x into h: register-resident vector kernel when the shapes allow
+    auto layernorm = [&](size_t g_off, size_t b_off) -> st_status {
+        ST_M_DISPATCH(
+            const T* gp = st::wptr<T>(m, g_off); const T* bp = st::wptr<T>(m, b_off);
+            if (d % 8 == 0 && d <= 8 * st::LN_THREADS * st::LN_MAXC && aligned16(gp) &&
+                aligned16(bp) && aligned16(x) && aligned16(h)) {
+                const int nc = (d / 8 + st::LN_THREADS - 1) / st::LN_THREADS;
+                auto* kern = nc <= 1 ? st::layernorm_vec_kernel<T, 1>
+                             : nc <= 2 ? st::layernorm_vec_kernel<T, 2>
+                             : nc <= 4 ? st::layernorm_vec_kernel<T, 4>
+                                       : st::layernorm_vec_kernel<T, 8>;
+                kern<<<rows, st::LN_THREADS, 0, s>>>((const T*)x, gp, bp, d, (T*)h);
+            } else {
+                st::layernorm_kernel<T><<<rows, 256, 0, s>>>((const T*)x, gp, bp, d, (T*)h);
+            });
+        ST_LAUNCH_CHECK();
+        return ST_OK;
+    };
     for (int l = 0; l < c.num_layers; ++l) {
         const auto& L = m->layers[l];
         void* kc = static_cast<char*>(k_cache) + (size_t)l * layer_elems * es;
         void* vc = static_cast<char*>(v_cache) + (size_t)l * layer_elems * es;
-        ST_M_DISPATCH(st::layernorm_kernel<T><<<rows, 256, 0, s>>>(
-            (const T*)x, st::wptr<T>(m, L.ln1_g), st::wptr<T>(m, L.ln1_b), d, (T*)h));
-        ST_LAUNCH_CHECK();
+        if (st_status e = layernorm(L.ln1_g, L.ln1_b)) return e;
         const size_t dd = (size_t)d * d;
         const long long qkv_stride = (static_cast<char*>(kn) - static_cast<char*>(q)) / (long long)es;
         if (L.wk == L.wq + dd && L.wv == L.wk + dd &&
@@ -332,17 +478,18 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
         a.o = o;
         if (st_status e = st_tree_attention(&a, stream)) return e;
         if (st_status e = st::gemm(m, o, L.wo, x, ht, rows, d, d, true, s)) return e;
-        ST_M_DISPATCH(st::layernorm_kernel<T><<<rows, 256, 0, s>>>(
-            (const T*)x, st::wptr<T>(m, L.ln2_g), st::wptr<T>(m, L.ln2_b), d, (T*)h));
-        ST_LAUNCH_CHECK();
+        if (st_status e = layernorm(L.ln2_g, L.ln2_b)) return e;
         if (st_status e = st::gemm(m, h, L.w1, f, ht, rows, F, d, false, s)) return e;
-        ST_M_DISPATCH(st::gelu_kernel<T><<<148 * 8, 256, 0, s>>>((T*)f, (int64_t)rows * F));
+        const int64_t nf = (int64_t)rows * F;
+        if (nf % 8 == 0 && aligned16(f)) {
+            ST_M_DISPATCH(st::gelu_vec_kernel<T><<<148 * 8, 256, 0, s>>>((uint4*)f, nf / 8));
+        } else {
+            ST_M_DISPATCH(st::gelu_kernel<T><<<148 * 8, 256, 0, s>>>((T*)f, nf));
+        }
         ST_LAUNCH_CHECK();
         if (st_status e = st::gemm(m, f, L.w2, x, ht, rows, d, F, true, s)) return e;
     }
-    ST_M_DISPATCH(st::layernorm_kernel<T><<<rows, 256, 0, s>>>(
-        (const T*)x, st::wptr<T>(m, m->lnf_g), st::wptr<T>(m, m->lnf_b), d, (T*)h));
-    ST_LAUNCH_CHECK();
+    if (st_status e = layernorm(m->lnf_g, m->lnf_b)) return e;
 #undef ST_M_DISPATCH
     return st::gemm(m, h, m->wout, logits, CUDA_R_32F, rows, c.vocab_size, d, false, s);
 }

@@ -97,6 +97,7 @@ struct TcParams {
     float scale;
     unsigned long long* trace;  // optional pipeline trace of CTA 0 (ST_K1_TRACE)
     int aligned_slack;          // whole-pair schedule allowed within this many tiles of stream-K
+    int trace_cta;              // CTA whose per-tile pipeline is traced (ST_K1_TRACE_CTA)
     // head-sharded output (st_tree_attention_allgather): rows go to every rank's
     // [B][T][H_out][D] buffer at head head_offset + h; null -> o with H_out = H
     void* const* o_peers;
@@ -116,7 +117,7 @@ constexpr int kTraceCta = 12;  // per-CTA globaltimer/clock slots of the ST_K1_T
 
 #define K1_TRACE(slot, idx)                                                       \
     do {                                                                          \
-        if (p.trace && blockIdx.x == 0 && (idx) < 64)                             \
+        if (p.trace && blockIdx.x == p.trace_cta && (idx) < 64)                   \
             p.trace[(slot) * 64 + (idx)] = clock64();                             \
     } while (0)
 
@@ -965,6 +966,7 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
     // diagnostic override of the whole-pair schedule threshold (ST_K1_SLACK=-1: always stream-K)
     static const int slack_env = getenv("ST_K1_SLACK") ? atoi(getenv("ST_K1_SLACK")) : (int)kAlignedSlack;
     prm.aligned_slack = slack_env;
+    prm.trace_cta = getenv("ST_K1_TRACE_CTA") ? atoi(getenv("ST_K1_TRACE_CTA")) : 0;
     static unsigned long long* trace_buf = nullptr;
     if (getenv("ST_K1_TRACE")) {
         if (!trace_buf) cudaMalloc(&trace_buf, (12 * 64 + kTraceCta * 1024) * sizeof(unsigned long long));

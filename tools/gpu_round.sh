@@ -18,3 +18,6 @@ ls -la $OUT
 timeout 600 python tools/sweep_c5.py --out gpurun_out/$TAG.c5_sweep.json > gpurun_out/$TAG.c5_sweep.txt 2>&1
 timeout 900 python bench.py --config c3 --steps 5 --warmup 2 > $OUT/$TAG.c3.json 2> $OUT/$TAG.c3.err
 timeout 120 python tools/c4_slice.py --out $OUT/$TAG.c4.json > $OUT/$TAG.c4.txt 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/$TAG.c3launches.csv \
+    python bench.py --config c3 --steps 1 --warmup 1 > /dev/null 2> $OUT/$TAG.c3ncu.err
+timeout 120 python tools/k1_trace.py $OUT/$TAG.k1trace.raw > $OUT/$TAG.trace.txt 2>&1

@@ -43,7 +43,7 @@ t = np.array(rows, dtype=np.int64)
 t0 = t[0][t[0] > 0].min()
 names = ["K issue", "V issue", "S issue", "PV issue", "S ready", "P done", "K full(mma)", "V full(mma)", "S loaded", "masked+max", "pv wait done", "rescaled"]
 print("tile " + " ".join(f"{x:>12s}" for x in names))
-for i in range(30):
+for i in range(40):
     print(f"{i:4d} " + " ".join(f"{(t[r][i] - t0) if t[r][i] else -1:12d}" for r in range(12)))
 
 st, en, nt = cta[:, 0], cta[:, 1], cta[:, 2]

@@ -1,12 +1,13 @@
 """Summarise ncu outputs into committed profiles/.
 
-  python tools/profile_summary.py <tag> <launches.csv> <k1.ncu-rep> [bench.json]
+  python tools/profile_summary.py <tag> <launches.csv> <k1.ncu-rep> [bench.json] [c3launches.csv]
 
 Writes profiles/<tag>_launches.md (per-kernel mean device time and share of
 the step from the `--metrics gpu__time_duration.sum` launch list),
 profiles/<tag>_k1_ncu.md (key counters of the `--set full` capture of K1) and
 profiles/k1_traffic.json (DRAM bytes per K1 launch, read by bench.py for the
-roofline `traffic` field).
+roofline `traffic` field), and with a C3 launch list profiles/<tag>_c3_launches.md
+(per-kernel totals of the last full C3 step).
 """
 import csv
 import json
@@ -80,6 +81,36 @@ def to_bytes(v, u):
     return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
 
 
+def c3_step(path):
+    """Per-kernel totals of the last complete C3 forward (embed_kernel starts one)."""
+    rows = list(csv.reader(open(path)))
+    hdr = None
+    seq = []
+    for r in rows:
+        if "Kernel Name" in r:
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            if d.get("Metric Name") == "gpu__time_duration.sum":
+                v = float(d["Metric Value"].replace(",", ""))
+                v = v / 1e3 if d.get("Metric Unit", "ns") == "ns" else v
+                seq.append((int(d["ID"]), d["Kernel Name"], v))
+    seq.sort()
+    starts = [i for i, (_, k, _) in enumerate(seq) if "embed_kernel" in k]
+    last = seq[starts[-1]:] if starts else seq
+    agg = defaultdict(lambda: [0, 0.0])
+    for _, k, v in last:
+        agg[k.split("(")[0][:70]][0] += 1
+        agg[k.split("(")[0][:70]][1] += v
+    total = sum(v[1] for v in agg.values())
+    out = [f"Last full step: {len(last)} kernels, {total / 1e3:.2f} ms serialised.\n",
+           "| kernel | launches | total µs | share |", "|---|---|---|---|"]
+    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        out.append(f"| `{k}` | {n} | {t:.1f} | {t / total:.3f} |")
+    return "\n".join(out)
+
+
 def main():
     tag, lcsv, rep = sys.argv[1:4]
     bench = json.load(open(sys.argv[4])) if len(sys.argv) > 4 else None
@@ -110,6 +141,12 @@ def main():
         json.dump({"tag": tag, "dram_bytes_per_launch": traffic,
                    "source": f"profiles/{tag}_k1_ncu.md"},
                   open(os.path.join(PROF, "k1_traffic.json"), "w"), indent=1)
+    if len(sys.argv) > 5:
+        with open(os.path.join(PROF, f"{tag}_c3_launches.md"), "w") as f:
+            f.write(f"# {tag}: C3 full stack (bench.py --config c3), one step, ncu launch list\n\n")
+            f.write("`nvjet_*` are cuBLAS GEMMs (QKV batched, WO / W2 with the residual as beta=1, "
+                    "W1, LM head); `tree_attn_tc_kernel` is K1 per layer.\n\n")
+            f.write(c3_step(sys.argv[5]) + "\n")
     print("wrote", PROF)
 
 
