@@ -14,23 +14,26 @@
 //     or stream-K (equal tile counts per CTA; a pair cut by a range boundary
 //     leaves partial (O, m, l) pieces that combine_kernel — launched with PDL —
 //     merges in fixed order: deterministic, no atomics in any reduction).
-//   * Warp roles (224 threads): warps 0-3 softmax/epilogue, warp 4 TMA producer
-//     for Q and K, warp 5 TMA producer for V, warp 6 MMA issuer (one lane).
-//   * TMA (SWIZZLE_128B) streams K and V tiles [128 rows x 128 d]: K ring 2,
-//     V ring 3 (M=64) / 2 (M=128); Q (rows >= T zero-filled by TMA) double-
-//     buffered for M=64 so the next pair's Q is in smem before its first S.
-//   * S = Q K^T and O += P V on tcgen05 (kind::f16, fp32 accumulate in TMEM).
-//     M=128 (T <= 128): one N=128 MMA per K=16 step; each softmax thread owns a
-//     query row. M=64 (T <= 64): every product is split into two N=64 MMAs
-//     whose accumulators land in TMEM lanes 0-15 and 16-31 of each subpartition,
-//     so all 32 lanes of a softmax warp hold data (half a row each: half the
-//     MUFU work per thread).
+//   * Warp roles: SW softmax/epilogue warps (4 for M=64, 8 for M=128), then a
+//     TMA producer for Q and K, a TMA producer for V and the MMA issuer (the
+//     whole warp runs its loop; one elected lane issues inside the asm).
+//   * TMA (SWIZZLE_128B) streams K and V tiles [128 rows x 128 d] through
+//     3-stage rings; Q (rows >= T zero-filled by TMA) double-buffered for M=64
+//     so the next pair's Q is in smem before its first S.
+//   * S = Q K^T (SS MMA) and O += P V (TS MMA: P read from TMEM) on tcgen05
+//     (kind::f16, fp32 accumulate). M=64 (T <= 64): every product is split into
+//     two N=64 MMAs whose accumulators land in TMEM lanes 0-15 and 16-31 of
+//     each subpartition, so all 32 lanes of a softmax warp hold data (half a
+//     row each); the two halves share (m, l) and O. M=128 (T <= 128, "DUAL"):
+//     warps w and w+4 read the same TMEM lanes and own one column half each,
+//     with their own running (m, l) and their own O accumulator (O_a += P_a
+//     V[0:64], O_b += P_b V[64:128]) — no cross-warp traffic per tile; the
+//     halves merge once per segment in the epilogue.
 //   * Softmax: tcgen05.ld of S (double-buffered in TMEM), the tree mask applied
 //     only on tiles that reach the tree rows (one 32-bit visibility word per 32
 //     columns), ex2 with lazy rescaling (the running max moves only when it
-//     grows by > 2^8; O is then rescaled in TMEM), P staged in registers and
-//     stored (f16/bf16) to a double-buffered smem tile in the UMMA K-major
-//     SW128 layout; V read MN-major by the P.V MMA.
+//     grows by > 2^8; O is then rescaled in TMEM), P written (f16/bf16) back
+//     into TMEM over the tile's own S columns; V read MN-major by the P.V MMA.
 //   * Masked rows are exact zeros in P, so they contribute +0 (reference
 //     transformer.hpp:13-16) and outputs do not depend on non-ancestor rows.
 #include <cuda.h>
@@ -56,7 +59,6 @@ constexpr int BN = 128;            // KV rows per tile
 constexpr int HD = 128;            // head dim
 constexpr uint32_t KV_ATOM = 128 * 128;             // 128 rows x 64 elems x 2 B
 constexpr uint32_t TILE_BYTES = 2 * KV_ATOM;        // 32 KB K or V tile
-constexpr int NUM_THREADS = 224;                     // 4 softmax + K-TMA + V-TMA + MMA warps
 constexpr int SLOT_FLOATS = 128 * HD + 2 * 128;      // partial O rows + m + l
 constexpr float kLazyThreshLog2 = 8.0f;
 // Batches of up to kTabB requests get their cumulative tile counts staged in
@@ -66,14 +68,22 @@ constexpr int kTabB = 128;
 
 // Per-M configuration: M = 64 query rows (T <= 64) or 128 (T <= 128).
 template <int M> struct Cfg {
-    static constexpr int SPLIT = M == 64 ? 2 : 1;           // threads per query row
+    // M=64: 4 softmax warps, the two column halves of a row in lanes l / l+16
+    // sharing one (m, l, O). M=128 ("DUAL"): 8 softmax warps, warps w and w+4
+    // read the same TMEM lanes and take one column half each, with their own
+    // running (m, l) and their own O accumulator, merged once per segment.
+    static constexpr bool DUAL = M == 128;
+    static constexpr int SW = M == 64 ? 4 : 8;              // softmax warps
+    static constexpr int THREADS = (SW + 3) * 32;           // + K-TMA, V-TMA, MMA warps
+    static constexpr int SPLIT = M == 64 ? 2 : 1;           // threads per query row in a warp
     static constexpr uint32_t A_ATOM = M * 128;             // M rows x 64 elems x 2 B
     static constexpr uint32_t A_BYTES = 2 * A_ATOM;         // Q or one P buffer
     static constexpr int QSTAGES = M == 64 ? 2 : 1;          // next pair's Q prefetched
     static constexpr int KSTAGES = 3;
     static constexpr int VSTAGES = 3;
     static constexpr uint32_t S_COLS = BN / SPLIT;          // TMEM columns per S buffer
-    static constexpr uint32_t O_COL = 2 * S_COLS;           // O accumulator column
+    static constexpr uint32_t O_COL = 2 * S_COLS;           // O accumulator column (DUAL: O_a)
+    static constexpr uint32_t OB_COL = O_COL + HD;          // DUAL: O_b
     static constexpr uint32_t TMEM_COLS = M == 64 ? 256 : 512;
     static constexpr uint32_t OFF_Q = 0;
     static constexpr uint32_t OFF_K = OFF_Q + QSTAGES * A_BYTES;
@@ -98,6 +108,7 @@ struct TcParams {
     unsigned long long* trace;  // optional pipeline trace of CTA 0 (ST_K1_TRACE)
     int aligned_slack;          // whole-pair schedule allowed within this many tiles of stream-K
     int trace_cta;              // CTA whose per-tile pipeline is traced (ST_K1_TRACE_CTA)
+    float* ml_xchg;             // DUAL: [gridDim.x][2][128][2] (m, l) of each column half
     // head-sharded output (st_tree_attention_allgather): rows go to every rank's
     // [B][T][H_out][D] buffer at head head_offset + h; null -> o with H_out = H
     void* const* o_peers;
@@ -248,14 +259,16 @@ __device__ __forceinline__ void store_row(T* dst_row, const float* v, float scal
 }
 
 template <class T, int M>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(Cfg<M>::THREADS, 1)
 tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const TcParams p) {
     using C = Cfg<M>;
     constexpr int KS = C::KSTAGES, VS = C::VSTAGES, QS = C::QSTAGES;
-    constexpr int SPLIT = C::SPLIT;          // threads per query row (2 for M=64)
-    constexpr int COLS = BN / SPLIT;         // S columns per thread per tile
-    constexpr int DCOLS = HD / SPLIT;        // O columns per thread
+    constexpr int SPLIT = C::SPLIT;          // threads per query row in a warp (2 for M=64)
+    constexpr bool DUAL = C::DUAL;
+    constexpr int SW = C::SW;                // softmax warps; then K-TMA, V-TMA, MMA
+    constexpr int COLS = BN / 2;             // S columns per thread per tile (one half)
+    constexpr int DCOLS = HD / 2;            // output d columns per thread
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -284,18 +297,18 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         for (int i = 0; i < VS; ++i) { mbar_init(v_full + i, 1); mbar_init(v_empty + i, 1); }
         for (int i = 0; i < 2; ++i) {
             mbar_init(s_full + i, 1);
-            mbar_init(p_full + i, 128);
+            mbar_init(p_full + i, SW * 32);
             mbar_init(pv_done + i, 1);
         }
-        mbar_init(o_empty, 128);
+        mbar_init(o_empty, SW * 32);
         fence_barrier_init();
     }
-    if (warp == 4 && lane == 0) {
+    if (warp == SW && lane == 0) {
         prefetch_tmap(&tm_q);
         prefetch_tmap(&tm_k);
     }
-    if (warp == 5 && lane == 0) prefetch_tmap(&tm_v);
-    if (warp == 6) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+    if (warp == SW + 1 && lane == 0) prefetch_tmap(&tm_v);
+    if (warp == SW + 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -368,7 +381,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         p.trace[12 * 64 + kTraceCta * blockIdx.x + 6] = clock64();
     }
 
-    if (warp == 4) {
+    if (warp == SW) {
         // ======================= TMA producer: Q and K =========================
         if (lane == 0) {
             uint32_t qc = 0, kc = 0;
@@ -394,7 +407,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 t += s.hi - s.lo;
             }
         }
-    } else if (warp == 5) {
+    } else if (warp == SW + 1) {
         // =========================== TMA producer: V ============================
         if (lane == 0) {
             uint32_t vc = 0;
@@ -413,9 +426,11 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 t += s.hi - s.lo;
             }
         }
-    } else if (warp == 6) {
+    } else if (warp == SW + 2) {
         // ============================ MMA issuer ==============================
-        // M=128: S = Q K^T (N=128) and O += P V (N=128), one accumulator each.
+        // M=128: S = Q K^T (N=128); O_a += P[:, 0:64] V[0:64] and
+        //        O_b += P[:, 64:128] V[64:128] (N=128, K=64 each), one
+        //        accumulator per column half of the softmax.
         // M=64 : every product is split into two N=64 MMAs whose accumulators
         //        land in TMEM lanes 0-15 and 16-31 of each subpartition (the
         //        interleaved M=64 layout), so all 32 softmax lanes hold data:
@@ -446,10 +461,13 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             const uint32_t pt = tmem + pb * C::S_COLS;
 #pragma unroll
             for (int kk = 0; kk < BN / 16; ++kk) {
-                const uint32_t acc = (i_local > 0 || kk > 0) ? 1u : 0u;
-                if constexpr (SPLIT == 1) {
-                    umma_f16_ts_warp(tmem + C::O_COL, pt + kk * 8, vd + ((kk * 2048) >> 4), idPV, acc);
+                const uint32_t acc = (i_local > 0 || (kk & 3) > 0) ? 1u : 0u;
+                if constexpr (DUAL) {  // half h's P sits at S columns [64h, 64h+32)
+                    const uint32_t h = kk >> 2;
+                    umma_f16_ts_warp(tmem + (h ? C::OB_COL : C::O_COL), pt + h * 64 + (kk & 3) * 8,
+                                     vd + ((kk * 2048) >> 4), idPV, acc);
                 } else {
+                    const uint32_t acc = (i_local > 0 || kk > 0) ? 1u : 0u;
                     umma_f16_ts_warp(tmem + C::O_COL, pt + kk * 8, vd + ((kk * 2048) >> 4), idPV, acc);
                     umma_f16_ts_warp(tmem + HI_LANES + C::O_COL, pt + HI_LANES + kk * 8,
                                      vd + ((KV_ATOM + kk * 2048) >> 4), idPV, acc);
@@ -507,14 +525,18 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             t += ntl;
         }
     } else {
-        // ===================== softmax + epilogue (warps 0-3) ==================
-        // Thread (warp w, lane t) reads TMEM lane 32w+t. M=128: query row
-        // 32w+t, all 128 kv columns / all 128 d. M=64: row 16w+(t&15) and the
-        // half h = t>>4 of the kv columns (S) and of d (O); the two halves of a
-        // row exchange max / sum with one shuffle.
-        const int half = SPLIT == 2 ? (lane >> 4) : 0;
-        const int r = SPLIT == 2 ? warp * 16 + (lane & 15) : warp * 32 + lane;
-        const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+        // ===================== softmax + epilogue (warps 0..SW-1) ==================
+        // Thread (warp w, lane t) reads TMEM lane 32(w%4)+t and owns column half
+        // `half` of its row's kv tile (S) and of d (output). M=64: row
+        // 16w+(t&15), half t>>4; the two halves of a row exchange max / sum with
+        // one shuffle and share O. M=128 (DUAL): row 32(w%4)+t, half w/4; each
+        // half keeps its own (m, l) and O accumulator, merged in the epilogue.
+        const int half = DUAL ? (warp >> 2) : (lane >> 4);
+        const int r = DUAL ? (warp & 3) * 32 + lane : warp * 16 + (lane & 15);
+        const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        const uint32_t s_half = DUAL ? half * COLS : 0;          // this half's S columns
+        const uint32_t o_own = DUAL ? (half ? C::OB_COL : C::O_COL) : C::O_COL;
+        constexpr int OWN_COLS = DUAL ? HD : DCOLS;              // O columns this thread rescales
         const float c = p.c_log2;
         const float thresh_raw = kLazyThreshLog2 / c;
         uint32_t sc = 0, pc = 0;
@@ -544,7 +566,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
 #pragma unroll
                     for (int ch = 0; ch < COLS / 32; ++ch) {
                         uint32_t raw[32];
-                        tmem_ld_32x32b_x32(lane_addr + sb * C::S_COLS + ch * 32, raw);
+                        tmem_ld_32x32b_x32(lane_addr + sb * C::S_COLS + s_half + ch * 32, raw);
                         tmem_ld_wait();
 #pragma unroll
                         for (int k = 0; k < 32; ++k) sv[ch * 32 + k] = __uint_as_float(raw[k]);
@@ -580,7 +602,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         mq[3] = fmaxf(mq[3], sv[k + 3]);
                     }
                     float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
-                    if constexpr (SPLIT == 2) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+                    if constexpr (!DUAL) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
                     const float m_new = fmaxf(m, mx);
                     if (threadIdx.x == 0) K1_TRACE(9, sc);
 
@@ -600,14 +622,14 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         mbar_wait(pv_done + (q1 & 1), (q1 >> 1) & 1);
                         tc_fence_after();
 #pragma unroll
-                        for (int ch = 0; ch < DCOLS / 32; ++ch) {
+                        for (int ch = 0; ch < OWN_COLS / 32; ++ch) {
                             uint32_t raw[32];
-                            tmem_ld_32x32b_x32(lane_addr + C::O_COL + ch * 32, raw);
+                            tmem_ld_32x32b_x32(lane_addr + o_own + ch * 32, raw);
                             tmem_ld_wait();
 #pragma unroll
                             for (int k = 0; k < 32; ++k)
                                 raw[k] = __float_as_uint(__uint_as_float(raw[k]) * alpha);
-                            tmem_st_32x32b_x32(lane_addr + C::O_COL + ch * 32, raw);
+                            tmem_st_32x32b_x32(lane_addr + o_own + ch * 32, raw);
                         }
                         tmem_st_wait();
                     }
@@ -622,12 +644,15 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         ls[k & 3] += p0 + p1;
                         pk[k] = pk2<T>::pack(p0, p1);
                     }
-                    // P (f16/bf16) into TMEM over this tile's S columns: 64
-                    // columns per row (2 elements each). M=64: the two lanes of a
-                    // row swap halves so both hold the full row (the P.V MMA of
-                    // each half-lane group reads A from its own lanes).
-                    const uint32_t pt = lane_addr + sb * C::S_COLS;
-                    if constexpr (SPLIT == 2) {
+                    // P (f16/bf16, 2 per column) into TMEM over this tile's S
+                    // columns. M=64: the two lanes of a row swap halves so both
+                    // hold the full row (64 columns; the P.V MMA of each half-lane
+                    // group reads A from its own lanes). DUAL: each half writes its
+                    // 32 columns at the start of its own S columns.
+                    const uint32_t pt = lane_addr + sb * C::S_COLS + s_half;
+                    if constexpr (DUAL) {
+                        tmem_st_32x32b_x32(pt, pk);
+                    } else {
                         uint32_t lo[32], hi[32];
 #pragma unroll
                         for (int k = 0; k < 32; ++k) {
@@ -637,9 +662,6 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         }
                         tmem_st_32x32b_x32(pt, lo);
                         tmem_st_32x32b_x32(pt + 32, hi);
-                    } else {
-                        tmem_st_32x32b_x32(pt, *reinterpret_cast<const uint32_t(*)[32]>(pk));
-                        tmem_st_32x32b_x32(pt + 32, *reinterpret_cast<const uint32_t(*)[32]>(pk + 32));
                     }
                     tmem_st_wait();
                     if (threadIdx.x == 0) K1_TRACE(10, sc);
@@ -663,17 +685,46 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             mbar_wait(pv_done + (q1 & 1), (q1 >> 1) & 1);
             if (threadIdx.x == 0) K1_GT(3);
             float l_row = l;
-            if constexpr (SPLIT == 2) l_row += __shfl_xor_sync(0xffffffffu, l, 16);
+            // DUAL: weights of the two halves' accumulators under the merged max
+            float wa = 1.f, wb = 0.f;
+            if constexpr (!DUAL) {
+                l_row += __shfl_xor_sync(0xffffffffu, l, 16);
+            } else {
+                // exchange (m, l) with the other half's thread of this row (the
+                // CTA's slice of the workspace; bar.sync orders it in the CTA)
+                float* xc = p.ml_xchg + (long long)blockIdx.x * (2 * 128 * 2);
+                xc[(half * 128 + r) * 2] = m;
+                xc[(half * 128 + r) * 2 + 1] = l;
+                named_bar_sync(1, SW * 32);
+                const float m_o = __ldcg(xc + ((1 - half) * 128 + r) * 2);
+                const float l_o = __ldcg(xc + ((1 - half) * 128 + r) * 2 + 1);
+                named_bar_sync(1, SW * 32);  // reads done before the next segment's writes
+                const float ma = half ? m_o : m, mb = half ? m : m_o;
+                const float la = half ? l_o : l, lb = half ? l : l_o;
+                const float mm = fmaxf(ma, mb);
+                wa = ma == -INFINITY ? 0.f : ex2((ma - mm) * c);
+                wb = mb == -INFINITY ? 0.f : ex2((mb - mm) * c);
+                l_row = la * wa + lb * wb;
+                m = mm;
+            }
             if (warp_live) {
                 tc_fence_after();
                 float ov[DCOLS];
 #pragma unroll
                 for (int ch = 0; ch < DCOLS / 32; ++ch) {
                     uint32_t raw[32];
-                    tmem_ld_32x32b_x32(lane_addr + C::O_COL + ch * 32, raw);
+                    // M=64: this lane's d half of the shared O. DUAL: d half
+                    // `half` of both accumulators, weighted.
+                    tmem_ld_32x32b_x32(lane_addr + C::O_COL + (DUAL ? half * DCOLS : 0) + ch * 32, raw);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) ov[ch * 32 + k] = __uint_as_float(raw[k]);
+                    for (int k = 0; k < 32; ++k) ov[ch * 32 + k] = __uint_as_float(raw[k]) * wa;
+                    if constexpr (DUAL) {
+                        tmem_ld_32x32b_x32(lane_addr + C::OB_COL + half * DCOLS + ch * 32, raw);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) ov[ch * 32 + k] += __uint_as_float(raw[k]) * wb;
+                    }
                 }
                 tc_fence_before();
                 mbar_arrive(o_empty);
@@ -717,7 +768,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         p.trace[12 * 64 + kTraceCta * blockIdx.x + 1] = gt;
         p.trace[12 * 64 + kTraceCta * blockIdx.x + 7] = clock64();
     }
-    if (warp == 6) tmem_dealloc<C::TMEM_COLS>(tmem);
+    if (warp == SW + 2) tmem_dealloc<C::TMEM_COLS>(tmem);
 }
 
 // Merge of the partial pieces of pairs that the stream-K schedule split over
@@ -897,9 +948,12 @@ bool tree_attention_tc_supported(const st_attn_args* a) {
            al(a->v_cache) && al(a->o) && (int64_t)a->B * a->H < (1ll << 31);
 }
 
+constexpr size_t kXchgFloats = 2 * 128 * 2;  // per CTA: (m, l) of both column halves (M=128)
+
 size_t tree_attention_tc_workspace(const st_attn_args* a) {
     return align_up((size_t)num_sms() * 2 * SLOT_FLOATS * sizeof(float), 256) +
-           (size_t)(num_sms() + 1) * 4 * sizeof(long long);
+           align_up((size_t)(num_sms() + 1) * 4 * sizeof(long long), 256) +
+           (size_t)num_sms() * kXchgFloats * sizeof(float);
 }
 
 // K1 and combine_kernel are both launched with programmatic dependent launch
@@ -914,7 +968,7 @@ size_t tree_attention_tc_workspace(const st_attn_args* a) {
                                              Cfg<MM>::SMEM_BYTES));                             \
             attr = true;                                                                        \
         }                                                                                       \
-        ST_CUDA_TRY(launch_pdl(tree_attn_tc_kernel<TT, MM>, dim3(G), dim3(NUM_THREADS),          \
+        ST_CUDA_TRY(launch_pdl(tree_attn_tc_kernel<TT, MM>, dim3(G), dim3(Cfg<MM>::THREADS),     \
                                Cfg<MM>::SMEM_BYTES, stream, tq, tk, tv, prm));                  \
         ST_CUDA_TRY(launch_pdl(combine_kernel<TT>, dim3(G), dim3(256), 0, stream, prm, G));     \
     } while (0)
@@ -952,6 +1006,8 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
     prm.partial = reinterpret_cast<float*>(a->workspace);
     prm.sched = reinterpret_cast<long long*>(reinterpret_cast<uint8_t*>(a->workspace) +
                                              align_up((size_t)G * 2 * SLOT_FLOATS * sizeof(float), 256));
+    prm.ml_xchg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(prm.sched) +
+                                           align_up((size_t)(G + 1) * 4 * sizeof(long long), 256));
     prm.B = a->B;
     prm.T = a->T;
     prm.H = a->H;
