@@ -65,6 +65,9 @@ constexpr float kLazyThreshLog2 = 8.0f;
 // shared memory once per CTA (one parallel round of global loads); larger
 // batches walk the lengths in global memory.
 constexpr int kTabB = 128;
+// Pieces a split pair may leave beyond its head: at most gridDim.x - 1 (the
+// host launches at most kMaxPieces + 1 CTAs).
+constexpr int kMaxPieces = 255;
 
 // Per-M configuration: M = 64 query rows (T <= 64) or 128 (T <= 128).
 template <int M> struct Cfg {
@@ -89,8 +92,15 @@ template <int M> struct Cfg {
     static constexpr uint32_t OFF_K = OFF_Q + QSTAGES * A_BYTES;
     static constexpr uint32_t OFF_V = OFF_K + KSTAGES * TILE_BYTES;
     static constexpr uint32_t OFF_BAR = OFF_V + VSTAGES * TILE_BYTES;
+    // A split pair's head owner stages the pair's other pieces into the drained
+    // K ring: (m, l) block, then M rows of O with a 16-byte pad per row (528 B
+    // stride: consecutive rows start 4 banks apart).
+    static constexpr uint32_t PIECE_ROW = HD * 4 + 16;
+    static constexpr uint32_t PIECE_SMEM = (1024 + M * PIECE_ROW + 127) / 128 * 128;
+    static constexpr int STAGED_PIECES = (KSTAGES * TILE_BYTES) / PIECE_SMEM;
     static constexpr uint32_t OFF_TAB = OFF_BAR + 256;     // per-request tile table
-    static constexpr uint32_t SMEM_BYTES = OFF_TAB + (kTabB + 4) * 4 + 1024;
+    static constexpr uint32_t OFF_PIECES = OFF_TAB + (kTabB + 4) * 4;  // head owner's piece list
+    static constexpr uint32_t SMEM_BYTES = OFF_PIECES + (kMaxPieces + 1) * 4 + 1024;
     static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
@@ -100,8 +110,8 @@ struct TcParams {
     const uint64_t* mask;
     void* o;
     float* lse;
-    float* partial;      // [gridDim.x * 2][SLOT_FLOATS]
-    long long* sched;    // [gridDim.x + 1][4]: range start, last pair start, last pair tiles
+    float* partial;      // [gridDim.x][SLOT_FLOATS]: the piece a CTA's first segment leaves
+    unsigned* flags;     // [gridDim.x]: 1 while that piece is published and not yet merged
     int B, T, H, W;
     float c_log2;        // scale * log2(e)
     float scale;
@@ -132,9 +142,13 @@ constexpr int kTraceCta = 12;  // per-CTA globaltimer/clock slots of the ST_K1_T
             p.trace[(slot) * 64 + (idx)] = clock64();                             \
     } while (0)
 
+// Tile indices over the pair-major sequence are 32-bit (the host rejects
+// launches with 2^31 or more tiles): 64-bit integer division is a ~70
+// instruction subroutine, and the schedule arithmetic sits on every CTA's
+// path to its first load.
 struct Seg {
     int b, h, lo, hi, ntiles;
-    long long pair_start;
+    uint32_t pair_start;
 };
 
 __device__ __forceinline__ int ntiles_of(const TcParams& p, int b) {
@@ -145,39 +159,42 @@ __device__ __forceinline__ int ntiles_of(const TcParams& p, int b) {
 // Segment starting at global tile t (t < t_end) of this CTA's range. `cum`
 // (shared memory, or null): cum[b] = tiles of requests < b, cum[kTabB+1..3] =
 // requests with tiles, min and max tiles per request.
-__device__ Seg find_seg(const TcParams& p, const int* cum, long long t, long long t_end) {
+__device__ Seg find_seg(const TcParams& p, const int* cum, uint32_t t, uint32_t t_end) {
     Seg s{};
+    const uint32_t H = (uint32_t)p.H;
     if (cum) {
         int lo = 0, hi = p.B;  // largest b with H*cum[b] <= t (skips empty requests)
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
-            if ((long long)p.H * cum[mid] <= t) lo = mid; else hi = mid;
+            if (H * (uint32_t)cum[mid] <= t) lo = mid; else hi = mid;
         }
-        const int nt = cum[lo + 1] - cum[lo];
-        const long long base = (long long)p.H * cum[lo];
-        const long long off = t - base;
+        const uint32_t nt = (uint32_t)(cum[lo + 1] - cum[lo]);
+        const uint32_t base = H * (uint32_t)cum[lo];
+        const uint32_t off = t - base;
+        const uint32_t hh = off / nt;
         s.b = lo;
-        s.h = (int)(off / nt);
-        s.lo = (int)(off % nt);
-        s.ntiles = nt;
-        s.pair_start = base + (long long)s.h * nt;
-        const long long h2 = s.lo + (t_end - t);
+        s.h = (int)hh;
+        s.lo = (int)(off - hh * nt);
+        s.ntiles = (int)nt;
+        s.pair_start = base + hh * nt;
+        const uint32_t h2 = (uint32_t)s.lo + (t_end - t);
         s.hi = (int)(h2 < nt ? h2 : nt);
         return s;
     }
-    long long base = 0;
+    uint32_t base = 0;
     for (int b = 0; b < p.B; ++b) {
-        const int nt = ntiles_of(p, b);
-        const long long span = (long long)p.H * nt;
+        const uint32_t nt = (uint32_t)ntiles_of(p, b);
+        const uint32_t span = H * nt;
         if (t < base + span) {
-            const long long off = t - base;
+            const uint32_t off = t - base;
+            const uint32_t hh = off / nt;
             s.b = b;
-            s.h = (int)(off / nt);
-            s.lo = (int)(off % nt);
-            s.ntiles = nt;
-            s.pair_start = base + (long long)s.h * nt;
-            const long long hi = s.lo + (t_end - t);
-            s.hi = (int)(hi < nt ? hi : nt);
+            s.h = (int)hh;
+            s.lo = (int)(off - hh * nt);
+            s.ntiles = (int)nt;
+            s.pair_start = base + hh * nt;
+            const uint32_t h2 = (uint32_t)s.lo + (t_end - t);
+            s.hi = (int)(h2 < nt ? h2 : nt);
             return s;
         }
         base += span;
@@ -187,25 +204,35 @@ __device__ Seg find_seg(const TcParams& p, const int* cum, long long t, long lon
 }
 
 // CTA work ranges over the pair-major tile sequence. Stream-K (equal tile
-// counts; pairs may be split, leaving partial pieces for combine_kernel) unless
-// every pair has the same tile count and whole-pair ranges cost at most
-// kAlignedSlack tiles more than perfect balance — then CTA c takes pairs
-// [c*Np/G, (c+1)*Np/G) and no pair is split (no partials, no merge).
-constexpr long long kAlignedSlack = 6;
+// counts; pairs may be split, leaving pieces that the pair's head owner merges
+// in-kernel) unless every pair has the same tile count and whole-pair ranges
+// cost at most aligned_slack tiles more than perfect balance — then CTA c
+// takes pairs [c*Np/G, (c+1)*Np/G) and no pair is split.
+constexpr int kAlignedSlack = 6;
 
 struct Sched {
-    long long total;
-    long long np;   // pairs with tiles
+    uint32_t total;
+    uint32_t np;    // pairs with tiles
     int nt;         // tiles per pair when uniform
     bool aligned;
+    double inv_g;   // 1 / G, for the exact floor(c * x / G) below
 };
 
-__device__ Sched make_sched(const TcParams& p, const int* cum, long long G) {
-    Sched s{0, 0, 0, false};
+// floor(x / G) for x < 2^53 with G <= 256: the double product is within a
+// relative 2^-52 of the quotient, then one integer correction each way.
+__device__ __forceinline__ uint32_t div_g(uint64_t x, uint32_t G, double inv_g) {
+    uint64_t q = (uint64_t)((double)x * inv_g);
+    if (q * G > x) --q;
+    if ((q + 1) * G <= x) ++q;
+    return (uint32_t)q;
+}
+
+__device__ Sched make_sched(const TcParams& p, const int* cum, uint32_t G) {
+    Sched s{0, 0, 0, false, 1.0 / (double)G};
     int lo = 1 << 30, hi = 0;
     if (cum) {
-        s.total = (long long)p.H * cum[p.B];
-        s.np = (long long)p.H * cum[kTabB + 1];
+        s.total = (uint32_t)p.H * (uint32_t)cum[p.B];
+        s.np = (uint32_t)p.H * (uint32_t)cum[kTabB + 1];
         lo = cum[kTabB + 2];
         hi = cum[kTabB + 3];
     }
@@ -216,19 +243,20 @@ __device__ Sched make_sched(const TcParams& p, const int* cum, long long G) {
             hi = max(hi, nt);
             s.np += p.H;
         }
-        s.total += (long long)p.H * nt;
+        s.total += (uint32_t)p.H * (uint32_t)nt;
     }
     if (s.np > 0 && lo == hi) {
         s.nt = lo;
-        const long long aligned_span = (s.np + G - 1) / G * s.nt;
-        const long long streamk_span = (s.total + G - 1) / G;
-        s.aligned = aligned_span <= streamk_span + p.aligned_slack;
+        const uint32_t aligned_span = div_g(s.np + G - 1, G, s.inv_g) * (uint32_t)s.nt;
+        const uint32_t streamk_span = div_g(s.total + G - 1, G, s.inv_g);
+        s.aligned = (long long)aligned_span <= (long long)streamk_span + p.aligned_slack;
     }
     return s;
 }
 
-__device__ __forceinline__ long long range_start(long long c, const Sched& s, long long G) {
-    return s.aligned ? (c * s.np / G) * s.nt : c * s.total / G;
+__device__ __forceinline__ uint32_t range_start(uint32_t c, const Sched& s, uint32_t G) {
+    return s.aligned ? div_g((uint64_t)c * s.np, G, s.inv_g) * (uint32_t)s.nt
+                     : div_g((uint64_t)c * s.total, G, s.inv_g);
 }
 
 template <class T> struct pk2;
@@ -286,7 +314,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     uint64_t* p_full = s_full + 2;       // [2]
     uint64_t* pv_done = p_full + 2;      // [2]
     uint64_t* o_empty = pv_done + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 1);
+    uint64_t* merge_full = o_empty + 1;  // staged pieces landed (head owner only)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(merge_full + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) K1_GT(8);
@@ -301,6 +330,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             mbar_init(pv_done + i, 1);
         }
         mbar_init(o_empty, SW * 32);
+        mbar_init(merge_full, 1);
         fence_barrier_init();
     }
     if (warp == SW && lane == 0) {
@@ -354,25 +384,10 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     __syncthreads();
     if (threadIdx.x == 0) K1_GT(9);
 
-    const long long G = gridDim.x;
+    const uint32_t G = gridDim.x;
     const Sched sched = make_sched(p, cum, G);
-    const long long total = sched.total;
-    const long long t_begin = range_start(blockIdx.x, sched, G);
-    const long long t_end = range_start(blockIdx.x + 1, sched, G);
-    if (threadIdx.x == 0) {  // schedule table for combine_kernel
-        long long* e = p.sched + 4 * blockIdx.x;
-        e[0] = t_begin;
-        if (t_end > t_begin) {
-            const Seg last = find_seg(p, cum, t_end - 1, t_end);
-            e[1] = last.pair_start;
-            e[2] = last.ntiles;
-            e[3] = (long long)last.b * p.H + last.h;
-        } else {
-            e[1] = -1;
-            e[2] = 0;
-        }
-        if (blockIdx.x == gridDim.x - 1) p.sched[4 * gridDim.x] = t_end;  // == total
-    }
+    const uint32_t t_begin = range_start(blockIdx.x, sched, G);
+    const uint32_t t_end = range_start(blockIdx.x + 1, sched, G);
     if (p.trace && threadIdx.x == 0) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
@@ -384,8 +399,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (warp == SW) {
         // ======================= TMA producer: Q and K =========================
         if (lane == 0) {
+            const uint64_t pol = l2_policy_evict_first();  // the KV stream is read once
             uint32_t qc = 0, kc = 0;
-            for (long long t = t_begin; t < t_end;) {
+            for (uint32_t t = t_begin; t < t_end;) {
                 const Seg s = find_seg(p, cum, t, t_end);
                 const uint32_t qb = qc % QS;
                 mbar_wait(q_empty + qb, ((qc / QS) & 1) ^ 1);
@@ -401,17 +417,66 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     if (kc == 0) K1_GT(5);
                     mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
                     uint8_t* dst = sm_k + st * TILE_BYTES;
-                    tma_load_3d(dst, &tm_k, k_full + st, 0, j * BN, bh);
-                    tma_load_3d(dst + KV_ATOM, &tm_k, k_full + st, 64, j * BN, bh);
+                    tma_load_3d_hint(dst, &tm_k, k_full + st, 0, j * BN, bh, pol);
+                    tma_load_3d_hint(dst + KV_ATOM, &tm_k, k_full + st, 64, j * BN, bh, pol);
                 }
                 t += s.hi - s.lo;
+            }
+        }
+        // If this range ends with a pair's head, stage the pair's other pieces
+        // (published by the following CTAs early in their ranges) into the K
+        // ring as soon as the last S MMA has drained it, so the softmax warps'
+        // merge reads shared memory instead of making L2 round trips.
+        if (t_end > t_begin) {
+            const Seg ls = find_seg(p, cum, t_end - 1, t_end);
+            const uint32_t pend = ls.pair_start + (uint32_t)ls.ntiles;
+            if (ls.pair_start >= t_begin && pend > t_end) {
+                const uint32_t kc = (uint32_t)(t_end - t_begin);  // K tiles this CTA loaded
+                const int n = __ldg(p.n_nodes + ls.b);
+                const int rows = n < M ? n : M;
+                if (lane == 0) {
+                    // piece list for the softmax warps; every piece's flag is
+                    // awaited here (normally long set) and re-armed for the
+                    // next launch, then the drained K ring receives the first
+                    // STAGED_PIECES pieces
+                    int* pieces = reinterpret_cast<int*>(smem + C::OFF_PIECES);
+                    int np = 0;
+                    for (uint32_t c2 = blockIdx.x + 1; c2 < G && np < kMaxPieces; ++c2) {
+                        const uint32_t rs = range_start(c2, sched, G);
+                        if (rs >= pend) break;
+                        if (range_start(c2 + 1, sched, G) == rs) continue;  // empty range
+                        wait_flag_gpu(p.flags + c2);
+                        p.flags[c2] = 0u;
+                        pieces[1 + np++] = (int)c2;
+                    }
+                    pieces[0] = np;
+                    for (uint32_t st = 0; st < (uint32_t)KS && st < kc; ++st) {
+                        const uint32_t k = kc - 1 - ((kc - 1 - st) % KS);  // last use of stage st
+                        mbar_wait(k_empty + st, (k / KS) & 1);
+                    }
+                    fence_proxy_async_global();
+                    const int ns = np < C::STAGED_PIECES ? np : C::STAGED_PIECES;
+                    mbar_arrive_expect_tx(merge_full, (uint32_t)ns * (1024u + (uint32_t)rows * HD * 4));
+                    K1_GT(11);
+                }
+                __syncwarp();
+                const int* pieces = reinterpret_cast<const int*>(smem + C::OFF_PIECES);
+                const int ns = pieces[0] < C::STAGED_PIECES ? pieces[0] : C::STAGED_PIECES;
+                for (int i = 0; i < ns; ++i) {
+                    const float* piece = p.partial + (long long)pieces[1 + i] * SLOT_FLOATS;
+                    uint8_t* dst = sm_k + i * C::PIECE_SMEM;
+                    if (lane == 0) bulk_load(dst, piece + 128 * HD, 1024, merge_full);
+                    for (int r = lane; r < rows; r += 32)
+                        bulk_load(dst + 1024 + r * C::PIECE_ROW, piece + r * HD, HD * 4, merge_full);
+                }
             }
         }
     } else if (warp == SW + 1) {
         // =========================== TMA producer: V ============================
         if (lane == 0) {
+            const uint64_t pol = l2_policy_evict_first();
             uint32_t vc = 0;
-            for (long long t = t_begin; t < t_end;) {
+            for (uint32_t t = t_begin; t < t_end;) {
                 const Seg s = find_seg(p, cum, t, t_end);
                 const int bh = s.b * p.H + s.h;
                 for (int j = s.lo; j < s.hi; ++j, ++vc) {
@@ -420,8 +485,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     K1_TRACE(1, vc);
                     mbar_arrive_expect_tx(v_full + st, TILE_BYTES);
                     uint8_t* dst = sm_v + st * TILE_BYTES;
-                    tma_load_3d(dst, &tm_v, v_full + st, 0, j * BN, bh);
-                    tma_load_3d(dst + KV_ATOM, &tm_v, v_full + st, 64, j * BN, bh);
+                    tma_load_3d_hint(dst, &tm_v, v_full + st, 0, j * BN, bh, pol);
+                    tma_load_3d_hint(dst + KV_ATOM, &tm_v, v_full + st, 64, j * BN, bh, pol);
                 }
                 t += s.hi - s.lo;
             }
@@ -479,7 +544,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             ++vc;
             ++pc;
         };
-        for (long long t = t_begin; t < t_end;) {
+        for (uint32_t t = t_begin; t < t_end;) {
             const Seg s = find_seg(p, cum, t, t_end);
             const int ntl = s.hi - s.lo;
             const uint32_t qb = qc % QS;
@@ -540,7 +605,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         const float c = p.c_log2;
         const float thresh_raw = kLazyThreshLog2 / c;
         uint32_t sc = 0, pc = 0;
-        for (long long t = t_begin; t < t_end;) {
+        for (uint32_t t = t_begin; t < t_end;) {
             const Seg s = find_seg(p, cum, t, t_end);
             const int ntl = s.hi - s.lo;
             const int n = __ldg(p.n_nodes + s.b);
@@ -676,9 +741,15 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             }
 
             // ---- segment epilogue: this thread's O columns from TMEM ----
+            // A segment is a whole pair (written out), a pair's head (lo == 0,
+            // the last segment of this range: this CTA merges the pair's other
+            // pieces into it and writes it out) or a later piece (lo > 0, the
+            // first segment of this range: published as (O, m, l) for the
+            // pair's head owner). The pieces were computed at the START of the
+            // following CTAs' ranges, so the head owner — at the END of its
+            // range — normally finds them ready.
             const bool full = (s.lo == 0 && s.hi == s.ntiles);
-            const int slot = (t == t_begin) ? 0 : 1;
-            float* sp = p.partial + ((long long)blockIdx.x * 2 + slot) * SLOT_FLOATS;
+            const bool head = (s.lo == 0 && !full);
             const int d0 = half * DCOLS;
             const long long orow = (((long long)s.b * p.T + r) * p.H_out + p.head_offset + s.h) * HD + d0;
             const uint32_t q1 = pc - 1;
@@ -707,54 +778,120 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 l_row = la * wa + lb * wb;
                 m = mm;
             }
+            // head: final (m, l) over this segment and the pieces of CTAs
+            // blockIdx.x+1, ... whose ranges start inside the pair (CTA order:
+            // deterministic); pass 2 below adds their O chunk by chunk
+            // (the first STAGED_PIECES pieces were staged into the drained K
+            // ring by the K producer warp; any further ones are read from L2)
+            float m_fin = m, l_fin = l_row;
+            const int* pieces = reinterpret_cast<const int*>(smem + C::OFF_PIECES);
+            int np = 0;
+            if (head) {
+                mbar_wait(merge_full, 0);
+                if (threadIdx.x == 0) K1_GT(10);
+                np = pieces[0];
+            }
+            if (head && valid) {
+                for (int i = 0; i < np; ++i) {
+                    float mp, lp;
+                    if (i < C::STAGED_PIECES) {
+                        const float* ml = reinterpret_cast<const float*>(sm_k + i * C::PIECE_SMEM);
+                        mp = ml[r];
+                        lp = ml[128 + r];
+                    } else {
+                        const float* piece = p.partial + (long long)pieces[1 + i] * SLOT_FLOATS;
+                        mp = __ldcg(piece + 128 * HD + r);
+                        lp = __ldcg(piece + 128 * HD + 128 + r);
+                    }
+                    const float mm = fmaxf(m_fin, mp);
+                    if (mm != -INFINITY) {
+                        l_fin = (m_fin == -INFINITY ? 0.f : l_fin * ex2((m_fin - mm) * c)) +
+                                (mp == -INFINITY ? 0.f : lp * ex2((mp - mm) * c));
+                        m_fin = mm;
+                    }
+                }
+            }
+            const bool publish = !full && !head;
+            const float w_self = (m == -INFINITY) ? 0.f : ex2((m - m_fin) * c);
+            const float inv = 1.f / l_fin;
+            float* sp = p.partial + (long long)blockIdx.x * SLOT_FLOATS;
             if (warp_live) {
                 tc_fence_after();
-                float ov[DCOLS];
-#pragma unroll
+#pragma unroll 1
                 for (int ch = 0; ch < DCOLS / 32; ++ch) {
+                    float ov[32];
                     uint32_t raw[32];
                     // M=64: this lane's d half of the shared O. DUAL: d half
                     // `half` of both accumulators, weighted.
                     tmem_ld_32x32b_x32(lane_addr + C::O_COL + (DUAL ? half * DCOLS : 0) + ch * 32, raw);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) ov[ch * 32 + k] = __uint_as_float(raw[k]) * wa;
+                    for (int k = 0; k < 32; ++k) ov[k] = __uint_as_float(raw[k]) * wa;
                     if constexpr (DUAL) {
                         tmem_ld_32x32b_x32(lane_addr + C::OB_COL + half * DCOLS + ch * 32, raw);
                         tmem_ld_wait();
 #pragma unroll
-                        for (int k = 0; k < 32; ++k) ov[ch * 32 + k] += __uint_as_float(raw[k]) * wb;
+                        for (int k = 0; k < 32; ++k) ov[k] += __uint_as_float(raw[k]) * wb;
+                    }
+                    if (!valid) continue;
+                    const int dc = d0 + ch * 32;
+                    if (publish) {  // later piece of a pair: unnormalised O for the head owner
+                        float4* po = reinterpret_cast<float4*>(sp + r * HD + dc);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            po[k] = make_float4(ov[4 * k], ov[4 * k + 1], ov[4 * k + 2], ov[4 * k + 3]);
+                        continue;
+                    }
+                    if (head) {
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) ov[k] *= w_self;
+                        for (int i = 0; i < np; ++i) {
+                            const bool staged = i < C::STAGED_PIECES;
+                            const float* piece = staged
+                                ? reinterpret_cast<const float*>(sm_k + i * C::PIECE_SMEM)
+                                : p.partial + (long long)pieces[1 + i] * SLOT_FLOATS;
+                            const float mp = staged ? piece[r] : __ldcg(piece + 128 * HD + r);
+                            if (mp == -INFINITY) continue;
+                            const float wp = ex2((mp - m_fin) * c);
+                            const float4* pp = staged
+                                ? reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(piece) + 1024 +
+                                                                  r * C::PIECE_ROW + dc * 4)
+                                : reinterpret_cast<const float4*>(piece + r * HD + dc);
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+                                const float4 x = staged ? pp[k] : __ldcg(pp + k);
+                                ov[4 * k] = fmaf(x.x, wp, ov[4 * k]);
+                                ov[4 * k + 1] = fmaf(x.y, wp, ov[4 * k + 1]);
+                                ov[4 * k + 2] = fmaf(x.z, wp, ov[4 * k + 2]);
+                                ov[4 * k + 3] = fmaf(x.w, wp, ov[4 * k + 3]);
+                            }
+                        }
+                    }
+                    if (p.o_peers) {  // fused all-gather: this row into every rank's buffer
+                        for (int k = 0; k < p.world; ++k)
+                            store_row<T, 32>(reinterpret_cast<T*>(p.o_peers[k]) + orow + ch * 32, ov, inv);
+                    } else {
+                        store_row<T, 32>(reinterpret_cast<T*>(p.o) + orow + ch * 32, ov, inv);
                     }
                 }
                 tc_fence_before();
-                mbar_arrive(o_empty);
-                if (valid) {
-                    if (full) {
-                        if (p.o_peers) {  // fused all-gather: this row into every rank's buffer
-                            for (int k = 0; k < p.world; ++k)
-                                store_row<T, DCOLS>(reinterpret_cast<T*>(p.o_peers[k]) + orow, ov, 1.f / l_row);
-                        } else {
-                            store_row<T, DCOLS>(reinterpret_cast<T*>(p.o) + orow, ov, 1.f / l_row);
-                        }
-                        if (p.lse && half == 0)
-                            p.lse[((long long)s.b * p.H + s.h) * p.T + r] = m * p.scale + __logf(l_row);
-                    } else {
-                        float4* po = reinterpret_cast<float4*>(sp + r * HD + d0);
-#pragma unroll
-                        for (int k = 0; k < DCOLS / 4; ++k)
-                            po[k] = make_float4(ov[4 * k], ov[4 * k + 1], ov[4 * k + 2], ov[4 * k + 3]);
-                        if (half == 0) {
-                            sp[128 * HD + r] = m;
-                            sp[128 * HD + 128 + r] = l_row;
-                        }
-                    }
+            }
+            mbar_arrive(o_empty);
+            if (publish) {
+                if (valid && half == 0) {
+                    sp[128 * HD + r] = m;
+                    sp[128 * HD + 128 + r] = l_row;
                 }
+                // bar.sync orders every thread's stores before thread 0's
+                // gpu-scope release (release is cumulative)
+                named_bar_sync(2, SW * 32);
+                if (threadIdx.x == 0) st_release_gpu(p.flags + blockIdx.x, 1u);
             } else {
-                mbar_arrive(o_empty);
+                if (valid && p.lse && half == 0)
+                    p.lse[((long long)s.b * p.H + s.h) * p.T + r] = m_fin * p.scale + __logf(l_fin);
             }
 
             if (threadIdx.x == 0) K1_GT(4);
-            // split pairs: the partial (O, m, l) pieces are merged by combine_kernel
             t += ntl;
         }
     }
@@ -769,138 +906,6 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         p.trace[12 * 64 + kTraceCta * blockIdx.x + 7] = clock64();
     }
     if (warp == SW + 2) tmem_dealloc<C::TMEM_COLS>(tmem);
-}
-
-// Merge of the partial pieces of pairs that the stream-K schedule split over
-// several CTAs. Block c handles the pair that starts in CTA c's range and
-// continues past it (at most one per CTA), read from the schedule table the
-// attention kernel published: its pieces are CTA c's last segment (slot 0 if
-// that segment is c's whole range, else slot 1) and the first segment (slot 0)
-// of each following non-empty CTA until the pair ends. Warp 0 gathers that
-// piece list once (32 table entries per ballot) into shared memory; then warp
-// w merges rows w, w+8, ... (RPW rows at a time, lane l owning d columns
-// [4l, 4l+4)) over the pieces in chunks of CHUNK, every load of a chunk in
-// flight together, with an online (m, l, O) merge across chunks. Fixed piece
-// order -> deterministic.
-template <class T>
-__global__ void __launch_bounds__(256, 1)
-combine_kernel(const TcParams p, int G) {
-    constexpr int CHUNK = 4;      // pieces loaded together
-    constexpr int RPW = 4;        // rows per warp in flight together
-    constexpr int MAXPIECES = 256;
-    __shared__ int s_slots[MAXPIECES];
-    __shared__ int s_np;
-    const int cta = blockIdx.x;
-    pdl_wait();  // the attention kernel's pieces and schedule table
-    pdl_trigger();
-    const long long* tab = p.sched;
-    const long long rs = __ldcg(tab + 4 * cta), re = __ldcg(tab + 4 * (cta + 1));
-    const long long ps = __ldcg(tab + 4 * cta + 1), nt = __ldcg(tab + 4 * cta + 2);
-    if (re <= rs || ps < rs || ps + nt <= re) return;  // empty / pair not started here / not split
-    const int bh = (int)__ldcg(tab + 4 * cta + 3);
-    const int b = bh / p.H, h = bh % p.H;
-    const long long pend = ps + nt;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp == 0) {
-        int np = 0;
-        if (lane == 0) s_slots[0] = cta * 2 + (ps == rs ? 0 : 1);
-        np = 1;
-        for (int base = cta + 1; base < G && np < MAXPIECES; base += 32) {
-            const int cc = base + lane;
-            long long r0 = pend, r1 = pend;
-            if (cc < G) {
-                r0 = __ldcg(tab + 4 * cc);
-                r1 = __ldcg(tab + 4 * (cc + 1));
-            }
-            const bool inside = r0 < pend;
-            const unsigned have = __ballot_sync(0xffffffffu, inside && r1 > r0);
-            const unsigned past = __ballot_sync(0xffffffffu, !inside);
-            // CTAs before the first one past the pair's end, with non-empty ranges
-            const unsigned upto = past ? ((1u << __ffs(past) - 1) - 1u) : 0xffffffffu;
-            const unsigned take = have & upto;
-            if ((take >> lane) & 1u) {
-                const int at = np + __popc(take & ((1u << lane) - 1u));
-                if (at < MAXPIECES) s_slots[at] = cc * 2;
-            }
-            np += __popc(take);
-            if (past) break;
-        }
-        if (lane == 0) s_np = min(np, MAXPIECES);
-    }
-    __syncthreads();
-    const int np = s_np;
-    const int n = __ldg(p.n_nodes + b);
-    const float c = p.c_log2;
-    const int nw = blockDim.x >> 5;
-    for (int r0 = warp; r0 < n; r0 += nw * RPW) {
-        float M_[RPW], L[RPW];
-        float4 acc[RPW];
-#pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-            M_[i] = -INFINITY;
-            L[i] = 0.f;
-            acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        for (int k0 = 0; k0 < np; k0 += CHUNK) {
-            float mk[RPW][CHUNK], lk[RPW][CHUNK];
-            float4 ok[RPW][CHUNK];
-#pragma unroll
-            for (int i = 0; i < RPW; ++i) {
-                const int r = r0 + i * nw;
-#pragma unroll
-                for (int k = 0; k < CHUNK; ++k) {
-                    mk[i][k] = -INFINITY;
-                    if (k0 + k < np && r < n) {
-                        const float* piece = p.partial + (long long)s_slots[k0 + k] * SLOT_FLOATS;
-                        mk[i][k] = __ldcg(piece + 128 * HD + r);
-                        lk[i][k] = __ldcg(piece + 128 * HD + 128 + r);
-                        ok[i][k] = __ldcg(reinterpret_cast<const float4*>(piece + r * HD) + lane);
-                    }
-                }
-            }
-#pragma unroll
-            for (int i = 0; i < RPW; ++i) {
-                float Mn = M_[i];
-#pragma unroll
-                for (int k = 0; k < CHUNK; ++k) Mn = fmaxf(Mn, mk[i][k]);
-                if (Mn == -INFINITY) continue;
-                const float sc0 = M_[i] == -INFINITY ? 0.f : ex2((M_[i] - Mn) * c);
-                L[i] *= sc0;
-                acc[i].x *= sc0;
-                acc[i].y *= sc0;
-                acc[i].z *= sc0;
-                acc[i].w *= sc0;
-#pragma unroll
-                for (int k = 0; k < CHUNK; ++k) {
-                    if (mk[i][k] != -INFINITY) {
-                        const float w = ex2((mk[i][k] - Mn) * c);
-                        L[i] += w * lk[i][k];
-                        acc[i].x += w * ok[i][k].x;
-                        acc[i].y += w * ok[i][k].y;
-                        acc[i].z += w * ok[i][k].z;
-                        acc[i].w += w * ok[i][k].w;
-                    }
-                }
-                M_[i] = Mn;
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-            const int r = r0 + i * nw;
-            if (r >= n) break;
-            const float inv = 1.f / L[i];
-            const long long orow = (((long long)b * p.T + r) * p.H_out + p.head_offset + h) * HD + 4 * lane;
-            const uint2 val = make_uint2(pk2<T>::pack(acc[i].x * inv, acc[i].y * inv),
-                                         pk2<T>::pack(acc[i].z * inv, acc[i].w * inv));
-            if (p.o_peers) {
-                for (int k = 0; k < p.world; ++k)
-                    *reinterpret_cast<uint2*>(reinterpret_cast<T*>(p.o_peers[k]) + orow) = val;
-            } else {
-                *reinterpret_cast<uint2*>(reinterpret_cast<T*>(p.o) + orow) = val;
-            }
-            if (p.lse && lane == 0) p.lse[((long long)b * p.H + h) * p.T + r] = M_[i] * p.scale + __logf(L[i]);
-        }
-    }
 }
 
 // ------------------------------------------------------------------ host --
@@ -945,20 +950,22 @@ bool tree_attention_tc_supported(const st_attn_args* a) {
     auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
     return (a->dtype == ST_F16 || a->dtype == ST_BF16) && a->D == HD && a->H == a->Hkv &&
            a->T <= 128 && a->W <= 2 && a->Lmax < (1ll << 31) && al(a->q) && al(a->k_cache) &&
-           al(a->v_cache) && al(a->o) && (int64_t)a->B * a->H < (1ll << 31);
+           al(a->v_cache) && al(a->o) &&
+           (int64_t)a->B * a->H * ((a->Lmax + BN - 1) / BN) < (1ll << 31);  // 32-bit tile indices
 }
 
 constexpr size_t kXchgFloats = 2 * 128 * 2;  // per CTA: (m, l) of both column halves (M=128)
 
+// Workspace: per CTA one piece slot, the (m, l) exchange of M=128 and the
+// piece flags (zero on first use; every launch leaves them zero).
 size_t tree_attention_tc_workspace(const st_attn_args* a) {
-    return align_up((size_t)num_sms() * 2 * SLOT_FLOATS * sizeof(float), 256) +
-           align_up((size_t)(num_sms() + 1) * 4 * sizeof(long long), 256) +
-           (size_t)num_sms() * kXchgFloats * sizeof(float);
+    return align_up((size_t)num_sms() * SLOT_FLOATS * sizeof(float), 256) +
+           align_up((size_t)num_sms() * kXchgFloats * sizeof(float), 256) +
+           (size_t)num_sms() * sizeof(unsigned);
 }
 
-// K1 and combine_kernel are both launched with programmatic dependent launch
-// (common.cuh): K1's prologue overlaps the previous kernel's tail, and the
-// combine is scheduled while K1 drains, blocking in pdl_wait() until it ends.
+// K1 is launched with programmatic dependent launch (common.cuh): its prologue
+// overlaps the previous kernel's tail. Split pairs are merged inside K1.
 #define ST_TRY_LAUNCH_TC(TT, MM)                                                                \
     do {                                                                                        \
         static bool attr = false;                                                               \
@@ -970,7 +977,6 @@ size_t tree_attention_tc_workspace(const st_attn_args* a) {
         }                                                                                       \
         ST_CUDA_TRY(launch_pdl(tree_attn_tc_kernel<TT, MM>, dim3(G), dim3(Cfg<MM>::THREADS),     \
                                Cfg<MM>::SMEM_BYTES, stream, tq, tk, tv, prm));                  \
-        ST_CUDA_TRY(launch_pdl(combine_kernel<TT>, dim3(G), dim3(256), 0, stream, prm, G));     \
     } while (0)
 
 st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st_peer_out* po) {
@@ -996,7 +1002,7 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
             return ST_ERR_CUDA;
         }
     }
-    const int G = num_sms();
+    const int G = num_sms() < kMaxPieces + 1 ? num_sms() : kMaxPieces + 1;
     TcParams prm;
     prm.prefix_len = a->prefix_len;
     prm.n_nodes = a->n_nodes;
@@ -1004,10 +1010,10 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
     prm.o = a->o;
     prm.lse = a->lse;
     prm.partial = reinterpret_cast<float*>(a->workspace);
-    prm.sched = reinterpret_cast<long long*>(reinterpret_cast<uint8_t*>(a->workspace) +
-                                             align_up((size_t)G * 2 * SLOT_FLOATS * sizeof(float), 256));
-    prm.ml_xchg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(prm.sched) +
-                                           align_up((size_t)(G + 1) * 4 * sizeof(long long), 256));
+    prm.ml_xchg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(a->workspace) +
+                                           align_up((size_t)G * SLOT_FLOATS * sizeof(float), 256));
+    prm.flags = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(prm.ml_xchg) +
+                                            align_up((size_t)G * kXchgFloats * sizeof(float), 256));
     prm.B = a->B;
     prm.T = a->T;
     prm.H = a->H;

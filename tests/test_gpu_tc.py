@@ -25,7 +25,10 @@ def capi():
 
 @pytest.mark.parametrize("dtype", [torch.float16, torch.bfloat16])
 @pytest.mark.parametrize("B,H,P_range", [(3, 2, (1, 60)), (4, 8, (100, 700)), (2, 3, (1000, 1300)),
-                                         (9, 16, (0, 300))])
+                                         (9, 16, (0, 300)),
+                                         # long pairs over ~2 tiles per CTA: one pair
+                                         # leaves ~70 pieces, past the staged ones
+                                         (1, 2, (19000, 20000))])
 def test_tc_matches_oracle(capi, restatement, dtype, B, H, P_range):
     rng = np.random.default_rng(B * 100 + H)
     bt = make_batch(restatement, rng, B, H, H, 128, dtype=dtype, P_range=P_range)

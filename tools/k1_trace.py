@@ -61,7 +61,8 @@ print("duration histogram:", hist[0].tolist(), [round(float(x), 1) for x in hist
 rel = lambda k: (cta[:, k] - cta[:, 0]) / 1e3  # noqa: E731
 mhz = (cta[:, 7] - cta[:, 6]) / (cta[:, 1] - cta[:, 0]) * 1e3
 print("SM clock from clock64/globaltimer (MHz): median %.0f min %.0f max %.0f" % (np.median(mhz), mhz.min(), mhz.max()))
-for k, name in [(8, "kernel entry"), (9, "setup done"), (5, "first K issue"), (3, "last PV done"), (4, "O read+written"), (1, "CTA end")]:
+for k, name in [(8, "kernel entry"), (9, "setup done"), (5, "first K issue"), (3, "last PV done"),
+                (11, "pieces staging"), (10, "pieces landed"), (4, "O read+written"), (1, "CTA end")]:
     v = rel(k)
     ok = cta[:, k] > 0
     if k == 8:
