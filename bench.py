@@ -43,7 +43,7 @@ sys.path.insert(0, ROOT)
 # C2
 B, T, H, D, L, V = 8, 64, 32, 128, 2048, 32000
 WIDTH, DEPTH = 8, 8            # 8 root-to-leaf paths, trimmed to exactly 64 nodes
-LAUNCHES_PER_STEP = 6          # append, masks, K1, K3 argmax, K3 walk, compact
+LAUNCHES_PER_STEP = 4          # append+masks, K1, K3 argmax, K3 walk+K2 compact
 METRIC = "tree-verify tokens/s"
 UNIT = "tokens/s"
 
@@ -278,17 +278,15 @@ def main():
 
     k1_events = []
 
-    def pre(qq, kn, vn, tk, pr, nd):
-        _capi.kv_append(kn, vn, P, nd, kc, vc)
-        _capi.build_masks(pr, nd, out=mask_buf)
+    def pre(qq, kn, vn, tk, pr, nd):   # K2 append + masks (one launch)
+        _capi.tree_prepare(kn, vn, P, nd, kc, vc, pr, out=mask_buf)
 
     def k1(qq, kn, vn, tk, pr, nd):
         _capi.tree_attention(qq, kc, vc, mask_buf, P, nd, out=out, workspace=ws_attn)
 
-    def post(qq, kn, vn, tk, pr, nd):
-        _, ver, ids, ln = _capi.verify_greedy(logits, tk, pr, nd, workspace=ws_ver,
-                                              want_argmax=False, out=vout)
-        _capi.kv_compact(ids, ln, P, kc, vc)
+    def post(qq, kn, vn, tk, pr, nd):  # K3 argmax, then the walk fused with K2 compaction
+        _capi.verify_greedy_compact(logits, tk, pr, nd, P, kc, vc, workspace=ws_ver,
+                                    want_argmax=False, out=vout)
 
     resident = (q, knew, vnew, tok, par, nn)
 

@@ -107,6 +107,13 @@ st_status st_kv_append(st_dtype dtype, int B, int T, int Hkv, int D, int64_t Lma
                        const void* k_new, const void* v_new, const int32_t* prefix_len,
                        const int32_t* n_nodes, void* k_cache, void* v_cache, void* stream);
 
+/* st_kv_append and st_build_masks in one launch (the two independent steps
+ * that precede K1): same effects as the two calls. */
+st_status st_tree_prepare(st_dtype dtype, int B, int T, int Hkv, int D, int64_t Lmax,
+                          const void* k_new, const void* v_new, const int32_t* prefix_len,
+                          const int32_t* n_nodes, void* k_cache, void* v_cache,
+                          const int32_t* parent, int W, uint64_t* mask, void* stream);
+
 /* Compact: keep the accepted root-to-node path, in place, for n_layers layers
  * (cache pointer of layer l = base + l * layer_stride elements):
  *   cache[b][h][P[b] + k] = cache[b][h][P[b] + ids[b][k]]   for k < n_keep[b]
@@ -142,6 +149,21 @@ st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32
                            const int32_t* budget, int32_t eos, int32_t* argmax,
                            int32_t* verified, int32_t* ids, int32_t* len, void* workspace,
                            void* stream);
+
+/* st_verify_greedy followed by st_kv_compact of the accepted rows
+ * (n_keep = len) over n_layers layers, in two launches instead of three: the
+ * walk is fused into the compaction kernel (every block of a request repeats
+ * the request's walk in shared memory, then moves its share of the KV heads).
+ * Same outputs as the two calls; requires T <= 1024, D * sizeof(dtype) a
+ * multiple of 16 and new_prefix_len (optional) not aliasing prefix_len. */
+st_status st_verify_greedy_compact(const float* logits, int B, int T, int V, const int32_t* tokens,
+                                   const int32_t* parent, const int32_t* n_nodes,
+                                   const int32_t* budget, int32_t eos, int32_t* argmax,
+                                   int32_t* verified, int32_t* ids, int32_t* len, void* workspace,
+                                   st_dtype dtype, int Hkv, int D, int64_t Lmax, int n_layers,
+                                   int64_t layer_stride, const int32_t* prefix_len,
+                                   int32_t* new_prefix_len, void* k_cache, void* v_cache,
+                                   void* stream);
 
 /* The walk alone, given per-node LLM outputs [B][T] (what the reference's
  * verify() consumes, token_tree.cpp:153-175); same outputs as st_verify_greedy. */

@@ -59,9 +59,12 @@ SIGNATURES = {
     "st_tree_attention_path": (_I, [C.POINTER(AttnArgs)]),
     "st_kv_append": (_I, [_I, _I, _I, _I, _I, _I64, _V, _V, _V, _V, _V, _V, _V]),
     "st_kv_compact": (_I, [_I, _I, _I, _I, _I64, _I, _I64, _V, _I, _V, _V, _V, _V, _V, _V]),
+    "st_tree_prepare": (_I, [_I, _I, _I, _I, _I, _I64, _V, _V, _V, _V, _V, _V, _V, _I, _V, _V]),
     "st_heads_gather_layout": (_I, [_I, _I, _I, _I, _I, _I, _V, _V, _V]),
     "st_verify_workspace_size": (_Z, [_I, _I]),
     "st_verify_greedy": (_I, [_V, _I, _I, _I, _V, _V, _V, _V, C.c_int32, _V, _V, _V, _V, _V, _V]),
+    "st_verify_greedy_compact": (_I, [_V, _I, _I, _I, _V, _V, _V, _V, C.c_int32, _V, _V, _V, _V, _V,
+                                      _I, _I, _I, _I64, _I, _I64, _V, _V, _V, _V, _V]),
     "st_verify_outputs": (_I, [_V, _I, _I, _V, _V, _V, _V, C.c_int32, _V, _V, _V, _V]),
     "st_verify_mss": (_I, [_V, _V, _I, _I, _I, _V, _V, _V, _F, _V, _I, _V, _V, _V, _V]),
     "st_build_masks": (_I, [_V, _V, _I, _I, _I, _V, _V]),
@@ -190,6 +193,18 @@ def kv_append(k_new, v_new, prefix_len, n_nodes, k_cache, v_cache, stream=None):
                              _ptr(v_cache), _stream(stream)))
 
 
+def tree_prepare(k_new, v_new, prefix_len, n_nodes, k_cache, v_cache, parent, W=None, out=None,
+                 stream=None):
+    """K2 append + ancestor masks in one launch; returns the [B, T, W] int64 masks."""
+    B, T, Hkv, D = k_new.shape
+    W = W or (T + 63) // 64
+    mask = out if out is not None else torch.empty((B, T, W), dtype=torch.int64, device=k_new.device)
+    check(lib().st_tree_prepare(DTYPES[k_new.dtype], B, T, Hkv, D, k_cache.shape[-2], _ptr(k_new),
+                                _ptr(v_new), _ptr(prefix_len), _ptr(n_nodes), _ptr(k_cache),
+                                _ptr(v_cache), _ptr(parent), W, _ptr(mask), _stream(stream)))
+    return mask
+
+
 def kv_compact(ids, n_keep, prefix_len, k_cache, v_cache, new_prefix_len=None, stream=None):
     """k_cache/v_cache: [L,B,Hkv,Lmax,D] (layer-major) or [B,Hkv,Lmax,D]."""
     if k_cache.dim() == 4:
@@ -239,6 +254,36 @@ def verify_greedy(logits, tokens, parent, n_nodes, budget=None, eos=-1, workspac
     check(lib().st_verify_greedy(_ptr(logits), B, T, V, _ptr(tokens), _ptr(parent), _ptr(n_nodes),
                                  _ptr(budget), int(eos), _ptr(argmax), _ptr(verified), _ptr(ids),
                                  _ptr(length), _ptr(workspace), _stream(stream)))
+    return argmax, verified, ids, length
+
+
+def verify_greedy_compact(logits, tokens, parent, n_nodes, prefix_len, k_cache, v_cache,
+                          budget=None, eos=-1, workspace=None, new_prefix_len=None, stream=None,
+                          want_argmax=True, out=None):
+    """verify_greedy + kv_compact(ids, len) in two launches (walk fused into the
+    compaction). k_cache/v_cache: [L,B,Hkv,Lmax,D] or [B,Hkv,Lmax,D]."""
+    B, T, V = logits.shape
+    dev = logits.device
+    argmax = torch.empty((B, T), dtype=torch.int32, device=dev) if want_argmax else None
+    if out is None:
+        verified = torch.full((B, T + 1), -1, dtype=torch.int32, device=dev)
+        ids = torch.full((B, T + 1), -1, dtype=torch.int32, device=dev)
+        length = torch.zeros(B, dtype=torch.int32, device=dev)
+    else:
+        verified, ids, length = out
+    if workspace is None:
+        workspace = verify_workspace(B, T, dev)
+    if k_cache.dim() == 4:
+        n_layers, layer_stride = 1, k_cache.numel()
+        _, Hkv, Lmax, D = k_cache.shape
+    else:
+        n_layers, layer_stride = k_cache.shape[0], k_cache[0].numel()
+        _, Hkv, Lmax, D = k_cache.shape[1:]
+    check(lib().st_verify_greedy_compact(
+        _ptr(logits), B, T, V, _ptr(tokens), _ptr(parent), _ptr(n_nodes), _ptr(budget), int(eos),
+        _ptr(argmax), _ptr(verified), _ptr(ids), _ptr(length), _ptr(workspace),
+        DTYPES[k_cache.dtype], Hkv, D, Lmax, n_layers, layer_stride, _ptr(prefix_len),
+        _ptr(new_prefix_len), _ptr(k_cache), _ptr(v_cache), _stream(stream)))
     return argmax, verified, ids, length
 
 

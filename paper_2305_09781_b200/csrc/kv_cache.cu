@@ -19,6 +19,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "tree_masks.cuh"
 
 namespace st {
 namespace {
@@ -31,14 +32,11 @@ constexpr int kAppendThreads = 128;
 constexpr int kAppendUnroll = 4;
 
 template <class V>
-__global__ void __launch_bounds__(kAppendThreads)
-kv_append_kernel(const char* __restrict__ k_new, const char* __restrict__ v_new,
-                 const int32_t* __restrict__ prefix_len, const int32_t* __restrict__ n_nodes,
-                 char* __restrict__ k_cache, char* __restrict__ v_cache, int T, int Hkv,
-                 int row_vecs, int64_t Lmax) {
-    pdl_wait();
-    pdl_trigger();
-    const int b = blockIdx.y, u = blockIdx.x;
+__device__ __forceinline__ void kv_append_row(const char* __restrict__ k_new, const char* __restrict__ v_new,
+                                              const int32_t* __restrict__ prefix_len,
+                                              const int32_t* __restrict__ n_nodes,
+                                              char* __restrict__ k_cache, char* __restrict__ v_cache,
+                                              int T, int Hkv, int row_vecs, int64_t Lmax, int b, int u) {
     if (u >= n_nodes[b]) return;
     const int64_t P = prefix_len[b];
     const int total = Hkv * row_vecs;
@@ -67,6 +65,37 @@ kv_append_kernel(const char* __restrict__ k_new, const char* __restrict__ v_new,
             }
         }
     }
+}
+
+template <class V>
+__global__ void __launch_bounds__(kAppendThreads)
+kv_append_kernel(const char* __restrict__ k_new, const char* __restrict__ v_new,
+                 const int32_t* __restrict__ prefix_len, const int32_t* __restrict__ n_nodes,
+                 char* __restrict__ k_cache, char* __restrict__ v_cache, int T, int Hkv,
+                 int row_vecs, int64_t Lmax) {
+    pdl_wait();
+    pdl_trigger();
+    kv_append_row<V>(k_new, v_new, prefix_len, n_nodes, k_cache, v_cache, T, Hkv, row_vecs, Lmax,
+                     blockIdx.y, blockIdx.x);
+}
+
+// st_tree_prepare: blocks x < T append tree row x of request y; the remaining
+// ceil(T / kAppendThreads) blocks build request y's masks.
+template <class V>
+__global__ void __launch_bounds__(kAppendThreads)
+tree_prepare_kernel(const char* __restrict__ k_new, const char* __restrict__ v_new,
+                    const int32_t* __restrict__ prefix_len, const int32_t* __restrict__ n_nodes,
+                    char* __restrict__ k_cache, char* __restrict__ v_cache, int T, int Hkv,
+                    int row_vecs, int64_t Lmax, const int32_t* __restrict__ parent, int W,
+                    uint64_t* __restrict__ mask) {
+    extern __shared__ int s_par[];  // T ints (mask blocks stage the parent row)
+    pdl_wait();
+    pdl_trigger();
+    if ((int)blockIdx.x < T)
+        kv_append_row<V>(k_new, v_new, prefix_len, n_nodes, k_cache, v_cache, T, Hkv, row_vecs, Lmax,
+                         blockIdx.y, blockIdx.x);
+    else
+        build_masks_block(parent, n_nodes, T, W, mask, blockIdx.x - T, blockIdx.y, s_par);
 }
 
 // One block per (layer, b): rows k = 1..n_keep-1 copied sequentially.
@@ -128,6 +157,33 @@ st_status st_kv_append(st_dtype dtype, int B, int T, int Hkv, int D, int64_t Lma
                                (const char*)v_new, prefix_len, n_nodes, (char*)k_cache,
                                (char*)v_cache, T, Hkv, (int)(vec ? row_bytes / 16 : row_bytes),
                                Lmax));
+    ST_LAUNCH_CHECK();
+    return ST_OK;
+}
+
+st_status st_tree_prepare(st_dtype dtype, int B, int T, int Hkv, int D, int64_t Lmax,
+                          const void* k_new, const void* v_new, const int32_t* prefix_len,
+                          const int32_t* n_nodes, void* k_cache, void* v_cache,
+                          const int32_t* parent, int W, uint64_t* mask, void* stream) {
+    if (st_status e = st::require_device()) return e;
+    ST_CHECK_ARG(B >= 0 && T >= 1 && Hkv >= 1 && D >= 1 && Lmax >= T, ST_ERR_SHAPE_MISMATCH,
+                 "bad shape");
+    ST_CHECK_ARG(W >= (T + 63) / 64 && W <= 32, ST_ERR_SHAPE_MISMATCH,
+                 "bad shape (need ceil(T/64) <= W <= 32)");
+    ST_CHECK_ARG(st::dtype_size(dtype) != 0, ST_ERR_INVALID_ARGUMENT, "bad dtype");
+    if (B == 0) return ST_OK;
+    ST_CHECK_ARG(k_new && v_new && prefix_len && n_nodes && k_cache && v_cache && parent && mask,
+                 ST_ERR_INVALID_ARGUMENT, "null pointer");
+    ST_CHECK_ARG(B <= 65535 && T <= 12288, ST_ERR_SHAPE_MISMATCH, "too many requests or nodes");
+    const int64_t row_bytes = (int64_t)D * st::dtype_size(dtype);
+    const dim3 grid(T + (T + st::kAppendThreads - 1) / st::kAppendThreads, B);
+    const size_t smem = (size_t)T * sizeof(int32_t);
+    const bool vec = row_bytes % 16 == 0;
+    ST_CUDA_TRY(st::launch_pdl(vec ? st::tree_prepare_kernel<int4> : st::tree_prepare_kernel<char>,
+                               grid, dim3(st::kAppendThreads), smem, st::as_stream(stream),
+                               (const char*)k_new, (const char*)v_new, prefix_len, n_nodes,
+                               (char*)k_cache, (char*)v_cache, T, Hkv,
+                               (int)(vec ? row_bytes / 16 : row_bytes), Lmax, parent, W, mask));
     ST_LAUNCH_CHECK();
     return ST_OK;
 }

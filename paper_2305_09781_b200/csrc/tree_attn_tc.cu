@@ -93,10 +93,11 @@ template <int M> struct Cfg {
     static constexpr uint32_t OFF_V = OFF_K + KSTAGES * TILE_BYTES;
     static constexpr uint32_t OFF_BAR = OFF_V + VSTAGES * TILE_BYTES;
     // A split pair's head owner stages the pair's other pieces into the drained
-    // K ring: (m, l) block, then M rows of O with a 16-byte pad per row (528 B
-    // stride: consecutive rows start 4 banks apart).
-    static constexpr uint32_t PIECE_ROW = HD * 4 + 16;
-    static constexpr uint32_t PIECE_SMEM = (1024 + M * PIECE_ROW + 127) / 128 * 128;
+    // K ring: the (m, l) block (1 KB), then the piece's M rows of O as four
+    // TMA boxes of [M rows][32 floats] with SWIZZLE_128B (bank-conflict-free
+    // row-per-thread reads).
+    static constexpr uint32_t PIECE_BOX = M * 128;
+    static constexpr uint32_t PIECE_SMEM = 1024 + 4 * PIECE_BOX;
     static constexpr int STAGED_PIECES = (KSTAGES * TILE_BYTES) / PIECE_SMEM;
     static constexpr uint32_t OFF_TAB = OFF_BAR + 256;     // per-request tile table
     static constexpr uint32_t OFF_PIECES = OFF_TAB + (kTabB + 4) * 4;  // head owner's piece list
@@ -289,7 +290,8 @@ __device__ __forceinline__ void store_row(T* dst_row, const float* v, float scal
 template <class T, int M>
 __global__ void __launch_bounds__(Cfg<M>::THREADS, 1)
 tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_v, const TcParams p) {
+                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_part,
+                    const TcParams p) {
     using C = Cfg<M>;
     constexpr int KS = C::KSTAGES, VS = C::VSTAGES, QS = C::QSTAGES;
     constexpr int SPLIT = C::SPLIT;          // threads per query row in a warp (2 for M=64)
@@ -336,6 +338,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (warp == SW && lane == 0) {
         prefetch_tmap(&tm_q);
         prefetch_tmap(&tm_k);
+        prefetch_tmap(&tm_part);
     }
     if (warp == SW + 1 && lane == 0) prefetch_tmap(&tm_v);
     if (warp == SW + 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
@@ -432,42 +435,42 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             const uint32_t pend = ls.pair_start + (uint32_t)ls.ntiles;
             if (ls.pair_start >= t_begin && pend > t_end) {
                 const uint32_t kc = (uint32_t)(t_end - t_begin);  // K tiles this CTA loaded
-                const int n = __ldg(p.n_nodes + ls.b);
-                const int rows = n < M ? n : M;
                 if (lane == 0) {
                     // piece list for the softmax warps; every piece's flag is
-                    // awaited here (normally long set) and re-armed for the
-                    // next launch, then the drained K ring receives the first
-                    // STAGED_PIECES pieces
+                    // awaited (and re-armed for the next launch) before its
+                    // copy is issued into the drained K ring (the first
+                    // STAGED_PIECES pieces) or, beyond those, before the final
+                    // arrival that releases the softmax warps to read it from L2
                     int* pieces = reinterpret_cast<int*>(smem + C::OFF_PIECES);
                     int np = 0;
                     for (uint32_t c2 = blockIdx.x + 1; c2 < G && np < kMaxPieces; ++c2) {
                         const uint32_t rs = range_start(c2, sched, G);
                         if (rs >= pend) break;
                         if (range_start(c2 + 1, sched, G) == rs) continue;  // empty range
-                        wait_flag_gpu(p.flags + c2);
-                        p.flags[c2] = 0u;
                         pieces[1 + np++] = (int)c2;
                     }
                     pieces[0] = np;
+                    const int ns = np < C::STAGED_PIECES ? np : C::STAGED_PIECES;
+                    mbar_expect_tx(merge_full, (uint32_t)ns * (1024u + 4u * C::PIECE_BOX));
                     for (uint32_t st = 0; st < (uint32_t)KS && st < kc; ++st) {
                         const uint32_t k = kc - 1 - ((kc - 1 - st) % KS);  // last use of stage st
                         mbar_wait(k_empty + st, (k / KS) & 1);
                     }
-                    fence_proxy_async_global();
-                    const int ns = np < C::STAGED_PIECES ? np : C::STAGED_PIECES;
-                    mbar_arrive_expect_tx(merge_full, (uint32_t)ns * (1024u + (uint32_t)rows * HD * 4));
                     K1_GT(11);
-                }
-                __syncwarp();
-                const int* pieces = reinterpret_cast<const int*>(smem + C::OFF_PIECES);
-                const int ns = pieces[0] < C::STAGED_PIECES ? pieces[0] : C::STAGED_PIECES;
-                for (int i = 0; i < ns; ++i) {
-                    const float* piece = p.partial + (long long)pieces[1 + i] * SLOT_FLOATS;
-                    uint8_t* dst = sm_k + i * C::PIECE_SMEM;
-                    if (lane == 0) bulk_load(dst, piece + 128 * HD, 1024, merge_full);
-                    for (int r = lane; r < rows; r += 32)
-                        bulk_load(dst + 1024 + r * C::PIECE_ROW, piece + r * HD, HD * 4, merge_full);
+                    for (int i = 0; i < np; ++i) {
+                        const int c2 = pieces[1 + i];
+                        wait_flag_gpu(p.flags + c2);
+                        p.flags[c2] = 0u;
+                        if (i < ns) {
+                            fence_proxy_async_global();
+                            uint8_t* dst = sm_k + i * C::PIECE_SMEM;
+                            bulk_load(dst, p.partial + (long long)c2 * SLOT_FLOATS + 128 * HD, 1024, merge_full);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j)
+                                tma_load_2d(dst + 1024 + j * C::PIECE_BOX, &tm_part, merge_full, 32 * j, c2 * 130);
+                        }
+                    }
+                    mbar_arrive(merge_full);
                 }
             }
         }
@@ -853,13 +856,16 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             const float mp = staged ? piece[r] : __ldcg(piece + 128 * HD + r);
                             if (mp == -INFINITY) continue;
                             const float wp = ex2((mp - m_fin) * c);
-                            const float4* pp = staged
-                                ? reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(piece) + 1024 +
-                                                                  r * C::PIECE_ROW + dc * 4)
-                                : reinterpret_cast<const float4*>(piece + r * HD + dc);
+                            // staged: box dc/32 of the piece, row r, 16-byte chunk k
+                            // at k ^ (r & 7) (SWIZZLE_128B)
+                            const uint8_t* sbox = reinterpret_cast<const uint8_t*>(piece) + 1024 +
+                                                  (dc >> 5) * C::PIECE_BOX + r * 128;
+                            const float4* pp = reinterpret_cast<const float4*>(piece + r * HD + dc);
 #pragma unroll
                             for (int k = 0; k < 8; ++k) {
-                                const float4 x = staged ? pp[k] : __ldcg(pp + k);
+                                const float4 x = staged
+                                    ? *reinterpret_cast<const float4*>(sbox + ((k ^ (r & 7)) << 4))
+                                    : __ldcg(pp + k);
                                 ov[4 * k] = fmaf(x.x, wp, ov[4 * k]);
                                 ov[4 * k + 1] = fmaf(x.y, wp, ov[4 * k + 1]);
                                 ov[4 * k + 2] = fmaf(x.z, wp, ov[4 * k + 2]);
@@ -976,7 +982,7 @@ size_t tree_attention_tc_workspace(const st_attn_args* a) {
             attr = true;                                                                        \
         }                                                                                       \
         ST_CUDA_TRY(launch_pdl(tree_attn_tc_kernel<TT, MM>, dim3(G), dim3(Cfg<MM>::THREADS),     \
-                               Cfg<MM>::SMEM_BYTES, stream, tq, tk, tv, prm));                  \
+                               Cfg<MM>::SMEM_BYTES, stream, tq, tk, tv, tp, prm));              \
     } while (0)
 
 st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st_peer_out* po) {
@@ -1010,6 +1016,16 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
     prm.o = a->o;
     prm.lse = a->lse;
     prm.partial = reinterpret_cast<float*>(a->workspace);
+    CUtensorMap tp;  // the piece slots as rows of 128 floats (130 rows per CTA slot)
+    {
+        const uint64_t dims[2] = {(uint64_t)HD, (uint64_t)G * (SLOT_FLOATS / HD)};
+        const uint64_t strides[1] = {HD * 4ull};
+        const uint32_t box[2] = {32, (uint32_t)(a->T <= 64 ? 64 : 128)};
+        if (!encode(&tp, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, prm.partial, dims, strides, box)) {
+            set_error("st_tree_attention: cuTensorMapEncodeTiled(workspace) failed");
+            return ST_ERR_CUDA;
+        }
+    }
     prm.ml_xchg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(a->workspace) +
                                            align_up((size_t)G * SLOT_FLOATS * sizeof(float), 256));
     prm.flags = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(prm.ml_xchg) +

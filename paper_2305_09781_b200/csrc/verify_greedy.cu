@@ -22,6 +22,7 @@
 #include <cfloat>
 
 #include "common.cuh"
+#include "tree_masks.cuh"
 
 namespace st {
 namespace {
@@ -49,6 +50,10 @@ __device__ void walk_warp(const int32_t* outs, const int32_t* __restrict__ token
     int32_t* vrow = verified + (int64_t)b * (T + 1);
     int32_t* irow = ids + (int64_t)b * (T + 1);
     int m = 0, cur = 0;
+    if (n <= 0) {  // no tree: nothing accepted
+        if (lane == 0) len[b] = 0;
+        return;
+    }
     if (n <= kWalkMax) {
         for (int v = lane; v < n; v += 32) {
             s_out[v] = coherent ? __ldcg(am + v) : am[v];
@@ -134,8 +139,9 @@ constexpr int kSplit = 4;   // blocks per logits row
 constexpr int kUnroll = 8;  // float4 loads in flight per thread (a 4000-float slice in one batch)
 
 // Phase 1: stream every live node's logits once; kSplit blocks per row each
-// reduce their slice to one order-preserving key and fold it in with
-// atomicMax (order-independent -> deterministic). No fences or tickets.
+// reduce their slice to one order-preserving key, written to its own slot
+// keys[b][u][part] (no atomics, nothing to reset; the consumer takes the max
+// of the kSplit keys — order-independent, hence deterministic).
 __global__ void __launch_bounds__(kThreads)
 greedy_argmax_kernel(const float* __restrict__ logits, int T, int V,
                      const int32_t* __restrict__ n_nodes, unsigned long long* keys) {
@@ -188,16 +194,24 @@ greedy_argmax_kernel(const float* __restrict__ logits, int T, int V,
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < kThreads / 32; ++w) best = max(best, red[w]);
-        atomicMax(keys + (int64_t)b * T + u, best);
+        keys[((int64_t)b * T + u) * kSplit + part] = best;
     }
 }
 
+// Greedy output of node v: the best of its kSplit slice keys.
+__device__ __forceinline__ int resolve_key(const unsigned long long* keys, int64_t row) {
+    unsigned long long k = 0;
+#pragma unroll
+    for (int j = 0; j < kSplit; ++j) k = max(k, __ldcg(keys + row * kSplit + j));
+    return key_index(k);
+}
+
 // Phase 2 (launched with programmatic dependent launch): one warp per request
-// resolves the argmax keys (resetting them for the next call), then walks.
+// resolves the argmax keys, then walks.
 __global__ void __launch_bounds__(32)
 greedy_walk_kernel(int T, const int32_t* __restrict__ tokens, const int32_t* __restrict__ parent,
                    const int32_t* __restrict__ n_nodes, const int32_t* __restrict__ budget,
-                   int32_t eos, int32_t* __restrict__ argmax_out, unsigned long long* keys,
+                   int32_t eos, int32_t* __restrict__ argmax_out, const unsigned long long* keys,
                    int32_t* argmax_ws, int32_t* __restrict__ verified, int32_t* __restrict__ ids,
                    int32_t* __restrict__ len) {
     pdl_wait();
@@ -207,9 +221,7 @@ greedy_walk_kernel(int T, const int32_t* __restrict__ tokens, const int32_t* __r
     const int n = n_nodes[b];
     int32_t* am = argmax_ws + (int64_t)b * T;
     for (int v = lane; v < n; v += 32) {
-        unsigned long long* kp = keys + (int64_t)b * T + v;
-        const int a = key_index(*kp);
-        *kp = 0ull;  // reset for the next call
+        const int a = resolve_key(keys, (int64_t)b * T + v);
         am[v] = a;
         if (argmax_out) argmax_out[(int64_t)b * T + v] = a;
     }
@@ -218,43 +230,134 @@ greedy_walk_kernel(int T, const int32_t* __restrict__ tokens, const int32_t* __r
               s_out, s_next);
 }
 
-// One thread per (request, node). The request's parent row is staged in
-// shared memory first; the walk up the parent chain (ids strictly decrease)
-// then emits the ancestor-or-self bits word by word, high word first, so no
-// per-thread word array is needed (nothing spills to local memory).
+// ------------------------------------------------ K3 walk fused with K2 ---
+// Walk + compaction in one launch (st_verify_greedy_compact): block (b, y)
+// resolves request b's greedy outputs, walks its tree in shared memory (every
+// block of the request repeats this tiny walk, so no grid-wide dependency is
+// needed), then moves the accepted rows of its `hpb` KV heads of one layer:
+//   cache[b][h][P + k] = cache[b][h][P + ids[k]],  k = 1 .. len-1.
+// ids are strictly increasing with ids[k] >= k, so a destination row k is
+// never a source of a later k; within a chunk of rows every source is loaded
+// before any destination is stored (one barrier), and chunks go in increasing
+// k — no sequential per-row chain. Block (b, 0) writes the walk's outputs.
+constexpr int kWcThreads = 256;
+constexpr int kWcVecs = 4;       // 16-byte vectors in flight per thread per chunk
+
+template <class V>
+__global__ void __launch_bounds__(kWcThreads)
+walk_compact_kernel(int T, const int32_t* __restrict__ tokens, const int32_t* __restrict__ parent,
+                    const int32_t* __restrict__ n_nodes, const int32_t* __restrict__ budget,
+                    int32_t eos, int32_t* __restrict__ argmax_out, const unsigned long long* keys,
+                    int32_t* __restrict__ verified, int32_t* __restrict__ ids,
+                    int32_t* __restrict__ len, char* k_cache, char* v_cache, int Hkv,
+                    int row_vecs, int64_t Lmax, int nhc, int hpb, int64_t layer_stride_bytes,
+                    const int32_t* __restrict__ prefix_len, int32_t* __restrict__ new_prefix_len) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ int s_out[kWalkMax], s_next[kWalkMax], s_ver[kWalkMax + 1], s_ids[kWalkMax + 1];
+    __shared__ int s_len, s_full;
+    const int b = blockIdx.x, layer = blockIdx.y / nhc, hc = blockIdx.y % nhc;
+    const int n = n_nodes[b];
+    const bool lead = blockIdx.y == 0;
+    const int32_t* tok = tokens + (int64_t)b * T;
+    const int32_t* par = parent + (int64_t)b * T;
+    for (int v = threadIdx.x; v < n; v += kWcThreads) {
+        const int a = resolve_key(keys, (int64_t)b * T + v);
+        s_out[v] = a;
+        s_next[v] = -1;
+        if (lead && argmax_out) argmax_out[(int64_t)b * T + v] = a;
+    }
+    __syncthreads();
+    for (int v = 1 + threadIdx.x; v < n; v += kWcThreads) {
+        const int u = par[v];
+        if (tok[v] == s_out[u]) s_next[u] = v;  // children have unique tokens: one writer
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int m = 0, cur = 0;
+        s_ids[0] = 0;
+        for (int nx = n > 0 ? s_next[0] : -1; nx >= 0; nx = s_next[cur]) {
+            s_ver[m] = s_out[cur];
+            s_ids[m + 1] = nx;
+            cur = nx;
+            ++m;
+        }
+        s_ver[m] = n > 0 ? s_out[cur] : 0;  // bonus token
+        s_full = n > 0 ? m + 1 : 0;
+        int L = s_full;
+        if (budget && L > budget[b]) L = budget[b] > 0 ? budget[b] : 0;
+        if (eos >= 0) {
+            for (int k = 0; k < L; ++k)
+                if (s_ver[k] == eos) { L = k + 1; break; }
+        }
+        s_len = L;
+    }
+    __syncthreads();
+    const int L = s_len;
+    const int64_t P = prefix_len[b];
+    if (lead) {
+        int32_t* vrow = verified + (int64_t)b * (T + 1);
+        int32_t* irow = ids + (int64_t)b * (T + 1);
+        // the whole walk (path + bonus), as st_verify_greedy writes it; len
+        // carries the budget / EOS truncation
+        for (int k = threadIdx.x; k < s_full; k += kWcThreads) {
+            vrow[k] = s_ver[k];
+            irow[k] = s_ids[k];
+        }
+        if (threadIdx.x == 0) {
+            len[b] = L;
+            if (new_prefix_len) new_prefix_len[b] = (int32_t)(P + L);
+        }
+    }
+    // ---- compaction of rows 1..L-1 for heads [hc*hpb, hc*hpb + hpb) of this layer ----
+    const int h0 = hc * hpb, nh = min(hpb, Hkv - h0);
+    if (L <= 1 || nh <= 0) return;
+    char* kl = k_cache + layer * layer_stride_bytes;
+    char* vl = v_cache + layer * layer_stride_bytes;
+    const int per_row = nh * row_vecs;                        // vectors of one row, all heads
+    const int rows_chunk = max(1, kWcThreads * kWcVecs / (2 * per_row));
+    for (int k0 = 1; k0 < L; k0 += rows_chunk) {
+        const int k1 = min(L, k0 + rows_chunk);
+        const int total = (k1 - k0) * per_row;
+        V kx[kWcVecs], vx[kWcVecs];
+        int64_t dst[kWcVecs];
+#pragma unroll
+        for (int r = 0; r < kWcVecs; ++r) {
+            const int i = threadIdx.x + r * kWcThreads;
+            dst[r] = -1;
+            if (i < total) {
+                const int kk = k0 + i / per_row, rem = i % per_row;
+                const int h = h0 + rem / row_vecs, e = rem % row_vecs;
+                const int src = s_ids[kk];
+                if (src != kk) {
+                    const int64_t base = ((int64_t)b * Hkv + h) * Lmax + P;
+                    const int64_t so = (base + src) * row_vecs + e;
+                    dst[r] = (base + kk) * row_vecs + e;
+                    kx[r] = reinterpret_cast<const V*>(kl)[so];
+                    vx[r] = reinterpret_cast<const V*>(vl)[so];
+                }
+            }
+        }
+        __syncthreads();  // every source of this chunk read before any store
+#pragma unroll
+        for (int r = 0; r < kWcVecs; ++r) {
+            if (dst[r] >= 0) {
+                reinterpret_cast<V*>(kl)[dst[r]] = kx[r];
+                reinterpret_cast<V*>(vl)[dst[r]] = vx[r];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// One thread per (request, node): tree_masks.cuh.
 __global__ void build_masks_kernel(const int32_t* __restrict__ parent,
                                    const int32_t* __restrict__ n_nodes, int T, int W,
                                    uint64_t* __restrict__ mask) {
     extern __shared__ int s_par[];
     pdl_wait();
     pdl_trigger();
-    const int b = blockIdx.y;
-    const int u = blockIdx.x * blockDim.x + threadIdx.x;
-    const int n = n_nodes[b];
-    const int upto = min(n, (int)((blockIdx.x + 1) * blockDim.x));  // nodes this block needs
-    const int32_t* par = parent + (int64_t)b * T;
-    for (int v = threadIdx.x; v < upto; v += blockDim.x) s_par[v] = par[v];
-    __syncthreads();
-    if (u >= T) return;
-    uint64_t* mu = mask + ((int64_t)b * T + u) * W;
-    int wi = W - 1;
-    if (u < n) {
-        uint64_t acc = 0;
-        for (int v = u; v >= 0;) {
-            const int vw = v >> 6;
-            while (wi > vw) {
-                mu[wi] = acc;
-                acc = 0;
-                --wi;
-            }
-            acc |= 1ull << (v & 63);
-            const int pv = s_par[v];
-            v = pv < v ? pv : -1;  // preorder: parent id < child id (stop on malformed input)
-        }
-        mu[wi] = acc;
-        --wi;
-    }
-    for (; wi >= 0; --wi) mu[wi] = 0;
+    build_masks_block(parent, n_nodes, T, W, mask, blockIdx.x, blockIdx.y, s_par);
 }
 
 }  // namespace
@@ -263,8 +366,8 @@ __global__ void build_masks_kernel(const int32_t* __restrict__ parent,
 extern "C" {
 
 size_t st_verify_workspace_size(int B, int T) {
-    // keys [B][T] u64 | tickets [B] | argmax scratch [B][T]   (zeroed once by the caller)
-    return (size_t)B * T * 8 + (size_t)B * sizeof(unsigned) + (size_t)B * T * sizeof(int32_t) + 512;
+    // slice keys [B][T][kSplit] u64 | argmax scratch [B][T]
+    return (size_t)B * T * st::kSplit * 8 + (size_t)B * T * sizeof(int32_t) + 512;
 }
 
 st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32_t* tokens,
@@ -280,9 +383,7 @@ st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32
     ST_CHECK_ARG((reinterpret_cast<uintptr_t>(workspace) & 7) == 0, ST_ERR_INVALID_ARGUMENT,
                  "workspace must be 8-byte aligned");
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(workspace);
-    unsigned* tickets = reinterpret_cast<unsigned*>(keys + (size_t)B * T);
-    int32_t* scratch = reinterpret_cast<int32_t*>(
-        (reinterpret_cast<uintptr_t>(tickets + B) + 15) & ~uintptr_t(15));
+    int32_t* scratch = reinterpret_cast<int32_t*>(keys + (size_t)B * T * st::kSplit);
     const dim3 grid(st::kSplit, T, B);
     auto strm = st::as_stream(stream);
     ST_CUDA_TRY(st::launch_pdl(st::greedy_argmax_kernel, grid, dim3(st::kThreads), 0, strm, logits,
@@ -291,6 +392,50 @@ st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32
     ST_CUDA_TRY(st::launch_pdl(st::greedy_walk_kernel, dim3(B), dim3(32), 0, strm, T, tokens,
                                parent, n_nodes, budget, eos, argmax, keys, scratch, verified, ids,
                                len));
+    ST_LAUNCH_CHECK();
+    return ST_OK;
+}
+
+st_status st_verify_greedy_compact(const float* logits, int B, int T, int V, const int32_t* tokens,
+                                   const int32_t* parent, const int32_t* n_nodes,
+                                   const int32_t* budget, int32_t eos, int32_t* argmax,
+                                   int32_t* verified, int32_t* ids, int32_t* len, void* workspace,
+                                   st_dtype dtype, int Hkv, int D, int64_t Lmax, int n_layers,
+                                   int64_t layer_stride, const int32_t* prefix_len,
+                                   int32_t* new_prefix_len, void* k_cache, void* v_cache,
+                                   void* stream) {
+    if (st_status e = st::require_device()) return e;
+    ST_CHECK_ARG(B >= 0 && T >= 1 && V >= 1 && Hkv >= 1 && D >= 1 && n_layers >= 1,
+                 ST_ERR_SHAPE_MISMATCH, "bad shape");
+    ST_CHECK_ARG(st::dtype_size(dtype) != 0, ST_ERR_INVALID_ARGUMENT, "bad dtype");
+    if (B == 0) return ST_OK;
+    ST_CHECK_ARG(logits && tokens && parent && n_nodes && verified && ids && len && workspace &&
+                     prefix_len && k_cache && v_cache,
+                 ST_ERR_INVALID_ARGUMENT, "null pointer");
+    ST_CHECK_ARG(new_prefix_len != prefix_len, ST_ERR_INVALID_ARGUMENT,
+                 "new_prefix_len must not alias prefix_len");
+    ST_CHECK_ARG(B <= 65535 && T <= st::kWalkMax, ST_ERR_SHAPE_MISMATCH,
+                 "B <= 65535 and T <= 1024 (use st_verify_greedy + st_kv_compact)");
+    ST_CHECK_ARG((reinterpret_cast<uintptr_t>(workspace) & 7) == 0, ST_ERR_INVALID_ARGUMENT,
+                 "workspace must be 8-byte aligned");
+    const int64_t row_bytes = (int64_t)D * st::dtype_size(dtype);
+    ST_CHECK_ARG(row_bytes % 16 == 0, ST_ERR_SHAPE_MISMATCH, "D * sizeof(dtype) must be a multiple of 16");
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(workspace);
+    auto strm = st::as_stream(stream);
+    ST_CUDA_TRY(st::launch_pdl(st::greedy_argmax_kernel, dim3(st::kSplit, T, B), dim3(st::kThreads), 0,
+                               strm, logits, T, V, n_nodes, keys));
+    ST_LAUNCH_CHECK();
+    // heads per block: about 2 KB of K+V per accepted row per block
+    const int row_vecs = (int)(row_bytes / 16);
+    const int hpb = std::max(1, std::min(Hkv, 64 / row_vecs));
+    const int nhc = (Hkv + hpb - 1) / hpb;
+    ST_CHECK_ARG((int64_t)n_layers * nhc <= 65535, ST_ERR_SHAPE_MISMATCH, "too many layers x heads");
+    const int64_t es = (int64_t)st::dtype_size(dtype);
+    ST_CUDA_TRY(st::launch_pdl(st::walk_compact_kernel<int4>, dim3(B, n_layers * nhc),
+                               dim3(st::kWcThreads), 0, strm, T, tokens, parent, n_nodes, budget,
+                               eos, argmax, (const unsigned long long*)keys, verified, ids, len,
+                               (char*)k_cache, (char*)v_cache, Hkv, row_vecs, Lmax, nhc, hpb,
+                               layer_stride * es, prefix_len, new_prefix_len));
     ST_LAUNCH_CHECK();
     return ST_OK;
 }

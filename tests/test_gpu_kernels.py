@@ -257,3 +257,71 @@ def test_heads_gather_layout(capi):
     torch.cuda.synchronize()
     ref = g.permute(1, 2, 0, 3, 4).reshape(3, 7, 32, 128)
     assert torch.equal(out, ref)
+
+
+def test_tree_prepare_matches_append_and_masks(capi, restatement):
+    """st_tree_prepare (one launch) == st_kv_append + st_build_masks, bitwise."""
+    rng = np.random.default_rng(5)
+    trees = [restatement.merge(random_seqs(rng, 1, 20, 12, 20), 4096) for _ in range(3)]
+    tok, par, dep, n = pack(trees, 150)
+    B, T, Hkv, D, Lmax = 3, 150, 4, 128, 600
+    dev = "cuda"
+    kc = torch.randn(B, Hkv, Lmax, D, device=dev).half()
+    vc = torch.randn(B, Hkv, Lmax, D, device=dev).half()
+    knew = torch.randn(B, T, Hkv, D, device=dev).half()
+    vnew = torch.randn(B, T, Hkv, D, device=dev).half()
+    P = torch.tensor([5, 300, 0], dtype=torch.int32, device=dev)
+    nd, pd = torch.tensor(n, device=dev), torch.tensor(par, device=dev)
+    k1, v1 = kc.clone(), vc.clone()
+    capi.kv_append(knew, vnew, P, nd, k1, v1)
+    m1 = capi.build_masks(pd, nd, 3)
+    k2, v2 = kc.clone(), vc.clone()
+    m2 = capi.tree_prepare(knew, vnew, P, nd, k2, v2, pd, W=3)
+    torch.cuda.synchronize()
+    assert torch.equal(k1, k2) and torch.equal(v1, v2)
+    for b in range(B):
+        assert torch.equal(m1[b, : n[b]], m2[b, : n[b]])
+
+
+@pytest.mark.parametrize("layers,Hkv", [(1, 32), (2, 6)])
+def test_verify_greedy_compact_matches_separate(capi, restatement, layers, Hkv):
+    """st_verify_greedy_compact (walk fused into the compaction) == st_verify_greedy
+    followed by st_kv_compact(ids, len): outputs, argmax, caches and new prefix
+    lengths bitwise; long accepted paths exercise the chunked in-place move."""
+    rng = np.random.default_rng(9 + layers)
+    V, D, Lmax = 777, 128, 256
+    trees = []
+    for i in range(5):
+        seqs = width_depth_seqs(rng, int(rng.integers(0, 8)), 8, 2 if i else 1, 30 if i < 3 else 6)
+        trees.append(restatement.merge(seqs, 1024))
+    tok, par, dep, n = pack(trees)
+    B, T = tok.shape
+    logits = rng.standard_normal((B, T, V)).astype(np.float32)
+    for b in range(B):
+        for u in range(n[b]):
+            kids = [v for v in range(n[b]) if par[b, v] == u]
+            if kids and (b == 0 or rng.random() < 0.95):
+                logits[b, u, tok[b, kids[0]]] = 10.0
+    dev = "cuda"
+    lg, tk, pr, nd = (torch.tensor(x, device=dev) for x in (logits, tok, par, n))
+    P = torch.tensor(rng.integers(0, 100, B), dtype=torch.int32, device=dev)
+    kc = torch.randn(layers, B, Hkv, Lmax, D, device=dev).half()
+    vc = torch.randn(layers, B, Hkv, Lmax, D, device=dev).half()
+    for budget, eos in [(None, -1), (np.array([3, 40, 1, 2, 9], np.int32), -1), (None, int(tok[1, 2]))]:
+        bud = None if budget is None else torch.tensor(budget[:B], device=dev)
+        k1, v1, k2, v2 = kc.clone(), vc.clone(), kc.clone(), vc.clone()
+        a1, ver1, ids1, ln1 = capi.verify_greedy(lg, tk, pr, nd, bud, eos)
+        np1 = torch.zeros(B, dtype=torch.int32, device=dev)
+        capi.kv_compact(ids1, ln1, P, k1, v1, np1)
+        np2 = torch.zeros(B, dtype=torch.int32, device=dev)
+        a2, ver2, ids2, ln2 = capi.verify_greedy_compact(lg, tk, pr, nd, P, k2, v2, bud, eos,
+                                                         new_prefix_len=np2)
+        torch.cuda.synchronize()
+        assert torch.equal(ln1, ln2)
+        for b in range(B):   # argmax rows are defined for live nodes only
+            assert torch.equal(a1[b, : n[b]], a2[b, : n[b]])
+        assert torch.equal(ver1, ver2) and torch.equal(ids1, ids2)
+        assert torch.equal(np1, np2)
+        assert torch.equal(k1, k2) and torch.equal(v1, v2)
+        if budget is None and eos < 0:
+            assert int(ln1.max()) > 20  # several row chunks moved

@@ -9,3 +9,4 @@ timeout 120 python tools/k1_trace.py $OUT/$TAG.k1trace.raw > $OUT/$TAG.trace.txt
 ST_K1_SLACK=-1 timeout 120 python tools/k1_trace.py $OUT/$TAG.sk.k1trace.raw > $OUT/$TAG.sk.trace.txt 2>&1
 ST_K1_SLACK=-1 timeout 300 python bench.py --no-cpu-baseline > $OUT/$TAG.sk.bench.json 2> $OUT/$TAG.sk.bench.err
 timeout 120 python tools/c4_slice.py --out $OUT/$TAG.c4.json > $OUT/$TAG.c4.txt 2>&1
+timeout 120 python tools/k1_trace.py $OUT/$TAG.c4.raw --B 8 --T 61 --H 8 --L 2048 > $OUT/$TAG.c4trace.txt 2>&1
