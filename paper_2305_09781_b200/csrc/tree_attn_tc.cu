@@ -100,8 +100,13 @@ template <int M> struct Cfg {
     static constexpr uint32_t PIECE_SMEM = 1024 + 4 * PIECE_BOX;
     static constexpr int STAGED_PIECES = (KSTAGES * TILE_BYTES) / PIECE_SMEM;
     static constexpr uint32_t OFF_TAB = OFF_BAR + 256;     // per-request tile table
-    static constexpr uint32_t OFF_PIECES = OFF_TAB + (kTabB + 4) * 4;  // head owner's piece list
-    static constexpr uint32_t SMEM_BYTES = OFF_PIECES + (kMaxPieces + 1) * 4 + 1024;
+    // DUAL: (m, l) of both column halves of every row, exchanged per segment
+    static constexpr uint32_t OFF_XCHG = OFF_TAB + (kTabB + 4) * 4;
+    static constexpr uint32_t SMEM_BYTES = OFF_XCHG + (DUAL ? 2 * 128 * 2 * 4 : 0);
+    // the head owner's piece list sits at the end of the drained K ring
+    static constexpr uint32_t OFF_PIECES = OFF_K + KSTAGES * TILE_BYTES - (kMaxPieces + 1) * 4;
+    static_assert(STAGED_PIECES * PIECE_SMEM <= KSTAGES * TILE_BYTES - (kMaxPieces + 1) * 4,
+                  "piece list overlaps the staged pieces");
     static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
@@ -119,21 +124,21 @@ struct TcParams {
     unsigned long long* trace;  // optional pipeline trace of CTA 0 (ST_K1_TRACE)
     int aligned_slack;          // whole-pair schedule allowed within this many tiles of stream-K
     int trace_cta;              // CTA whose per-tile pipeline is traced (ST_K1_TRACE_CTA)
-    float* ml_xchg;             // DUAL: [gridDim.x][2][128][2] (m, l) of each column half
     // head-sharded output (st_tree_attention_allgather): rows go to every rank's
     // [B][T][H_out][D] buffer at head head_offset + h; null -> o with H_out = H
     void* const* o_peers;
     int world, head_offset, H_out;
 };
 
-constexpr int kTraceCta = 12;  // per-CTA globaltimer/clock slots of the ST_K1_TRACE dump
+constexpr int kTraceCta = 12;   // per-CTA globaltimer/clock slots of the ST_K1_TRACE dump
+constexpr int kTraceRows = 16;  // per-tile (rows 0-11) and per-segment (12-15) clock rows
 
 #define K1_GT(k)                                                                  \
     do {                                                                          \
         if (p.trace) {                                                            \
             unsigned long long gt_;                                               \
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt_));               \
-            p.trace[12 * 64 + kTraceCta * blockIdx.x + (k)] = gt_;                        \
+            p.trace[kTraceRows * 64 + kTraceCta * blockIdx.x + (k)] = gt_;                        \
         }                                                                         \
     } while (0)
 
@@ -209,7 +214,7 @@ __device__ Seg find_seg(const TcParams& p, const int* cum, uint32_t t, uint32_t 
 // in-kernel) unless every pair has the same tile count and whole-pair ranges
 // cost at most aligned_slack tiles more than perfect balance — then CTA c
 // takes pairs [c*Np/G, (c+1)*Np/G) and no pair is split.
-constexpr int kAlignedSlack = 6;
+constexpr int kAlignedSlack = 3;
 
 struct Sched {
     uint32_t total;
@@ -299,9 +304,10 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     constexpr int SW = C::SW;                // softmax warps; then K-TMA, V-TMA, MMA
     constexpr int COLS = BN / 2;             // S columns per thread per tile (one half)
     constexpr int DCOLS = HD / 2;            // output d columns per thread
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+    // SWIZZLE_128B tiles need 1024-byte alignment: the dynamic window starts
+    // after the 1 KB the hardware reserves per CTA (checked below)
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw;
     uint8_t* sm_q = smem + C::OFF_Q;
     uint8_t* sm_k = smem + C::OFF_K;
     uint8_t* sm_v = smem + C::OFF_V;
@@ -323,6 +329,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (threadIdx.x == 0) K1_GT(8);
 
     if (threadIdx.x == 0) {
+        if (smem_u32(smem) & 1023u) __trap();  // misaligned dynamic shared memory
         for (int i = 0; i < QS; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
         for (int i = 0; i < KS; ++i) { mbar_init(k_full + i, 1); mbar_init(k_empty + i, 1); }
         for (int i = 0; i < VS; ++i) { mbar_init(v_full + i, 1); mbar_init(v_empty + i, 1); }
@@ -394,9 +401,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (p.trace && threadIdx.x == 0) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
-        p.trace[12 * 64 + kTraceCta * blockIdx.x] = gt;
-        p.trace[12 * 64 + kTraceCta * blockIdx.x + 2] = (unsigned long long)(t_end - t_begin);
-        p.trace[12 * 64 + kTraceCta * blockIdx.x + 6] = clock64();
+        p.trace[kTraceRows * 64 + kTraceCta * blockIdx.x] = gt;
+        p.trace[kTraceRows * 64 + kTraceCta * blockIdx.x + 2] = (unsigned long long)(t_end - t_begin);
+        p.trace[kTraceRows * 64 + kTraceCta * blockIdx.x + 6] = clock64();
     }
 
     if (warp == SW) {
@@ -441,6 +448,11 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     // copy is issued into the drained K ring (the first
                     // STAGED_PIECES pieces) or, beyond those, before the final
                     // arrival that releases the softmax warps to read it from L2
+                    // the list and the staged pieces live in the K ring: drain it
+                    for (uint32_t st = 0; st < (uint32_t)KS && st < kc; ++st) {
+                        const uint32_t k = kc - 1 - ((kc - 1 - st) % KS);  // last use of stage st
+                        mbar_wait(k_empty + st, (k / KS) & 1);
+                    }
                     int* pieces = reinterpret_cast<int*>(smem + C::OFF_PIECES);
                     int np = 0;
                     for (uint32_t c2 = blockIdx.x + 1; c2 < G && np < kMaxPieces; ++c2) {
@@ -452,10 +464,6 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     pieces[0] = np;
                     const int ns = np < C::STAGED_PIECES ? np : C::STAGED_PIECES;
                     mbar_expect_tx(merge_full, (uint32_t)ns * (1024u + 4u * C::PIECE_BOX));
-                    for (uint32_t st = 0; st < (uint32_t)KS && st < kc; ++st) {
-                        const uint32_t k = kc - 1 - ((kc - 1 - st) % KS);  // last use of stage st
-                        mbar_wait(k_empty + st, (k / KS) & 1);
-                    }
                     K1_GT(11);
                     for (int i = 0; i < np; ++i) {
                         const int c2 = pieces[1 + i];
@@ -608,19 +616,41 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         const float c = p.c_log2;
         const float thresh_raw = kLazyThreshLog2 / c;
         uint32_t sc = 0, pc = 0;
+        // A segment's metadata (node count, prefix length, this row's mask
+        // words) is loaded by the previous segment's epilogue — all four loads
+        // independent, in flight while that epilogue runs — so a segment
+        // transition costs no global round trip on the softmax path.
+        struct Meta {
+            int n, P;
+            uint64_t mw0, mw1;
+        };
+        auto load_meta = [&](const Seg& sg) {
+            Meta mt;
+            mt.n = __ldg(p.n_nodes + sg.b);
+            mt.P = __ldg(p.prefix_len + sg.b);
+            mt.mw0 = mt.mw1 = 0;
+            if (r < p.T) {
+                const uint64_t* mr = p.mask + ((long long)sg.b * p.T + r) * p.W;
+                mt.mw0 = __ldg(mr);
+                if (p.W > 1) mt.mw1 = __ldg(mr + 1);
+            }
+            return mt;
+        };
+        Seg s_next{};
+        Meta m_next{};
+        if (t_begin < t_end) {
+            s_next = find_seg(p, cum, t_begin, t_end);
+            m_next = load_meta(s_next);
+        }
+        uint32_t segn = 0;  // segments done (trace index)
         for (uint32_t t = t_begin; t < t_end;) {
-            const Seg s = find_seg(p, cum, t, t_end);
+            const Seg s = s_next;
             const int ntl = s.hi - s.lo;
-            const int n = __ldg(p.n_nodes + s.b);
-            const int P = __ldg(p.prefix_len + s.b);
+            const int n = m_next.n;
+            const int P = m_next.P;
             const bool valid = r < n;
             const bool warp_live = __any_sync(0xffffffffu, valid);
-            uint64_t mw0 = 0, mw1 = 0;
-            if (valid) {
-                const uint64_t* mr = p.mask + ((long long)s.b * p.T + r) * p.W;
-                mw0 = __ldg(mr);
-                if (p.W > 1) mw1 = __ldg(mr + 1);
-            }
+            const uint64_t mw0 = valid ? m_next.mw0 : 0, mw1 = valid ? m_next.mw1 : 0;
             float m = -INFINITY, l = 0.f;   // l: this thread's share of the row sum
             for (int i = 0; i < ntl; ++i) {
                 const int j = s.lo + i;
@@ -751,6 +781,10 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             // pair's head owner). The pieces were computed at the START of the
             // following CTAs' ranges, so the head owner — at the END of its
             // range — normally finds them ready.
+            if (t + ntl < t_end) {
+                s_next = find_seg(p, cum, t + ntl, t_end);
+                m_next = load_meta(s_next);
+            }
             const bool full = (s.lo == 0 && s.hi == s.ntiles);
             const bool head = (s.lo == 0 && !full);
             const int d0 = half * DCOLS;
@@ -758,21 +792,22 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             const uint32_t q1 = pc - 1;
             mbar_wait(pv_done + (q1 & 1), (q1 >> 1) & 1);
             if (threadIdx.x == 0) K1_GT(3);
+            if (threadIdx.x == 0) K1_TRACE(12, segn);
             float l_row = l;
             // DUAL: weights of the two halves' accumulators under the merged max
             float wa = 1.f, wb = 0.f;
             if constexpr (!DUAL) {
                 l_row += __shfl_xor_sync(0xffffffffu, l, 16);
             } else {
-                // exchange (m, l) with the other half's thread of this row (the
-                // CTA's slice of the workspace; bar.sync orders it in the CTA)
-                float* xc = p.ml_xchg + (long long)blockIdx.x * (2 * 128 * 2);
-                xc[(half * 128 + r) * 2] = m;
-                xc[(half * 128 + r) * 2 + 1] = l;
+                // exchange (m, l) with the other half's thread of this row
+                // through shared memory (bar.sync orders it in the CTA)
+                float2* xc = reinterpret_cast<float2*>(smem + C::OFF_XCHG);
+                xc[half * 128 + r] = make_float2(m, l);
                 named_bar_sync(1, SW * 32);
-                const float m_o = __ldcg(xc + ((1 - half) * 128 + r) * 2);
-                const float l_o = __ldcg(xc + ((1 - half) * 128 + r) * 2 + 1);
+                const float2 o2 = xc[(1 - half) * 128 + r];
+                const float m_o = o2.x, l_o = o2.y;
                 named_bar_sync(1, SW * 32);  // reads done before the next segment's writes
+                if (threadIdx.x == 0) K1_TRACE(13, segn);
                 const float ma = half ? m_o : m, mb = half ? m : m_o;
                 const float la = half ? l_o : l, lb = half ? l : l_o;
                 const float mm = fmaxf(ma, mb);
@@ -882,6 +917,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 }
                 tc_fence_before();
             }
+            if (threadIdx.x == 0) K1_TRACE(14, segn);
             mbar_arrive(o_empty);
             if (publish) {
                 if (valid && half == 0) {
@@ -898,6 +934,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             }
 
             if (threadIdx.x == 0) K1_GT(4);
+            if (threadIdx.x == 0) K1_TRACE(15, segn);
+            ++segn;
             t += ntl;
         }
     }
@@ -908,8 +946,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (p.trace && threadIdx.x == 0) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
-        p.trace[12 * 64 + kTraceCta * blockIdx.x + 1] = gt;
-        p.trace[12 * 64 + kTraceCta * blockIdx.x + 7] = clock64();
+        p.trace[kTraceRows * 64 + kTraceCta * blockIdx.x + 1] = gt;
+        p.trace[kTraceRows * 64 + kTraceCta * blockIdx.x + 7] = clock64();
     }
     if (warp == SW + 2) tmem_dealloc<C::TMEM_COLS>(tmem);
 }
@@ -960,13 +998,11 @@ bool tree_attention_tc_supported(const st_attn_args* a) {
            (int64_t)a->B * a->H * ((a->Lmax + BN - 1) / BN) < (1ll << 31);  // 32-bit tile indices
 }
 
-constexpr size_t kXchgFloats = 2 * 128 * 2;  // per CTA: (m, l) of both column halves (M=128)
 
-// Workspace: per CTA one piece slot, the (m, l) exchange of M=128 and the
-// piece flags (zero on first use; every launch leaves them zero).
+// Workspace: per CTA one piece slot and one piece flag (zero on first use;
+// every launch leaves the flags zero).
 size_t tree_attention_tc_workspace(const st_attn_args* a) {
     return align_up((size_t)num_sms() * SLOT_FLOATS * sizeof(float), 256) +
-           align_up((size_t)num_sms() * kXchgFloats * sizeof(float), 256) +
            (size_t)num_sms() * sizeof(unsigned);
 }
 
@@ -1026,10 +1062,8 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
             return ST_ERR_CUDA;
         }
     }
-    prm.ml_xchg = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(a->workspace) +
-                                           align_up((size_t)G * SLOT_FLOATS * sizeof(float), 256));
-    prm.flags = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(prm.ml_xchg) +
-                                            align_up((size_t)G * kXchgFloats * sizeof(float), 256));
+    prm.flags = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(a->workspace) +
+                                            align_up((size_t)G * SLOT_FLOATS * sizeof(float), 256));
     prm.B = a->B;
     prm.T = a->T;
     prm.H = a->H;
@@ -1047,8 +1081,8 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
     prm.trace_cta = getenv("ST_K1_TRACE_CTA") ? atoi(getenv("ST_K1_TRACE_CTA")) : 0;
     static unsigned long long* trace_buf = nullptr;
     if (getenv("ST_K1_TRACE")) {
-        if (!trace_buf) cudaMalloc(&trace_buf, (12 * 64 + kTraceCta * 1024) * sizeof(unsigned long long));
-        cudaMemsetAsync(trace_buf, 0, (12 * 64 + kTraceCta * 1024) * sizeof(unsigned long long), stream);
+        if (!trace_buf) cudaMalloc(&trace_buf, (kTraceRows * 64 + kTraceCta * 1024) * sizeof(unsigned long long));
+        cudaMemsetAsync(trace_buf, 0, (kTraceRows * 64 + kTraceCta * 1024) * sizeof(unsigned long long), stream);
         prm.trace = trace_buf;
     }
     const bool m64 = a->T <= 64;
@@ -1059,15 +1093,15 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
     }
     ST_LAUNCH_CHECK();
     if (prm.trace) {  // diagnostic only: dump CTA 0's pipeline timestamps
-        static unsigned long long h[12 * 64 + kTraceCta * 1024];
+        static unsigned long long h[kTraceRows * 64 + kTraceCta * 1024];
         cudaMemcpyAsync(h, prm.trace, sizeof h, cudaMemcpyDeviceToHost, stream);
         cudaStreamSynchronize(stream);
         if (FILE* f = fopen(getenv("ST_K1_TRACE"), "a")) {
-            for (int r = 0; r < 12; ++r) {
+            for (int r = 0; r < kTraceRows; ++r) {
                 for (int i = 0; i < 64; ++i) fprintf(f, "%llu ", h[r * 64 + i]);
                 fprintf(f, "\n");
             }
-            for (int i = 0; i < kTraceCta * G; ++i) fprintf(f, "%llu ", h[12 * 64 + i]);
+            for (int i = 0; i < kTraceCta * G; ++i) fprintf(f, "%llu ", h[kTraceRows * 64 + i]);
             fprintf(f, "\n");
             fclose(f);
         }

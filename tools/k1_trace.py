@@ -37,14 +37,18 @@ for _ in range(3):
     _capi.tree_attention(q, kc, vc, mask, P, n, workspace=ws)
 torch.cuda.synchronize()
 lines = [list(map(int, l.split())) for l in open(out)]
-rows = lines[-13:-1]
+rows = lines[-17:-1]
 cta = np.array(lines[-1], dtype=np.int64).reshape(-1, 12)
 t = np.array(rows, dtype=np.int64)
 t0 = t[0][t[0] > 0].min()
 names = ["K issue", "V issue", "S issue", "PV issue", "S ready", "P done", "K full(mma)", "V full(mma)", "S loaded", "masked+max", "pv wait done", "rescaled"]
 print("tile " + " ".join(f"{x:>12s}" for x in names))
-for i in range(40):
+for i in range(64):
     print(f"{i:4d} " + " ".join(f"{(t[r][i] - t0) if t[r][i] else -1:12d}" for r in range(12)))
+print("segment epilogues (cycles rel. to first K load): PV done | (m,l) merged | O stored | end")
+for i in range(64):
+    if t[12][i]:
+        print(f"{i:4d} " + " ".join(f"{(t[r][i] - t0) if t[r][i] else -1:12d}" for r in range(12, 16)))
 
 st, en, nt = cta[:, 0], cta[:, 1], cta[:, 2]
 t0g = st.min()
