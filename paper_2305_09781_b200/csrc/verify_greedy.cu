@@ -135,8 +135,8 @@ __device__ __forceinline__ int key_index(unsigned long long k) {
     return k == ~0ull ? 0 : (int)(~(uint32_t)(k & 0xffffffffu));
 }
 
-constexpr int kSplit = 4;   // blocks per logits row
-constexpr int kUnroll = 8;  // float4 loads in flight per thread (a 4000-float slice in one batch)
+constexpr int kSplit = 8;   // blocks per logits row (tools/argmax_bench.cu: 8 x 4 loads beat 4 x 8)
+constexpr int kUnroll = 4;  // float4 loads in flight per thread (a 4000-float slice in one batch)
 
 // Phase 1: stream every live node's logits once; kSplit blocks per row each
 // reduce their slice to one order-preserving key, written to its own slot

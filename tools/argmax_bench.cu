@@ -1,0 +1,100 @@
+// Diagnostic microbenchmark: the K3 logits-streaming argmax (verify_greedy.cu)
+// at the C2 shape (B=8, T=64, V=32000 fp32 = 65.5 MB) for several
+// (blocks per row, float4 loads in flight per thread, threads per block)
+// configurations, cycling over 3 logits buffers (196 MB > L2).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/argmax_bench tools/argmax_bench.cu
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+
+__device__ __forceinline__ unsigned long long arg_key(float v, int i) {
+    if (v != v) {
+        if (i == 0) return ~0ull;
+        v = -INFINITY;
+    }
+    uint32_t u = __float_as_uint(v);
+    u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+    return ((unsigned long long)u << 32) | (uint32_t)(~(uint32_t)i);
+}
+
+template <int SPLIT, int UNROLL, int NT>
+__global__ void __launch_bounds__(NT) argmax_kernel(const float* __restrict__ logits, int T, int V,
+                                                    unsigned long long* keys) {
+    const int part = blockIdx.x, u = blockIdx.y, b = blockIdx.z;
+    const float* row = logits + ((int64_t)b * T + u) * V;
+    const int nv = V >> 2;
+    const int per = (nv + SPLIT - 1) / SPLIT;
+    const int lo = part * per, hi = min(nv, lo + per);
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    float bv = -INFINITY;
+    int bi = lo + (int)threadIdx.x < hi ? (lo + (int)threadIdx.x) * 4 : -1;
+    for (int base = lo + threadIdx.x; base < hi; base += NT * UNROLL) {
+        float4 x[UNROLL];
+#pragma unroll
+        for (int k = 0; k < UNROLL; ++k) {
+            const int j = base + k * NT;
+            x[k] = j < hi ? __ldcs(r4 + j) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        }
+#pragma unroll
+        for (int k = 0; k < UNROLL; ++k) {
+            const int j = (base + k * NT) * 4;
+            if (x[k].x > bv) { bv = x[k].x; bi = j; }
+            if (x[k].y > bv) { bv = x[k].y; bi = j + 1; }
+            if (x[k].z > bv) { bv = x[k].z; bi = j + 2; }
+            if (x[k].w > bv) { bv = x[k].w; bi = j + 3; }
+        }
+    }
+    unsigned long long best = bi >= 0 ? arg_key(bv, bi) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    __shared__ unsigned long long red[NT / 32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) red[warp] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < NT / 32; ++w) best = max(best, red[w]);
+        keys[((int64_t)b * T + u) * SPLIT + part] = best;
+    }
+}
+
+template <int SPLIT, int UNROLL, int NT>
+void run(float* const* bufs, unsigned long long* keys, int B, int T, int V) {
+    dim3 grid(SPLIT, T, B);
+    for (int i = 0; i < 6; ++i) argmax_kernel<SPLIT, UNROLL, NT><<<grid, NT>>>(bufs[i % 3], T, V, keys);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 60;
+    cudaEventRecord(e0);
+    for (int i = 0; i < iters; ++i) argmax_kernel<SPLIT, UNROLL, NT><<<grid, NT>>>(bufs[i % 3], T, V, keys);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double us = ms * 1e3 / iters;
+    const double bytes = 4.0 * B * T * V;
+    printf("split %d unroll %2d threads %4d: %7.2f us  %6.0f GB/s\n", SPLIT, UNROLL, NT, us, bytes / us / 1e3);
+}
+
+int main() {
+    const int B = 8, T = 64, V = 32000;
+    float* bufs[3];
+    for (auto& p : bufs) {
+        cudaMalloc(&p, (size_t)B * T * V * 4);
+        cudaMemset(p, 0, (size_t)B * T * V * 4);
+    }
+    unsigned long long* keys;
+    cudaMalloc(&keys, (size_t)B * T * 16 * 8);
+    run<4, 8, 256>(bufs, keys, B, T, V);
+    run<2, 16, 256>(bufs, keys, B, T, V);
+    run<1, 16, 512>(bufs, keys, B, T, V);
+    run<2, 8, 512>(bufs, keys, B, T, V);
+    run<8, 4, 256>(bufs, keys, B, T, V);
+    run<8, 8, 128>(bufs, keys, B, T, V);
+    run<16, 4, 128>(bufs, keys, B, T, V);
+    run<4, 4, 512>(bufs, keys, B, T, V);
+    run<4, 8, 256>(bufs, keys, B, T, V);
+    return 0;
+}
