@@ -118,7 +118,8 @@ struct TcParams {
     float* lse;
     float* partial;      // [gridDim.x][SLOT_FLOATS]: the piece a CTA's first segment leaves
     unsigned* flags;     // [gridDim.x]: 1 while that piece is published and not yet merged
-    int B, T, H, W;
+    int B, T, H, W;      // H: KV heads (one (b, h) pair per request and KV head)
+    int G, Hq;           // query heads per KV head (GQA group), query heads = G * H
     float c_log2;        // scale * log2(e)
     float scale;
     unsigned long long* trace;  // optional pipeline trace of CTA 0 (ST_K1_TRACE)
@@ -416,8 +417,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 const uint32_t qb = qc % QS;
                 mbar_wait(q_empty + qb, ((qc / QS) & 1) ^ 1);
                 mbar_arrive_expect_tx(q_full + qb, C::A_BYTES);
-                tma_load_4d(sm_q + qb * C::A_BYTES, &tm_q, q_full + qb, 0, s.h, 0, s.b);
-                tma_load_4d(sm_q + qb * C::A_BYTES + C::A_ATOM, &tm_q, q_full + qb, 64, s.h, 0, s.b);
+                // box {64 d, G heads, M/G nodes}: smem row = node * G + head
+                tma_load_4d(sm_q + qb * C::A_BYTES, &tm_q, q_full + qb, 0, s.h * p.G, 0, s.b);
+                tma_load_4d(sm_q + qb * C::A_BYTES + C::A_ATOM, &tm_q, q_full + qb, 64, s.h * p.G, 0, s.b);
                 ++qc;
                 const int bh = s.b * p.H + s.h;
                 for (int j = s.lo; j < s.hi; ++j, ++kc) {
@@ -609,6 +611,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         // half keeps its own (m, l) and O accumulator, merged in the epilogue.
         const int half = DUAL ? (warp >> 2) : (lane >> 4);
         const int r = DUAL ? (warp & 3) * 32 + lane : warp * 16 + (lane & 15);
+        // Q/S/O row r holds tree node u_r of query head g_r of the pair's
+        // KV-head group (the Q box lays rows out node-major, head-minor)
+        const int u_r = r / p.G, g_r = r - u_r * p.G;
         const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         const uint32_t s_half = DUAL ? half * COLS : 0;          // this half's S columns
         const uint32_t o_own = DUAL ? (half ? C::OB_COL : C::O_COL) : C::O_COL;
@@ -629,8 +634,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             mt.n = __ldg(p.n_nodes + sg.b);
             mt.P = __ldg(p.prefix_len + sg.b);
             mt.mw0 = mt.mw1 = 0;
-            if (r < p.T) {
-                const uint64_t* mr = p.mask + ((long long)sg.b * p.T + r) * p.W;
+            if (u_r < p.T) {
+                const uint64_t* mr = p.mask + ((long long)sg.b * p.T + u_r) * p.W;
                 mt.mw0 = __ldg(mr);
                 if (p.W > 1) mt.mw1 = __ldg(mr + 1);
             }
@@ -648,7 +653,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             const int ntl = s.hi - s.lo;
             const int n = m_next.n;
             const int P = m_next.P;
-            const bool valid = r < n;
+            const bool valid = u_r < n;
             const bool warp_live = __any_sync(0xffffffffu, valid);
             const uint64_t mw0 = valid ? m_next.mw0 : 0, mw1 = valid ? m_next.mw1 : 0;
             float m = -INFINITY, l = 0.f;   // l: this thread's share of the row sum
@@ -788,7 +793,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             const bool full = (s.lo == 0 && s.hi == s.ntiles);
             const bool head = (s.lo == 0 && !full);
             const int d0 = half * DCOLS;
-            const long long orow = (((long long)s.b * p.T + r) * p.H_out + p.head_offset + s.h) * HD + d0;
+            const long long orow =
+                (((long long)s.b * p.T + u_r) * p.H_out + p.head_offset + s.h * p.G + g_r) * HD + d0;
             const uint32_t q1 = pc - 1;
             mbar_wait(pv_done + (q1 & 1), (q1 >> 1) & 1);
             if (threadIdx.x == 0) K1_GT(3);
@@ -930,7 +936,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 if (threadIdx.x == 0) st_release_gpu(p.flags + blockIdx.x, 1u);
             } else {
                 if (valid && p.lse && half == 0)
-                    p.lse[((long long)s.b * p.H + s.h) * p.T + r] = m_fin * p.scale + __logf(l_fin);
+                    p.lse[((long long)s.b * p.Hq + s.h * p.G + g_r) * p.T + u_r] = m_fin * p.scale + __logf(l_fin);
             }
 
             if (threadIdx.x == 0) K1_GT(4);
@@ -992,10 +998,14 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 bool tree_attention_tc_supported(const st_attn_args* a) {
     auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-    return (a->dtype == ST_F16 || a->dtype == ST_BF16) && a->D == HD && a->H == a->Hkv &&
-           a->T <= 128 && a->W <= 2 && a->Lmax < (1ll << 31) && al(a->q) && al(a->k_cache) &&
+    // GQA: G = H/Hkv query heads share a KV head; a pair's Q tile holds G*T
+    // rows (M = 64 or 128), so G must divide M and G*T fit in it
+    const int G = a->Hkv > 0 && a->H % a->Hkv == 0 ? a->H / a->Hkv : 0;
+    const int M = (int64_t)G * a->T <= 64 ? 64 : 128;
+    return (a->dtype == ST_F16 || a->dtype == ST_BF16) && a->D == HD && G >= 1 && M % G == 0 &&
+           (int64_t)G * a->T <= 128 && a->W <= 2 && a->Lmax < (1ll << 31) && al(a->q) && al(a->k_cache) &&
            al(a->v_cache) && al(a->o) &&
-           (int64_t)a->B * a->H * ((a->Lmax + BN - 1) / BN) < (1ll << 31);  // 32-bit tile indices
+           (int64_t)a->B * a->Hkv * ((a->Lmax + BN - 1) / BN) < (1ll << 31);  // 32-bit tile indices
 }
 
 
@@ -1028,7 +1038,9 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
     {
         const uint64_t dims[4] = {(uint64_t)HD, (uint64_t)a->H, (uint64_t)a->T, (uint64_t)a->B};
         const uint64_t strides[3] = {HD * 2ull, (uint64_t)a->H * HD * 2, (uint64_t)a->T * a->H * HD * 2};
-        const uint32_t box[4] = {64, 1, (uint32_t)(a->T <= 64 ? 64 : 128), 1};
+        const int G = a->H / a->Hkv;
+        const uint32_t M = (int64_t)G * a->T <= 64 ? 64 : 128;
+        const uint32_t box[4] = {64, (uint32_t)G, M / G, 1};
         if (!encode(&tq, dt, 4, a->q, dims, strides, box)) {
             set_error("st_tree_attention: cuTensorMapEncodeTiled(q) failed");
             return ST_ERR_CUDA;
@@ -1056,7 +1068,7 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
     {
         const uint64_t dims[2] = {(uint64_t)HD, (uint64_t)G * (SLOT_FLOATS / HD)};
         const uint64_t strides[1] = {HD * 4ull};
-        const uint32_t box[2] = {32, (uint32_t)(a->T <= 64 ? 64 : 128)};
+        const uint32_t box[2] = {32, (uint32_t)((int64_t)(a->H / a->Hkv) * a->T <= 64 ? 64 : 128)};
         if (!encode(&tp, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, prm.partial, dims, strides, box)) {
             set_error("st_tree_attention: cuTensorMapEncodeTiled(workspace) failed");
             return ST_ERR_CUDA;
@@ -1066,7 +1078,9 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
                                             align_up((size_t)G * SLOT_FLOATS * sizeof(float), 256));
     prm.B = a->B;
     prm.T = a->T;
-    prm.H = a->H;
+    prm.H = a->Hkv;
+    prm.G = a->H / a->Hkv;
+    prm.Hq = a->H;
     prm.W = a->W;
     prm.scale = (float)a->scale;
     prm.c_log2 = (float)(a->scale * 1.4426950408889634);
@@ -1085,7 +1099,7 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
         cudaMemsetAsync(trace_buf, 0, (kTraceRows * 64 + kTraceCta * 1024) * sizeof(unsigned long long), stream);
         prm.trace = trace_buf;
     }
-    const bool m64 = a->T <= 64;
+    const bool m64 = (int64_t)prm.G * a->T <= 64;
     if (a->dtype == ST_F16) {
         if (m64) { ST_TRY_LAUNCH_TC(__half, 64); } else { ST_TRY_LAUNCH_TC(__half, 128); }
     } else {

@@ -136,3 +136,23 @@ def test_tc_c2_shape_sampled_heads(capi, restatement):
         got = out[b, : n[b], h].double().cpu().numpy()
         worst = max(worst, np.abs(got - ref[: n[b]]).max())
     assert worst <= 2e-3, worst
+
+
+@pytest.mark.parametrize("G,T,dtype", [(2, 32, torch.float16), (4, 16, torch.bfloat16),
+                                       (8, 16, torch.float16), (4, 32, torch.bfloat16),
+                                       (2, 64, torch.float16), (16, 8, torch.float16)])
+def test_tc_gqa_head_groups(capi, restatement, G, T, dtype):
+    """GQA: G query heads share each KV head; the tcgen05 kernel stacks the
+    group's G*T query rows into one M=64/128 tile per (request, KV head), so
+    every KV tile read serves G heads. Checked against the f64 restatement
+    (same rounded inputs), with LSE, ragged trees and split pairs."""
+    rng = np.random.default_rng(G * 100 + T)
+    w = 2 if T < 16 else 3
+    trees = [restatement.merge(width_depth_seqs(rng, int(rng.integers(0, 50)), 50, w, (T - 1) // w),
+                               4096) for _ in range(5)]   # <= 1 + w*depth <= T nodes
+    Hkv = 3
+    bt = make_batch(restatement, rng, 5, G * Hkv, Hkv, 128, trees=trees, T=T, P_range=(0, 900),
+                    dtype=dtype)
+    assert capi is not None
+    out, lse = run_k1(capi, bt, dtype, force_path=2, lse=True)
+    check_k1(restatement, bt, out, dtype, lse)
