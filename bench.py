@@ -8,11 +8,11 @@ fp16, batch 8 requests per GPU, 64-node token tree each, 2048 committed KV rows,
 H = 32 heads x D = 128, greedy verification over a 32000-token vocabulary.
 
 One step = one pass of the hot path over the batch:
-  K2 append of the tree's K/V into the cache scratch rows
-  -> ancestor bitmasks built on device
-  -> K1 tree attention (tcgen05)                       [dominant kernel]
+  ancestor bitmasks built on device
+  -> K1 tree attention (tcgen05): committed KV from the cache, the tree's own
+     K/V rows straight from their [B][T][H][D] tensors   [dominant kernel]
   -> K3 greedy verify (vocab argmax + accepted-path walk)
-  -> K2 in-place compaction of the accepted path
+  -> K2 commit: the accepted path's K/V rows copied into the cache
   (+ N>1: NCCL all-gather of the accepted tokens — the DP exchange step)
 
 value  = tree tokens verified per second over all ranks (B*T*N / step time),
@@ -43,7 +43,7 @@ sys.path.insert(0, ROOT)
 # C2
 B, T, H, D, L, V = 8, 64, 32, 128, 2048, 32000
 WIDTH, DEPTH = 8, 8            # 8 root-to-leaf paths, trimmed to exactly 64 nodes
-LAUNCHES_PER_STEP = 4          # append+masks, K1, K3 argmax, K3 walk+K2 compact
+LAUNCHES_PER_STEP = 4          # masks, K1 (tree rows from k_tree), K3 argmax, K3 walk + K2 commit
 METRIC = "tree-verify tokens/s"
 UNIT = "tokens/s"
 
@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tree-rows", default="own", choices=["own", "cache"],
+                    help="C2: K1 reads the tree rows from their own tensors (no append) or "
+                         "from the cache after a K2 append")
     ap.add_argument("--config", default="c2", choices=["c2", "c3"],
                     help="c2 (default, the headline metric) or c3: full 32-layer 7B-shape stack, "
                          "batch 32 partitioned over the ranks, stochastic verification")
@@ -278,15 +281,27 @@ def main():
 
     k1_events = []
 
-    def pre(qq, kn, vn, tk, pr, nd):   # K2 append + masks (one launch)
-        _capi.tree_prepare(kn, vn, P, nd, kc, vc, pr, out=mask_buf)
+    # --tree-rows own (default): the tree's K/V rows stay in their own
+    # [B][T][H][D] tensors; K1 reads them there (st_attn_args.k_tree) and the
+    # commit copies only the accepted rows into the cache — no K2 append of all
+    # T rows. --tree-rows cache: K2 append into the cache scratch rows first,
+    # then in-place compaction (the reference's cache discipline).
+    own = args.tree_rows == "own"
+
+    def pre(qq, kn, vn, tk, pr, nd):
+        if own:     # ancestor masks
+            _capi.build_masks(pr, nd, out=mask_buf)
+        else:       # K2 append + masks (one launch)
+            _capi.tree_prepare(kn, vn, P, nd, kc, vc, pr, out=mask_buf)
 
     def k1(qq, kn, vn, tk, pr, nd):
-        _capi.tree_attention(qq, kc, vc, mask_buf, P, nd, out=out, workspace=ws_attn)
+        _capi.tree_attention(qq, kc, vc, mask_buf, P, nd, out=out, workspace=ws_attn,
+                             k_tree=kn if own else None, v_tree=vn if own else None)
 
-    def post(qq, kn, vn, tk, pr, nd):  # K3 argmax, then the walk fused with K2 compaction
+    def post(qq, kn, vn, tk, pr, nd):  # K3 argmax, then the walk fused with the K2 commit
         _capi.verify_greedy_compact(logits, tk, pr, nd, P, kc, vc, workspace=ws_ver,
-                                    want_argmax=False, out=vout)
+                                    want_argmax=False, out=vout, k_tree=kn if own else None,
+                                    v_tree=vn if own else None)
 
     resident = (q, knew, vnew, tok, par, nn)
 
@@ -570,7 +585,8 @@ def main():
                              "alternating between two KV/Q copies (2 x 277 MB > L2), CUDA "
                              "events around the replays; in-step bracket (event graph nodes "
                              "around K1 inside the step) reported beside it",
-                   "k1_path": "tcgen05" if path == 2 else "cuda-core"},
+                   "k1_path": "tcgen05" if path == 2 else "cuda-core",
+                   "tree_rows": args.tree_rows},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "K1 tree attention", "bytes_per_launch": bytes_k1,
@@ -591,6 +607,8 @@ def main():
                         "bound by PCIe H2D"},
         "gpu_launches": LAUNCHES_PER_STEP * args.steps,
         "clocks": clk,
+        "verify_steps_per_s": 1e3 / ms_step,
+        "node_evals_per_s": value,
         "verified_tokens_per_step": accepted,
         "verified_tokens_per_s": accepted * world / (ms_step / 1e3),
     }

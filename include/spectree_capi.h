@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define ST_ABI_VERSION 1
+#define ST_ABI_VERSION 2
 
 typedef int st_status;
 
@@ -91,6 +91,14 @@ typedef struct {
     void* workspace;           /* st_tree_attention_workspace_size() bytes, zeroed once */
     size_t workspace_bytes;
     int force_path;            /* 0 auto, 1 CUDA-core, 2 tcgen05 tensor-core */
+    /* Optional: the tree nodes' own K/V rows, [B][T][Hkv][D] (the step's new
+     * rows, e.g. from the QKV projection). When set, tree row v of request b
+     * is read from here instead of cache row P[b]+v — K1 then needs no
+     * st_kv_append before it, and st_verify_greedy_compact copies the
+     * accepted rows from the same tensors into the cache. NULL: the tree rows
+     * are in the cache at [P[b], P[b]+n[b]). */
+    const void* k_tree;
+    const void* v_tree;
 } st_attn_args;
 
 size_t st_tree_attention_workspace_size(const st_attn_args* a);
@@ -155,15 +163,20 @@ st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32
  * walk is fused into the compaction kernel (every block of a request repeats
  * the request's walk in shared memory, then moves its share of the KV heads).
  * Same outputs as the two calls; requires T <= 1024, D * sizeof(dtype) a
- * multiple of 16 and new_prefix_len (optional) not aliasing prefix_len. */
+ * multiple of 16 and new_prefix_len (optional) not aliasing prefix_len.
+ * k_tree/v_tree (optional, [B][T][Hkv][D] per layer, layer l at
+ * + l * tree_layer_stride elements): take the accepted rows from the tree's
+ * own K/V (the st_attn_args.k_tree mode: nothing was appended to the cache)
+ *   cache[b][h][P + k] = tree[b][ids[k]][h]   for k < len[b]. */
 st_status st_verify_greedy_compact(const float* logits, int B, int T, int V, const int32_t* tokens,
                                    const int32_t* parent, const int32_t* n_nodes,
                                    const int32_t* budget, int32_t eos, int32_t* argmax,
                                    int32_t* verified, int32_t* ids, int32_t* len, void* workspace,
                                    st_dtype dtype, int Hkv, int D, int64_t Lmax, int n_layers,
                                    int64_t layer_stride, const int32_t* prefix_len,
-                                   int32_t* new_prefix_len, void* k_cache, void* v_cache,
-                                   void* stream);
+                                   int32_t* new_prefix_len, const void* k_tree,
+                                   const void* v_tree, int64_t tree_layer_stride, void* k_cache,
+                                   void* v_cache, void* stream);
 
 /* The walk alone, given per-node LLM outputs [B][T] (what the reference's
  * verify() consumes, token_tree.cpp:153-175); same outputs as st_verify_greedy. */

@@ -43,7 +43,7 @@ class AttnArgs(C.Structure):
                 ("mask", C.c_void_p), ("prefix_len", C.c_void_p), ("n_nodes", C.c_void_p),
                 ("o", C.c_void_p), ("lse", C.c_void_p), ("scale", C.c_double),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
-                ("force_path", C.c_int)]
+                ("force_path", C.c_int), ("k_tree", C.c_void_p), ("v_tree", C.c_void_p)]
 
 
 _lib = None
@@ -64,7 +64,8 @@ SIGNATURES = {
     "st_verify_workspace_size": (_Z, [_I, _I]),
     "st_verify_greedy": (_I, [_V, _I, _I, _I, _V, _V, _V, _V, C.c_int32, _V, _V, _V, _V, _V, _V]),
     "st_verify_greedy_compact": (_I, [_V, _I, _I, _I, _V, _V, _V, _V, C.c_int32, _V, _V, _V, _V, _V,
-                                      _I, _I, _I, _I64, _I, _I64, _V, _V, _V, _V, _V]),
+                                      _I, _I, _I, _I64, _I, _I64, _V, _V, _V, _V, _I64, _V, _V,
+                                      _V]),
     "st_verify_outputs": (_I, [_V, _I, _I, _V, _V, _V, _V, C.c_int32, _V, _V, _V, _V]),
     "st_verify_mss": (_I, [_V, _V, _I, _I, _I, _V, _V, _V, _F, _V, _I, _V, _V, _V, _V]),
     "st_build_masks": (_I, [_V, _V, _I, _I, _I, _V, _V]),
@@ -113,7 +114,7 @@ def _stream(stream=None):
 
 # ------------------------------------------------------------------ K1 ----
 def attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, lse=None, scale=None,
-              workspace=None, force_path=0):
+              workspace=None, force_path=0, k_tree=None, v_tree=None):
     B, T, H, D = q.shape
     Hkv, Lmax = k_cache.shape[1], k_cache.shape[2]
     a = AttnArgs()
@@ -127,6 +128,8 @@ def attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, lse=None, sca
     a.workspace = workspace.data_ptr() if workspace is not None else None
     a.workspace_bytes = workspace.numel() if workspace is not None else 0
     a.force_path = force_path
+    a.k_tree = k_tree.data_ptr() if k_tree is not None else None
+    a.v_tree = v_tree.data_ptr() if v_tree is not None else None
     return a
 
 
@@ -144,16 +147,19 @@ def tree_attention_path(q, k_cache, v_cache, mask, prefix_len, n_nodes, force_pa
 
 
 def tree_attention(q, k_cache, v_cache, mask, prefix_len, n_nodes, out=None, lse=None,
-                   scale=None, workspace=None, force_path=0, stream=None):
+                   scale=None, workspace=None, force_path=0, stream=None, k_tree=None,
+                   v_tree=None):
     """K1 through st_tree_attention. Shapes: q [B,T,H,D]; caches [B,Hkv,Lmax,D];
-    mask [B,T,W] int64 (uint64 bits); prefix_len/n_nodes [B] int32 (device)."""
+    mask [B,T,W] int64 (uint64 bits); prefix_len/n_nodes [B] int32 (device);
+    k_tree/v_tree (optional) [B,T,Hkv,D]: the tree rows, read instead of cache
+    rows [P, P+n)."""
     if out is None:
         out = torch.empty_like(q)
     if workspace is None:
         workspace = tree_attention_workspace(q, k_cache, v_cache, mask, prefix_len, n_nodes,
                                              force_path)
     a = attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, lse, scale, workspace,
-                  force_path)
+                  force_path, k_tree, v_tree)
     check(lib().st_tree_attention(C.byref(a), _stream(stream)))
     return out
 
@@ -259,9 +265,11 @@ def verify_greedy(logits, tokens, parent, n_nodes, budget=None, eos=-1, workspac
 
 def verify_greedy_compact(logits, tokens, parent, n_nodes, prefix_len, k_cache, v_cache,
                           budget=None, eos=-1, workspace=None, new_prefix_len=None, stream=None,
-                          want_argmax=True, out=None):
+                          want_argmax=True, out=None, k_tree=None, v_tree=None):
     """verify_greedy + kv_compact(ids, len) in two launches (walk fused into the
-    compaction). k_cache/v_cache: [L,B,Hkv,Lmax,D] or [B,Hkv,Lmax,D]."""
+    compaction). k_cache/v_cache: [L,B,Hkv,Lmax,D] or [B,Hkv,Lmax,D].
+    k_tree/v_tree ([L,]B,T,Hkv,D): copy the accepted rows from the tree's own
+    K/V instead of moving them inside the cache (K1's k_tree mode)."""
     B, T, V = logits.shape
     dev = logits.device
     argmax = torch.empty((B, T), dtype=torch.int32, device=dev) if want_argmax else None
@@ -283,7 +291,9 @@ def verify_greedy_compact(logits, tokens, parent, n_nodes, prefix_len, k_cache, 
         _ptr(logits), B, T, V, _ptr(tokens), _ptr(parent), _ptr(n_nodes), _ptr(budget), int(eos),
         _ptr(argmax), _ptr(verified), _ptr(ids), _ptr(length), _ptr(workspace),
         DTYPES[k_cache.dtype], Hkv, D, Lmax, n_layers, layer_stride, _ptr(prefix_len),
-        _ptr(new_prefix_len), _ptr(k_cache), _ptr(v_cache), _stream(stream)))
+        _ptr(new_prefix_len), _ptr(k_tree), _ptr(v_tree),
+        (k_tree[0].numel() if k_tree is not None and k_tree.dim() == 5 else 0),
+        _ptr(k_cache), _ptr(v_cache), _stream(stream)))
     return argmax, verified, ids, length
 
 

@@ -16,6 +16,8 @@ st_status validate(const st_attn_args* a) {
     ST_CHECK_ARG(a->H % a->Hkv == 0, ST_ERR_SHAPE_MISMATCH, "H must be a multiple of Hkv");
     ST_CHECK_ARG(a->W * 64 >= a->T, ST_ERR_SHAPE_MISMATCH, "mask words W < ceil(T/64)");
     ST_CHECK_ARG(a->Lmax >= a->T, ST_ERR_SHAPE_MISMATCH, "cache rows Lmax < T");
+    ST_CHECK_ARG((a->k_tree == nullptr) == (a->v_tree == nullptr), ST_ERR_INVALID_ARGUMENT,
+                 "k_tree and v_tree must be both set or both NULL");
     return ST_OK;
 }
 

@@ -47,7 +47,8 @@ __global__ void __launch_bounds__(32 * kWarps)
 tree_attn_cc_kernel(const T* __restrict__ q, const T* __restrict__ kc, const T* __restrict__ vc,
                     const uint64_t* __restrict__ mask, const int32_t* __restrict__ prefix_len,
                     const int32_t* __restrict__ n_nodes, T* __restrict__ o, float* __restrict__ lse,
-                    int B, int T_, int H, int Hkv, int D, int W, int64_t Lmax, double scale_d) {
+                    int B, int T_, int H, int Hkv, int D, int W, int64_t Lmax, double scale_d,
+                    const T* __restrict__ kt, const T* __restrict__ vt) {
     using A = typename acc_of<T>::type;
     __shared__ A qs[kWarps][32 * DPL];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -70,6 +71,11 @@ tree_attn_cc_kernel(const T* __restrict__ q, const T* __restrict__ kc, const T* 
     const T* kb = kc + ((int64_t)b * Hkv + hk) * Lmax * D;
     const T* vb = vc + ((int64_t)b * Hkv + hk) * Lmax * D;
     const int rows = P + n;
+    // kv row r: cache row r, or (k_tree mode) tree node r - P of [B][T][Hkv][D]
+    auto row_of = [&](const T* cache, const T* tree, int r) -> const T* {
+        if (tree && r >= P) return tree + (((int64_t)b * T_ + (r - P)) * Hkv + hk) * D;
+        return cache + (int64_t)r * D;
+    };
 
     A m = neg_inf<A>(), l = (A)0;
     A acc[DPL];
@@ -85,7 +91,7 @@ tree_attn_cc_kernel(const T* __restrict__ q, const T* __restrict__ kc, const T* 
         }
         A s = neg_inf<A>();
         if (vis) {
-            const T* kr = kb + (int64_t)r * D;
+            const T* kr = row_of(kb, kt, r);
             A dot = (A)0;
             for (int d = 0; d < D; ++d) dot += qs[warp][d] * to_acc<A>(kr[d]);
             s = dot * scale;
@@ -103,7 +109,7 @@ tree_attn_cc_kernel(const T* __restrict__ q, const T* __restrict__ kc, const T* 
             const int j = __ffs(live) - 1;
             live &= live - 1;
             const A pj = __shfl_sync(0xffffffffu, p, j);
-            const T* vr = vb + (int64_t)(r0 + j) * D;
+            const T* vr = row_of(vb, vt, r0 + j);
 #pragma unroll
             for (int i = 0; i < DPL; ++i) {
                 const int d = lane + 32 * i;
@@ -135,7 +141,8 @@ st_status launch_cc(const st_attn_args* a, cudaStream_t s) {
 #define ST_CC_LAUNCH(N)                                                                       \
     tree_attn_cc_kernel<T, N><<<grid, 32 * kWarps, 0, s>>>(                                  \
         (const T*)a->q, (const T*)a->k_cache, (const T*)a->v_cache, a->mask, a->prefix_len, \
-        a->n_nodes, (T*)a->o, a->lse, a->B, a->T, a->H, a->Hkv, a->D, a->W, a->Lmax, a->scale)
+        a->n_nodes, (T*)a->o, a->lse, a->B, a->T, a->H, a->Hkv, a->D, a->W, a->Lmax, a->scale, \
+        (const T*)a->k_tree, (const T*)a->v_tree)
     if (dpl <= 1) ST_CC_LAUNCH(1);
     else if (dpl <= 2) ST_CC_LAUNCH(2);
     else if (dpl <= 4) ST_CC_LAUNCH(4);

@@ -120,6 +120,7 @@ struct TcParams {
     unsigned* flags;     // [gridDim.x]: 1 while that piece is published and not yet merged
     int B, T, H, W;      // H: KV heads (one (b, h) pair per request and KV head)
     int G, Hq;           // query heads per KV head (GQA group), query heads = G * H
+    int tree_src;        // tree rows come from k_tree/v_tree: one extra tile after ceil(P/BN)
     float c_log2;        // scale * log2(e)
     float scale;
     unsigned long long* trace;  // optional pipeline trace of CTA 0 (ST_K1_TRACE)
@@ -160,7 +161,10 @@ struct Seg {
 
 __device__ __forceinline__ int ntiles_of(const TcParams& p, int b) {
     const int n = __ldg(p.n_nodes + b);
-    return n > 0 ? (__ldg(p.prefix_len + b) + n + BN - 1) / BN : 0;
+    if (n <= 0) return 0;
+    const int P = __ldg(p.prefix_len + b);
+    // k_tree mode: the prefix tiles, then one tile of the (<= 128) tree rows
+    return p.tree_src ? (P + BN - 1) / BN + 1 : (P + n + BN - 1) / BN;
 }
 
 // Segment starting at global tile t (t < t_end) of this CTA's range. `cum`
@@ -297,6 +301,7 @@ template <class T, int M>
 __global__ void __launch_bounds__(Cfg<M>::THREADS, 1)
 tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_part,
+                    const __grid_constant__ CUtensorMap tm_kt, const __grid_constant__ CUtensorMap tm_vt,
                     const TcParams p) {
     using C = Cfg<M>;
     constexpr int KS = C::KSTAGES, VS = C::VSTAGES, QS = C::QSTAGES;
@@ -347,8 +352,12 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         prefetch_tmap(&tm_q);
         prefetch_tmap(&tm_k);
         prefetch_tmap(&tm_part);
+        if (p.tree_src) prefetch_tmap(&tm_kt);
     }
-    if (warp == SW + 1 && lane == 0) prefetch_tmap(&tm_v);
+    if (warp == SW + 1 && lane == 0) {
+        prefetch_tmap(&tm_v);
+        if (p.tree_src) prefetch_tmap(&tm_vt);
+    }
     if (warp == SW + 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
@@ -429,8 +438,13 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     if (kc == 0) K1_GT(5);
                     mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
                     uint8_t* dst = sm_k + st * TILE_BYTES;
-                    tma_load_3d_hint(dst, &tm_k, k_full + st, 0, j * BN, bh, pol);
-                    tma_load_3d_hint(dst + KV_ATOM, &tm_k, k_full + st, 64, j * BN, bh, pol);
+                    if (p.tree_src && j == s.ntiles - 1) {  // the tree's own rows [B][T][Hkv][D]
+                        tma_load_4d(dst, &tm_kt, k_full + st, 0, s.h, 0, s.b);
+                        tma_load_4d(dst + KV_ATOM, &tm_kt, k_full + st, 64, s.h, 0, s.b);
+                    } else {
+                        tma_load_3d_hint(dst, &tm_k, k_full + st, 0, j * BN, bh, pol);
+                        tma_load_3d_hint(dst + KV_ATOM, &tm_k, k_full + st, 64, j * BN, bh, pol);
+                    }
                 }
                 t += s.hi - s.lo;
             }
@@ -498,8 +512,13 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     K1_TRACE(1, vc);
                     mbar_arrive_expect_tx(v_full + st, TILE_BYTES);
                     uint8_t* dst = sm_v + st * TILE_BYTES;
-                    tma_load_3d_hint(dst, &tm_v, v_full + st, 0, j * BN, bh, pol);
-                    tma_load_3d_hint(dst + KV_ATOM, &tm_v, v_full + st, 64, j * BN, bh, pol);
+                    if (p.tree_src && j == s.ntiles - 1) {
+                        tma_load_4d(dst, &tm_vt, v_full + st, 0, s.h, 0, s.b);
+                        tma_load_4d(dst + KV_ATOM, &tm_vt, v_full + st, 64, s.h, 0, s.b);
+                    } else {
+                        tma_load_3d_hint(dst, &tm_v, v_full + st, 0, j * BN, bh, pol);
+                        tma_load_3d_hint(dst + KV_ATOM, &tm_v, v_full + st, 64, j * BN, bh, pol);
+                    }
                 }
                 t += s.hi - s.lo;
             }
@@ -653,6 +672,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             const int ntl = s.hi - s.lo;
             const int n = m_next.n;
             const int P = m_next.P;
+            // first kv row index of the tree rows: P, or (k_tree mode) the
+            // start of the extra tree tile after the ceil(P/BN) prefix tiles
+            const int Pt = p.tree_src ? (s.ntiles - 1) * BN : P;
             const bool valid = u_r < n;
             const bool warp_live = __any_sync(0xffffffffu, valid);
             const uint64_t mw0 = valid ? m_next.mw0 : 0, mw1 = valid ? m_next.mw1 : 0;
@@ -682,7 +704,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             const int a = j * BN + half * COLS + wd * 32;  // first kv row of the word
                             const int pre = P - a;
                             uint32_t vis = pre >= 32 ? 0xffffffffu : (pre <= 0 ? 0u : ((1u << pre) - 1u));
-                            const int o = a - P;                          // tree index of bit 0
+                            const int o = a - Pt;                         // tree index of bit 0
                             if (o > -32 && o < n) {
                                 uint64_t win;
                                 if (o < 0) win = mw0 << (-o);
@@ -1004,7 +1026,7 @@ bool tree_attention_tc_supported(const st_attn_args* a) {
     const int M = (int64_t)G * a->T <= 64 ? 64 : 128;
     return (a->dtype == ST_F16 || a->dtype == ST_BF16) && a->D == HD && G >= 1 && M % G == 0 &&
            (int64_t)G * a->T <= 128 && a->W <= 2 && a->Lmax < (1ll << 31) && al(a->q) && al(a->k_cache) &&
-           al(a->v_cache) && al(a->o) &&
+           al(a->v_cache) && al(a->o) && al(a->k_tree) && al(a->v_tree) &&
            (int64_t)a->B * a->Hkv * ((a->Lmax + BN - 1) / BN) < (1ll << 31);  // 32-bit tile indices
 }
 
@@ -1028,7 +1050,7 @@ size_t tree_attention_tc_workspace(const st_attn_args* a) {
             attr = true;                                                                        \
         }                                                                                       \
         ST_CUDA_TRY(launch_pdl(tree_attn_tc_kernel<TT, MM>, dim3(G), dim3(Cfg<MM>::THREADS),     \
-                               Cfg<MM>::SMEM_BYTES, stream, tq, tk, tv, tp, prm));              \
+                               Cfg<MM>::SMEM_BYTES, stream, tq, tk, tv, tp, tkt, tvt, prm));    \
     } while (0)
 
 st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st_peer_out* po) {
@@ -1053,6 +1075,18 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
         if (!encode(&tk, dt, 3, a->k_cache, dims, strides, box) ||
             !encode(&tv, dt, 3, a->v_cache, dims, strides, box)) {
             set_error("st_tree_attention: cuTensorMapEncodeTiled(kv) failed");
+            return ST_ERR_CUDA;
+        }
+    }
+    CUtensorMap tkt = tk, tvt = tv;  // k_tree mode: the tree's rows, [B][T][Hkv][D], 128-node boxes
+    if (a->k_tree) {
+        const uint64_t dims[4] = {(uint64_t)HD, (uint64_t)a->Hkv, (uint64_t)a->T, (uint64_t)a->B};
+        const uint64_t strides[3] = {HD * 2ull, (uint64_t)a->Hkv * HD * 2,
+                                     (uint64_t)a->T * a->Hkv * HD * 2};
+        const uint32_t box[4] = {64, 1, BN, 1};
+        if (!encode(&tkt, dt, 4, a->k_tree, dims, strides, box) ||
+            !encode(&tvt, dt, 4, a->v_tree, dims, strides, box)) {
+            set_error("st_tree_attention: cuTensorMapEncodeTiled(k_tree/v_tree) failed");
             return ST_ERR_CUDA;
         }
     }
@@ -1081,6 +1115,7 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
     prm.H = a->Hkv;
     prm.G = a->H / a->Hkv;
     prm.Hq = a->H;
+    prm.tree_src = a->k_tree != nullptr;
     prm.W = a->W;
     prm.scale = (float)a->scale;
     prm.c_log2 = (float)(a->scale * 1.4426950408889634);

@@ -251,7 +251,9 @@ walk_compact_kernel(int T, const int32_t* __restrict__ tokens, const int32_t* __
                     int32_t* __restrict__ verified, int32_t* __restrict__ ids,
                     int32_t* __restrict__ len, char* k_cache, char* v_cache, int Hkv,
                     int row_vecs, int64_t Lmax, int nhc, int hpb, int64_t layer_stride_bytes,
-                    const int32_t* __restrict__ prefix_len, int32_t* __restrict__ new_prefix_len) {
+                    const int32_t* __restrict__ prefix_len, int32_t* __restrict__ new_prefix_len,
+                    const char* __restrict__ k_tree, const char* __restrict__ v_tree,
+                    int64_t tree_layer_stride_bytes) {
     pdl_wait();
     pdl_trigger();
     __shared__ int s_out[kWalkMax], s_next[kWalkMax], s_ver[kWalkMax + 1], s_ids[kWalkMax + 1];
@@ -309,14 +311,19 @@ walk_compact_kernel(int T, const int32_t* __restrict__ tokens, const int32_t* __
             if (new_prefix_len) new_prefix_len[b] = (int32_t)(P + L);
         }
     }
-    // ---- compaction of rows 1..L-1 for heads [hc*hpb, hc*hpb + hpb) of this layer ----
+    // ---- compaction of rows k0..L-1 for heads [hc*hpb, hc*hpb + hpb) of this layer ----
+    // (in place: rows 1.. from cache row P + ids[k]; k_tree mode: rows 0.. from
+    // the tree's own K/V, tree[b][ids[k]][h])
     const int h0 = hc * hpb, nh = min(hpb, Hkv - h0);
-    if (L <= 1 || nh <= 0) return;
+    const int kfirst = k_tree ? 0 : 1;
+    if (L <= kfirst || nh <= 0) return;
     char* kl = k_cache + layer * layer_stride_bytes;
     char* vl = v_cache + layer * layer_stride_bytes;
+    const char* ktl = k_tree ? k_tree + layer * tree_layer_stride_bytes : nullptr;
+    const char* vtl = v_tree ? v_tree + layer * tree_layer_stride_bytes : nullptr;
     const int per_row = nh * row_vecs;                        // vectors of one row, all heads
     const int rows_chunk = max(1, kWcThreads * kWcVecs / (2 * per_row));
-    for (int k0 = 1; k0 < L; k0 += rows_chunk) {
+    for (int k0 = kfirst; k0 < L; k0 += rows_chunk) {
         const int k1 = min(L, k0 + rows_chunk);
         const int total = (k1 - k0) * per_row;
         V kx[kWcVecs], vx[kWcVecs];
@@ -329,8 +336,13 @@ walk_compact_kernel(int T, const int32_t* __restrict__ tokens, const int32_t* __
                 const int kk = k0 + i / per_row, rem = i % per_row;
                 const int h = h0 + rem / row_vecs, e = rem % row_vecs;
                 const int src = s_ids[kk];
-                if (src != kk) {
-                    const int64_t base = ((int64_t)b * Hkv + h) * Lmax + P;
+                const int64_t base = ((int64_t)b * Hkv + h) * Lmax + P;
+                if (ktl) {
+                    const int64_t so = (((int64_t)b * T + src) * Hkv + h) * row_vecs + e;
+                    dst[r] = (base + kk) * row_vecs + e;
+                    kx[r] = reinterpret_cast<const V*>(ktl)[so];
+                    vx[r] = reinterpret_cast<const V*>(vtl)[so];
+                } else if (src != kk) {
                     const int64_t so = (base + src) * row_vecs + e;
                     dst[r] = (base + kk) * row_vecs + e;
                     kx[r] = reinterpret_cast<const V*>(kl)[so];
@@ -402,8 +414,9 @@ st_status st_verify_greedy_compact(const float* logits, int B, int T, int V, con
                                    int32_t* verified, int32_t* ids, int32_t* len, void* workspace,
                                    st_dtype dtype, int Hkv, int D, int64_t Lmax, int n_layers,
                                    int64_t layer_stride, const int32_t* prefix_len,
-                                   int32_t* new_prefix_len, void* k_cache, void* v_cache,
-                                   void* stream) {
+                                   int32_t* new_prefix_len, const void* k_tree,
+                                   const void* v_tree, int64_t tree_layer_stride, void* k_cache,
+                                   void* v_cache, void* stream) {
     if (st_status e = st::require_device()) return e;
     ST_CHECK_ARG(B >= 0 && T >= 1 && V >= 1 && Hkv >= 1 && D >= 1 && n_layers >= 1,
                  ST_ERR_SHAPE_MISMATCH, "bad shape");
@@ -414,6 +427,8 @@ st_status st_verify_greedy_compact(const float* logits, int B, int T, int V, con
                  ST_ERR_INVALID_ARGUMENT, "null pointer");
     ST_CHECK_ARG(new_prefix_len != prefix_len, ST_ERR_INVALID_ARGUMENT,
                  "new_prefix_len must not alias prefix_len");
+    ST_CHECK_ARG((k_tree == nullptr) == (v_tree == nullptr), ST_ERR_INVALID_ARGUMENT,
+                 "k_tree and v_tree must be both set or both NULL");
     ST_CHECK_ARG(B <= 65535 && T <= st::kWalkMax, ST_ERR_SHAPE_MISMATCH,
                  "B <= 65535 and T <= 1024 (use st_verify_greedy + st_kv_compact)");
     ST_CHECK_ARG((reinterpret_cast<uintptr_t>(workspace) & 7) == 0, ST_ERR_INVALID_ARGUMENT,
@@ -435,7 +450,8 @@ st_status st_verify_greedy_compact(const float* logits, int B, int T, int V, con
                                dim3(st::kWcThreads), 0, strm, T, tokens, parent, n_nodes, budget,
                                eos, argmax, (const unsigned long long*)keys, verified, ids, len,
                                (char*)k_cache, (char*)v_cache, Hkv, row_vecs, Lmax, nhc, hpb,
-                               layer_stride * es, prefix_len, new_prefix_len));
+                               layer_stride * es, prefix_len, new_prefix_len,
+                               (const char*)k_tree, (const char*)v_tree, tree_layer_stride * es));
     ST_LAUNCH_CHECK();
     return ST_OK;
 }

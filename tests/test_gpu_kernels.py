@@ -17,7 +17,11 @@ from tests.treegen import masks, pack, random_seqs, width_depth_seqs
 
 pytestmark = pytest.mark.gpu
 
-TOL = {torch.float64: 1e-12, torch.float32: 2e-6, torch.float16: 2e-3, torch.bfloat16: 2e-3}
+# max-abs vs the f64 restatement on the same rounded inputs. bf16 keeps 8
+# mantissa bits (f16: 11): rounding P before P.V and rounding O each cost up to
+# ~2^-9 relative, so bf16 gets 4e-3 where f16 meets 2e-3 (measured worst cases:
+# f16 3.7e-4, bf16 3.1e-3 on the same tree batch).
+TOL = {torch.float64: 1e-12, torch.float32: 2e-6, torch.float16: 2e-3, torch.bfloat16: 4e-3}
 
 
 @pytest.fixture(scope="module")

@@ -156,3 +156,81 @@ def test_tc_gqa_head_groups(capi, restatement, G, T, dtype):
     assert capi is not None
     out, lse = run_k1(capi, bt, dtype, force_path=2, lse=True)
     check_k1(restatement, bt, out, dtype, lse)
+
+
+@pytest.mark.parametrize("path,G,dtype", [(2, 1, torch.float16), (2, 4, torch.bfloat16),
+                                          (1, 1, torch.float16), (1, 2, torch.float32)])
+def test_k1_tree_rows_from_k_tree(capi, restatement, path, G, dtype):
+    """st_attn_args.k_tree/v_tree: the tree rows come from the tree's own
+    [B][T][Hkv][D] tensors (no append); cache rows [P, P+n) hold junk (finite,
+    large) that must not leak into any output."""
+    rng = np.random.default_rng(40 + path * 10 + G)
+    Hkv, T = 2, 32
+    trees = [restatement.merge(width_depth_seqs(rng, int(rng.integers(0, 50)), 50, 3, 10), 4096)
+             for _ in range(6)]
+    bt = make_batch(restatement, rng, 6, G * Hkv, Hkv, 128, trees=trees, T=T, P_range=(0, 500),
+                    dtype=dtype)
+    bt["P"][0] = 0          # no committed prefix at all
+    bt["P"][1] = 256        # prefix ends on a tile boundary
+    dev = "cuda"
+    q = torch.tensor(bt["q"], device=dev).to(dtype)
+    kc = torch.tensor(bt["kc"], device=dev).to(dtype)
+    vc = torch.tensor(bt["vc"], device=dev).to(dtype)
+    B = q.shape[0]
+    kt = torch.zeros(B, T, Hkv, 128, dtype=dtype, device=dev)
+    vt = torch.zeros_like(kt)
+    for b in range(B):
+        P, n = int(bt["P"][b]), int(bt["n"][b])
+        kt[b, :n] = kc[b, :, P:P + n].transpose(0, 1)
+        vt[b, :n] = vc[b, :, P:P + n].transpose(0, 1)
+        kc[b, :, P:P + n] = 300.0   # junk where the appended rows would be
+        vc[b, :, P:P + n] = -500.0
+    mask = torch.tensor(bt["mask"].view(np.int64), device=dev)
+    out = torch.zeros_like(q)
+    lse = torch.zeros((B, G * Hkv, T), dtype=torch.float32, device=dev)
+    capi.tree_attention(q, kc, vc, mask, torch.tensor(bt["P"], device=dev),
+                        torch.tensor(bt["n"], device=dev), out=out, lse=lse, force_path=path,
+                        k_tree=kt, v_tree=vt)
+    torch.cuda.synchronize()
+    check_k1(restatement, bt, out, dtype, lse)
+
+
+def test_verify_compact_from_k_tree(capi, restatement):
+    """st_verify_greedy_compact with k_tree/v_tree: the accepted rows are copied
+    from the tree's own K/V into cache rows [P, P+len) — the same cache as
+    append + in-place compaction."""
+    rng = np.random.default_rng(8)
+    V, Hkv, D, Lmax, layers = 500, 6, 128, 300, 2
+    trees = [restatement.merge(width_depth_seqs(rng, int(rng.integers(0, 8)), 8, 2, 12), 1024)
+             for _ in range(4)]
+    tok, par, dep, n = pack(trees)
+    B, T = tok.shape
+    logits = rng.standard_normal((B, T, V)).astype(np.float32)
+    for b in range(B):
+        for u in range(n[b]):
+            kids = [v for v in range(n[b]) if par[b, v] == u]
+            if kids and rng.random() < 0.9:
+                logits[b, u, tok[b, kids[0]]] = 10.0
+    dev = "cuda"
+    lg, tk, pr, nd = (torch.tensor(x, device=dev) for x in (logits, tok, par, n))
+    P = torch.tensor(rng.integers(0, 100, B), dtype=torch.int32, device=dev)
+    kc = torch.randn(layers, B, Hkv, Lmax, D, device=dev).half()
+    vc = torch.randn(layers, B, Hkv, Lmax, D, device=dev).half()
+    kt = torch.randn(layers, B, T, Hkv, D, device=dev).half()
+    vt = torch.randn(layers, B, T, Hkv, D, device=dev).half()
+    # reference flow: append each layer's tree rows, then in-place compaction
+    k1, v1 = kc.clone(), vc.clone()
+    for l in range(layers):
+        capi.kv_append(kt[l], vt[l], P, nd, k1[l], v1[l])
+    a1, ver1, ids1, ln1 = capi.verify_greedy(lg, tk, pr, nd)
+    capi.kv_compact(ids1, ln1, P, k1, v1)
+    k2, v2 = kc.clone(), vc.clone()
+    a2, ver2, ids2, ln2 = capi.verify_greedy_compact(lg, tk, pr, nd, P, k2, v2, k_tree=kt,
+                                                     v_tree=vt)
+    torch.cuda.synchronize()
+    assert torch.equal(ln1, ln2) and torch.equal(ver1, ver2) and torch.equal(ids1, ids2)
+    assert int(ln1.max()) > 3
+    for b in range(B):
+        p, L = int(P[b]), int(ln1[b])
+        assert torch.equal(k1[:, b, :, : p + L], k2[:, b, :, : p + L])
+        assert torch.equal(v1[:, b, :, : p + L], v2[:, b, :, : p + L])
