@@ -86,9 +86,12 @@ def lib():
     """Load libspectree_b200.so (fails loudly: no fallback exists)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(_LIB_PATH):
-            raise SpectreeError(102, f"{_LIB_PATH} missing: run __graft_entry__.build()")
-        L = C.CDLL(_LIB_PATH)
+        # ST_LIB_VARIANT (diagnostic A/B runs only): an alternative build of the
+        # same library, e.g. build/variants/<name>.so
+        path = os.environ.get("ST_LIB_VARIANT") or _LIB_PATH
+        if not os.path.exists(path):
+            raise SpectreeError(102, f"{path} missing: run __graft_entry__.build()")
+        L = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             if hasattr(L, name):
                 fn = getattr(L, name)
