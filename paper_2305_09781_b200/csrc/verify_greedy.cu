@@ -138,17 +138,105 @@ __device__ __forceinline__ int key_index(unsigned long long k) {
 constexpr int kSplit = 8;   // blocks per logits row (tools/argmax_bench.cu: 8 x 4 loads beat 4 x 8)
 constexpr int kUnroll = 4;  // float4 loads in flight per thread (a 4000-float slice in one batch)
 
+// Block-level walk of request b (blockDim.x threads, n <= kWalkMax):
+// greedy outputs from the slice keys, every node's matching child found in
+// parallel (children have distinct tokens: at most one matches), the pointer
+// chase from the root, then the engine's budget truncation and EOS cut
+// (engine.cpp:110-121). Results in shared memory: s_ids/s_ver [0, *s_full)
+// and the truncated length *s_len. `lead`: also write argmax_out, the
+// verified/ids rows and len to global memory.
+struct WalkSmem {
+    int out[kWalkMax], next[kWalkMax], ver[kWalkMax + 1], ids[kWalkMax + 1];
+    int len, full;
+};
+
+__device__ unsigned long long resolve_max(const unsigned long long* keys, int64_t row);
+
+__device__ void walk_block(WalkSmem& w, const unsigned long long* keys, int T, int b, int n,
+                           const int32_t* __restrict__ tokens, const int32_t* __restrict__ parent,
+                           const int32_t* __restrict__ budget, int32_t eos, bool lead,
+                           int32_t* __restrict__ argmax_out, int32_t* __restrict__ verified,
+                           int32_t* __restrict__ ids, int32_t* __restrict__ len) {
+    const int32_t* tok = tokens + (int64_t)b * T;
+    const int32_t* par = parent + (int64_t)b * T;
+    for (int v = threadIdx.x; v < n; v += blockDim.x) {
+        const int a = key_index(resolve_max(keys, (int64_t)b * T + v));
+        w.out[v] = a;
+        w.next[v] = -1;
+        if (lead && argmax_out) argmax_out[(int64_t)b * T + v] = a;
+    }
+    __syncthreads();
+    for (int v = 1 + threadIdx.x; v < n; v += blockDim.x) {
+        const int u = par[v];
+        if (tok[v] == w.out[u]) w.next[u] = v;  // one writer per u
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int m = 0, cur = 0;
+        w.ids[0] = 0;
+        for (int nx = n > 0 ? w.next[0] : -1; nx >= 0; nx = w.next[cur]) {
+            w.ver[m] = w.out[cur];
+            w.ids[m + 1] = nx;
+            cur = nx;
+            ++m;
+        }
+        w.ver[m] = n > 0 ? w.out[cur] : 0;  // bonus token
+        w.full = n > 0 ? m + 1 : 0;
+        int L = w.full;
+        if (budget && L > budget[b]) L = budget[b] > 0 ? budget[b] : 0;
+        if (eos >= 0) {
+            for (int k = 0; k < L; ++k)
+                if (w.ver[k] == eos) { L = k + 1; break; }
+        }
+        w.len = L;
+    }
+    __syncthreads();
+    if (lead) {
+        // the whole walk (path + bonus); len carries the budget / EOS truncation
+        int32_t* vrow = verified + (int64_t)b * (T + 1);
+        int32_t* irow = ids + (int64_t)b * (T + 1);
+        for (int k = threadIdx.x; k < w.full; k += blockDim.x) {
+            vrow[k] = w.ver[k];
+            irow[k] = w.ids[k];
+        }
+        if (threadIdx.x == 0) len[b] = w.len;
+    }
+}
+
 // Phase 1: stream every live node's logits once; kSplit blocks per row each
 // reduce their slice to one order-preserving key, written to its own slot
 // keys[b][u][part] (no atomics, nothing to reset; the consumer takes the max
 // of the kSplit keys — order-independent, hence deterministic).
+//
+// Fused walk (`counters` != NULL, T <= kWalkMax): after publishing its key a
+// block counts itself in (threadfence + atomicAdd, the classic last-block
+// pattern — no block ever waits for another); the block that completes
+// request b's n*kSplit keys runs the walk for b and re-arms the counter. One
+// launch instead of argmax + a dependent walk kernel.
+struct WalkArgs {
+    unsigned* counters;  // [B], zero between calls
+    const int32_t* tokens;
+    const int32_t* parent;
+    const int32_t* budget;
+    int32_t eos;
+    int32_t* argmax_out;
+    int32_t* verified;
+    int32_t* ids;
+    int32_t* len;
+};
+
 __global__ void __launch_bounds__(kThreads)
 greedy_argmax_kernel(const float* __restrict__ logits, int T, int V,
-                     const int32_t* __restrict__ n_nodes, unsigned long long* keys) {
+                     const int32_t* __restrict__ n_nodes, unsigned long long* keys,
+                     const WalkArgs wa) {
     pdl_wait();
-    pdl_trigger();  // let the walk kernel get scheduled while the rows stream
+    pdl_trigger();  // let the next kernel get scheduled while the rows stream
     const int part = blockIdx.x, u = blockIdx.y, b = blockIdx.z;
-    if (u >= n_nodes[b]) return;
+    const int n = n_nodes[b];
+    if (u >= n) {
+        if (wa.counters && n <= 0 && u == 0 && part == 0 && threadIdx.x == 0) wa.len[b] = 0;
+        return;
+    }
     const float* row = logits + ((int64_t)b * T + u) * V;
     const bool vec = ((reinterpret_cast<uintptr_t>(row) & 15) == 0) && (V % 4 == 0);
     unsigned long long best = 0;
@@ -192,18 +280,34 @@ greedy_argmax_kernel(const float* __restrict__ logits, int T, int V,
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) red[warp] = best;
     __syncthreads();
+    __shared__ bool s_last;
     if (threadIdx.x == 0) {
         for (int w = 1; w < kThreads / 32; ++w) best = max(best, red[w]);
         keys[((int64_t)b * T + u) * kSplit + part] = best;
+        if (wa.counters) {
+            __threadfence();  // the key before the count
+            s_last = atomicAdd(wa.counters + b, 1u) == (unsigned)(n * kSplit) - 1u;
+        }
     }
+    if (!wa.counters) return;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();  // every other block's key is visible (they fenced before counting)
+    __shared__ WalkSmem w;
+    walk_block(w, keys, T, b, n, wa.tokens, wa.parent, wa.budget, wa.eos, true, wa.argmax_out,
+               wa.verified, wa.ids, wa.len);
+    if (threadIdx.x == 0) wa.counters[b] = 0u;  // re-armed for the next call
 }
 
 // Greedy output of node v: the best of its kSplit slice keys.
-__device__ __forceinline__ int resolve_key(const unsigned long long* keys, int64_t row) {
+__device__ unsigned long long resolve_max(const unsigned long long* keys, int64_t row) {
     unsigned long long k = 0;
 #pragma unroll
     for (int j = 0; j < kSplit; ++j) k = max(k, __ldcg(keys + row * kSplit + j));
-    return key_index(k);
+    return k;
+}
+__device__ __forceinline__ int resolve_key(const unsigned long long* keys, int64_t row) {
+    return key_index(resolve_max(keys, row));
 }
 
 // Phase 2 (launched with programmatic dependent launch): one warp per request
@@ -253,64 +357,26 @@ walk_compact_kernel(int T, const int32_t* __restrict__ tokens, const int32_t* __
                     int row_vecs, int64_t Lmax, int nhc, int hpb, int64_t layer_stride_bytes,
                     const int32_t* __restrict__ prefix_len, int32_t* __restrict__ new_prefix_len,
                     const char* __restrict__ k_tree, const char* __restrict__ v_tree,
-                    int64_t tree_layer_stride_bytes) {
+                    int64_t tree_layer_stride_bytes, int walk_done) {
     pdl_wait();
     pdl_trigger();
-    __shared__ int s_out[kWalkMax], s_next[kWalkMax], s_ver[kWalkMax + 1], s_ids[kWalkMax + 1];
-    __shared__ int s_len, s_full;
+    __shared__ WalkSmem w;
     const int b = blockIdx.x, layer = blockIdx.y / nhc, hc = blockIdx.y % nhc;
     const int n = n_nodes[b];
     const bool lead = blockIdx.y == 0;
-    const int32_t* tok = tokens + (int64_t)b * T;
-    const int32_t* par = parent + (int64_t)b * T;
-    for (int v = threadIdx.x; v < n; v += kWcThreads) {
-        const int a = resolve_key(keys, (int64_t)b * T + v);
-        s_out[v] = a;
-        s_next[v] = -1;
-        if (lead && argmax_out) argmax_out[(int64_t)b * T + v] = a;
+    if (walk_done) {  // the argmax kernel already walked: accepted ids and len from global
+        const int L0 = len[b];
+        for (int k = threadIdx.x; k < L0; k += kWcThreads) w.ids[k] = ids[(int64_t)b * (T + 1) + k];
+        if (threadIdx.x == 0) w.len = L0;
+        __syncthreads();
+    } else {
+        walk_block(w, keys, T, b, n, tokens, parent, budget, eos, lead, argmax_out, verified, ids,
+                   len);
     }
-    __syncthreads();
-    for (int v = 1 + threadIdx.x; v < n; v += kWcThreads) {
-        const int u = par[v];
-        if (tok[v] == s_out[u]) s_next[u] = v;  // children have unique tokens: one writer
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int m = 0, cur = 0;
-        s_ids[0] = 0;
-        for (int nx = n > 0 ? s_next[0] : -1; nx >= 0; nx = s_next[cur]) {
-            s_ver[m] = s_out[cur];
-            s_ids[m + 1] = nx;
-            cur = nx;
-            ++m;
-        }
-        s_ver[m] = n > 0 ? s_out[cur] : 0;  // bonus token
-        s_full = n > 0 ? m + 1 : 0;
-        int L = s_full;
-        if (budget && L > budget[b]) L = budget[b] > 0 ? budget[b] : 0;
-        if (eos >= 0) {
-            for (int k = 0; k < L; ++k)
-                if (s_ver[k] == eos) { L = k + 1; break; }
-        }
-        s_len = L;
-    }
-    __syncthreads();
-    const int L = s_len;
+    const int* s_ids = w.ids;
+    const int L = w.len;
     const int64_t P = prefix_len[b];
-    if (lead) {
-        int32_t* vrow = verified + (int64_t)b * (T + 1);
-        int32_t* irow = ids + (int64_t)b * (T + 1);
-        // the whole walk (path + bonus), as st_verify_greedy writes it; len
-        // carries the budget / EOS truncation
-        for (int k = threadIdx.x; k < s_full; k += kWcThreads) {
-            vrow[k] = s_ver[k];
-            irow[k] = s_ids[k];
-        }
-        if (threadIdx.x == 0) {
-            len[b] = L;
-            if (new_prefix_len) new_prefix_len[b] = (int32_t)(P + L);
-        }
-    }
+    if (lead && threadIdx.x == 0 && new_prefix_len) new_prefix_len[b] = (int32_t)(P + L);
     // ---- compaction of rows k0..L-1 for heads [hc*hpb, hc*hpb + hpb) of this layer ----
     // (in place: rows 1.. from cache row P + ids[k]; k_tree mode: rows 0.. from
     // the tree's own K/V, tree[b][ids[k]][h])
@@ -378,8 +444,10 @@ __global__ void build_masks_kernel(const int32_t* __restrict__ parent,
 extern "C" {
 
 size_t st_verify_workspace_size(int B, int T) {
-    // slice keys [B][T][kSplit] u64 | argmax scratch [B][T]
-    return (size_t)B * T * st::kSplit * 8 + (size_t)B * T * sizeof(int32_t) + 512;
+    // slice keys [B][T][kSplit] u64 | argmax scratch [B][T] | walk counters [B]
+    // (zeroed once by the caller; every call leaves the counters zero)
+    return (size_t)B * T * st::kSplit * 8 + (size_t)B * T * sizeof(int32_t) +
+           (size_t)B * sizeof(unsigned) + 512;
 }
 
 st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32_t* tokens,
@@ -396,10 +464,19 @@ st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32
                  "workspace must be 8-byte aligned");
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(workspace);
     int32_t* scratch = reinterpret_cast<int32_t*>(keys + (size_t)B * T * st::kSplit);
+    unsigned* counters = reinterpret_cast<unsigned*>(scratch + (size_t)B * T);
     const dim3 grid(st::kSplit, T, B);
     auto strm = st::as_stream(stream);
+    if (T <= st::kWalkMax) {  // one launch: the last argmax block of each request walks it
+        const st::WalkArgs wa{counters, tokens, parent, budget, eos, argmax, verified, ids, len};
+        ST_CUDA_TRY(st::launch_pdl(st::greedy_argmax_kernel, grid, dim3(st::kThreads), 0, strm,
+                                   logits, T, V, n_nodes, keys, wa));
+        ST_LAUNCH_CHECK();
+        return ST_OK;
+    }
+    const st::WalkArgs none{};
     ST_CUDA_TRY(st::launch_pdl(st::greedy_argmax_kernel, grid, dim3(st::kThreads), 0, strm, logits,
-                               T, V, n_nodes, keys));
+                               T, V, n_nodes, keys, none));
     ST_LAUNCH_CHECK();
     ST_CUDA_TRY(st::launch_pdl(st::greedy_walk_kernel, dim3(B), dim3(32), 0, strm, T, tokens,
                                parent, n_nodes, budget, eos, argmax, keys, scratch, verified, ids,
@@ -437,8 +514,13 @@ st_status st_verify_greedy_compact(const float* logits, int B, int T, int V, con
     ST_CHECK_ARG(row_bytes % 16 == 0, ST_ERR_SHAPE_MISMATCH, "D * sizeof(dtype) must be a multiple of 16");
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(workspace);
     auto strm = st::as_stream(stream);
+    // argmax, then the compaction kernel, every block of which repeats its
+    // request's walk (measured: fusing the walk into the argmax kernel's last
+    // block instead costs 1.8 us per C2 step here — the compaction has to
+    // follow as a kernel anyway, so it only lengthens the argmax tail)
+    const st::WalkArgs none{};
     ST_CUDA_TRY(st::launch_pdl(st::greedy_argmax_kernel, dim3(st::kSplit, T, B), dim3(st::kThreads), 0,
-                               strm, logits, T, V, n_nodes, keys));
+                               strm, logits, T, V, n_nodes, keys, none));
     ST_LAUNCH_CHECK();
     // heads per block: about 2 KB of K+V per accepted row per block
     const int row_vecs = (int)(row_bytes / 16);
@@ -451,7 +533,7 @@ st_status st_verify_greedy_compact(const float* logits, int B, int T, int V, con
                                eos, argmax, (const unsigned long long*)keys, verified, ids, len,
                                (char*)k_cache, (char*)v_cache, Hkv, row_vecs, Lmax, nhc, hpb,
                                layer_stride * es, prefix_len, new_prefix_len,
-                               (const char*)k_tree, (const char*)v_tree, tree_layer_stride * es));
+                               (const char*)k_tree, (const char*)v_tree, tree_layer_stride * es, 0));
     ST_LAUNCH_CHECK();
     return ST_OK;
 }
