@@ -216,16 +216,23 @@ __device__ Seg find_seg(const TcParams& p, const int* cum, uint32_t t, uint32_t 
 
 // CTA work ranges over the pair-major tile sequence. Stream-K (equal tile
 // counts; pairs may be split, leaving pieces that the pair's head owner merges
-// in-kernel) unless every pair has the same tile count and whole-pair ranges
-// cost at most aligned_slack tiles more than perfect balance — then CTA c
-// takes pairs [c*Np/G, (c+1)*Np/G) and no pair is split.
+// in-kernel) unless every pair has the same tile count and a static shape is
+// within aligned_slack tiles of perfect balance:
+//   * aligned: CTA c takes pairs [c*Np/G, (c+1)*Np/G), no pair is split;
+//   * split (Np <= G/2): every pair is cut into S = G/Np equal pieces, one
+//     per CTA (CTAs past Np*S idle) — each CTA has a single segment, so no
+//     CTA pays a second epilogue or a piece publish between two segments,
+//     which is what small batches (C4's 64 pairs x 17 tiles) lose to.
 constexpr int kAlignedSlack = 3;
+
+enum : int { kStreamK = 0, kAligned = 1, kSplit = 2 };
 
 struct Sched {
     uint32_t total;
     uint32_t np;    // pairs with tiles
     int nt;         // tiles per pair when uniform
-    bool aligned;
+    int mode;       // kStreamK / kAligned / kSplit
+    uint32_t S;     // kSplit: pieces per pair
     double inv_g;   // 1 / G, for the exact floor(c * x / G) below
 };
 
@@ -239,7 +246,7 @@ __device__ __forceinline__ uint32_t div_g(uint64_t x, uint32_t G, double inv_g) 
 }
 
 __device__ Sched make_sched(const TcParams& p, const int* cum, uint32_t G) {
-    Sched s{0, 0, 0, false, 1.0 / (double)G};
+    Sched s{0, 0, 0, kStreamK, 1, 1.0 / (double)G};
     int lo = 1 << 30, hi = 0;
     if (cum) {
         s.total = (uint32_t)p.H * (uint32_t)cum[p.B];
@@ -258,16 +265,28 @@ __device__ Sched make_sched(const TcParams& p, const int* cum, uint32_t G) {
     }
     if (s.np > 0 && lo == hi) {
         s.nt = lo;
-        const uint32_t aligned_span = div_g(s.np + G - 1, G, s.inv_g) * (uint32_t)s.nt;
-        const uint32_t streamk_span = div_g(s.total + G - 1, G, s.inv_g);
-        s.aligned = (long long)aligned_span <= (long long)streamk_span + p.aligned_slack;
+        const long long aligned_span = div_g(s.np + G - 1, G, s.inv_g) * (uint32_t)s.nt;
+        const long long streamk_span = div_g(s.total + G - 1, G, s.inv_g);
+        const uint32_t S = s.np <= G ? min(G / s.np, (uint32_t)s.nt) : 0;
+        const long long split_span = S >= 2 ? (s.nt + S - 1) / S : 1ll << 40;
+        if (aligned_span <= streamk_span + p.aligned_slack) {
+            s.mode = kAligned;
+        } else if (split_span <= streamk_span + p.aligned_slack) {
+            s.mode = kSplit;
+            s.S = S;
+        }
     }
     return s;
 }
 
 __device__ __forceinline__ uint32_t range_start(uint32_t c, const Sched& s, uint32_t G) {
-    return s.aligned ? div_g((uint64_t)c * s.np, G, s.inv_g) * (uint32_t)s.nt
-                     : div_g((uint64_t)c * s.total, G, s.inv_g);
+    if (s.mode == kAligned) return div_g((uint64_t)c * s.np, G, s.inv_g) * (uint32_t)s.nt;
+    if (s.mode == kSplit) {
+        if (c >= s.np * s.S) return s.total;
+        const uint32_t pr = c / s.S, k = c - pr * s.S;
+        return pr * (uint32_t)s.nt + (k * (uint32_t)s.nt) / s.S;
+    }
+    return div_g((uint64_t)c * s.total, G, s.inv_g);
 }
 
 template <class T> struct pk2;

@@ -234,3 +234,19 @@ def test_verify_compact_from_k_tree(capi, restatement):
         p, L = int(P[b]), int(ln1[b])
         assert torch.equal(k1[:, b, :, : p + L], k2[:, b, :, : p + L])
         assert torch.equal(v1[:, b, :, : p + L], v2[:, b, :, : p + L])
+
+
+@pytest.mark.parametrize("B,H,P,T", [(2, 4, 3000, 32), (8, 8, 2048, 61), (1, 3, 700, 128)])
+def test_tc_split_schedule(capi, restatement, B, H, P, T):
+    """Uniform pairs with Np <= G/2 take the split schedule: every pair cut into
+    S = G/Np equal single-segment pieces (S = 18 for 8 pairs: the head owner
+    merges 17 pieces, 2 staged in shared memory and the rest from L2)."""
+    rng = np.random.default_rng(B * 7 + H)
+    w = 3 if T >= 16 else 2
+    trees = [restatement.merge(width_depth_seqs(rng, int(rng.integers(0, 50)), 50, w, (T - 1) // w),
+                               4096) for _ in range(B)]
+    bt = make_batch(restatement, rng, B, H, H, 128, trees=trees, T=T, P_range=(P, P),
+                    dtype=torch.float16)
+    bt["n"][:] = bt["n"].max()   # uniform tile counts (pad the node counts)
+    out, lse = run_k1(capi, bt, torch.float16, force_path=2, lse=True)
+    check_k1(restatement, bt, out, torch.float16, lse)
