@@ -59,6 +59,78 @@ __global__ void __launch_bounds__(NT) argmax_kernel(const float* __restrict__ lo
     }
 }
 
+// Persistent variant: G blocks loop over the B*T*SPLIT slices (grid-stride),
+// the next slice's loads issued before the current slice is reduced.
+template <int SPLIT, int UNROLL, int NT>
+__global__ void __launch_bounds__(NT) argmax_persist(const float* __restrict__ logits, int T, int V,
+                                                     unsigned long long* keys, int nslices) {
+    const int nv = V >> 2;
+    const int per = (nv + SPLIT - 1) / SPLIT;
+    __shared__ unsigned long long red[2][NT / 32];
+    int sl = blockIdx.x;
+    float4 x[UNROLL];
+    auto load = [&](int s_, float4 (&dst)[UNROLL]) {
+        const int part = s_ % SPLIT, row = s_ / SPLIT;
+        const float4* r4 = reinterpret_cast<const float4*>(logits + (int64_t)row * V);
+        const int lo = part * per, hi = min(nv, lo + per);
+#pragma unroll
+        for (int k = 0; k < UNROLL; ++k) {
+            const int j = lo + threadIdx.x + k * NT;
+            dst[k] = j < hi ? __ldcs(r4 + j) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        }
+    };
+    if (sl < nslices) load(sl, x);
+    int it = 0;
+    for (; sl < nslices; sl += gridDim.x, ++it) {
+        float4 y[UNROLL];
+        const int nx = sl + gridDim.x;
+        if (nx < nslices) load(nx, y);
+        const int part = sl % SPLIT;
+        const int lo = part * per;
+        float bv = -INFINITY;
+        int bi = (lo + (int)threadIdx.x) * 4;
+#pragma unroll
+        for (int k = 0; k < UNROLL; ++k) {
+            const int j = (lo + threadIdx.x + k * NT) * 4;
+            if (x[k].x > bv) { bv = x[k].x; bi = j; }
+            if (x[k].y > bv) { bv = x[k].y; bi = j + 1; }
+            if (x[k].z > bv) { bv = x[k].z; bi = j + 2; }
+            if (x[k].w > bv) { bv = x[k].w; bi = j + 3; }
+        }
+        unsigned long long best = arg_key(bv, bi);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (lane == 0) red[it & 1][warp] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < NT / 32; ++w) best = max(best, red[it & 1][w]);
+            keys[sl] = best;
+        }
+#pragma unroll
+        for (int k = 0; k < UNROLL; ++k) x[k] = y[k];
+    }
+}
+
+template <int SPLIT, int UNROLL, int NT>
+void run_p(float* const* bufs, unsigned long long* keys, int B, int T, int V, int blocks) {
+    const int ns = B * T * SPLIT;
+    for (int i = 0; i < 6; ++i) argmax_persist<SPLIT, UNROLL, NT><<<blocks, NT>>>(bufs[i % 3], T, V, keys, ns);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 60;
+    cudaEventRecord(e0);
+    for (int i = 0; i < iters; ++i) argmax_persist<SPLIT, UNROLL, NT><<<blocks, NT>>>(bufs[i % 3], T, V, keys, ns);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double us = ms * 1e3 / iters;
+    printf("persistent split %d unroll %2d threads %4d blocks %4d: %7.2f us  %6.0f GB/s\n", SPLIT, UNROLL, NT,
+           blocks, us, 4.0 * B * T * V / us / 1e3);
+}
+
 template <int SPLIT, int UNROLL, int NT>
 void run(float* const* bufs, unsigned long long* keys, int B, int T, int V) {
     dim3 grid(SPLIT, T, B);
@@ -96,5 +168,12 @@ int main() {
     run<16, 4, 128>(bufs, keys, B, T, V);
     run<4, 4, 512>(bufs, keys, B, T, V);
     run<4, 8, 256>(bufs, keys, B, T, V);
+    run_p<8, 4, 256>(bufs, keys, B, T, V, 148 * 4);
+    run_p<8, 4, 256>(bufs, keys, B, T, V, 148 * 8);
+    run_p<16, 2, 256>(bufs, keys, B, T, V, 148 * 8);
+    run_p<4, 8, 256>(bufs, keys, B, T, V, 148 * 4);
+    run_p<4, 8, 256>(bufs, keys, B, T, V, 148 * 8);
+    run_p<2, 16, 256>(bufs, keys, B, T, V, 148 * 4);
+    run<8, 4, 256>(bufs, keys, B, T, V);
     return 0;
 }
