@@ -295,8 +295,11 @@ def main():
             _capi.tree_prepare(kn, vn, P, nd, kc, vc, pr, out=mask_buf)
 
     def k1(qq, kn, vn, tk, pr, nd):
+        # early_kv: the kernel before K1 (masks / append+masks) writes neither the
+        # lengths nor the committed rows [0, P), so K1 streams them while it drains
         _capi.tree_attention(qq, kc, vc, mask_buf, P, nd, out=out, workspace=ws_attn,
-                             k_tree=kn if own else None, v_tree=vn if own else None)
+                             k_tree=kn if own else None, v_tree=vn if own else None,
+                             early_kv=True)
 
     def post(qq, kn, vn, tk, pr, nd):  # K3 argmax, then the walk fused with the K2 commit
         _capi.verify_greedy_compact(logits, tk, pr, nd, P, kc, vc, workspace=ws_ver,

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define ST_ABI_VERSION 2
+#define ST_ABI_VERSION 3
 
 typedef int st_status;
 
@@ -99,6 +99,13 @@ typedef struct {
      * are in the cache at [P[b], P[b]+n[b]). */
     const void* k_tree;
     const void* v_tree;
+    /* Optional promise (0 = off): the kernel launched right before K1 on the
+     * stream writes neither prefix_len / n_nodes nor the committed cache rows
+     * [0, P[b]). K1 (tcgen05 path, programmatic dependent launch) then builds
+     * its schedule and starts streaming those rows while that kernel drains,
+     * before griddepcontrol.wait; Q, the masks and tree rows are still read
+     * after the wait. */
+    int early_kv;
 } st_attn_args;
 
 size_t st_tree_attention_workspace_size(const st_attn_args* a);

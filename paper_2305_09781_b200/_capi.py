@@ -43,7 +43,8 @@ class AttnArgs(C.Structure):
                 ("mask", C.c_void_p), ("prefix_len", C.c_void_p), ("n_nodes", C.c_void_p),
                 ("o", C.c_void_p), ("lse", C.c_void_p), ("scale", C.c_double),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
-                ("force_path", C.c_int), ("k_tree", C.c_void_p), ("v_tree", C.c_void_p)]
+                ("force_path", C.c_int), ("k_tree", C.c_void_p), ("v_tree", C.c_void_p),
+                ("early_kv", C.c_int)]
 
 
 _lib = None
@@ -117,7 +118,7 @@ def _stream(stream=None):
 
 # ------------------------------------------------------------------ K1 ----
 def attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, lse=None, scale=None,
-              workspace=None, force_path=0, k_tree=None, v_tree=None):
+              workspace=None, force_path=0, k_tree=None, v_tree=None, early_kv=False):
     B, T, H, D = q.shape
     Hkv, Lmax = k_cache.shape[1], k_cache.shape[2]
     a = AttnArgs()
@@ -133,6 +134,7 @@ def attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, lse=None, sca
     a.force_path = force_path
     a.k_tree = k_tree.data_ptr() if k_tree is not None else None
     a.v_tree = v_tree.data_ptr() if v_tree is not None else None
+    a.early_kv = 1 if early_kv else 0
     return a
 
 
@@ -151,7 +153,7 @@ def tree_attention_path(q, k_cache, v_cache, mask, prefix_len, n_nodes, force_pa
 
 def tree_attention(q, k_cache, v_cache, mask, prefix_len, n_nodes, out=None, lse=None,
                    scale=None, workspace=None, force_path=0, stream=None, k_tree=None,
-                   v_tree=None):
+                   v_tree=None, early_kv=False):
     """K1 through st_tree_attention. Shapes: q [B,T,H,D]; caches [B,Hkv,Lmax,D];
     mask [B,T,W] int64 (uint64 bits); prefix_len/n_nodes [B] int32 (device);
     k_tree/v_tree (optional) [B,T,Hkv,D]: the tree rows, read instead of cache
@@ -162,7 +164,7 @@ def tree_attention(q, k_cache, v_cache, mask, prefix_len, n_nodes, out=None, lse
         workspace = tree_attention_workspace(q, k_cache, v_cache, mask, prefix_len, n_nodes,
                                              force_path)
     a = attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, lse, scale, workspace,
-                  force_path, k_tree, v_tree)
+                  force_path, k_tree, v_tree, early_kv)
     check(lib().st_tree_attention(C.byref(a), _stream(stream)))
     return out
 

@@ -121,6 +121,7 @@ struct TcParams {
     int B, T, H, W;      // H: KV heads (one (b, h) pair per request and KV head)
     int G, Hq;           // query heads per KV head (GQA group), query heads = G * H
     int tree_src;        // tree rows come from k_tree/v_tree: one extra tile after ceil(P/BN)
+    int early_kv;        // st_attn_args.early_kv: stream committed KV before griddepcontrol.wait
     float c_log2;        // scale * log2(e)
     float scale;
     unsigned long long* trace;  // optional pipeline trace of CTA 0 (ST_K1_TRACE)
@@ -383,8 +384,12 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     // Everything above touches no other kernel's output; from here on the
-    // lengths, masks, Q and the KV cache are read.
-    pdl_wait();
+    // lengths, masks, Q and the KV cache are read. early_kv: the caller
+    // guarantees the previous kernel writes neither the lengths nor the
+    // committed KV rows [0, P), so the schedule and the first prefix tiles of
+    // each ring go ahead of griddepcontrol.wait; every warp that reads Q, the
+    // masks, tree rows or another CTA's output waits first.
+    if (!p.early_kv) pdl_wait();
     int* cum = p.B <= kTabB ? reinterpret_cast<int*>(smem + C::OFF_TAB) : nullptr;
     if (cum && warp == 0) {
         int v[kTabB / 32];
@@ -440,8 +445,25 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         if (lane == 0) {
             const uint64_t pol = l2_policy_evict_first();  // the KV stream is read once
             uint32_t qc = 0, kc = 0;
+            bool waited = !p.early_kv;
             for (uint32_t t = t_begin; t < t_end;) {
                 const Seg s = find_seg(p, cum, t, t_end);
+                int j = s.lo;
+                if (!waited) {  // early_kv: up to KS committed-prefix K tiles before the wait
+                    const int P0 = __ldg(p.prefix_len + s.b);
+                    const int bh0 = s.b * p.H + s.h;
+                    for (; j < s.hi && kc < (uint32_t)KS &&
+                           (p.tree_src ? j < s.ntiles - 1 : j * BN + BN <= P0);
+                         ++j, ++kc) {
+                        const uint32_t st = kc;  // first use of each stage: nothing to wait for
+                        mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
+                        uint8_t* dst = sm_k + st * TILE_BYTES;
+                        tma_load_3d_hint(dst, &tm_k, k_full + st, 0, j * BN, bh0, pol);
+                        tma_load_3d_hint(dst + KV_ATOM, &tm_k, k_full + st, 64, j * BN, bh0, pol);
+                    }
+                    pdl_wait();
+                    waited = true;
+                }
                 const uint32_t qb = qc % QS;
                 mbar_wait(q_empty + qb, ((qc / QS) & 1) ^ 1);
                 mbar_arrive_expect_tx(q_full + qb, C::A_BYTES);
@@ -450,7 +472,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 tma_load_4d(sm_q + qb * C::A_BYTES + C::A_ATOM, &tm_q, q_full + qb, 64, s.h * p.G, 0, s.b);
                 ++qc;
                 const int bh = s.b * p.H + s.h;
-                for (int j = s.lo; j < s.hi; ++j, ++kc) {
+                for (; j < s.hi; ++j, ++kc) {
                     const uint32_t st = kc % KS, ph = (kc / KS) & 1;
                     mbar_wait(k_empty + st, ph ^ 1);
                     K1_TRACE(0, kc);
@@ -522,10 +544,26 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         if (lane == 0) {
             const uint64_t pol = l2_policy_evict_first();
             uint32_t vc = 0;
+            bool waited = !p.early_kv;
             for (uint32_t t = t_begin; t < t_end;) {
                 const Seg s = find_seg(p, cum, t, t_end);
                 const int bh = s.b * p.H + s.h;
-                for (int j = s.lo; j < s.hi; ++j, ++vc) {
+                int j = s.lo;
+                if (!waited) {  // early_kv: up to VS committed-prefix V tiles before the wait
+                    const int P0 = __ldg(p.prefix_len + s.b);
+                    for (; j < s.hi && vc < (uint32_t)VS &&
+                           (p.tree_src ? j < s.ntiles - 1 : j * BN + BN <= P0);
+                         ++j, ++vc) {
+                        const uint32_t st = vc;
+                        mbar_arrive_expect_tx(v_full + st, TILE_BYTES);
+                        uint8_t* dst = sm_v + st * TILE_BYTES;
+                        tma_load_3d_hint(dst, &tm_v, v_full + st, 0, j * BN, bh, pol);
+                        tma_load_3d_hint(dst + KV_ATOM, &tm_v, v_full + st, 64, j * BN, bh, pol);
+                    }
+                    pdl_wait();
+                    waited = true;
+                }
+                for (; j < s.hi; ++j, ++vc) {
                     const uint32_t st = vc % VS, ph = (vc / VS) & 1;
                     mbar_wait(v_empty + st, ph ^ 1);
                     K1_TRACE(1, vc);
@@ -681,6 +719,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         };
         Seg s_next{};
         Meta m_next{};
+        if (p.early_kv) pdl_wait();  // masks and lengths below; outputs written later
         if (t_begin < t_end) {
             s_next = find_seg(p, cum, t_begin, t_end);
             m_next = load_meta(s_next);
@@ -1135,6 +1174,7 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
     prm.G = a->H / a->Hkv;
     prm.Hq = a->H;
     prm.tree_src = a->k_tree != nullptr;
+    prm.early_kv = a->early_kv != 0;
     prm.W = a->W;
     prm.scale = (float)a->scale;
     prm.c_log2 = (float)(a->scale * 1.4426950408889634);

@@ -158,9 +158,10 @@ def test_tc_gqa_head_groups(capi, restatement, G, T, dtype):
     check_k1(restatement, bt, out, dtype, lse)
 
 
-@pytest.mark.parametrize("path,G,dtype", [(2, 1, torch.float16), (2, 4, torch.bfloat16),
-                                          (1, 1, torch.float16), (1, 2, torch.float32)])
-def test_k1_tree_rows_from_k_tree(capi, restatement, path, G, dtype):
+@pytest.mark.parametrize("path,G,dtype,early", [(2, 1, torch.float16, False), (2, 4, torch.bfloat16, False),
+                                                (2, 1, torch.float16, True), (2, 4, torch.float16, True),
+                                                (1, 1, torch.float16, False), (1, 2, torch.float32, False)])
+def test_k1_tree_rows_from_k_tree(capi, restatement, path, G, dtype, early):
     """st_attn_args.k_tree/v_tree: the tree rows come from the tree's own
     [B][T][Hkv][D] tensors (no append); cache rows [P, P+n) hold junk (finite,
     large) that must not leak into any output."""
@@ -188,9 +189,12 @@ def test_k1_tree_rows_from_k_tree(capi, restatement, path, G, dtype):
     mask = torch.tensor(bt["mask"].view(np.int64), device=dev)
     out = torch.zeros_like(q)
     lse = torch.zeros((B, G * Hkv, T), dtype=torch.float32, device=dev)
-    capi.tree_attention(q, kc, vc, mask, torch.tensor(bt["P"], device=dev),
-                        torch.tensor(bt["n"], device=dev), out=out, lse=lse, force_path=path,
-                        k_tree=kt, v_tree=vt)
+    Pd, nd = torch.tensor(bt["P"], device=dev), torch.tensor(bt["n"], device=dev)
+    q_src = q.clone()
+    q.zero_()
+    q.copy_(q_src)   # the kernel right before K1 writes Q (allowed with early_kv)
+    capi.tree_attention(q, kc, vc, mask, Pd, nd, out=out, lse=lse, force_path=path,
+                        k_tree=kt, v_tree=vt, early_kv=early)
     torch.cuda.synchronize()
     check_k1(restatement, bt, out, dtype, lse)
 
