@@ -418,6 +418,9 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
     a.scale = 1.0 / std::sqrt((double)Dh);
     a.workspace = ws;
     a.workspace_bytes = st_tree_attention_workspace_size(&a);
+    // K1's predecessor is the layer's K2 append (tree rows [P, P+n) only): the
+    // committed rows and the lengths are stable, so K1 may stream them early
+    a.early_kv = 1;
     const size_t layer_elems = (size_t)B * H * Lmax * Dh;
     const cudaDataType_t ht = st::cuda_type(m->dtype);
 
