@@ -21,3 +21,6 @@ timeout 120 python tools/c4_slice.py --out $OUT/$TAG.c4.json > $OUT/$TAG.c4.txt 
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/$TAG.c3launches.csv \
     python bench.py --config c3 --steps 1 --warmup 1 > /dev/null 2> $OUT/$TAG.c3ncu.err
 timeout 120 python tools/k1_trace.py $OUT/$TAG.k1trace.raw > $OUT/$TAG.trace.txt 2>&1
+timeout 600 python tools/sweep_gqa.py --out $OUT/$TAG.gqa_sweep.json > $OUT/$TAG.gqa_sweep.txt 2>&1
+timeout 300 python tools/step_breakdown.py > $OUT/$TAG.step_breakdown.txt 2>&1
+timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/$TAG.ref.json 2> $OUT/$TAG.ref.err
