@@ -19,6 +19,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "kv_move.cuh"
 #include "tree_masks.cuh"
 
 namespace st {
@@ -98,39 +99,28 @@ tree_prepare_kernel(const char* __restrict__ k_new, const char* __restrict__ v_n
         build_masks_block(parent, n_nodes, T, W, mask, blockIdx.x - T, blockIdx.y, s_par);
 }
 
-// One block per (layer, b): rows k = 1..n_keep-1 copied sequentially.
+// st_kv_compact: block (b, layer * nhc + hc) moves the accepted rows of its
+// hpb KV heads of one layer (kv_move.cuh: chunked, no per-row barrier chain).
 template <class V>
-__global__ void kv_compact_kernel(const int32_t* __restrict__ ids, int ids_stride,
-                                  const int32_t* __restrict__ n_keep,
-                                  const int32_t* __restrict__ prefix_len,
-                                  int32_t* __restrict__ new_prefix_len, char* k_cache,
-                                  char* v_cache, int Hkv, int64_t row_bytes, int64_t Lmax,
-                                  int64_t layer_stride_bytes) {
+__global__ void __launch_bounds__(256)
+kv_compact_kernel(const int32_t* __restrict__ ids, int ids_stride, const int32_t* __restrict__ n_keep,
+                  const int32_t* __restrict__ prefix_len, int32_t* __restrict__ new_prefix_len,
+                  char* k_cache, char* v_cache, int Hkv, int row_vecs, int64_t Lmax,
+                  int64_t layer_stride_bytes, int nhc, int hpb) {
+    extern __shared__ int s_ids[];  // ids_stride ints
     pdl_wait();
     pdl_trigger();
-    const int b = blockIdx.x, layer = blockIdx.y;
-    const int keep = n_keep[b];
+    const int b = blockIdx.x, layer = blockIdx.y / nhc, hc = blockIdx.y % nhc;
+    const int keep = min(n_keep[b], ids_stride);
     const int64_t P = prefix_len[b];
-    const int32_t* idb = ids + (int64_t)b * ids_stride;
-    char* kl = k_cache + layer * layer_stride_bytes;
-    char* vl = v_cache + layer * layer_stride_bytes;
-    const int64_t nvec = row_bytes / (int64_t)sizeof(V);
-    for (int k = 1; k < keep; ++k) {
-        const int src_row = idb[k];
-        if (src_row != k) {
-            for (int64_t i = threadIdx.x; i < (int64_t)Hkv * nvec; i += blockDim.x) {
-                const int h = (int)(i / nvec);
-                const int64_t e = i % nvec;
-                const int64_t base = ((int64_t)b * Hkv + h) * Lmax;
-                const int64_t s = (base + P + src_row) * row_bytes;
-                const int64_t d = (base + P + k) * row_bytes;
-                reinterpret_cast<V*>(kl + d)[e] = reinterpret_cast<const V*>(kl + s)[e];
-                reinterpret_cast<V*>(vl + d)[e] = reinterpret_cast<const V*>(vl + s)[e];
-            }
-        }
-        __syncthreads();
-    }
-    if (new_prefix_len && layer == 0 && threadIdx.x == 0) new_prefix_len[b] = (int32_t)(P + keep);
+    for (int k = threadIdx.x; k < keep; k += blockDim.x) s_ids[k] = ids[(int64_t)b * ids_stride + k];
+    __syncthreads();
+    if (new_prefix_len && blockIdx.y == 0 && threadIdx.x == 0) new_prefix_len[b] = (int32_t)(P + keep);
+    const int h0 = hc * hpb, nh = min(hpb, Hkv - h0);
+    if (keep <= 1 || nh <= 0) return;
+    move_rows_block<V>(s_ids, keep, 1, b, h0, nh, Hkv, row_vecs, Lmax, P,
+                       k_cache + layer * layer_stride_bytes, v_cache + layer * layer_stride_bytes,
+                       nullptr, nullptr, 0);
 }
 
 }  // namespace
@@ -199,15 +189,21 @@ st_status st_kv_compact(st_dtype dtype, int B, int Hkv, int D, int64_t Lmax, int
     if (B == 0) return ST_OK;
     ST_CHECK_ARG(ids && n_keep && prefix_len && k_cache && v_cache, ST_ERR_INVALID_ARGUMENT,
                  "null pointer");
+    ST_CHECK_ARG(ids_stride <= 16384, ST_ERR_SHAPE_MISMATCH, "ids_stride > 16384");
     const int64_t es = (int64_t)st::dtype_size(dtype);
     const int64_t row_bytes = (int64_t)D * es;
-    const dim3 grid(B, n_layers);
+    const bool vec = row_bytes % 16 == 0;
+    const int row_vecs = (int)(vec ? row_bytes / 16 : row_bytes);
+    // heads per block: about 2 KB of K+V per accepted row per block
+    const int hpb = std::max(1, std::min(Hkv, (vec ? 64 : 1024) / std::max(1, row_vecs)));
+    const int nhc = (Hkv + hpb - 1) / hpb;
+    ST_CHECK_ARG(B <= 2147483647 && (int64_t)n_layers * nhc <= 65535, ST_ERR_SHAPE_MISMATCH,
+                 "too many layers x heads");
     auto s = st::as_stream(stream);
-    ST_CUDA_TRY(st::launch_pdl(row_bytes % 16 == 0 ? st::kv_compact_kernel<int4>
-                                                    : st::kv_compact_kernel<char>,
-                               grid, dim3(256), 0, s, ids, ids_stride, n_keep, prefix_len,
-                               new_prefix_len, (char*)k_cache, (char*)v_cache, Hkv, row_bytes,
-                               Lmax, layer_stride * es));
+    ST_CUDA_TRY(st::launch_pdl(vec ? st::kv_compact_kernel<int4> : st::kv_compact_kernel<char>,
+                               dim3(B, n_layers * nhc), dim3(256), (size_t)ids_stride * sizeof(int), s,
+                               ids, ids_stride, n_keep, prefix_len, new_prefix_len, (char*)k_cache,
+                               (char*)v_cache, Hkv, row_vecs, Lmax, layer_stride * es, nhc, hpb));
     ST_LAUNCH_CHECK();
     return ST_OK;
 }

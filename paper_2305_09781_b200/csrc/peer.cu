@@ -9,7 +9,7 @@ namespace st {
 namespace {
 
 __global__ void peer_signal_kernel(uint32_t* const* signals, int world, int rank, uint32_t epoch) {
-    pdl_wait();  // K1 (and its combine) have completed: their peer stores are performed
+    pdl_wait();  // K1 has completed: its peer stores are performed
     const int k = threadIdx.x;
     if (k < world) {
         __threadfence_system();

@@ -8,12 +8,16 @@
 // attention core :270-299) collapsed into one masked pass.
 //
 // Design:
-//   * Persistent, one CTA per SM, over the pair-major sequence of every (b, h)
-//     pair's 128-row KV tiles. Ranges are either whole pairs (when all pairs
-//     have the same tile count and that balances within kAlignedSlack tiles)
-//     or stream-K (equal tile counts per CTA; a pair cut by a range boundary
-//     leaves partial (O, m, l) pieces that combine_kernel — launched with PDL —
-//     merges in fixed order: deterministic, no atomics in any reduction).
+//   * Persistent, one CTA per SM, over the pair-major sequence of every
+//     (b, KV head) pair's 128-row KV tiles. Ranges are whole pairs, equal
+//     single-segment pieces of every pair (small uniform batches), or
+//     stream-K (equal tile counts per CTA). A pair cut by range boundaries
+//     leaves pieces (O, m, l) that the pair's head owner merges in-kernel, in
+//     CTA order (deterministic, no atomics in any reduction), after staging
+//     them into its drained K ring with TMA.
+//   * GQA: the G query heads of a KV head share one M-row Q tile (row r =
+//     node r/G of head r%G). k_tree mode: the tree rows come from their own
+//     [B][T][Hkv][D] tensors as one extra tile after the prefix tiles.
 //   * Warp roles: SW softmax/epilogue warps (4 for M=64, 8 for M=128), then a
 //     TMA producer for Q and K, a TMA producer for V and the MMA issuer (the
 //     whole warp runs its loop; one elected lane issues inside the asm).

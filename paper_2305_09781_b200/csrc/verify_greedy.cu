@@ -22,6 +22,7 @@
 #include <cfloat>
 
 #include "common.cuh"
+#include "kv_move.cuh"
 #include "tree_masks.cuh"
 
 namespace st {
@@ -345,7 +346,6 @@ greedy_walk_kernel(int T, const int32_t* __restrict__ tokens, const int32_t* __r
 // before any destination is stored (one barrier), and chunks go in increasing
 // k — no sequential per-row chain. Block (b, 0) writes the walk's outputs.
 constexpr int kWcThreads = 256;
-constexpr int kWcVecs = 4;       // 16-byte vectors in flight per thread per chunk
 
 template <class V>
 __global__ void __launch_bounds__(kWcThreads)
@@ -387,45 +387,7 @@ walk_compact_kernel(int T, const int32_t* __restrict__ tokens, const int32_t* __
     char* vl = v_cache + layer * layer_stride_bytes;
     const char* ktl = k_tree ? k_tree + layer * tree_layer_stride_bytes : nullptr;
     const char* vtl = v_tree ? v_tree + layer * tree_layer_stride_bytes : nullptr;
-    const int per_row = nh * row_vecs;                        // vectors of one row, all heads
-    const int rows_chunk = max(1, kWcThreads * kWcVecs / (2 * per_row));
-    for (int k0 = kfirst; k0 < L; k0 += rows_chunk) {
-        const int k1 = min(L, k0 + rows_chunk);
-        const int total = (k1 - k0) * per_row;
-        V kx[kWcVecs], vx[kWcVecs];
-        int64_t dst[kWcVecs];
-#pragma unroll
-        for (int r = 0; r < kWcVecs; ++r) {
-            const int i = threadIdx.x + r * kWcThreads;
-            dst[r] = -1;
-            if (i < total) {
-                const int kk = k0 + i / per_row, rem = i % per_row;
-                const int h = h0 + rem / row_vecs, e = rem % row_vecs;
-                const int src = s_ids[kk];
-                const int64_t base = ((int64_t)b * Hkv + h) * Lmax + P;
-                if (ktl) {
-                    const int64_t so = (((int64_t)b * T + src) * Hkv + h) * row_vecs + e;
-                    dst[r] = (base + kk) * row_vecs + e;
-                    kx[r] = reinterpret_cast<const V*>(ktl)[so];
-                    vx[r] = reinterpret_cast<const V*>(vtl)[so];
-                } else if (src != kk) {
-                    const int64_t so = (base + src) * row_vecs + e;
-                    dst[r] = (base + kk) * row_vecs + e;
-                    kx[r] = reinterpret_cast<const V*>(kl)[so];
-                    vx[r] = reinterpret_cast<const V*>(vl)[so];
-                }
-            }
-        }
-        __syncthreads();  // every source of this chunk read before any store
-#pragma unroll
-        for (int r = 0; r < kWcVecs; ++r) {
-            if (dst[r] >= 0) {
-                reinterpret_cast<V*>(kl)[dst[r]] = kx[r];
-                reinterpret_cast<V*>(vl)[dst[r]] = vx[r];
-            }
-        }
-        __syncthreads();
-    }
+    move_rows_block<V>(s_ids, L, kfirst, b, h0, nh, Hkv, row_vecs, Lmax, P, kl, vl, ktl, vtl, T);
 }
 
 // One thread per (request, node): tree_masks.cuh.
