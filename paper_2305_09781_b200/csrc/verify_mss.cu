@@ -11,13 +11,16 @@
 //             else p = norm(max(p - q_v, 0))        (residual renormalisation)
 //         emit inverse-CDF sample of p with r = U[k++]; stop
 //
-// One 256-thread block per request keeps the working distribution p[V] in
+// One 1024-thread block per request keeps the working distribution p[V] in
 // shared memory. Every vocabulary reduction uses the fixed order of the
-// contract: thread t owns the contiguous chunk [t*CH, (t+1)*CH) and sums it
-// sequentially, warps combine their 32 chunk sums with an xor butterfly and
-// the 8 warp sums are added in order; the exponential is the contract's
-// exp_spec (fma Horner polynomial + exact power-of-two scaling); all fp32
-// operations use explicit _rn intrinsics so nothing is contracted.
+// contract: chunk owner t (threads 0..255) sums the contiguous chunk
+// [t*CH, (t+1)*CH) sequentially, warps 0..7 combine their 32 chunk sums with an
+// xor butterfly and the 8 warp sums are added in order; the exponential is the
+// contract's exp_spec (fma Horner polynomial + exact power-of-two scaling); all
+// fp32 operations use explicit _rn intrinsics so nothing is contracted.
+// Element-wise passes (exp, normalisation, max) use all 1024 threads, and
+// every global read is batched (16-32 independent loads in flight per thread)
+// so a vocabulary pass costs a few memory round trips, not one per element.
 #include <cfloat>
 
 #include "common.cuh"
@@ -25,7 +28,9 @@
 namespace st {
 namespace {
 
-constexpr int NT = 256;
+constexpr int NT = 256;       // reduction lanes of the contract (chunk owners)
+constexpr int NTHR = 1024;    // threads per block
+constexpr int kBatch = 16;    // independent global loads in flight per thread
 
 __device__ __forceinline__ float exp_spec(float x) {
     if (!(x > -104.0f)) return 0.0f;
@@ -45,13 +50,14 @@ __device__ __forceinline__ float exp_spec(float x) {
                      __uint_as_float((uint32_t)27 << 23));
 }
 
-// Combine per-thread chunk partials in the contract order; result broadcast.
+// Combine the chunk owners' partials (threads 0..255; other threads pass
+// anything) in the contract order; result broadcast to all threads.
 __device__ float combine_spec(float part, float* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) part = __fadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
     __syncthreads();
-    if (lane == 0) red[warp] = part;
+    if (lane == 0 && warp < NT / 32) red[warp] = part;
     __syncthreads();
     float tot = red[0];
 #pragma unroll
@@ -59,6 +65,7 @@ __device__ float combine_spec(float part, float* red) {
     return tot;
 }
 
+// max over all threads (exact and order-independent)
 __device__ float block_max(float v, float* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -67,27 +74,52 @@ __device__ float block_max(float v, float* red) {
     if (lane == 0) red[warp] = v;
     __syncthreads();
     float m = red[0];
-#pragma unroll
-    for (int w = 1; w < NT / 32; ++w) m = fmaxf(m, red[w]);
+#pragma unroll 4
+    for (int w = 1; w < NTHR / 32; ++w) m = fmaxf(m, red[w]);
     return m;
 }
 
-__global__ void __launch_bounds__(NT)
+// Chunk owner's sequential sum of f(p[i], g[i]) over [c0, c1), the global row g
+// read kBatch elements at a time (all loads of a batch in flight).
+constexpr int kChunkBatch = 32;
+template <class F>
+__device__ __forceinline__ float chunk_sum_g(const float* p, const float* __restrict__ g, int c0, int c1,
+                                             F f) {
+    float a = 0.0f;
+    for (int i0 = c0; i0 < c1; i0 += kChunkBatch) {
+        float x[kChunkBatch];
+#pragma unroll
+        for (int j = 0; j < kChunkBatch; ++j) x[j] = i0 + j < c1 ? __ldg(g + i0 + j) : 0.0f;
+#pragma unroll
+        for (int j = 0; j < kChunkBatch; ++j)
+            if (i0 + j < c1) a = __fadd_rn(a, f(p[i0 + j], x[j]));
+    }
+    return a;
+}
+
+__global__ void __launch_bounds__(NTHR)
 mss_kernel(const float* __restrict__ logits, const float* __restrict__ q, int T, int V,
            const int32_t* __restrict__ tokens, const int32_t* __restrict__ parent,
            const int32_t* __restrict__ n_nodes, float temperature,
            const float* __restrict__ uniforms, int n_uniforms, int32_t* __restrict__ verified,
            int32_t* __restrict__ ids, int32_t* __restrict__ len) {
-    extern __shared__ float p[];  // [V]
-    __shared__ float red[NT / 32];
+    extern __shared__ float p[];  // [V], then the request's parent / token rows
+    __shared__ float red[NTHR / 32];
     __shared__ float cum[NT], csum[NT];
     __shared__ int sh_pick;
     const int b = blockIdx.x, tid = threadIdx.x;
     const int n = n_nodes[b];
     const int CH = (V + NT - 1) / NT;
-    const int c0 = tid * CH, c1 = min(V, c0 + CH);
-    const int32_t* tok = tokens + (int64_t)b * T;
-    const int32_t* par = parent + (int64_t)b * T;
+    const bool owner = tid < NT;  // chunk owner of the contract's reductions
+    const int c0 = owner ? tid * CH : 0, c1 = owner ? min(V, c0 + CH) : 0;
+    // the tree staged once: the child scan below reads it for every visited
+    // node (from global memory it was one dependent round trip per node id)
+    int32_t* par = reinterpret_cast<int32_t*>(p + V);
+    int32_t* tok = par + T;
+    for (int v = tid; v < n; v += NTHR) {
+        par[v] = parent[(int64_t)b * T + v];
+        tok[v] = tokens[(int64_t)b * T + v];
+    }
     const float* U = uniforms + (int64_t)b * n_uniforms;
     int32_t* vrow = verified + (int64_t)b * (T + 1);
     int32_t* irow = ids + (int64_t)b * (T + 1);
@@ -100,18 +132,29 @@ mss_kernel(const float* __restrict__ logits, const float* __restrict__ q, int T,
         // ---- p = softmax(z[u] / tau) in the contract's arithmetic ----
         const float* z = logits + ((int64_t)b * T + u) * V;
         float mx = -INFINITY;
-        for (int i = tid; i < V; i += NT) {
-            const float zi = z[i];
-            p[i] = zi;
-            mx = fmaxf(mx, zi);
+        for (int i0 = tid; i0 < V; i0 += NTHR * kBatch) {
+            float x[kBatch];
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                const int i = i0 + j * NTHR;
+                x[j] = i < V ? __ldg(z + i) : -INFINITY;
+            }
+#pragma unroll
+            for (int j = 0; j < kBatch; ++j) {
+                const int i = i0 + j * NTHR;
+                if (i < V) {
+                    p[i] = x[j];
+                    mx = fmaxf(mx, x[j]);
+                }
+            }
         }
         mx = block_max(mx, red);
-        for (int i = tid; i < V; i += NT) p[i] = exp_spec(__fmul_rn(__fsub_rn(p[i], mx), inv_tau));
+        for (int i = tid; i < V; i += NTHR) p[i] = exp_spec(__fmul_rn(__fsub_rn(p[i], mx), inv_tau));
         __syncthreads();
         float a = 0.0f;
         for (int i = c0; i < c1; ++i) a = __fadd_rn(a, p[i]);
         const float S = combine_spec(a, red);
-        for (int i = tid; i < V; i += NT) p[i] = __fdiv_rn(p[i], S);
+        for (int i = tid; i < V; i += NTHR) p[i] = __fdiv_rn(p[i], S);
         __syncthreads();
 
         // ---- children of u in ascending id order ----
@@ -125,12 +168,23 @@ mss_kernel(const float* __restrict__ logits, const float* __restrict__ q, int T,
                 next = v;
                 break;
             }
-            float s2 = 0.0f;
-            for (int i = c0; i < c1; ++i) s2 = __fadd_rn(s2, fmaxf(__fsub_rn(p[i], qv[i]), 0.0f));
+            const float s2 = chunk_sum_g(p, qv, c0, c1,
+                                         [](float pi, float qi) { return fmaxf(__fsub_rn(pi, qi), 0.0f); });
             const float S2 = combine_spec(s2, red);
-            if (S2 > 0.0f) {
-                for (int i = c0; i < c1; ++i)
-                    p[i] = __fdiv_rn(fmaxf(__fsub_rn(p[i], qv[i]), 0.0f), S2);
+            if (S2 > 0.0f) {  // element-wise: every thread, q read kBatch at a time
+                for (int i0 = tid; i0 < V; i0 += NTHR * kBatch) {
+                    float x[kBatch];
+#pragma unroll
+                    for (int j = 0; j < kBatch; ++j) {
+                        const int i = i0 + j * NTHR;
+                        x[j] = i < V ? __ldg(qv + i) : 0.0f;
+                    }
+#pragma unroll
+                    for (int j = 0; j < kBatch; ++j) {
+                        const int i = i0 + j * NTHR;
+                        if (i < V) p[i] = __fdiv_rn(fmaxf(__fsub_rn(p[i], x[j]), 0.0f), S2);
+                    }
+                }
             }
             __syncthreads();
         }
@@ -148,7 +202,7 @@ mss_kernel(const float* __restrict__ logits, const float* __restrict__ q, int T,
         const float r = U[k++];
         float c = 0.0f;
         for (int i = c0; i < c1; ++i) c = __fadd_rn(c, p[i]);
-        csum[tid] = c;
+        if (owner) csum[tid] = c;
         __syncthreads();
         if (tid == 0) {
             float run = 0.0f;
@@ -202,15 +256,16 @@ extern "C" st_status st_verify_mss(const float* logits, const float* q, int B, i
     if (B == 0) return ST_OK;
     ST_CHECK_ARG(logits && q && tokens && parent && n_nodes && uniforms && verified && ids && len,
                  ST_ERR_INVALID_ARGUMENT, "null pointer");
-    const size_t smem = (size_t)V * sizeof(float);
-    ST_CHECK_ARG(smem <= 200 * 1024, ST_ERR_UNSUPPORTED, "vocabulary too large for K4 (V <= 51200)");
+    const size_t smem = (size_t)V * sizeof(float) + 2 * (size_t)T * sizeof(int32_t);
+    ST_CHECK_ARG(smem <= 200 * 1024, ST_ERR_UNSUPPORTED,
+                 "vocabulary too large for K4 (V * 4 + T * 8 <= 200 KB)");
     static size_t attr_set = 0;
     if (smem > 48 * 1024 && smem > attr_set) {
         ST_CUDA_TRY(cudaFuncSetAttribute(st::mss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem));
         attr_set = smem;
     }
-    st::mss_kernel<<<B, st::NT, smem, st::as_stream(stream)>>>(logits, q, T, V, tokens, parent,
+    st::mss_kernel<<<B, st::NTHR, smem, st::as_stream(stream)>>>(logits, q, T, V, tokens, parent,
                                                                n_nodes, temperature, uniforms,
                                                                n_uniforms, verified, ids, len);
     ST_LAUNCH_CHECK();
