@@ -254,3 +254,51 @@ def test_tc_split_schedule(capi, restatement, B, H, P, T):
     bt["n"][:] = bt["n"].max()   # uniform tile counts (pad the node counts)
     out, lse = run_k1(capi, bt, torch.float16, force_path=2, lse=True)
     check_k1(restatement, bt, out, torch.float16, lse)
+
+
+def test_tc_fuzz(capi, restatement):
+    """Random configurations through the tcgen05 kernel vs the f64 restatement:
+    GQA group, tree width/depth, ragged prefixes (incl. 0 and tile
+    boundaries), dtype, tree rows in the cache or in their own tensors,
+    early_kv. Every schedule (whole pairs, equal pieces, stream-K) occurs."""
+    rng = np.random.default_rng(2024)
+    dev = "cuda"
+    for case in range(24):
+        G = int(rng.choice([1, 1, 2, 4, 8]))
+        T = int(rng.choice([8, 16, 32, 61, 64, 100, 128]))
+        while G * T > 128:
+            T //= 2
+        Hkv = int(rng.integers(1, 5))
+        B = int(rng.integers(1, 7))
+        dtype = torch.float16 if rng.random() < 0.6 else torch.bfloat16
+        w = int(rng.integers(1, 5))
+        trees = [restatement.merge(width_depth_seqs(rng, int(rng.integers(0, 40)), 40, w,
+                                                    max(1, (T - 1) // w)), 4096) for _ in range(B)]
+        uniform = rng.random() < 0.3
+        lo = int(rng.choice([0, 1, 127, 128, 300]))
+        P_range = (lo, lo) if uniform else (lo, lo + int(rng.integers(0, 700)))
+        bt = make_batch(restatement, rng, B, G * Hkv, Hkv, 128, trees=trees, T=T, P_range=P_range,
+                        dtype=dtype)
+        if uniform:
+            bt["n"][:] = bt["n"].max()
+        own, early = bool(rng.random() < 0.5), bool(rng.random() < 0.5)
+        q = torch.tensor(bt["q"], device=dev).to(dtype)
+        kc = torch.tensor(bt["kc"], device=dev).to(dtype)
+        vc = torch.tensor(bt["vc"], device=dev).to(dtype)
+        kt = vt = None
+        if own:
+            kt = torch.zeros(B, T, Hkv, 128, dtype=dtype, device=dev)
+            vt = torch.zeros_like(kt)
+            for b in range(B):
+                P, n = int(bt["P"][b]), int(bt["n"][b])
+                kt[b, :n] = kc[b, :, P:P + n].transpose(0, 1)
+                vt[b, :n] = vc[b, :, P:P + n].transpose(0, 1)
+                kc[b, :, P:P + n] = 7.0
+                vc[b, :, P:P + n] = -9.0
+        out = torch.zeros_like(q)
+        lse = torch.zeros((B, G * Hkv, T), dtype=torch.float32, device=dev)
+        capi.tree_attention(q, kc, vc, torch.tensor(bt["mask"].view(np.int64), device=dev),
+                            torch.tensor(bt["P"], device=dev), torch.tensor(bt["n"], device=dev),
+                            out=out, lse=lse, force_path=2, k_tree=kt, v_tree=vt, early_kv=early)
+        torch.cuda.synchronize()
+        check_k1(restatement, bt, out, dtype, lse)
