@@ -24,6 +24,7 @@ struct st_model {
     void* buf = nullptr;
     size_t elems = 0;
     cublasHandle_t blas = nullptr;
+    void* blas_ws = nullptr;  // cuBLAS workspace: lets the heuristics pick split-K / stream-K kernels
     // element offsets into buf
     size_t tok, pos, lnf_g, lnf_b, wout;
     struct Layer {
@@ -338,7 +339,10 @@ st_status st_model_create(const st_model_config* cfg, uint64_t seed, st_dtype dt
     else
         st::gen_weights_kernel<__nv_bfloat16><<<blocks, 256>>>((__nv_bfloat16*)m->buf, (int64_t)at,
                                                                seed, 0);
-    if (cudaDeviceSynchronize() != cudaSuccess || cublasCreate(&m->blas) != CUBLAS_STATUS_SUCCESS) {
+    constexpr size_t kBlasWs = 64ull << 20;
+    if (cudaDeviceSynchronize() != cudaSuccess || cublasCreate(&m->blas) != CUBLAS_STATUS_SUCCESS ||
+        cudaMalloc(&m->blas_ws, kBlasWs) != cudaSuccess ||
+        cublasSetWorkspace(m->blas, m->blas_ws, kBlasWs) != CUBLAS_STATUS_SUCCESS) {
         cudaGetLastError();
         cudaFree(m->buf);
         delete m;
@@ -352,6 +356,7 @@ st_status st_model_create(const st_model_config* cfg, uint64_t seed, st_dtype dt
 void st_model_destroy(st_model* m) {
     if (!m) return;
     if (m->blas) cublasDestroy(m->blas);
+    if (m->blas_ws) cudaFree(m->blas_ws);
     if (m->buf) cudaFree(m->buf);
     delete m;
 }
