@@ -11,25 +11,30 @@
 //             else p = norm(max(p - q_v, 0))        (residual renormalisation)
 //         emit inverse-CDF sample of p with r = U[k++]; stop
 //
-// One 1024-thread block per request keeps the working distribution p[V] in
-// shared memory. Every vocabulary reduction uses the fixed order of the
-// contract: chunk owner t (threads 0..255) sums the contiguous chunk
-// [t*CH, (t+1)*CH) sequentially, warps 0..7 combine their 32 chunk sums with an
-// xor butterfly and the 8 warp sums are added in order; the exponential is the
-// contract's exp_spec (fma Horner polynomial + exact power-of-two scaling); all
-// fp32 operations use explicit _rn intrinsics so nothing is contracted.
-// Element-wise passes (exp, normalisation, max) use all 1024 threads, and
-// every global read is batched (16-32 independent loads in flight per thread)
-// so a vocabulary pass costs a few memory round trips, not one per element.
+// One thread-block cluster of 4 CTAs (1024 threads each) per request keeps the
+// working distribution p[V] in the cluster's shared memory, a quarter per CTA.
+// Every vocabulary reduction uses the fixed order of the contract: chunk owner
+// t (of 256) sums the contiguous chunk [t*CH, (t+1)*CH) sequentially, the 8
+// warps of chunk owners combine their 32 chunk sums with an xor butterfly and
+// the 8 warp sums are added in order (exchanged over DSMEM); the exponential is
+// the contract's exp_spec (fma Horner polynomial + exact power-of-two
+// scaling); all fp32 operations use explicit _rn intrinsics so nothing is
+// contracted. Element-wise passes (exp, normalisation, residual) use all 4096
+// threads, every global read is batched, and each rejected child's q row is
+// staged in shared memory once (read by the residual sum and the
+// renormalisation).
 #include <cfloat>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace st {
 namespace {
 
 constexpr int NT = 256;       // reduction lanes of the contract (chunk owners)
-constexpr int NTHR = 1024;    // threads per block
 constexpr int kBatch = 16;    // independent global loads in flight per thread
 
 __device__ __forceinline__ float exp_spec(float x) {
@@ -50,112 +55,133 @@ __device__ __forceinline__ float exp_spec(float x) {
                      __uint_as_float((uint32_t)27 << 23));
 }
 
-// Combine the chunk owners' partials (threads 0..255; other threads pass
-// anything) in the contract order; result broadcast to all threads.
-__device__ float combine_spec(float part, float* red) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) part = __fadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
-    __syncthreads();
-    if (lane == 0 && warp < NT / 32) red[warp] = part;
-    __syncthreads();
-    float tot = red[0];
-#pragma unroll
-    for (int w = 1; w < NT / 32; ++w) tot = __fadd_rn(tot, red[w]);
-    return tot;
-}
+// ------------------------------------------------------------------------
+// Cluster version: one thread-block cluster of CN CTAs per request. CTA k of
+// the cluster owns the contract's chunks [k*OWN, (k+1)*OWN) — vocabulary
+// elements [k*OWN*CH, (k+1)*OWN*CH) — in its shared memory, so every
+// element-wise pass and every global read is spread over CN SMs. The fixed-
+// order reductions are unchanged: chunk owners sum their chunks
+// sequentially, the 8 warp butterflies of the contract are warps 0..1 of
+// each CTA (global warp 2k+w), and the warp sums are broadcast into every
+// CTA's shared memory over DSMEM (double-buffered slots, one cluster barrier
+// per reduction) and added in the contract's order — bit-identical to the
+// single-CTA kernel and to the oracle. Remote p[t] reads (accept test,
+// inverse-CDF scan) go through DSMEM as well.
+constexpr int CN = 4;              // CTAs per request (measured: 2 -> 147 us, 4 -> 132, 8 -> 189 at C3)
+constexpr int NTC = 1024;          // threads per CTA
+constexpr int OWN = NT / CN;       // chunk owners per CTA (2 warps)
+static_assert(OWN % 32 == 0, "chunk owners fill whole warps");
 
-// max over all threads (exact and order-independent)
-__device__ float block_max(float v, float* red) {
+struct MssCluster {
+    float red[NTC / 32];           // CTA-local max
+    float xsum[2][NT / 32];        // contract warp sums, every CTA's copy (double-buffered)
+    float xmax[2][CN];             // per-CTA maxima
+    float csum[NT];                // all chunk sums (inverse CDF; leader)
+    float cum[NT];
+    float pt, qt;                  // p[t], q_v[t] of the current accept test
+    int pick;
+};
+
+__device__ __forceinline__ float cluster_max(float v, MssCluster& sh, int slot, cg::cluster_group& cl) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) sh.red[warp] = v;
     __syncthreads();
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    float m = red[0];
-#pragma unroll 4
-    for (int w = 1; w < NTHR / 32; ++w) m = fmaxf(m, red[w]);
+    if (threadIdx.x < CN) {  // thread j sends this CTA's max to CTA j
+        float m = sh.red[0];
+        for (int w = 1; w < NTC / 32; ++w) m = fmaxf(m, sh.red[w]);
+        MssCluster* dst = cl.map_shared_rank(&sh, threadIdx.x);
+        dst->xmax[slot][cl.block_rank()] = m;
+    }
+    cl.sync();
+    float m = sh.xmax[slot][0];
+#pragma unroll
+    for (int j = 1; j < CN; ++j) m = fmaxf(m, sh.xmax[slot][j]);
     return m;
 }
 
-// Chunk owner's sequential sum of f(p[i], g[i]) over [c0, c1), the global row g
-// read kBatch elements at a time (all loads of a batch in flight).
-constexpr int kChunkBatch = 32;
-template <class F>
-__device__ __forceinline__ float chunk_sum_g(const float* p, const float* __restrict__ g, int c0, int c1,
-                                             F f) {
-    float a = 0.0f;
-    for (int i0 = c0; i0 < c1; i0 += kChunkBatch) {
-        float x[kChunkBatch];
+// the contract's combine: owners' chunk partials, butterfly per (global) warp,
+// the 8 warp sums added in order
+__device__ __forceinline__ float cluster_combine(float part, MssCluster& sh, int slot, cg::cluster_group& cl) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (warp < OWN / 32) {
 #pragma unroll
-        for (int j = 0; j < kChunkBatch; ++j) x[j] = i0 + j < c1 ? __ldg(g + i0 + j) : 0.0f;
-#pragma unroll
-        for (int j = 0; j < kChunkBatch; ++j)
-            if (i0 + j < c1) a = __fadd_rn(a, f(p[i0 + j], x[j]));
+        for (int o = 16; o > 0; o >>= 1) part = __fadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+        if (lane < CN) {  // lane j sends this warp's sum to CTA j
+            MssCluster* dst = cl.map_shared_rank(&sh, lane);
+            dst->xsum[slot][cl.block_rank() * (OWN / 32) + warp] = part;
+        }
     }
-    return a;
+    cl.sync();
+    float tot = sh.xsum[slot][0];
+#pragma unroll
+    for (int w = 1; w < NT / 32; ++w) tot = __fadd_rn(tot, sh.xsum[slot][w]);
+    return tot;
 }
 
-__global__ void __launch_bounds__(NTHR)
-mss_kernel(const float* __restrict__ logits, const float* __restrict__ q, int T, int V,
-           const int32_t* __restrict__ tokens, const int32_t* __restrict__ parent,
-           const int32_t* __restrict__ n_nodes, float temperature,
-           const float* __restrict__ uniforms, int n_uniforms, int32_t* __restrict__ verified,
-           int32_t* __restrict__ ids, int32_t* __restrict__ len) {
-    extern __shared__ float p[];  // [V], then the request's parent / token rows
-    __shared__ float red[NTHR / 32];
-    __shared__ float cum[NT], csum[NT];
-    __shared__ int sh_pick;
-    const int b = blockIdx.x, tid = threadIdx.x;
+__global__ void __cluster_dims__(CN, 1, 1) __launch_bounds__(NTC)
+mss_cluster_kernel(const float* __restrict__ logits, const float* __restrict__ q, int T, int V,
+                   const int32_t* __restrict__ tokens, const int32_t* __restrict__ parent,
+                   const int32_t* __restrict__ n_nodes, float temperature,
+                   const float* __restrict__ uniforms, int n_uniforms, int32_t* __restrict__ verified,
+                   int32_t* __restrict__ ids, int32_t* __restrict__ len) {
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ float p[];  // this CTA's elements [e0, e1), then the tree
+    __shared__ MssCluster sh;
+    const int kr = (int)cl.block_rank();
+    const int b = blockIdx.x / CN, tid = threadIdx.x;
     const int n = n_nodes[b];
     const int CH = (V + NT - 1) / NT;
-    const bool owner = tid < NT;  // chunk owner of the contract's reductions
-    const int c0 = owner ? tid * CH : 0, c1 = owner ? min(V, c0 + CH) : 0;
-    // the tree staged once: the child scan below reads it for every visited
-    // node (from global memory it was one dependent round trip per node id)
-    int32_t* par = reinterpret_cast<int32_t*>(p + V);
+    const int SPAN = OWN * CH;                       // elements per CTA (last may be short)
+    const int e0 = min(V, kr * SPAN), e1 = min(V, e0 + SPAN), ne = e1 - e0;
+    const bool owner = tid < OWN;
+    const int gc = kr * OWN + tid;                   // global chunk of an owner
+    const int c0 = owner ? min(V, gc * CH) - e0 : 0, c1 = owner ? min(V, (gc + 1) * CH) - e0 : 0;
+    float* qs = p + SPAN;  // the current child's q slice, staged once per child
+    int32_t* par = reinterpret_cast<int32_t*>(qs + SPAN);
     int32_t* tok = par + T;
-    for (int v = tid; v < n; v += NTHR) {
+    for (int v = tid; v < n; v += NTC) {
         par[v] = parent[(int64_t)b * T + v];
         tok[v] = tokens[(int64_t)b * T + v];
     }
     const float* U = uniforms + (int64_t)b * n_uniforms;
     int32_t* vrow = verified + (int64_t)b * (T + 1);
     int32_t* irow = ids + (int64_t)b * (T + 1);
+    const bool lead = kr == 0;
     const float inv_tau = __fdiv_rn(1.0f, temperature);
-    int u = 0, k = 0, m = 0;
-    if (tid == 0) irow[0] = 0;
+    int u = 0, k = 0, m = 0, rc = 0;  // rc: reduction counter (slot parity), identical in all CTAs
+    if (lead && tid == 0) irow[0] = 0;
 
     for (;;) {
-        __syncthreads();  // every reader of the previous p is done
+        cl.sync();  // every remote reader of the previous p is done
         // ---- p = softmax(z[u] / tau) in the contract's arithmetic ----
-        const float* z = logits + ((int64_t)b * T + u) * V;
+        const float* z = logits + ((int64_t)b * T + u) * V + e0;
         float mx = -INFINITY;
-        for (int i0 = tid; i0 < V; i0 += NTHR * kBatch) {
+        for (int i0 = tid; i0 < ne; i0 += NTC * kBatch) {
             float x[kBatch];
 #pragma unroll
             for (int j = 0; j < kBatch; ++j) {
-                const int i = i0 + j * NTHR;
-                x[j] = i < V ? __ldg(z + i) : -INFINITY;
+                const int i = i0 + j * NTC;
+                x[j] = i < ne ? __ldg(z + i) : -INFINITY;
             }
 #pragma unroll
             for (int j = 0; j < kBatch; ++j) {
-                const int i = i0 + j * NTHR;
-                if (i < V) {
+                const int i = i0 + j * NTC;
+                if (i < ne) {
                     p[i] = x[j];
                     mx = fmaxf(mx, x[j]);
                 }
             }
         }
-        mx = block_max(mx, red);
-        for (int i = tid; i < V; i += NTHR) p[i] = exp_spec(__fmul_rn(__fsub_rn(p[i], mx), inv_tau));
+        mx = cluster_max(mx, sh, (rc++) & 1, cl);
+        for (int i = tid; i < ne; i += NTC) p[i] = exp_spec(__fmul_rn(__fsub_rn(p[i], mx), inv_tau));
         __syncthreads();
         float a = 0.0f;
         for (int i = c0; i < c1; ++i) a = __fadd_rn(a, p[i]);
-        const float S = combine_spec(a, red);
-        for (int i = tid; i < V; i += NTHR) p[i] = __fdiv_rn(p[i], S);
-        __syncthreads();
+        const float S = cluster_combine(a, sh, (rc++) & 1, cl);
+        for (int i = tid; i < ne; i += NTC) p[i] = __fdiv_rn(p[i], S);
+        cl.sync();  // p final in every CTA before any remote p[t] read
 
         // ---- children of u in ascending id order ----
         int next = -1;
@@ -164,32 +190,41 @@ mss_kernel(const float* __restrict__ logits, const float* __restrict__ q, int T,
             const float r = U[k++];
             const int32_t t = tok[v];
             const float* qv = q + ((int64_t)b * T + v) * V;
-            if (__fmul_rn(r, qv[t]) <= p[t]) {
+            // stage this CTA's slice of q_v (one batch of loads in flight per
+            // thread) while thread 0 fetches p[t] (DSMEM) and q_v[t] for the test
+            const float* qe = qv + e0;
+            for (int i0 = tid; i0 < ne; i0 += NTC * kBatch) {
+                float x[kBatch];
+#pragma unroll
+                for (int j = 0; j < kBatch; ++j) {
+                    const int i = i0 + j * NTC;
+                    x[j] = i < ne ? __ldg(qe + i) : 0.0f;
+                }
+#pragma unroll
+                for (int j = 0; j < kBatch; ++j) {
+                    const int i = i0 + j * NTC;
+                    if (i < ne) qs[i] = x[j];
+                }
+            }
+            if (tid == 0) {
+                const int kt = t / SPAN;
+                sh.pt = cl.map_shared_rank(p, kt)[t - kt * SPAN];
+                sh.qt = __ldg(qv + t);
+            }
+            __syncthreads();
+            if (__fmul_rn(r, sh.qt) <= sh.pt) {
                 next = v;
                 break;
             }
-            const float s2 = chunk_sum_g(p, qv, c0, c1,
-                                         [](float pi, float qi) { return fmaxf(__fsub_rn(pi, qi), 0.0f); });
-            const float S2 = combine_spec(s2, red);
-            if (S2 > 0.0f) {  // element-wise: every thread, q read kBatch at a time
-                for (int i0 = tid; i0 < V; i0 += NTHR * kBatch) {
-                    float x[kBatch];
-#pragma unroll
-                    for (int j = 0; j < kBatch; ++j) {
-                        const int i = i0 + j * NTHR;
-                        x[j] = i < V ? __ldg(qv + i) : 0.0f;
-                    }
-#pragma unroll
-                    for (int j = 0; j < kBatch; ++j) {
-                        const int i = i0 + j * NTHR;
-                        if (i < V) p[i] = __fdiv_rn(fmaxf(__fsub_rn(p[i], x[j]), 0.0f), S2);
-                    }
-                }
-            }
-            __syncthreads();
+            float s2 = 0.0f;
+            for (int i = c0; i < c1; ++i) s2 = __fadd_rn(s2, fmaxf(__fsub_rn(p[i], qs[i]), 0.0f));
+            const float S2 = cluster_combine(s2, sh, (rc++) & 1, cl);
+            if (S2 > 0.0f)
+                for (int i = tid; i < ne; i += NTC) p[i] = __fdiv_rn(fmaxf(__fsub_rn(p[i], qs[i]), 0.0f), S2);
+            cl.sync();  // renormalised p everywhere before the next remote read
         }
         if (next >= 0) {
-            if (tid == 0) {
+            if (lead && tid == 0) {
                 vrow[m] = tok[next];
                 irow[m + 1] = next;
             }
@@ -198,44 +233,44 @@ mss_kernel(const float* __restrict__ logits, const float* __restrict__ q, int T,
             continue;
         }
 
-        // ---- inverse-CDF sample of p ----
+        // ---- inverse-CDF sample of p (the leader scans; p read over DSMEM) ----
         const float r = U[k++];
         float c = 0.0f;
         for (int i = c0; i < c1; ++i) c = __fadd_rn(c, p[i]);
-        if (owner) csum[tid] = c;
-        __syncthreads();
-        if (tid == 0) {
+        if (owner) cl.map_shared_rank(&sh, 0)->csum[gc] = c;
+        cl.sync();
+        if (lead && tid == 0) {
             float run = 0.0f;
             for (int t = 0; t < NT; ++t) {
-                run = __fadd_rn(run, csum[t]);
-                cum[t] = run;
+                run = __fadd_rn(run, sh.csum[t]);
+                sh.cum[t] = run;
             }
-            const float target = __fmul_rn(r, cum[NT - 1]);
+            const float target = __fmul_rn(r, sh.cum[NT - 1]);
             int tc = -1;
             for (int t = 0; t < NT; ++t)
-                if (cum[t] > target) { tc = t; break; }
+                if (sh.cum[t] > target) { tc = t; break; }
             if (tc < 0)
                 for (int t = NT - 1; t >= 0; --t)
-                    if (csum[t] > 0.0f) { tc = t; break; }
+                    if (sh.csum[t] > 0.0f) { tc = t; break; }
             int pick = 0;
             if (tc >= 0) {
-                float acc = tc > 0 ? cum[tc - 1] : 0.0f;
+                const int kt = (tc * CH) / SPAN;
+                const float* pr = cl.map_shared_rank(p, kt) - kt * SPAN;  // global element index
+                float acc = tc > 0 ? sh.cum[tc - 1] : 0.0f;
                 int last_pos = -1;
                 pick = -1;
                 for (int i = tc * CH; i < min(V, (tc + 1) * CH); ++i) {
-                    acc = __fadd_rn(acc, p[i]);
-                    if (p[i] > 0.0f) last_pos = i;
+                    const float pi = pr[i];
+                    acc = __fadd_rn(acc, pi);
+                    if (pi > 0.0f) last_pos = i;
                     if (acc > target) { pick = i; break; }
                 }
                 if (pick < 0) pick = last_pos >= 0 ? last_pos : tc * CH;
             }
-            sh_pick = pick;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            vrow[m] = sh_pick;
+            vrow[m] = pick;
             len[b] = m + 1;
         }
+        cl.sync();  // the leader's remote reads are done before any CTA exits
         break;
     }
 }
@@ -256,18 +291,21 @@ extern "C" st_status st_verify_mss(const float* logits, const float* q, int B, i
     if (B == 0) return ST_OK;
     ST_CHECK_ARG(logits && q && tokens && parent && n_nodes && uniforms && verified && ids && len,
                  ST_ERR_INVALID_ARGUMENT, "null pointer");
-    const size_t smem = (size_t)V * sizeof(float) + 2 * (size_t)T * sizeof(int32_t);
+    // one cluster of CN CTAs per request; each CTA holds its OWN chunks of p
+    const int CH = (V + st::NT - 1) / st::NT;
+    const size_t smem = 2 * (size_t)st::OWN * CH * sizeof(float) + 2 * (size_t)T * sizeof(int32_t);
     ST_CHECK_ARG(smem <= 200 * 1024, ST_ERR_UNSUPPORTED,
-                 "vocabulary too large for K4 (V * 4 + T * 8 <= 200 KB)");
+                 "vocabulary / tree too large for K4 (2 * V/4 * 4 + T * 8 <= 200 KB)");
+    ST_CHECK_ARG((int64_t)B * st::CN <= 2147483647, ST_ERR_SHAPE_MISMATCH, "too many requests");
     static size_t attr_set = 0;
     if (smem > 48 * 1024 && smem > attr_set) {
-        ST_CUDA_TRY(cudaFuncSetAttribute(st::mss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
+        ST_CUDA_TRY(cudaFuncSetAttribute(st::mss_cluster_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = smem;
     }
-    st::mss_kernel<<<B, st::NTHR, smem, st::as_stream(stream)>>>(logits, q, T, V, tokens, parent,
-                                                               n_nodes, temperature, uniforms,
-                                                               n_uniforms, verified, ids, len);
+    st::mss_cluster_kernel<<<B * st::CN, st::NTC, smem, st::as_stream(stream)>>>(
+        logits, q, T, V, tokens, parent, n_nodes, temperature, uniforms, n_uniforms, verified, ids,
+        len);
     ST_LAUNCH_CHECK();
     return ST_OK;
 }
