@@ -131,6 +131,74 @@ void run_p(float* const* bufs, unsigned long long* keys, int B, int T, int V, in
            blocks, us, 4.0 * B * T * V / us / 1e3);
 }
 
+// TMA variant: the block's slice arrives in shared memory through one (or a
+// few) cp.async.bulk copies completing on an mbarrier, then the threads scan it.
+template <int SPLIT, int NT>
+__global__ void __launch_bounds__(NT) argmax_bulk(const float* __restrict__ logits, int T, int V,
+                                                  unsigned long long* keys) {
+    extern __shared__ __align__(128) float sl[];
+    __shared__ __align__(8) unsigned long long bar;
+    __shared__ unsigned long long red[NT / 32];
+    const int part = blockIdx.x, u = blockIdx.y, b = blockIdx.z;
+    const float* row = logits + ((int64_t)b * T + u) * V;
+    const int per = (V + SPLIT - 1) / SPLIT;
+    const int lo = part * per, hi = min(V, lo + per), cnt = hi - lo;
+    const uint32_t bar_a = (uint32_t)__cvta_generic_to_shared(&bar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(bar_a));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t bytes = (uint32_t)cnt * 4;  // multiple of 16 when per % 4 == 0
+        asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(bar_a), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"((uint32_t)__cvta_generic_to_shared(sl)), "l"(row + lo), "r"(bytes), "r"(bar_a)
+                     : "memory");
+    }
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(bar_a) : "memory");
+    float bv = -INFINITY;
+    int bi = threadIdx.x < cnt ? lo + threadIdx.x : -1;
+    for (int i = threadIdx.x; i < cnt; i += NT) {
+        const float x = sl[i];
+        if (x > bv) { bv = x; bi = lo + i; }
+    }
+    unsigned long long best = bi >= 0 ? arg_key(bv, bi) : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) red[warp] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < NT / 32; ++w) best = max(best, red[w]);
+        keys[((int64_t)b * T + u) * SPLIT + part] = best;
+    }
+}
+
+template <int SPLIT, int NT>
+void run_b(float* const* bufs, unsigned long long* keys, int B, int T, int V) {
+    dim3 grid(SPLIT, T, B);
+    const size_t smem = (size_t)((V + SPLIT - 1) / SPLIT) * 4;
+    cudaFuncSetAttribute(argmax_bulk<SPLIT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int i = 0; i < 6; ++i) argmax_bulk<SPLIT, NT><<<grid, NT, smem>>>(bufs[i % 3], T, V, keys);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 60;
+    cudaEventRecord(e0);
+    for (int i = 0; i < iters; ++i) argmax_bulk<SPLIT, NT><<<grid, NT, smem>>>(bufs[i % 3], T, V, keys);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double us = ms * 1e3 / iters;
+    printf("bulk split %d threads %4d: %7.2f us  %6.0f GB/s  (%s)\n", SPLIT, NT, us,
+           4.0 * B * T * V / us / 1e3, cudaGetErrorString(cudaGetLastError()));
+}
+
 template <int SPLIT, int UNROLL, int NT>
 void run(float* const* bufs, unsigned long long* keys, int B, int T, int V) {
     dim3 grid(SPLIT, T, B);
@@ -174,6 +242,11 @@ int main() {
     run_p<4, 8, 256>(bufs, keys, B, T, V, 148 * 4);
     run_p<4, 8, 256>(bufs, keys, B, T, V, 148 * 8);
     run_p<2, 16, 256>(bufs, keys, B, T, V, 148 * 4);
+    run<8, 4, 256>(bufs, keys, B, T, V);
+    run_b<8, 256>(bufs, keys, B, T, V);
+    run_b<4, 256>(bufs, keys, B, T, V);
+    run_b<2, 512>(bufs, keys, B, T, V);
+    run_b<16, 128>(bufs, keys, B, T, V);
     run<8, 4, 256>(bufs, keys, B, T, V);
     return 0;
 }
