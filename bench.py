@@ -64,6 +64,16 @@ def parse():
     return ap.parse_args()
 
 
+def dist_device(local):
+    """GPU and process-group backend of this rank: NCCL, one GPU per rank.
+    BENCH_SHARED_GPU_TEST=1 (code-path test only, numbers meaningless) lets N
+    ranks share the visible GPUs over gloo, so the N>1 path runs on one GPU."""
+    import torch
+    if os.environ.get("BENCH_SHARED_GPU_TEST") == "1":
+        return local % max(1, torch.cuda.device_count()), "gloo"
+    return local, "nccl"
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -239,11 +249,12 @@ def main():
 
     rank, world, local = dist_env()
     assert world == args.gpus or "RANK" not in os.environ, "--gpus must match WORLD_SIZE"
+    local, backend = dist_device(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     numa_cpus = bind_to_gpu_numa(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
 
     # ---- synthetic inputs of the C2 shape (per rank: B requests) ----
     trees = c2_trees(lambda s: TokenTree.merge_sequences(s, 1 << 20), 1000 + rank, V)
@@ -638,10 +649,11 @@ def run_c3(args):
     from paper_2305_09781_b200.tree import TokenTree, TreeBatch
 
     rank, world, local = dist_env()
+    local, backend = dist_device(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
     NL, d, Hh, Vv, BG = 32, 4096, 32, 32000, 32
     lo, hi = shard_range(BG, world, rank)
     Bl = hi - lo
