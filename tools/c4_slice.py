@@ -60,13 +60,26 @@ def main():
         _capi.tree_attention(q, kc, vc, mask, P, n, out=out, workspace=ws)
         _capi.heads_gather_layout(gathered, WORLD, out=full)
     torch.cuda.synchronize()
+    # device time: each timed loop is captured in a CUDA graph (back-to-back
+    # launches from Python would measure the host's per-call overhead here —
+    # the K1 of this slice is ~20 us)
+    def graph_of(fn):
+        g_ = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_):
+            for _ in range(args.iters):
+                fn()
+        return g_
+
+    g_k1 = graph_of(lambda: _capi.tree_attention(q, kc, vc, mask, P, n, out=out, workspace=ws))
+    g_lay = graph_of(lambda: _capi.heads_gather_layout(gathered, WORLD, out=full))
+    for g_ in (g_k1, g_lay):
+        g_.replay()
+    torch.cuda.synchronize()
     e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     e[0].record()
-    for _ in range(args.iters):
-        _capi.tree_attention(q, kc, vc, mask, P, n, out=out, workspace=ws)
+    g_k1.replay()
     e[1].record()
-    for _ in range(args.iters):
-        _capi.heads_gather_layout(gathered, WORLD, out=full)
+    g_lay.replay()
     e[2].record()
     torch.cuda.synchronize()
     k1_us = e[0].elapsed_time(e[1]) * 1e3 / args.iters
@@ -82,10 +95,12 @@ def main():
     for _ in range(3):
         g.attention(q, kc, vc, mask, P, n, workspace=ws)
     torch.cuda.synchronize()
+    g_f = graph_of(lambda: g.attention(q, kc, vc, mask, P, n, workspace=ws))
+    g_f.replay()
+    torch.cuda.synchronize()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record()
-    for _ in range(args.iters):
-        g.attention(q, kc, vc, mask, P, n, workspace=ws)
+    g_f.replay()
     f1.record()
     torch.cuda.synchronize()
     fused_us = f0.elapsed_time(f1) * 1e3 / args.iters
