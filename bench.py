@@ -300,8 +300,8 @@ def main():
     own = args.tree_rows == "own"
 
     def pre(qq, kn, vn, tk, pr, nd):
-        if own:     # ancestor masks
-            _capi.build_masks(pr, nd, out=mask_buf)
+        if own:     # ancestor masks, built while the previous step's commit drains
+            _capi.build_masks(pr, nd, out=mask_buf, early=True)
         else:       # K2 append + masks (one launch)
             _capi.tree_prepare(kn, vn, P, nd, kc, vc, pr, out=mask_buf)
 

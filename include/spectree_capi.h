@@ -278,6 +278,12 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
  * (reference TokenTree::ancestors, token_tree.cpp:130-139, as a bitset). */
 st_status st_build_masks(const int32_t* parent, const int32_t* n_nodes, int B, int T, int W,
                          uint64_t* mask, void* stream);
+/* Same masks, under the caller's promise that the kernel launched right
+ * before it on the stream neither writes parent / n_nodes nor reads or writes
+ * mask (e.g. the previous verification step's commit): the masks are built
+ * while that kernel drains (programmatic dependent launch). */
+st_status st_build_masks_early(const int32_t* parent, const int32_t* n_nodes, int B, int T, int W,
+                               uint64_t* mask, void* stream);
 
 #ifdef __cplusplus
 }

@@ -70,6 +70,7 @@ SIGNATURES = {
     "st_verify_outputs": (_I, [_V, _I, _I, _V, _V, _V, _V, C.c_int32, _V, _V, _V, _V]),
     "st_verify_mss": (_I, [_V, _V, _I, _I, _I, _V, _V, _V, _F, _V, _I, _V, _V, _V, _V]),
     "st_build_masks": (_I, [_V, _V, _I, _I, _I, _V, _V]),
+    "st_build_masks_early": (_I, [_V, _V, _I, _I, _I, _V, _V]),
     "st_model_create": (_I, [_V, C.c_uint64, _I, _V]),
     "st_model_destroy": (None, [_V]),
     "st_model_param_count": (_Z, [_V]),
@@ -317,12 +318,16 @@ def verify_mss(logits, q, tokens, parent, n_nodes, temperature, uniforms, stream
 
 
 # ---------------------------------------------------------------- masks ----
-def build_masks(parent, n_nodes, W=None, stream=None, out=None):
+def build_masks(parent, n_nodes, W=None, stream=None, out=None, early=False):
+    """Ancestor masks [B, T, W] int64. early=True: st_build_masks_early (the
+    previous kernel on the stream neither writes parent/n_nodes nor touches
+    the mask buffer)."""
     B, T = parent.shape
     W = W or (T + 63) // 64
     mask = out if out is not None else torch.empty((B, T, W), dtype=torch.int64,
                                                    device=parent.device)
-    check(lib().st_build_masks(_ptr(parent), _ptr(n_nodes), B, T, W, _ptr(mask), _stream(stream)))
+    fn = lib().st_build_masks_early if early else lib().st_build_masks
+    check(fn(_ptr(parent), _ptr(n_nodes), B, T, W, _ptr(mask), _stream(stream)))
     return mask
 
 

@@ -391,13 +391,17 @@ walk_compact_kernel(int T, const int32_t* __restrict__ tokens, const int32_t* __
 }
 
 // One thread per (request, node): tree_masks.cuh.
+// early: the caller promises the previous kernel on the stream neither writes
+// parent / n_nodes nor touches mask, so the masks are built while it drains and
+// the kernel only waits for it before exiting (keeping completion transitive).
 __global__ void build_masks_kernel(const int32_t* __restrict__ parent,
                                    const int32_t* __restrict__ n_nodes, int T, int W,
-                                   uint64_t* __restrict__ mask) {
+                                   uint64_t* __restrict__ mask, int early) {
     extern __shared__ int s_par[];
-    pdl_wait();
+    if (!early) pdl_wait();
     pdl_trigger();
     build_masks_block(parent, n_nodes, T, W, mask, blockIdx.x, blockIdx.y, s_par);
+    if (early) pdl_wait();
 }
 
 }  // namespace
@@ -515,8 +519,8 @@ st_status st_verify_outputs(const int32_t* outputs, int B, int T, const int32_t*
     return ST_OK;
 }
 
-st_status st_build_masks(const int32_t* parent, const int32_t* n_nodes, int B, int T, int W,
-                         uint64_t* mask, void* stream) {
+static st_status build_masks(const int32_t* parent, const int32_t* n_nodes, int B, int T, int W,
+                             uint64_t* mask, int early, void* stream) {
     if (st_status e = st::require_device()) return e;
     ST_CHECK_ARG(B >= 0 && T >= 1 && W >= (T + 63) / 64 && W <= 32, ST_ERR_SHAPE_MISMATCH,
                  "bad shape (need ceil(T/64) <= W <= 32)");
@@ -525,9 +529,19 @@ st_status st_build_masks(const int32_t* parent, const int32_t* n_nodes, int B, i
     const dim3 grid((T + 127) / 128, B);
     const size_t smem = (size_t)std::min(T, 128 * (int)grid.x) * sizeof(int32_t);
     ST_CUDA_TRY(st::launch_pdl(st::build_masks_kernel, grid, dim3(128), smem, st::as_stream(stream),
-                               parent, n_nodes, T, W, mask));
+                               parent, n_nodes, T, W, mask, early));
     ST_LAUNCH_CHECK();
     return ST_OK;
+}
+
+st_status st_build_masks(const int32_t* parent, const int32_t* n_nodes, int B, int T, int W,
+                         uint64_t* mask, void* stream) {
+    return build_masks(parent, n_nodes, B, T, W, mask, 0, stream);
+}
+
+st_status st_build_masks_early(const int32_t* parent, const int32_t* n_nodes, int B, int T, int W,
+                               uint64_t* mask, void* stream) {
+    return build_masks(parent, n_nodes, B, T, W, mask, 1, stream);
 }
 
 }  // extern "C"

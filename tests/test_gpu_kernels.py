@@ -130,13 +130,15 @@ def test_k1_deterministic_and_non_ancestor_invariant(capi, restatement):
     assert not torch.equal(a[0, 4:6], c[0, 4:6])
 
 
-def test_build_masks_matches_oracle(capi, restatement):
+@pytest.mark.parametrize("early", [False, True])
+def test_build_masks_matches_oracle(capi, restatement, early):
     rng = np.random.default_rng(3)
     trees = [restatement.merge(random_seqs(rng, 1, 20, 12, 20), 4096) for _ in range(4)]
     tok, par, dep, n = pack(trees, 150)
     W = 3
     ref = masks(restatement, par, n, W)
-    got = capi.build_masks(torch.tensor(par, device="cuda"), torch.tensor(n, device="cuda"), W)
+    got = capi.build_masks(torch.tensor(par, device="cuda"), torch.tensor(n, device="cuda"), W,
+                           early=early)
     got = got.cpu().numpy().view(np.uint64)
     for b in range(4):
         np.testing.assert_array_equal(got[b, : n[b]], ref[b, : n[b]])
