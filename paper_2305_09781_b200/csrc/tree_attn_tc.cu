@@ -97,9 +97,10 @@ template <int M> struct Cfg {
     static constexpr uint32_t OFF_V = OFF_K + KSTAGES * TILE_BYTES;
     static constexpr uint32_t OFF_BAR = OFF_V + VSTAGES * TILE_BYTES;
     // A split pair's head owner stages the pair's other pieces into the drained
-    // K ring: the (m, l) block (1 KB), then the piece's M rows of O as four
-    // TMA boxes of [M rows][32 floats] with SWIZZLE_128B (bank-conflict-free
-    // row-per-thread reads).
+    // K ring: the (m, l) block (1 KB), then the piece's O, stored column-block
+    // major — float4 (r, 4j..4j+3) at j*M + r — so the publishing warps' stores
+    // coalesce (a warp writes 512 contiguous bytes per instruction), one bulk
+    // copy stages it, and the row-per-thread reads are bank-conflict-free.
     static constexpr uint32_t PIECE_BOX = M * 128;
     static constexpr uint32_t PIECE_SMEM = 1024 + 4 * PIECE_BOX;
     static constexpr int STAGED_PIECES = (KSTAGES * TILE_BYTES) / PIECE_SMEM;
@@ -324,7 +325,7 @@ __device__ __forceinline__ void store_row(T* dst_row, const float* v, float scal
 template <class T, int M>
 __global__ void __launch_bounds__(Cfg<M>::THREADS, 1)
 tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_part,
+                    const __grid_constant__ CUtensorMap tm_v,
                     const __grid_constant__ CUtensorMap tm_kt, const __grid_constant__ CUtensorMap tm_vt,
                     const TcParams p) {
     using C = Cfg<M>;
@@ -375,7 +376,6 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (warp == SW && lane == 0) {
         prefetch_tmap(&tm_q);
         prefetch_tmap(&tm_k);
-        prefetch_tmap(&tm_part);
         if (p.tree_src) prefetch_tmap(&tm_kt);
     }
     if (warp == SW + 1 && lane == 0) {
@@ -534,9 +534,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             fence_proxy_async_global();
                             uint8_t* dst = sm_k + i * C::PIECE_SMEM;
                             bulk_load(dst, p.partial + (long long)c2 * SLOT_FLOATS + 128 * HD, 1024, merge_full);
-#pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                tma_load_2d(dst + 1024 + j * C::PIECE_BOX, &tm_part, merge_full, 32 * j, c2 * 130);
+                            bulk_load(dst + 1024, p.partial + (long long)c2 * SLOT_FLOATS, 4 * C::PIECE_BOX, merge_full);
                         }
                     }
                     mbar_arrive(merge_full);
@@ -964,10 +962,10 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     if (!valid) continue;
                     const int dc = d0 + ch * 32;
                     if (publish) {  // later piece of a pair: unnormalised O for the head owner
-                        float4* po = reinterpret_cast<float4*>(sp + r * HD + dc);
+                        float4* po = reinterpret_cast<float4*>(sp) + (dc >> 2) * M + r;
 #pragma unroll
                         for (int k = 0; k < 8; ++k)
-                            po[k] = make_float4(ov[4 * k], ov[4 * k + 1], ov[4 * k + 2], ov[4 * k + 3]);
+                            po[k * M] = make_float4(ov[4 * k], ov[4 * k + 1], ov[4 * k + 2], ov[4 * k + 3]);
                         continue;
                     }
                     if (head) {
@@ -981,16 +979,14 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             const float mp = staged ? piece[r] : __ldcg(piece + 128 * HD + r);
                             if (mp == -INFINITY) continue;
                             const float wp = ex2((mp - m_fin) * c);
-                            // staged: box dc/32 of the piece, row r, 16-byte chunk k
-                            // at k ^ (r & 7) (SWIZZLE_128B)
-                            const uint8_t* sbox = reinterpret_cast<const uint8_t*>(piece) + 1024 +
-                                                  (dc >> 5) * C::PIECE_BOX + r * 128;
-                            const float4* pp = reinterpret_cast<const float4*>(piece + r * HD + dc);
+                            // float4 (r, dc + 4k) at (dc/4 + k) * M + r of the piece's O
+                            const float4* pp =
+                                reinterpret_cast<const float4*>(staged ? reinterpret_cast<const uint8_t*>(piece) + 1024
+                                                                       : reinterpret_cast<const uint8_t*>(piece)) +
+                                (dc >> 2) * M + r;
 #pragma unroll
                             for (int k = 0; k < 8; ++k) {
-                                const float4 x = staged
-                                    ? *reinterpret_cast<const float4*>(sbox + ((k ^ (r & 7)) << 4))
-                                    : __ldcg(pp + k);
+                                const float4 x = staged ? pp[k * M] : __ldcg(pp + k * M);
                                 ov[4 * k] = fmaf(x.x, wp, ov[4 * k]);
                                 ov[4 * k + 1] = fmaf(x.y, wp, ov[4 * k + 1]);
                                 ov[4 * k + 2] = fmaf(x.z, wp, ov[4 * k + 2]);
@@ -1112,7 +1108,7 @@ size_t tree_attention_tc_workspace(const st_attn_args* a) {
             attr = true;                                                                        \
         }                                                                                       \
         ST_CUDA_TRY(launch_pdl(tree_attn_tc_kernel<TT, MM>, dim3(G), dim3(Cfg<MM>::THREADS),     \
-                               Cfg<MM>::SMEM_BYTES, stream, tq, tk, tv, tp, tkt, tvt, prm));    \
+                               Cfg<MM>::SMEM_BYTES, stream, tq, tk, tv, tkt, tvt, prm));    \
     } while (0)
 
 st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st_peer_out* po) {
@@ -1160,16 +1156,6 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
     prm.o = a->o;
     prm.lse = a->lse;
     prm.partial = reinterpret_cast<float*>(a->workspace);
-    CUtensorMap tp;  // the piece slots as rows of 128 floats (130 rows per CTA slot)
-    {
-        const uint64_t dims[2] = {(uint64_t)HD, (uint64_t)G * (SLOT_FLOATS / HD)};
-        const uint64_t strides[1] = {HD * 4ull};
-        const uint32_t box[2] = {32, (uint32_t)((int64_t)(a->H / a->Hkv) * a->T <= 64 ? 64 : 128)};
-        if (!encode(&tp, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, prm.partial, dims, strides, box)) {
-            set_error("st_tree_attention: cuTensorMapEncodeTiled(workspace) failed");
-            return ST_ERR_CUDA;
-        }
-    }
     prm.flags = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(a->workspace) +
                                             align_up((size_t)G * SLOT_FLOATS * sizeof(float), 256));
     prm.B = a->B;
