@@ -131,6 +131,7 @@ struct TcParams {
     float scale;
     unsigned long long* trace;  // optional pipeline trace of CTA 0 (ST_K1_TRACE)
     int aligned_slack;          // whole-pair schedule allowed within this many tiles of stream-K
+    int head_extra;             // split schedule: extra tiles for each pair's head piece
     int trace_cta;              // CTA whose per-tile pipeline is traced (ST_K1_TRACE_CTA)
     // head-sharded output (st_tree_attention_allgather): rows go to every rank's
     // [B][T][H_out][D] buffer at head head_offset + h; null -> o with H_out = H
@@ -230,6 +231,8 @@ __device__ Seg find_seg(const TcParams& p, const int* cum, uint32_t t, uint32_t 
 //     CTA pays a second epilogue or a piece publish between two segments,
 //     which is what small batches (C4's 64 pairs x 17 tiles) lose to.
 constexpr int kAlignedSlack = 3;
+// Split schedule: extra tiles given to each pair's head piece (ST_K1_HEADX overrides)
+constexpr int kHeadExtra = 1;
 
 enum : int { kStreamK = 0, kAligned = 1, kSplit = 2 };
 
@@ -240,6 +243,7 @@ struct Sched {
     int mode;       // kStreamK / kAligned / kSplit
     uint32_t S;     // kSplit: pieces per pair
     double inv_g;   // 1 / G, for the exact floor(c * x / G) below
+    uint32_t hx;    // kSplit: extra tiles of a pair's head piece   // 1 / G, for the exact floor(c * x / G) below
 };
 
 // floor(x / G) for x < 2^53 with G <= 256: the double product is within a
@@ -252,7 +256,7 @@ __device__ __forceinline__ uint32_t div_g(uint64_t x, uint32_t G, double inv_g) 
 }
 
 __device__ Sched make_sched(const TcParams& p, const int* cum, uint32_t G) {
-    Sched s{0, 0, 0, kStreamK, 1, 1.0 / (double)G};
+    Sched s{0, 0, 0, kStreamK, 1, 1.0 / (double)G, 0};
     int lo = 1 << 30, hi = 0;
     if (cum) {
         s.total = (uint32_t)p.H * (uint32_t)cum[p.B];
@@ -280,6 +284,7 @@ __device__ Sched make_sched(const TcParams& p, const int* cum, uint32_t G) {
         } else if (split_span <= streamk_span + p.aligned_slack) {
             s.mode = kSplit;
             s.S = S;
+            s.hx = min((uint32_t)p.head_extra, (uint32_t)s.nt - S);
         }
     }
     return s;
@@ -290,7 +295,9 @@ __device__ __forceinline__ uint32_t range_start(uint32_t c, const Sched& s, uint
     if (s.mode == kSplit) {
         if (c >= s.np * s.S) return s.total;
         const uint32_t pr = c / s.S, k = c - pr * s.S;
-        return pr * (uint32_t)s.nt + (k * (uint32_t)s.nt) / s.S;
+        // the head piece gets hx extra tiles: the later pieces (all running
+        // beside it) are published by the time it reaches its merge
+        return pr * (uint32_t)s.nt + (k == 0 ? 0u : s.hx + (k * ((uint32_t)s.nt - s.hx)) / s.S);
     }
     return div_g((uint64_t)c * s.total, G, s.inv_g);
 }
@@ -1176,6 +1183,8 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
     // diagnostic override of the whole-pair schedule threshold (ST_K1_SLACK=-1: always stream-K)
     static const int slack_env = getenv("ST_K1_SLACK") ? atoi(getenv("ST_K1_SLACK")) : (int)kAlignedSlack;
     prm.aligned_slack = slack_env;
+    static const int hx_env = getenv("ST_K1_HEADX") ? atoi(getenv("ST_K1_HEADX")) : (int)kHeadExtra;
+    prm.head_extra = hx_env < 0 ? 0 : hx_env;
     prm.trace_cta = getenv("ST_K1_TRACE_CTA") ? atoi(getenv("ST_K1_TRACE_CTA")) : 0;
     static unsigned long long* trace_buf = nullptr;
     if (getenv("ST_K1_TRACE")) {
