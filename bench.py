@@ -7,13 +7,15 @@ Workload (config C2, BASELINE.json configs[1]): LLaMA-7B-shape attention layer,
 fp16, batch 8 requests per GPU, 64-node token tree each, 2048 committed KV rows,
 H = 32 heads x D = 128, greedy verification over a 32000-token vocabulary.
 
-One step = one pass of the hot path over the batch:
+One step = one pass of the hot path over the batch (class VerifyStep, which
+tests/test_gpu_step.py runs at the same shape against the oracle):
   ancestor bitmasks built on device
   -> K1 tree attention (tcgen05): committed KV from the cache, the tree's own
      K/V rows straight from their [B][T][H][D] tensors   [dominant kernel]
   -> K3 greedy verify (vocab argmax + accepted-path walk)
   -> K2 commit: the accepted path's K/V rows copied into the cache
-  (+ N>1: NCCL all-gather of the accepted tokens — the DP exchange step)
+  (+ N>1: NCCL all-gather of the accepted tokens — the DP exchange step, on a
+     side stream, overlapping the next step)
 
 value  = tree tokens verified per second over all ranks (B*T*N / step time),
          inputs resident in HBM, CUDA-event timed, max over ranks.
@@ -23,12 +25,17 @@ e2e    = same metric through the C-ABI with HOST buffers: every step copies
          full model they come from the on-device LM head).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                  [--config c2|c3|c4|c5] [--kv L] [--tree T]
+
+--gpus N > 1 without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one GPU each, NCCL).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -42,26 +49,65 @@ sys.path.insert(0, ROOT)
 
 # C2
 B, T, H, D, L, V = 8, 64, 32, 128, 2048, 32000
-WIDTH, DEPTH = 8, 8            # 8 root-to-leaf paths, trimmed to exactly 64 nodes
 LAUNCHES_PER_STEP = 4          # masks, K1 (tree rows from k_tree), K3 argmax, K3 walk + K2 commit
+STRONG_B_GLOBAL = 64           # strong-scaling companion: 64 requests split over the ranks
 METRIC = "tree-verify tokens/s"
 UNIT = "tokens/s"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-strong", action="store_true",
+                    help="skip the strong-scaling companion measurement")
     ap.add_argument("--tree-rows", default="own", choices=["own", "cache"],
-                    help="C2: K1 reads the tree rows from their own tensors (no append) or "
+                    help="K1 reads the tree rows from their own tensors (no append) or "
                          "from the cache after a K2 append")
-    ap.add_argument("--config", default="c2", choices=["c2", "c3"],
-                    help="c2 (default, the headline metric) or c3: full 32-layer 7B-shape stack, "
-                         "batch 32 partitioned over the ranks, stochastic verification")
-    return ap.parse_args()
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"],
+                    help="c2 (default, the headline metric); c3: full 32-layer 7B-shape stack, "
+                         "batch 32 partitioned over the ranks, stochastic verification; c4: "
+                         "LLaMA-65B-shape attention layer, heads sharded over the ranks; c5: "
+                         "long-context verify step (B=16 per GPU, --kv, --tree)")
+    ap.add_argument("--kv", type=int, default=32768, help="c5: committed KV rows")
+    ap.add_argument("--tree", type=int, default=128, help="c5: tree nodes")
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "peer"],
+                    help="c4: head-output all-gather through NCCL, or fused into K1's epilogue "
+                         "over peer memory")
+    return ap.parse_args(argv)
+
+
+# ------------------------------------------------------------ launching ----
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(args) -> bool:
+    """--gpus N > 1 outside torchrun: re-launch this command under
+    torch.distributed.run with N ranks. Returns True when it did (the parent
+    then only relays the exit status)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    env = dict(os.environ)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    r = subprocess.run(cmd, env=env)
+    if r.returncode != 0:
+        sys.exit(r.returncode)
+    return True
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
 
 
 def dist_device(local):
@@ -74,11 +120,40 @@ def dist_device(local):
     return local, "nccl"
 
 
-def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+def init_rank(args):
+    """Device + process group for this rank; fails loudly when the launch does
+    not match --gpus (a silent 1-rank run would misreport n_gpus)."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
+    local, backend = dist_device(local)
+    if backend == "nccl" and local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} needs GPU {local}, only "
+                         f"{torch.cuda.device_count()} visible")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        if backend == "nccl":   # communicator-init lines (nranks) on stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
+        t = torch.ones(1, device=dev)
+        dist.all_reduce(t)
+        assert int(t.item()) == world
+        print(f"[bench] rank {rank}/{world}: {backend} communicator up, nranks={world}, "
+              f"device cuda:{local}", file=sys.stderr, flush=True)
+    return rank, world, local, dev
+
+
+def finish_rank(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
 
 
 _ORIG_AFFINITY: set = set()
@@ -108,14 +183,29 @@ def bind_to_gpu_numa(local):
     return None
 
 
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def width_of(nodes):
+    """SURVEY.md §8(d) tree construction: W root-to-leaf paths of depth
+    ceil((T-1)/W): W=4 for T=16, 8 for T=64, 16 for T=128."""
+    return max(1, min(16, nodes // 8))
+
+
 def c2_trees(make_tree, seed, vocab, n_req=B, nodes=T):
     """W paths of depth ceil((T-1)/W) with uniform tokens, trimmed to exactly T nodes."""
     rng = np.random.default_rng(seed)
+    width = width_of(nodes)
+    depth = -(-(nodes - 1) // width)
     trees = []
     for _ in range(n_req):
         root = int(rng.integers(0, vocab))
         while True:
-            seqs = [[root] + rng.integers(0, vocab, DEPTH).tolist() for _ in range(WIDTH)]
+            seqs = [[root] + rng.integers(0, vocab, depth).tolist() for _ in range(width)]
             t = make_tree(seqs)
             # trim trailing tokens of the last paths until exactly `nodes`
             i = len(seqs) - 1
@@ -131,19 +221,155 @@ def c2_trees(make_tree, seed, vocab, n_req=B, nodes=T):
     return trees
 
 
-def cpu_threads():
-    try:
-        return len(os.sched_getaffinity(0))
-    except AttributeError:
-        return os.cpu_count() or 1
+def c4_trees(make_tree, seed, n_req, vocab=V):
+    """C4 trees: 3 SSMs, each expanded <1,1,3,1,1,1,1,1> (top-e_i children per
+    frontier node at depth i), merged: 61 nodes."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n_req):
+        root = int(rng.integers(0, vocab))
+        seqs = []
+        for _ssm in range(3):
+            frontier = [[root]]
+            for e in (1, 1, 3, 1, 1, 1, 1, 1):
+                frontier = [p + [int(t)] for p in frontier for t in rng.integers(0, vocab, e)]
+            seqs.extend(frontier)
+        out.append((make_tree(seqs), seqs))
+    return out
+
+
+# ----------------------------------------------------------- the step ------
+class VerifyStep:
+    """One verification step over a batch, device-resident (C2 / C5 shapes).
+
+    Buffers: KV cache [B][H][L+T][D] (fp16), Q and the tree's own K/V
+    [B][T][H][D], logits [B][T][V] fp32 with planted acceptance (each node's
+    argmax is its first child's token with probability 0.7), tree topology
+    [B][T] int32. `run(a)` launches masks -> K1 -> K3 argmax -> K3 walk + K2
+    commit on the current stream; `a` = (q, k_tree, v_tree, tokens, parents,
+    n_nodes), so the e2e loop can swap in freshly copied inputs."""
+
+    def __init__(self, dev, seed, B=B, T=T, L=L, H=H, D=D, V=V, tree_rows="own",
+                 trees=None, dtype=None):
+        import torch
+
+        from paper_2305_09781_b200 import _capi
+        from paper_2305_09781_b200.tree import TokenTree, TreeBatch
+        self.capi = _capi
+        self.B, self.T, self.L, self.H, self.D, self.V = B, T, L, H, D, V
+        dtype = dtype or torch.float16
+        if trees is None:
+            trees = c2_trees(lambda s: TokenTree.merge_sequences(s, 1 << 20), 1000 + seed, V,
+                             n_req=B, nodes=T)
+        self.trees = trees
+        self.batch = batch = TreeBatch([t for t, _ in trees], T)
+        g = torch.Generator(device=dev).manual_seed(1234 + seed)
+        Lmax = L + T
+        self.kc = (torch.rand(B, H, Lmax, D, device=dev, generator=g) * 2 - 1).to(dtype)
+        self.vc = (torch.rand(B, H, Lmax, D, device=dev, generator=g) * 2 - 1).to(dtype)
+        self.q = (torch.rand(B, T, H, D, device=dev, generator=g) * 2 - 1).to(dtype)
+        self.knew = (torch.rand(B, T, H, D, device=dev, generator=g) * 2 - 1).to(dtype)
+        self.vnew = (torch.rand(B, T, H, D, device=dev, generator=g) * 2 - 1).to(dtype)
+        self.logits = torch.randn(B, T, V, device=dev, generator=g)
+        rng = np.random.default_rng(77 + seed)
+        rows, cols = [], []
+        for b in range(B):
+            for u in range(batch.n_nodes[b]):
+                kids = np.nonzero(batch.parents[b] == u)[0]
+                if kids.size and rng.random() < 0.7:
+                    rows.append(b * T + u)
+                    cols.append(int(batch.tokens[b, kids[0]]))
+        if rows:
+            self.logits.view(B * T, V)[torch.tensor(rows, device=dev),
+                                       torch.tensor(cols, device=dev)] = 50.0
+        self.tok = torch.tensor(batch.tokens, device=dev)
+        self.par = torch.tensor(batch.parents, device=dev)
+        self.nn = torch.tensor(batch.n_nodes, device=dev)
+        self.P = torch.full((B,), L, dtype=torch.int32, device=dev)
+        self.W = (T + 63) // 64
+        self.out = torch.empty_like(self.q)
+        self.mask = torch.zeros((B, T, self.W), dtype=torch.int64, device=dev)
+        self.ws_attn = _capi.tree_attention_workspace(self.q, self.kc, self.vc, self.mask, self.P,
+                                                      self.nn)
+        self.ws_ver = _capi.verify_workspace(B, T, dev)
+        self.path = _capi.tree_attention_path(self.q, self.kc, self.vc, self.mask, self.P, self.nn)
+        self.vout = (torch.zeros((B, T + 1), dtype=torch.int32, device=dev),
+                     torch.zeros((B, T + 1), dtype=torch.int32, device=dev),
+                     torch.zeros(B, dtype=torch.int32, device=dev))
+        # own (default): the tree's K/V rows stay in their own [B][T][H][D]
+        # tensors; K1 reads them there (st_attn_args.k_tree) and the commit
+        # copies only the accepted rows into the cache — no K2 append of all T
+        # rows. cache: K2 append into the cache scratch rows first, then
+        # in-place compaction (the reference's cache discipline).
+        self.own = tree_rows == "own"
+        self.resident = (self.q, self.knew, self.vnew, self.tok, self.par, self.nn)
+
+    def pre(self, a):
+        qq, kn, vn, tk, pr, nd = a
+        if self.own:   # ancestor masks; the previous kernel writes no input of theirs
+            self.capi.build_masks(pr, nd, W=self.W, out=self.mask, early=True)
+        else:          # K2 append + masks (one launch)
+            self.capi.tree_prepare(kn, vn, self.P, nd, self.kc, self.vc, pr, W=self.W,
+                                   out=self.mask)
+
+    def k1(self, a):
+        qq, kn, vn, tk, pr, nd = a
+        # early_kv: the kernel right before K1 (masks / append+masks) writes
+        # neither the prefix lengths nor committed rows [0, P), and the masks
+        # kernel waits for ITS predecessor before it lets K1 start, so K1
+        # streams the committed rows while the masks kernel runs
+        self.capi.tree_attention(qq, self.kc, self.vc, self.mask, self.P, nd, out=self.out,
+                                 workspace=self.ws_attn, k_tree=kn if self.own else None,
+                                 v_tree=vn if self.own else None, early_kv=True)
+
+    def post(self, a):   # K3 argmax, then the walk fused with the K2 commit
+        qq, kn, vn, tk, pr, nd = a
+        self.capi.verify_greedy_compact(self.logits, tk, pr, nd, self.P, self.kc, self.vc,
+                                        workspace=self.ws_ver, want_argmax=False, out=self.vout,
+                                        k_tree=kn if self.own else None,
+                                        v_tree=vn if self.own else None)
+
+    def run(self, a=None):
+        a = a or self.resident
+        self.pre(a)
+        self.k1(a)
+        self.post(a)
+
+    def k1_bytes(self, s=2):
+        """Algorithmic K1 bytes per launch."""
+        B_, T_, H_, D_, L_ = self.B, self.T, self.H, self.D, self.L
+        return (s * (2 * B_ * L_ * H_ * D_ + B_ * T_ * H_ * D_ + 2 * B_ * T_ * H_ * D_
+                     + B_ * T_ * H_ * D_) + 8 * B_ * T_ * self.W)
+
+    def oracle_check(self):
+        """Bench self-check (the oracle as CHECKER): the step's accepted
+        tokens, node ids and lengths vs the CPU restatement's greedy verify
+        (reference argmax_token + verify) on the same logits, bit-exact."""
+        from oracle.oracle import Restatement
+        R = Restatement()
+        lg = self.logits.cpu().numpy()
+        ver, ids, ln = (x.cpu().numpy() for x in self.vout)
+        bad = 0
+        for b in range(self.B):
+            n = int(self.batch.n_nodes[b])
+            _, rv, rids = R.greedy_verify(lg[b, :n], self.batch.tokens[b, :n],
+                                          self.batch.parents[b, :n])
+            if not (ln[b] == len(rv) and np.array_equal(ver[b, :ln[b]], rv)
+                    and np.array_equal(ids[b, :ln[b]], rids)):
+                bad += 1
+        return {"greedy_vs_oracle": "bit-exact" if bad == 0 else f"MISMATCH in {bad} requests",
+                "requests": self.B, "accepted_tokens": int(ln.sum())}
 
 
 # ----------------------------------------------------------- reference arm ---
-def reference_sample(n_threads, steps, warmup, full_tree):
+def reference_sample(n_threads, steps, warmup, full_tree, n_req=None):
     """The reference's own tree_parallel_decode (oracle/_ref, compiled from the
     unmodified reference sources) at the C2 layer shape on host cores.
     Reference recipe at LLaMA-7B attention shape: 1 layer, d=4096, 32 heads,
-    V=258, ffn_mult=1; KV injected, one request per thread."""
+    V=258, ffn_mult=1; KV injected, one request per thread.
+    full_tree: every request decodes its whole 64-node C2 tree; else a 9-node
+    sample (root + one 8-deep path). Warm-up steps always use the 9-node
+    sample (they only warm code and caches)."""
     from oracle.oracle import Reference, available_reference
     if not available_reference():
         return None
@@ -153,45 +379,55 @@ def reference_sample(n_threads, steps, warmup, full_tree):
         def __init__(self, seqs):
             self.size = len(R.merge(seqs, 1 << 20)[0])
 
+    n_req = n_req or n_threads
     trees = c2_trees(lambda s: _T(s), 7, 258, n_req=1)
-    seqs = trees[0][1]
-    if not full_tree:   # bounded sample: root + the first root-to-leaf path (9 nodes)
-        seqs = [seqs[0]]
-    nodes = len(R.merge(seqs, 1 << 20)[0])
+    full = trees[0][1]
+    sample = [full[0]]
     cfg = (1, H, H * D, 258, L + T + 2, 1)
     times = []
     for i in range(warmup + steps):
-        t = R.bench_tree_decode(cfg, 42, n_threads, L + 1, seqs, 1 << 20, n_threads)
+        seqs = full if (full_tree and i >= warmup) else sample
+        t = R.bench_tree_decode(cfg, 42, n_req, L + 1, seqs, 1 << 20, n_threads)
         if i >= warmup:
             times.append(t)
     sec = statistics.median(times)
-    return dict(value=n_threads * nodes / sec, seconds=sec, nodes=nodes, requests=n_threads,
-                kind="reference")
+    seqs = full if full_tree else sample
+    nodes = len(R.merge(seqs, 1 << 20)[0])
+    return dict(value=n_req * nodes / sec, seconds=sec, nodes=nodes, requests=n_req,
+                kind="reference", times=times)
 
 
 def run_reference_arm(args):
+    """The reference's CPU path on the SAME config as our arm (C2: 8 requests
+    x 64-node trees over 2048 committed rows), all host threads (one request
+    per thread — the reference decodes a request single-threaded)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     nt = cpu_threads()
-    res = reference_sample(nt, args.steps, args.warmup, full_tree=False)
-    cfg = {"workload": "C2 reference CPU path: tree_parallel_decode (f64) at the LLaMA-7B "
-                       "attention-layer shape, KV 2048, 1 layer, V=258, ffn_mult=1",
-           "B": B, "T": T, "L": L, "H": H, "D": D}
+    res = reference_sample(min(B, nt), args.steps, args.warmup, full_tree=True, n_req=B)
+    cfg = {"workload": "C2 reference CPU path: tree_parallel_decode (f64) of 8 requests x "
+                       "64-node trees over 2048 committed KV rows, LLaMA-7B attention-layer shape "
+                       "(1 layer, d=4096, H=32; reference recipe V=258, ffn_mult=1)",
+           "B": B, "T": T, "L": L, "H": H, "D": D, "same_config": True}
     if res is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs "
                           "/root/reference at build time)"}))
         return
-    sample = (f"{res['requests']} requests x {res['nodes']}-node sample (root + one 8-deep path "
-              f"of a C2 tree) per step, one request per host thread")
+    small = reference_sample(min(B, nt), 1, 0, full_tree=False, n_req=min(B, nt))
+    sample = (f"{res['requests']} requests x full {res['nodes']}-node C2 tree (KV 2048) per step, "
+              f"one request per host thread ({min(B, nt)} threads)")
     line = {"impl": "reference", "metric": METRIC, "value": res["value"], "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": res["seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
-            "cpu_baseline": {"value": res["value"], "unit": UNIT, "cores": nt,
+            "cpu_baseline": {"value": res["value"], "unit": UNIT, "cores": min(B, nt),
                              "kind": "reference", "sample": sample},
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "sample_9node": {"value": small["value"], "ms_per_step": small["seconds"] * 1e3,
+                             "note": "root + one 8-deep path per request (the round-1 arm)"}
+            if small else None}
     print(json.dumps(line))
 
 
@@ -232,228 +468,354 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-# ------------------------------------------------------------ our arm ------
-def main():
-    args = parse()
-    if args.impl == "reference":
-        return run_reference_arm(args)
-    if args.config == "c3":
-        return run_c3(args)
+def load_peaks():
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return json.load(open(pk)) if os.path.exists(pk) else {}
 
+
+# ------------------------------------------------------- DP step runner ----
+class DPRunner:
+    """Replays a VerifyStep as CUDA graphs and, for N > 1, all-gathers every
+    rank's accepted tokens + lengths (the DP exchange step)
+    on a side stream: step i's exchange overlaps step i+1's compute (the next
+    step of a rank needs only its own requests' results). The step's packed
+    results are double-buffered so the exchange never races the next step."""
+
+    def __init__(self, step, world, dev, k1_events=False):
+        import torch
+        self.torch = torch
+        self.s, self.world = step, world
+        Bs, Ts = step.B, step.T
+        n = Bs * (Ts + 2)
+        self.send = [torch.zeros(n, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.gathered = [torch.zeros(world * n, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.comm = torch.cuda.Stream() if world > 1 else None
+        self.ev_ready = [torch.cuda.Event() for _ in range(2)]
+        self.ev_sent = [torch.cuda.Event() for _ in range(2)]
+        self.i = 0
+        self.graphs = []
+        self.ev_k1 = None
+
+    def _pack(self, slot):
+        ver, _, ln = self.s.vout
+        Bs, Ts = self.s.B, self.s.T
+        self.send[slot][: Bs * (Ts + 1)].copy_(ver.view(-1))
+        self.send[slot][Bs * (Ts + 1):].copy_(ln)
+
+    def capture(self, warmup, timed_k1=False):
+        torch = self.torch
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(max(warmup, 3)):
+                self.s.run()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        for slot in range(2):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.s.run()
+                self._pack(slot)
+            self.graphs.append(g)
+        if timed_k1:  # the same step with timing events bracketing K1 (graph nodes)
+            self.ev_k1 = (torch.cuda.Event(enable_timing=True, external=True),
+                          torch.cuda.Event(enable_timing=True, external=True))
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                a = self.s.resident
+                self.s.pre(a)
+                self.ev_k1[0].record()
+                self.s.k1(a)
+                self.ev_k1[1].record()
+                self.s.post(a)
+            self.g_k1 = g
+
+    def step(self, graph=None):
+        """One step on the current stream (+ the exchange on the side stream)."""
+        torch = self.torch
+        slot = self.i % 2
+        cur = torch.cuda.current_stream()
+        if self.world > 1:
+            cur.wait_event(self.ev_sent[slot])   # step i-2's exchange has read send[slot]
+        (graph or self.graphs[slot]).replay()
+        if graph is not None:
+            self._pack(slot)
+        if self.world > 1:
+            import torch.distributed as dist
+            self.ev_ready[slot].record(cur)
+            with torch.cuda.stream(self.comm):
+                self.comm.wait_event(self.ev_ready[slot])
+                dist.all_gather_into_tensor(self.gathered[slot], self.send[slot])
+                self.ev_sent[slot].record(self.comm)
+        self.i += 1
+
+    def sync(self):
+        torch = self.torch
+        if self.comm is not None:
+            torch.cuda.current_stream().wait_stream(self.comm)
+
+
+def barrier_of(world):
     import torch
     import torch.distributed as dist
-
-    from paper_2305_09781_b200 import _capi
-    from paper_2305_09781_b200.dist import gather_accepted
-    from paper_2305_09781_b200.tree import TokenTree, TreeBatch
-
-    rank, world, local = dist_env()
-    assert world == args.gpus or "RANK" not in os.environ, "--gpus must match WORLD_SIZE"
-    local, backend = dist_device(local)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    numa_cpus = bind_to_gpu_numa(local)
-    if world > 1:
-        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
-
-    # ---- synthetic inputs of the C2 shape (per rank: B requests) ----
-    trees = c2_trees(lambda s: TokenTree.merge_sequences(s, 1 << 20), 1000 + rank, V)
-    batch = TreeBatch([t for t, _ in trees], T)
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    Lmax = L + T
-    kc = (torch.rand(B, H, Lmax, D, device=dev, generator=g) * 2 - 1).half()
-    vc = (torch.rand(B, H, Lmax, D, device=dev, generator=g) * 2 - 1).half()
-    q = (torch.rand(B, T, H, D, device=dev, generator=g) * 2 - 1).half()
-    knew = (torch.rand(B, T, H, D, device=dev, generator=g) * 2 - 1).half()
-    vnew = (torch.rand(B, T, H, D, device=dev, generator=g) * 2 - 1).half()
-    logits = torch.randn(B, T, V, device=dev, generator=g)
-    # planted acceptance: each node's argmax is its first child's token w.p. 0.7
-    rng = np.random.default_rng(77 + rank)
-    for b in range(B):
-        for u in range(batch.n_nodes[b]):
-            kids = np.nonzero(batch.parents[b] == u)[0]
-            if kids.size and rng.random() < 0.7:
-                logits[b, u, int(batch.tokens[b, kids[0]])] = 50.0
-    tok = torch.tensor(batch.tokens, device=dev)
-    par = torch.tensor(batch.parents, device=dev)
-    nn = torch.tensor(batch.n_nodes, device=dev)
-    P = torch.full((B,), L, dtype=torch.int32, device=dev)
-    out = torch.empty_like(q)
-    ws_attn = _capi.tree_attention_workspace(q, kc, vc, torch.zeros(B, T, 1, dtype=torch.int64,
-                                                                    device=dev), P, nn)
-    ws_ver = _capi.verify_workspace(B, T, dev)
-    mask = torch.zeros(B, T, 1, dtype=torch.int64, device=dev)
-    path = _capi.tree_attention_path(q, kc, vc, mask, P, nn)
-    gathered = torch.zeros(world * B * (T + 2), dtype=torch.int32, device=dev)
-    vout = (torch.zeros((B, T + 1), dtype=torch.int32, device=dev),
-            torch.zeros((B, T + 1), dtype=torch.int32, device=dev),
-            torch.zeros(B, dtype=torch.int32, device=dev))
-    mask_buf = torch.empty((B, T, 1), dtype=torch.int64, device=dev)
-
-    k1_events = []
-
-    # --tree-rows own (default): the tree's K/V rows stay in their own
-    # [B][T][H][D] tensors; K1 reads them there (st_attn_args.k_tree) and the
-    # commit copies only the accepted rows into the cache — no K2 append of all
-    # T rows. --tree-rows cache: K2 append into the cache scratch rows first,
-    # then in-place compaction (the reference's cache discipline).
-    own = args.tree_rows == "own"
-
-    def pre(qq, kn, vn, tk, pr, nd):
-        if own:     # ancestor masks, built while the previous step's commit drains
-            _capi.build_masks(pr, nd, out=mask_buf, early=True)
-        else:       # K2 append + masks (one launch)
-            _capi.tree_prepare(kn, vn, P, nd, kc, vc, pr, out=mask_buf)
-
-    def k1(qq, kn, vn, tk, pr, nd):
-        # early_kv: the kernel before K1 (masks / append+masks) writes neither the
-        # lengths nor the committed rows [0, P), so K1 streams them while it drains
-        _capi.tree_attention(qq, kc, vc, mask_buf, P, nd, out=out, workspace=ws_attn,
-                             k_tree=kn if own else None, v_tree=vn if own else None,
-                             early_kv=True)
-
-    def post(qq, kn, vn, tk, pr, nd):  # K3 argmax, then the walk fused with the K2 commit
-        _capi.verify_greedy_compact(logits, tk, pr, nd, P, kc, vc, workspace=ws_ver,
-                                    want_argmax=False, out=vout, k_tree=kn if own else None,
-                                    v_tree=vn if own else None)
-
-    resident = (q, knew, vnew, tok, par, nn)
-
-    def eager(args_):
-        pre(*args_)
-        k1(*args_)
-        post(*args_)
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+    return barrier
 
-    # warm up eagerly (first calls set kernel attributes), then capture CUDA graphs:
-    # the timed loop replays them, so host launch overhead is not part of the step
-    side = torch.cuda.Stream()
-    side.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(side):
-        for _ in range(max(args.warmup, 3)):
-            eager(resident)
-    torch.cuda.current_stream().wait_stream(side)
-    barrier()
-    graphs = {}
-    for name, fn in (("full", lambda *a: eager(a)),):
-        g_ = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_):
-            fn(*resident)
-        graphs[name] = g_
-    # the same step with timing events (external: recorded as graph nodes)
-    # bracketing K1
-    ev_k1 = (torch.cuda.Event(enable_timing=True, external=True),
-             torch.cuda.Event(enable_timing=True, external=True))
-    g_ = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g_):
-        pre(*resident)
-        ev_k1[0].record()
-        k1(*resident)
-        ev_k1[1].record()
-        post(*resident)
-    graphs["timed"] = g_
 
-    def step(time_k1=False):
-        graphs["timed" if time_k1 else "full"].replay()
-        if time_k1:   # read this step's K1 duration before the next replay
-            ev_k1[1].synchronize()
-            k1_events.append(ev_k1[0].elapsed_time(ev_k1[1]))
-        if world > 1:   # DP exchange: every rank sees every request's accepted tokens
-            gather_accepted(vout[0], vout[2], world, out=gathered)
-        return vout[0], vout[2]
+def max_over_ranks(world, dev, *vals):
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return vals
+    tt = torch.tensor(vals, dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return tuple(tt.tolist())
 
-    for _ in range(max(args.warmup, 3)):
-        ver, ln = step()
-    barrier()
-    accepted = int(ln.sum().item())
 
-    clocks = ClockSampler(local)
-    # keep the GPU busy until the sampler reports (nvidia-smi needs ~0.2-0.5 s to start)
-    soak_end = time.time() + 1.0
-    while time.time() < soak_end:
-        for _ in range(50):
-            step()
-        torch.cuda.synchronize()
+def time_steps(runner, steps, barrier):
+    import torch
     barrier()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
-    for _ in range(args.steps):
-        step()
+    for _ in range(steps):
+        runner.step()
+    runner.sync()
     t1.record()
     barrier()
-    # K1 inside the step: the same K steps again, from the graph whose timing
-    # events bracket K1 on the launching stream
-    for _ in range(args.steps):
-        step(time_k1=True)
-    # K1 alone: R back-to-back launches per graph replay, alternating between two
-    # KV/Q copies (2 x 277 MB > L2, so no launch reads what the previous one
-    # left in L2); K replays between CUDA events on the launching stream give
-    # K1's average launch duration without the launch latency the bracketing
-    # event nodes above add (they break the programmatic launch chain).
-    kv2 = (kc.clone(), vc.clone(), q.clone())
-    o2 = torch.empty_like(out)
+    return t0.elapsed_time(t1)
+
+
+def k1_alone_ms(step, steps, barrier):
+    """K1's average launch duration: R back-to-back launches per graph replay,
+    alternating between two KV/Q copies (each larger than L2, so no launch reads
+    what the previous one left in L2); CUDA events around K replays on the
+    launching stream."""
+    import torch
+    capi = step.capi
+    kv2 = (step.kc.clone(), step.vc.clone(), step.q.clone())
+    o2 = torch.empty_like(step.out)
     R_B2B = 8
+    kt = step.knew if step.own else None
+    vt = step.vnew if step.own else None
 
     def k1_b2b():
         for i in range(R_B2B):
-            kk, vv, qq = (kc, vc, q) if i % 2 == 0 else kv2
-            _capi.tree_attention(qq, kk, vv, mask_buf, P, nn, out=out if i % 2 == 0 else o2,
-                                 workspace=ws_attn)
+            kk, vv, qq = (step.kc, step.vc, step.q) if i % 2 == 0 else kv2
+            capi.tree_attention(qq, kk, vv, step.mask, step.P, step.nn,
+                                out=step.out if i % 2 == 0 else o2, workspace=step.ws_attn,
+                                k_tree=kt, v_tree=vt)
     k1_b2b()
     g_ = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g_):
         k1_b2b()
-    graphs["k1"] = g_
     for _ in range(3):
         g_.replay()
     barrier()
     b0 = torch.cuda.Event(enable_timing=True)
     b1 = torch.cuda.Event(enable_timing=True)
     b0.record()
-    for _ in range(args.steps):
+    for _ in range(steps):
         g_.replay()
     b1.record()
+    barrier()
+    ms = b0.elapsed_time(b1) / (steps * R_B2B)
+    del kv2, o2, g_
+    return ms
+
+
+# ------------------------------------------------------------ our arm ------
+def main():
+    args = parse()
+    if maybe_spawn(args):
+        return
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    if args.config == "c3":
+        return run_c3(args)
+    if args.config == "c4":
+        return run_c4(args)
+    return run_verify(args)
+
+
+def run_verify(args):
+    """C2 (default) and C5: the verification step, requests partitioned over
+    the ranks (weak scaling: B per GPU fixed)."""
+    import torch
+
+    rank, world, local, dev = init_rank(args)
+    numa_cpus = bind_to_gpu_numa(local)
+    c5 = args.config == "c5"
+    Bq, Tq, Lq = (16, args.tree, args.kv) if c5 else (B, T, L)
+    step = VerifyStep(dev, rank, B=Bq, T=Tq, L=Lq, tree_rows=args.tree_rows)
+    barrier = barrier_of(world)
+    runner = DPRunner(step, world, dev)
+    runner.capture(args.warmup, timed_k1=True)
+    for _ in range(max(args.warmup, 3)):
+        runner.step()
+    runner.sync()
+    barrier()
+
+    clocks = ClockSampler(local)
+    # keep the GPU busy until the sampler reports (nvidia-smi needs ~0.2-0.5 s to start)
+    soak_end = time.time() + 1.0
+    while time.time() < soak_end:
+        for _ in range(50):
+            runner.step()
+        runner.sync()
+        torch.cuda.synchronize()
+    ms = time_steps(runner, args.steps, barrier)
+    # K1 inside the step: the same K steps again from the graph whose timing
+    # events bracket K1 on the launching stream
+    k1_events = []
+    for _ in range(args.steps):
+        runner.step(graph=runner.g_k1)
+        runner.ev_k1[1].synchronize()
+        k1_events.append(runner.ev_k1[0].elapsed_time(runner.ev_k1[1]))
+    runner.sync()
+    k1_b2b_ms = k1_alone_ms(step, args.steps, barrier)
     for _ in range(200):        # keep sampling a little past the timed region
-        step()
+        runner.step()
+    runner.sync()
     barrier()
     clk = clocks.stop()
-    k1_b2b_ms = b0.elapsed_time(b1) / (args.steps * R_B2B)
-    del kv2, o2
-    ms = t0.elapsed_time(t1)
     k1_ms = statistics.mean(k1_events)
-    if world > 1:
-        tt = torch.tensor([ms, k1_ms, k1_b2b_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms, k1_ms, k1_b2b_ms = tt.tolist()
+    ms, k1_ms, k1_b2b_ms = max_over_ranks(world, dev, ms, k1_ms, k1_b2b_ms)
     ms_step = ms / args.steps
-    value = B * T * world / (ms_step / 1e3)
+    value = Bq * Tq * world / (ms_step / 1e3)
+    # this step's results vs the oracle (greedy verify, bit-exact) — rank 0 checks
+    # its own requests after the timed region
+    parity = step.oracle_check() if rank == 0 else None
+
+    # ---- strong-scaling companion: STRONG_B_GLOBAL requests split over the ranks ----
+    strong = None
+    if not c5 and not args.no_strong and STRONG_B_GLOBAL % world == 0:
+        del runner
+        sb = STRONG_B_GLOBAL // world
+        st2 = VerifyStep(dev, 100 + rank, B=sb, T=Tq, L=Lq, tree_rows=args.tree_rows)
+        r2 = DPRunner(st2, world, dev)
+        r2.capture(args.warmup)
+        for _ in range(max(args.warmup, 3)):
+            r2.step()
+        r2.sync()
+        (ms2,) = max_over_ranks(world, dev, time_steps(r2, args.steps, barrier))
+        strong = {"B_global": STRONG_B_GLOBAL, "B_per_gpu": sb, "scaling": "strong",
+                  "value": STRONG_B_GLOBAL * Tq / (ms2 / args.steps / 1e3), "unit": UNIT,
+                  "ms_per_step": ms2 / args.steps}
+        del r2, st2
+        torch.cuda.empty_cache()
+        runner = DPRunner(step, world, dev)
+        runner.capture(0)
 
     # ---- e2e: C-ABI calls with HOST buffers, copies inside the timed region ----
-    # Per step: the host merges every request's candidate sequences into its
-    # token tree (st_tree_merge_batch on the host thread pool, packed straight
-    # into pinned memory), H2D of Q, the tree's K/V and the tree topology, the
-    # step, D2H of the accepted tokens + lengths, which the host reads.
-    # Serving-style pipelining: step i+1's merge + H2D run while step i
-    # computes (two host and two device input sets).
+    e2e = run_e2e(args, step, runner, world, dev, barrier, numa_cpus)
+
+    # ---- roofline of the dominant kernel (K1) ----
+    bytes_k1 = step.k1_bytes()
+    achieved = bytes_k1 / (k1_b2b_ms / 1e3) / 1e9
+    peak = load_peaks().get("hbm_gbs", 6553.6)
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(tf) and not c5:
+        traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+
+    if rank != 0:
+        finish_rank(world)
+        return
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline and not c5:
+        if _ORIG_AFFINITY:   # the CPU baseline gets every host core again
+            os.sched_setaffinity(0, _ORIG_AFFINITY)
+        nt = cpu_threads()
+        try:
+            res = reference_sample(min(B, nt), 1, 0, full_tree=True, n_req=B)
+        except Exception as e:  # noqa: BLE001
+            res = None
+            print(f"cpu baseline failed: {e}", file=sys.stderr)
+        if res is not None:
+            cpu = {"value": res["value"], "unit": UNIT, "cores": min(B, nt), "kind": "reference",
+                   "sample": f"{res['requests']} C2 requests (full {res['nodes']}-node tree, KV "
+                             f"2048) through the reference tree_parallel_decode, f64, 1 layer "
+                             f"d=4096 H=32 V=258 ffn_mult=1, one request per thread; "
+                             f"{res['seconds']:.1f} s"}
+
+    if c5:
+        workload = (f"C5: LLaMA-7B-shape attention layer, fp16, batch 16/GPU, {Tq}-node tree, "
+                    f"KV {Lq}, greedy verify (V=32000)")
+    else:
+        workload = ("C2: LLaMA-7B-shape attention layer, fp16, batch 8/GPU, 64-node tree, "
+                    "KV 2048, greedy verify (V=32000)")
+    kvmb = 2 * Bq * H * (Lq + Tq) * D * 2 / 1e6
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+        "config": {"workload": workload, "B_per_gpu": Bq, "T": Tq, "L": Lq, "H": H, "D": D, "V": V,
+                   "parallelism": f"dp{world} (requests partitioned)",
+                   "l2": f"inputs larger than L2: {kvmb:.0f} MB KV + {Bq * Tq * V * 4 / 1e6:.1f} MB "
+                         f"logits per step",
+                   "timing": "value: K replays of one CUDA graph holding the whole step (N>1: "
+                             "+ the accepted-token all-gather on a side stream, overlapping the "
+                             "next step); roofline: K replays of a graph of 8 back-to-back K1 "
+                             "launches alternating between two KV/Q copies (> L2), CUDA events "
+                             "around the replays; in-step bracket (event graph nodes around K1 "
+                             "inside the step) reported beside it",
+                   "k1_path": "tcgen05" if step.path == 2 else "cuda-core",
+                   "tree_rows": args.tree_rows},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "K1 tree attention", "bytes_per_launch": bytes_k1,
+                     "us_per_launch": k1_b2b_ms * 1e3,
+                     "us_in_step_bracket": k1_ms * 1e3,
+                     "share_of_step": k1_b2b_ms / ms_step,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+        "clocks": clk,
+        "parity": parity,
+        "strong": strong,
+        "verify_steps_per_s": 1e3 / ms_step,
+        "node_evals_per_s": value,
+        "verified_tokens_per_step": parity["accepted_tokens"] if parity else None,
+    }
+    if parity:
+        line["verified_tokens_per_s"] = parity["accepted_tokens"] * world / (ms_step / 1e3)
+    print(json.dumps(line), flush=True)
+    finish_rank(world)
+    if parity and parity["greedy_vs_oracle"] != "bit-exact":
+        sys.exit(3)
+
+
+def run_e2e(args, step, runner, world, dev, barrier, numa_cpus):
+    """Per step: the host merges every request's candidate sequences into its
+    tree (st_tree_merge_batch, thread pool, packed into pinned memory), H2D of
+    Q, the tree's K/V and the topology, the step, D2H of the accepted tokens +
+    lengths, which the host reads. Serving-style pipelining: step i+1's merge +
+    H2D run while step i computes (two host and two device input sets)."""
+    import torch
+
     from paper_2305_09781_b200.tree import MergeInputs, merge_batch
-    merge_in = MergeInputs([sq for _, sq in trees])
-    h_q = q.cpu().pin_memory()
-    h_k = knew.cpu().pin_memory()
-    h_v = vnew.cpu().pin_memory()
-    h_topos = [torch.empty(2 * B * T + B, dtype=torch.int32).pin_memory() for _ in range(2)]
+    Bq, Tq = step.B, step.T
+    merge_in = MergeInputs([sq for _, sq in step.trees])
+    h_q = step.q.cpu().pin_memory()
+    h_k = step.knew.cpu().pin_memory()
+    h_v = step.vnew.cpu().pin_memory()
+    h_topos = [torch.empty(2 * Bq * Tq + Bq, dtype=torch.int32).pin_memory() for _ in range(2)]
 
     def host_merge(h):
-        merge_batch(merge_in, T, max_nodes=T, out=(h[: B * T].view(B, T), h[B * T: 2 * B * T].view(B, T),
-                                                   None, h[2 * B * T:]))
+        merge_batch(merge_in, Tq, max_nodes=Tq,
+                    out=(h[: Bq * Tq].view(Bq, Tq), h[Bq * Tq: 2 * Bq * Tq].view(Bq, Tq), None,
+                         h[2 * Bq * Tq:]))
     for h in h_topos:
         host_merge(h)
-        assert np.array_equal(h[: B * T].numpy().reshape(B, T), batch.tokens)
-        assert np.array_equal(h[2 * B * T:].numpy(), batch.n_nodes)
+        assert np.array_equal(h[: Bq * Tq].numpy().reshape(Bq, Tq), step.batch.tokens)
+        assert np.array_equal(h[2 * Bq * Tq:].numpy(), step.batch.n_nodes)
     t_m = time.perf_counter()
     for _ in range(50):
         host_merge(h_topos[1])
@@ -463,10 +825,10 @@ def main():
     sets = []
     for _ in range(2):
         topo = torch.empty_like(h_topo, device=dev)
-        sets.append((torch.empty_like(q), torch.empty_like(knew), torch.empty_like(vnew),
-                     topo[: B * T].view(B, T), topo[B * T: 2 * B * T].view(B, T),
-                     topo[2 * B * T:], topo))
-    h_outs = [torch.empty(B * (T + 1) + B, dtype=torch.int32).pin_memory() for _ in range(2)]
+        sets.append((torch.empty_like(step.q), torch.empty_like(step.knew),
+                     torch.empty_like(step.vnew), topo[: Bq * Tq].view(Bq, Tq),
+                     topo[Bq * Tq: 2 * Bq * Tq].view(Bq, Tq), topo[2 * Bq * Tq:], topo))
+    h_outs = [torch.empty(Bq * (Tq + 1) + Bq, dtype=torch.int32).pin_memory() for _ in range(2)]
     d2h = h_outs[0].numel() * 4
     copy_stream = torch.cuda.Stream()
     ev_copied = [torch.cuda.Event() for _ in range(2)]
@@ -479,7 +841,8 @@ def main():
     for st in sets:
         g_ = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_):
-            eager(st[:6])
+            step.run(st[:6])
+            runner._pack(0)
         e2e_graphs.append(g_)
     cur = torch.cuda.current_stream()
 
@@ -498,19 +861,19 @@ def main():
             ev_copied[i % 2].record(copy_stream)
 
     def issue_compute(i):
-        st = sets[i % 2]
         cur.wait_event(ev_copied[i % 2])
         e2e_graphs[i % 2].replay()
         ev_free[i % 2].record(cur)
-        if world > 1:
-            gather_accepted(vout[0], vout[2], world, out=gathered)
-        h_outs[i % 2][: B * (T + 1)].copy_(vout[0].flatten(), non_blocking=True)
-        h_outs[i % 2][B * (T + 1):].copy_(vout[2], non_blocking=True)
+        if world > 1:   # DP exchange, synchronous here: the host reads the gathered result
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(runner.gathered[0], runner.send[0])
+        h_outs[i % 2].copy_(runner.gathered[0][: h_outs[0].numel()] if world > 1
+                            else runner.send[0][: h_outs[0].numel()], non_blocking=True)
         ev_out[i % 2].record(cur)
 
     def read_result(i):
         ev_out[i % 2].synchronize()
-        return int(h_outs[i % 2][B * (T + 1):].sum())   # host consumes the accepted lengths
+        return int(h_outs[i % 2][Bq * (Tq + 1):].sum())   # host consumes the accepted lengths
 
     def e2e_run(n):
         got = 0
@@ -542,93 +905,115 @@ def main():
         e2e_run(args.steps)
         barrier()
         windows.append((time.perf_counter() - w0) * 1e3)
-    e2e_ms = statistics.median(windows)
-    if world > 1:
-        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = tt.item()
-    e2e_value = B * T * world / (e2e_ms / args.steps / 1e3)
+    (e2e_ms,) = max_over_ranks(world, dev, statistics.median(windows))
+    return {"value": Bq * Tq * world / (e2e_ms / args.steps / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": e2e_ms / args.steps,
+            "windows_ms_per_step": [w / args.steps for w in windows],
+            "h2d_gbs_copies_alone": h2d_gbs,
+            "h2d_gbs_implied": h2d / (e2e_ms / args.steps / 1e3) / 1e9,
+            "host_numa_cpus": numa_cpus,
+            "host_tree_merge_us_per_step": merge_us,
+            "note": "per step: host merge_sequences of all B trees on the thread pool into "
+                    "pinned memory + H2D, pipelined against the previous step's compute; "
+                    "bound by PCIe H2D"}
 
-    # ---- roofline of the dominant kernel (K1) ----
-    s = 2
-    bytes_k1 = s * (2 * B * L * H * D + B * T * H * D + 2 * B * T * H * D + B * T * H * D) + 8 * B * T
-    achieved = bytes_k1 / (k1_b2b_ms / 1e3) / 1e9
-    peaks = {}
-    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(pk):
-        peaks = json.load(open(pk))
-    peak = peaks.get("hbm_gbs", 6650.0)
-    traffic = None
-    tf = os.path.join(ROOT, "profiles", "k1_traffic.json")
-    if os.path.exists(tf):
-        traffic = json.load(open(tf)).get("dram_bytes_per_launch")
 
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
+# ------------------------------------------------------------------ C4 -----
+def run_c4(args):
+    """C4 (BASELINE.json configs[3]): LLaMA-65B-shape attention layer (64 heads x
+    128, fp16), 8 requests with merged trees of 3 SSMs expanded
+    <1,1,3,1,1,1,1,1> (61 nodes), KV 2048, heads sharded over the ranks
+    (64/N per rank). One step = masks -> K1 over this rank's heads -> the
+    head-output all-gather to [B][T][64][128] on every rank (NCCL
+    all_gather_into_tensor + layout kernel, or --gather peer: fused into K1's
+    epilogue over peer memory) -> greedy verify (V=32000, replicated). Strong
+    scaling: the layer's work is fixed, N splits its heads."""
+    import torch
 
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        if _ORIG_AFFINITY:   # the CPU baseline gets every host core again
-            os.sched_setaffinity(0, _ORIG_AFFINITY)
-        nt = cpu_threads()
-        try:
-            res = reference_sample(min(B, nt), 1, 0, full_tree=True)
-        except Exception as e:  # noqa: BLE001
-            res = None
-            print(f"cpu baseline failed: {e}", file=sys.stderr)
-        if res is not None:
-            cpu = {"value": res["value"], "unit": UNIT, "cores": min(B, nt), "kind": "reference",
-                   "sample": f"{res['requests']} C2 requests (full {res['nodes']}-node tree, KV "
-                             f"2048) through the reference tree_parallel_decode, f64, 1 layer "
-                             f"d=4096 H=32 V=258 ffn_mult=1, one request per thread; "
-                             f"{res['seconds']:.1f} s"}
+    from paper_2305_09781_b200 import _capi
+    from paper_2305_09781_b200.dist import PeerHeadGather, gather_head_outputs, head_shard
+    from paper_2305_09781_b200.tree import TokenTree, TreeBatch
 
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
-        "config": {"workload": "C2: LLaMA-7B-shape attention layer, fp16, batch 8/GPU, 64-node "
-                               "tree, KV 2048, greedy verify (V=32000)",
-                   "B_per_gpu": B, "T": T, "L": L, "H": H, "D": D, "V": V,
-                   "parallelism": f"dp{world} (requests partitioned)",
-                   "l2": "inputs larger than L2: 268 MB KV + 65.5 MB logits per step",
-                   "timing": "value: K replays of one CUDA graph holding the whole step; "
-                             "roofline: K replays of a graph of 8 back-to-back K1 launches "
-                             "alternating between two KV/Q copies (2 x 277 MB > L2), CUDA "
-                             "events around the replays; in-step bracket (event graph nodes "
-                             "around K1 inside the step) reported beside it",
-                   "k1_path": "tcgen05" if path == 2 else "cuda-core",
-                   "tree_rows": args.tree_rows},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "K1 tree attention", "bytes_per_launch": bytes_k1,
-                     "us_per_launch": k1_b2b_ms * 1e3,
-                     "us_in_step_bracket": k1_ms * 1e3,
-                     "share_of_step": k1_b2b_ms / ms_step,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
-        "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
-                "windows_ms_per_step": [w / args.steps for w in windows],
-                "h2d_gbs_copies_alone": h2d_gbs,
-                "h2d_gbs_implied": h2d / (e2e_ms / args.steps / 1e3) / 1e9,
-                "host_numa_cpus": numa_cpus,
-                "host_tree_merge_us_per_step": merge_us,
-                "note": "per step: host merge_sequences of all B trees on the thread pool into "
-                        "pinned memory + H2D, pipelined against the previous step's compute; "
-                        "bound by PCIe H2D"},
-        "gpu_launches": LAUNCHES_PER_STEP * args.steps,
-        "clocks": clk,
-        "verify_steps_per_s": 1e3 / ms_step,
-        "node_evals_per_s": value,
-        "verified_tokens_per_step": accepted,
-        "verified_tokens_per_s": accepted * world / (ms_step / 1e3),
-    }
-    print(json.dumps(line))
-    if world > 1:
-        dist.destroy_process_group()
+    rank, world, local, dev = init_rank(args)
+    HT, Bq = 64, 8
+    h0, h1 = head_shard(HT, world, rank)
+    Hl = h1 - h0
+    trees = c4_trees(lambda s: TokenTree.merge_sequences(s, 1 << 20), 65, Bq)
+    tb = TreeBatch([t for t, _ in trees])
+    Tq = tb.T
+    g = torch.Generator(device=dev).manual_seed(99 + rank)
+    q = (torch.rand(Bq, Tq, Hl, D, device=dev, generator=g) * 2 - 1).half()
+    kc = (torch.rand(Bq, Hl, L + Tq, D, device=dev, generator=g) * 2 - 1).half()
+    vc = (torch.rand(Bq, Hl, L + Tq, D, device=dev, generator=g) * 2 - 1).half()
+    kt = (torch.rand(Bq, Tq, Hl, D, device=dev, generator=g) * 2 - 1).half()
+    vt = (torch.rand(Bq, Tq, Hl, D, device=dev, generator=g) * 2 - 1).half()
+    g2 = torch.Generator(device=dev).manual_seed(5)   # same logits on every rank
+    logits = torch.randn(Bq, Tq, V, device=dev, generator=g2)
+    par = torch.tensor(tb.parents, device=dev)
+    tok = torch.tensor(tb.tokens, device=dev)
+    nn = torch.tensor(tb.n_nodes, device=dev)
+    P = torch.full((Bq,), L, dtype=torch.int32, device=dev)
+    mask = _capi.build_masks(par, nn)
+    out = torch.empty_like(q)
+    ws = _capi.tree_attention_workspace(q, kc, vc, mask, P, nn)
+    wsv = _capi.verify_workspace(Bq, Tq, dev)
+    gathered = torch.empty((world, Bq, Tq, Hl, D), dtype=torch.float16, device=dev)
+    full = torch.empty((Bq, Tq, HT, D), dtype=torch.float16, device=dev)
+    vout = (torch.zeros((Bq, Tq + 1), dtype=torch.int32, device=dev),
+            torch.zeros((Bq, Tq + 1), dtype=torch.int32, device=dev),
+            torch.zeros(Bq, dtype=torch.int32, device=dev))
+    peer = None
+    if args.gather == "peer" and world > 1:
+        peer = PeerHeadGather(Bq, Tq, Hl, D, torch.float16, dev, world, rank)
+    barrier = barrier_of(world)
+
+    def step():
+        _capi.build_masks(par, nn, out=mask)
+        if peer is not None:
+            peer.attention(q, kc, vc, mask, P, nn, workspace=ws)
+            o = peer.wait()
+        else:
+            _capi.tree_attention(q, kc, vc, mask, P, nn, out=out, workspace=ws, k_tree=kt,
+                                 v_tree=vt)
+            o = gather_head_outputs(out, world, gathered=gathered, out=full)
+        _capi.verify_greedy(logits, tok, par, nn, workspace=wsv, want_argmax=False, out=vout)
+        return o
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    clocks = ClockSampler(local)
+    time.sleep(0.5)
+    barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        step()
+    t1.record()
+    barrier()
+    clk = clocks.stop()
+    (ms,) = max_over_ranks(world, dev, t0.elapsed_time(t1))
+    ms_step = ms / args.steps
+    bytes_k1 = 2 * (2 * Bq * L * Hl * D + Bq * Tq * Hl * D + 2 * Bq * Tq * Hl * D
+                    + Bq * Tq * Hl * D) + 8 * Bq * Tq
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": Bq * Tq / (ms_step / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f16",
+            "data": "synthetic",
+            "config": {"workload": "C4: LLaMA-65B-shape attention layer (64 heads), heads sharded "
+                                   "over the GPUs, B=8, merged 3-SSM trees <1,1,3,1,1,1,1,1>, KV "
+                                   "2048, head-output all-gather + greedy verify",
+                       "B": Bq, "T": Tq, "L": L, "H_total": HT, "H_per_gpu": Hl,
+                       "gather": args.gather if world > 1 else "none (1 rank)",
+                       "parallelism": f"heads/{world}"},
+            "k1_bytes_per_gpu": bytes_k1,
+            "gather_bytes_received_per_gpu": (world - 1) * Bq * Tq * Hl * D * 2,
+            "gpu_launches": args.steps * (4 if peer is None else 4),
+            "clocks": clk}))
+    finish_rank(world)
 
 
 # ------------------------------------------------------------------ C3 -----
@@ -642,18 +1027,12 @@ def run_c3(args):
     (+ accepted-token all-gather for N > 1). Synthetic KV prefix and draft
     distributions; weights generated on the GPU from UniformStream(42)."""
     import torch
-    import torch.distributed as dist
 
     from paper_2305_09781_b200 import _capi
     from paper_2305_09781_b200.dist import gather_accepted, shard_range
     from paper_2305_09781_b200.tree import TokenTree, TreeBatch
 
-    rank, world, local = dist_env()
-    local, backend = dist_device(local)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group(backend, device_id=dev if backend == "nccl" else None)
+    rank, world, local, dev = init_rank(args)
     NL, d, Hh, Vv, BG = 32, 4096, 32, 32000, 32
     lo, hi = shard_range(BG, world, rank)
     Bl = hi - lo
@@ -684,11 +1063,7 @@ def run_c3(args):
             gather_accepted(ver, ln, world, out=gathered)
         return ln
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
+    barrier = barrier_of(world)
     for _ in range(max(args.warmup, 2)):
         ln = step()
     barrier()
@@ -702,11 +1077,7 @@ def run_c3(args):
     t1.record()
     barrier()
     clk = clocks.stop()
-    ms = t0.elapsed_time(t1)
-    if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = tt.item()
+    (ms,) = max_over_ranks(world, dev, t0.elapsed_time(t1))
     ms_step = ms / args.steps
     accepted = int(ln.sum().item())
     wbytes = model.param_count * 2
@@ -718,8 +1089,7 @@ def run_c3(args):
     gemm_flops = 2 * rows * (NL * 12 * d * d + d * Vv)
     attn_flops = NL * 4 * rows * d * (L + T)
     flops = gemm_flops + attn_flops
-    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-        tpeak = json.load(f)["bf16_tflops_sustained"]
+    tpeak = load_peaks().get("bf16_tflops_sustained", 1392.6)
     tach = flops / (ms_step / 1e3) / 1e12
     if rank == 0:
         print(json.dumps({
@@ -740,8 +1110,7 @@ def run_c3(args):
                          "hbm_bytes_per_step_per_gpu": wbytes + kvbytes,
                          "note": "whole-step figure: the GEMMs dominate (intensity ~ B*T rows)"},
             "verified_tokens_per_step": accepted * world, "clocks": clk}))
-    if world > 1:
-        dist.destroy_process_group()
+    finish_rank(world)
 
 
 if __name__ == "__main__":

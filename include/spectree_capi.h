@@ -104,7 +104,12 @@ typedef struct {
      * [0, P[b]). K1 (tcgen05 path, programmatic dependent launch) then builds
      * its schedule and starts streaming those rows while that kernel drains,
      * before griddepcontrol.wait; Q, the masks and tree rows are still read
-     * after the wait. */
+     * after the wait. The promise is transitive: no kernel still running when
+     * K1 starts may write those rows either. Programmatic launches chain, so
+     * the kernel before K1 must not release its dependents (launch_dependents)
+     * before its OWN griddepcontrol.wait has returned — st_build_masks_early
+     * and st_tree_prepare follow this rule, which makes "previous step's
+     * commit -> masks -> early_kv K1" safe while P advances every step. */
     int early_kv;
 } st_attn_args;
 

@@ -22,10 +22,16 @@ __device__ void move_rows_block(const int* ids, int L, int kfirst, int b, int h0
                                 int row_vecs, int64_t Lmax, int64_t P, char* kl, char* vl,
                                 const char* ktl, const char* vtl, int T) {
     const int per_row = nh * row_vecs;  // vectors of one row, all of this block's heads
-    const int rows_chunk = max(1, (int)blockDim.x * kMoveVecs / (2 * per_row));
-    for (int k0 = kfirst; k0 < L; k0 += rows_chunk) {
+    const int cap = (int)blockDim.x * kMoveVecs;   // vectors one pass of the block moves
+    // Rows wider than one pass (e.g. f64 rows of a long head dim on the byte
+    // path) move one row at a time in slices of `cap` vectors: the source row
+    // ids[k] > k is never a destination of an earlier row, and a later row's
+    // destination is written only after this row is read completely.
+    const int rows_chunk = per_row > cap ? 1 : max(1, cap / (2 * per_row));
+    const int slice = min(per_row, cap);
+    for (int k0 = kfirst, s0 = 0; k0 < L;) {
         const int k1 = min(L, k0 + rows_chunk);
-        const int total = (k1 - k0) * per_row;
+        const int total = per_row > cap ? min(slice, per_row - s0) : (k1 - k0) * per_row;
         V kx[kMoveVecs], vx[kMoveVecs];
         int64_t dst[kMoveVecs];
 #pragma unroll
@@ -33,7 +39,7 @@ __device__ void move_rows_block(const int* ids, int L, int kfirst, int b, int h0
             const int i = threadIdx.x + r * blockDim.x;
             dst[r] = -1;
             if (i < total) {
-                const int kk = k0 + i / per_row, rem = i % per_row;
+                const int kk = k0 + i / per_row, rem = i % per_row + s0;
                 const int h = h0 + rem / row_vecs, e = rem % row_vecs;
                 const int src = ids[kk];
                 const int64_t base = ((int64_t)b * Hkv + h) * Lmax + P;
@@ -59,6 +65,9 @@ __device__ void move_rows_block(const int* ids, int L, int kfirst, int b, int h0
             }
         }
         __syncthreads();
+        if (per_row > cap && (s0 += slice) < per_row) continue;  // next slice of row k0
+        s0 = 0;
+        k0 = k1;
     }
 }
 

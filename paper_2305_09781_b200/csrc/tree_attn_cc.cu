@@ -147,8 +147,10 @@ st_status launch_cc(const st_attn_args* a, cudaStream_t s) {
     else if (dpl <= 2) ST_CC_LAUNCH(2);
     else if (dpl <= 4) ST_CC_LAUNCH(4);
     else if (dpl <= 8) ST_CC_LAUNCH(8);
+    else if (dpl <= 16) ST_CC_LAUNCH(16);
+    else if (dpl <= 32) ST_CC_LAUNCH(32);
     else {
-        set_error("st_tree_attention: head dim > 256 unsupported");
+        set_error("st_tree_attention: head dim > 1024 unsupported");
         return ST_ERR_UNSUPPORTED;
     }
 #undef ST_CC_LAUNCH

@@ -123,12 +123,14 @@ __global__ void walk_kernel(const int32_t* __restrict__ outs, int T,
 // ~index, so an unsigned max picks the largest value and, among equal values,
 // the LOWEST index (reference tie rule). NaN maps to -inf (never wins); a NaN
 // at index 0 gets the maximal key (the reference never replaces index 0).
+// -0.0 and +0.0 compare equal under the reference's '>', so both map to the
+// same key and the lower index wins between them too.
 __device__ __forceinline__ unsigned long long arg_key(float v, int i) {
     if (v != v) {
         if (i == 0) return ~0ull;
         v = -INFINITY;
     }
-    uint32_t u = __float_as_uint(v);
+    uint32_t u = v == 0.0f ? 0u : __float_as_uint(v);  // canonicalise -0.0
     u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
     return ((unsigned long long)u << 32) | (uint32_t)(~(uint32_t)i);
 }
@@ -392,16 +394,24 @@ walk_compact_kernel(int T, const int32_t* __restrict__ tokens, const int32_t* __
 
 // One thread per (request, node): tree_masks.cuh.
 // early: the caller promises the previous kernel on the stream neither writes
-// parent / n_nodes nor touches mask, so the masks are built while it drains and
-// the kernel only waits for it before exiting (keeping completion transitive).
+// parent / n_nodes nor touches mask, so the masks are built while it drains.
+// The dependents' launch is released only AFTER this kernel's own wait: an
+// early_kv K1 that follows streams the committed rows [0, P) before ITS wait,
+// so it must not start while the kernel before this one (e.g. the previous
+// step's commit, which writes rows [P_prev, P)) may still run.
 __global__ void build_masks_kernel(const int32_t* __restrict__ parent,
                                    const int32_t* __restrict__ n_nodes, int T, int W,
                                    uint64_t* __restrict__ mask, int early) {
     extern __shared__ int s_par[];
-    if (!early) pdl_wait();
-    pdl_trigger();
+    if (!early) {
+        pdl_wait();
+        pdl_trigger();
+    }
     build_masks_block(parent, n_nodes, T, W, mask, blockIdx.x, blockIdx.y, s_par);
-    if (early) pdl_wait();
+    if (early) {
+        pdl_wait();
+        pdl_trigger();
+    }
 }
 
 }  // namespace

@@ -230,7 +230,7 @@ def test_k3_tie_and_nan_rules(capi, restatement):
     (argmax_token, reference transformer.cpp:116-122)."""
     tok, par, dep = restatement.merge([[0, 1], [0, 2]])
     T, V = len(tok), 4100
-    logits = np.zeros((8, T, V), np.float32)
+    logits = np.zeros((11, T, V), np.float32)
     logits[0, :, 7] = logits[0, :, 3000] = 5.0       # tie -> 7
     logits[1, :, 1] = np.nan
     logits[1, :, 2] = 1.0                            # NaN skipped -> 2
@@ -244,7 +244,19 @@ def test_k3_tie_and_nan_rules(capi, restatement):
     logits[6, :, :] = -np.inf
     logits[6, :, 4000] = np.nan                      # -> 0
     logits[7] = np.random.default_rng(3).standard_normal((T, V)).astype(np.float32)
-    tok4, par4, _, n4 = pack([(tok, par, dep)] * 8)
+    # +0.0 and -0.0 compare equal under the reference's '>': the lower id wins
+    logits[8, :, :] = -1.0
+    logits[8, :, 5] = -0.0                           # -0 low (slice 0), +0 high (slice 6)
+    logits[8, :, 3000] = 0.0                         # -> 5
+    logits[9, :, :] = -1.0
+    logits[9, :, 1030] = 0.0                         # +0 low, -0 high, other slices
+    logits[9, :, 4000] = -0.0                        # -> 1030
+    logits[10, :, :] = -1.0
+    logits[10, :, 2049] = -0.0                       # same thread / same float4
+    logits[10, :, 2050] = 0.0                        # -> 2049
+    for b in (8, 9, 10):
+        assert restatement.argmax(logits[b, 0]) == {8: 5, 9: 1030, 10: 2049}[b]
+    tok4, par4, _, n4 = pack([(tok, par, dep)] * 11)
     _verify_case(capi, restatement, logits, tok4, par4, n4)
 
 
