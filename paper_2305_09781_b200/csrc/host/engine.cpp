@@ -125,7 +125,8 @@ GenerationResult run_speculative(const ModelWeights& llm,
     KVCache cache(llm.config);
     {
         std::lock_guard<std::recursive_mutex> lock(detail::compat_mutex());
-        detail::set_device_authoritative(cache, true);
+        // tree scratch rows past max_positions: node u of a tree lands at row P + u
+        detail::set_device_authoritative(cache, true, std::max(opts.max_tree_nodes, 1));
         prefill_device(llm, cache, req.prompt);  // the first tree pass recomputes the root row
     }
     // device staging for the walk: tok | parent | n | budget, outputs: verified | ids | len

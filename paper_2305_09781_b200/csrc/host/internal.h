@@ -31,8 +31,12 @@ struct DeviceKV {
 std::recursive_mutex& compat_mutex();
 cudaStream_t compat_stream();
 
-// Engine-private caches keep their rows on the device only.
-void set_device_authoritative(KVCache& cache, bool on);
+// Engine-private caches keep their rows on the device only. Turning it on
+// first sizes the device mirror for max_positions + scratch_rows rows: a tree
+// pass writes node u at row P + u (rows are indexed by node id, positions by
+// depth), so a branching tree near the position limit needs up to
+// max_tree_nodes rows past P while its positions stay below max_positions.
+void set_device_authoritative(KVCache& cache, bool on, int scratch_rows = 0);
 
 // One batched pass in device-authoritative mode; returns the per-row greedy
 // outputs and (via argmax_dev) their device copy, valid until the next pass.

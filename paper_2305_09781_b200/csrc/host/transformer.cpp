@@ -188,16 +188,29 @@ struct DeviceModel {
     }
 };
 
+// Hash of EVERY weight (an in-place edit anywhere must re-upload; a sampled
+// hash missed edits between samples). Four independent multiply-xor lanes keep
+// it at memory speed — far below the reference's own per-node weight traffic.
 uint64_t fingerprint(const ModelWeights& w) {
     uint64_t h = 1469598103934665603ull;
     auto mixv = [&](const std::vector<double>& v) {
-        const size_t step = std::max<size_t>(1, v.size() / 4096);
-        for (size_t i = 0; i < v.size(); i += step) {
+        uint64_t a[4] = {h, h ^ 0x9e3779b97f4a7c15ull, h ^ 0xbf58476d1ce4e5b9ull,
+                         h ^ 0x94d049bb133111ebull};
+        const size_t n = v.size(), n4 = n & ~size_t(3);
+        const auto* p = reinterpret_cast<const unsigned char*>(v.data());
+        for (size_t i = 0; i < n4; i += 4)
+            for (int j = 0; j < 4; ++j) {
+                uint64_t b;
+                std::memcpy(&b, p + (i + j) * 8, 8);
+                a[j] = (a[j] ^ b) * 0x100000001b3ull;
+            }
+        for (size_t i = n4; i < n; ++i) {
             uint64_t b;
-            std::memcpy(&b, &v[i], 8);
-            h = (h ^ b) * 1099511628211ull;
+            std::memcpy(&b, p + i * 8, 8);
+            a[0] = (a[0] ^ b) * 0x100000001b3ull;
         }
-        h = (h ^ v.size()) * 1099511628211ull;
+        for (int j = 0; j < 4; ++j) h = (h ^ a[j]) * 1099511628211ull;
+        h = (h ^ n) * 1099511628211ull;
     };
     const auto& c = w.config;
     for (int x : {c.num_layers, c.num_heads, c.d_model, c.vocab_size, c.max_positions, c.ffn_mult})
@@ -748,7 +761,12 @@ namespace spectree::detail {
 std::recursive_mutex& compat_mutex() { return g_mu; }
 cudaStream_t compat_stream() { return stream(); }
 
-void set_device_authoritative(KVCache& cache, bool on) { cache.device().authoritative = on; }
+void set_device_authoritative(KVCache& cache, bool on, int scratch_rows) {
+    DeviceKV& dk = cache.device();
+    if (on && !dk.authoritative)
+        ensure_rows(dk, cache.config().max_positions + std::max(scratch_rows, 0));
+    dk.authoritative = on;
+}
 
 std::vector<TokenId> device_pass(const ModelWeights& w, KVCache& cache,
                                  const std::vector<TokenId>& tokens,

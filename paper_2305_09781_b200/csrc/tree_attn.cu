@@ -1,9 +1,14 @@
 // K1 dispatcher: st_tree_attention (C-ABI) -> CUDA-core or tcgen05 kernel.
 //
-// Dispatch rule (north star: tensor cores "only where GQA head-grouping x
-// tree width makes them dense enough to pay"): half-precision inputs with
-// D == 128 and (H/Hkv) * T >= 16 go to the tcgen05 kernel; everything else
-// (f32/f64 parity runs, tiny trees) to the CUDA-core kernel.
+// Dispatch rule: half-precision inputs with D == 128 go to the tcgen05
+// kernel; f32/f64 (the reference-parity runs) and other head dims to the
+// CUDA-core kernel. Small trees (G*T < 16) used to go to the CUDA-core kernel
+// because their MMAs are mostly zero rows (north star: tensor cores "only where
+// GQA head-grouping x tree width makes them dense enough to pay"), but what
+// pays at ANY tree size is the tiling: the tcgen05 kernel streams each KV tile
+// once for all of a pair's rows, the CUDA-core kernel once per (node, head) —
+// 300-700x apart on the GQA sweep (profiles/gqa_sweep.json) — and an
+// M=64 tile with a few live rows skips the softmax of its empty warps.
 #include "common.cuh"
 #include "tree_attn.h"
 
@@ -30,8 +35,7 @@ st_status validate_ptrs(const st_attn_args* a) {
 
 int choose_path(const st_attn_args* a) {
     if (a->force_path == 1 || a->force_path == 2) return a->force_path;
-    const bool dense = (int64_t)(a->H / a->Hkv) * a->T >= 16;
-    return (dense && st::tree_attention_tc_supported(a)) ? 2 : 1;
+    return st::tree_attention_tc_supported(a) ? 2 : 1;
 }
 
 }  // namespace
@@ -81,7 +85,7 @@ st_status st_tree_attention_allgather(const st_attn_args* a, const st_peer_out* 
     if (a->B == 0) return ST_OK;
     if (choose_path(a) != 2 || !st::tree_attention_tc_supported(a)) {
         st::set_error("st_tree_attention_allgather: needs the tcgen05 path (f16/bf16, D == 128, "
-                      "(H/Hkv)*T >= 16)");
+                      "(H/Hkv)*T <= 128)");
         return ST_ERR_UNSUPPORTED;
     }
     const size_t need = st::tree_attention_tc_workspace(a);

@@ -55,11 +55,12 @@ def oracle_pairs(R, q, kc, vc, mask, P, n, pairs, kt=None, vt=None):
         hk = h // G
         Pb, nb = int(P[b]), int(n[b])
         qq = q[b, :, h].double().cpu().numpy().reshape(1, T, 1, D)
-        kk = kc[b, hk, : Pb + nb].double().cpu().numpy()
-        vv = vc[b, hk, : Pb + nb].double().cpu().numpy()
-        if kt is not None:
-            kk[Pb:] = kt[b, :nb, hk].double().cpu().numpy()
-            vv[Pb:] = vt[b, :nb, hk].double().cpu().numpy()
+        if kt is not None:   # committed rows, then the tree's own rows
+            kk = torch.cat([kc[b, hk, :Pb], kt[b, :nb, hk]]).double().cpu().numpy()
+            vv = torch.cat([vc[b, hk, :Pb], vt[b, :nb, hk]]).double().cpu().numpy()
+        else:
+            kk = kc[b, hk, : Pb + nb].double().cpu().numpy()
+            vv = vc[b, hk, : Pb + nb].double().cpu().numpy()
         o = R.tree_attention(qq, kk[None, None].copy(), vv[None, None].copy(),
                              np.ascontiguousarray(mask[b:b + 1]), np.array([Pb], np.int32),
                              np.array([nb], np.int32), D ** -0.5)

@@ -304,3 +304,30 @@ def test_tc_fuzz(capi, restatement):
                             out=out, lse=lse, force_path=2, k_tree=kt, v_tree=vt, early_kv=early)
         torch.cuda.synchronize()
         check_k1(restatement, bt, out, dtype, lse)
+
+
+@pytest.mark.parametrize("T,G,dtype", [(1, 1, torch.float16), (2, 1, torch.bfloat16),
+                                       (4, 1, torch.float16), (8, 1, torch.float16),
+                                       (4, 2, torch.bfloat16), (15, 1, torch.float16)])
+def test_tc_small_trees_auto_path(capi, restatement, T, G, dtype):
+    """G*T < 16 (a few live query rows per tile): the auto dispatch now takes
+    the tcgen05 kernel (one pass over the KV for all rows), checked against the
+    f64 restatement with ragged prefixes, split pairs and LSE."""
+    rng = np.random.default_rng(300 + T * 10 + G)
+    Hkv = 4
+    trees = []
+    for _ in range(6):
+        w = 1 if T <= 2 else 2
+        t = restatement.merge(width_depth_seqs(rng, int(rng.integers(0, 50)), 50, w,
+                                               max(0, (T - 1) // w)), 4096)
+        trees.append(tuple(a[:T] for a in t))
+    bt = make_batch(restatement, rng, 6, G * Hkv, Hkv, 128, trees=trees, T=T,
+                    P_range=(0, 3000), dtype=dtype)
+    dev = "cuda"
+    q = torch.tensor(bt["q"], device=dev).to(dtype)
+    kc = torch.tensor(bt["kc"], device=dev).to(dtype)
+    mask = torch.tensor(bt["mask"].view(np.int64), device=dev)
+    Pd, nd = torch.tensor(bt["P"], device=dev), torch.tensor(bt["n"], device=dev)
+    assert capi.tree_attention_path(q, kc, kc, mask, Pd, nd) == 2
+    out, lse = run_k1(capi, bt, dtype, force_path=0, lse=True)
+    check_k1(restatement, bt, out, dtype, lse)
