@@ -1104,7 +1104,10 @@ size_t tree_attention_tc_workspace(const st_attn_args* a) {
 }
 
 // K1 is launched with programmatic dependent launch (common.cuh): its prologue
-// overlaps the previous kernel's tail. Split pairs are merged inside K1.
+// overlaps the previous kernel's tail. Split pairs are merged inside K1: a
+// pair's head CTA waits for flags the piece CTAs release, so the grid (one CTA
+// per SM) is launched cooperatively — co-residency guaranteed by the runtime,
+// not assumed (ST_K1_COOP=0 turns it off for A/B runs).
 #define ST_TRY_LAUNCH_TC(TT, MM)                                                                \
     do {                                                                                        \
         static bool attr = false;                                                               \
@@ -1114,8 +1117,8 @@ size_t tree_attention_tc_workspace(const st_attn_args* a) {
                                              Cfg<MM>::SMEM_BYTES));                             \
             attr = true;                                                                        \
         }                                                                                       \
-        ST_CUDA_TRY(launch_pdl(tree_attn_tc_kernel<TT, MM>, dim3(G), dim3(Cfg<MM>::THREADS),     \
-                               Cfg<MM>::SMEM_BYTES, stream, tq, tk, tv, tkt, tvt, prm));    \
+        ST_CUDA_TRY(launch_pdl_ex(tree_attn_tc_kernel<TT, MM>, dim3(G), dim3(Cfg<MM>::THREADS),  \
+                                  Cfg<MM>::SMEM_BYTES, stream, coop, tq, tk, tv, tkt, tvt, prm)); \
     } while (0)
 
 st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st_peer_out* po) {
@@ -1192,6 +1195,7 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
         cudaMemsetAsync(trace_buf, 0, (kTraceRows * 64 + kTraceCta * 1024) * sizeof(unsigned long long), stream);
         prm.trace = trace_buf;
     }
+    static const bool coop = !(getenv("ST_K1_COOP") && atoi(getenv("ST_K1_COOP")) == 0);
     const bool m64 = (int64_t)prm.G * a->T <= 64;
     if (a->dtype == ST_F16) {
         if (m64) { ST_TRY_LAUNCH_TC(__half, 64); } else { ST_TRY_LAUNCH_TC(__half, 128); }
