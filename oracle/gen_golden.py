@@ -167,7 +167,58 @@ def decode_fixture(R, cfg, seed, prompt, seqs, max_nodes=64, apply_fix=True):
     return logits, toks, tok, par, dep
 
 
+def expansion_ref(R, cfg, seed, prefix, expansion):
+    """Expansion tree from the reference's own TransformerSsm::next_log_probs:
+    at depth i every frontier path keeps its e_i most likely next tokens (ties:
+    lower token id) — the rule speculator.hpp documents for
+    expansion_speculate."""
+    frontier = [[]]
+    for e in expansion:
+        nxt = []
+        for f in frontier:
+            lp = R.next_log_probs(cfg, seed, list(prefix) + f)
+            order = sorted(range(len(lp)), key=lambda t: (-lp[t], t))[:e]
+            nxt.extend(f + [t] for t in order)
+        frontier = nxt
+    return [[int(prefix[-1])] + f for f in frontier]
+
+
+def drafts(R):
+    """Draft-generation golden: the reference beam_speculate (TransformerSsm)
+    for several prefixes / (width, depth) / EOS, and expansion trees scored by
+    the reference next_log_probs. Plain text for tests/cpp/engine_parity_test.cpp."""
+    cfg, seed = (2, 2, 32, 64, 128, 4), 61
+    rng = np.random.default_rng(61)
+    lines = [" ".join(map(str, cfg)) + f" {seed}"]
+    cases = []
+    for width, depth in [(1, 4), (2, 4), (4, 2), (4, 8), (2, 16), (3, 5)]:
+        prefix = rng.integers(0, cfg[3], int(rng.integers(1, 9))).tolist()
+        cases.append(("beam", prefix, width, depth, -1))
+    full = R.beam_speculate(cfg, seed, [7, 3, 9], 4, 6)
+    cases.append(("beam", [7, 3, 9], 4, 6, int(full[1][2])))   # EOS mid-beam: finished beams carried
+    cases.append(("beam", [7, 3, 9], 2, 6, int(full[0][1])))
+    lines.append(str(len(cases)))
+    for kind, prefix, width, depth, eos in cases:
+        seqs = R.beam_speculate(cfg, seed, prefix, width, depth, eos)
+        lines.append(f"{len(prefix)} " + " ".join(map(str, prefix)) + f" {width} {depth} {eos} {len(seqs)}")
+        lines.extend(f"{len(q)} " + " ".join(map(str, q)) for q in seqs)
+    exps = [[1, 1, 3, 1, 1, 1, 1, 1], [2, 2, 1], [4]]
+    lines.append(str(len(exps)))
+    for e in exps:
+        prefix = rng.integers(0, cfg[3], 5).tolist()
+        seqs = expansion_ref(R, cfg, seed, prefix, e)
+        lines.append(f"{len(prefix)} " + " ".join(map(str, prefix)) + f" {len(e)} " +
+                     " ".join(map(str, e)) + f" {len(seqs)}")
+        lines.extend(f"{len(q)} " + " ".join(map(str, q)) for q in seqs)
+    with open(os.path.join(GOLDEN, "drafts_toy.txt"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "drafts":   # only the draft fixtures
+        build(ref=True)
+        drafts(Reference())
+        return
     build(ref=True)
     R = Reference()
     os.makedirs(GOLDEN, exist_ok=True)
@@ -233,6 +284,7 @@ def main():
         f.write(f"{len(prompt)} " + " ".join(map(str, prompt.tolist())) + "\n")
         f.write(f"{len(inc)} " + " ".join(map(str, inc.tolist())) + "\n")
         f.write(f"{inc_steps} {spec_steps}\n")
+    drafts(R)
     print("golden fixtures written to", GOLDEN)
     for f in sorted(os.listdir(GOLDEN)):
         print(f"  {f}: {os.path.getsize(os.path.join(GOLDEN, f))} bytes")

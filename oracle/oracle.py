@@ -200,6 +200,9 @@ class Reference:
         L.ref_bench_tree_decode.argtypes = cfg + [C.c_uint64, C.c_int, C.c_int, _i32p, _i32p,
                                                   C.c_int, C.c_int, C.c_int]
         L.ref_bench_tree_decode.restype = C.c_double
+        L.ref_beam_speculate.argtypes = cfg + [C.c_uint64, _i32p, C.c_int, C.c_int, C.c_int,
+                                               C.c_int32, _i32p, _i32p, C.c_int, _ip]
+        L.ref_next_log_probs.argtypes = cfg + [C.c_uint64, _i32p, C.c_int, _f64p]
 
     def _check(self, st, what):
         if st != 0:
@@ -300,6 +303,26 @@ class Reference:
                                                       seq, cap, C.byref(n), C.byref(steps)),
                     "run_speculative")
         return seq[: n.value].copy(), steps.value
+
+    def beam_speculate(self, cfg, seed, prefix, width, depth, eos=-1):
+        prefix = np.ascontiguousarray(prefix, np.int32)
+        cap = (len(prefix) + depth + 1) * width + 1
+        flat = np.zeros(cap, np.int32)
+        lens = np.zeros(width + 1, np.int32)
+        n = C.c_int(0)
+        self._check(self.lib.ref_beam_speculate(*cfg, seed, prefix, len(prefix), width, depth, eos,
+                                                flat, lens, cap, C.byref(n)), "beam_speculate")
+        out, at = [], 0
+        for i in range(n.value):
+            out.append(flat[at: at + lens[i]].tolist())
+            at += lens[i]
+        return out
+
+    def next_log_probs(self, cfg, seed, ctx):
+        ctx = np.ascontiguousarray(ctx, np.int32)
+        out = np.zeros(cfg[3], np.float64)
+        self._check(self.lib.ref_next_log_probs(*cfg, seed, ctx, len(ctx), out), "next_log_probs")
+        return out
 
     def bench_tree_decode(self, cfg, seed, n_requests, prefix_len, seqs, max_nodes, n_threads):
         flat, lens = _flatten(seqs)

@@ -321,4 +321,38 @@ double ref_bench_tree_decode(int layers, int heads, int d_model, int vocab, int 
     return st == 0 ? secs : -static_cast<double>(st < 0 ? 1000 : st);
 }
 
+// beam_speculate (proj/src/speculator.cpp:97-169) with a TransformerSsm over
+// init_random_weights(cfg, seed): the sequences flattened (lens[i] tokens each).
+int ref_beam_speculate(int layers, int heads, int d_model, int vocab, int max_pos, int ffn_mult,
+                       uint64_t seed, const int32_t* prefix, int prefix_len, int width, int depth,
+                       int32_t eos, int32_t* flat, int32_t* lens, int cap, int* nseq) {
+    return guarded([&] {
+        const ModelConfig c = make_cfg(layers, heads, d_model, vocab, max_pos, ffn_mult);
+        TransformerSsm ssm(0, cached_weights(c, seed));
+        const auto seqs = beam_speculate(ssm, std::span<const TokenId>(prefix, prefix_len),
+                                         SpecConfig{width, depth}, eos);
+        int at = 0;
+        for (size_t i = 0; i < seqs.size(); ++i) {
+            if (at + (int)seqs[i].size() > cap) return -1;
+            std::copy(seqs[i].begin(), seqs[i].end(), flat + at);
+            lens[i] = (int32_t)seqs[i].size();
+            at += (int)seqs[i].size();
+        }
+        *nseq = (int)seqs.size();
+        return 0;
+    });
+}
+
+// TransformerSsm::next_log_probs (proj/src/speculator.cpp:85-95).
+int ref_next_log_probs(int layers, int heads, int d_model, int vocab, int max_pos, int ffn_mult,
+                       uint64_t seed, const int32_t* ctx, int n, double* out) {
+    return guarded([&] {
+        const ModelConfig c = make_cfg(layers, heads, d_model, vocab, max_pos, ffn_mult);
+        TransformerSsm ssm(0, cached_weights(c, seed));
+        const auto lp = ssm.next_log_probs(std::span<const TokenId>(ctx, n));
+        std::copy(lp.begin(), lp.end(), out);
+        return 0;
+    });
+}
+
 }  // extern "C"
