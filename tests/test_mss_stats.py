@@ -45,9 +45,12 @@ def setup(rng):
 def draws(rng, q, n):
     """Per trial: child tokens t1 ~ q1, t2 ~ q2, t3 ~ q3; the tree in preorder
     with children ascending by token: root, then the smaller of (t1, t2)..."""
-    t1 = rng.choice(V, n, p=q[1].astype(np.float64))
-    t2 = rng.choice(V, n, p=q[2].astype(np.float64))
-    t3 = rng.choice(V, n, p=q[3].astype(np.float64))
+    def pr(row):   # the fp32 draft row as a float64 distribution
+        x = row.astype(np.float64)
+        return x / x.sum()
+    t1 = rng.choice(V, n, p=pr(q[1]))
+    t2 = rng.choice(V, n, p=pr(q[2]))
+    t3 = rng.choice(V, n, p=pr(q[3]))
     return t1, t2, t3
 
 
