@@ -125,6 +125,8 @@ struct TcParams {
     unsigned* flags;     // [gridDim.x]: 1 while that piece is published and not yet merged
     int B, T, H, W;      // H: KV heads (one (b, h) pair per request and KV head)
     int G, Hq;           // query heads per KV head (GQA group), query heads = G * H
+    int R;               // row blocks per pair: G*T <= 128 -> 1; <= 256 -> 2 (CTAs 2s, 2s+1
+                         // take the two 128-row blocks of schedule slot s)
     int tree_src;        // tree rows come from k_tree/v_tree: one extra tile after ceil(P/BN)
     int early_kv;        // st_attn_args.early_kv: stream committed KV before griddepcontrol.wait
     float c_log2;        // scale * log2(e)
@@ -170,8 +172,13 @@ __device__ __forceinline__ int ntiles_of(const TcParams& p, int b) {
     const int n = __ldg(p.n_nodes + b);
     if (n <= 0) return 0;
     const int P = __ldg(p.prefix_len + b);
-    // k_tree mode: the prefix tiles, then one tile of the (<= 128) tree rows
-    return p.tree_src ? (P + BN - 1) / BN + 1 : (P + n + BN - 1) / BN;
+    // k_tree mode: the prefix tiles, then ceil(n/BN) tiles of the tree rows
+    return p.tree_src ? (P + BN - 1) / BN + (n + BN - 1) / BN : (P + n + BN - 1) / BN;
+}
+
+// k_tree mode: the segment's last tree_tiles tiles are the tree's own rows
+__device__ __forceinline__ int tree_tiles(const TcParams& p, const Seg& s) {
+    return s.ntiles - (__ldg(p.prefix_len + s.b) + BN - 1) / BN;
 }
 
 // Segment starting at global tile t (t < t_end) of this CTA's range. `cum`
@@ -329,7 +336,10 @@ __device__ __forceinline__ void store_row(T* dst_row, const float* v, float scal
     }
 }
 
-template <class T, int M>
+// MW: ancestor-mask words held per row (2: T <= 128; 4: T <= 256, the
+// two-row-block instantiation — kept separate so the common case keeps its
+// registers).
+template <class T, int M, int MW>
 __global__ void __launch_bounds__(Cfg<M>::THREADS, 1)
 tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v,
@@ -439,10 +449,16 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     __syncthreads();
     if (threadIdx.x == 0) K1_GT(9);
 
-    const uint32_t G = gridDim.x;
+    // Schedule slots: with R = 2 row blocks per pair, CTAs 2s and 2s+1 take
+    // slot s's tile range for Q rows [0, 128) and [128, 256) of each pair, so
+    // both stream the same KV tiles at the same time (the second read is an L2
+    // hit) and each runs the M=128 pipeline unchanged.
+    const uint32_t G = gridDim.x / (uint32_t)p.R;
+    const uint32_t slot = blockIdx.x / (uint32_t)p.R;
+    const int rblk = (int)(blockIdx.x - slot * (uint32_t)p.R);
     const Sched sched = make_sched(p, cum, G);
-    const uint32_t t_begin = range_start(blockIdx.x, sched, G);
-    const uint32_t t_end = range_start(blockIdx.x + 1, sched, G);
+    const uint32_t t_begin = range_start(slot, sched, G);
+    const uint32_t t_end = range_start(slot + 1, sched, G);
     if (p.trace && threadIdx.x == 0) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
@@ -460,11 +476,12 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             for (uint32_t t = t_begin; t < t_end;) {
                 const Seg s = find_seg(p, cum, t, t_end);
                 int j = s.lo;
+                const int jt0 = p.tree_src ? s.ntiles - tree_tiles(p, s) : 1 << 30;  // first tree tile
                 if (!waited) {  // early_kv: up to KS committed-prefix K tiles before the wait
                     const int P0 = __ldg(p.prefix_len + s.b);
                     const int bh0 = s.b * p.H + s.h;
                     for (; j < s.hi && kc < (uint32_t)KS &&
-                           (p.tree_src ? j < s.ntiles - 1 : j * BN + BN <= P0);
+                           (p.tree_src ? j < jt0 : j * BN + BN <= P0);
                          ++j, ++kc) {
                         const uint32_t st = kc;  // first use of each stage: nothing to wait for
                         mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
@@ -478,9 +495,11 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 const uint32_t qb = qc % QS;
                 mbar_wait(q_empty + qb, ((qc / QS) & 1) ^ 1);
                 mbar_arrive_expect_tx(q_full + qb, C::A_BYTES);
-                // box {64 d, G heads, M/G nodes}: smem row = node * G + head
-                tma_load_4d(sm_q + qb * C::A_BYTES, &tm_q, q_full + qb, 0, s.h * p.G, 0, s.b);
-                tma_load_4d(sm_q + qb * C::A_BYTES + C::A_ATOM, &tm_q, q_full + qb, 64, s.h * p.G, 0, s.b);
+                // box {64 d, G heads, M/G nodes}: smem row = node * G + head;
+                // row block rblk starts at node rblk * M / G
+                const int node0 = rblk * (M / p.G);
+                tma_load_4d(sm_q + qb * C::A_BYTES, &tm_q, q_full + qb, 0, s.h * p.G, node0, s.b);
+                tma_load_4d(sm_q + qb * C::A_BYTES + C::A_ATOM, &tm_q, q_full + qb, 64, s.h * p.G, node0, s.b);
                 ++qc;
                 const int bh = s.b * p.H + s.h;
                 for (; j < s.hi; ++j, ++kc) {
@@ -490,9 +509,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     if (kc == 0) K1_GT(5);
                     mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
                     uint8_t* dst = sm_k + st * TILE_BYTES;
-                    if (p.tree_src && j == s.ntiles - 1) {  // the tree's own rows [B][T][Hkv][D]
-                        tma_load_4d(dst, &tm_kt, k_full + st, 0, s.h, 0, s.b);
-                        tma_load_4d(dst + KV_ATOM, &tm_kt, k_full + st, 64, s.h, 0, s.b);
+                    if (j >= jt0) {  // the tree's own rows [B][T][Hkv][D], 128 nodes per tile
+                        tma_load_4d(dst, &tm_kt, k_full + st, 0, s.h, (j - jt0) * BN, s.b);
+                        tma_load_4d(dst + KV_ATOM, &tm_kt, k_full + st, 64, s.h, (j - jt0) * BN, s.b);
                     } else {
                         tma_load_3d_hint(dst, &tm_k, k_full + st, 0, j * BN, bh, pol);
                         tma_load_3d_hint(dst + KV_ATOM, &tm_k, k_full + st, 64, j * BN, bh, pol);
@@ -523,11 +542,11 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     }
                     int* pieces = reinterpret_cast<int*>(smem + C::OFF_PIECES);
                     int np = 0;
-                    for (uint32_t c2 = blockIdx.x + 1; c2 < G && np < kMaxPieces; ++c2) {
+                    for (uint32_t c2 = slot + 1; c2 < G && np < kMaxPieces; ++c2) {
                         const uint32_t rs = range_start(c2, sched, G);
                         if (rs >= pend) break;
                         if (range_start(c2 + 1, sched, G) == rs) continue;  // empty range
-                        pieces[1 + np++] = (int)c2;
+                        pieces[1 + np++] = (int)(c2 * (uint32_t)p.R) + rblk;  // same row block
                     }
                     pieces[0] = np;
                     const int ns = np < C::STAGED_PIECES ? np : C::STAGED_PIECES;
@@ -558,10 +577,11 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 const Seg s = find_seg(p, cum, t, t_end);
                 const int bh = s.b * p.H + s.h;
                 int j = s.lo;
+                const int jt0 = p.tree_src ? s.ntiles - tree_tiles(p, s) : 1 << 30;  // first tree tile
                 if (!waited) {  // early_kv: up to VS committed-prefix V tiles before the wait
                     const int P0 = __ldg(p.prefix_len + s.b);
                     for (; j < s.hi && vc < (uint32_t)VS &&
-                           (p.tree_src ? j < s.ntiles - 1 : j * BN + BN <= P0);
+                           (p.tree_src ? j < jt0 : j * BN + BN <= P0);
                          ++j, ++vc) {
                         const uint32_t st = vc;
                         mbar_arrive_expect_tx(v_full + st, TILE_BYTES);
@@ -578,9 +598,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     K1_TRACE(1, vc);
                     mbar_arrive_expect_tx(v_full + st, TILE_BYTES);
                     uint8_t* dst = sm_v + st * TILE_BYTES;
-                    if (p.tree_src && j == s.ntiles - 1) {
-                        tma_load_4d(dst, &tm_vt, v_full + st, 0, s.h, 0, s.b);
-                        tma_load_4d(dst + KV_ATOM, &tm_vt, v_full + st, 64, s.h, 0, s.b);
+                    if (j >= jt0) {
+                        tma_load_4d(dst, &tm_vt, v_full + st, 0, s.h, (j - jt0) * BN, s.b);
+                        tma_load_4d(dst + KV_ATOM, &tm_vt, v_full + st, 64, s.h, (j - jt0) * BN, s.b);
                     } else {
                         tma_load_3d_hint(dst, &tm_v, v_full + st, 0, j * BN, bh, pol);
                         tma_load_3d_hint(dst + KV_ATOM, &tm_v, v_full + st, 64, j * BN, bh, pol);
@@ -698,7 +718,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         const int r = DUAL ? (warp & 3) * 32 + lane : warp * 16 + (lane & 15);
         // Q/S/O row r holds tree node u_r of query head g_r of the pair's
         // KV-head group (the Q box lays rows out node-major, head-minor)
-        const int u_r = r / p.G, g_r = r - u_r * p.G;
+        const int rr = rblk * M + r;  // row within the pair's G*T rows
+        const int u_r = rr / p.G, g_r = rr - u_r * p.G;
         const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         const uint32_t s_half = DUAL ? half * COLS : 0;          // this half's S columns
         const uint32_t o_own = DUAL ? (half ? C::OB_COL : C::O_COL) : C::O_COL;
@@ -712,17 +733,19 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         // transition costs no global round trip on the softmax path.
         struct Meta {
             int n, P;
-            uint64_t mw0, mw1;
+            uint64_t mw[MW];   // this row's ancestor words
         };
         auto load_meta = [&](const Seg& sg) {
             Meta mt;
             mt.n = __ldg(p.n_nodes + sg.b);
             mt.P = __ldg(p.prefix_len + sg.b);
-            mt.mw0 = mt.mw1 = 0;
+#pragma unroll
+            for (int w = 0; w < MW; ++w) mt.mw[w] = 0;
             if (u_r < p.T) {
                 const uint64_t* mr = p.mask + ((long long)sg.b * p.T + u_r) * p.W;
-                mt.mw0 = __ldg(mr);
-                if (p.W > 1) mt.mw1 = __ldg(mr + 1);
+#pragma unroll
+                for (int w = 0; w < MW; ++w)
+                    if (w < p.W) mt.mw[w] = __ldg(mr + w);
             }
             return mt;
         };
@@ -741,10 +764,12 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             const int P = m_next.P;
             // first kv row index of the tree rows: P, or (k_tree mode) the
             // start of the extra tree tile after the ceil(P/BN) prefix tiles
-            const int Pt = p.tree_src ? (s.ntiles - 1) * BN : P;
+            const int Pt = p.tree_src ? (s.ntiles - (n + BN - 1) / BN) * BN : P;
             const bool valid = u_r < n;
             const bool warp_live = __any_sync(0xffffffffu, valid);
-            const uint64_t mw0 = valid ? m_next.mw0 : 0, mw1 = valid ? m_next.mw1 : 0;
+            uint64_t mw[MW];
+#pragma unroll
+            for (int w = 0; w < MW; ++w) mw[w] = valid ? m_next.mw[w] : 0;
             float m = -INFINITY, l = 0.f;   // l: this thread's share of the row sum
             for (int i = 0; i < ntl; ++i) {
                 const int j = s.lo + i;
@@ -773,12 +798,21 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             uint32_t vis = pre >= 32 ? 0xffffffffu : (pre <= 0 ? 0u : ((1u << pre) - 1u));
                             const int o = a - Pt;                         // tree index of bit 0
                             if (o > -32 && o < n) {
-                                uint64_t win;
-                                if (o < 0) win = mw0 << (-o);
-                                else if (o == 0) win = mw0;
-                                else if (o < 64) win = (mw0 >> o) | (mw1 << (64 - o));
-                                else win = mw1 >> (o - 64);
-                                vis |= (uint32_t)win;
+                                // bits [o, o + 32) of the row's 256-bit ancestor mask
+                                uint32_t win;
+                                if (o < 0) {
+                                    win = (uint32_t)(mw[0] << (-o));
+                                } else {
+                                    const int wd0 = o >> 6, sh = o & 63;
+                                    uint64_t lo = 0, hi = 0;
+#pragma unroll
+                                    for (int w = 0; w < MW; ++w) {
+                                        if (w == wd0) lo = mw[w];
+                                        if (w == wd0 + 1) hi = mw[w];
+                                    }
+                                    win = (uint32_t)(sh ? (lo >> sh) | (hi << (64 - sh)) : lo);
+                                }
+                                vis |= win;
                             }
 #pragma unroll
                             for (int k = 0; k < 32; ++k)
@@ -1085,12 +1119,13 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 bool tree_attention_tc_supported(const st_attn_args* a) {
     auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-    // GQA: G = H/Hkv query heads share a KV head; a pair's Q tile holds G*T
-    // rows (M = 64 or 128), so G must divide M and G*T fit in it
+    // GQA: G = H/Hkv query heads share a KV head; a pair's Q rows are its G*T
+    // (node, head) rows in M-row blocks (M = 64 or 128; G*T > 128: two blocks
+    // of 128 on a CTA pair), so G must divide M and G*T <= 256
     const int G = a->Hkv > 0 && a->H % a->Hkv == 0 ? a->H / a->Hkv : 0;
     const int M = (int64_t)G * a->T <= 64 ? 64 : 128;
     return (a->dtype == ST_F16 || a->dtype == ST_BF16) && a->D == HD && G >= 1 && M % G == 0 &&
-           (int64_t)G * a->T <= 128 && a->W <= 2 && a->Lmax < (1ll << 31) && al(a->q) && al(a->k_cache) &&
+           (int64_t)G * a->T <= 256 && a->W <= 4 && a->Lmax < (1ll << 31) && al(a->q) && al(a->k_cache) &&
            al(a->v_cache) && al(a->o) && al(a->k_tree) && al(a->v_tree) &&
            (int64_t)a->B * a->Hkv * ((a->Lmax + BN - 1) / BN) < (1ll << 31);  // 32-bit tile indices
 }
@@ -1108,16 +1143,16 @@ size_t tree_attention_tc_workspace(const st_attn_args* a) {
 // pair's head CTA waits for flags the piece CTAs release, so the grid (one CTA
 // per SM) is launched cooperatively — co-residency guaranteed by the runtime,
 // not assumed (ST_K1_COOP=0 turns it off for A/B runs).
-#define ST_TRY_LAUNCH_TC(TT, MM)                                                                \
+#define ST_TRY_LAUNCH_TC(TT, MM, MW)                                                            \
     do {                                                                                        \
         static bool attr = false;                                                               \
         if (!attr) {                                                                            \
-            ST_CUDA_TRY(cudaFuncSetAttribute(tree_attn_tc_kernel<TT, MM>,                       \
+            ST_CUDA_TRY(cudaFuncSetAttribute(tree_attn_tc_kernel<TT, MM, MW>,                   \
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,       \
                                              Cfg<MM>::SMEM_BYTES));                             \
             attr = true;                                                                        \
         }                                                                                       \
-        ST_CUDA_TRY(launch_pdl_ex(tree_attn_tc_kernel<TT, MM>, dim3(G), dim3(Cfg<MM>::THREADS),  \
+        ST_CUDA_TRY(launch_pdl_ex(tree_attn_tc_kernel<TT, MM, MW>, dim3(G), dim3(Cfg<MM>::THREADS), \
                                   Cfg<MM>::SMEM_BYTES, stream, coop, tq, tk, tv, tkt, tvt, prm)); \
     } while (0)
 
@@ -1158,7 +1193,8 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
             return ST_ERR_CUDA;
         }
     }
-    const int G = num_sms() < kMaxPieces + 1 ? num_sms() : kMaxPieces + 1;
+    const int R = (int64_t)(a->H / a->Hkv) * a->T <= 128 ? 1 : 2;   // row blocks per pair
+    const int G = (num_sms() < kMaxPieces + 1 ? num_sms() : kMaxPieces + 1) / R * R;
     TcParams prm;
     prm.prefix_len = a->prefix_len;
     prm.n_nodes = a->n_nodes;
@@ -1173,6 +1209,7 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
     prm.H = a->Hkv;
     prm.G = a->H / a->Hkv;
     prm.Hq = a->H;
+    prm.R = R;
     prm.tree_src = a->k_tree != nullptr;
     prm.early_kv = a->early_kv != 0;
     prm.W = a->W;
@@ -1197,10 +1234,15 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
     }
     static const bool coop = !(getenv("ST_K1_COOP") && atoi(getenv("ST_K1_COOP")) == 0);
     const bool m64 = (int64_t)prm.G * a->T <= 64;
+    const bool mw4 = a->W > 2;   // T > 128
     if (a->dtype == ST_F16) {
-        if (m64) { ST_TRY_LAUNCH_TC(__half, 64); } else { ST_TRY_LAUNCH_TC(__half, 128); }
+        if (m64) ST_TRY_LAUNCH_TC(__half, 64, 2);
+        else if (!mw4) ST_TRY_LAUNCH_TC(__half, 128, 2);
+        else ST_TRY_LAUNCH_TC(__half, 128, 4);
     } else {
-        if (m64) { ST_TRY_LAUNCH_TC(__nv_bfloat16, 64); } else { ST_TRY_LAUNCH_TC(__nv_bfloat16, 128); }
+        if (m64) ST_TRY_LAUNCH_TC(__nv_bfloat16, 64, 2);
+        else if (!mw4) ST_TRY_LAUNCH_TC(__nv_bfloat16, 128, 2);
+        else ST_TRY_LAUNCH_TC(__nv_bfloat16, 128, 4);
     }
     ST_LAUNCH_CHECK();
     if (prm.trace) {  // diagnostic only: dump CTA 0's pipeline timestamps

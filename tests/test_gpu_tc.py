@@ -331,3 +331,52 @@ def test_tc_small_trees_auto_path(capi, restatement, T, G, dtype):
     assert capi.tree_attention_path(q, kc, kc, mask, Pd, nd) == 2
     out, lse = run_k1(capi, bt, dtype, force_path=0, lse=True)
     check_k1(restatement, bt, out, dtype, lse)
+
+
+@pytest.mark.parametrize("T,G,width,own,dtype,P_range", [
+    (256, 1, 16, False, torch.float16, (50, 3000)),
+    (256, 1, 32, True, torch.float16, (0, 700)),
+    (200, 1, 20, True, torch.bfloat16, (1000, 1300)),
+    (129, 1, 16, False, torch.float16, (127, 129)),
+    (100, 2, 11, True, torch.float16, (300, 2500)),   # G*T = 200: two row blocks
+    (64, 4, 8, False, torch.bfloat16, (0, 900)),      # G*T = 256
+])
+def test_tc_large_trees_two_row_blocks(capi, restatement, T, G, width, own, dtype, P_range):
+    """G*T in (128, 256] (the reference bench's --max-tree-nodes 256,
+    proj/tests/cli_roundtrip.cmake:69-71): each pair's rows are split into two
+    128-row blocks run by a CTA pair over the same KV tiles; up to 4 mask
+    words; k_tree mode with two tree tiles. Checked against the f64
+    restatement with LSE, ragged prefixes and split pairs."""
+    rng = np.random.default_rng(T * 3 + G + int(own))
+    Hkv, B = 3, 5
+    depth = -(-(T - 1) // width)
+    trees = []
+    for _ in range(B):
+        t = restatement.merge(width_depth_seqs(rng, int(rng.integers(0, 500)), 500, width, depth),
+                              1 << 20)
+        trees.append(tuple(a[:T] for a in t))
+    bt = make_batch(restatement, rng, B, G * Hkv, Hkv, 128, trees=trees, T=T, P_range=P_range,
+                    dtype=dtype)
+    assert bt["W"] == (T + 63) // 64
+    dev = "cuda"
+    q = torch.tensor(bt["q"], device=dev).to(dtype)
+    kc = torch.tensor(bt["kc"], device=dev).to(dtype)
+    vc = torch.tensor(bt["vc"], device=dev).to(dtype)
+    mask = torch.tensor(bt["mask"].view(np.int64), device=dev)
+    Pd, nd = torch.tensor(bt["P"], device=dev), torch.tensor(bt["n"], device=dev)
+    assert capi.tree_attention_path(q, kc, vc, mask, Pd, nd) == 2
+    kt = vt = None
+    if own:
+        kt = torch.zeros(B, T, Hkv, 128, dtype=dtype, device=dev)
+        vt = torch.zeros_like(kt)
+        for b in range(B):
+            P, n = int(bt["P"][b]), int(bt["n"][b])
+            kt[b, :n] = kc[b, :, P:P + n].transpose(0, 1)
+            vt[b, :n] = vc[b, :, P:P + n].transpose(0, 1)
+            kc[b, :, P:P + n] = 5.0
+            vc[b, :, P:P + n] = -3.0
+    out = torch.zeros_like(q)
+    lse = torch.zeros((B, G * Hkv, T), dtype=torch.float32, device=dev)
+    capi.tree_attention(q, kc, vc, mask, Pd, nd, out=out, lse=lse, k_tree=kt, v_tree=vt)
+    torch.cuda.synchronize()
+    check_k1(restatement, bt, out, dtype, lse)
