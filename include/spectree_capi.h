@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define ST_ABI_VERSION 3
+#define ST_ABI_VERSION 4
 
 typedef int st_status;
 
@@ -277,6 +277,64 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
                                 const int32_t* prefix_len, const int32_t* n_nodes, void* k_cache,
                                 void* v_cache, int64_t Lmax, float* logits, void* workspace,
                                 size_t workspace_bytes, void* stream);
+
+/* The model's configuration and element type. */
+void st_model_get_config(const st_model* m, st_model_config* out);
+st_dtype st_model_get_dtype(const st_model* m);
+
+/* ------------------------------------------------ device-resident engine ---
+ * The reference's speculative loop (run_speculative, proj/src/engine.cpp:64-141)
+ * for a batch of requests, resident on the device in f16/bf16 (SURVEY.md §8(f)
+ * 3 and 4). Each st_engine_step (no host sync; capturable in a CUDA graph):
+ * the draft model grows every live request's expansion tree <e_1..e_depth>
+ * on the GPU (a masked tree pass per level + a top-e kernel), the LLM verifies
+ * all trees in one tree pass, K3 walks them with budget truncation and the EOS
+ * cut on the device, K2 commits the accepted rows of both caches, and the
+ * accepted tokens are appended to the device sequences. ssm = NULL drafts with
+ * the LLM itself; depth = 0 decodes one token per step (incremental greedy).
+ * Trees are stored level by level (parent[u] < u). */
+typedef struct st_engine st_engine;
+typedef struct {
+    int max_batch;       /* requests */
+    int max_prompt;      /* longest prompt */
+    int depth;           /* draft levels d (0..16) */
+    int expansion[16];   /* e_1..e_d in [1, 8]: children kept per frontier node */
+    int32_t eos;         /* < 0: none */
+} st_engine_config;
+st_status st_engine_create(st_model* llm, st_model* ssm, const st_engine_config* cfg,
+                           st_engine** out);
+void st_engine_destroy(st_engine* e);
+int st_engine_tree_nodes(const st_engine* e);
+/* host prompts (flattened), lengths and token budgets; prefills both models */
+st_status st_engine_start(st_engine* e, int B, const int32_t* prompts, const int32_t* prompt_lens,
+                          const int32_t* budgets, void* stream);
+st_status st_engine_step(st_engine* e, void* stream);
+/* the last step's accepted tokens [B][T+1], lengths [B], done flags [B] (host; syncs) */
+st_status st_engine_read(st_engine* e, int32_t* verified, int32_t* len, int32_t* done,
+                         void* stream);
+/* request b's sequence (prompt + generated) into host out[cap] (syncs) */
+st_status st_engine_sequence(st_engine* e, int b, int32_t* out, int cap, int* n_out,
+                             void* stream);
+
+/* ----------------------------------------------------- NCCL (DP exchange) ---
+ * The data-parallel exchange of the verification step:
+ * requests are partitioned over the ranks, and after each step every rank
+ * all-gathers its requests' accepted tokens + lengths. NCCL is loaded at run
+ * time (libnccl.so.2), so single-GPU users need none. One rank calls
+ * st_comm_get_unique_id and shares the id out of band. */
+typedef struct st_comm st_comm;
+#define ST_COMM_ID_BYTES 128
+st_status st_comm_get_unique_id(uint8_t* id);
+st_status st_comm_init(int nranks, int rank, const uint8_t* id, st_comm** out);
+st_status st_comm_allgather(st_comm* c, const void* send, void* recv, size_t bytes_per_rank,
+                            void* stream);
+/* pack verified [B][T+1] + len [B] into pack [B*(T+2)], all-gather into
+ * gathered [nranks][B*(T+2)] */
+st_status st_comm_gather_accepted(st_comm* c, const int32_t* verified, const int32_t* len, int B,
+                                  int T, int32_t* pack, int32_t* gathered, void* stream);
+int st_comm_size(const st_comm* c);
+int st_comm_rank(const st_comm* c);
+void st_comm_destroy(st_comm* c);
 
 /* --------------------------------------------------------- tree packing ---
  * Device-side ancestor bitmask build: mask[b][u] = mask[b][parent[u]] | bit(u)

@@ -81,6 +81,22 @@ SIGNATURES = {
     "st_tree_attention_allgather": (_I, [C.POINTER(AttnArgs), C.POINTER(PeerOut), _V]),
     "st_peer_signal": (_I, [_V, _I, _I, C.c_uint32, _V]),
     "st_peer_wait": (_I, [_V, _I, C.c_uint32, _V]),
+    "st_model_get_config": (None, [_V, _V]),
+    "st_model_get_dtype": (_I, [_V]),
+    "st_engine_create": (_I, [_V, _V, _V, _V]),
+    "st_engine_destroy": (None, [_V]),
+    "st_engine_tree_nodes": (_I, [_V]),
+    "st_engine_start": (_I, [_V, _I, _V, _V, _V, _V]),
+    "st_engine_step": (_I, [_V, _V]),
+    "st_engine_read": (_I, [_V, _V, _V, _V, _V]),
+    "st_engine_sequence": (_I, [_V, _I, _V, _I, C.POINTER(_I), _V]),
+    "st_comm_get_unique_id": (_I, [_V]),
+    "st_comm_init": (_I, [_I, _I, _V, _V]),
+    "st_comm_allgather": (_I, [_V, _V, _V, _Z, _V]),
+    "st_comm_gather_accepted": (_I, [_V, _V, _V, _I, _I, _V, _V, _V]),
+    "st_comm_size": (_I, [_V]),
+    "st_comm_rank": (_I, [_V]),
+    "st_comm_destroy": (None, [_V]),
 }
 
 
@@ -380,3 +396,104 @@ class DeviceModel:
                                           k_cache.shape[-2], _ptr(logits), _ptr(self._ws),
                                           self._ws.numel(), _stream(stream)))
         return logits
+
+
+# ------------------------------------------------------ device engine ----
+class EngineConfig(C.Structure):
+    _fields_ = [("max_batch", C.c_int), ("max_prompt", C.c_int), ("depth", C.c_int),
+                ("expansion", C.c_int * 16), ("eos", C.c_int32)]
+
+
+class Engine:
+    """The device-resident speculative engine (st_engine_*): drafting with
+    expansion trees on the GPU, LLM tree verification, greedy walk + commit
+    with budgets / EOS on the device. ssm=None drafts with the LLM itself;
+    expansion=() decodes one token per step."""
+
+    def __init__(self, llm: DeviceModel, ssm: DeviceModel | None, max_batch: int, max_prompt: int,
+                 expansion=(), eos: int = -1):
+        cfg = EngineConfig()
+        cfg.max_batch, cfg.max_prompt, cfg.depth, cfg.eos = max_batch, max_prompt, len(expansion), eos
+        for i, e in enumerate(expansion):
+            cfg.expansion[i] = int(e)
+        h = C.c_void_p()
+        check(lib().st_engine_create(llm.handle, ssm.handle if ssm is not None else None,
+                                     C.byref(cfg), C.byref(h)))
+        self.handle, self.llm, self.ssm, self.B = h, llm, ssm, max_batch
+        self.T = int(lib().st_engine_tree_nodes(h))
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib().st_engine_destroy(self.handle)
+            self.handle = None
+
+    def start(self, prompts, budgets, stream=None):
+        import numpy as np
+        flat = np.array([t for p in prompts for t in p], np.int32)
+        lens = np.array([len(p) for p in prompts], np.int32)
+        bud = np.array(budgets, np.int32)
+        p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        check(lib().st_engine_start(self.handle, len(prompts), p(flat), p(lens), p(bud),
+                                    _stream(stream)))
+
+    def step(self, stream=None):
+        check(lib().st_engine_step(self.handle, _stream(stream)))
+
+    def read(self, stream=None):
+        import numpy as np
+        ver = np.zeros((self.B, self.T + 1), np.int32)
+        ln = np.zeros(self.B, np.int32)
+        done = np.zeros(self.B, np.int32)
+        p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        check(lib().st_engine_read(self.handle, p(ver), p(ln), p(done), _stream(stream)))
+        return ver, ln, done
+
+    def sequence(self, b, stream=None):
+        import numpy as np
+        cap = 1 << 16
+        out = np.zeros(cap, np.int32)
+        n = C.c_int(0)
+        check(lib().st_engine_sequence(self.handle, int(b), out.ctypes.data_as(C.c_void_p), cap,
+                                       C.byref(n), _stream(stream)))
+        return out[: n.value].tolist()
+
+    def run(self, prompts, budgets, max_steps=100000, stream=None):
+        """Generate until every request is done; returns (sequences, steps)."""
+        self.start(prompts, budgets, stream)
+        steps = 0
+        while steps < max_steps:
+            self.step(stream)
+            steps += 1
+            _, _, done = self.read(stream)
+            if done[: len(prompts)].all():
+                break
+        return [self.sequence(b, stream) for b in range(len(prompts))], steps
+
+
+# ------------------------------------------------------------ NCCL comm ----
+class Comm:
+    """st_comm_*: NCCL communicator of the C-ABI (DP exchange of accepted tokens)."""
+
+    def __init__(self, nranks: int, rank: int, unique_id: bytes):
+        assert len(unique_id) == 128
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        check(lib().st_comm_init(int(nranks), int(rank), buf, C.byref(h)))
+        self.handle = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib().st_comm_get_unique_id(buf))
+        return bytes(buf)
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib().st_comm_destroy(self.handle)
+            self.handle = None
+
+    def gather_accepted(self, verified, length, pack, gathered, stream=None):
+        B, T1 = verified.shape
+        check(lib().st_comm_gather_accepted(self.handle, _ptr(verified), _ptr(length), B, T1 - 1,
+                                            _ptr(pack), _ptr(gathered), _stream(stream)))
+        return gathered

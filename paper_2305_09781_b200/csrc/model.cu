@@ -364,6 +364,12 @@ void st_model_destroy(st_model* m) {
 
 size_t st_model_param_count(const st_model* m) { return m ? m->elems : 0; }
 
+void st_model_get_config(const st_model* m, st_model_config* out) {
+    if (m && out) *out = m->cfg;
+}
+
+st_dtype st_model_get_dtype(const st_model* m) { return m ? m->dtype : ST_F16; }
+
 size_t st_model_workspace_size(const st_model* m, int B, int T) {
     if (!m) return 0;
     const size_t rows = (size_t)B * T, d = m->cfg.d_model, F = (size_t)m->cfg.ffn_mult * d;
