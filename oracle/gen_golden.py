@@ -214,10 +214,33 @@ def drafts(R):
         f.write("\n".join(lines) + "\n")
 
 
+def engine_c1(R):
+    """Reference engine run on the C1 model shape for the f16 device engine:
+    run_incremental and run_speculative (self-drafting, b=1, d=4), plus the
+    reference's f64 top-2 logit gap at every generated position (the device
+    engine is f16: positions whose f64 gap is within f16 noise are not
+    comparable). Seed 14 was picked (scan of seeds 1-59) because all 24
+    generated positions keep a gap >= 5e-3 — reference-recipe models have very
+    flat logits (gaps ~1e-2)."""
+    cfg, seed, prompt = (2, 4, 256, 258, 256, 4), 14, np.array([5, 9, 2, 7, 4], np.int32)
+    inc, inc_steps = R.run_incremental(cfg, seed, prompt, 24)
+    spec, spec_steps = R.run_speculative_self(cfg, seed, prompt, 24, 1, 4)
+    gaps = []
+    for i in range(len(prompt), len(inc)):
+        t = np.sort(R.per_path_logits(cfg, seed, inc[:i], []))[-2:]
+        gaps.append(t[1] - t[0])
+    np.savez_compressed(os.path.join(GOLDEN, "engine_c1.npz"), cfg=np.array(cfg), seed=seed,
+                        prompt=prompt, incremental=inc, speculative=spec,
+                        incremental_steps=inc_steps, speculative_steps=spec_steps,
+                        gaps=np.array(gaps))
+
+
 def main():
-    if len(sys.argv) > 1 and sys.argv[1] == "drafts":   # only the draft fixtures
+    if len(sys.argv) > 1 and sys.argv[1] == "drafts":   # only the round-2 fixtures
         build(ref=True)
-        drafts(Reference())
+        R = Reference()
+        drafts(R)
+        engine_c1(R)
         return
     build(ref=True)
     R = Reference()
@@ -285,6 +308,7 @@ def main():
         f.write(f"{len(inc)} " + " ".join(map(str, inc.tolist())) + "\n")
         f.write(f"{inc_steps} {spec_steps}\n")
     drafts(R)
+    engine_c1(R)
     print("golden fixtures written to", GOLDEN)
     for f in sorted(os.listdir(GOLDEN)):
         print(f"  {f}: {os.path.getsize(os.path.join(GOLDEN, f))} bytes")

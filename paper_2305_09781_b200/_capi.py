@@ -368,7 +368,10 @@ class DeviceModel:
 
     def __del__(self):
         if getattr(self, "handle", None):
-            lib().st_model_destroy(self.handle)
+            try:
+                lib().st_model_destroy(self.handle)
+            except TypeError:   # interpreter shutdown: module globals already cleared
+                pass
             self.handle = None
 
     @property
@@ -424,7 +427,10 @@ class Engine:
 
     def __del__(self):
         if getattr(self, "handle", None):
-            lib().st_engine_destroy(self.handle)
+            try:
+                lib().st_engine_destroy(self.handle)
+            except TypeError:   # interpreter shutdown
+                pass
             self.handle = None
 
     def start(self, prompts, budgets, stream=None):
@@ -489,7 +495,10 @@ class Comm:
 
     def __del__(self):
         if getattr(self, "handle", None):
-            lib().st_comm_destroy(self.handle)
+            try:
+                lib().st_comm_destroy(self.handle)
+            except TypeError:   # interpreter shutdown
+                pass
             self.handle = None
 
     def gather_accepted(self, verified, length, pack, gathered, stream=None):
