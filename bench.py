@@ -335,6 +335,18 @@ class VerifyStep:
         self.k1(a)
         self.post(a)
 
+    def plan(self, a=None):
+        """The same step as a native plan (st_verify_plan: the four launches
+        issued by C++ with programmatic dependent launch; consecutive runs
+        chain across steps, K1's tensor maps encoded once)."""
+        qq, kn, vn, tk, pr, nd = a or self.resident
+        return self.capi.VerifyPlan(qq, self.kc, self.vc, self.mask, self.P, nd, self.out,
+                                    self.ws_attn, tk, pr, self.logits, self.ws_ver, *self.vout,
+                                    k_tree=kn if self.own else None,
+                                    v_tree=vn if self.own else None,
+                                    k_new=None if self.own else kn,
+                                    v_new=None if self.own else vn, early_kv=True)
+
     def k1_bytes(self, s=2):
         """Algorithmic K1 bytes per launch."""
         B_, T_, H_, D_, L_ = self.B, self.T, self.H, self.D, self.L
@@ -481,9 +493,10 @@ class DPRunner:
     step of a rank needs only its own requests' results). The step's packed
     results are double-buffered so the exchange never races the next step."""
 
-    def __init__(self, step, world, dev, k1_events=False):
+    def __init__(self, step, world, dev, native=True):
         import torch
         self.torch = torch
+        self.native = native
         self.s, self.world = step, world
         Bs, Ts = step.B, step.T
         n = Bs * (Ts + 2)
@@ -511,6 +524,10 @@ class DPRunner:
                 self.s.run()
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
+        if self.native:
+            self.plan = self.s.plan()
+            self.plan.run()
+            torch.cuda.synchronize()
         for slot in range(2):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
@@ -537,9 +554,14 @@ class DPRunner:
         cur = torch.cuda.current_stream()
         if self.world > 1:
             cur.wait_event(self.ev_sent[slot])   # step i-2's exchange has read send[slot]
-        (graph or self.graphs[slot]).replay()
-        if graph is not None:
-            self._pack(slot)
+        if graph is None and self.native:
+            self.plan.run()
+            if self.world > 1:
+                self._pack(slot)
+        else:
+            (graph or self.graphs[slot]).replay()
+            if graph is not None:
+                self._pack(slot)
         if self.world > 1:
             import torch.distributed as dist
             self.ev_ready[slot].record(cur)
@@ -669,6 +691,9 @@ def run_verify(args):
         runner.sync()
         torch.cuda.synchronize()
     ms = time_steps(runner, args.steps, barrier)
+    runner.native = False   # the same step as one CUDA-graph replay per step (reported)
+    ms_graph = time_steps(runner, args.steps, barrier)
+    runner.native = True
     # K1 inside the step: the same K steps again from the graph whose timing
     # events bracket K1 on the launching stream
     k1_events = []
@@ -684,7 +709,7 @@ def run_verify(args):
     barrier()
     clk = clocks.stop()
     k1_ms = statistics.mean(k1_events)
-    ms, k1_ms, k1_b2b_ms = max_over_ranks(world, dev, ms, k1_ms, k1_b2b_ms)
+    ms, k1_ms, k1_b2b_ms, ms_graph = max_over_ranks(world, dev, ms, k1_ms, k1_b2b_ms, ms_graph)
     ms_step = ms / args.steps
     value = Bq * Tq * world / (ms_step / 1e3)
     # this step's results vs the oracle (greedy verify, bit-exact) — rank 0 checks
@@ -759,9 +784,12 @@ def run_verify(args):
                    "parallelism": f"dp{world} (requests partitioned)",
                    "l2": f"inputs larger than L2: {kvmb:.0f} MB KV + {Bq * Tq * V * 4 / 1e6:.1f} MB "
                          f"logits per step",
-                   "timing": "value: K replays of one CUDA graph holding the whole step (N>1: "
-                             "+ the accepted-token all-gather on a side stream, overlapping the "
-                             "next step); roofline: K replays of a graph of 8 back-to-back K1 "
+                   "timing": "value: K steps, each one st_verify_plan_run (the step's four "
+                             "launches issued natively with programmatic dependent launch, "
+                             "chaining across steps; N>1: + the accepted-token all-gather on a "
+                             "side stream, overlapping the next step), CUDA events around the K "
+                             "steps; graph_ms_per_step: the same step as one CUDA-graph replay "
+                             "per step; roofline: K replays of a graph of 8 back-to-back K1 "
                              "launches alternating between two KV/Q copies (> L2), CUDA events "
                              "around the replays; in-step bracket (event graph nodes around K1 "
                              "inside the step) reported beside it",
@@ -780,6 +808,7 @@ def run_verify(args):
         "clocks": clk,
         "parity": parity,
         "strong": strong,
+        "graph_ms_per_step": ms_graph / args.steps,
         "verify_steps_per_s": 1e3 / ms_step,
         "node_evals_per_s": value,
         "verified_tokens_per_step": parity["accepted_tokens"] if parity else None,
@@ -837,13 +866,7 @@ def run_e2e(args, step, runner, world, dev, barrier, numa_cpus):
     for st in sets:   # warm + capture one full-step graph per input set
         st[6].copy_(h_topo)
         st[0].copy_(h_q), st[1].copy_(h_k), st[2].copy_(h_v)
-    e2e_graphs = []
-    for st in sets:
-        g_ = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_):
-            step.run(st[:6])
-            runner._pack(0)
-        e2e_graphs.append(g_)
+    plans = [step.plan(st[:6]) for st in sets]   # one prepared step per input set
     cur = torch.cuda.current_stream()
 
     def issue_copy(i, merge=True):
@@ -862,13 +885,16 @@ def run_e2e(args, step, runner, world, dev, barrier, numa_cpus):
 
     def issue_compute(i):
         cur.wait_event(ev_copied[i % 2])
-        e2e_graphs[i % 2].replay()
+        plans[i % 2].run()
         ev_free[i % 2].record(cur)
         if world > 1:   # DP exchange, synchronous here: the host reads the gathered result
             import torch.distributed as dist
+            runner._pack(0)
             dist.all_gather_into_tensor(runner.gathered[0], runner.send[0])
-        h_outs[i % 2].copy_(runner.gathered[0][: h_outs[0].numel()] if world > 1
-                            else runner.send[0][: h_outs[0].numel()], non_blocking=True)
+            h_outs[i % 2].copy_(runner.gathered[0][: h_outs[0].numel()], non_blocking=True)
+        else:
+            h_outs[i % 2][: Bq * (Tq + 1)].copy_(step.vout[0].view(-1), non_blocking=True)
+            h_outs[i % 2][Bq * (Tq + 1):].copy_(step.vout[2], non_blocking=True)
         ev_out[i % 2].record(cur)
 
     def read_result(i):

@@ -278,6 +278,37 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
                                 void* v_cache, int64_t Lmax, float* logits, void* workspace,
                                 size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------- verification step plan ---
+ * One verification step of a batch as a prepared object:
+ * ancestor masks -> K1 -> K3 argmax -> K3 walk + K2 commit, from the tree's
+ * own K/V rows (attn.k_tree/v_tree) or, with k_tree == NULL, after a K2 append
+ * of k_new/v_new into the cache. st_verify_plan_run issues the four launches
+ * with programmatic dependent launch, so back-to-back steps chain without a
+ * boundary; K1's tensor maps are encoded once at creation. attn.mask is the
+ * plan's mask buffer [B][T][W] (written by every run); attn.early_kv may be
+ * set (the masks / append kernel before K1 honours the transitivity rule).
+ * All pointers stay fixed for the plan's lifetime (their contents may change). */
+typedef struct st_verify_plan st_verify_plan;
+typedef struct {
+    st_attn_args attn;
+    const int32_t* tokens;       /* [B][T] */
+    const int32_t* parent;       /* [B][T] */
+    const float* logits;         /* [B][T][V] */
+    int V;
+    const int32_t* budget;       /* optional [B] */
+    int32_t eos;                 /* < 0: none */
+    int32_t* verified;           /* [B][T+1] */
+    int32_t* ids;                /* [B][T+1] */
+    int32_t* len;                /* [B] */
+    void* verify_workspace;      /* st_verify_workspace_size(B, T) bytes, zeroed once */
+    int32_t* new_prefix_len;     /* optional [B]: P + len */
+    const void* k_new;           /* cache mode only: [B][T][Hkv][D] rows to append */
+    const void* v_new;
+} st_verify_step_desc;
+st_status st_verify_plan_create(const st_verify_step_desc* d, st_verify_plan** out);
+st_status st_verify_plan_run(st_verify_plan* p, void* stream);
+void st_verify_plan_destroy(st_verify_plan* p);
+
 /* The model's configuration and element type. */
 void st_model_get_config(const st_model* m, st_model_config* out);
 st_dtype st_model_get_dtype(const st_model* m);

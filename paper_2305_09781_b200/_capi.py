@@ -97,6 +97,9 @@ SIGNATURES = {
     "st_comm_size": (_I, [_V]),
     "st_comm_rank": (_I, [_V]),
     "st_comm_destroy": (None, [_V]),
+    "st_verify_plan_create": (_I, [_V, _V]),
+    "st_verify_plan_run": (_I, [_V, _V]),
+    "st_verify_plan_destroy": (None, [_V]),
 }
 
 
@@ -506,3 +509,54 @@ class Comm:
         check(lib().st_comm_gather_accepted(self.handle, _ptr(verified), _ptr(length), B, T1 - 1,
                                             _ptr(pack), _ptr(gathered), _stream(stream)))
         return gathered
+
+
+# ------------------------------------------------- verification step plan ----
+class StepDesc(C.Structure):
+    _fields_ = [("attn", AttnArgs), ("tokens", C.c_void_p), ("parent", C.c_void_p),
+                ("logits", C.c_void_p), ("V", C.c_int), ("budget", C.c_void_p), ("eos", C.c_int32),
+                ("verified", C.c_void_p), ("ids", C.c_void_p), ("len", C.c_void_p),
+                ("verify_workspace", C.c_void_p), ("new_prefix_len", C.c_void_p),
+                ("k_new", C.c_void_p), ("v_new", C.c_void_p)]
+
+
+class VerifyPlan:
+    """st_verify_plan_*: one verification step (masks -> K1 -> argmax -> walk +
+    commit) prepared once and re-launched; consecutive runs chain with
+    programmatic dependent launch. Holds references to every tensor it uses."""
+
+    def __init__(self, q, k_cache, v_cache, mask, prefix_len, n_nodes, out, workspace, tokens,
+                 parent, logits, verify_ws, verified, ids, length, k_tree=None, v_tree=None,
+                 k_new=None, v_new=None, early_kv=True, budget=None, eos=-1, new_prefix_len=None):
+        self._keep = [q, k_cache, v_cache, mask, prefix_len, n_nodes, out, workspace, tokens, parent,
+                      logits, verify_ws, verified, ids, length, k_tree, v_tree, k_new, v_new,
+                      budget, new_prefix_len]
+        d = StepDesc()
+        d.attn = attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, workspace=workspace,
+                           k_tree=k_tree, v_tree=v_tree, early_kv=early_kv)
+        d.tokens, d.parent, d.logits = tokens.data_ptr(), parent.data_ptr(), logits.data_ptr()
+        d.V = logits.shape[-1]
+        d.budget = budget.data_ptr() if budget is not None else None
+        d.eos = int(eos)
+        d.verified, d.ids, d.len = verified.data_ptr(), ids.data_ptr(), length.data_ptr()
+        d.verify_workspace = verify_ws.data_ptr()
+        d.new_prefix_len = new_prefix_len.data_ptr() if new_prefix_len is not None else None
+        d.k_new = k_new.data_ptr() if k_new is not None else None
+        d.v_new = v_new.data_ptr() if v_new is not None else None
+        h = C.c_void_p()
+        check(lib().st_verify_plan_create(C.byref(d), C.byref(h)))
+        self.handle = h
+        self._run = lib().st_verify_plan_run
+
+    def run(self, stream=None):
+        st = self._run(self.handle, _stream(stream))
+        if st != 0:
+            check(st)
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            try:
+                lib().st_verify_plan_destroy(self.handle)
+            except TypeError:   # interpreter shutdown
+                pass
+            self.handle = None

@@ -115,31 +115,7 @@ template <int M> struct Cfg {
     static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
-struct TcParams {
-    const int32_t* prefix_len;
-    const int32_t* n_nodes;
-    const uint64_t* mask;
-    void* o;
-    float* lse;
-    float* partial;      // [gridDim.x][SLOT_FLOATS]: the piece a CTA's first segment leaves
-    unsigned* flags;     // [gridDim.x]: 1 while that piece is published and not yet merged
-    int B, T, H, W;      // H: KV heads (one (b, h) pair per request and KV head)
-    int G, Hq;           // query heads per KV head (GQA group), query heads = G * H
-    int R;               // row blocks per pair: G*T <= 128 -> 1; <= 256 -> 2 (CTAs 2s, 2s+1
-                         // take the two 128-row blocks of schedule slot s)
-    int tree_src;        // tree rows come from k_tree/v_tree: one extra tile after ceil(P/BN)
-    int early_kv;        // st_attn_args.early_kv: stream committed KV before griddepcontrol.wait
-    float c_log2;        // scale * log2(e)
-    float scale;
-    unsigned long long* trace;  // optional pipeline trace of CTA 0 (ST_K1_TRACE)
-    int aligned_slack;          // whole-pair schedule allowed within this many tiles of stream-K
-    int head_extra;             // split schedule: extra tiles for each pair's head piece
-    int trace_cta;              // CTA whose per-tile pipeline is traced (ST_K1_TRACE_CTA)
-    // head-sharded output (st_tree_attention_allgather): rows go to every rank's
-    // [B][T][H_out][D] buffer at head head_offset + h; null -> o with H_out = H
-    void* const* o_peers;
-    int world, head_offset, H_out;
-};
+// TcParams: tree_attn.h
 
 constexpr int kTraceCta = 12;   // per-CTA globaltimer/clock slots of the ST_K1_TRACE dump
 constexpr int kTraceRows = 16;  // per-tile (rows 0-11) and per-segment (12-15) clock rows
@@ -1138,35 +1114,40 @@ size_t tree_attention_tc_workspace(const st_attn_args* a) {
            (size_t)num_sms() * sizeof(unsigned);
 }
 
+namespace {
+
 // K1 is launched with programmatic dependent launch (common.cuh): its prologue
 // overlaps the previous kernel's tail. Split pairs are merged inside K1: a
 // pair's head CTA waits for flags the piece CTAs release, so the grid (one CTA
 // per SM) is launched cooperatively — co-residency guaranteed by the runtime,
 // not assumed (ST_K1_COOP=0 turns it off for A/B runs).
-#define ST_TRY_LAUNCH_TC(TT, MM, MW)                                                            \
-    do {                                                                                        \
-        static bool attr = false;                                                               \
-        if (!attr) {                                                                            \
-            ST_CUDA_TRY(cudaFuncSetAttribute(tree_attn_tc_kernel<TT, MM, MW>,                   \
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,       \
-                                             Cfg<MM>::SMEM_BYTES));                             \
-            attr = true;                                                                        \
-        }                                                                                       \
-        ST_CUDA_TRY(launch_pdl_ex(tree_attn_tc_kernel<TT, MM, MW>, dim3(G), dim3(Cfg<MM>::THREADS), \
-                                  Cfg<MM>::SMEM_BYTES, stream, coop, tq, tk, tv, tkt, tvt, prm)); \
-    } while (0)
+template <class TT, int MM, int MW>
+st_status launch_tc(const TcLaunch& L, cudaStream_t stream) {
+    static bool attr = false;
+    if (!attr) {
+        ST_CUDA_TRY(cudaFuncSetAttribute(tree_attn_tc_kernel<TT, MM, MW>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg<MM>::SMEM_BYTES));
+        attr = true;
+    }
+    ST_CUDA_TRY(launch_pdl_ex(tree_attn_tc_kernel<TT, MM, MW>, dim3(L.grid), dim3(Cfg<MM>::THREADS),
+                              Cfg<MM>::SMEM_BYTES, stream, L.coop, L.tq, L.tk, L.tv, L.tkt, L.tvt,
+                              L.prm));
+    return ST_OK;
+}
 
-st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st_peer_out* po) {
+}  // namespace
+
+st_status tree_attention_tc_prepare(const st_attn_args* a, const st_peer_out* po, TcLaunch* L) {
     const CUtensorMapDataType dt =
         a->dtype == ST_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-    CUtensorMap tq, tk, tv;
     {
         const uint64_t dims[4] = {(uint64_t)HD, (uint64_t)a->H, (uint64_t)a->T, (uint64_t)a->B};
         const uint64_t strides[3] = {HD * 2ull, (uint64_t)a->H * HD * 2, (uint64_t)a->T * a->H * HD * 2};
         const int G = a->H / a->Hkv;
         const uint32_t M = (int64_t)G * a->T <= 64 ? 64 : 128;
         const uint32_t box[4] = {64, (uint32_t)G, M / G, 1};
-        if (!encode(&tq, dt, 4, a->q, dims, strides, box)) {
+        if (!encode(&L->tq, dt, 4, a->q, dims, strides, box)) {
             set_error("st_tree_attention: cuTensorMapEncodeTiled(q) failed");
             return ST_ERR_CUDA;
         }
@@ -1175,27 +1156,28 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
         const uint64_t dims[3] = {(uint64_t)HD, (uint64_t)a->Lmax, (uint64_t)a->B * a->Hkv};
         const uint64_t strides[2] = {HD * 2ull, (uint64_t)a->Lmax * HD * 2};
         const uint32_t box[3] = {64, BN, 1};
-        if (!encode(&tk, dt, 3, a->k_cache, dims, strides, box) ||
-            !encode(&tv, dt, 3, a->v_cache, dims, strides, box)) {
+        if (!encode(&L->tk, dt, 3, a->k_cache, dims, strides, box) ||
+            !encode(&L->tv, dt, 3, a->v_cache, dims, strides, box)) {
             set_error("st_tree_attention: cuTensorMapEncodeTiled(kv) failed");
             return ST_ERR_CUDA;
         }
     }
-    CUtensorMap tkt = tk, tvt = tv;  // k_tree mode: the tree's rows, [B][T][Hkv][D], 128-node boxes
+    L->tkt = L->tk;  // k_tree mode: the tree's rows, [B][T][Hkv][D], 128-node boxes
+    L->tvt = L->tv;
     if (a->k_tree) {
         const uint64_t dims[4] = {(uint64_t)HD, (uint64_t)a->Hkv, (uint64_t)a->T, (uint64_t)a->B};
         const uint64_t strides[3] = {HD * 2ull, (uint64_t)a->Hkv * HD * 2,
                                      (uint64_t)a->T * a->Hkv * HD * 2};
         const uint32_t box[4] = {64, 1, BN, 1};
-        if (!encode(&tkt, dt, 4, a->k_tree, dims, strides, box) ||
-            !encode(&tvt, dt, 4, a->v_tree, dims, strides, box)) {
+        if (!encode(&L->tkt, dt, 4, a->k_tree, dims, strides, box) ||
+            !encode(&L->tvt, dt, 4, a->v_tree, dims, strides, box)) {
             set_error("st_tree_attention: cuTensorMapEncodeTiled(k_tree/v_tree) failed");
             return ST_ERR_CUDA;
         }
     }
     const int R = (int64_t)(a->H / a->Hkv) * a->T <= 128 ? 1 : 2;   // row blocks per pair
     const int G = (num_sms() < kMaxPieces + 1 ? num_sms() : kMaxPieces + 1) / R * R;
-    TcParams prm;
+    TcParams& prm = L->prm;
     prm.prefix_len = a->prefix_len;
     prm.n_nodes = a->n_nodes;
     prm.mask = a->mask;
@@ -1226,28 +1208,44 @@ st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st
     static const int hx_env = getenv("ST_K1_HEADX") ? atoi(getenv("ST_K1_HEADX")) : (int)kHeadExtra;
     prm.head_extra = hx_env < 0 ? 0 : hx_env;
     prm.trace_cta = getenv("ST_K1_TRACE_CTA") ? atoi(getenv("ST_K1_TRACE_CTA")) : 0;
+    static const bool coop = !(getenv("ST_K1_COOP") && atoi(getenv("ST_K1_COOP")) == 0);
+    L->coop = coop;
+    L->grid = G;
+    L->m64 = (int64_t)prm.G * a->T <= 64;
+    L->mw4 = a->W > 2;   // T > 128
+    L->f16 = a->dtype == ST_F16;
+    return ST_OK;
+}
+
+st_status tree_attention_tc_launch(const TcLaunch& L, cudaStream_t stream) {
+    st_status r;
+    if (L.f16) {
+        r = L.m64 ? launch_tc<__half, 64, 2>(L, stream)
+            : !L.mw4 ? launch_tc<__half, 128, 2>(L, stream) : launch_tc<__half, 128, 4>(L, stream);
+    } else {
+        r = L.m64 ? launch_tc<__nv_bfloat16, 64, 2>(L, stream)
+            : !L.mw4 ? launch_tc<__nv_bfloat16, 128, 2>(L, stream)
+                     : launch_tc<__nv_bfloat16, 128, 4>(L, stream);
+    }
+    if (r != ST_OK) return r;
+    ST_LAUNCH_CHECK();
+    return ST_OK;
+}
+
+st_status tree_attention_tc(const st_attn_args* a, cudaStream_t stream, const st_peer_out* po) {
+    TcLaunch L;
+    if (st_status e = tree_attention_tc_prepare(a, po, &L)) return e;
     static unsigned long long* trace_buf = nullptr;
+    const int G = L.grid;
     if (getenv("ST_K1_TRACE")) {
         if (!trace_buf) cudaMalloc(&trace_buf, (kTraceRows * 64 + kTraceCta * 1024) * sizeof(unsigned long long));
         cudaMemsetAsync(trace_buf, 0, (kTraceRows * 64 + kTraceCta * 1024) * sizeof(unsigned long long), stream);
-        prm.trace = trace_buf;
+        L.prm.trace = trace_buf;
     }
-    static const bool coop = !(getenv("ST_K1_COOP") && atoi(getenv("ST_K1_COOP")) == 0);
-    const bool m64 = (int64_t)prm.G * a->T <= 64;
-    const bool mw4 = a->W > 2;   // T > 128
-    if (a->dtype == ST_F16) {
-        if (m64) ST_TRY_LAUNCH_TC(__half, 64, 2);
-        else if (!mw4) ST_TRY_LAUNCH_TC(__half, 128, 2);
-        else ST_TRY_LAUNCH_TC(__half, 128, 4);
-    } else {
-        if (m64) ST_TRY_LAUNCH_TC(__nv_bfloat16, 64, 2);
-        else if (!mw4) ST_TRY_LAUNCH_TC(__nv_bfloat16, 128, 2);
-        else ST_TRY_LAUNCH_TC(__nv_bfloat16, 128, 4);
-    }
-    ST_LAUNCH_CHECK();
-    if (prm.trace) {  // diagnostic only: dump CTA 0's pipeline timestamps
+    if (st_status e = tree_attention_tc_launch(L, stream)) return e;
+    if (L.prm.trace) {  // diagnostic only: dump CTA 0's pipeline timestamps
         static unsigned long long h[kTraceRows * 64 + kTraceCta * 1024];
-        cudaMemcpyAsync(h, prm.trace, sizeof h, cudaMemcpyDeviceToHost, stream);
+        cudaMemcpyAsync(h, L.prm.trace, sizeof h, cudaMemcpyDeviceToHost, stream);
         cudaStreamSynchronize(stream);
         if (FILE* f = fopen(getenv("ST_K1_TRACE"), "a")) {
             for (int r = 0; r < kTraceRows; ++r) {

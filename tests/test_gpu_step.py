@@ -75,14 +75,16 @@ def worst_err(out, ref):
                for (b, h), r in ref.items())
 
 
-@pytest.mark.parametrize("tree_rows", ["own", "cache"])
-def test_c2_bench_step_full_shape(capi, restatement, tree_rows):
+@pytest.mark.parametrize("tree_rows,native", [("own", True), ("own", False), ("cache", True)])
+def test_c2_bench_step_full_shape(capi, restatement, tree_rows, native):
+    """native: the step as st_verify_plan_run (what bench.py times); else one
+    CUDA-graph replay of the Python-issued launches."""
     import bench
     dev = torch.device("cuda", 0)
     st = bench.VerifyStep(dev, 0, tree_rows=tree_rows)
     assert st.path == 2, "C2 must take the tcgen05 K1 path"
     kc0, vc0 = st.kc.clone(), st.vc.clone()
-    runner = bench.DPRunner(st, 1, dev)
+    runner = bench.DPRunner(st, 1, dev, native=native)
     runner.capture(0)
     # capture() ran the step eagerly 3x: restore the cache, then ONE graph replay
     st.kc.copy_(kc0)

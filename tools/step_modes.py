@@ -44,6 +44,25 @@ def timed(fn, reps):
     return e0.elapsed_time(e1) * 1e3 / reps
 
 
+# variant: no masks kernel in the chain (masks precomputed once), K1 right after
+# the previous step's commit (early_kv off: that commit writes committed rows)
+st.capi.build_masks(st.par, st.nn, W=st.W, out=st.mask)
+
+
+def run_nomask():
+    a = st.resident
+    st.capi.tree_attention(st.q, st.kc, st.vc, st.mask, st.P, st.nn, out=st.out,
+                           workspace=st.ws_attn, k_tree=st.knew, v_tree=st.vnew, early_kv=False)
+    st.post(a)
+
+
+gn = torch.cuda.CUDAGraph()
+run_nomask()
+torch.cuda.synchronize()
+with torch.cuda.graph(gn):
+    for _ in range(10):
+        run_nomask()
+
 for rnd in range(2):
     a = timed(g1.replay, 100)
     b = timed(g10.replay, 10) / 10
@@ -51,4 +70,6 @@ for rnd in range(2):
     extra = ""
     if hasattr(st, "run_native"):
         extra = f"  native {timed(st.run_native, 100):6.1f}"
-    print(f"graph/step {a:6.1f} us  graph/10 {b:6.1f} us  eager {c:6.1f} us{extra}")
+    d = timed(gn.replay, 10) / 10
+    print(f"graph/step {a:6.1f} us  graph/10 {b:6.1f} us  eager {c:6.1f} us  "
+          f"graph/10 without masks kernel {d:6.1f} us{extra}")
