@@ -23,7 +23,7 @@ from paper_2305_09781_b200 import _capi  # noqa: E402
 from paper_2305_09781_b200.tree import TokenTree, TreeBatch  # noqa: E402
 
 B, H, D = 16, 32, 128
-WIDTH = {16: 4, 32: 8, 64: 8, 128: 16}
+WIDTH = {16: 4, 32: 8, 64: 8, 128: 16, 256: 16}
 
 
 def trees_of(T, seed):
@@ -51,7 +51,7 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "c5_sweep.json"))
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--Ls", default="4096,8192,16384,32768")
-    ap.add_argument("--Ts", default="16,32,64,128")
+    ap.add_argument("--Ts", default="16,32,64,128,256")
     args = ap.parse_args()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
