@@ -1,5 +1,6 @@
-"""The reference's OWN C++ unit suites (proj/tests/token_tree_test.cpp and
-proj/tests/transformer_test.cpp, compiled unchanged by tests/cpp/Makefile
+"""The reference's OWN C++ unit suites (proj/tests/token_tree_test.cpp,
+proj/tests/transformer_test.cpp and acceptance criteria #2/#3/#4/#7 of
+proj/tests/acceptance_test.cpp, compiled unchanged by tests/cpp/Makefile
 against include/spectree + libspectree_b200.so) and our engine parity test,
 run on the GPU. Tolerances are the reference's own (tokens exact, logits
 <= 1e-9, bitwise where the reference asserts bitwise)."""
@@ -14,7 +15,8 @@ BIN = os.path.join(ROOT, "build", "reftests")
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name", ["token_tree_test", "transformer_test", "engine_parity_test"])
+@pytest.mark.parametrize("name", ["token_tree_test", "transformer_test", "engine_parity_test",
+                                  "acceptance_subset_test"])
 def test_suite(name):
     import torch
     if not torch.cuda.is_available():
@@ -25,4 +27,8 @@ def test_suite(name):
     r = subprocess.run([path], capture_output=True, text=True, timeout=900)
     print(r.stdout[-4000:])
     assert r.returncode == 0, r.stdout[-6000:] + r.stderr[-2000:]
-    assert "failed: 0" in r.stdout
+    if name == "acceptance_subset_test":   # reference acceptance criteria #2, #3, #4, #7
+        assert "acceptance subset: 0 failed" in r.stdout
+        assert r.stdout.count("[PASS]") == 4
+    else:
+        assert "failed: 0" in r.stdout

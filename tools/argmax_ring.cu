@@ -130,6 +130,60 @@ __global__ void __launch_bounds__(NT + 32) argmax_ring(const float* __restrict__
     }
 }
 
+
+// Equal-share single wave: G blocks (resident all at once), block c scans the
+// contiguous float4 range [c*N/G, (c+1)*N/G) of the flattened [rows][V/4]
+// logits; a range spans a few rows, and the block writes one key per row
+// piece into keys[row][slot], slot = c - first block touching the row.
+template <int NT, int UNR>
+__global__ void __launch_bounds__(NT) argmax_share(const float* __restrict__ logits, int rows, int V,
+                                                   unsigned long long* keys) {
+    const int nv = V >> 2;
+    const long long N = (long long)rows * nv;
+    const long long lo = (long long)blockIdx.x * N / gridDim.x;
+    const long long hi = (long long)(blockIdx.x + 1) * N / gridDim.x;
+    const float4* r4 = reinterpret_cast<const float4*>(logits);
+    __shared__ unsigned long long red[NT / 32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (long long a = lo; a < hi;) {
+        const int row = (int)(a / nv);
+        const long long rend = min(hi, (long long)(row + 1) * nv);
+        float bv = -INFINITY;
+        int bi = -1;
+        for (long long base = a + threadIdx.x; base < rend; base += (long long)NT * UNR) {
+            float4 x[UNR];
+#pragma unroll
+            for (int k = 0; k < UNR; ++k) {
+                const long long j = base + (long long)k * NT;
+                x[k] = j < rend ? __ldcs(r4 + j) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+            }
+#pragma unroll
+            for (int k = 0; k < UNR; ++k) {
+                const long long j = base + (long long)k * NT;
+                if (j >= rend) continue;
+                const int e = (int)(j - (long long)row * nv) * 4;
+                if (bi < 0) { bv = x[k].x; bi = e; }
+                else if (x[k].x > bv) { bv = x[k].x; bi = e; }
+                if (x[k].y > bv) { bv = x[k].y; bi = e + 1; }
+                if (x[k].z > bv) { bv = x[k].z; bi = e + 2; }
+                if (x[k].w > bv) { bv = x[k].w; bi = e + 3; }
+            }
+        }
+        unsigned long long best = bi >= 0 ? arg_key(bv, bi) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+        if (lane == 0) red[warp] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int w = 1; w < NT / 32; ++w) best = max(best, red[w]);
+            const long long first = ((long long)row * nv * gridDim.x) / N;  // first block touching row
+            keys[(long long)row * 8 + (blockIdx.x - first)] = best;
+        }
+        __syncthreads();
+        a = rend;
+    }
+}
+
 template <class F>
 double timeit(F&& launch, int iters = 60) {
     for (int i = 0; i < 6; ++i) launch(i);
@@ -175,6 +229,27 @@ void ring(float* const* bufs, unsigned long long* keys, unsigned long long* ref,
            cudaGetErrorString(cudaGetLastError()));
 }
 
+template <int NT, int UNR>
+void share(float* const* bufs, unsigned long long* keys, unsigned long long* ref, int rows, int V, int G) {
+    const double us = timeit([&](int i) { argmax_share<NT, UNR><<<G, NT>>>(bufs[i % 3], rows, V, keys); });
+    cudaMemset(keys, 0, (size_t)rows * 8 * 8);
+    argmax_share<NT, UNR><<<G, NT>>>(bufs[0], rows, V, keys);
+    static unsigned long long h[8 * 64 * 8], r[8 * 64 * 8];
+    cudaMemcpy(h, keys, sizeof h, cudaMemcpyDeviceToHost);
+    cudaMemcpy(r, ref, sizeof r, cudaMemcpyDeviceToHost);
+    int bad = 0;
+    for (int row = 0; row < rows; ++row) {
+        unsigned long long a = 0, b = 0;
+        for (int j = 0; j < 8; ++j) {
+            a = a > h[row * 8 + j] ? a : h[row * 8 + j];
+            b = b > r[row * 8 + j] ? b : r[row * 8 + j];
+        }
+        bad += a != b;
+    }
+    printf("share NT %3d unroll %d blocks %5d: %7.2f us  %6.0f GB/s  bad %d  (%s)\n", NT, UNR, G, us,
+           4.0 * rows * V / us / 1e3, bad, cudaGetErrorString(cudaGetLastError()));
+}
+
 __global__ void fill(float* p, size_t n, unsigned seed) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         unsigned x = (unsigned)i * 2654435761u ^ seed;
@@ -201,6 +276,12 @@ int main() {
         const double us = timeit([&](int i) { argmax_grid<<<dim3(8, T, B), 256>>>(bufs[i % 3], T, V, ref); });
         printf("grid (8 x T x B) x 256: %7.2f us  %6.0f GB/s\n", us, 4.0 * rows * V / us / 1e3);
         argmax_grid<<<dim3(8, T, B), 256>>>(bufs[0], T, V, ref);
+        share<256, 4>(bufs, keys, ref, rows, V, nsm * 8);
+        share<256, 8>(bufs, keys, ref, rows, V, nsm * 8);
+        share<512, 4>(bufs, keys, ref, rows, V, nsm * 4);
+        share<256, 4>(bufs, keys, ref, rows, V, nsm * 16);
+        share<128, 8>(bufs, keys, ref, rows, V, nsm * 16);
+        share<256, 2>(bufs, keys, ref, rows, V, nsm * 8);
         ring<256, 4>(bufs, keys, ref, rows, V, 4, 1, nsm);
         ring<256, 6>(bufs, keys, ref, rows, V, 4, 1, nsm);
         ring<512, 6>(bufs, keys, ref, rows, V, 4, 1, nsm);
