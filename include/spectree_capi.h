@@ -309,6 +309,17 @@ st_status st_verify_plan_create(const st_verify_step_desc* d, st_verify_plan** o
 st_status st_verify_plan_run(st_verify_plan* p, void* stream);
 void st_verify_plan_destroy(st_verify_plan* p);
 
+/* ------------------------------------------------------- around-path GEMM ---
+ * The device decoder's projections: C[z] (op)= A · W[z] on
+ * the tcgen05 tensor cores, fp32 accumulate, the decoder's elementwise work
+ * fused into the epilogue. A [M][lda] row-major, W [Z][K][ldw] row-major (the
+ * stored weight layout), C [Z][M][ldc] (c_stride_z elements apart); f16/bf16
+ * in; C f16/bf16, or f32 for ST_GEMM_STORE_F32. lda, ldw multiples of 8. */
+enum { ST_GEMM_STORE = 0, ST_GEMM_GELU = 1, ST_GEMM_ADD_TO = 2, ST_GEMM_STORE_F32 = 3 };
+st_status st_gemm(st_dtype dtype, int M, int N, int K, int Z, const void* A, int lda,
+                  const void* W, int ldw, void* C, int ldc, int64_t c_stride_z, int epilogue,
+                  void* stream);
+
 /* The model's configuration and element type. */
 void st_model_get_config(const st_model* m, st_model_config* out);
 st_dtype st_model_get_dtype(const st_model* m);

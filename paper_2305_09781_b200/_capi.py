@@ -100,6 +100,7 @@ SIGNATURES = {
     "st_verify_plan_create": (_I, [_V, _V]),
     "st_verify_plan_run": (_I, [_V, _V]),
     "st_verify_plan_destroy": (None, [_V]),
+    "st_gemm": (_I, [_I, _I, _I, _I, _I, _V, _I, _V, _I, _V, _I, _I64, _I, _V]),
 }
 
 
@@ -560,3 +561,23 @@ class VerifyPlan:
             except TypeError:   # interpreter shutdown
                 pass
             self.handle = None
+
+
+# ------------------------------------------------------------- GEMM ----
+GEMM_EPI = {"store": 0, "gelu": 1, "add_to": 2, "store_f32": 3}
+
+
+def gemm(a, w, out=None, epilogue="store", stream=None):
+    """C (op)= A @ W on the tcgen05 GEMM (st_gemm). a [M][K]; w [K][N] or
+    [Z][K][N]; out [M][N] / [Z][M][N] (f32 for epilogue="store_f32")."""
+    M, K = a.shape
+    Z = 1 if w.dim() == 2 else w.shape[0]
+    N = w.shape[-1]
+    if out is None:
+        dt = torch.float32 if epilogue == "store_f32" else a.dtype
+        out = torch.empty((M, N) if w.dim() == 2 else (Z, M, N), dtype=dt, device=a.device)
+    check(lib().st_gemm(DTYPES[a.dtype], M, N, K, Z, _ptr(a), a.stride(0), _ptr(w), w.stride(-2),
+                        _ptr(out),
+                        out.stride(-2), (M * out.stride(-2)) if Z > 1 else 0, GEMM_EPI[epilogue],
+                        _stream(stream)))
+    return out

@@ -1,0 +1,371 @@
+// Around-path projections of the device decoder: a
+// hand-written sm_100a GEMM, C[z] (op)= A · W[z], on the 5th-gen tensor cores
+// with the decoder's elementwise work fused into the epilogue — the reference
+// runs one f64 matvec per tree node per matrix (proj/src/transformer.cpp:
+// 262-319); here every projection is one GEMM over all B·T tree rows.
+//
+//   A [M][K] row-major f16/bf16 (activations; K-major UMMA operand)
+//   W [Z][K][N] row-major f16/bf16 (weights as stored: MN-major UMMA operand)
+//   C [Z][M][N] (ldc, c_stride_z) f16/bf16 or f32
+//   epilogue: store | GELU (erf form, transformer.cpp:67) | add-to (residual:
+//   C += A·W, the pre-LN blocks' x + ...) | store f32 (LM-head logits)
+//
+// Design: persistent, one CTA per SM over 128 x 256 output tiles (m fastest, so
+// the CTAs working at one time share each W tile through L2); warp roles:
+// a TMA producer (A box 64x128, W as four 64x64 boxes per 64-deep K block,
+// SWIZZLE_128B, 4-stage ring of 48 KB), an MMA issuer (tcgen05.mma kind::f16
+// M=128 N=256 K=16, fp32 accumulators double-buffered in TMEM: 2 x 256
+// columns, so one tile's epilogue overlaps the next tile's MMAs), and four
+// epilogue warps (tcgen05.ld 32 columns at a time -> epilogue op -> 16-byte
+// global stores).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <type_traits>
+
+#include "common.cuh"
+#include "gemm.h"
+#include "sm100.cuh"
+
+namespace st {
+namespace {
+
+using namespace sm100;
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr uint32_t A_BYTES = BM * BK * 2;            // 16 KB
+constexpr uint32_t B_ATOM = BK * 128;                // 64 K rows x 128 B (64 N elements)
+constexpr uint32_t B_BYTES = 4 * B_ATOM;             // 32 KB
+constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;  // 48 KB
+constexpr uint32_t OFF_BAR = STAGES * STAGE_BYTES;
+constexpr uint32_t SMEM_BYTES = OFF_BAR + 256;
+constexpr int THREADS = 6 * 32;  // producer, MMA, 4 epilogue warps
+
+struct GemmParams {
+    void* C;
+    long long c_stride_z;  // elements
+    int ldc;
+    int M, N, K, Z;
+    int nm, nn, nk;        // tile counts
+    int vec;               // 16-byte stores allowed (aligned C rows)
+};
+
+template <class T> struct pk;
+template <> struct pk<__half> {
+    static __device__ __forceinline__ uint32_t two(float a, float b) {
+        __half2 h = __floats2half2_rn(a, b);
+        return *reinterpret_cast<uint32_t*>(&h);
+    }
+    static __device__ __forceinline__ float lo(uint32_t w) {
+        return __half2float(__ushort_as_half((unsigned short)(w & 0xffffu)));
+    }
+    static __device__ __forceinline__ float hi(uint32_t w) {
+        return __half2float(__ushort_as_half((unsigned short)(w >> 16)));
+    }
+    static __device__ __forceinline__ __half one(float a) { return __float2half_rn(a); }
+    static __device__ __forceinline__ float get(__half x) { return __half2float(x); }
+};
+template <> struct pk<__nv_bfloat16> {
+    static __device__ __forceinline__ uint32_t two(float a, float b) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+        return *reinterpret_cast<uint32_t*>(&h);
+    }
+    static __device__ __forceinline__ float lo(uint32_t w) { return __uint_as_float(w << 16); }
+    static __device__ __forceinline__ float hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+    static __device__ __forceinline__ __nv_bfloat16 one(float a) { return __float2bfloat16_rn(a); }
+    static __device__ __forceinline__ float get(__nv_bfloat16 x) { return __bfloat162float(x); }
+};
+
+// Apply the epilogue to one row's 32 accumulator columns [col0, col0+32) and
+// store them.
+template <class T, int EPI>
+__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int row, int col0,
+                                               float (&v)[32]) {
+    if (row >= p.M) return;
+    if constexpr (EPI == kGemmGelu) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] = gelu_erf(v[k]);
+    }
+    const bool full = col0 + 32 <= p.N;
+    if constexpr (EPI == kGemmStoreF32) {
+        float* c = reinterpret_cast<float*>(p.C) + z * p.c_stride_z + (long long)row * p.ldc + col0;
+        if (full && p.vec) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                reinterpret_cast<float4*>(c)[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+                if (col0 + k < p.N) c[k] = v[k];
+        }
+    } else {
+        T* c = reinterpret_cast<T*>(p.C) + z * p.c_stride_z + (long long)row * p.ldc + col0;
+        if (full && p.vec) {
+            uint4* c4 = reinterpret_cast<uint4*>(c);
+            if constexpr (EPI == kGemmAddTo) {
+                uint4 old[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) old[q] = c4[q];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t w[4] = {old[q].x, old[q].y, old[q].z, old[q].w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        v[q * 8 + 2 * e] += pk<T>::lo(w[e]);
+                        v[q * 8 + 2 * e + 1] += pk<T>::hi(w[e]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                c4[q] = make_uint4(pk<T>::two(v[q * 8], v[q * 8 + 1]), pk<T>::two(v[q * 8 + 2], v[q * 8 + 3]),
+                                   pk<T>::two(v[q * 8 + 4], v[q * 8 + 5]), pk<T>::two(v[q * 8 + 6], v[q * 8 + 7]));
+        } else {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+                if (col0 + k < p.N) {
+                    float x = v[k];
+                    if constexpr (EPI == kGemmAddTo) x += pk<T>::get(c[k]);
+                    c[k] = pk<T>::one(x);
+                }
+            }
+        }
+    }
+}
+
+template <class T, int EPI>
+__global__ void __launch_bounds__(THREADS, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+            const GemmParams p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* empty = full + STAGES;
+    uint64_t* acc_full = empty + STAGES;   // [2]
+    uint64_t* acc_empty = acc_full + 2;    // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        if (smem_u32(smem) & 1023u) __trap();
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(acc_full + i, 1);
+            mbar_init(acc_empty + i, 4 * 32);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tm_a);
+        prefetch_tmap(&tm_b);
+    }
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_wait();       // A (and C for add-to) come from the previous kernel
+    pdl_trigger();
+    const int tiles = p.nm * p.nn * p.Z;
+
+    if (warp == 0) {
+        // ============================ TMA producer ============================
+        if (lane == 0) {
+            uint32_t kc = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int mb = t % p.nm, rest = t / p.nm, nb = rest % p.nn, z = rest / p.nn;
+                for (int kb = 0; kb < p.nk; ++kb, ++kc) {
+                    const uint32_t s = kc % STAGES;
+                    mbar_wait(empty + s, ((kc / STAGES) & 1) ^ 1);
+                    mbar_arrive_expect_tx(full + s, STAGE_BYTES);
+                    uint8_t* a = smem + s * STAGE_BYTES;
+                    tma_load_2d(a, &tm_a, full + s, kb * BK, mb * BM);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        tma_load_3d(a + A_BYTES + j * B_ATOM, &tm_b, full + s, nb * BN + j * 64,
+                                    kb * BK, z);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ============================= MMA issuer =============================
+        constexpr uint32_t fmt = std::is_same<T, __half>::value ? 0u : 1u;
+        constexpr uint32_t idesc = idesc_f16(fmt, BM, BN, 0, 1);  // A K-major, W MN-major
+        uint32_t kc = 0, ac = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++ac) {
+            const uint32_t acc = ac & 1;
+            mbar_wait(acc_empty + acc, ((ac >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem + acc * BN;
+            for (int kb = 0; kb < p.nk; ++kb, ++kc) {
+                const uint32_t s = kc % STAGES;
+                mbar_wait(full + s, (kc / STAGES) & 1);
+                tc_fence_after();
+                const uint32_t a_base = smem_u32(smem + s * STAGE_BYTES);
+                const uint64_t ad = smem_desc(a_base, 16, 1024);
+                const uint64_t bd = smem_desc(a_base + A_BYTES, B_ATOM, 1024);
+#pragma unroll
+                for (int kk = 0; kk < BK / 16; ++kk)
+                    umma_f16_ss_warp(d, ad + ((kk * 32) >> 4), bd + ((kk * 2048) >> 4), idesc,
+                                     (kb | kk) ? 1u : 0u);
+                umma_commit_warp(empty + s);
+            }
+            umma_commit_warp(acc_full + acc);
+        }
+    } else {
+        // ============================== epilogue ==============================
+        const int q = warp & 3;  // TMEM lane quadrant this warp may access
+        const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+        uint32_t ac = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++ac) {
+            const int mb = t % p.nm, rest = t / p.nm, nb = rest % p.nn, z = rest / p.nn;
+            const uint32_t acc = ac & 1;
+            mbar_wait(acc_full + acc, (ac >> 1) & 1);
+            tc_fence_after();
+            const int row = mb * BM + q * 32 + lane;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                const int col0 = nb * BN + c * 32;
+                if (col0 >= p.N) break;
+                uint32_t raw[32];
+                tmem_ld_32x32b_x32(lane_base + acc * BN + c * 32, raw);
+                tmem_ld_wait();
+                float v[32];
+#pragma unroll
+                for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(raw[k]);
+                epilogue_chunk<T, EPI>(p, z, row, col0, v);
+            }
+            tc_fence_before();
+            mbar_arrive(acc_empty + acc);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return n;
+}
+
+template <class T, int EPI>
+st_status launch(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb,
+                 const GemmParams& p, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        ST_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<T, EPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        attr = true;
+    }
+    const int tiles = p.nm * p.nn * p.Z;
+    const int grid = tiles < sm_count() ? tiles : sm_count();
+    ST_CUDA_TRY(launch_pdl(gemm_kernel<T, EPI>, dim3(grid), dim3(THREADS), SMEM_BYTES, s, ta, tb, p));
+    (void)g;
+    return ST_OK;
+}
+
+}  // namespace
+
+bool gemm_supported(const GemmArgs& g) {
+    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    return (g.dtype == ST_F16 || g.dtype == ST_BF16) && g.M >= 1 && g.N >= 1 && g.K >= 1 &&
+           g.Z >= 1 && g.ldw >= g.N && g.ldw % 8 == 0 && g.lda >= g.K && g.lda % 8 == 0 &&
+           al(g.A) && al(g.W);
+}
+
+st_status gemm_sm100(const GemmArgs& g, cudaStream_t s) {
+    ST_CHECK_ARG(gemm_supported(g), ST_ERR_UNSUPPORTED,
+                 "gemm: f16/bf16, lda and ldw multiples of 8, 16-byte aligned A / W");
+    auto enc = encoder();
+    ST_CHECK_ARG(enc != nullptr, ST_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const CUtensorMapDataType dt =
+        g.dtype == ST_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    CUtensorMap ta, tb;
+    const uint32_t es[3] = {1, 1, 1};
+    {
+        const uint64_t dims[2] = {(uint64_t)g.K, (uint64_t)g.M};
+        const uint64_t strides[1] = {(uint64_t)g.lda * 2};
+        const uint32_t box[2] = {BK, BM};
+        if (enc(&ta, dt, 2, const_cast<void*>(g.A), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            set_error("gemm: cuTensorMapEncodeTiled(A) failed");
+            return ST_ERR_CUDA;
+        }
+    }
+    {
+        const uint64_t dims[3] = {(uint64_t)g.N, (uint64_t)g.K, (uint64_t)g.Z};
+        const uint64_t strides[2] = {(uint64_t)g.ldw * 2, (uint64_t)g.ldw * g.K * 2};
+        const uint32_t box[3] = {64, BK, 1};
+        if (enc(&tb, dt, 3, const_cast<void*>(g.W), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            set_error("gemm: cuTensorMapEncodeTiled(W) failed");
+            return ST_ERR_CUDA;
+        }
+    }
+    GemmParams p;
+    p.C = g.C;
+    p.c_stride_z = g.c_stride_z;
+    p.ldc = g.ldc;
+    p.M = g.M;
+    p.N = g.N;
+    p.K = g.K;
+    p.Z = g.Z;
+    p.nm = (g.M + BM - 1) / BM;
+    p.nn = (g.N + BN - 1) / BN;
+    p.nk = (g.K + BK - 1) / BK;
+    const size_t cbytes = g.epi == kGemmStoreF32 ? 4 : 2;
+    p.vec = (reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && ((size_t)g.ldc * cbytes) % 16 == 0 &&
+            ((size_t)g.c_stride_z * cbytes) % 16 == 0;
+#define ST_GEMM_EPI(TT)                                                              \
+    switch (g.epi) {                                                                 \
+        case kGemmStore: return launch<TT, kGemmStore>(g, ta, tb, p, s);             \
+        case kGemmGelu: return launch<TT, kGemmGelu>(g, ta, tb, p, s);               \
+        case kGemmAddTo: return launch<TT, kGemmAddTo>(g, ta, tb, p, s);             \
+        case kGemmStoreF32: return launch<TT, kGemmStoreF32>(g, ta, tb, p, s);       \
+    }
+    if (g.dtype == ST_F16) {
+        ST_GEMM_EPI(__half)
+    } else {
+        ST_GEMM_EPI(__nv_bfloat16)
+    }
+#undef ST_GEMM_EPI
+    set_error("gemm: bad epilogue");
+    return ST_ERR_INVALID_ARGUMENT;
+}
+
+}  // namespace st
+
+extern "C" st_status st_gemm(st_dtype dtype, int M, int N, int K, int Z, const void* A, int lda,
+                             const void* W, int ldw, void* C, int ldc, int64_t c_stride_z,
+                             int epilogue, void* stream) {
+    if (st_status e = st::require_device()) return e;
+    ST_CHECK_ARG(A && W && C, ST_ERR_INVALID_ARGUMENT, "null pointer");
+    st::GemmArgs g{dtype, A, lda, W, ldw, C, c_stride_z, ldc, M, N, K, Z, epilogue};
+    if (st_status e = st::gemm_sm100(g, st::as_stream(stream))) return e;
+    ST_LAUNCH_CHECK();
+    return ST_OK;
+}

@@ -2,29 +2,29 @@
 // shapes: "batched around-path GEMMs" for the C3 full
 // stack). The reference runs one f64 matvec per tree node per matrix
 // (proj/src/transformer.cpp:262-319); here every projection is ONE GEMM over
-// all B*T tree rows of the batch (cuBLAS — plain library GEMMs, fp32
-// accumulate), and the verification hot path in between is ours: K2 append of
-// the rows' K/V into the per-layer cache, K1 masked tree attention.
+// all B*T tree rows of the batch — the hand-written tcgen05 GEMM of gemm.cu,
+// fp32 accumulate, with GELU (FFN-1) and the residual adds (WO, FFN-2) fused
+// into its epilogue — and the verification hot path in between is ours: K2
+// append of the rows' K/V into the per-layer cache, K1 masked tree attention.
 //
 // Weights follow init_random_weights exactly (proj/src/transformer.cpp:71-114):
 // every tensor is drawn from ONE UniformStream(seed) in the serialized order
 // (tok, pos, per layer [ln1 g,b, wq, wk, wv, wo, ln2 g,b, w1, w2], lnf g,b,
 // W_out), U(-0.08, 0.08) — generated on the device (value i is a pure function
 // of (seed, i)) and rounded to the model dtype.
-#include <cublas_v2.h>
-
 #include <cmath>
 #include <vector>
 
 #include "common.cuh"
+#include "gemm.h"
 
 struct st_model {
     st_model_config cfg;
     st_dtype dtype;
     void* buf = nullptr;
     size_t elems = 0;
-    cublasHandle_t blas = nullptr;
-    void* blas_ws = nullptr;  // cuBLAS workspace: lets the heuristics pick split-K / stream-K kernels
+    void* wout_pad = nullptr;  // W_out with its row stride padded to a multiple of 8 (TMA)
+    int ldw_out = 0;
     // element offsets into buf
     size_t tok, pos, lnf_g, lnf_b, wout;
     struct Layer {
@@ -97,15 +97,6 @@ __global__ void layernorm_kernel(const T* __restrict__ x, const T* __restrict__ 
     for (int c = threadIdx.x; c < d; c += blockDim.x)
         orow[c] = from_acc<T>(to_acc<float>(g[c]) * (to_acc<float>(xr[c]) - mean) * inv +
                               to_acc<float>(b[c]));
-}
-
-template <class T>
-__global__ void gelu_kernel(T* __restrict__ x, int64_t n) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const float v = to_acc<float>(x[i]);
-        x[i] = from_acc<T>(0.5f * v * (1.f + erff(v * 0.70710678118654752f)));
-    }
 }
 
 // 8 half-precision values <-> one 16-byte vector
@@ -192,89 +183,11 @@ layernorm_vec_kernel(const T* __restrict__ x, const T* __restrict__ g, const T* 
     }
 }
 
-// GELU (erf form, reference transformer.cpp:67): 0.5 v (1 + erf(v / sqrt 2)).
-// 1 + erf(x) via Abramowitz & Stegun 7.1.26 (|erf error| <= 1.5e-7, far below
-// the f16/bf16 output resolution), evaluated as erfc(|x|) = poly(t) e^{-x^2}
-// for x < 0 so the small values of the negative tail keep their relative
-// accuracy (no 1 - erf cancellation). Branch-free: 2 MUFU ops (approximate
-// reciprocal and exp2, each ~2 ulp) + 7 FMAs instead of erff's branchy
-// evaluation.
-__device__ __forceinline__ float gelu_f(float v) {
-    const float x = v * 0.70710678118654752f;
-    const float a = fabsf(x);
-    const float t = __fdividef(1.f, fmaf(0.3275911f, a, 1.f));  // MUFU.RCP: ~1 ulp, no Newton step
-    float y = fmaf(1.061405429f, t, -1.453152027f);
-    y = fmaf(y, t, 1.421413741f);
-    y = fmaf(y, t, -0.284496736f);
-    y = fmaf(y, t, 0.254829592f);
-    y *= t * __expf(-a * a);          // erfc(|x|)
-    const float one_plus_erf = x >= 0.f ? 2.f - y : y;
-    return 0.5f * v * one_plus_erf;
-}
-
-// GELU in place, 8 values per 16-byte access; each thread keeps GELU_ILP
-// independent loads in flight before its stores (in place, so the compiler
-// cannot hoist the next load over the previous store by itself).
-constexpr int GELU_ILP = 4;
-template <class T>
-__global__ void gelu_vec_kernel(uint4* __restrict__ x, int64_t n8) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n8;
-         i0 += stride * GELU_ILP) {
-        uint4 u[GELU_ILP];
-#pragma unroll
-        for (int r = 0; r < GELU_ILP; ++r)
-            if (i0 + r * stride < n8) u[r] = x[i0 + r * stride];
-#pragma unroll
-        for (int r = 0; r < GELU_ILP; ++r) {
-            if (i0 + r * stride < n8) {
-                float f[8];
-                unpack8<T>(u[r], f);
-#pragma unroll
-                for (int k = 0; k < 8; ++k) f[k] = gelu_f(f[k]);
-                x[i0 + r * stride] = pack8<T>(f);
-            }
-        }
-    }
-}
-
-cudaDataType_t cuda_type(st_dtype t) { return t == ST_F16 ? CUDA_R_16F : CUDA_R_16BF; }
-
-// Row-major C[M][N] (+)= A[M][K] * W[K][N]  (column-major view: C^T = W^T A^T)
-st_status gemm(st_model* m, const void* A, size_t w_off, void* C, cudaDataType_t ctype, int M, int N,
-               int K, bool accumulate, cudaStream_t s) {
-    const float alpha = 1.f, beta = accumulate ? 1.f : 0.f;
-    const size_t es = dtype_size(m->dtype);
-    const void* W = static_cast<const char*>(m->buf) + w_off * es;
-    cublasSetStream(m->blas, s);
-    const cublasStatus_t st =
-        cublasGemmEx(m->blas, CUBLAS_OP_N, CUBLAS_OP_N, N, M, K, &alpha, W, cuda_type(m->dtype), N,
-                     A, cuda_type(m->dtype), K, &beta, C, ctype, N, CUBLAS_COMPUTE_32F,
-                     CUBLAS_GEMM_DEFAULT);
-    if (st != CUBLAS_STATUS_SUCCESS) {
-        set_error("cublasGemmEx failed: status " + std::to_string((int)st));
-        return ST_ERR_CUDA;
-    }
-    return ST_OK;
-}
-
-// `batch` GEMMs sharing the activation A: C_i = A W_i, W_i at w_off + i*w_stride
-// elements, C_i at C + i*c_stride elements (one launch for Q/K/V).
-st_status gemm_shared_a(st_model* m, const void* A, size_t w_off, size_t w_stride, void* C,
-                        long long c_stride, int batch, int M, int N, int K, cudaStream_t s) {
-    const float alpha = 1.f, beta = 0.f;
-    const size_t es = dtype_size(m->dtype);
-    const void* W = static_cast<const char*>(m->buf) + w_off * es;
-    cublasSetStream(m->blas, s);
-    const cublasStatus_t st = cublasGemmStridedBatchedEx(
-        m->blas, CUBLAS_OP_N, CUBLAS_OP_N, N, M, K, &alpha, W, cuda_type(m->dtype), N,
-        (long long)w_stride, A, cuda_type(m->dtype), K, 0, &beta, C, cuda_type(m->dtype), N,
-        c_stride, batch, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
-    if (st != CUBLAS_STATUS_SUCCESS) {
-        set_error("cublasGemmStridedBatchedEx failed: status " + std::to_string((int)st));
-        return ST_ERR_CUDA;
-    }
-    return ST_OK;
+// Row-major C[z] (op)= A W[z] on the tcgen05 GEMM (gemm.cu).
+st_status gemm(st_model* m, const void* A, const void* W, int ldw, void* C, int ldc, int M, int N,
+               int K, int Z, long long c_stride_z, int epi, cudaStream_t s) {
+    GemmArgs g{m->dtype, A, K, W, ldw, C, c_stride_z, ldc, M, N, K, Z, epi};
+    return gemm_sm100(g, s);
 }
 
 template <class T>
@@ -297,6 +210,8 @@ st_status st_model_create(const st_model_config* cfg, uint64_t seed, st_dtype dt
     ST_CHECK_ARG(c.num_layers >= 1 && c.num_heads >= 1 && c.d_model >= 1 && c.vocab_size >= 2 &&
                      c.max_positions >= 1 && c.ffn_mult >= 1 && c.d_model % c.num_heads == 0,
                  ST_ERR_SHAPE_MISMATCH, "bad model config");
+    ST_CHECK_ARG(c.d_model % 8 == 0, ST_ERR_UNSUPPORTED,
+                 "device model needs d_model % 8 == 0 (16-byte rows for the TMA-fed GEMMs)");
     auto* m = new st_model;
     m->cfg = c;
     m->dtype = dtype;
@@ -340,11 +255,20 @@ st_status st_model_create(const st_model_config* cfg, uint64_t seed, st_dtype dt
     else
         st::gen_weights_kernel<__nv_bfloat16><<<blocks, 256>>>((__nv_bfloat16*)m->buf, (int64_t)at,
                                                                seed, 0);
-    constexpr size_t kBlasWs = 64ull << 20;
-    if (cudaDeviceSynchronize() != cudaSuccess || cublasCreate(&m->blas) != CUBLAS_STATUS_SUCCESS ||
-        cudaMalloc(&m->blas_ws, kBlasWs) != cudaSuccess ||
-        cublasSetWorkspace(m->blas, m->blas_ws, kBlasWs) != CUBLAS_STATUS_SUCCESS) {
+    // the LM head's W_out [d][V]: TMA needs 16-byte row strides, so a vocabulary
+    // that is not a multiple of 8 gets a copy with padded rows (zeros past V)
+    m->ldw_out = (int)((V + 7) / 8 * 8);
+    bool ok = cudaDeviceSynchronize() == cudaSuccess;
+    if (ok && (size_t)m->ldw_out != V) {
+        const size_t es = st::dtype_size(dtype);
+        ok = cudaMalloc(&m->wout_pad, d * m->ldw_out * es) == cudaSuccess &&
+             cudaMemset(m->wout_pad, 0, d * m->ldw_out * es) == cudaSuccess &&
+             cudaMemcpy2D(m->wout_pad, m->ldw_out * es, static_cast<char*>(m->buf) + m->wout * es,
+                          V * es, V * es, d, cudaMemcpyDeviceToDevice) == cudaSuccess;
+    }
+    if (!ok) {
         cudaGetLastError();
+        if (m->wout_pad) cudaFree(m->wout_pad);
         cudaFree(m->buf);
         delete m;
         st::set_error("st_model_create: init failed");
@@ -356,8 +280,7 @@ st_status st_model_create(const st_model_config* cfg, uint64_t seed, st_dtype dt
 
 void st_model_destroy(st_model* m) {
     if (!m) return;
-    if (m->blas) cublasDestroy(m->blas);
-    if (m->blas_ws) cudaFree(m->blas_ws);
+    if (m->wout_pad) cudaFree(m->wout_pad);
     if (m->buf) cudaFree(m->buf);
     delete m;
 }
@@ -434,7 +357,7 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
     // committed rows and the lengths are stable, so K1 may stream them early
     a.early_kv = 1;
     const size_t layer_elems = (size_t)B * H * Lmax * Dh;
-    const cudaDataType_t ht = st::cuda_type(m->dtype);
+    auto Wp = [&](size_t off) -> const void* { return static_cast<const char*>(m->buf) + off * es; };
 
 #define ST_M_DISPATCH(...)                                                   \
     if (m->dtype == ST_F16) {                                                \
@@ -477,12 +400,16 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
         if (L.wk == L.wq + dd && L.wv == L.wk + dd &&
             static_cast<char*>(vn) - static_cast<char*>(kn) == qkv_stride * (long long)es) {
             // wq|wk|wv are consecutive in the serialized order: one batched launch
-            if (st_status e = st::gemm_shared_a(m, h, L.wq, dd, q, qkv_stride, 3, rows, d, d, s))
+            if (st_status e = st::gemm(m, h, Wp(L.wq), d, q, d, rows, d, d, 3, qkv_stride,
+                                       st::kGemmStore, s))
                 return e;
         } else {
-            if (st_status e = st::gemm(m, h, L.wq, q, ht, rows, d, d, false, s)) return e;
-            if (st_status e = st::gemm(m, h, L.wk, kn, ht, rows, d, d, false, s)) return e;
-            if (st_status e = st::gemm(m, h, L.wv, vn, ht, rows, d, d, false, s)) return e;
+            if (st_status e = st::gemm(m, h, Wp(L.wq), d, q, d, rows, d, d, 1, 0, st::kGemmStore, s))
+                return e;
+            if (st_status e = st::gemm(m, h, Wp(L.wk), d, kn, d, rows, d, d, 1, 0, st::kGemmStore, s))
+                return e;
+            if (st_status e = st::gemm(m, h, Wp(L.wv), d, vn, d, rows, d, d, 1, 0, st::kGemmStore, s))
+                return e;
         }
         if (st_status e = st_kv_append(m->dtype, B, T, H, Dh, Lmax, kn, vn, prefix_len, n_nodes, kc,
                                        vc, stream))
@@ -492,21 +419,21 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
         a.v_cache = vc;
         a.o = o;
         if (st_status e = st_tree_attention(&a, stream)) return e;
-        if (st_status e = st::gemm(m, o, L.wo, x, ht, rows, d, d, true, s)) return e;
+        // x += o W_o (residual add in the epilogue)
+        if (st_status e = st::gemm(m, o, Wp(L.wo), d, x, d, rows, d, d, 1, 0, st::kGemmAddTo, s))
+            return e;
         if (st_status e = layernorm(L.ln2_g, L.ln2_b)) return e;
-        if (st_status e = st::gemm(m, h, L.w1, f, ht, rows, F, d, false, s)) return e;
-        const int64_t nf = (int64_t)rows * F;
-        if (nf % 8 == 0 && aligned16(f)) {
-            ST_M_DISPATCH(st::gelu_vec_kernel<T><<<148 * 8, 256, 0, s>>>((uint4*)f, nf / 8));
-        } else {
-            ST_M_DISPATCH(st::gelu_kernel<T><<<148 * 8, 256, 0, s>>>((T*)f, nf));
-        }
-        ST_LAUNCH_CHECK();
-        if (st_status e = st::gemm(m, f, L.w2, x, ht, rows, d, F, true, s)) return e;
+        // f = gelu(h W_1) (GELU in the epilogue), then x += f W_2
+        if (st_status e = st::gemm(m, h, Wp(L.w1), F, f, F, rows, F, d, 1, 0, st::kGemmGelu, s))
+            return e;
+        if (st_status e = st::gemm(m, f, Wp(L.w2), d, x, d, rows, d, F, 1, 0, st::kGemmAddTo, s))
+            return e;
     }
     if (st_status e = layernorm(m->lnf_g, m->lnf_b)) return e;
 #undef ST_M_DISPATCH
-    return st::gemm(m, h, m->wout, logits, CUDA_R_32F, rows, c.vocab_size, d, false, s);
+    const void* wout = m->wout_pad ? m->wout_pad : Wp(m->wout);
+    return st::gemm(m, h, wout, m->ldw_out, logits, c.vocab_size, rows, c.vocab_size, d, 1, 0,
+                    st::kGemmStoreF32, s);
 }
 
 }  // extern "C"
