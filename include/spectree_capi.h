@@ -314,15 +314,11 @@ void st_verify_plan_destroy(st_verify_plan* p);
  * the tcgen05 tensor cores, fp32 accumulate, the decoder's elementwise work
  * fused into the epilogue. A [M][lda] row-major, W [Z][K][ldw] row-major (the
  * stored weight layout), C [Z][M][ldc] (c_stride_z elements apart); f16/bf16
- * in; C f16/bf16, or f32 for ST_GEMM_STORE_F32. lda, ldw multiples of 8.
- * workspace (optional, st_gemm_workspace_size() bytes, zeroed once): lets the
- * last wave of tiles be split into equal (tile, k-block) ranges over all SMs
- * (stream-K) instead of leaving SMs idle; NULL = whole tiles only. */
+ * in; C f16/bf16, or f32 for ST_GEMM_STORE_F32. lda, ldw multiples of 8. */
 enum { ST_GEMM_STORE = 0, ST_GEMM_GELU = 1, ST_GEMM_ADD_TO = 2, ST_GEMM_STORE_F32 = 3 };
-size_t st_gemm_workspace_size(void);
 st_status st_gemm(st_dtype dtype, int M, int N, int K, int Z, const void* A, int lda,
                   const void* W, int ldw, void* C, int ldc, int64_t c_stride_z, int epilogue,
-                  void* workspace, size_t workspace_bytes, void* stream);
+                  void* stream);
 
 /* The model's configuration and element type. */
 void st_model_get_config(const st_model* m, st_model_config* out);

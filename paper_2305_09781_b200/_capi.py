@@ -100,8 +100,7 @@ SIGNATURES = {
     "st_verify_plan_create": (_I, [_V, _V]),
     "st_verify_plan_run": (_I, [_V, _V]),
     "st_verify_plan_destroy": (None, [_V]),
-    "st_gemm": (_I, [_I, _I, _I, _I, _I, _V, _I, _V, _I, _V, _I, _I64, _I, _V, _Z, _V]),
-    "st_gemm_workspace_size": (_Z, []),
+    "st_gemm": (_I, [_I, _I, _I, _I, _I, _V, _I, _V, _I, _V, _I, _I64, _I, _V]),
 }
 
 
@@ -568,19 +567,7 @@ class VerifyPlan:
 GEMM_EPI = {"store": 0, "gelu": 1, "add_to": 2, "store_f32": 3}
 
 
-_gemm_ws = {}
-
-
-def gemm_workspace(device):
-    """The stream-K workspace (zeroed once; flags are re-armed by every call)."""
-    key = str(device)
-    if key not in _gemm_ws:
-        _gemm_ws[key] = torch.zeros(int(lib().st_gemm_workspace_size()), dtype=torch.uint8,
-                                    device=device)
-    return _gemm_ws[key]
-
-
-def gemm(a, w, out=None, epilogue="store", stream=None, stream_k=True):
+def gemm(a, w, out=None, epilogue="store", stream=None):
     """C (op)= A @ W on the tcgen05 GEMM (st_gemm). a [M][K]; w [K][N] or
     [Z][K][N]; out [M][N] / [Z][M][N] (f32 for epilogue="store_f32")."""
     M, K = a.shape
@@ -589,10 +576,8 @@ def gemm(a, w, out=None, epilogue="store", stream=None, stream_k=True):
     if out is None:
         dt = torch.float32 if epilogue == "store_f32" else a.dtype
         out = torch.empty((M, N) if w.dim() == 2 else (Z, M, N), dtype=dt, device=a.device)
-    ws = gemm_workspace(a.device) if stream_k else None
     check(lib().st_gemm(DTYPES[a.dtype], M, N, K, Z, _ptr(a), a.stride(0), _ptr(w), w.stride(-2),
                         _ptr(out),
                         out.stride(-2), (M * out.stride(-2)) if Z > 1 else 0, GEMM_EPI[epilogue],
-                        _ptr(ws) if ws is not None else None, ws.numel() if ws is not None else 0,
                         _stream(stream)))
     return out

@@ -49,44 +49,7 @@ struct GemmParams {
     int M, N, K, Z;
     int nm, nn, nk;        // tile counts
     int vec;               // 16-byte stores allowed (aligned C rows)
-    // schedule: tiles [0, dp_tiles) whole (tile t on CTA t % G), then the
-    // remaining sk_tiles split into G equal ranges of (tile, k-block) units
-    int dp_tiles, sk_tiles;
-    float* partial;        // [G][BM*BN] fp32 split-tile pieces (stream-K)
-    unsigned* flags;       // [G] piece published (re-armed by the consumer)
 };
-
-// One unit of a CTA's work: tile t, k-blocks [kb0, kb1).
-struct Work {
-    int t, kb0, kb1;
-};
-
-__device__ __forceinline__ long long sk_start(const GemmParams& p, int c) {
-    return (long long)p.sk_tiles * p.nk * c / gridDim.x;
-}
-
-// The i-th work item of this CTA (false when done): its whole tiles first,
-// then the segments of its stream-K range.
-__device__ __forceinline__ bool work_at(const GemmParams& p, int i, Work& w, long long& u) {
-    const int G = gridDim.x;
-    const int ndp = (p.dp_tiles - (int)blockIdx.x + G - 1) / G;
-    if (i < ndp) {
-        w.t = blockIdx.x + i * G;
-        w.kb0 = 0;
-        w.kb1 = p.nk;
-        return true;
-    }
-    if (i == ndp) u = sk_start(p, blockIdx.x);
-    const long long u1 = sk_start(p, blockIdx.x + 1);
-    if (u >= u1) return false;
-    const int ts = (int)(u / p.nk);
-    w.t = p.dp_tiles + ts;
-    w.kb0 = (int)(u - (long long)ts * p.nk);
-    const long long tile_end = (long long)(ts + 1) * p.nk;
-    w.kb1 = (int)((tile_end < u1 ? tile_end : u1) - (long long)ts * p.nk);
-    u += w.kb1 - w.kb0;
-    return true;
-}
 
 template <class T> struct pk;
 template <> struct pk<__half> {
@@ -205,16 +168,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CU
     const uint32_t tmem = *tmem_slot;
     pdl_wait();       // A (and C for add-to) come from the previous kernel
     pdl_trigger();
+    const int tiles = p.nm * p.nn * p.Z;
+
     if (warp == 0) {
         // ============================ TMA producer ============================
         if (lane == 0) {
             uint32_t kc = 0;
-            Work w;
-            long long u = 0;
-            for (int i = 0; work_at(p, i, w, u); ++i) {
-                const int t = w.t;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
                 const int mb = t % p.nm, rest = t / p.nm, nb = rest % p.nn, z = rest / p.nn;
-                for (int kb = w.kb0; kb < w.kb1; ++kb, ++kc) {
+                for (int kb = 0; kb < p.nk; ++kb, ++kc) {
                     const uint32_t s = kc % STAGES;
                     mbar_wait(empty + s, ((kc / STAGES) & 1) ^ 1);
                     mbar_arrive_expect_tx(full + s, STAGE_BYTES);
@@ -232,14 +194,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CU
         constexpr uint32_t fmt = std::is_same<T, __half>::value ? 0u : 1u;
         constexpr uint32_t idesc = idesc_f16(fmt, BM, BN, 0, 1);  // A K-major, W MN-major
         uint32_t kc = 0, ac = 0;
-        Work w;
-        long long u = 0;
-        for (int i = 0; work_at(p, i, w, u); ++i, ++ac) {
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++ac) {
             const uint32_t acc = ac & 1;
             mbar_wait(acc_empty + acc, ((ac >> 1) & 1) ^ 1);
             tc_fence_after();
             const uint32_t d = tmem + acc * BN;
-            for (int kb = w.kb0; kb < w.kb1; ++kb, ++kc) {
+            for (int kb = 0; kb < p.nk; ++kb, ++kc) {
                 const uint32_t s = kc % STAGES;
                 mbar_wait(full + s, (kc / STAGES) & 1);
                 tc_fence_after();
@@ -249,7 +209,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CU
 #pragma unroll
                 for (int kk = 0; kk < BK / 16; ++kk)
                     umma_f16_ss_warp(d, ad + ((kk * 32) >> 4), bd + ((kk * 2048) >> 4), idesc,
-                                     (kb > w.kb0 || kk) ? 1u : 0u);
+                                     (kb | kk) ? 1u : 0u);
                 umma_commit_warp(empty + s);
             }
             umma_commit_warp(acc_full + acc);
@@ -259,72 +219,26 @@ gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CU
         const int q = warp & 3;  // TMEM lane quadrant this warp may access
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
         uint32_t ac = 0;
-        Work w;
-        long long u = 0;
-        const int r = q * 32 + lane;  // this thread's row of the tile
-        for (int i = 0; work_at(p, i, w, u); ++i, ++ac) {
-            const int t = w.t;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++ac) {
             const int mb = t % p.nm, rest = t / p.nm, nb = rest % p.nn, z = rest / p.nn;
             const uint32_t acc = ac & 1;
-            // stream-K: a segment that starts past k-block 0 is a PIECE (first
-            // segment of this CTA's range) and leaves its fp32 partial for the
-            // tile's owner; the segment holding k-block 0 of a split tile is
-            // its OWNER (last segment of the owner's range) and adds the
-            // pieces of the following CTAs, in CTA order (deterministic)
-            const bool piece = w.kb0 > 0;
-            const bool owner = !piece && w.kb1 < p.nk;
-            int np = 0, first = 0;
-            if (owner) {
-                const long long tile_end = (long long)(t - p.dp_tiles + 1) * p.nk;
-                first = blockIdx.x + 1;
-                while (first + np < (int)gridDim.x && sk_start(p, first + np) < tile_end) ++np;
-                for (int j = 0; j < np; ++j) wait_flag_gpu(p.flags + first + j);
-            }
             mbar_wait(acc_full + acc, (ac >> 1) & 1);
             tc_fence_after();
-            const int row = mb * BM + r;
-            float4* mine = reinterpret_cast<float4*>(p.partial + (long long)blockIdx.x * BM * BN);
+            const int row = mb * BM + q * 32 + lane;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 const int col0 = nb * BN + c * 32;
-                if (!piece && col0 >= p.N) break;
+                if (col0 >= p.N) break;
                 uint32_t raw[32];
                 tmem_ld_32x32b_x32(lane_base + acc * BN + c * 32, raw);
                 tmem_ld_wait();
                 float v[32];
 #pragma unroll
                 for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(raw[k]);
-                if (piece) {  // float4 (r, 4j..4j+3) of chunk c at (c*8 + j)*BM + r: coalesced
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        mine[(c * 8 + j) * BM + r] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-                    continue;
-                }
-                for (int pc = 0; pc < np; ++pc) {
-                    const float4* other =
-                        reinterpret_cast<const float4*>(p.partial + (long long)(first + pc) * BM * BN);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const float4 x = __ldcg(other + (c * 8 + j) * BM + r);
-                        v[4 * j] += x.x;
-                        v[4 * j + 1] += x.y;
-                        v[4 * j + 2] += x.z;
-                        v[4 * j + 3] += x.w;
-                    }
-                }
                 epilogue_chunk<T, EPI>(p, z, row, col0, v);
             }
             tc_fence_before();
             mbar_arrive(acc_empty + acc);
-            if (piece) {  // every epilogue thread's stores, then one gpu-scope release
-                named_bar_sync(1, 4 * 32);
-                if (threadIdx.x == 2 * 32) st_release_gpu(p.flags + blockIdx.x, 1u);
-            }
-            if (owner) {  // re-arm the pieces' flags for the next launch (all reads done)
-                named_bar_sync(1, 4 * 32);
-                if (threadIdx.x == 2 * 32)
-                    for (int j = 0; j < np; ++j) p.flags[first + j] = 0u;
-            }
         }
     }
     tc_fence_before();
@@ -367,19 +281,12 @@ st_status launch(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb
     }
     const int tiles = p.nm * p.nn * p.Z;
     const int grid = tiles < sm_count() ? tiles : sm_count();
-    // stream-K owners wait for pieces of other CTAs: cooperative launch
-    // guarantees they are all resident (one CTA per SM either way)
-    ST_CUDA_TRY(launch_pdl_ex(gemm_kernel<T, EPI>, dim3(grid), dim3(THREADS), SMEM_BYTES, s,
-                              p.sk_tiles > 0, ta, tb, p));
+    ST_CUDA_TRY(launch_pdl(gemm_kernel<T, EPI>, dim3(grid), dim3(THREADS), SMEM_BYTES, s, ta, tb, p));
     (void)g;
     return ST_OK;
 }
 
 }  // namespace
-
-size_t gemm_workspace_size() {
-    return (size_t)sm_count() * BM * BN * sizeof(float) + (size_t)sm_count() * sizeof(unsigned) + 256;
-}
 
 bool gemm_supported(const GemmArgs& g) {
     auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
@@ -430,27 +337,6 @@ st_status gemm_sm100(const GemmArgs& g, cudaStream_t s) {
     p.nm = (g.M + BM - 1) / BM;
     p.nn = (g.N + BN - 1) / BN;
     p.nk = (g.K + BK - 1) / BK;
-    // Schedule: whole tiles in full waves, the last (partial) wave plus one full
-    // wave spread over all CTAs as equal (tile, k-block) ranges (stream-K), so
-    // no SM idles through a fractional last wave. Needs the workspace (fp32
-    // pieces + flags, zeroed once) and at least two k-blocks per CTA.
-    const int tiles = p.nm * p.nn * p.Z;
-    const int G = tiles < sm_count() ? tiles : sm_count();
-    p.dp_tiles = tiles;
-    p.sk_tiles = 0;
-    p.partial = nullptr;
-    p.flags = nullptr;
-    if (g.workspace && g.workspace_bytes >= gemm_workspace_size() && tiles % G != 0 && tiles > G) {
-        const int waves = tiles / G;
-        const int sk = tiles - (waves - 1) * G;
-        if ((long long)sk * p.nk >= 2LL * G) {
-            p.dp_tiles = tiles - sk;
-            p.sk_tiles = sk;
-            p.partial = reinterpret_cast<float*>(g.workspace);
-            p.flags = reinterpret_cast<unsigned*>(static_cast<char*>(g.workspace) +
-                                                  (size_t)sm_count() * BM * BN * sizeof(float));
-        }
-    }
     const size_t cbytes = g.epi == kGemmStoreF32 ? 4 : 2;
     p.vec = (reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && ((size_t)g.ldc * cbytes) % 16 == 0 &&
             ((size_t)g.c_stride_z * cbytes) % 16 == 0;
@@ -473,15 +359,12 @@ st_status gemm_sm100(const GemmArgs& g, cudaStream_t s) {
 
 }  // namespace st
 
-extern "C" size_t st_gemm_workspace_size(void) { return st::gemm_workspace_size(); }
-
 extern "C" st_status st_gemm(st_dtype dtype, int M, int N, int K, int Z, const void* A, int lda,
                              const void* W, int ldw, void* C, int ldc, int64_t c_stride_z,
-                             int epilogue, void* workspace, size_t workspace_bytes, void* stream) {
+                             int epilogue, void* stream) {
     if (st_status e = st::require_device()) return e;
     ST_CHECK_ARG(A && W && C, ST_ERR_INVALID_ARGUMENT, "null pointer");
-    st::GemmArgs g{dtype, A, lda, W, ldw, C, c_stride_z, ldc, M, N, K, Z, epilogue, workspace,
-                   workspace_bytes};
+    st::GemmArgs g{dtype, A, lda, W, ldw, C, c_stride_z, ldc, M, N, K, Z, epilogue};
     if (st_status e = st::gemm_sm100(g, st::as_stream(stream))) return e;
     ST_LAUNCH_CHECK();
     return ST_OK;

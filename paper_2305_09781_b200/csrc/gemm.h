@@ -24,11 +24,8 @@ struct GemmArgs {
     int ldc;                // elements
     int M, N, K, Z;
     int epi;
-    void* workspace = nullptr;   // gemm_workspace_size() bytes, zeroed once (stream-K pieces)
-    size_t workspace_bytes = 0;
 };
 
-size_t gemm_workspace_size();
 bool gemm_supported(const GemmArgs& g);
 st_status gemm_sm100(const GemmArgs& g, cudaStream_t s);
 

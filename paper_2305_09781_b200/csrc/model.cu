@@ -185,9 +185,8 @@ layernorm_vec_kernel(const T* __restrict__ x, const T* __restrict__ g, const T* 
 
 // Row-major C[z] (op)= A W[z] on the tcgen05 GEMM (gemm.cu).
 st_status gemm(st_model* m, const void* A, const void* W, int ldw, void* C, int ldc, int M, int N,
-               int K, int Z, long long c_stride_z, int epi, void* ws, cudaStream_t s) {
-    GemmArgs g{m->dtype, A, K, W, ldw, C, c_stride_z, ldc, M, N, K, Z, epi, ws,
-               gemm_workspace_size()};
+               int K, int Z, long long c_stride_z, int epi, cudaStream_t s) {
+    GemmArgs g{m->dtype, A, K, W, ldw, C, c_stride_z, ldc, M, N, K, Z, epi};
     return gemm_sm100(g, s);
 }
 
@@ -307,8 +306,7 @@ size_t st_model_workspace_size(const st_model* m, int B, int T) {
     a.W = (T + 63) / 64;
     a.Lmax = T;
     const size_t es = st::dtype_size(m->dtype);
-    return rows * (6 * d + F) * es + st_tree_attention_workspace_size(&a) +
-           st::gemm_workspace_size() + 9 * 256;
+    return rows * (6 * d + F) * es + st_tree_attention_workspace_size(&a) + 8 * 256;
 }
 
 st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens,
@@ -340,7 +338,6 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
     void* vn = take((size_t)rows * d * es);
     void* o = take((size_t)rows * d * es);
     void* f = take((size_t)rows * F * es);
-    void* gws = take(st::gemm_workspace_size());  // stream-K pieces + flags (zeroed once)
     st_attn_args a{};
     a.dtype = m->dtype;
     a.B = B;
@@ -404,14 +401,14 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
             static_cast<char*>(vn) - static_cast<char*>(kn) == qkv_stride * (long long)es) {
             // wq|wk|wv are consecutive in the serialized order: one batched launch
             if (st_status e = st::gemm(m, h, Wp(L.wq), d, q, d, rows, d, d, 3, qkv_stride,
-                                       st::kGemmStore, gws, s))
+                                       st::kGemmStore, s))
                 return e;
         } else {
-            if (st_status e = st::gemm(m, h, Wp(L.wq), d, q, d, rows, d, d, 1, 0, st::kGemmStore, gws, s))
+            if (st_status e = st::gemm(m, h, Wp(L.wq), d, q, d, rows, d, d, 1, 0, st::kGemmStore, s))
                 return e;
-            if (st_status e = st::gemm(m, h, Wp(L.wk), d, kn, d, rows, d, d, 1, 0, st::kGemmStore, gws, s))
+            if (st_status e = st::gemm(m, h, Wp(L.wk), d, kn, d, rows, d, d, 1, 0, st::kGemmStore, s))
                 return e;
-            if (st_status e = st::gemm(m, h, Wp(L.wv), d, vn, d, rows, d, d, 1, 0, st::kGemmStore, gws, s))
+            if (st_status e = st::gemm(m, h, Wp(L.wv), d, vn, d, rows, d, d, 1, 0, st::kGemmStore, s))
                 return e;
         }
         if (st_status e = st_kv_append(m->dtype, B, T, H, Dh, Lmax, kn, vn, prefix_len, n_nodes, kc,
@@ -423,20 +420,20 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
         a.o = o;
         if (st_status e = st_tree_attention(&a, stream)) return e;
         // x += o W_o (residual add in the epilogue)
-        if (st_status e = st::gemm(m, o, Wp(L.wo), d, x, d, rows, d, d, 1, 0, st::kGemmAddTo, gws, s))
+        if (st_status e = st::gemm(m, o, Wp(L.wo), d, x, d, rows, d, d, 1, 0, st::kGemmAddTo, s))
             return e;
         if (st_status e = layernorm(L.ln2_g, L.ln2_b)) return e;
         // f = gelu(h W_1) (GELU in the epilogue), then x += f W_2
-        if (st_status e = st::gemm(m, h, Wp(L.w1), F, f, F, rows, F, d, 1, 0, st::kGemmGelu, gws, s))
+        if (st_status e = st::gemm(m, h, Wp(L.w1), F, f, F, rows, F, d, 1, 0, st::kGemmGelu, s))
             return e;
-        if (st_status e = st::gemm(m, f, Wp(L.w2), d, x, d, rows, d, F, 1, 0, st::kGemmAddTo, gws, s))
+        if (st_status e = st::gemm(m, f, Wp(L.w2), d, x, d, rows, d, F, 1, 0, st::kGemmAddTo, s))
             return e;
     }
     if (st_status e = layernorm(m->lnf_g, m->lnf_b)) return e;
 #undef ST_M_DISPATCH
     const void* wout = m->wout_pad ? m->wout_pad : Wp(m->wout);
     return st::gemm(m, h, wout, m->ldw_out, logits, c.vocab_size, rows, c.vocab_size, d, 1, 0,
-                    st::kGemmStoreF32, gws, s);
+                    st::kGemmStoreF32, s);
 }
 
 }  // extern "C"
