@@ -21,6 +21,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <type_traits>
 
@@ -247,6 +248,198 @@ gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CU
     if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
+// ---------------------------------------------------------- CTA-pair GEMM ---
+// The same GEMM on 256 x 256 output tiles computed by a CTA PAIR (cluster of
+// 2) with tcgen05.mma.cta_group::2 (M=256, N=256, K=16): CTA r of the pair
+// loads rows [128r, 128r+128) of the A tile and columns [128r, 128r+128) of the
+// W tile (32 KB per 64-deep K block instead of 48 KB per CTA: the pair reads
+// each A and W byte once), the leader (rank 0) issues the MMAs over both CTAs'
+// shared memory, each CTA's TMEM holds its 128 rows of the 256-column
+// accumulator, and each CTA's four epilogue warps store their own rows.
+constexpr int P_STAGES = 6;
+constexpr uint32_t PA_BYTES = 128 * BK * 2;             // 16 KB: this CTA's A half
+constexpr uint32_t PB_BYTES = 2 * B_ATOM;               // 16 KB: this CTA's W half (128 N)
+constexpr uint32_t P_STAGE = PA_BYTES + PB_BYTES;       // 32 KB
+constexpr uint32_t P_OFF_BAR = P_STAGES * P_STAGE;
+constexpr uint32_t P_SMEM = P_OFF_BAR + 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// the leader CTA's copy of a barrier (shared::cluster address with the peer bit cleared)
+__device__ __forceinline__ uint32_t leader_addr(const void* p) { return smem_u32(p) & 0xFEFFFFFFu; }
+__device__ __forceinline__ void tma2_load_2d(void* dst, const CUtensorMap* m, uint32_t bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void tma2_load_3d(void* dst, const CUtensorMap* m, uint32_t bar, int c0, int c1,
+                                             int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void umma2_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// commit: arrive on the barrier at this offset in BOTH CTAs of the pair
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
+        ::"r"(smem_u32(bar)), "h"((unsigned short)3)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+template <class T, int EPI>
+__global__ void __launch_bounds__(THREADS, 1)
+gemm2_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+             const GemmParams p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + P_OFF_BAR);
+    uint64_t* empty = full + P_STAGES;
+    uint64_t* acc_full = empty + P_STAGES;   // [2]
+    uint64_t* acc_empty = acc_full + 2;      // [2] (leader: both CTAs' epilogue warps arrive)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    if (threadIdx.x == 0) {
+        if (smem_u32(smem) & 1023u) __trap();
+        for (int i = 0; i < P_STAGES; ++i) {
+            mbar_init(full + i, 1);
+            mbar_init(empty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(acc_full + i, 1);
+            mbar_init(acc_empty + i, 2 * 4);   // lane 0 of 4 epilogue warps x 2 CTAs
+        }
+        fence_barrier_init();
+    }
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tm_a);
+        prefetch_tmap(&tm_b);
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync();       // both CTAs' barriers initialised, TMEM allocated
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    pdl_trigger();
+    const int nm2 = (p.M + 255) / 256;
+    const int tiles = nm2 * p.nn * p.Z;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+    if (warp == 0) {
+        // ========================= TMA producer (both CTAs) ======================
+        if (lane == 0) {
+            uint32_t kc = 0;
+            for (int t = cid; t < tiles; t += ncl) {
+                const int mb = t % nm2, rest = t / nm2, nb = rest % p.nn, z = rest / p.nn;
+                for (int kb = 0; kb < p.nk; ++kb, ++kc) {
+                    const uint32_t s = kc % P_STAGES;
+                    mbar_wait(empty + s, ((kc / P_STAGES) & 1) ^ 1);
+                    // the leader's full barrier counts both CTAs' bytes
+                    if (rank == 0) mbar_arrive_expect_tx(full + s, 2 * P_STAGE);
+                    const uint32_t fb = leader_addr(full + s);
+                    uint8_t* a = smem + s * P_STAGE;
+                    tma2_load_2d(a, &tm_a, fb, kb * BK, mb * 256 + (int)rank * 128);
+#pragma unroll
+                    for (int j = 0; j < 2; ++j)
+                        tma2_load_3d(a + PA_BYTES + j * B_ATOM, &tm_b, fb,
+                                     nb * BN + (int)rank * 128 + j * 64, kb * BK, z);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (leader CTA only) ======================
+        if (rank == 0) {
+            constexpr uint32_t fmt = std::is_same<T, __half>::value ? 0u : 1u;
+            constexpr uint32_t idesc = idesc_f16(fmt, 256, BN, 0, 1);
+            uint32_t kc = 0, ac = 0;
+            for (int t = cid; t < tiles; t += ncl, ++ac) {
+                const uint32_t acc = ac & 1;
+                mbar_wait(acc_empty + acc, ((ac >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + acc * BN;
+                for (int kb = 0; kb < p.nk; ++kb, ++kc) {
+                    const uint32_t s = kc % P_STAGES;
+                    mbar_wait(full + s, (kc / P_STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t a_base = smem_u32(smem + s * P_STAGE);
+                    const uint64_t ad = smem_desc(a_base, 16, 1024);
+                    const uint64_t bd = smem_desc(a_base + PA_BYTES, B_ATOM, 1024);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk)
+                        umma2_warp(d, ad + ((kk * 32) >> 4), bd + ((kk * 2048) >> 4), idesc,
+                                   (kb | kk) ? 1u : 0u);
+                    umma2_commit_both(empty + s);
+                }
+                umma2_commit_both(acc_full + acc);
+            }
+        }
+    } else {
+        // ======================= epilogue (both CTAs) ============================
+        const int q = warp & 3;
+        const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+        const uint32_t ae0 = leader_addr(acc_empty), ae1 = leader_addr(acc_empty + 1);
+        uint32_t ac = 0;
+        for (int t = cid; t < tiles; t += ncl, ++ac) {
+            const int mb = t % nm2, rest = t / nm2, nb = rest % p.nn, z = rest / p.nn;
+            const uint32_t acc = ac & 1;
+            mbar_wait(acc_full + acc, (ac >> 1) & 1);
+            tc_fence_after();
+            const int row = mb * 256 + (int)rank * 128 + q * 32 + lane;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                const int col0 = nb * BN + c * 32;
+                if (col0 >= p.N) break;
+                uint32_t raw[32];
+                tmem_ld_32x32b_x32(lane_base + acc * BN + c * 32, raw);
+                tmem_ld_wait();
+                float v[32];
+#pragma unroll
+                for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(raw[k]);
+                epilogue_chunk<T, EPI>(p, z, row, col0, v);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(acc ? ae1 : ae0);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();       // no CTA leaves while its peer may still use its memory
+    tc_fence_after();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -283,6 +476,49 @@ st_status launch(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb
     const int grid = tiles < sm_count() ? tiles : sm_count();
     ST_CUDA_TRY(launch_pdl(gemm_kernel<T, EPI>, dim3(grid), dim3(THREADS), SMEM_BYTES, s, ta, tb, p));
     (void)g;
+    return ST_OK;
+}
+
+template <class T, int EPI>
+st_status launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p,
+                      cudaStream_t s) {
+    static int max_clusters = 0;
+    if (!max_clusters) {
+        ST_CUDA_TRY(cudaFuncSetAttribute(gemm2_kernel<T, EPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM));
+        ST_CUDA_TRY(cudaFuncSetAttribute(gemm2_kernel<T, EPI>,
+                                         cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * sm_count());
+        cfg.blockDim = dim3(THREADS);
+        cfg.dynamicSmemBytes = P_SMEM;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        ST_CUDA_TRY(cudaOccupancyMaxActiveClusters(&max_clusters, gemm2_kernel<T, EPI>, &cfg));
+        if (max_clusters < 1) max_clusters = 1;
+    }
+    const int tiles = ((p.M + 255) / 256) * p.nn * p.Z;
+    const int clusters = tiles < max_clusters ? tiles : max_clusters;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = P_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    ST_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm2_kernel<T, EPI>, ta, tb, p));
     return ST_OK;
 }
 
@@ -340,12 +576,18 @@ st_status gemm_sm100(const GemmArgs& g, cudaStream_t s) {
     const size_t cbytes = g.epi == kGemmStoreF32 ? 4 : 2;
     p.vec = (reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && ((size_t)g.ldc * cbytes) % 16 == 0 &&
             ((size_t)g.c_stride_z * cbytes) % 16 == 0;
+    static const bool pair_env = !(getenv("ST_GEMM_PAIR") && atoi(getenv("ST_GEMM_PAIR")) == 0);
+    const bool pair = pair_env && g.M >= 256;
 #define ST_GEMM_EPI(TT)                                                              \
     switch (g.epi) {                                                                 \
-        case kGemmStore: return launch<TT, kGemmStore>(g, ta, tb, p, s);             \
-        case kGemmGelu: return launch<TT, kGemmGelu>(g, ta, tb, p, s);               \
-        case kGemmAddTo: return launch<TT, kGemmAddTo>(g, ta, tb, p, s);             \
-        case kGemmStoreF32: return launch<TT, kGemmStoreF32>(g, ta, tb, p, s);       \
+        case kGemmStore: return pair ? launch_pair<TT, kGemmStore>(ta, tb, p, s)     \
+                                     : launch<TT, kGemmStore>(g, ta, tb, p, s);      \
+        case kGemmGelu: return pair ? launch_pair<TT, kGemmGelu>(ta, tb, p, s)       \
+                                    : launch<TT, kGemmGelu>(g, ta, tb, p, s);        \
+        case kGemmAddTo: return pair ? launch_pair<TT, kGemmAddTo>(ta, tb, p, s)     \
+                                     : launch<TT, kGemmAddTo>(g, ta, tb, p, s);      \
+        case kGemmStoreF32: return pair ? launch_pair<TT, kGemmStoreF32>(ta, tb, p, s) \
+                                        : launch<TT, kGemmStoreF32>(g, ta, tb, p, s); \
     }
     if (g.dtype == ST_F16) {
         ST_GEMM_EPI(__half)

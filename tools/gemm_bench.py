@@ -1,4 +1,4 @@
-"""Diagnostic: the tcgen05 GEMM (st_gemm) vs cuBLAS (torch.matmul) at the C3
+"""Diagnostic (ST_GEMM_PAIR=0: single-CTA tiles only): the tcgen05 GEMM (st_gemm) vs cuBLAS (torch.matmul) at the C3
 projection shapes (M = B*T = 2048 rows, d = 4096, FFN 16384, V = 32000), f16,
 CUDA events, mean of N launches after warm-up.
 
