@@ -67,11 +67,13 @@ def parse(argv=None):
     ap.add_argument("--tree-rows", default="own", choices=["own", "cache"],
                     help="K1 reads the tree rows from their own tensors (no append) or "
                          "from the cache after a K2 append")
-    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5"],
+    ap.add_argument("--config", default="c2", choices=["c2", "c3", "c4", "c5", "c3e"],
                     help="c2 (default, the headline metric); c3: full 32-layer 7B-shape stack, "
                          "batch 32 partitioned over the ranks, stochastic verification; c4: "
                          "LLaMA-65B-shape attention layer, heads sharded over the ranks; c5: "
-                         "long-context verify step (B=16 per GPU, --kv, --tree)")
+                         "long-context verify step (B=16 per GPU, --kv, --tree); c3e: C3 model "
+                         "shapes end to end through the device engine (st_engine: GPU drafting, "
+                         "greedy tree verification, generation until every budget is spent)")
     ap.add_argument("--kv", type=int, default=32768, help="c5: committed KV rows")
     ap.add_argument("--tree", type=int, default=128, help="c5: tree nodes")
     ap.add_argument("--gather", default="nccl", choices=["nccl", "peer"],
@@ -661,6 +663,8 @@ def main():
         return run_c3(args)
     if args.config == "c4":
         return run_c4(args)
+    if args.config == "c3e":
+        return run_c3e(args)
     return run_verify(args)
 
 
@@ -1136,6 +1140,67 @@ def run_c3(args):
                          "hbm_bytes_per_step_per_gpu": wbytes + kvbytes,
                          "note": "whole-step figure: the GEMMs dominate (intensity ~ B*T rows)"},
             "verified_tokens_per_step": accepted * world, "clocks": clk}))
+    finish_rank(world)
+
+
+# ---------------------------------------------------------------- C3 e2e ----
+def run_c3e(args):
+    """C3 model shapes END TO END through the device-resident engine
+    (st_engine): LLM = LLaMA-7B-shape stack (reference recipe: 32 layers,
+    d=4096, 32 heads, FFN x4, V=32000), draft model = a 2-layer model of the
+    same width, 32 requests partitioned over the ranks, 128-token prompts,
+    expansion trees <1,1,3,1,1,1,1,1> drafted on the GPU, greedy tree
+    verification, 64 new tokens per request. Timed: prompt upload + prefill +
+    every step until all budgets are spent, with the per-step D2H read of the
+    accepted tokens (what a serving loop does). Random weights: the draft model
+    does not predict the LLM, so most steps accept the bonus token only — the
+    number measures the engine's machinery at C3 shapes, not acceptance."""
+    import torch
+
+    from paper_2305_09781_b200 import _capi
+
+    rank, world, local, dev = init_rank(args)
+    NL, d, Hh, Vv, BG, PROMPT, NEW = 32, 4096, 32, 32000, 32, 128, 64
+    lo = BG * rank // world
+    Bl = BG * (rank + 1) // world - lo
+    expansion = (1, 1, 3, 1, 1, 1, 1, 1)
+    llm = _capi.DeviceModel(NL, Hh, d, Vv, PROMPT + NEW + 64, 4, seed=42, dtype=torch.float16)
+    ssm = _capi.DeviceModel(2, Hh, d, Vv, PROMPT + NEW + 64, 4, seed=7, dtype=torch.float16)
+    eng = _capi.Engine(llm, ssm, Bl, PROMPT, expansion=expansion)
+    rng = np.random.default_rng(11 + rank)
+    prompts = [rng.integers(0, Vv, PROMPT).tolist() for _ in range(Bl)]
+    budgets = [NEW] * Bl
+    barrier = barrier_of(world)
+    eng.run(prompts, [4] * Bl)          # warm-up (kernel attributes, tensor maps)
+    barrier()
+    clocks = ClockSampler(local)
+    time.sleep(0.5)
+    barrier()
+    t0 = time.perf_counter()
+    seqs, steps = eng.run(prompts, budgets)
+    barrier()
+    wall = time.perf_counter() - t0
+    clk = clocks.stop()
+    generated = sum(len(q) - PROMPT for q in seqs)
+    (wall, steps_max) = max_over_ranks(world, dev, wall, float(steps))
+    total = generated * world if world > 1 else generated
+    if rank == 0:
+        print(json.dumps({
+            "metric": "generated tokens/s (C3 shapes, device engine, end to end)",
+            "value": total / wall, "unit": "tokens/s", "n_gpus": world, "steps": int(steps_max),
+            "warmup": 1, "ms_per_step": wall / steps_max * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+            "config": {"workload": "C3 shapes through st_engine: 32-layer d=4096 LLM, 2-layer "
+                                   "draft model, expansion <1,1,3,1,1,1,1,1> drafted on the GPU, "
+                                   "greedy verification, 128-token prompts, 64 new tokens",
+                       "B_global": BG, "B_per_gpu": Bl, "tree_nodes": eng.T,
+                       "parallelism": f"dp{world} (requests partitioned)"},
+            "tokens_per_step_per_request": generated / max(1, Bl) / max(1, steps),
+            "e2e": {"value": total / wall, "unit": "tokens/s",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": (eng.T + 3) * Bl * 4,
+                    "note": "prompts uploaded once; per step only the accepted tokens, lengths "
+                            "and done flags come back"},
+            "clocks": clk}))
     finish_rank(world)
 
 
