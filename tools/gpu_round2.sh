@@ -21,3 +21,7 @@ timeout 600 python tools/sweep_gqa.py --out $OUT/$TAG.gqa_sweep.json > $OUT/$TAG
 timeout 300 python bench.py --config c4 > $OUT/$TAG.c4.json 2> $OUT/$TAG.c4.err; echo "c4 rc=$?"
 timeout 120 python tools/c4_slice.py --out $OUT/$TAG.c4_slice.json > $OUT/$TAG.c4_slice.txt 2>&1; echo "c4 slice rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/$TAG.ref.json 2> $OUT/$TAG.ref.err; echo "ref rc=$?"
+timeout 300 python tools/gemm_bench.py > $OUT/$TAG.gemm.txt 2>&1; echo "gemm rc=$?"
+timeout 600 python bench.py --config c3 --steps 5 --warmup 2 > $OUT/$TAG.c3.json 2> $OUT/$TAG.c3.err; echo "c3 rc=$?"
+timeout 600 python bench.py --config c3e > $OUT/$TAG.c3e.json 2> $OUT/$TAG.c3e.err; echo "c3e rc=$?"
+timeout 300 python tools/step_modes.py > $OUT/$TAG.step_modes.txt 2>&1; echo "modes rc=$?"
