@@ -1,5 +1,6 @@
 """The reference's OWN C++ unit suites (proj/tests/token_tree_test.cpp,
-proj/tests/transformer_test.cpp and acceptance criteria #2/#3/#4/#7 of
+proj/tests/transformer_test.cpp, proj/tests/engine_test.cpp and acceptance
+criteria #2/#3/#4/#7 of
 proj/tests/acceptance_test.cpp, compiled unchanged by tests/cpp/Makefile
 against include/spectree + libspectree_b200.so) and our engine parity test,
 run on the GPU. Tolerances are the reference's own (tokens exact, logits
@@ -15,8 +16,8 @@ BIN = os.path.join(ROOT, "build", "reftests")
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name", ["token_tree_test", "transformer_test", "engine_parity_test",
-                                  "acceptance_subset_test"])
+@pytest.mark.parametrize("name", ["token_tree_test", "transformer_test", "engine_test",
+                                  "engine_parity_test", "acceptance_subset_test"])
 def test_suite(name):
     import torch
     if not torch.cuda.is_available():
