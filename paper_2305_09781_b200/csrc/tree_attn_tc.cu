@@ -446,7 +446,10 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (warp == SW) {
         // ======================= TMA producer: Q and K =========================
         if (lane == 0) {
-            const uint64_t pol = l2_policy_evict_first();  // the KV stream is read once
+            // the KV stream is read once (R = 1): evict_first keeps Q, masks and
+            // pieces in L2. With two row blocks (R = 2) both CTAs of a slot read
+            // every tile: normal priority, so the second read finds it in L2.
+            const uint64_t pol = p.R == 1 ? l2_policy_evict_first() : l2_policy_evict_normal();
             uint32_t qc = 0, kc = 0;
             bool waited = !p.early_kv;
             for (uint32_t t = t_begin; t < t_end;) {
@@ -546,7 +549,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     } else if (warp == SW + 1) {
         // =========================== TMA producer: V ============================
         if (lane == 0) {
-            const uint64_t pol = l2_policy_evict_first();
+            const uint64_t pol = p.R == 1 ? l2_policy_evict_first() : l2_policy_evict_normal();
             uint32_t vc = 0;
             bool waited = !p.early_kv;
             for (uint32_t t = t_begin; t < t_end;) {
