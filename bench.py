@@ -1052,9 +1052,10 @@ def run_c3(args):
     recipe: 32 layers, d=4096, 32 heads, FFN x4, V=32000, learned positions), a
     global batch of 32 requests partitioned over the ranks (strong scaling),
     64-node trees over 2048 committed rows, stochastic multi-step speculative
-    sampling (K4). One step = tree embedding -> 32 x [LN, QKV/WO/FFN GEMMs, K2
-    append, K1] -> LM head -> K4 MSS verify -> K2 compaction on all 32 layers
-    (+ accepted-token all-gather for N > 1). Synthetic KV prefix and draft
+    sampling (K4). One step = tree embedding -> 32 x [LN, QKV GEMM (tree K/V
+    kept per layer), K1 (k_tree mode), WO/FFN GEMMs with fused GELU / residual]
+    -> LM head -> K4 MSS verify -> K2 commit of the accepted rows of all 32
+    layers (+ accepted-token all-gather for N > 1). Synthetic KV prefix and draft
     distributions; weights generated on the GPU from UniformStream(42)."""
     import torch
 
@@ -1085,10 +1086,14 @@ def run_c3(args):
     logits = torch.empty(Bl, T, Vv, dtype=torch.float32, device=dev)
     gathered = torch.zeros(world * Bl * (T + 2), dtype=torch.int32, device=dev)
 
+    # k_tree mode: every layer's tree K/V stay in tree_qkv (no per-layer
+    # append); the accepted rows of all 32 layers are committed from there
+    tree_qkv = model.new_tree_qkv(Bl, T)
+
     def step():
-        model.tree_forward(tok, pos, mask, P, nn, kc, vc, logits=logits)
+        model.tree_forward(tok, pos, mask, P, nn, kc, vc, logits=logits, tree_qkv=tree_qkv)
         ver, ids, ln = _capi.verify_mss(logits, qd, tok, par, nn, 1.0, U)
-        _capi.kv_compact(ids, ln, P, kc, vc)
+        _capi.kv_commit_tree(ids, ln, P, tree_qkv, kc, vc, T)
         if world > 1:
             gather_accepted(ver, ln, world, out=gathered)
         return ln

@@ -145,6 +145,17 @@ st_status st_kv_compact(st_dtype dtype, int B, int Hkv, int D, int64_t Lmax, int
                         const int32_t* n_keep, const int32_t* prefix_len,
                         int32_t* new_prefix_len, void* k_cache, void* v_cache, void* stream);
 
+/* The same commit from the tree's own K/V (K1's k_tree mode: no append
+ * preceded it): cache[l][b][h][P + k] = tree[l][b][ids[k]][h] for k in
+ * [0, n_keep[b]); tree layer l at k_tree + l * tree_layer_stride elements,
+ * [B][T][Hkv][D] each. */
+st_status st_kv_commit_tree(st_dtype dtype, int B, int T, int Hkv, int D, int64_t Lmax,
+                            int n_layers, int64_t layer_stride, const int32_t* ids,
+                            int ids_stride, const int32_t* n_keep, const int32_t* prefix_len,
+                            int32_t* new_prefix_len, const void* k_tree, const void* v_tree,
+                            int64_t tree_layer_stride, void* k_cache, void* v_cache,
+                            void* stream);
+
 /* Head-sharded attention (C4): reorder an all-gathered
  * [world][B][T][Hl][D] (rank r's K1 output for heads r*Hl..r*Hl+Hl-1) into
  * [B][T][world*Hl][D]. */
@@ -277,6 +288,18 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
                                 const int32_t* prefix_len, const int32_t* n_nodes, void* k_cache,
                                 void* v_cache, int64_t Lmax, float* logits, void* workspace,
                                 size_t workspace_bytes, void* stream);
+/* The same pass in K1's k_tree mode: every layer's Q|K|V projection is written
+ * to tree_qkv [num_layers][3][B*T][d_model] and K1 reads the tree rows from
+ * there — no per-layer K2 append into the caches (rows [P, P+n) untouched).
+ * After verification, st_kv_commit_tree(ids, len, ..., k_tree = tree_qkv +
+ * B*T*d, v_tree = tree_qkv + 2*B*T*d, tree_layer_stride = 3*B*T*d) commits the
+ * accepted rows of every layer. */
+st_status st_model_tree_forward_kt(st_model* m, int B, int T, const int32_t* tokens,
+                                   const int32_t* positions, const uint64_t* mask, int W,
+                                   const int32_t* prefix_len, const int32_t* n_nodes,
+                                   void* k_cache, void* v_cache, int64_t Lmax, void* tree_qkv,
+                                   float* logits, void* workspace, size_t workspace_bytes,
+                                   void* stream);
 
 /* ------------------------------------------------- verification step plan ---
  * One verification step of a batch as a prepared object:

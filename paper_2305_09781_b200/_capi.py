@@ -100,6 +100,10 @@ SIGNATURES = {
     "st_verify_plan_create": (_I, [_V, _V]),
     "st_verify_plan_run": (_I, [_V, _V]),
     "st_verify_plan_destroy": (None, [_V]),
+    "st_kv_commit_tree": (_I, [_I, _I, _I, _I, _I, _I64, _I, _I64, _V, _I, _V, _V, _V, _V, _V,
+                               _I64, _V, _V, _V]),
+    "st_model_tree_forward_kt": (_I, [_V, _I, _I, _V, _V, _V, _I, _V, _V, _V, _V, _I64, _V, _V,
+                                      _V, _Z, _V]),
     "st_gemm": (_I, [_I, _I, _I, _I, _I, _V, _I, _V, _I, _V, _I, _I64, _I, _V]),
 }
 
@@ -252,6 +256,22 @@ def kv_compact(ids, n_keep, prefix_len, k_cache, v_cache, new_prefix_len=None, s
                               _stream(stream)))
 
 
+def kv_commit_tree(ids, n_keep, prefix_len, tree_qkv, k_cache, v_cache, T, new_prefix_len=None,
+                   stream=None):
+    """Commit the accepted rows of every layer from tree_qkv
+    ([L][3][B*T][d], DeviceModel.new_tree_qkv) into the caches [L][B][H][Lmax][D]."""
+    n_layers, B, Hkv, Lmax, D = k_cache.shape
+    rows = tree_qkv.shape[2]
+    assert rows == B * T
+    k_tree = tree_qkv[0, 1]
+    v_tree = tree_qkv[0, 2]
+    check(lib().st_kv_commit_tree(DTYPES[k_cache.dtype], B, T, Hkv, D, Lmax, n_layers,
+                                  k_cache[0].numel(), _ptr(ids), ids.shape[-1], _ptr(n_keep),
+                                  _ptr(prefix_len), _ptr(new_prefix_len), _ptr(k_tree),
+                                  _ptr(v_tree), tree_qkv[0].numel(), _ptr(k_cache), _ptr(v_cache),
+                                  _stream(stream)))
+
+
 def heads_gather_layout(gathered, world, out=None, stream=None):
     """[world, B, T, Hl, D] -> [B, T, world*Hl, D] (C4 head-sharded outputs)."""
     W, B, T, Hl, D = gathered.shape
@@ -388,8 +408,15 @@ class DeviceModel:
         return (torch.zeros(shape, dtype=self.dtype, device=device),
                 torch.zeros(shape, dtype=self.dtype, device=device))
 
+    def new_tree_qkv(self, B, T, device="cuda"):
+        """[num_layers][3][B*T][d_model] buffer for tree_forward's k_tree mode."""
+        c = self.cfg
+        return torch.zeros((c.num_layers, 3, B * T, c.d_model), dtype=self.dtype, device=device)
+
     def tree_forward(self, tokens, positions, mask, prefix_len, n_nodes, k_cache, v_cache,
-                     logits=None, stream=None):
+                     logits=None, stream=None, tree_qkv=None):
+        """tree_qkv (optional, new_tree_qkv): K1's k_tree mode — the tree rows
+        stay in tree_qkv (no per-layer append); commit with kv_commit_tree."""
         B, T = tokens.shape
         if logits is None:
             logits = torch.empty((B, T, self.cfg.vocab_size), dtype=torch.float32,
@@ -397,11 +424,19 @@ class DeviceModel:
         need = int(lib().st_model_workspace_size(self.handle, B, T))
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.zeros(need, dtype=torch.uint8, device=tokens.device)
-        check(lib().st_model_tree_forward(self.handle, B, T, _ptr(tokens), _ptr(positions),
-                                          _ptr(mask), mask.shape[-1], _ptr(prefix_len),
-                                          _ptr(n_nodes), _ptr(k_cache), _ptr(v_cache),
-                                          k_cache.shape[-2], _ptr(logits), _ptr(self._ws),
-                                          self._ws.numel(), _stream(stream)))
+        if tree_qkv is None:
+            check(lib().st_model_tree_forward(self.handle, B, T, _ptr(tokens), _ptr(positions),
+                                              _ptr(mask), mask.shape[-1], _ptr(prefix_len),
+                                              _ptr(n_nodes), _ptr(k_cache), _ptr(v_cache),
+                                              k_cache.shape[-2], _ptr(logits), _ptr(self._ws),
+                                              self._ws.numel(), _stream(stream)))
+        else:
+            check(lib().st_model_tree_forward_kt(self.handle, B, T, _ptr(tokens), _ptr(positions),
+                                                 _ptr(mask), mask.shape[-1], _ptr(prefix_len),
+                                                 _ptr(n_nodes), _ptr(k_cache), _ptr(v_cache),
+                                                 k_cache.shape[-2], _ptr(tree_qkv), _ptr(logits),
+                                                 _ptr(self._ws), self._ws.numel(),
+                                                 _stream(stream)))
         return logits
 
 

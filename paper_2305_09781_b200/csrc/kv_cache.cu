@@ -99,14 +99,17 @@ tree_prepare_kernel(const char* __restrict__ k_new, const char* __restrict__ v_n
         build_masks_block(parent, n_nodes, T, W, mask, blockIdx.x - T, blockIdx.y, s_par);
 }
 
-// st_kv_compact: block (b, layer * nhc + hc) moves the accepted rows of its
-// hpb KV heads of one layer (kv_move.cuh: chunked, no per-row barrier chain).
+// st_kv_compact / st_kv_commit_tree: block (b, layer * nhc + hc) moves the
+// accepted rows of its hpb KV heads of one layer (kv_move.cuh: chunked, no
+// per-row barrier chain) — in place (rows 1.. from cache row P + ids[k]), or
+// from the tree's own K/V (k_tree != NULL: rows 0.. from tree[b][ids[k]][h]).
 template <class V>
 __global__ void __launch_bounds__(256)
 kv_compact_kernel(const int32_t* __restrict__ ids, int ids_stride, const int32_t* __restrict__ n_keep,
                   const int32_t* __restrict__ prefix_len, int32_t* __restrict__ new_prefix_len,
                   char* k_cache, char* v_cache, int Hkv, int row_vecs, int64_t Lmax,
-                  int64_t layer_stride_bytes, int nhc, int hpb) {
+                  int64_t layer_stride_bytes, int nhc, int hpb, const char* k_tree,
+                  const char* v_tree, int64_t tree_layer_stride_bytes, int T) {
     extern __shared__ int s_ids[];  // ids_stride ints
     pdl_wait();
     pdl_trigger();
@@ -117,10 +120,12 @@ kv_compact_kernel(const int32_t* __restrict__ ids, int ids_stride, const int32_t
     __syncthreads();
     if (new_prefix_len && blockIdx.y == 0 && threadIdx.x == 0) new_prefix_len[b] = (int32_t)(P + keep);
     const int h0 = hc * hpb, nh = min(hpb, Hkv - h0);
-    if (keep <= 1 || nh <= 0) return;
-    move_rows_block<V>(s_ids, keep, 1, b, h0, nh, Hkv, row_vecs, Lmax, P,
+    const int kfirst = k_tree ? 0 : 1;
+    if (keep <= kfirst || nh <= 0) return;
+    move_rows_block<V>(s_ids, keep, kfirst, b, h0, nh, Hkv, row_vecs, Lmax, P,
                        k_cache + layer * layer_stride_bytes, v_cache + layer * layer_stride_bytes,
-                       nullptr, nullptr, 0);
+                       k_tree ? k_tree + layer * tree_layer_stride_bytes : nullptr,
+                       v_tree ? v_tree + layer * tree_layer_stride_bytes : nullptr, T);
 }
 
 }  // namespace
@@ -178,10 +183,11 @@ st_status st_tree_prepare(st_dtype dtype, int B, int T, int Hkv, int D, int64_t 
     return ST_OK;
 }
 
-st_status st_kv_compact(st_dtype dtype, int B, int Hkv, int D, int64_t Lmax, int n_layers,
-                        int64_t layer_stride, const int32_t* ids, int ids_stride,
-                        const int32_t* n_keep, const int32_t* prefix_len,
-                        int32_t* new_prefix_len, void* k_cache, void* v_cache, void* stream) {
+static st_status kv_commit(st_dtype dtype, int B, int Hkv, int D, int64_t Lmax, int n_layers,
+                           int64_t layer_stride, const int32_t* ids, int ids_stride,
+                           const int32_t* n_keep, const int32_t* prefix_len,
+                           int32_t* new_prefix_len, const void* k_tree, const void* v_tree, int T,
+                           int64_t tree_layer_stride, void* k_cache, void* v_cache, void* stream) {
     if (st_status e = st::require_device()) return e;
     ST_CHECK_ARG(B >= 0 && Hkv >= 1 && D >= 1 && n_layers >= 1 && ids_stride >= 1,
                  ST_ERR_SHAPE_MISMATCH, "bad shape");
@@ -203,9 +209,30 @@ st_status st_kv_compact(st_dtype dtype, int B, int Hkv, int D, int64_t Lmax, int
     ST_CUDA_TRY(st::launch_pdl(vec ? st::kv_compact_kernel<int4> : st::kv_compact_kernel<char>,
                                dim3(B, n_layers * nhc), dim3(256), (size_t)ids_stride * sizeof(int), s,
                                ids, ids_stride, n_keep, prefix_len, new_prefix_len, (char*)k_cache,
-                               (char*)v_cache, Hkv, row_vecs, Lmax, layer_stride * es, nhc, hpb));
+                               (char*)v_cache, Hkv, row_vecs, Lmax, layer_stride * es, nhc, hpb,
+                               (const char*)k_tree, (const char*)v_tree, tree_layer_stride * es, T));
     ST_LAUNCH_CHECK();
     return ST_OK;
+}
+
+st_status st_kv_compact(st_dtype dtype, int B, int Hkv, int D, int64_t Lmax, int n_layers,
+                        int64_t layer_stride, const int32_t* ids, int ids_stride,
+                        const int32_t* n_keep, const int32_t* prefix_len,
+                        int32_t* new_prefix_len, void* k_cache, void* v_cache, void* stream) {
+    return kv_commit(dtype, B, Hkv, D, Lmax, n_layers, layer_stride, ids, ids_stride, n_keep,
+                     prefix_len, new_prefix_len, nullptr, nullptr, 0, 0, k_cache, v_cache, stream);
+}
+
+st_status st_kv_commit_tree(st_dtype dtype, int B, int T, int Hkv, int D, int64_t Lmax,
+                            int n_layers, int64_t layer_stride, const int32_t* ids,
+                            int ids_stride, const int32_t* n_keep, const int32_t* prefix_len,
+                            int32_t* new_prefix_len, const void* k_tree, const void* v_tree,
+                            int64_t tree_layer_stride, void* k_cache, void* v_cache,
+                            void* stream) {
+    ST_CHECK_ARG(k_tree && v_tree && T >= 1, ST_ERR_INVALID_ARGUMENT, "k_tree / v_tree / T");
+    return kv_commit(dtype, B, Hkv, D, Lmax, n_layers, layer_stride, ids, ids_stride, n_keep,
+                     prefix_len, new_prefix_len, k_tree, v_tree, T, tree_layer_stride, k_cache,
+                     v_cache, stream);
 }
 
 }  // extern "C"

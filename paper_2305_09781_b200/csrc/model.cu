@@ -309,11 +309,11 @@ size_t st_model_workspace_size(const st_model* m, int B, int T) {
     return rows * (6 * d + F) * es + st_tree_attention_workspace_size(&a) + 8 * 256;
 }
 
-st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens,
-                                const int32_t* positions, const uint64_t* mask, int W,
-                                const int32_t* prefix_len, const int32_t* n_nodes, void* k_cache,
-                                void* v_cache, int64_t Lmax, float* logits, void* workspace,
-                                size_t workspace_bytes, void* stream) {
+static st_status tree_forward(st_model* m, int B, int T, const int32_t* tokens,
+                              const int32_t* positions, const uint64_t* mask, int W,
+                              const int32_t* prefix_len, const int32_t* n_nodes, void* k_cache,
+                              void* v_cache, int64_t Lmax, void* tree_qkv, float* logits,
+                              void* workspace, size_t workspace_bytes, void* stream) {
     if (st_status e = st::require_device()) return e;
     ST_CHECK_ARG(m && tokens && positions && mask && prefix_len && n_nodes && k_cache && v_cache &&
                      logits && workspace,
@@ -353,8 +353,9 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
     a.scale = 1.0 / std::sqrt((double)Dh);
     a.workspace = ws;
     a.workspace_bytes = st_tree_attention_workspace_size(&a);
-    // K1's predecessor is the layer's K2 append (tree rows [P, P+n) only): the
-    // committed rows and the lengths are stable, so K1 may stream them early
+    // K1's predecessor is the layer's K2 append (tree rows [P, P+n) only) or,
+    // in k_tree mode, the QKV GEMM: the committed rows and the lengths are
+    // stable, so K1 may stream them early
     a.early_kv = 1;
     const size_t layer_elems = (size_t)B * H * Lmax * Dh;
     auto Wp = [&](size_t off) -> const void* { return static_cast<const char*>(m->buf) + off * es; };
@@ -396,6 +397,11 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
         void* vc = static_cast<char*>(v_cache) + (size_t)l * layer_elems * es;
         if (st_status e = layernorm(L.ln1_g, L.ln1_b)) return e;
         const size_t dd = (size_t)d * d;
+        if (tree_qkv) {  // k_tree mode: this layer's Q|K|V stay in the caller's buffer
+            q = static_cast<char*>(tree_qkv) + (size_t)l * 3 * rows * d * es;
+            kn = static_cast<char*>(q) + (size_t)rows * d * es;
+            vn = static_cast<char*>(kn) + (size_t)rows * d * es;
+        }
         const long long qkv_stride = (static_cast<char*>(kn) - static_cast<char*>(q)) / (long long)es;
         if (L.wk == L.wq + dd && L.wv == L.wk + dd &&
             static_cast<char*>(vn) - static_cast<char*>(kn) == qkv_stride * (long long)es) {
@@ -411,13 +417,17 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
             if (st_status e = st::gemm(m, h, Wp(L.wv), d, vn, d, rows, d, d, 1, 0, st::kGemmStore, s))
                 return e;
         }
-        if (st_status e = st_kv_append(m->dtype, B, T, H, Dh, Lmax, kn, vn, prefix_len, n_nodes, kc,
-                                       vc, stream))
-            return e;
+        if (!tree_qkv) {
+            if (st_status e = st_kv_append(m->dtype, B, T, H, Dh, Lmax, kn, vn, prefix_len, n_nodes,
+                                           kc, vc, stream))
+                return e;
+        }
         a.q = q;
         a.k_cache = kc;
         a.v_cache = vc;
         a.o = o;
+        a.k_tree = tree_qkv ? kn : nullptr;
+        a.v_tree = tree_qkv ? vn : nullptr;
         if (st_status e = st_tree_attention(&a, stream)) return e;
         // x += o W_o (residual add in the epilogue)
         if (st_status e = st::gemm(m, o, Wp(L.wo), d, x, d, rows, d, d, 1, 0, st::kGemmAddTo, s))
@@ -434,6 +444,26 @@ st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens
     const void* wout = m->wout_pad ? m->wout_pad : Wp(m->wout);
     return st::gemm(m, h, wout, m->ldw_out, logits, c.vocab_size, rows, c.vocab_size, d, 1, 0,
                     st::kGemmStoreF32, s);
+}
+
+st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens,
+                                const int32_t* positions, const uint64_t* mask, int W,
+                                const int32_t* prefix_len, const int32_t* n_nodes, void* k_cache,
+                                void* v_cache, int64_t Lmax, float* logits, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+    return tree_forward(m, B, T, tokens, positions, mask, W, prefix_len, n_nodes, k_cache, v_cache,
+                        Lmax, nullptr, logits, workspace, workspace_bytes, stream);
+}
+
+st_status st_model_tree_forward_kt(st_model* m, int B, int T, const int32_t* tokens,
+                                   const int32_t* positions, const uint64_t* mask, int W,
+                                   const int32_t* prefix_len, const int32_t* n_nodes,
+                                   void* k_cache, void* v_cache, int64_t Lmax, void* tree_qkv,
+                                   float* logits, void* workspace, size_t workspace_bytes,
+                                   void* stream) {
+    ST_CHECK_ARG(tree_qkv != nullptr, ST_ERR_INVALID_ARGUMENT, "null tree_qkv");
+    return tree_forward(m, B, T, tokens, positions, mask, W, prefix_len, n_nodes, k_cache, v_cache,
+                        Lmax, tree_qkv, logits, workspace, workspace_bytes, stream);
 }
 
 }  // extern "C"

@@ -79,3 +79,68 @@ def test_c1_logits_match_reference(capi, restatement, golden, dtype, tol):
         assert gap[u] <= 2 * tol, f"node {u}: argmax differs with reference top-2 gap {gap[u]:.3e}"
     print(f"{dtype}: greedy agreement {n - len(disagree)}/{n}; disagreements at reference "
           f"top-2 gaps {[float(gap[u]) for u in disagree]}")
+
+
+def test_tree_forward_k_tree_mode_and_commit(capi, restatement):
+    """st_model_tree_forward_kt (K1 reads each layer's tree rows from the
+    Q|K|V buffer, no per-layer append) gives the same logits as the append
+    mode within f16 accumulation-order noise, leaves cache rows [P, P+n)
+    untouched, and st_kv_commit_tree of the accepted ids produces exactly the
+    caches that append + in-place compaction produce."""
+    from tests.treegen import pack, width_depth_seqs
+    rng = np.random.default_rng(5)
+    L_, H, d, V = 2, 4, 512, 512
+    model = capi.DeviceModel(L_, H, d, V, 256, 4, seed=9, dtype=torch.float16)
+    trees = [restatement.merge(width_depth_seqs(rng, int(rng.integers(0, V)), V, 3, 5), 1024)
+             for _ in range(3)]
+    tok, par, dep, n = pack(trees)
+    B, T = tok.shape
+    dev = "cuda"
+    P = torch.tensor([40, 7, 100], dtype=torch.int32, device=dev)
+    tk, pr, nd = (torch.tensor(x, device=dev) for x in (tok, par, n))
+    pos = (P[:, None] + torch.tensor(dep, device=dev)).to(torch.int32)
+    mask = capi.build_masks(pr, nd)
+    kc, vc = model.new_cache(B, 128 + T)
+    kc.uniform_(-1, 1)
+    vc.uniform_(-1, 1)
+    k1, v1 = kc.clone(), vc.clone()
+    la = model.tree_forward(tk, pos, mask, P, nd, k1, v1)
+    k2, v2 = kc.clone(), vc.clone()
+    qkv = model.new_tree_qkv(B, T)
+    lb = model.tree_forward(tk, pos, mask, P, nd, k2, v2, tree_qkv=qkv)
+    torch.cuda.synchronize()
+    for b in range(B):
+        k = int(n[b])
+        assert (la[b, :k] - lb[b, :k]).abs().max().item() < 2e-3
+    assert torch.equal(k2, kc) and torch.equal(v2, vc)   # no append in k_tree mode
+    # an accepted path per request: root + first-child chain of length 3
+    ids = torch.full((B, T + 1), -1, dtype=torch.int32, device=dev)
+    keep = torch.zeros(B, dtype=torch.int32, device=dev)
+    for b in range(B):
+        path = [0]
+        while len(path) < 3:
+            kids = [v for v in range(int(n[b])) if par[b, v] == path[-1]]
+            if not kids:
+                break
+            path.append(kids[0])
+        ids[b, :len(path)] = torch.tensor(path, dtype=torch.int32)
+        keep[b] = len(path)
+    capi.kv_compact(ids, keep, P, k1, v1)
+    capi.kv_commit_tree(ids, keep, P, qkv, k2, v2, T)
+    torch.cuda.synchronize()
+    Dh = d // H
+    for b in range(B):
+        p0, e = int(P[b]), int(P[b]) + int(keep[b])
+        # rows below P untouched; layer 0 identical to append + compaction
+        # (its inputs do not depend on attention)
+        assert torch.equal(k2[:, b, :, :p0], kc[:, b, :, :p0])
+        assert torch.equal(k1[0, b, :, :e], k2[0, b, :, :e])
+        assert torch.equal(v1[0, b, :, :e], v2[0, b, :, :e])
+        # every layer: committed row P+k == that layer's tree K/V row ids[k]
+        for layer in range(L_):
+            for k in range(int(keep[b])):
+                src = b * T + int(ids[b, k])
+                kt = qkv[layer, 1, src].view(H, Dh)
+                vt = qkv[layer, 2, src].view(H, Dh)
+                assert torch.equal(k2[layer, b, :, p0 + k], kt)
+                assert torch.equal(v2[layer, b, :, p0 + k], vt)

@@ -227,26 +227,15 @@ int main() {
     }
     unsigned long long* keys;
     cudaMalloc(&keys, (size_t)B * T * 16 * 8);
-    run<4, 8, 256>(bufs, keys, B, T, V);
-    run<2, 16, 256>(bufs, keys, B, T, V);
-    run<1, 16, 512>(bufs, keys, B, T, V);
-    run<2, 8, 512>(bufs, keys, B, T, V);
-    run<8, 4, 256>(bufs, keys, B, T, V);
-    run<8, 8, 128>(bufs, keys, B, T, V);
-    run<16, 4, 128>(bufs, keys, B, T, V);
-    run<4, 4, 512>(bufs, keys, B, T, V);
-    run<4, 8, 256>(bufs, keys, B, T, V);
-    run_p<8, 4, 256>(bufs, keys, B, T, V, 148 * 4);
-    run_p<8, 4, 256>(bufs, keys, B, T, V, 148 * 8);
-    run_p<16, 2, 256>(bufs, keys, B, T, V, 148 * 8);
-    run_p<4, 8, 256>(bufs, keys, B, T, V, 148 * 4);
-    run_p<4, 8, 256>(bufs, keys, B, T, V, 148 * 8);
-    run_p<2, 16, 256>(bufs, keys, B, T, V, 148 * 4);
-    run<8, 4, 256>(bufs, keys, B, T, V);
-    run_b<8, 256>(bufs, keys, B, T, V);
-    run_b<4, 256>(bufs, keys, B, T, V);
-    run_b<2, 512>(bufs, keys, B, T, V);
-    run_b<16, 128>(bufs, keys, B, T, V);
-    run<8, 4, 256>(bufs, keys, B, T, V);
+    for (int rep = 0; rep < 2; ++rep) {
+        run<8, 4, 256>(bufs, keys, B, T, V);
+        run<7, 5, 256>(bufs, keys, B, T, V);
+        run<9, 4, 256>(bufs, keys, B, T, V);
+        run<10, 4, 256>(bufs, keys, B, T, V);
+        run<6, 6, 256>(bufs, keys, B, T, V);
+        run<12, 3, 256>(bufs, keys, B, T, V);
+        run<14, 3, 256>(bufs, keys, B, T, V);
+        run<16, 2, 256>(bufs, keys, B, T, V);
+    }
     return 0;
 }
