@@ -49,7 +49,7 @@ sys.path.insert(0, ROOT)
 
 # C2
 B, T, H, D, L, V = 8, 64, 32, 128, 2048, 32000
-LAUNCHES_PER_STEP = 3          # K1 (masks derived inside, tree rows from k_tree), K3 argmax, walk + commit
+LAUNCHES_PER_STEP = 4          # masks, K1 (tree rows from k_tree), K3 argmax, K3 walk + K2 commit
 STRONG_B_GLOBAL = 64           # strong-scaling companion: 64 requests split over the ranks
 METRIC = "tree-verify tokens/s"
 UNIT = "tokens/s"
@@ -64,9 +64,6 @@ def parse(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-strong", action="store_true",
                     help="skip the strong-scaling companion measurement")
-    ap.add_argument("--masks", default="k1", choices=["k1", "kernel"],
-                    help="ancestor masks derived inside K1 from the parents (default) or built "
-                         "by a separate kernel before it")
     ap.add_argument("--tree-rows", default="own", choices=["own", "cache"],
                     help="K1 reads the tree rows from their own tensors (no append) or "
                          "from the cache after a K2 append")
@@ -255,7 +252,7 @@ class VerifyStep:
     n_nodes), so the e2e loop can swap in freshly copied inputs."""
 
     def __init__(self, dev, seed, B=B, T=T, L=L, H=H, D=D, V=V, tree_rows="own",
-                 trees=None, dtype=None, masks="k1"):
+                 trees=None, dtype=None):
         import torch
 
         from paper_2305_09781_b200 import _capi
@@ -307,16 +304,10 @@ class VerifyStep:
         # rows. cache: K2 append into the cache scratch rows first, then
         # in-place compaction (the reference's cache discipline).
         self.own = tree_rows == "own"
-        # masks="k1": K1 derives the ancestor masks from the parents itself
-        # (st_attn_args.parent), so nothing runs between the previous step's
-        # commit and K1; "kernel": st_build_masks_early before an early_kv K1
-        self.derive = masks == "k1" and self.own
         self.resident = (self.q, self.knew, self.vnew, self.tok, self.par, self.nn)
 
     def pre(self, a):
         qq, kn, vn, tk, pr, nd = a
-        if self.derive:
-            return
         if self.own:   # ancestor masks; the previous kernel writes no input of theirs
             self.capi.build_masks(pr, nd, W=self.W, out=self.mask, early=True)
         else:          # K2 append + masks (one launch)
@@ -331,8 +322,7 @@ class VerifyStep:
         # streams the committed rows while the masks kernel runs
         self.capi.tree_attention(qq, self.kc, self.vc, self.mask, self.P, nd, out=self.out,
                                  workspace=self.ws_attn, k_tree=kn if self.own else None,
-                                 v_tree=vn if self.own else None, early_kv=not self.derive,
-                                 parent=pr if self.derive else None)
+                                 v_tree=vn if self.own else None, early_kv=True)
 
     def post(self, a):   # K3 argmax, then the walk fused with the K2 commit
         qq, kn, vn, tk, pr, nd = a
@@ -357,8 +347,7 @@ class VerifyStep:
                                     k_tree=kn if self.own else None,
                                     v_tree=vn if self.own else None,
                                     k_new=None if self.own else kn,
-                                    v_new=None if self.own else vn, early_kv=not self.derive,
-                                    derive_masks=self.derive)
+                                    v_new=None if self.own else vn, early_kv=True)
 
     def k1_bytes(self, s=2):
         """Algorithmic K1 bytes per launch."""
@@ -688,7 +677,7 @@ def run_verify(args):
     numa_cpus = bind_to_gpu_numa(local)
     c5 = args.config == "c5"
     Bq, Tq, Lq = (16, args.tree, args.kv) if c5 else (B, T, L)
-    step = VerifyStep(dev, rank, B=Bq, T=Tq, L=Lq, tree_rows=args.tree_rows, masks=args.masks)
+    step = VerifyStep(dev, rank, B=Bq, T=Tq, L=Lq, tree_rows=args.tree_rows)
     barrier = barrier_of(world)
     runner = DPRunner(step, world, dev)
     runner.capture(args.warmup, timed_k1=True)
@@ -736,8 +725,7 @@ def run_verify(args):
     if not c5 and not args.no_strong and STRONG_B_GLOBAL % world == 0:
         del runner
         sb = STRONG_B_GLOBAL // world
-        st2 = VerifyStep(dev, 100 + rank, B=sb, T=Tq, L=Lq, tree_rows=args.tree_rows,
-                         masks=args.masks)
+        st2 = VerifyStep(dev, 100 + rank, B=sb, T=Tq, L=Lq, tree_rows=args.tree_rows)
         r2 = DPRunner(st2, world, dev)
         r2.capture(args.warmup)
         for _ in range(max(args.warmup, 3)):
@@ -810,7 +798,7 @@ def run_verify(args):
                              "around the replays; in-step bracket (event graph nodes around K1 "
                              "inside the step) reported beside it",
                    "k1_path": "tcgen05" if step.path == 2 else "cuda-core",
-                   "tree_rows": args.tree_rows, "masks": args.masks},
+                   "tree_rows": args.tree_rows},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "K1 tree attention", "bytes_per_launch": bytes_k1,
@@ -820,7 +808,7 @@ def run_verify(args):
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)"},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": (LAUNCHES_PER_STEP + (0 if step.derive else 1)) * args.steps,
+        "gpu_launches": LAUNCHES_PER_STEP * args.steps,
         "clocks": clk,
         "parity": parity,
         "strong": strong,

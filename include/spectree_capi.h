@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define ST_ABI_VERSION 5
+#define ST_ABI_VERSION 4
 
 typedef int st_status;
 
@@ -111,11 +111,6 @@ typedef struct {
      * and st_tree_prepare follow this rule, which makes "previous step's
      * commit -> masks -> early_kv K1" safe while P advances every step. */
     int early_kv;
-    /* Optional [B][T] preorder parents (parent[u] < u). When set, K1 derives
-     * the ancestor masks itself — written into `mask`, which is then scratch
-     * of [B][T][W] — so no st_build_masks launch precedes it (the tcgen05
-     * path computes them in its prologue while the first KV tiles load). */
-    const int32_t* parent;
 } st_attn_args;
 
 size_t st_tree_attention_workspace_size(const st_attn_args* a);

@@ -44,7 +44,7 @@ class AttnArgs(C.Structure):
                 ("o", C.c_void_p), ("lse", C.c_void_p), ("scale", C.c_double),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
                 ("force_path", C.c_int), ("k_tree", C.c_void_p), ("v_tree", C.c_void_p),
-                ("early_kv", C.c_int), ("parent", C.c_void_p)]
+                ("early_kv", C.c_int)]
 
 
 _lib = None
@@ -143,8 +143,7 @@ def _stream(stream=None):
 
 # ------------------------------------------------------------------ K1 ----
 def attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, lse=None, scale=None,
-              workspace=None, force_path=0, k_tree=None, v_tree=None, early_kv=False,
-              parent=None):
+              workspace=None, force_path=0, k_tree=None, v_tree=None, early_kv=False):
     B, T, H, D = q.shape
     Hkv, Lmax = k_cache.shape[1], k_cache.shape[2]
     a = AttnArgs()
@@ -161,7 +160,6 @@ def attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, lse=None, sca
     a.k_tree = k_tree.data_ptr() if k_tree is not None else None
     a.v_tree = v_tree.data_ptr() if v_tree is not None else None
     a.early_kv = 1 if early_kv else 0
-    a.parent = parent.data_ptr() if parent is not None else None
     return a
 
 
@@ -180,19 +178,18 @@ def tree_attention_path(q, k_cache, v_cache, mask, prefix_len, n_nodes, force_pa
 
 def tree_attention(q, k_cache, v_cache, mask, prefix_len, n_nodes, out=None, lse=None,
                    scale=None, workspace=None, force_path=0, stream=None, k_tree=None,
-                   v_tree=None, early_kv=False, parent=None):
+                   v_tree=None, early_kv=False):
     """K1 through st_tree_attention. Shapes: q [B,T,H,D]; caches [B,Hkv,Lmax,D];
     mask [B,T,W] int64 (uint64 bits); prefix_len/n_nodes [B] int32 (device);
     k_tree/v_tree (optional) [B,T,Hkv,D]: the tree rows, read instead of cache
-    rows [P, P+n); parent (optional) [B,T] int32: K1 derives the masks itself
-    into `mask` (scratch)."""
+    rows [P, P+n)."""
     if out is None:
         out = torch.empty_like(q)
     if workspace is None:
         workspace = tree_attention_workspace(q, k_cache, v_cache, mask, prefix_len, n_nodes,
                                              force_path)
     a = attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, lse, scale, workspace,
-                  force_path, k_tree, v_tree, early_kv, parent)
+                  force_path, k_tree, v_tree, early_kv)
     check(lib().st_tree_attention(C.byref(a), _stream(stream)))
     return out
 
@@ -566,15 +563,13 @@ class VerifyPlan:
 
     def __init__(self, q, k_cache, v_cache, mask, prefix_len, n_nodes, out, workspace, tokens,
                  parent, logits, verify_ws, verified, ids, length, k_tree=None, v_tree=None,
-                 k_new=None, v_new=None, early_kv=True, budget=None, eos=-1, new_prefix_len=None,
-                 derive_masks=False):
+                 k_new=None, v_new=None, early_kv=True, budget=None, eos=-1, new_prefix_len=None):
         self._keep = [q, k_cache, v_cache, mask, prefix_len, n_nodes, out, workspace, tokens, parent,
                       logits, verify_ws, verified, ids, length, k_tree, v_tree, k_new, v_new,
                       budget, new_prefix_len]
         d = StepDesc()
         d.attn = attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, workspace=workspace,
-                           k_tree=k_tree, v_tree=v_tree, early_kv=early_kv,
-                           parent=parent if derive_masks else None)
+                           k_tree=k_tree, v_tree=v_tree, early_kv=early_kv)
         d.tokens, d.parent, d.logits = tokens.data_ptr(), parent.data_ptr(), logits.data_ptr()
         d.V = logits.shape[-1]
         d.budget = budget.data_ptr() if budget is not None else None

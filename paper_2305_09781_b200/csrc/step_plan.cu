@@ -25,9 +25,6 @@ st_status st_verify_plan_create(const st_verify_step_desc* d, st_verify_plan** o
                  ST_ERR_INVALID_ARGUMENT, "null pointer");
     ST_CHECK_ARG(a.k_tree || (d->k_new && d->v_new), ST_ERR_INVALID_ARGUMENT,
                  "cache mode (k_tree == NULL) needs k_new / v_new to append");
-    ST_CHECK_ARG(!(a.parent && a.early_kv), ST_ERR_INVALID_ARGUMENT,
-                 "attn.parent (masks derived in K1) puts the previous step's commit right "
-                 "before K1: early_kv must be 0");
     ST_CHECK_ARG(d->V >= 1 && a.B >= 1 && a.T >= 1, ST_ERR_SHAPE_MISMATCH, "bad shape");
     auto* p = new st_verify_plan;
     p->d = *d;
@@ -52,10 +49,7 @@ st_status st_verify_plan_run(st_verify_plan* p, void* stream) {
     const st_verify_step_desc& d = p->d;
     const st_attn_args& a = d.attn;
     uint64_t* mask = const_cast<uint64_t*>(a.mask);
-    if (a.k_tree && a.parent) {
-        // K1 derives the masks itself: nothing runs between the previous
-        // step's commit and K1
-    } else if (a.k_tree) {  // the tree rows stay in their own tensors: masks only
+    if (a.k_tree) {  // the tree rows stay in their own tensors: masks only
         if (st_status e = st_build_masks_early(d.parent, a.n_nodes, a.B, a.T, a.W, mask, stream))
             return e;
     } else {         // the reference's cache discipline: K2 append + masks

@@ -70,11 +70,6 @@ st_status st_tree_attention(const st_attn_args* a, void* stream) {
         }
         return st::tree_attention_tc(a, st::as_stream(stream));
     }
-    if (a->parent) {  // the CUDA-core kernel reads prebuilt masks
-        if (st_status e = st_build_masks(a->parent, a->n_nodes, a->B, a->T, a->W,
-                                         const_cast<uint64_t*>(a->mask), stream))
-            return e;
-    }
     return st::tree_attention_cc(a, st::as_stream(stream));
 }
 

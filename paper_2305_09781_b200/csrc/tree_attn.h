@@ -28,10 +28,6 @@ struct TcParams {
     int aligned_slack;          // whole-pair schedule allowed within this many tiles of stream-K
     int head_extra;             // split schedule: extra tiles for each pair's head piece
     int trace_cta;              // CTA whose per-tile pipeline is traced (ST_K1_TRACE_CTA)
-    // st_attn_args.parent: the kernel derives the ancestor masks of the
-    // requests in its range into mask_w (then read back instead of `mask`)
-    const int32_t* parent;
-    uint64_t* mask_w;
     // head-sharded output (st_tree_attention_allgather): rows go to every rank's
     // [B][T][H_out][D] buffer at head head_offset + h; null -> o with H_out = H
     void* const* o_peers;

@@ -724,39 +724,13 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 const uint64_t* mr = p.mask + ((long long)sg.b * p.T + u_r) * p.W;
 #pragma unroll
                 for (int w = 0; w < MW; ++w)
-                    if (w < p.W) mt.mw[w] = p.parent ? __ldcg(mr + w) : __ldg(mr + w);
+                    if (w < p.W) mt.mw[w] = __ldg(mr + w);
             }
             return mt;
         };
         Seg s_next{};
         Meta m_next{};
         if (p.early_kv) pdl_wait();  // masks and lengths below; outputs written later
-        if (p.parent) {
-            // Ancestor masks of every request this range touches (st_attn_args.parent):
-            // mask[u] = bits of u's root path, walked up the parent chain. Other
-            // CTAs may write the same words — with identical values. The first KV
-            // tiles are loading meanwhile, so this hides behind the first S.
-            for (uint32_t t = t_begin; t < t_end;) {
-                const Seg sg = find_seg(p, cum, t, t_end);
-                const int nb = __ldg(p.n_nodes + sg.b);
-                const int32_t* par = p.parent + (long long)sg.b * p.T;
-                for (int u = threadIdx.x; u < nb; u += SW * 32) {
-                    uint64_t w4[4] = {0, 0, 0, 0};
-                    for (int v = u; v >= 0 && v < p.T; v = __ldg(par + v)) {
-                        const uint64_t bit = 1ull << (v & 63);
-#pragma unroll
-                        for (int w = 0; w < 4; ++w)
-                            if ((v >> 6) == w) w4[w] |= bit;
-                    }
-                    uint64_t* mr = p.mask_w + ((long long)sg.b * p.T + u) * p.W;
-#pragma unroll
-                    for (int w = 0; w < 4; ++w)
-                        if (w < p.W) mr[w] = w4[w];
-                }
-                t += sg.hi - sg.lo;
-            }
-            named_bar_sync(3, SW * 32);  // this CTA's softmax warps read them next
-        }
         if (t_begin < t_end) {
             s_next = find_seg(p, cum, t_begin, t_end);
             m_next = load_meta(s_next);
@@ -1226,8 +1200,6 @@ st_status tree_attention_tc_prepare(const st_attn_args* a, const st_peer_out* po
     prm.W = a->W;
     prm.scale = (float)a->scale;
     prm.c_log2 = (float)(a->scale * 1.4426950408889634);
-    prm.parent = a->parent;
-    prm.mask_w = const_cast<uint64_t*>(a->mask);
     prm.o_peers = po ? po->out : nullptr;
     prm.world = po ? po->world : 1;
     prm.head_offset = po ? po->rank * a->H : 0;

@@ -22,7 +22,6 @@ import pytest
 import torch
 
 from tests.treegen import masks, pack, width_depth_seqs
-from tests.treegen import masks as masks_of
 
 pytestmark = pytest.mark.gpu
 
@@ -76,16 +75,13 @@ def worst_err(out, ref):
                for (b, h), r in ref.items())
 
 
-@pytest.mark.parametrize("tree_rows,native,masks", [("own", True, "k1"), ("own", False, "k1"),
-                                                    ("own", True, "kernel"), ("cache", True, "kernel")])
-def test_c2_bench_step_full_shape(capi, restatement, tree_rows, native, masks):
+@pytest.mark.parametrize("tree_rows,native", [("own", True), ("own", False), ("cache", True)])
+def test_c2_bench_step_full_shape(capi, restatement, tree_rows, native):
     """native: the step as st_verify_plan_run (what bench.py times); else one
-    CUDA-graph replay of the Python-issued launches. masks="k1": K1 derives
-    the ancestor masks from the parents (st_attn_args.parent) — checked against
-    the oracle's masks too."""
+    CUDA-graph replay of the Python-issued launches."""
     import bench
     dev = torch.device("cuda", 0)
-    st = bench.VerifyStep(dev, 0, tree_rows=tree_rows, masks=masks)
+    st = bench.VerifyStep(dev, 0, tree_rows=tree_rows)
     assert st.path == 2, "C2 must take the tcgen05 K1 path"
     kc0, vc0 = st.kc.clone(), st.vc.clone()
     runner = bench.DPRunner(st, 1, dev, native=native)
@@ -94,7 +90,6 @@ def test_c2_bench_step_full_shape(capi, restatement, tree_rows, native, masks):
     st.kc.copy_(kc0)
     st.vc.copy_(vc0)
     st.out.zero_()
-    st.mask.fill_(-1)   # K1 (masks="k1") or the masks kernel must rebuild them
     for t in st.vout:
         t.fill_(-7)
     runner.step()
@@ -103,9 +98,8 @@ def test_c2_bench_step_full_shape(capi, restatement, tree_rows, native, masks):
 
     B, T, H = st.B, st.T, st.H
     par, n = st.batch.parents, st.batch.n_nodes
-    m = masks_of(restatement, par, n, st.W)
-    for b in range(B):   # rows past n are never read (nor, when K1 derives them, written)
-        assert torch.equal(st.mask[b, : n[b]].cpu(), torch.tensor(m[b, : n[b]].view(np.int64))), b
+    m = masks(restatement, par, n, st.W)
+    assert torch.equal(st.mask.cpu(), torch.tensor(m.view(np.int64))), "device masks"
     # K1: all 256 (request, head) pairs
     pairs = [(b, h) for b in range(B) for h in range(H)]
     P = st.P.cpu().numpy()

@@ -380,53 +380,3 @@ def test_tc_large_trees_two_row_blocks(capi, restatement, T, G, width, own, dtyp
     capi.tree_attention(q, kc, vc, mask, Pd, nd, out=out, lse=lse, k_tree=kt, v_tree=vt)
     torch.cuda.synchronize()
     check_k1(restatement, bt, out, dtype, lse)
-
-
-@pytest.mark.parametrize("T,G,own", [(64, 1, True), (61, 1, False), (16, 4, True), (128, 1, True),
-                                     (200, 1, True), (8, 8, False), (256, 1, False)])
-def test_tc_masks_derived_in_kernel(capi, restatement, T, G, own):
-    """st_attn_args.parent: K1 builds the ancestor masks itself (the mask
-    buffer is scratch, pre-filled with junk here) — outputs vs the f64
-    restatement, and the buffer's live rows vs the oracle's masks."""
-    rng = np.random.default_rng(500 + T + G)
-    Hkv, B = 2, 6
-    w = max(1, min(16, T // 8))
-    depth = -(-(T - 1) // w)
-    trees = []
-    for _ in range(B):
-        t = restatement.merge(width_depth_seqs(rng, int(rng.integers(0, 300)), 300, w, depth),
-                              1 << 20)
-        trees.append(tuple(a[:T] for a in t))
-    bt = make_batch(restatement, rng, B, G * Hkv, Hkv, 128, trees=trees, T=T,
-                    P_range=(0, 1500), dtype=torch.float16)
-    bt["n"][2] = 0   # an empty request
-    dev = "cuda"
-    q = torch.tensor(bt["q"], device=dev).half()
-    kc = torch.tensor(bt["kc"], device=dev).half()
-    vc = torch.tensor(bt["vc"], device=dev).half()
-    Pd, nd = torch.tensor(bt["P"], device=dev), torch.tensor(bt["n"], device=dev)
-    par = torch.tensor(bt["par"], device=dev)
-    kt = vt = None
-    if own:
-        kt = torch.zeros(B, T, Hkv, 128, dtype=torch.float16, device=dev)
-        vt = torch.zeros_like(kt)
-        for b in range(B):
-            P, n = int(bt["P"][b]), int(bt["n"][b])
-            kt[b, :n] = kc[b, :, P:P + n].transpose(0, 1)
-            vt[b, :n] = vc[b, :, P:P + n].transpose(0, 1)
-            kc[b, :, P:P + n] = 4.0
-    mask = torch.full(bt["mask"].shape, -1, dtype=torch.int64, device=dev)
-    out = torch.zeros_like(q)
-    lse = torch.zeros((B, G * Hkv, T), dtype=torch.float32, device=dev)
-    assert capi.tree_attention_path(q, kc, vc, mask, Pd, nd) == 2
-    capi.tree_attention(q, kc, vc, mask, Pd, nd, out=out, lse=lse, k_tree=kt, v_tree=vt,
-                        parent=par)
-    torch.cuda.synchronize()
-    keep = [b for b in range(B) if bt["n"][b] > 0]
-    sub = {k: (v[keep] if isinstance(v, np.ndarray) and v.shape[:1] == (B,) else v)
-           for k, v in bt.items()}
-    check_k1(restatement, sub, out[keep], torch.float16, lse[keep])
-    m = mask.cpu().numpy().view(np.uint64)
-    for b in keep:
-        n = int(bt["n"][b])
-        np.testing.assert_array_equal(m[b, :n], bt["mask"][b, :n])
