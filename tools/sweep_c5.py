@@ -23,7 +23,7 @@ from paper_2305_09781_b200 import _capi  # noqa: E402
 from paper_2305_09781_b200.tree import TokenTree, TreeBatch  # noqa: E402
 
 B, H, D = 16, 32, 128
-WIDTH = {16: 4, 32: 8, 64: 8, 128: 16, 256: 16}
+WIDTH = {4: 2, 8: 2, 16: 4, 32: 8, 64: 8, 128: 16, 256: 16}
 
 
 def trees_of(T, seed):
