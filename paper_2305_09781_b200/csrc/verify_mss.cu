@@ -37,6 +37,20 @@ namespace {
 constexpr int NT = 256;       // reduction lanes of the contract (chunk owners)
 constexpr int kBatch = 16;    // independent global loads in flight per thread
 
+// Asynchronous global -> shared copies (the next child's q slice is fetched
+// while the current child is tested and its residual computed).
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ float exp_spec(float x) {
     if (!(x > -104.0f)) return 0.0f;
     const float t = __fmul_rn(x, 1.44269504f);
@@ -138,9 +152,17 @@ mss_cluster_kernel(const float* __restrict__ logits, const float* __restrict__ q
     const bool owner = tid < OWN;
     const int gc = kr * OWN + tid;                   // global chunk of an owner
     const int c0 = owner ? min(V, gc * CH) - e0 : 0, c1 = owner ? min(V, (gc + 1) * CH) - e0 : 0;
-    float* qs = p + SPAN;  // the current child's q slice, staged once per child
-    int32_t* par = reinterpret_cast<int32_t*>(qs + SPAN);
+    float* qbuf = p + SPAN;  // two q slices: the current child's and the next child's (prefetch)
+    int32_t* par = reinterpret_cast<int32_t*>(qbuf + 2 * SPAN);
     int32_t* tok = par + T;
+    int32_t* kids = tok + T;  // children of the current node, ascending id
+    // this CTA's slice of child v's draft row, copied asynchronously into buffer `slot`
+    auto prefetch_q = [&](int v, int slot) {
+        const float* qe = q + ((int64_t)b * T + v) * V + e0;
+        float* dst = qbuf + slot * SPAN;
+        for (int i = tid; i < ne; i += NTC) cp_async4(dst + i, qe + i);
+        cp_async_commit();
+    };
     for (int v = tid; v < n; v += NTC) {
         par[v] = parent[(int64_t)b * T + v];
         tok[v] = tokens[(int64_t)b * T + v];
@@ -155,6 +177,18 @@ mss_cluster_kernel(const float* __restrict__ logits, const float* __restrict__ q
 
     for (;;) {
         cl.sync();  // every remote reader of the previous p is done
+        // children of u (ascending id); the first one's q slice starts loading now,
+        // behind the softmax
+        __shared__ int nkids;
+        if (tid == 0) {
+            int c = 0;
+            for (int v = u + 1; v < n; ++v)
+                if (par[v] == u) kids[c++] = v;
+            nkids = c;
+        }
+        __syncthreads();
+        const int nk = nkids;
+        if (nk > 0) prefetch_q(kids[0], 0);
         // ---- p = softmax(z[u] / tau) in the contract's arithmetic ----
         const float* z = logits + ((int64_t)b * T + u) * V + e0;
         float mx = -INFINITY;
@@ -185,34 +219,24 @@ mss_cluster_kernel(const float* __restrict__ logits, const float* __restrict__ q
 
         // ---- children of u in ascending id order ----
         int next = -1;
-        for (int v = u + 1; v < n; ++v) {
-            if (par[v] != u) continue;
+        for (int ci = 0; ci < nk; ++ci) {
+            const int v = kids[ci];
+            const float* qs = qbuf + (ci & 1) * SPAN;
+            // the next child's slice loads while this child is tested
+            // (buffer (ci+1)&1 was last read before the previous cluster barrier)
+            if (ci + 1 < nk) prefetch_q(kids[ci + 1], (ci + 1) & 1);
             const float r = U[k++];
             const int32_t t = tok[v];
             const float* qv = q + ((int64_t)b * T + v) * V;
-            // stage this CTA's slice of q_v (one batch of loads in flight per
-            // thread) while thread 0 fetches p[t] (DSMEM) and q_v[t] for the test
-            const float* qe = qv + e0;
-            for (int i0 = tid; i0 < ne; i0 += NTC * kBatch) {
-                float x[kBatch];
-#pragma unroll
-                for (int j = 0; j < kBatch; ++j) {
-                    const int i = i0 + j * NTC;
-                    x[j] = i < ne ? __ldg(qe + i) : 0.0f;
-                }
-#pragma unroll
-                for (int j = 0; j < kBatch; ++j) {
-                    const int i = i0 + j * NTC;
-                    if (i < ne) qs[i] = x[j];
-                }
-            }
-            if (tid == 0) {
+            if (tid == 0) {  // p[t] (DSMEM) and q_v[t] for the test
                 const int kt = t / SPAN;
                 sh.pt = cl.map_shared_rank(p, kt)[t - kt * SPAN];
                 sh.qt = __ldg(qv + t);
             }
+            if (ci + 1 < nk) cp_async_wait<1>(); else cp_async_wait<0>();  // this child's slice
             __syncthreads();
             if (__fmul_rn(r, sh.qt) <= sh.pt) {
+                cp_async_wait<0>();  // drain the prefetch before the buffers are reused
                 next = v;
                 break;
             }
@@ -239,36 +263,56 @@ mss_cluster_kernel(const float* __restrict__ logits, const float* __restrict__ q
         for (int i = c0; i < c1; ++i) c = __fadd_rn(c, p[i]);
         if (owner) cl.map_shared_rank(&sh, 0)->csum[gc] = c;
         cl.sync();
-        if (lead && tid == 0) {
-            float run = 0.0f;
-            for (int t = 0; t < NT; ++t) {
-                run = __fadd_rn(run, sh.csum[t]);
-                sh.cum[t] = run;
+        if (lead && tid < 32) {  // warp 0 of the leader
+            __shared__ float target_s;
+            __shared__ int tc_s;
+            if (tid == 0) {
+                float run = 0.0f;
+                for (int t = 0; t < NT; ++t) {
+                    run = __fadd_rn(run, sh.csum[t]);
+                    sh.cum[t] = run;
+                }
+                const float target = __fmul_rn(r, sh.cum[NT - 1]);
+                int tc = -1;
+                for (int t = 0; t < NT; ++t)
+                    if (sh.cum[t] > target) { tc = t; break; }
+                if (tc < 0)
+                    for (int t = NT - 1; t >= 0; --t)
+                        if (sh.csum[t] > 0.0f) { tc = t; break; }
+                target_s = target;
+                tc_s = tc;
             }
-            const float target = __fmul_rn(r, sh.cum[NT - 1]);
-            int tc = -1;
-            for (int t = 0; t < NT; ++t)
-                if (sh.cum[t] > target) { tc = t; break; }
-            if (tc < 0)
-                for (int t = NT - 1; t >= 0; --t)
-                    if (sh.csum[t] > 0.0f) { tc = t; break; }
+            __syncwarp();
+            const int tc = tc_s;
             int pick = 0;
             if (tc >= 0) {
-                const int kt = (tc * CH) / SPAN;
+                // the chosen chunk, fetched over DSMEM by the whole warp (independent
+                // loads) into local scratch, then scanned sequentially in the
+                // contract's order by lane 0
+                const int lo = tc * CH, hi = min(V, (tc + 1) * CH);
+                const int kt = lo / SPAN;
                 const float* pr = cl.map_shared_rank(p, kt) - kt * SPAN;  // global element index
-                float acc = tc > 0 ? sh.cum[tc - 1] : 0.0f;
-                int last_pos = -1;
-                pick = -1;
-                for (int i = tc * CH; i < min(V, (tc + 1) * CH); ++i) {
-                    const float pi = pr[i];
-                    acc = __fadd_rn(acc, pi);
-                    if (pi > 0.0f) last_pos = i;
-                    if (acc > target) { pick = i; break; }
+                float* loc = qbuf;  // the q slices are free here
+                for (int i = lo + tid; i < hi; i += 32) loc[i - lo] = pr[i];
+                __syncwarp();
+                if (tid == 0) {
+                    const float target = target_s;
+                    float acc = tc > 0 ? sh.cum[tc - 1] : 0.0f;
+                    int last_pos = -1;
+                    pick = -1;
+                    for (int i = lo; i < hi; ++i) {
+                        const float pi = loc[i - lo];
+                        acc = __fadd_rn(acc, pi);
+                        if (pi > 0.0f) last_pos = i;
+                        if (acc > target) { pick = i; break; }
+                    }
+                    if (pick < 0) pick = last_pos >= 0 ? last_pos : lo;
                 }
-                if (pick < 0) pick = last_pos >= 0 ? last_pos : tc * CH;
             }
-            vrow[m] = pick;
-            len[b] = m + 1;
+            if (tid == 0) {
+                vrow[m] = pick;
+                len[b] = m + 1;
+            }
         }
         cl.sync();  // the leader's remote reads are done before any CTA exits
         break;
@@ -292,10 +336,11 @@ extern "C" st_status st_verify_mss(const float* logits, const float* q, int B, i
     ST_CHECK_ARG(logits && q && tokens && parent && n_nodes && uniforms && verified && ids && len,
                  ST_ERR_INVALID_ARGUMENT, "null pointer");
     // one cluster of CN CTAs per request; each CTA holds its OWN chunks of p
+    // and two q slices (current child + prefetched next child)
     const int CH = (V + st::NT - 1) / st::NT;
-    const size_t smem = 2 * (size_t)st::OWN * CH * sizeof(float) + 2 * (size_t)T * sizeof(int32_t);
+    const size_t smem = 3 * (size_t)st::OWN * CH * sizeof(float) + 3 * (size_t)T * sizeof(int32_t);
     ST_CHECK_ARG(smem <= 200 * 1024, ST_ERR_UNSUPPORTED,
-                 "vocabulary / tree too large for K4 (2 * V/4 * 4 + T * 8 <= 200 KB)");
+                 "vocabulary / tree too large for K4 (3 * V/4 * 4 + T * 12 <= 200 KB)");
     ST_CHECK_ARG((int64_t)B * st::CN <= 2147483647, ST_ERR_SHAPE_MISMATCH, "too many requests");
     static size_t attr_set = 0;
     if (smem > 48 * 1024 && smem > attr_set) {
