@@ -131,3 +131,34 @@ def test_engine_matches_reference_engine_golden(capi, golden, expansion):
     assert seqs[0][:stop] == ref[:stop]
     if expansion == (1, 1, 1, 1):   # same step count as the reference's perfect speculator
         assert steps == int(g["speculative_steps"])
+
+
+def test_comm_single_rank_gather_accepted(capi):
+    """st_comm_*: the C-ABI NCCL module (DP exchange). One GPU per call here
+    (NCCL refuses two ranks on one device), so this checks the single-rank
+    communicator end to end: unique id -> init -> gather_accepted packs the
+    verified tokens + lengths exactly as the multi-rank layout expects."""
+    uid = capi.Comm.unique_id()
+    comm = capi.Comm(1, 0, uid)
+    B, T = 5, 7
+    ver = torch.randint(0, 1000, (B, T + 1), dtype=torch.int32, device="cuda")
+    ln = torch.randint(1, T + 2, (B,), dtype=torch.int32, device="cuda")
+    pack = torch.empty(B * (T + 2), dtype=torch.int32, device="cuda")
+    gathered = torch.empty(1 * B * (T + 2), dtype=torch.int32, device="cuda")
+    comm.gather_accepted(ver, ln, pack, gathered)
+    torch.cuda.synchronize()
+    assert torch.equal(gathered[: B * (T + 1)].view(B, T + 1), ver)
+    assert torch.equal(gathered[B * (T + 1):], ln)
+
+
+def test_engine_bf16_incremental_matches_speculative(capi):
+    c = _cfg()
+    llm = capi.DeviceModel(c["layers"], c["heads"], c["d"], c["V"], c["maxpos"], 4, seed=31,
+                           dtype=torch.bfloat16)
+    inc = capi.Engine(llm, None, len(PROMPTS), 8, expansion=())
+    seqs_inc, _ = inc.run(PROMPTS, BUDGETS)
+    spec = capi.Engine(llm, None, len(PROMPTS), 8, expansion=(2, 1, 1))
+    seqs_spec, _ = spec.run(PROMPTS, BUDGETS)
+    for p, a, b in zip(PROMPTS, seqs_inc, seqs_spec):
+        assert len(b) == len(a)
+        _agree(capi, llm, a, b, len(p))
