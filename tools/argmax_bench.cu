@@ -19,7 +19,23 @@ __device__ __forceinline__ unsigned long long arg_key(float v, int i) {
     return ((unsigned long long)u << 32) | (uint32_t)(~(uint32_t)i);
 }
 
-template <int SPLIT, int UNROLL, int NT>
+// LD: 0 __ldcs (ld.global.cs), 1 ld.global.nc.L1::no_allocate.L2::256B,
+// 2 ld.global.L1::no_allocate.L2::256B, 3 __ldg
+template <int LD>
+__device__ __forceinline__ float4 ld4(const float4* p) {
+    if constexpr (LD == 0) return __ldcs(p);
+    if constexpr (LD == 3) return __ldg(p);
+    float4 v;
+    if constexpr (LD == 1)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    else
+        asm volatile("ld.global.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+
+template <int SPLIT, int UNROLL, int NT, int LD = 0>
 __global__ void __launch_bounds__(NT) argmax_kernel(const float* __restrict__ logits, int T, int V,
                                                     unsigned long long* keys) {
     const int part = blockIdx.x, u = blockIdx.y, b = blockIdx.z;
@@ -35,7 +51,7 @@ __global__ void __launch_bounds__(NT) argmax_kernel(const float* __restrict__ lo
 #pragma unroll
         for (int k = 0; k < UNROLL; ++k) {
             const int j = base + k * NT;
-            x[k] = j < hi ? __ldcs(r4 + j) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+            x[k] = j < hi ? ld4<LD>(r4 + j) : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
         }
 #pragma unroll
         for (int k = 0; k < UNROLL; ++k) {
@@ -199,23 +215,23 @@ void run_b(float* const* bufs, unsigned long long* keys, int B, int T, int V) {
            4.0 * B * T * V / us / 1e3, cudaGetErrorString(cudaGetLastError()));
 }
 
-template <int SPLIT, int UNROLL, int NT>
+template <int SPLIT, int UNROLL, int NT, int LD = 0>
 void run(float* const* bufs, unsigned long long* keys, int B, int T, int V) {
     dim3 grid(SPLIT, T, B);
-    for (int i = 0; i < 6; ++i) argmax_kernel<SPLIT, UNROLL, NT><<<grid, NT>>>(bufs[i % 3], T, V, keys);
+    for (int i = 0; i < 6; ++i) argmax_kernel<SPLIT, UNROLL, NT, LD><<<grid, NT>>>(bufs[i % 3], T, V, keys);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int iters = 60;
     cudaEventRecord(e0);
-    for (int i = 0; i < iters; ++i) argmax_kernel<SPLIT, UNROLL, NT><<<grid, NT>>>(bufs[i % 3], T, V, keys);
+    for (int i = 0; i < iters; ++i) argmax_kernel<SPLIT, UNROLL, NT, LD><<<grid, NT>>>(bufs[i % 3], T, V, keys);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     const double us = ms * 1e3 / iters;
     const double bytes = 4.0 * B * T * V;
-    printf("split %d unroll %2d threads %4d: %7.2f us  %6.0f GB/s\n", SPLIT, UNROLL, NT, us, bytes / us / 1e3);
+    printf("split %d unroll %2d threads %4d ld %d: %7.2f us  %6.0f GB/s\n", SPLIT, UNROLL, NT, LD, us, bytes / us / 1e3);
 }
 
 int main() {
@@ -229,6 +245,12 @@ int main() {
     cudaMalloc(&keys, (size_t)B * T * 16 * 8);
     for (int rep = 0; rep < 2; ++rep) {
         run<8, 4, 256>(bufs, keys, B, T, V);
+        run<8, 4, 256, 1>(bufs, keys, B, T, V);
+        run<8, 4, 256, 2>(bufs, keys, B, T, V);
+        run<8, 4, 256, 3>(bufs, keys, B, T, V);
+        run<4, 8, 256, 1>(bufs, keys, B, T, V);
+        run<8, 4, 512, 1>(bufs, keys, B, T, V);
+        run<16, 2, 256, 1>(bufs, keys, B, T, V);
         run<7, 5, 256>(bufs, keys, B, T, V);
         run<9, 4, 256>(bufs, keys, B, T, V);
         run<10, 4, 256>(bufs, keys, B, T, V);

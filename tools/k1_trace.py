@@ -16,6 +16,8 @@ ap.add_argument("--B", type=int, default=8)
 ap.add_argument("--T", type=int, default=64)
 ap.add_argument("--H", type=int, default=32)
 ap.add_argument("--L", type=int, default=2048)
+ap.add_argument("--Hkv", type=int, default=0)
+ap.add_argument("--chain", action="store_true")
 args = ap.parse_args()
 out = args.out
 os.environ["ST_K1_TRACE"] = out
@@ -24,11 +26,13 @@ if os.path.exists(out):
 from paper_2305_09781_b200 import _capi  # noqa: E402
 
 B, T, H, D, L = args.B, args.T, args.H, 128, args.L
+HKV = args.Hkv or H
 dev = "cuda"
 q = torch.randn(B, T, H, D, device=dev).half()
-kc = torch.randn(B, H, L + T, D, device=dev).half()
-vc = torch.randn(B, H, L + T, D, device=dev).half()
-par = torch.tensor([[-1] + [0] * (T - 1)] * B, dtype=torch.int32, device=dev)
+kc = torch.randn(B, HKV, L + T, D, device=dev).half()
+vc = torch.randn(B, HKV, L + T, D, device=dev).half()
+par0 = [-1] + (list(range(T - 1)) if args.chain else [0] * (T - 1))
+par = torch.tensor([par0] * B, dtype=torch.int32, device=dev)
 n = torch.full((B,), T, dtype=torch.int32, device=dev)
 P = torch.full((B,), L, dtype=torch.int32, device=dev)
 mask = _capi.build_masks(par, n)
