@@ -28,6 +28,8 @@ struct TcParams {
     int aligned_slack;          // whole-pair schedule allowed within this many tiles of stream-K
     int head_extra;             // split schedule: extra tiles for each pair's head piece
     int trace_cta;              // CTA whose per-tile pipeline is traced (ST_K1_TRACE_CTA)
+    unsigned long long g_magic; // floor(2^64 / G) + 1, G = schedule slots: exact floor(x / G)
+                                // for x < 2^40 as one 64-bit high multiply
     // head-sharded output (st_tree_attention_allgather): rows go to every rank's
     // [B][T][H_out][D] buffer at head head_offset + h; null -> o with H_out = H
     void* const* o_peers;

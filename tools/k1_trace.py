@@ -54,6 +54,12 @@ for i in range(64):
     if t[12][i]:
         print(f"{i:4d} " + " ".join(f"{(t[r][i] - t0) if t[r][i] else -1:12d}" for r in range(12, 16)))
 
+su = t[15][56:64]
+if su[0]:
+    print("traced CTA startup (cycles after entry): tmem+barriers %d | lengths table %d | schedule %d | "
+          "K producer fast start: begin %d, scheduled %d, Q + first ring issued %d" % tuple(int(x - su[0]) if x else -1 for x in su[1:7]))
+
+
 st, en, nt = cta[:, 0], cta[:, 1], cta[:, 2]
 t0g = st.min()
 print("\nper-CTA (us): start min/median/max %.2f %.2f %.2f | end min/median/max %.2f %.2f %.2f" % (
