@@ -263,14 +263,6 @@ constexpr uint32_t P_STAGE = PA_BYTES + PB_BYTES;       // 32 KB
 constexpr uint32_t P_OFF_BAR = P_STAGES * P_STAGE;
 constexpr uint32_t P_SMEM = P_OFF_BAR + 256;
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 // the leader CTA's copy of a barrier (shared::cluster address with the peer bit cleared)
 __device__ __forceinline__ uint32_t leader_addr(const void* p) { return smem_u32(p) & 0xFEFFFFFFu; }
 __device__ __forceinline__ void tma2_load_2d(void* dst, const CUtensorMap* m, uint32_t bar, int c0, int c1) {
@@ -306,9 +298,6 @@ __device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
         "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
         ::"r"(smem_u32(bar)), "h"((unsigned short)3)
         : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 template <class T, int EPI>

@@ -30,6 +30,9 @@ struct TcParams {
     int trace_cta;              // CTA whose per-tile pipeline is traced (ST_K1_TRACE_CTA)
     unsigned long long g_magic; // floor(2^64 / G) + 1, G = schedule slots: exact floor(x / G)
                                 // for x < 2^40 as one 64-bit high multiply
+    int cluster2;               // launched as 2-CTA clusters: split pairs of two pieces merge
+                                // over DSMEM (the piece's (O, m, l) copied into the head's
+                                // drained K ring) instead of the global publish / flag path
     // head-sharded output (st_tree_attention_allgather): rows go to every rank's
     // [B][T][H_out][D] buffer at head head_offset + h; null -> o with H_out = H
     void* const* o_peers;

@@ -313,6 +313,10 @@ __device__ __forceinline__ First warp_first_seg(const TcParams& p, uint32_t G, u
         x = ntiles_of(p, lane);
         Pl = __ldg(p.prefix_len + lane);
     }
+    if (p.trace) {  // (stamp once every lane's loads have landed)
+        const bool all = __all_sync(0xffffffffu, x >= 0 && Pl >= 0);
+        if (lane == 0 && all) K1_TRACE(13, 56);
+    }
     int inc = x;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -326,10 +330,13 @@ __device__ __forceinline__ First warp_first_seg(const TcParams& p, uint32_t G, u
     sc.np = H * (uint32_t)__popc(__ballot_sync(0xffffffffu, x > 0));
     const int lo = __reduce_min_sync(0xffffffffu, x > 0 ? x : 1 << 30);
     const int hi = __reduce_max_sync(0xffffffffu, x);
+    if (lane == 0) K1_TRACE(13, 57);
     sched_finish(p, sc, lo, hi, G);
+    if (lane == 0) K1_TRACE(13, 58);
     First f{};
     f.t_begin = range_start(slot, sc, G);
     f.t_end = range_start(slot + 1, sc, G);
+    if (lane == 0) K1_TRACE(13, 59);
     if (f.t_begin < f.t_end) {
         // largest b with H * cum[b] <= t (skips empty requests), as find_seg
         const uint32_t bal = __ballot_sync(0xffffffffu, lane < p.B && H * (uint32_t)excl <= f.t_begin);
@@ -412,23 +419,11 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     uint64_t* pv_done = p_full + 2;      // [2]
     uint64_t* o_empty = pv_done + 2;
     uint64_t* merge_full = o_empty + 1;  // staged pieces landed (head owner only)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(merge_full + 1);
+    uint64_t* peer_ready = merge_full + 1;  // DSMEM merge: the head's K ring is drained (piece only)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(peer_ready + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) K1_GT(8);
-    uint32_t pf_sink = 0;
-    {
-        // Prefetch the parameter block's constant-cache lines, one uniform
-        // load per 64 B, all in flight together (nothing waits on them): the
-        // schedule below reads a dozen fields in a dependent chain, and a cold
-        // constant line costs ~400-600 cycles (tools/cbank_latency.cu) where a
-        // hit costs ~50 — that chain was most of K1's ~6.5k-cycle startup.
-        // (lane i loads word 16i: one divergent load, every line's miss in
-        // flight together; the warp reduction consumes it so ptxas keeps it)
-        const uint32_t* pw = reinterpret_cast<const uint32_t*>(&p);
-        constexpr int kLines = (int)(sizeof(TcParams) + 63) / 64;
-        pf_sink = __reduce_or_sync(0xffffffffu, lane < kLines ? pw[lane * 16] : 0u);
-    }
     // startup stamps of the traced CTA (clock64): row 15, columns 56-63
     if (threadIdx.x == 0) K1_TRACE(15, 56);
 
@@ -444,6 +439,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         }
         mbar_init(o_empty, SW * 32);
         mbar_init(merge_full, 1);
+        mbar_init(peer_ready, 1);
         fence_barrier_init();
     }
     if (warp == SW && lane == 0) {
@@ -569,6 +565,13 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     const Sched sched = make_sched(p, cum, G);
     const uint32_t t_begin = range_start(slot, sched, G);
     const uint32_t t_end = range_start(slot + 1, sched, G);
+    // DSMEM merge (uniform over the grid): 2-CTA clusters and a split schedule
+    // of two pieces per pair — pair k's head is CTA 2k (cluster rank 0), its
+    // piece CTA 2k+1 (rank 1), so the piece's (O, m, l) goes straight into the
+    // head's drained K ring with one shared::cluster bulk copy completing on
+    // the head's merge_full barrier: no global publish, no gpu-scope release,
+    // no flag polling, no staging copy back out of L2.
+    const bool dsm = p.cluster2 && sched.mode == kSplit && sched.S == 2 && p.R == 1;
     if (p.trace && threadIdx.x == 0) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
@@ -663,17 +666,25 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         mbar_wait(k_empty + st, (k / KS) & 1);
                     }
                     int* pieces = reinterpret_cast<int*>(smem + C::OFF_PIECES);
+                    if (dsm) {  // the one piece arrives from cluster rank 1 by DSMEM
+                        pieces[0] = 1;
+                        pieces[1] = (int)blockIdx.x + 1;
+                        mbar_expect_tx(merge_full, 1024u + 4u * C::PIECE_BOX);
+                        K1_GT(11);
+                        mbar_arrive_cluster(mapa_rank(peer_ready, 1));  // ring drained: send it
+                        mbar_arrive(merge_full);
+                    }
                     int np = 0;
-                    for (uint32_t c2 = slot + 1; c2 < G && np < kMaxPieces; ++c2) {
+                    for (uint32_t c2 = slot + 1; c2 < (dsm ? 0u : G) && np < kMaxPieces; ++c2) {
                         const uint32_t rs = range_start(c2, sched, G);
                         if (rs >= pend) break;
                         if (range_start(c2 + 1, sched, G) == rs) continue;  // empty range
                         pieces[1 + np++] = (int)(c2 * (uint32_t)p.R) + rblk;  // same row block
                     }
-                    pieces[0] = np;
+                    if (!dsm) pieces[0] = np;
                     const int ns = np < C::STAGED_PIECES ? np : C::STAGED_PIECES;
-                    mbar_expect_tx(merge_full, (uint32_t)ns * (1024u + 4u * C::PIECE_BOX));
-                    K1_GT(11);
+                    if (!dsm) mbar_expect_tx(merge_full, (uint32_t)ns * (1024u + 4u * C::PIECE_BOX));
+                    if (!dsm) K1_GT(11);
                     for (int i = 0; i < np; ++i) {
                         const int c2 = pieces[1 + i];
                         wait_flag_gpu(p.flags + c2);
@@ -685,7 +696,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             bulk_load(dst + 1024, p.partial + (long long)c2 * SLOT_FLOATS, 4 * C::PIECE_BOX, merge_full);
                         }
                     }
-                    mbar_arrive(merge_full);
+                    if (!dsm) mbar_arrive(merge_full);
                 }
             }
         }
@@ -1083,6 +1094,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             if (head) {
                 mbar_wait(merge_full, 0);
                 if (threadIdx.x == 0) K1_GT(10);
+                if (threadIdx.x == 0) K1_TRACE(13, 40);
                 np = pieces[0];
             }
             if (head && valid) {
@@ -1105,6 +1117,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     }
                 }
             }
+            if (threadIdx.x == 0) K1_TRACE(13, 41);
             const bool publish = !full && !head;
             const float w_self = (m == -INFINITY) ? 0.f : ex2((m - m_fin) * c);
             const float inv = 1.f / l_fin;
@@ -1130,7 +1143,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     if (!valid) continue;
                     const int dc = d0 + ch * 32;
                     if (publish) {  // later piece of a pair: unnormalised O for the head owner
-                        float4* po = reinterpret_cast<float4*>(sp) + (dc >> 2) * M + r;
+                        // (DSMEM: into this CTA's drained K ring, in the head's staged layout)
+                        float4* po = reinterpret_cast<float4*>(dsm ? reinterpret_cast<float*>(sm_k + 1024) : sp) +
+                                     (dc >> 2) * M + r;
 #pragma unroll
                         for (int k = 0; k < 8; ++k)
                             po[k * M] = make_float4(ov[4 * k], ov[4 * k + 1], ov[4 * k + 2], ov[4 * k + 3]);
@@ -1162,18 +1177,35 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             }
                         }
                     }
+                    if (threadIdx.x == 0) K1_TRACE(13, 42 + 2 * ch);
                     if (p.o_peers) {  // fused all-gather: this row into every rank's buffer
                         for (int k = 0; k < p.world; ++k)
                             store_row<T, 32>(reinterpret_cast<T*>(p.o_peers[k]) + orow + ch * 32, ov, inv);
                     } else {
                         store_row<T, 32>(reinterpret_cast<T*>(p.o) + orow + ch * 32, ov, inv);
                     }
+                    if (threadIdx.x == 0) K1_TRACE(13, 43 + 2 * ch);
                 }
                 tc_fence_before();
             }
             if (threadIdx.x == 0) K1_TRACE(14, segn);
             mbar_arrive(o_empty);
-            if (publish) {
+            if (publish && dsm) {
+                float* ml = reinterpret_cast<float*>(sm_k);
+                if (valid && half == 0) {
+                    ml[r] = m;
+                    ml[128 + r] = l_row;
+                }
+                named_bar_sync(2, SW * 32);
+                if (threadIdx.x == 0) {
+                    // the head's ring is free once its producer says so; the
+                    // generic-proxy stores above are made visible to the bulk copy
+                    mbar_wait(peer_ready, 0);
+                    fence_proxy_async_smem();
+                    bulk_s2s_cluster(mapa_rank(sm_k, 0), sm_k, 1024u + 4u * C::PIECE_BOX,
+                                     mapa_rank(merge_full, 0));
+                }
+            } else if (publish) {
                 if (valid && half == 0) {
                     sp[128 * HD + r] = m;
                     sp[128 * HD + 128 + r] = l_row;
@@ -1197,6 +1229,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    // DSMEM merge: no CTA leaves while its peer may still copy out of / into it
+    if (dsm) cluster_sync();
     if (p.trace && threadIdx.x == 0) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
@@ -1204,7 +1238,6 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         p.trace[kTraceRows * 64 + kTraceCta * blockIdx.x + 7] = clock64();
     }
     if (warp == SW + 2) tmem_dealloc<C::TMEM_COLS>(tmem);
-    if (pf_sink == 0x9E3779B9u && p.B < 0) __trap();  // never true: keeps the prefetch
 }
 
 // ------------------------------------------------------------------ host --
@@ -1276,15 +1309,37 @@ namespace {
 template <class TT, int MM, int MW>
 st_status launch_tc(const TcLaunch& L, cudaStream_t stream) {
     static bool attr = false;
+    static int max_pairs = 0;  // co-resident 2-CTA clusters
     if (!attr) {
         ST_CUDA_TRY(cudaFuncSetAttribute(tree_attn_tc_kernel<TT, MM, MW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg<MM>::SMEM_BYTES));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(L.grid);
+        cfg.blockDim = dim3(Cfg<MM>::THREADS);
+        cfg.dynamicSmemBytes = Cfg<MM>::SMEM_BYTES;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&max_pairs, tree_attn_tc_kernel<TT, MM, MW>, &cfg) != cudaSuccess) {
+            (void)cudaGetLastError();
+            max_pairs = 0;
+        }
         attr = true;
     }
+    // 2-CTA clusters (the DSMEM merge of two-piece split pairs) whenever every
+    // pair of the grid fits at once; ST_K1_CLUSTER=0 keeps the global path
+    static const bool allow = !(getenv("ST_K1_CLUSTER") && atoi(getenv("ST_K1_CLUSTER")) == 0);
+    const bool clus = allow && L.grid % 2 == 0 && 2 * max_pairs >= L.grid;
+    TcParams prm = L.prm;
+    prm.cluster2 = clus ? 1 : 0;
     ST_CUDA_TRY(launch_pdl_ex(tree_attn_tc_kernel<TT, MM, MW>, dim3(L.grid), dim3(Cfg<MM>::THREADS),
-                              Cfg<MM>::SMEM_BYTES, stream, L.coop, L.tq, L.tk, L.tv, L.tkt, L.tvt,
-                              L.prm));
+                              Cfg<MM>::SMEM_BYTES, stream, L.coop, clus ? 2 : 1, L.tq, L.tk, L.tv, L.tkt,
+                              L.tvt, prm));
     return ST_OK;
 }
 
@@ -1361,6 +1416,7 @@ st_status tree_attention_tc_prepare(const st_attn_args* a, const st_peer_out* po
     prm.head_extra = hx_env < 0 ? 0 : hx_env;
     prm.trace_cta = getenv("ST_K1_TRACE_CTA") ? atoi(getenv("ST_K1_TRACE_CTA")) : 0;
     prm.g_magic = ~0ull / (unsigned long long)(G / R) + 1ull;  // floor(2^64 / slots) + 1
+    prm.cluster2 = 0;  // set per launch (launch_tc)
     static const bool coop = !(getenv("ST_K1_COOP") && atoi(getenv("ST_K1_COOP")) == 0);
     L->coop = coop;
     L->grid = G;

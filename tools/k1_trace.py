@@ -60,6 +60,15 @@ if su[0]:
           "K producer fast start: begin %d, scheduled %d, Q + first ring issued %d" % tuple(int(x - su[0]) if x else -1 for x in su[1:7]))
 
 
+w = t[13][56:60]
+if w[0]:
+    print("warp_first_seg (cycles after fast-start begin): loads %d | scan %d | sched %d | ranges %d" % tuple(int(x - su[4]) for x in w))
+
+e = t[13][40:46]
+if e[0] and t[12][0]:
+    print("head epilogue (cycles after its PV done): merged pieces landed %d | (m,l) merged %d | chunk0 merged %d, stored %d | chunk1 merged %d, stored %d"
+          % tuple(int(x - t[12][0]) if x else -1 for x in e))
+
 st, en, nt = cta[:, 0], cta[:, 1], cta[:, 2]
 t0g = st.min()
 print("\nper-CTA (us): start min/median/max %.2f %.2f %.2f | end min/median/max %.2f %.2f %.2f" % (
