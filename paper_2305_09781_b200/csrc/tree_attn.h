@@ -30,6 +30,7 @@ struct TcParams {
     int trace_cta;              // CTA whose per-tile pipeline is traced (ST_K1_TRACE_CTA)
     unsigned long long g_magic; // floor(2^64 / G) + 1, G = schedule slots: exact floor(x / G)
                                 // for x < 2^40 as one 64-bit high multiply
+    int most_aligned;           // whole pairs when 4G/5 <= pairs <= G (ST_K1_MOST=0: off)
     int cluster2;               // launched as 2-CTA clusters: split pairs of two pieces merge
                                 // over DSMEM (the piece's (O, m, l) copied into the head's
                                 // drained K ring) instead of the global publish / flag path
