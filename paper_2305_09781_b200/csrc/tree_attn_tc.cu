@@ -282,7 +282,11 @@ __device__ __forceinline__ void sched_finish(const TcParams& p, Sched& s, int lo
         } else if (split_span <= streamk_span + p.aligned_slack) {
             s.mode = kSplit;
             s.S = S;
-            s.hx = min((uint32_t)p.head_extra, (uint32_t)s.nt - S);
+            // the symmetric DSMEM exchange (M=128 pairs of two pieces on
+            // 2-CTA clusters) wants equal halves; otherwise the head piece
+            // takes extra tiles, so the other pieces are in by its last P.V
+            const bool sym = p.cluster2 && S == 2 && p.R == 1 && p.G * p.T > 64;
+            s.hx = sym ? 0u : min((uint32_t)p.head_extra, (uint32_t)s.nt - S);
         }
     }
 }
@@ -425,8 +429,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     uint64_t* pv_done = p_full + 2;      // [2]
     uint64_t* o_empty = pv_done + 2;
     uint64_t* merge_full = o_empty + 1;  // staged pieces landed (head owner only)
-    uint64_t* peer_ready = merge_full + 1;  // DSMEM merge: the head's K ring is drained (piece only)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(peer_ready + 1);
+    uint64_t* peer_ready = merge_full + 1;  // DSMEM exchange: the peer's K ring is drained
+    uint64_t* xchg_full = peer_ready + 1;   // DSMEM exchange: the peer's (m, l) + O half landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xchg_full + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) K1_GT(8);
@@ -446,6 +451,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         mbar_init(o_empty, SW * 32);
         mbar_init(merge_full, 1);
         mbar_init(peer_ready, 1);
+        mbar_init(xchg_full, DUAL ? 128 : 1);  // DUAL: one sending thread per row in the peer
         fence_barrier_init();
     }
     if (warp == SW && lane == 0) {
@@ -484,6 +490,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     // segment's first ring-full of tiles (and, unless early_kv, its Q) before
     // the lengths table below exists; the loops further down resume after the
     // pre-issued tiles. early_kv: only committed-prefix tiles, as in the loops.
+    // (Scheduling before the CTA barrier, overlapping the TMEM allocation,
+    // measured no earlier first load and a slower C2 K1.)
     const bool fast = p.B <= 32;
     First f0{};
     uint32_t pre_n = 0;   // first-segment tiles this producer already issued
@@ -498,12 +506,14 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             const uint64_t pol = p.R == 1 ? l2_policy_evict_first() : l2_policy_evict_normal();
             const int jt0 = p.tree_src ? (f0.P + BN - 1) / BN : 1 << 30;  // first tree tile
             const int bh0 = s0.b * p.H + s0.h;
+            if (kside) K1_TRACE(13, 48);
             if (kside && !p.early_kv) {
                 mbar_arrive_expect_tx(q_full, C::A_BYTES);
                 const int node0 = rblk * (M / p.G);
                 tma_load_4d(sm_q, &tm_q, q_full, 0, s0.h * p.G, node0, s0.b);
                 tma_load_4d(sm_q + C::A_ATOM, &tm_q, q_full, 64, s0.h * p.G, node0, s0.b);
                 pre_q = true;
+                K1_TRACE(13, 49);
             }
             uint64_t* full = kside ? k_full : v_full;
             uint8_t* ring = kside ? sm_k : sm_v;
@@ -523,6 +533,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     tma_load_3d_hint(dst, mc, full + pre_n, 0, j * BN, bh0, pol);
                     tma_load_3d_hint(dst + KV_ATOM, mc, full + pre_n, 64, j * BN, bh0, pol);
                 }
+                if (kside) K1_TRACE(13, 50 + pre_n);
             }
             if (kside) K1_TRACE(15, 62);
             if (kside && pre_n > 0) K1_GT(5);
@@ -655,7 +666,33 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         // (published by the following CTAs early in their ranges) into the K
         // ring as soon as the last S MMA has drained it, so the softmax warps'
         // merge reads shared memory instead of making L2 round trips.
-        if (t_end > t_begin) {
+        if (t_end > t_begin && dsm) {
+            // DSMEM merge of a pair's two pieces on one 2-CTA cluster.
+            //   M=64: the head (rank 0, one tile more) receives the piece's O
+            //   in the first K stage its last tiles free — stage kc % KS once
+            //   S of tile kc - KS is done (or the never-used stage kc) — so the
+            //   piece pushes it while the head still runs its last tile.
+            //   DUAL: both CTAs receive the other's half once the whole ring
+            //   has drained (symmetric exchange).
+            if (lane == 0) {
+                const uint32_t kc = (uint32_t)(t_end - t_begin);
+                if constexpr (!DUAL) {
+                    if ((blockIdx.x & 1u) == 0) {
+                        if (kc >= (uint32_t)KS) mbar_wait(k_empty + kc % KS, ((kc - KS) / KS) & 1);
+                        mbar_arrive_expect_tx(xchg_full, 4u * C::PIECE_BOX + 8u * M);
+                        K1_GT(11);
+                        mbar_arrive_cluster(mapa_rank(peer_ready, 1));
+                    }
+                } else {
+                    for (uint32_t st = 0; st < (uint32_t)KS && st < kc; ++st) {
+                        const uint32_t k = kc - 1 - ((kc - 1 - st) % KS);  // last use of stage st
+                        mbar_wait(k_empty + st, (k / KS) & 1);
+                    }
+                    K1_GT(11);
+                    mbar_arrive_cluster(mapa_rank(peer_ready, (blockIdx.x & 1u) ^ 1u));
+                }
+            }
+        } else if (t_end > t_begin) {
             const Seg ls = find_seg(p, cum, t_end - 1, t_end);
             const uint32_t pend = ls.pair_start + (uint32_t)ls.ntiles;
             if (ls.pair_start >= t_begin && pend > t_end) {
@@ -672,25 +709,17 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         mbar_wait(k_empty + st, (k / KS) & 1);
                     }
                     int* pieces = reinterpret_cast<int*>(smem + C::OFF_PIECES);
-                    if (dsm) {  // the one piece arrives from cluster rank 1 by DSMEM
-                        pieces[0] = 1;
-                        pieces[1] = (int)blockIdx.x + 1;
-                        mbar_expect_tx(merge_full, 1024u + 4u * C::PIECE_BOX);
-                        K1_GT(11);
-                        mbar_arrive_cluster(mapa_rank(peer_ready, 1));  // ring drained: send it
-                        mbar_arrive(merge_full);
-                    }
                     int np = 0;
-                    for (uint32_t c2 = slot + 1; c2 < (dsm ? 0u : G) && np < kMaxPieces; ++c2) {
+                    for (uint32_t c2 = slot + 1; c2 < G && np < kMaxPieces; ++c2) {
                         const uint32_t rs = range_start(c2, sched, G);
                         if (rs >= pend) break;
                         if (range_start(c2 + 1, sched, G) == rs) continue;  // empty range
                         pieces[1 + np++] = (int)(c2 * (uint32_t)p.R) + rblk;  // same row block
                     }
-                    if (!dsm) pieces[0] = np;
+                    pieces[0] = np;
                     const int ns = np < C::STAGED_PIECES ? np : C::STAGED_PIECES;
-                    if (!dsm) mbar_expect_tx(merge_full, (uint32_t)ns * (1024u + 4u * C::PIECE_BOX));
-                    if (!dsm) K1_GT(11);
+                    mbar_expect_tx(merge_full, (uint32_t)ns * (1024u + 4u * C::PIECE_BOX));
+                    K1_GT(11);
                     for (int i = 0; i < np; ++i) {
                         const int c2 = pieces[1 + i];
                         wait_flag_gpu(p.flags + c2);
@@ -702,7 +731,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             bulk_load(dst + 1024, p.partial + (long long)c2 * SLOT_FLOATS, 4 * C::PIECE_BOX, merge_full);
                         }
                     }
-                    if (!dsm) mbar_arrive(merge_full);
+                    mbar_arrive(merge_full);
                 }
             }
         }
@@ -1089,142 +1118,328 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 l_row = la * wa + lb * wb;
                 m = mm;
             }
-            // head: final (m, l) over this segment and the pieces of CTAs
-            // blockIdx.x+1, ... whose ranges start inside the pair (CTA order:
-            // deterministic); pass 2 below adds their O chunk by chunk
-            // (the first STAGED_PIECES pieces were staged into the drained K
-            // ring by the K producer warp; any further ones are read from L2)
-            float m_fin = m, l_fin = l_row;
-            const int* pieces = reinterpret_cast<const int*>(smem + C::OFF_PIECES);
-            int np = 0;
-            if (head) {
-                mbar_wait(merge_full, 0);
-                if (threadIdx.x == 0) K1_GT(10);
-                if (threadIdx.x == 0) K1_TRACE(13, 40);
-                np = pieces[0];
-            }
-            if (head && valid) {
-                for (int i = 0; i < np; ++i) {
-                    float mp, lp;
-                    if (i < C::STAGED_PIECES) {
-                        const float* ml = reinterpret_cast<const float*>(sm_k + i * C::PIECE_SMEM);
-                        mp = ml[r];
-                        lp = ml[128 + r];
-                    } else {
-                        const float* piece = p.partial + (long long)pieces[1 + i] * SLOT_FLOATS;
-                        mp = __ldcg(piece + 128 * HD + r);
-                        lp = __ldcg(piece + 128 * HD + 128 + r);
-                    }
-                    const float mm = fmaxf(m_fin, mp);
-                    if (mm != -INFINITY) {
-                        l_fin = (m_fin == -INFINITY ? 0.f : l_fin * ex2((m_fin - mm) * c)) +
-                                (mp == -INFINITY ? 0.f : lp * ex2((mp - mm) * c));
-                        m_fin = mm;
-                    }
-                }
-            }
-            if (threadIdx.x == 0) K1_TRACE(13, 41);
-            const bool publish = !full && !head;
-            const float w_self = (m == -INFINITY) ? 0.f : ex2((m - m_fin) * c);
-            const float inv = 1.f / l_fin;
-            float* sp = p.partial + (long long)blockIdx.x * SLOT_FLOATS;
-            if (warp_live) {
-                tc_fence_after();
-#pragma unroll 1
-                for (int ch = 0; ch < DCOLS / 32; ++ch) {
-                    float ov[32];
-                    uint32_t raw[32];
-                    // M=64: this lane's d half of the shared O. DUAL: d half
-                    // `half` of both accumulators, weighted.
-                    tmem_ld_32x32b_x32(lane_addr + C::O_COL + (DUAL ? half * DCOLS : 0) + ch * 32, raw);
-                    tmem_ld_wait();
+            if (dsm && !DUAL) {
+                // ==== DSMEM merge, M=64: the pair's head (rank 0) and piece ====
+                // (rank 1) sit in one 2-CTA cluster. The piece stages its O,
+                // float4 (r, 4q..4q+3) at q * M + r, and its (m, l) in its own
+                // drained K ring and bulk-copies them (cluster shared memory,
+                // completing on the head's xchg_full) into the head's first
+                // freed K stage and its idle second Q buffer (one segment per
+                // CTA in this schedule) while the head still runs its last
+                // tile; the head merges and writes the rows out. (Per-thread
+                // st.shared::cluster stores + a release arrive measured
+                // slower: the release waits for every remote store.)
+                const uint32_t rank = blockIdx.x & 1u;
+                float ov[DCOLS];
+                if (warp_live) {
+                    tc_fence_after();
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) ov[k] = __uint_as_float(raw[k]) * wa;
+                    for (int ch = 0; ch < DCOLS / 32; ++ch) {
+                        uint32_t raw[32];
+                        tmem_ld_32x32b_x32(lane_addr + C::O_COL + ch * 32, raw);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) ov[ch * 32 + k] = __uint_as_float(raw[k]);
+                    }
+                    tc_fence_before();
+                }
+                const uint32_t khead = rank ? (uint32_t)s.lo : (uint32_t)ntl;  // the head's K tiles
+                uint8_t* rx = sm_k + (khead >= (uint32_t)KS ? khead % KS : khead) * TILE_BYTES;
+                float* mlb = reinterpret_cast<float*>(sm_q + C::A_BYTES);
+                const bool stamp = threadIdx.x == 0;
+                if (stamp) K1_TRACE(14, 40 + 4 * rank);
+                if (rank) {
+                    // O and (m, l) into this CTA's own drained K ring, then two
+                    // bulk copies into the head's, completing on its xchg_full
+                    float* lo_o = reinterpret_cast<float*>(sm_k);
+                    float* lo_ml = reinterpret_cast<float*>(sm_k + 4 * C::PIECE_BOX);
+                    if (half == 0) reinterpret_cast<float2*>(lo_ml)[r] = make_float2(m, l_row);
+                    if (warp_live) {
+                        float4* po = reinterpret_cast<float4*>(lo_o) + half * (DCOLS / 4) * M + r;
+#pragma unroll
+                        for (int q = 0; q < DCOLS / 4; ++q)
+                            po[q * M] = make_float4(ov[4 * q], ov[4 * q + 1], ov[4 * q + 2], ov[4 * q + 3]);
+                    }
+                    fence_proxy_async_smem();
+                    named_bar_sync(2, SW * 32);
+                    if (stamp) K1_TRACE(14, 46);
+                    if (threadIdx.x == 0) {
+                        mbar_wait_cluster(peer_ready, 0);
+                        K1_TRACE(14, 45);
+                        bulk_s2s_cluster(mapa_rank(rx, 0), lo_o, 4u * C::PIECE_BOX, mapa_rank(xchg_full, 0));
+                        bulk_s2s_cluster(mapa_rank(mlb, 0), lo_ml, 8u * M, mapa_rank(xchg_full, 0));
+                        K1_TRACE(14, 47);
+                    }
+                } else {
+                    mbar_wait_cluster(xchg_full, 0);
+                    if (threadIdx.x == 0) K1_GT(10);
+                    if (stamp) K1_TRACE(14, 41);
+                    const float2 ml = reinterpret_cast<const float2*>(mlb)[r];
+                    const float mf = fmaxf(m, ml.x);
+                    const float w_self = m == -INFINITY ? 0.f : ex2((m - mf) * c);
+                    const float wp = ml.x == -INFINITY ? 0.f : ex2((ml.x - mf) * c);
+                    const float lf = l_row * w_self + ml.y * wp;
+                    if (valid) {
+                        const float4* pp = reinterpret_cast<const float4*>(rx) + half * (DCOLS / 4) * M + r;
+#pragma unroll
+                        for (int q = 0; q < DCOLS / 4; ++q) {
+                            const float4 x = pp[q * M];
+                            ov[4 * q] = fmaf(x.x, wp, ov[4 * q] * w_self);
+                            ov[4 * q + 1] = fmaf(x.y, wp, ov[4 * q + 1] * w_self);
+                            ov[4 * q + 2] = fmaf(x.z, wp, ov[4 * q + 2] * w_self);
+                            ov[4 * q + 3] = fmaf(x.w, wp, ov[4 * q + 3] * w_self);
+                        }
+                        if (stamp) K1_TRACE(14, 43);
+                        const float inv = 1.f / lf;
+                        if (p.o_peers) {  // fused all-gather: this row into every rank's buffer
+                            for (int k = 0; k < p.world; ++k)
+                                store_row<T, DCOLS>(reinterpret_cast<T*>(p.o_peers[k]) + orow, ov, inv);
+                        } else {
+                            store_row<T, DCOLS>(reinterpret_cast<T*>(p.o) + orow, ov, inv);
+                        }
+                        if (p.lse && half == 0)
+                            p.lse[((long long)s.b * p.Hq + s.h * p.G + g_r) * p.T + u_r] = mf * p.scale + __logf(lf);
+                    }
+                    if (stamp) K1_TRACE(14, 42);
+                }
+                mbar_arrive(o_empty);
+            } else if (dsm) {
+                // ==== DSMEM exchange, DUAL: the pair's two pieces sit in one 2-CTA ====
+                // cluster (piece index = cluster rank) and finish together. CTA
+                // `rank` finalises d columns [64 rank, 64 rank + 64): the threads
+                // holding the other d half (one per row) store their (m, l) and
+                // O columns into the peer's drained K ring and arrive on its
+                // xchg_full; the threads holding this CTA's half wait for the
+                // peer's, merge in piece order and write the rows out.
+                const uint32_t rank = blockIdx.x & 1u;
+                const bool sender = (uint32_t)half != rank;
+                // this thread's d half of O, 32 columns at a time (DUAL: both
+                // accumulators, weighted). M=64: a row's two d halves sit in
+                // one warp, one sending, one receiving, so both chunks are read
+                // (warp-collective) before any lane waits; DUAL: the halves
+                // are whole warps and read chunk by chunk.
+                float ov[DUAL ? 1 : DCOLS];
+                auto chunk = [&](int ch, float (&cv)[32]) {
                     if constexpr (DUAL) {
+                        uint32_t raw[32];
+                        tmem_ld_32x32b_x32(lane_addr + C::O_COL + half * DCOLS + ch * 32, raw);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) cv[k] = __uint_as_float(raw[k]) * wa;
                         tmem_ld_32x32b_x32(lane_addr + C::OB_COL + half * DCOLS + ch * 32, raw);
                         tmem_ld_wait();
 #pragma unroll
-                        for (int k = 0; k < 32; ++k) ov[k] += __uint_as_float(raw[k]) * wb;
+                        for (int k = 0; k < 32; ++k) cv[k] += __uint_as_float(raw[k]) * wb;
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) cv[k] = ov[ch * 32 + k];
                     }
-                    if (!valid) continue;
-                    const int dc = d0 + ch * 32;
-                    if (publish) {  // later piece of a pair: unnormalised O for the head owner
-                        // (DSMEM: into this CTA's drained K ring, in the head's staged layout)
-                        float4* po = reinterpret_cast<float4*>(dsm ? reinterpret_cast<float*>(sm_k + 1024) : sp) +
-                                     (dc >> 2) * M + r;
+                };
+                if (warp_live) tc_fence_after();
+                if constexpr (!DUAL) {
+                    if (warp_live) {
 #pragma unroll
-                        for (int k = 0; k < 8; ++k)
-                            po[k * M] = make_float4(ov[4 * k], ov[4 * k + 1], ov[4 * k + 2], ov[4 * k + 3]);
-                        continue;
-                    }
-                    if (head) {
+                        for (int ch = 0; ch < DCOLS / 32; ++ch) {
+                            uint32_t raw[32];
+                            tmem_ld_32x32b_x32(lane_addr + C::O_COL + ch * 32, raw);
+                            tmem_ld_wait();
 #pragma unroll
-                        for (int k = 0; k < 32; ++k) ov[k] *= w_self;
-                        for (int i = 0; i < np; ++i) {
-                            const bool staged = i < C::STAGED_PIECES;
-                            const float* piece = staged
-                                ? reinterpret_cast<const float*>(sm_k + i * C::PIECE_SMEM)
-                                : p.partial + (long long)pieces[1 + i] * SLOT_FLOATS;
-                            const float mp = staged ? piece[r] : __ldcg(piece + 128 * HD + r);
-                            if (mp == -INFINITY) continue;
-                            const float wp = ex2((mp - m_fin) * c);
-                            // float4 (r, dc + 4k) at (dc/4 + k) * M + r of the piece's O
-                            const float4* pp =
-                                reinterpret_cast<const float4*>(staged ? reinterpret_cast<const uint8_t*>(piece) + 1024
-                                                                       : reinterpret_cast<const uint8_t*>(piece)) +
-                                (dc >> 2) * M + r;
-#pragma unroll
-                            for (int k = 0; k < 8; ++k) {
-                                const float4 x = staged ? pp[k * M] : __ldcg(pp + k * M);
-                                ov[4 * k] = fmaf(x.x, wp, ov[4 * k]);
-                                ov[4 * k + 1] = fmaf(x.y, wp, ov[4 * k + 1]);
-                                ov[4 * k + 2] = fmaf(x.z, wp, ov[4 * k + 2]);
-                                ov[4 * k + 3] = fmaf(x.w, wp, ov[4 * k + 3]);
-                            }
+                            for (int k = 0; k < 32; ++k) ov[ch * 32 + k] = __uint_as_float(raw[k]);
                         }
                     }
-                    if (threadIdx.x == 0) K1_TRACE(13, 42 + 2 * ch);
-                    if (p.o_peers) {  // fused all-gather: this row into every rank's buffer
-                        for (int k = 0; k < p.world; ++k)
-                            store_row<T, 32>(reinterpret_cast<T*>(p.o_peers[k]) + orow + ch * 32, ov, inv);
-                    } else {
-                        store_row<T, 32>(reinterpret_cast<T*>(p.o) + orow + ch * 32, ov, inv);
+                }
+                // receive area in the drained K ring: (m, l) as float2[M], then
+                // the O half as float4 (r, 4q..4q+3) at q * M + r
+                float* xb = reinterpret_cast<float*>(sm_k);
+                // trace stamps (row 14, columns 40-47): thread 0 and the first
+                // thread of the other d half (lane 16 for M=64, warp 4 DUAL)
+                const bool stamp = threadIdx.x == 0 || threadIdx.x == (DUAL ? 128 : 16);
+                if (stamp) K1_TRACE(14, 40 + (sender ? 4 : 0));
+                if (sender) {
+                    const uint32_t peer = rank ^ 1u;
+                    mbar_wait_cluster(peer_ready, 0);
+                    if (stamp) K1_TRACE(14, 45);
+                    st_cluster_v2(mapa_rank(xb + 2 * r, peer), m, l_row);
+                    if (warp_live) {
+                        const uint32_t ob = mapa_rank(xb + 2 * 128, peer) + 16u * (uint32_t)r;
+#pragma unroll
+                        for (int ch = 0; ch < DCOLS / 32; ++ch) {
+                            float cv[32];
+                            chunk(ch, cv);
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                st_cluster_v4(ob + 16u * (uint32_t)((ch * 8 + q) * M), cv[4 * q], cv[4 * q + 1],
+                                              cv[4 * q + 2], cv[4 * q + 3]);
+                        }
                     }
-                    if (threadIdx.x == 0) K1_TRACE(13, 43 + 2 * ch);
+                    if (stamp) K1_TRACE(14, 46);
+                    mbar_arrive_cluster(mapa_rank(xchg_full, peer));
+                    if (stamp) K1_TRACE(14, 47);
+                } else {
+                    mbar_wait_cluster(xchg_full, 0);
+                    if (threadIdx.x == 0) K1_GT(10);
+                    if (stamp) K1_TRACE(14, 41);
+                    const float2 ml = reinterpret_cast<const float2*>(xb)[r];
+                    // piece order (rank 0 first), whichever CTA finalises the half
+                    const float m0 = rank ? ml.x : m, l0 = rank ? ml.y : l_row;
+                    const float m1 = rank ? m : ml.x, l1 = rank ? l_row : ml.y;
+                    const float mf = fmaxf(m0, m1);
+                    const float w0 = m0 == -INFINITY ? 0.f : ex2((m0 - mf) * c);
+                    const float w1 = m1 == -INFINITY ? 0.f : ex2((m1 - mf) * c);
+                    const float lf = l0 * w0 + l1 * w1;
+                    const float inv = 1.f / lf;
+                    if (warp_live) {
+                        const float4* pp = reinterpret_cast<const float4*>(xb + 2 * 128) + r;
+#pragma unroll
+                        for (int ch = 0; ch < DCOLS / 32; ++ch) {
+                            float cv[32];
+                            chunk(ch, cv);
+                            if (!valid) continue;
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const float4 x = pp[(ch * 8 + q) * M];
+                                const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) {
+                                    const float a0 = rank ? xs[k] : cv[4 * q + k];
+                                    const float a1 = rank ? cv[4 * q + k] : xs[k];
+                                    cv[4 * q + k] = fmaf(a1, w1, a0 * w0);
+                                }
+                            }
+                            if (p.o_peers) {  // fused all-gather: this row into every rank's buffer
+                                for (int k = 0; k < p.world; ++k)
+                                    store_row<T, 32>(reinterpret_cast<T*>(p.o_peers[k]) + orow + ch * 32, cv, inv);
+                            } else {
+                                store_row<T, 32>(reinterpret_cast<T*>(p.o) + orow + ch * 32, cv, inv);
+                            }
+                        }
+                        if (valid && p.lse && rank == 0)
+                            p.lse[((long long)s.b * p.Hq + s.h * p.G + g_r) * p.T + u_r] = mf * p.scale + __logf(lf);
+                    }
+                    if (stamp) K1_TRACE(14, 42);
                 }
-                tc_fence_before();
-            }
-            if (threadIdx.x == 0) K1_TRACE(14, segn);
-            mbar_arrive(o_empty);
-            if (publish && dsm) {
-                float* ml = reinterpret_cast<float*>(sm_k);
-                if (valid && half == 0) {
-                    ml[r] = m;
-                    ml[128 + r] = l_row;
-                }
-                named_bar_sync(2, SW * 32);
-                if (threadIdx.x == 0) {
-                    // the head's ring is free once its producer says so; the
-                    // generic-proxy stores above are made visible to the bulk copy
-                    mbar_wait(peer_ready, 0);
-                    fence_proxy_async_smem();
-                    bulk_s2s_cluster(mapa_rank(sm_k, 0), sm_k, 1024u + 4u * C::PIECE_BOX,
-                                     mapa_rank(merge_full, 0));
-                }
-            } else if (publish) {
-                if (valid && half == 0) {
-                    sp[128 * HD + r] = m;
-                    sp[128 * HD + 128 + r] = l_row;
-                }
-                // bar.sync orders every thread's stores before thread 0's
-                // gpu-scope release (release is cumulative)
-                named_bar_sync(2, SW * 32);
-                if (threadIdx.x == 0) st_release_gpu(p.flags + blockIdx.x, 1u);
+                if (warp_live) tc_fence_before();
+                mbar_arrive(o_empty);
             } else {
-                if (valid && p.lse && half == 0)
-                    p.lse[((long long)s.b * p.Hq + s.h * p.G + g_r) * p.T + u_r] = m_fin * p.scale + __logf(l_fin);
+                // head: final (m, l) over this segment and the pieces of CTAs
+                // blockIdx.x+1, ... whose ranges start inside the pair (CTA order:
+                // deterministic); pass 2 below adds their O chunk by chunk
+                // (the first STAGED_PIECES pieces were staged into the drained K
+                // ring by the K producer warp; any further ones are read from L2)
+                float m_fin = m, l_fin = l_row;
+                const int* pieces = reinterpret_cast<const int*>(smem + C::OFF_PIECES);
+                int np = 0;
+                if (head) {
+                    mbar_wait(merge_full, 0);
+                    if (threadIdx.x == 0) K1_GT(10);
+                    if (threadIdx.x == 0) K1_TRACE(13, 40);
+                    np = pieces[0];
+                }
+                if (head && valid) {
+                    for (int i = 0; i < np; ++i) {
+                        float mp, lp;
+                        if (i < C::STAGED_PIECES) {
+                            const float* ml = reinterpret_cast<const float*>(sm_k + i * C::PIECE_SMEM);
+                            mp = ml[r];
+                            lp = ml[128 + r];
+                        } else {
+                            const float* piece = p.partial + (long long)pieces[1 + i] * SLOT_FLOATS;
+                            mp = __ldcg(piece + 128 * HD + r);
+                            lp = __ldcg(piece + 128 * HD + 128 + r);
+                        }
+                        const float mm = fmaxf(m_fin, mp);
+                        if (mm != -INFINITY) {
+                            l_fin = (m_fin == -INFINITY ? 0.f : l_fin * ex2((m_fin - mm) * c)) +
+                                    (mp == -INFINITY ? 0.f : lp * ex2((mp - mm) * c));
+                            m_fin = mm;
+                        }
+                    }
+                }
+                if (threadIdx.x == 0) K1_TRACE(13, 41);
+                const bool publish = !full && !head;
+                const float w_self = (m == -INFINITY) ? 0.f : ex2((m - m_fin) * c);
+                const float inv = 1.f / l_fin;
+                float* sp = p.partial + (long long)blockIdx.x * SLOT_FLOATS;
+                if (warp_live) {
+                    tc_fence_after();
+    #pragma unroll 1
+                    for (int ch = 0; ch < DCOLS / 32; ++ch) {
+                        float ov[32];
+                        uint32_t raw[32];
+                        // M=64: this lane's d half of the shared O. DUAL: d half
+                        // `half` of both accumulators, weighted.
+                        tmem_ld_32x32b_x32(lane_addr + C::O_COL + (DUAL ? half * DCOLS : 0) + ch * 32, raw);
+                        tmem_ld_wait();
+    #pragma unroll
+                        for (int k = 0; k < 32; ++k) ov[k] = __uint_as_float(raw[k]) * wa;
+                        if constexpr (DUAL) {
+                            tmem_ld_32x32b_x32(lane_addr + C::OB_COL + half * DCOLS + ch * 32, raw);
+                            tmem_ld_wait();
+    #pragma unroll
+                            for (int k = 0; k < 32; ++k) ov[k] += __uint_as_float(raw[k]) * wb;
+                        }
+                        if (!valid) continue;
+                        const int dc = d0 + ch * 32;
+                        if (publish) {  // later piece of a pair: unnormalised O for the head owner
+                            float4* po = reinterpret_cast<float4*>(sp) + (dc >> 2) * M + r;
+    #pragma unroll
+                            for (int k = 0; k < 8; ++k)
+                                po[k * M] = make_float4(ov[4 * k], ov[4 * k + 1], ov[4 * k + 2], ov[4 * k + 3]);
+                            continue;
+                        }
+                        if (head) {
+    #pragma unroll
+                            for (int k = 0; k < 32; ++k) ov[k] *= w_self;
+                            for (int i = 0; i < np; ++i) {
+                                const bool staged = i < C::STAGED_PIECES;
+                                const float* piece = staged
+                                    ? reinterpret_cast<const float*>(sm_k + i * C::PIECE_SMEM)
+                                    : p.partial + (long long)pieces[1 + i] * SLOT_FLOATS;
+                                const float mp = staged ? piece[r] : __ldcg(piece + 128 * HD + r);
+                                if (mp == -INFINITY) continue;
+                                const float wp = ex2((mp - m_fin) * c);
+                                // float4 (r, dc + 4k) at (dc/4 + k) * M + r of the piece's O
+                                const float4* pp =
+                                    reinterpret_cast<const float4*>(staged ? reinterpret_cast<const uint8_t*>(piece) + 1024
+                                                                           : reinterpret_cast<const uint8_t*>(piece)) +
+                                    (dc >> 2) * M + r;
+    #pragma unroll
+                                for (int k = 0; k < 8; ++k) {
+                                    const float4 x = staged ? pp[k * M] : __ldcg(pp + k * M);
+                                    ov[4 * k] = fmaf(x.x, wp, ov[4 * k]);
+                                    ov[4 * k + 1] = fmaf(x.y, wp, ov[4 * k + 1]);
+                                    ov[4 * k + 2] = fmaf(x.z, wp, ov[4 * k + 2]);
+                                    ov[4 * k + 3] = fmaf(x.w, wp, ov[4 * k + 3]);
+                                }
+                            }
+                        }
+                        if (threadIdx.x == 0) K1_TRACE(13, 42 + 2 * ch);
+                        if (p.o_peers) {  // fused all-gather: this row into every rank's buffer
+                            for (int k = 0; k < p.world; ++k)
+                                store_row<T, 32>(reinterpret_cast<T*>(p.o_peers[k]) + orow + ch * 32, ov, inv);
+                        } else {
+                            store_row<T, 32>(reinterpret_cast<T*>(p.o) + orow + ch * 32, ov, inv);
+                        }
+                        if (threadIdx.x == 0) K1_TRACE(13, 43 + 2 * ch);
+                    }
+                    tc_fence_before();
+                }
+                if (threadIdx.x == 0) K1_TRACE(14, segn);
+                mbar_arrive(o_empty);
+                if (publish) {
+                    if (valid && half == 0) {
+                        sp[128 * HD + r] = m;
+                        sp[128 * HD + 128 + r] = l_row;
+                    }
+                    // bar.sync orders every thread's stores before thread 0's
+                    // gpu-scope release (release is cumulative)
+                    named_bar_sync(2, SW * 32);
+                    if (threadIdx.x == 0) st_release_gpu(p.flags + blockIdx.x, 1u);
+                } else {
+                    if (valid && p.lse && half == 0)
+                        p.lse[((long long)s.b * p.Hq + s.h * p.G + g_r) * p.T + u_r] = m_fin * p.scale + __logf(l_fin);
+                }
             }
-
             if (threadIdx.x == 0) K1_GT(4);
             if (threadIdx.x == 0) K1_TRACE(15, segn);
             ++segn;

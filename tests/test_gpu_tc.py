@@ -240,13 +240,16 @@ def test_verify_compact_from_k_tree(capi, restatement):
         assert torch.equal(v1[:, b, :, : p + L], v2[:, b, :, : p + L])
 
 
-@pytest.mark.parametrize("B,H,P,T", [(2, 4, 3000, 32), (8, 8, 2048, 61), (1, 3, 700, 128)])
+@pytest.mark.parametrize("B,H,P,T", [(2, 4, 3000, 32), (8, 8, 2048, 61), (8, 8, 1500, 100),
+                                     (1, 3, 700, 128)])
 def test_tc_split_schedule(capi, restatement, B, H, P, T):
     """Uniform pairs with Np <= G/2 take the split schedule: every pair cut into
     S = G/Np single-segment pieces, the head piece min(kHeadExtra, nt - S)
     tiles longer (S = 18 for 8 pairs: the head owner merges 17 pieces, 2 staged
-    in shared memory and the rest from L2; the third case has nt == S, so no
-    extra tile)."""
+    in shared memory and the rest from L2; the last case has nt == S, so no
+    extra tile). 64 pairs (C4's per-rank slice, M=64, and an M=128 tree) give
+    S = 2 on 2-CTA clusters: two equal pieces that exchange (m, l) and one d
+    half of O over DSMEM, each CTA writing the other half."""
     rng = np.random.default_rng(B * 7 + H)
     w = 3 if T >= 16 else 2
     trees = [restatement.merge(width_depth_seqs(rng, int(rng.integers(0, 50)), 50, w, (T - 1) // w),

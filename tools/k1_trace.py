@@ -60,10 +60,21 @@ if su[0]:
           "K producer fast start: begin %d, scheduled %d, Q + first ring issued %d" % tuple(int(x - su[0]) if x else -1 for x in su[1:7]))
 
 
+fi = t[13][48:54]
+if fi[0]:
+    print("fast-start issue (cycles after scheduled): policy %d | Q %d | stage0 %d | stage1 %d | stage2 %d"
+          % tuple(int(x - su[5]) if x else -1 for x in fi[:5]))
 w = t[13][56:60]
 if w[0]:
     print("warp_first_seg (cycles after fast-start begin): loads %d | scan %d | sched %d | ranges %d" % tuple(int(x - su[4]) for x in w))
 
+x = t[14][40:48]
+if x[0] or x[4]:
+    pv = t[12][0]
+    f = lambda v: int(v - pv) if v else -1  # noqa: E731
+    print("DSMEM exchange (cycles after the traced CTA's last PV done): receiver: O read %d, peer half landed %d, "
+          "merged %d, stored %d | sender: O read %d, peer ring free %d, staged %d, copies issued %d"
+          % (f(x[0]), f(x[1]), f(x[3]), f(x[2]), f(x[4]), f(x[5]), f(x[6]), f(x[7])))
 e = t[13][40:46]
 if e[0] and t[12][0]:
     print("head epilogue (cycles after its PV done): merged pieces landed %d | (m,l) merged %d | chunk0 merged %d, stored %d | chunk1 merged %d, stored %d"
