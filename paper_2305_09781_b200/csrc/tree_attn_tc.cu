@@ -394,6 +394,28 @@ __device__ __forceinline__ void store_row(T* dst_row, const float* v, float scal
     }
 }
 
+// One 128-row K or V tile (both 64-column SWIZZLE_128B halves) into `dst`,
+// from the cache ([B*Hkv][Lmax][D], rows from `row`) or, `tree`, from the
+// tree's own rows ([B][T][Hkv][D]). mc (two row blocks per pair on a 2-CTA
+// cluster): this CTA loads only d half `rank` and multicasts it into both
+// CTAs' rings, so each tile is read from L2 once and every ring still gets
+// the whole tile (each CTA's barrier expects the full tile bytes).
+__device__ __forceinline__ void load_kv_tile(uint8_t* dst, uint64_t* bar, const CUtensorMap* cache_map,
+                                             const CUtensorMap* tree_map, bool tree, int row, int h, int b,
+                                             int bh, uint64_t pol, bool mc, int rank) {
+    if (mc) {
+        uint8_t* d = dst + rank * KV_ATOM;
+        if (tree) tma_load_4d_mc(d, tree_map, bar, 64 * rank, h, row, b, 0x3);
+        else tma_load_3d_mc(d, cache_map, bar, 64 * rank, row, bh, 0x3, pol);
+    } else if (tree) {
+        tma_load_4d(dst, tree_map, bar, 0, h, row, b);
+        tma_load_4d(dst + KV_ATOM, tree_map, bar, 64, h, row, b);
+    } else {
+        tma_load_3d_hint(dst, cache_map, bar, 0, row, bh, pol);
+        tma_load_3d_hint(dst + KV_ATOM, cache_map, bar, 64, row, bh, pol);
+    }
+}
+
 // MW: ancestor-mask words held per row (2: T <= 128; 4: T <= 256, the
 // two-row-block instantiation — kept separate so the common case keeps its
 // registers).
@@ -441,8 +463,11 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     if (threadIdx.x == 0) {
         if (smem_u32(smem) & 1023u) __trap();  // misaligned dynamic shared memory
         for (int i = 0; i < QS; ++i) { mbar_init(q_full + i, 1); mbar_init(q_empty + i, 1); }
-        for (int i = 0; i < KS; ++i) { mbar_init(k_full + i, 1); mbar_init(k_empty + i, 1); }
-        for (int i = 0; i < VS; ++i) { mbar_init(v_full + i, 1); mbar_init(v_empty + i, 1); }
+        // mc: a stage is free once BOTH CTAs' MMAs have read it (the MMA
+        // warps commit to the empty barriers of the whole cluster)
+        const uint32_t ne = M == 128 && p.R == 2 && p.cluster2 ? 2u : 1u;
+        for (int i = 0; i < KS; ++i) { mbar_init(k_full + i, 1); mbar_init(k_empty + i, ne); }
+        for (int i = 0; i < VS; ++i) { mbar_init(v_full + i, 1); mbar_init(v_empty + i, ne); }
         for (int i = 0; i < 2; ++i) {
             mbar_init(s_full + i, 1);
             mbar_init(p_full + i, SW * 32);
@@ -464,8 +489,13 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         if (p.tree_src) prefetch_tmap(&tm_vt);
     }
     if (warp == SW + 2) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+    // two row blocks per pair on a 2-CTA cluster: the slot's CTAs multicast
+    // K/V tiles into each other's rings, so both must have initialised their
+    // barriers before either issues a load
+    const bool mc = M == 128 && p.R == 2 && p.cluster2;  // (M=64 pairs never take two row blocks)
     tc_fence_before();
-    __syncthreads();
+    if (mc) cluster_sync();
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) K1_TRACE(15, 57);
@@ -503,7 +533,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         if (lane == 0 && f0.t_begin < f0.t_end) {
             const Seg& s0 = f0.s;
             const bool kside = warp == SW;
-            const uint64_t pol = p.R == 1 ? l2_policy_evict_first() : l2_policy_evict_normal();
+            const uint64_t pol = p.R == 1 || mc ? l2_policy_evict_first() : l2_policy_evict_normal();
             const int jt0 = p.tree_src ? (f0.P + BN - 1) / BN : 1 << 30;  // first tree tile
             const int bh0 = s0.b * p.H + s0.h;
             if (kside) K1_TRACE(13, 48);
@@ -517,7 +547,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             }
             uint64_t* full = kside ? k_full : v_full;
             uint8_t* ring = kside ? sm_k : sm_v;
-            const CUtensorMap* mc = kside ? &tm_k : &tm_v;
+            const CUtensorMap* mcache = kside ? &tm_k : &tm_v;
             const CUtensorMap* mt = kside ? &tm_kt : &tm_vt;
             const uint32_t cap = kside ? (uint32_t)KS : (uint32_t)VS;
             for (int j = s0.lo; j < s0.hi && pre_n < cap &&
@@ -525,14 +555,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                  ++j, ++pre_n) {
                 // first use of each stage: nothing to wait for
                 mbar_arrive_expect_tx(full + pre_n, TILE_BYTES);
-                uint8_t* dst = ring + pre_n * TILE_BYTES;
-                if (j >= jt0) {
-                    tma_load_4d(dst, mt, full + pre_n, 0, s0.h, (j - jt0) * BN, s0.b);
-                    tma_load_4d(dst + KV_ATOM, mt, full + pre_n, 64, s0.h, (j - jt0) * BN, s0.b);
-                } else {
-                    tma_load_3d_hint(dst, mc, full + pre_n, 0, j * BN, bh0, pol);
-                    tma_load_3d_hint(dst + KV_ATOM, mc, full + pre_n, 64, j * BN, bh0, pol);
-                }
+                const bool tr = j >= jt0;
+                load_kv_tile(ring + pre_n * TILE_BYTES, full + pre_n, mcache, mt, tr, (tr ? j - jt0 : j) * BN,
+                             s0.h, s0.b, bh0, pol, mc, rblk);
                 if (kside) K1_TRACE(13, 50 + pre_n);
             }
             if (kside) K1_TRACE(15, 62);
@@ -604,7 +629,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             // the KV stream is read once (R = 1): evict_first keeps Q, masks and
             // pieces in L2. With two row blocks (R = 2) both CTAs of a slot read
             // every tile: normal priority, so the second read finds it in L2.
-            const uint64_t pol = p.R == 1 ? l2_policy_evict_first() : l2_policy_evict_normal();
+            const uint64_t pol = p.R == 1 || mc ? l2_policy_evict_first() : l2_policy_evict_normal();
             uint32_t qc = 0, kc = 0;
             bool waited = !p.early_kv;
             for (uint32_t t = t_begin; t < t_end;) {
@@ -624,9 +649,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                          ++j, ++kc) {
                         const uint32_t st = kc;  // first use of each stage: nothing to wait for
                         mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
-                        uint8_t* dst = sm_k + st * TILE_BYTES;
-                        tma_load_3d_hint(dst, &tm_k, k_full + st, 0, j * BN, bh0, pol);
-                        tma_load_3d_hint(dst + KV_ATOM, &tm_k, k_full + st, 64, j * BN, bh0, pol);
+                        load_kv_tile(sm_k + st * TILE_BYTES, k_full + st, &tm_k, &tm_kt, false, j * BN, s.h,
+                                     s.b, bh0, pol, mc, rblk);
                     }
                     pdl_wait();
                     waited = true;
@@ -650,14 +674,10 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     K1_TRACE(0, kc);
                     if (kc == 0) K1_GT(5);
                     mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
-                    uint8_t* dst = sm_k + st * TILE_BYTES;
-                    if (j >= jt0) {  // the tree's own rows [B][T][Hkv][D], 128 nodes per tile
-                        tma_load_4d(dst, &tm_kt, k_full + st, 0, s.h, (j - jt0) * BN, s.b);
-                        tma_load_4d(dst + KV_ATOM, &tm_kt, k_full + st, 64, s.h, (j - jt0) * BN, s.b);
-                    } else {
-                        tma_load_3d_hint(dst, &tm_k, k_full + st, 0, j * BN, bh, pol);
-                        tma_load_3d_hint(dst + KV_ATOM, &tm_k, k_full + st, 64, j * BN, bh, pol);
-                    }
+                    // (tree tiles: the tree's own rows [B][T][Hkv][D], 128 nodes per tile)
+                    const bool tr = j >= jt0;
+                    load_kv_tile(sm_k + st * TILE_BYTES, k_full + st, &tm_k, &tm_kt, tr, (tr ? j - jt0 : j) * BN,
+                                 s.h, s.b, bh, pol, mc, rblk);
                 }
                 t += s.hi - s.lo;
             }
@@ -738,7 +758,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     } else if (warp == SW + 1) {
         // =========================== TMA producer: V ============================
         if (lane == 0) {
-            const uint64_t pol = p.R == 1 ? l2_policy_evict_first() : l2_policy_evict_normal();
+            const uint64_t pol = p.R == 1 || mc ? l2_policy_evict_first() : l2_policy_evict_normal();
             uint32_t vc = 0;
             bool waited = !p.early_kv;
             for (uint32_t t = t_begin; t < t_end;) {
@@ -758,9 +778,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                          ++j, ++vc) {
                         const uint32_t st = vc;
                         mbar_arrive_expect_tx(v_full + st, TILE_BYTES);
-                        uint8_t* dst = sm_v + st * TILE_BYTES;
-                        tma_load_3d_hint(dst, &tm_v, v_full + st, 0, j * BN, bh, pol);
-                        tma_load_3d_hint(dst + KV_ATOM, &tm_v, v_full + st, 64, j * BN, bh, pol);
+                        load_kv_tile(sm_v + st * TILE_BYTES, v_full + st, &tm_v, &tm_vt, false, j * BN, s.h,
+                                     s.b, bh, pol, mc, rblk);
                     }
                     pdl_wait();
                     waited = true;
@@ -770,14 +789,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     mbar_wait(v_empty + st, ph ^ 1);
                     K1_TRACE(1, vc);
                     mbar_arrive_expect_tx(v_full + st, TILE_BYTES);
-                    uint8_t* dst = sm_v + st * TILE_BYTES;
-                    if (j >= jt0) {
-                        tma_load_4d(dst, &tm_vt, v_full + st, 0, s.h, (j - jt0) * BN, s.b);
-                        tma_load_4d(dst + KV_ATOM, &tm_vt, v_full + st, 64, s.h, (j - jt0) * BN, s.b);
-                    } else {
-                        tma_load_3d_hint(dst, &tm_v, v_full + st, 0, j * BN, bh, pol);
-                        tma_load_3d_hint(dst + KV_ATOM, &tm_v, v_full + st, 64, j * BN, bh, pol);
-                    }
+                    const bool tr = j >= jt0;
+                    load_kv_tile(sm_v + st * TILE_BYTES, v_full + st, &tm_v, &tm_vt, tr, (tr ? j - jt0 : j) * BN,
+                                 s.h, s.b, bh, pol, mc, rblk);
                 }
                 t += s.hi - s.lo;
             }
@@ -831,7 +845,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             }
             K1_TRACE(3, pc);
             umma_commit_warp(pv_done + pb);
-            umma_commit_warp(v_empty + st);
+            if (mc) umma_commit_warp_mc(v_empty + st, 0x3);
+            else umma_commit_warp(v_empty + st);
             ++vc;
             ++pc;
         };
@@ -870,7 +885,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 }
                 K1_TRACE(2, sc);
                 umma_commit_warp(s_full + sb);
-                umma_commit_warp(k_empty + st);
+                if (mc) umma_commit_warp_mc(k_empty + st, 0x3);
+                else umma_commit_warp(k_empty + st);
                 if (i == ntl - 1) umma_commit_warp(q_empty + qb);
                 ++kc;
                 ++sc;
@@ -1451,7 +1467,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     __syncthreads();
     tc_fence_after();
     // DSMEM merge: no CTA leaves while its peer may still copy out of / into it
-    if (dsm) cluster_sync();
+    // (mc: no CTA leaves while its peer may still multicast into it or
+    // commit to its barriers)
+    if (dsm || mc) cluster_sync();
     if (p.trace && threadIdx.x == 0) {
         unsigned long long gt;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(gt));
