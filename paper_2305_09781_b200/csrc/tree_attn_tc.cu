@@ -381,8 +381,25 @@ template <> struct pk2<__nv_bfloat16> {
     }
 };
 
+// A thread's NCOL output values of one row (scaled, rounded to T). Rows of a
+// warp are a head's stride apart, so every store is its own request: 32-byte
+// (sector) stores halve the request count when the row is 32-byte aligned.
 template <class T, int NCOL>
 __device__ __forceinline__ void store_row(T* dst_row, const float* v, float scale) {
+    if ((reinterpret_cast<uintptr_t>(dst_row) & 31) == 0) {
+#pragma unroll
+        for (int ch = 0; ch < NCOL / 16; ++ch) {
+            uint32_t w8[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                w8[k] = pk2<T>::pack(v[ch * 16 + 2 * k] * scale, v[ch * 16 + 2 * k + 1] * scale);
+            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst_row + ch * 16),
+                         "r"(w8[0]), "r"(w8[1]), "r"(w8[2]), "r"(w8[3]), "r"(w8[4]), "r"(w8[5]), "r"(w8[6]),
+                         "r"(w8[7])
+                         : "memory");
+        }
+        return;
+    }
     uint4* dst = reinterpret_cast<uint4*>(dst_row);
 #pragma unroll
     for (int ch = 0; ch < NCOL / 8; ++ch) {
