@@ -354,6 +354,34 @@ __host__ __device__ constexpr uint32_t idesc_f16(uint32_t fmt, uint32_t M, uint3
            ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+// Packed fp32 pair math (sm_100: FFMA2 / FADD2, one issue slot for two lanes'
+// worth of work) and the three-input max (FMNMX3); same rounding as the
+// scalar fmaf / add / fmaxf.
+__device__ __forceinline__ void ffma2_bcast(float x0, float x1, float b, float c, float& y0, float& y1) {
+    asm("{\n\t.reg .b64 a, bb, cc, d;\n\t"
+        "mov.b64 a, {%2, %3};\n\t"
+        "mov.b64 bb, {%4, %4};\n\t"
+        "mov.b64 cc, {%5, %5};\n\t"
+        "fma.rn.f32x2 d, a, bb, cc;\n\t"
+        "mov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(y0), "=f"(y1)
+        : "f"(x0), "f"(x1), "f"(b), "f"(c));
+}
+__device__ __forceinline__ void fadd2_acc(float& s0, float& s1, float x0, float x1) {
+    asm("{\n\t.reg .b64 a, b;\n\t"
+        "mov.b64 a, {%0, %1};\n\t"
+        "mov.b64 b, {%2, %3};\n\t"
+        "add.rn.f32x2 a, a, b;\n\t"
+        "mov.b64 {%0, %1}, a;\n\t}"
+        : "+f"(s0), "+f"(s1)
+        : "f"(x0), "f"(x1));
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -1025,15 +1025,14 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                                 if (!((vis >> k) & 1u)) sv[wd * 32 + k] = -INFINITY;
                         }
                     }
-                    float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+                    // row max: two chains of three-input maxes (FMNMX3)
+                    float mq0 = -INFINITY, mq1 = -INFINITY;
 #pragma unroll
                     for (int k = 0; k < COLS; k += 4) {
-                        mq[0] = fmaxf(mq[0], sv[k]);
-                        mq[1] = fmaxf(mq[1], sv[k + 1]);
-                        mq[2] = fmaxf(mq[2], sv[k + 2]);
-                        mq[3] = fmaxf(mq[3], sv[k + 3]);
+                        mq0 = fmax3(mq0, sv[k], sv[k + 1]);
+                        mq1 = fmax3(mq1, sv[k + 2], sv[k + 3]);
                     }
-                    float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+                    float mx = fmaxf(mq0, mq1);
                     if constexpr (!DUAL) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
                     const float m_new = fmaxf(m, mx);
                     if (threadIdx.x == 0) K1_TRACE(9, sc);
@@ -1067,13 +1066,17 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     }
                     if (threadIdx.x == 0) K1_TRACE(11, sc);
                     const float base = (m == -INFINITY) ? 0.f : m * c;
+                    // exponentials two columns per issue slot: s*c - base as
+                    // one FFMA2, the running sums as FADD2 (four partial sums)
                     float ls[4] = {0.f, 0.f, 0.f, 0.f};
                     uint32_t pk[COLS / 2];
 #pragma unroll
                     for (int k = 0; k < COLS / 2; ++k) {
-                        const float p0 = ex2(fmaf(sv[2 * k], c, -base));
-                        const float p1 = ex2(fmaf(sv[2 * k + 1], c, -base));
-                        ls[k & 3] += p0 + p1;
+                        float x0, x1;
+                        ffma2_bcast(sv[2 * k], sv[2 * k + 1], c, -base, x0, x1);
+                        const float p0 = ex2(x0);
+                        const float p1 = ex2(x1);
+                        fadd2_acc(ls[2 * (k & 1)], ls[2 * (k & 1) + 1], p0, p1);
                         pk[k] = pk2<T>::pack(p0, p1);
                     }
                     // P (f16/bf16, 2 per column) into TMEM over this tile's S
