@@ -202,6 +202,21 @@ def _verify_case(capi, restatement, logits, tok, par, n, budget=None, eos=-1):
         assert ln[b] == L
         np.testing.assert_array_equal(ver[b, :L], rv[:L])
         np.testing.assert_array_equal(ids[b, :L], rids[:L])
+    # the same walk through the fused walk+commit path (the C2 step's K3):
+    # bit-exact with the above, twice in a row on one workspace
+    B, T = tok.shape
+    kc = torch.zeros((B, 1, T + 1, 8), dtype=torch.float16, device=dev)
+    ws = capi.verify_workspace(B, T, dev)
+    for _ in range(2):
+        am2, ver2, ids2, ln2 = capi.verify_greedy_compact(
+            torch.tensor(logits, device=dev), torch.tensor(tok, device=dev),
+            torch.tensor(par, device=dev), torch.tensor(n, device=dev),
+            torch.zeros(B, dtype=torch.int32, device=dev), kc, kc.clone(),
+            None if budget is None else torch.tensor(budget, device=dev), eos, workspace=ws)
+        np.testing.assert_array_equal(ln2.cpu().numpy(), ln)
+        for b in range(len(n)):
+            np.testing.assert_array_equal(ver2[b, : ln[b]].cpu().numpy(), ver[b, : ln[b]])
+            np.testing.assert_array_equal(ids2[b, : ln[b]].cpu().numpy(), ids[b, : ln[b]])
 
 
 def test_k3_greedy_verify_matches_oracle(capi, restatement):
@@ -258,6 +273,14 @@ def test_k3_tie_and_nan_rules(capi, restatement):
         assert restatement.argmax(logits[b, 0]) == {8: 5, 9: 1030, 10: 2049}[b]
     tok4, par4, _, n4 = pack([(tok, par, dep)] * 11)
     _verify_case(capi, restatement, logits, tok4, par4, n4)
+    # V % 4 == 0 (the vectorised argmax), ragged trees with dead rows (n < T)
+    # and the slice boundaries of V = 4096
+    lg2 = np.full((11, T, 4096), -1.0, np.float32)
+    lg2[:, :, :4096] = logits[:, :, :4096]
+    lg2[4, :, 3999] = -5.0
+    n5 = n4.copy()
+    n5[1] = 1
+    _verify_case(capi, restatement, lg2, tok4, par4, n5)
 
 
 def test_library_fails_loudly_without_device_path(capi):
