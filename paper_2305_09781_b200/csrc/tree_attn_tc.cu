@@ -1642,7 +1642,11 @@ st_status tree_attention_tc_prepare(const st_attn_args* a, const st_peer_out* po
         }
     }
     const int R = (int64_t)(a->H / a->Hkv) * a->T <= 128 ? 1 : 2;   // row blocks per pair
-    const int G = (num_sms() < kMaxPieces + 1 ? num_sms() : kMaxPieces + 1) / R * R;
+    // ST_K1_GRID (diagnostic): fewer CTAs than SMs, e.g. to measure the HBM
+    // rate K1 keeps on a subset of the SMs
+    static const int grid_env = getenv("ST_K1_GRID") ? atoi(getenv("ST_K1_GRID")) : 0;
+    const int sms = grid_env > 0 && grid_env < num_sms() ? grid_env : num_sms();
+    const int G = (sms < kMaxPieces + 1 ? sms : kMaxPieces + 1) / R * R;
     TcParams& prm = L->prm;
     prm.prefix_len = a->prefix_len;
     prm.n_nodes = a->n_nodes;
