@@ -309,6 +309,63 @@ def test_tc_fuzz(capi, restatement):
         check_k1(restatement, bt, out, dtype, lse)
 
 
+def test_tc_fuzz_cluster_paths(capi, restatement):
+    """Random configurations aimed at the 2-CTA cluster paths vs the f64
+    restatement: uniform batches of 50-74 pairs (the split schedule with two
+    pieces per pair — M=64: the piece's bulk copy into the head's first freed
+    K stage; M=128: the symmetric half exchange) and trees past 128 rows (two
+    row blocks per pair, K/V tiles multicast into both CTAs of a slot), with
+    dtype, k_tree and early_kv drawn at random."""
+    rng = np.random.default_rng(4096)
+    dev = "cuda"
+    for case in range(16):
+        two_blocks = case % 3 == 2
+        dtype = torch.float16 if rng.random() < 0.6 else torch.bfloat16
+        if two_blocks:   # 128 < G*T <= 256, ragged everything
+            G = int(rng.choice([1, 2]))
+            T = int(rng.integers(129, 257)) // G
+            Hkv = int(rng.integers(1, 4))
+            B = int(rng.integers(1, 5))
+            uniform = False
+        else:            # 50..74 uniform pairs -> two pieces per pair
+            G = int(rng.choice([1, 1, 2, 4]))
+            T = int(rng.choice([16, 40, 61, 64, 100, 128])) // G
+            np_target = int(rng.integers(50, 75))
+            Hkv = int(rng.choice([d for d in range(1, 9) if np_target // d >= 1]))
+            B = max(1, np_target // Hkv)
+            uniform = True
+        w = int(rng.integers(1, 5))
+        trees = [restatement.merge(width_depth_seqs(rng, int(rng.integers(0, 40)), 40, w,
+                                                    max(1, (T - 1) // w)), 4096) for _ in range(B)]
+        lo = int(rng.choice([0, 127, 128, 700, 1500]))
+        P_range = (lo, lo) if uniform else (lo, lo + int(rng.integers(0, 900)))
+        bt = make_batch(restatement, rng, B, G * Hkv, Hkv, 128, trees=trees, T=T, P_range=P_range,
+                        dtype=dtype)
+        if uniform:
+            bt["n"][:] = bt["n"].max()
+        own, early = bool(rng.random() < 0.5), bool(rng.random() < 0.5)
+        q = torch.tensor(bt["q"], device=dev).to(dtype)
+        kc = torch.tensor(bt["kc"], device=dev).to(dtype)
+        vc = torch.tensor(bt["vc"], device=dev).to(dtype)
+        kt = vt = None
+        if own:   # the tree rows from their own tensors; the cache's copy poisoned
+            kt = torch.zeros(B, T, Hkv, 128, dtype=dtype, device=dev)
+            vt = torch.zeros_like(kt)
+            for b in range(B):
+                P, n = int(bt["P"][b]), int(bt["n"][b])
+                kt[b, :n] = kc[b, :, P:P + n].transpose(0, 1)
+                vt[b, :n] = vc[b, :, P:P + n].transpose(0, 1)
+                kc[b, :, P:P + n] = 7.0
+                vc[b, :, P:P + n] = -9.0
+        out = torch.zeros_like(q)
+        lse = torch.zeros((B, G * Hkv, T), dtype=torch.float32, device=dev)
+        capi.tree_attention(q, kc, vc, torch.tensor(bt["mask"].view(np.int64), device=dev),
+                            torch.tensor(bt["P"], device=dev), torch.tensor(bt["n"], device=dev),
+                            out=out, lse=lse, force_path=2, k_tree=kt, v_tree=vt, early_kv=early)
+        torch.cuda.synchronize()
+        check_k1(restatement, bt, out, dtype, lse)
+
+
 @pytest.mark.parametrize("T,G,dtype", [(1, 1, torch.float16), (2, 1, torch.bfloat16),
                                        (4, 1, torch.float16), (8, 1, torch.float16),
                                        (4, 2, torch.bfloat16), (15, 1, torch.float16)])
