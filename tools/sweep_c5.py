@@ -10,6 +10,7 @@ ceil((T-1)/W), W = 4/8/8/16 for T = 16/32/64/128, trimmed to exactly T nodes.
   python tools/sweep_c5.py [--out profiles/c5_sweep.json]
 """
 import argparse
+import time
 import json
 import os
 import sys
@@ -52,7 +53,39 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--Ls", default="4096,8192,16384,32768")
     ap.add_argument("--Ts", default="16,32,64,128,256")
+    ap.add_argument("--cool", type=float, default=0.0,
+                    help="seconds idle before each point (0: back to back, clocks as they fall)")
     args = ap.parse_args()
+    try:   # SM clock / power sampled DURING each point's timed loop (the sweep runs power-capped)
+        import threading
+
+        import pynvml
+        pynvml.nvmlInit()
+        nvh = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+    except Exception:  # noqa: BLE001
+        nvh = None
+
+    def sampled(fn):
+        """Run fn() while a thread samples the SM clock and board power (median)."""
+        if nvh is None:
+            fn()
+            return None, None
+        got, stop = [], threading.Event()
+
+        def poll():
+            while not stop.is_set():
+                got.append((pynvml.nvmlDeviceGetClockInfo(nvh, pynvml.NVML_CLOCK_SM),
+                            pynvml.nvmlDeviceGetPowerUsage(nvh) / 1e3))
+                time.sleep(0.002)
+        th = threading.Thread(target=poll)
+        th.start()
+        fn()
+        stop.set()
+        th.join()
+        if not got:
+            return None, None
+        got.sort()
+        return got[len(got) // 2][0], round(sorted(g[1] for g in got)[len(got) // 2])
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
@@ -73,23 +106,29 @@ def main():
         for L in Ls:
             P = torch.full((B,), L, dtype=torch.int32, device=dev)
             ws = _capi.tree_attention_workspace(q, kc, vc, mask, P, n)
+            if args.cool > 0:
+                time.sleep(args.cool)
             for _ in range(3):
                 _capi.tree_attention(q, kc, vc, mask, P, n, out=out, workspace=ws)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(args.iters):
-                _capi.tree_attention(q, kc, vc, mask, P, n, out=out, workspace=ws)
-            e1.record()
-            torch.cuda.synchronize()
+
+            def timed():
+                e0.record()
+                for _ in range(args.iters):
+                    _capi.tree_attention(q, kc, vc, mask, P, n, out=out, workspace=ws)
+                e1.record()
+                torch.cuda.synchronize()
+            mhz, pw = sampled(timed)
             us = e0.elapsed_time(e1) * 1e3 / args.iters
             W = (T + 63) // 64
             byts = 2 * (2 * B * L * H * D + B * T * H * D + 2 * B * T * H * D + B * T * H * D) + 8 * B * T * W
             gbs = byts / (us * 1e-6) / 1e9
-            row = dict(L=L, T=T, B=B, us=us, bytes=byts, gbs=gbs, frac=gbs / peak,
+            row = dict(L=L, T=T, B=B, us=us, bytes=byts, gbs=gbs, frac=gbs / peak, sm_mhz=mhz, power_w=pw,
                        path=_capi.tree_attention_path(q, kc, vc, mask, P, n))
             rows.append(row)
-            print(f"L={L:6d} T={T:4d}: {us:8.1f} us  {gbs:7.0f} GB/s  {gbs / peak:5.3f} of measured peak")
+            print(f"L={L:6d} T={T:4d}: {us:8.1f} us  {gbs:7.0f} GB/s  {gbs / peak:5.3f} of measured peak"
+                  f"  (SM {mhz} MHz, {pw} W)")
     json.dump({"config": "C5: B=16, H=32, D=128, fp16", "peak_gbs": peak, "rows": rows},
               open(args.out, "w"), indent=1)
 
