@@ -863,7 +863,12 @@ def run_e2e(args, step, runner, world, dev, barrier, numa_cpus):
                      topo[Bq * Tq: 2 * Bq * Tq].view(Bq, Tq), topo[2 * Bq * Tq:], topo))
     h_outs = [torch.empty(Bq * (Tq + 1) + Bq, dtype=torch.int32).pin_memory() for _ in range(2)]
     d2h = h_outs[0].numel() * 4
-    copy_stream = torch.cuda.Stream()
+    # the H2D of a step is split over two copy streams (two copy engines): a
+    # single stream leaves PCIe headroom on some hosts (ST_E2E_STREAMS=1: one)
+    n_cs = max(1, int(os.environ.get("ST_E2E_STREAMS", "2")))
+    copy_streams = [torch.cuda.Stream() for _ in range(n_cs)]
+    copy_stream = copy_streams[0]
+    ev_copied_cs = [[torch.cuda.Event() for _ in range(n_cs)] for _ in range(2)]
     ev_copied = [torch.cuda.Event() for _ in range(2)]
     ev_free = [torch.cuda.Event() for _ in range(2)]
     ev_out = [torch.cuda.Event() for _ in range(2)]
@@ -879,12 +884,21 @@ def run_e2e(args, step, runner, world, dev, barrier, numa_cpus):
         if merge:   # host buffer i%2 was last read by step i-2's copy
             ev_copied[i % 2].synchronize()
             host_merge(h)
+        # each of Q, K, V split into n_cs row ranges, one per copy stream
+        for j, cs in enumerate(copy_streams):
+            with torch.cuda.stream(cs):
+                cs.wait_event(ev_free[i % 2])
+                for dst, src in ((st[0], h_q), (st[1], h_k), (st[2], h_v)):
+                    d_, s_ = dst.view(-1), src.view(-1)
+                    n_ = d_.numel()
+                    a_, b_ = n_ * j // n_cs, n_ * (j + 1) // n_cs
+                    d_[a_:b_].copy_(s_[a_:b_], non_blocking=True)
+                if j == 0:
+                    st[6].copy_(h, non_blocking=True)
+                ev_copied_cs[i % 2][j].record(cs)
         with torch.cuda.stream(copy_stream):
-            copy_stream.wait_event(ev_free[i % 2])
-            st[0].copy_(h_q, non_blocking=True)
-            st[1].copy_(h_k, non_blocking=True)
-            st[2].copy_(h_v, non_blocking=True)
-            st[6].copy_(h, non_blocking=True)
+            for j in range(1, n_cs):
+                copy_stream.wait_event(ev_copied_cs[i % 2][j])
             ev_copied[i % 2].record(copy_stream)
 
     def issue_compute(i):
@@ -941,6 +955,7 @@ def run_e2e(args, step, runner, world, dev, barrier, numa_cpus):
             "ms_per_step": e2e_ms / args.steps,
             "windows_ms_per_step": [w / args.steps for w in windows],
             "h2d_gbs_copies_alone": h2d_gbs,
+            "h2d_copy_streams": n_cs,
             "h2d_gbs_implied": h2d / (e2e_ms / args.steps / 1e3) / 1e9,
             "host_numa_cpus": numa_cpus,
             "host_tree_merge_us_per_step": merge_us,
