@@ -41,7 +41,8 @@ struct TcParams {
 };
 // A prepared tcgen05 launch: tensor maps encoded once (a plan re-launches it).
 struct TcLaunch {
-    CUtensorMap tq, tk, tv, tkt, tvt;
+    CUtensorMap tq, tk, tv, tkt, tvt;  // one box = both d halves of a tile
+    CUtensorMap tk1, tv1, tkt1, tvt1;  // one d half (multicast two-row-block loads)
     TcParams prm;
     int grid;
     bool coop, m64, mw4, f16;

@@ -411,25 +411,26 @@ __device__ __forceinline__ void store_row(T* dst_row, const float* v, float scal
     }
 }
 
-// One 128-row K or V tile (both 64-column SWIZZLE_128B halves) into `dst`,
-// from the cache ([B*Hkv][Lmax][D], rows from `row`) or, `tree`, from the
-// tree's own rows ([B][T][Hkv][D]). mc (two row blocks per pair on a 2-CTA
-// cluster): this CTA loads only d half `rank` and multicasts it into both
-// CTAs' rings, so each tile is read from L2 once and every ring still gets
-// the whole tile (each CTA's barrier expects the full tile bytes).
+// One 128-row K or V tile into `dst` as two 64-column SWIZZLE_128B atoms
+// [d half][128 rows][64] — ONE TMA: the maps view D = 128 as (64, half) with
+// the half dimension (stride 128 B) outside the rows — from the cache
+// ([B*Hkv][Lmax][D], rows from `row`; map dims (64, Lmax, 2, B*Hkv)) or,
+// `tree`, from the tree's own rows ([B][T][Hkv][D]; (64, Hkv, T, 2, B)).
+// mc (two row blocks per pair on a 2-CTA cluster; maps with a one-half box):
+// this CTA loads only d half `rank` and multicasts it into both CTAs' rings,
+// so each tile is read from L2 once and every ring still gets the whole tile
+// (each CTA's barrier expects the full tile bytes).
 __device__ __forceinline__ void load_kv_tile(uint8_t* dst, uint64_t* bar, const CUtensorMap* cache_map,
                                              const CUtensorMap* tree_map, bool tree, int row, int h, int b,
                                              int bh, uint64_t pol, bool mc, int rank) {
     if (mc) {
         uint8_t* d = dst + rank * KV_ATOM;
-        if (tree) tma_load_4d_mc(d, tree_map, bar, 64 * rank, h, row, b, 0x3);
-        else tma_load_3d_mc(d, cache_map, bar, 64 * rank, row, bh, 0x3, pol);
+        if (tree) tma_load_5d_mc(d, tree_map, bar, 0, h, row, rank, b, 0x3);
+        else tma_load_4d_mc_hint(d, cache_map, bar, 0, row, rank, bh, 0x3, pol);
     } else if (tree) {
-        tma_load_4d(dst, tree_map, bar, 0, h, row, b);
-        tma_load_4d(dst + KV_ATOM, tree_map, bar, 64, h, row, b);
+        tma_load_5d(dst, tree_map, bar, 0, h, row, 0, b);
     } else {
-        tma_load_3d_hint(dst, cache_map, bar, 0, row, bh, pol);
-        tma_load_3d_hint(dst + KV_ATOM, cache_map, bar, 64, row, bh, pol);
+        tma_load_4d_hint(dst, cache_map, bar, 0, row, 0, bh, pol);
     }
 }
 
@@ -557,8 +558,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             if (kside && !p.early_kv) {
                 mbar_arrive_expect_tx(q_full, C::A_BYTES);
                 const int node0 = rblk * (M / p.G);
-                tma_load_4d(sm_q, &tm_q, q_full, 0, s0.h * p.G, node0, s0.b);
-                tma_load_4d(sm_q + C::A_ATOM, &tm_q, q_full, 64, s0.h * p.G, node0, s0.b);
+                tma_load_5d(sm_q, &tm_q, q_full, 0, s0.h * p.G, node0, 0, s0.b);  // both d halves
                 pre_q = true;
                 K1_TRACE(13, 49);
             }
@@ -679,9 +679,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     // box {64 d, G heads, M/G nodes}: smem row = node * G + head;
                     // row block rblk starts at node rblk * M / G
                     const int node0 = rblk * (M / p.G);
-                    tma_load_4d(sm_q + qb * C::A_BYTES, &tm_q, q_full + qb, 0, s.h * p.G, node0, s.b);
-                    tma_load_4d(sm_q + qb * C::A_BYTES + C::A_ATOM, &tm_q, q_full + qb, 64, s.h * p.G,
-                                node0, s.b);
+                    tma_load_5d(sm_q + qb * C::A_BYTES, &tm_q, q_full + qb, 0, s.h * p.G, node0, 0, s.b);
                 }
                 ++qc;
                 const int bh = s.b * p.H + s.h;
@@ -1527,7 +1525,7 @@ bool encode(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* ptr, c
             const uint64_t* strides_bytes, const uint32_t* box) {
     auto fn = get_encode();
     if (!fn) return false;
-    uint32_t es[4] = {1, 1, 1, 1};
+    uint32_t es[5] = {1, 1, 1, 1, 1};  // element strides, up to rank 5
     return fn(m, dt, rank, const_cast<void*>(ptr), dims, strides_bytes, box, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -1596,9 +1594,12 @@ st_status launch_tc(const TcLaunch& L, cudaStream_t stream) {
     const bool clus = allow && L.grid % 2 == 0 && 2 * max_pairs >= L.grid;
     TcParams prm = L.prm;
     prm.cluster2 = clus ? 1 : 0;
+    // two row blocks per pair on clusters: each CTA multicasts one d half
+    // (the kernel's `mc`), so it gets the one-half maps
+    const bool mc = MM == 128 && L.prm.R == 2 && clus;
     ST_CUDA_TRY(launch_pdl_ex(tree_attn_tc_kernel<TT, MM, MW>, dim3(L.grid), dim3(Cfg<MM>::THREADS),
-                              Cfg<MM>::SMEM_BYTES, stream, L.coop, clus ? 2 : 1, L.tq, L.tk, L.tv, L.tkt,
-                              L.tvt, prm));
+                              Cfg<MM>::SMEM_BYTES, stream, L.coop, clus ? 2 : 1, L.tq, mc ? L.tk1 : L.tk,
+                              mc ? L.tv1 : L.tv, mc ? L.tkt1 : L.tkt, mc ? L.tvt1 : L.tvt, prm));
     return ST_OK;
 }
 
@@ -1608,35 +1609,45 @@ st_status tree_attention_tc_prepare(const st_attn_args* a, const st_peer_out* po
     const CUtensorMapDataType dt =
         a->dtype == ST_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     {
-        const uint64_t dims[4] = {(uint64_t)HD, (uint64_t)a->H, (uint64_t)a->T, (uint64_t)a->B};
-        const uint64_t strides[3] = {HD * 2ull, (uint64_t)a->H * HD * 2, (uint64_t)a->T * a->H * HD * 2};
+        // D = 128 as (64, half): dims (64, H, T, 2, B), the half (stride 128 B)
+        // outside the nodes, so one box lands as the two K-major atoms
+        const uint64_t dims[5] = {64, (uint64_t)a->H, (uint64_t)a->T, 2, (uint64_t)a->B};
+        const uint64_t strides[4] = {HD * 2ull, (uint64_t)a->H * HD * 2, 128, (uint64_t)a->T * a->H * HD * 2};
         const int G = a->H / a->Hkv;
         const uint32_t M = (int64_t)G * a->T <= 64 ? 64 : 128;
-        const uint32_t box[4] = {64, (uint32_t)G, M / G, 1};
-        if (!encode(&L->tq, dt, 4, a->q, dims, strides, box)) {
+        const uint32_t box[5] = {64, (uint32_t)G, M / G, 2, 1};
+        if (!encode(&L->tq, dt, 5, a->q, dims, strides, box)) {
             set_error("st_tree_attention: cuTensorMapEncodeTiled(q) failed");
             return ST_ERR_CUDA;
         }
     }
     {
-        const uint64_t dims[3] = {(uint64_t)HD, (uint64_t)a->Lmax, (uint64_t)a->B * a->Hkv};
-        const uint64_t strides[2] = {HD * 2ull, (uint64_t)a->Lmax * HD * 2};
-        const uint32_t box[3] = {64, BN, 1};
-        if (!encode(&L->tk, dt, 3, a->k_cache, dims, strides, box) ||
-            !encode(&L->tv, dt, 3, a->v_cache, dims, strides, box)) {
+        // (64, Lmax, 2, B*Hkv): one box = both d halves of a 128-row tile;
+        // the one-half maps feed the multicast two-row-block loads
+        const uint64_t dims[4] = {64, (uint64_t)a->Lmax, 2, (uint64_t)a->B * a->Hkv};
+        const uint64_t strides[3] = {HD * 2ull, 128, (uint64_t)a->Lmax * HD * 2};
+        const uint32_t box[4] = {64, BN, 2, 1}, box1[4] = {64, BN, 1, 1};
+        if (!encode(&L->tk, dt, 4, a->k_cache, dims, strides, box) ||
+            !encode(&L->tv, dt, 4, a->v_cache, dims, strides, box) ||
+            !encode(&L->tk1, dt, 4, a->k_cache, dims, strides, box1) ||
+            !encode(&L->tv1, dt, 4, a->v_cache, dims, strides, box1)) {
             set_error("st_tree_attention: cuTensorMapEncodeTiled(kv) failed");
             return ST_ERR_CUDA;
         }
     }
     L->tkt = L->tk;  // k_tree mode: the tree's rows, [B][T][Hkv][D], 128-node boxes
     L->tvt = L->tv;
+    L->tkt1 = L->tk1;
+    L->tvt1 = L->tv1;
     if (a->k_tree) {
-        const uint64_t dims[4] = {(uint64_t)HD, (uint64_t)a->Hkv, (uint64_t)a->T, (uint64_t)a->B};
-        const uint64_t strides[3] = {HD * 2ull, (uint64_t)a->Hkv * HD * 2,
+        const uint64_t dims[5] = {64, (uint64_t)a->Hkv, (uint64_t)a->T, 2, (uint64_t)a->B};
+        const uint64_t strides[4] = {HD * 2ull, (uint64_t)a->Hkv * HD * 2, 128,
                                      (uint64_t)a->T * a->Hkv * HD * 2};
-        const uint32_t box[4] = {64, 1, BN, 1};
-        if (!encode(&L->tkt, dt, 4, a->k_tree, dims, strides, box) ||
-            !encode(&L->tvt, dt, 4, a->v_tree, dims, strides, box)) {
+        const uint32_t box[5] = {64, 1, BN, 2, 1}, box1[5] = {64, 1, BN, 1, 1};
+        if (!encode(&L->tkt, dt, 5, a->k_tree, dims, strides, box) ||
+            !encode(&L->tvt, dt, 5, a->v_tree, dims, strides, box) ||
+            !encode(&L->tkt1, dt, 5, a->k_tree, dims, strides, box1) ||
+            !encode(&L->tvt1, dt, 5, a->v_tree, dims, strides, box1)) {
             set_error("st_tree_attention: cuTensorMapEncodeTiled(k_tree/v_tree) failed");
             return ST_ERR_CUDA;
         }
