@@ -50,6 +50,7 @@ struct GemmParams {
     int M, N, K, Z;
     int nm, nn, nk;        // tile counts
     int vec;               // 16-byte stores allowed (aligned C rows)
+    int wmerge;            // N % 64 == 0: the W map views N as (64, N/64), one box per K block
 };
 
 template <class T> struct pk;
@@ -183,10 +184,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CU
                     mbar_arrive_expect_tx(full + s, STAGE_BYTES);
                     uint8_t* a = smem + s * STAGE_BYTES;
                     tma_load_2d(a, &tm_a, full + s, kb * BK, mb * BM);
+                    if (p.wmerge) {  // the four 64-column W atoms in one box
+                        tma_load_4d(a + A_BYTES, &tm_b, full + s, 0, kb * BK, nb * (BN / 64), z);
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        tma_load_3d(a + A_BYTES + j * B_ATOM, &tm_b, full + s, nb * BN + j * 64,
-                                    kb * BK, z);
+                        for (int j = 0; j < 4; ++j)
+                            tma_load_3d(a + A_BYTES + j * B_ATOM, &tm_b, full + s, nb * BN + j * 64,
+                                        kb * BK, z);
+                    }
                 }
             }
         }
@@ -280,6 +285,14 @@ __device__ __forceinline__ void tma2_load_3d(void* dst, const CUtensorMap* m, ui
         "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
+__device__ __forceinline__ void tma2_load_4d(void* dst, const CUtensorMap* m, uint32_t bar, int c0, int c1,
+                                             int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
 __device__ __forceinline__ void umma2_warp(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
                                            uint32_t idesc, uint32_t accumulate) {
     asm volatile(
@@ -358,10 +371,14 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
                     const uint32_t fb = leader_addr(full + s);
                     uint8_t* a = smem + s * P_STAGE;
                     tma2_load_2d(a, &tm_a, fb, kb * BK, mb * 256 + (int)rank * 128);
+                    if (p.wmerge) {  // this CTA's two 64-column W atoms in one box
+                        tma2_load_4d(a + PA_BYTES, &tm_b, fb, 0, kb * BK, (nb * BN + (int)rank * 128) / 64, z);
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < 2; ++j)
-                        tma2_load_3d(a + PA_BYTES + j * B_ATOM, &tm_b, fb,
-                                     nb * BN + (int)rank * 128 + j * 64, kb * BK, z);
+                        for (int j = 0; j < 2; ++j)
+                            tma2_load_3d(a + PA_BYTES + j * B_ATOM, &tm_b, fb,
+                                         nb * BN + (int)rank * 128 + j * 64, kb * BK, z);
+                    }
                 }
             }
         }
@@ -540,7 +557,24 @@ st_status gemm_sm100(const GemmArgs& g, cudaStream_t s) {
             return ST_ERR_CUDA;
         }
     }
-    {
+    static const bool pair_env = !(getenv("ST_GEMM_PAIR") && atoi(getenv("ST_GEMM_PAIR")) == 0);
+    const bool pair = pair_env && g.M >= 256;
+    // N % 64 == 0: W viewed as (64, K, N/64, Z) — the 64-column block index a
+    // dimension of stride 128 B outside K — so a CTA's 2 (pair) or 4 W atoms
+    // of a K block are one box (one TMA issue instead of 2 / 4)
+    const bool wmerge = g.N % 64 == 0;
+    if (wmerge) {
+        const uint64_t dims[4] = {64, (uint64_t)g.K, (uint64_t)g.N / 64, (uint64_t)g.Z};
+        const uint64_t strides[3] = {(uint64_t)g.ldw * 2, 128, (uint64_t)g.ldw * g.K * 2};
+        const uint32_t box[4] = {64, BK, pair ? 2u : 4u, 1};
+        const uint32_t es4[4] = {1, 1, 1, 1};
+        if (enc(&tb, dt, 4, const_cast<void*>(g.W), dims, strides, box, es4,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+            set_error("gemm: cuTensorMapEncodeTiled(W, merged) failed");
+            return ST_ERR_CUDA;
+        }
+    } else {
         const uint64_t dims[3] = {(uint64_t)g.N, (uint64_t)g.K, (uint64_t)g.Z};
         const uint64_t strides[2] = {(uint64_t)g.ldw * 2, (uint64_t)g.ldw * g.K * 2};
         const uint32_t box[3] = {64, BK, 1};
@@ -565,8 +599,7 @@ st_status gemm_sm100(const GemmArgs& g, cudaStream_t s) {
     const size_t cbytes = g.epi == kGemmStoreF32 ? 4 : 2;
     p.vec = (reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && ((size_t)g.ldc * cbytes) % 16 == 0 &&
             ((size_t)g.c_stride_z * cbytes) % 16 == 0;
-    static const bool pair_env = !(getenv("ST_GEMM_PAIR") && atoi(getenv("ST_GEMM_PAIR")) == 0);
-    const bool pair = pair_env && g.M >= 256;
+    p.wmerge = wmerge ? 1 : 0;
 #define ST_GEMM_EPI(TT)                                                              \
     switch (g.epi) {                                                                 \
         case kGemmStore: return pair ? launch_pair<TT, kGemmStore>(ta, tb, p, s)     \
