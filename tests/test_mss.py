@@ -101,3 +101,46 @@ def test_k4_bitexact_vs_oracle(restatement, V, tau):
         accepted += len(rv) - 1
     if V > 1:
         assert accepted > 0  # the planted agreement must produce some acceptances
+
+
+@pytest.mark.gpu
+def test_k4_c3_bench_shape(restatement):
+    """K4 exactly as bench.py --config c3 runs it — 32 requests x 64-node trees
+    built like the bench's (bench.c2_trees), V = 32000, tau = 1.0, drafts
+    softmax(3 z) — bit-exact against the oracle for every request, with
+    planted agreement so acceptance chains (and rejections with residual
+    resampling) both occur."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import bench
+    from paper_2305_09781_b200 import _capi
+    from paper_2305_09781_b200.tree import TokenTree, TreeBatch
+    V, Bq, T, tau = 32000, 32, 64, 1.0
+    rng = np.random.default_rng(3000)
+    trees = bench.c2_trees(lambda s_: TokenTree.merge_sequences(s_, 1 << 20), 3000, V, n_req=Bq)
+    tb = TreeBatch([t for t, _ in trees], T)
+    tok, par, n = np.array(tb.tokens), np.array(tb.parents), np.array(tb.n_nodes)
+    logits = (rng.standard_normal((Bq, T, V)) * 3.0).astype(np.float32)
+    q = softmax(rng.standard_normal((Bq, T, V)).astype(np.float32) * 3.0)
+    for b in range(Bq):
+        for v in range(1, n[b]):
+            q[b, v] *= 0.3
+            q[b, v, tok[b, v]] += 0.7
+            if rng.random() < 0.5:
+                logits[b, par[b, v], tok[b, v]] += 18.0
+    U = rng.uniform(0, 1, (Bq, T + 1)).astype(np.float32)
+    dev = "cuda"
+    ver, ids, ln = _capi.verify_mss(torch.tensor(logits, device=dev), torch.tensor(q, device=dev),
+                                    torch.tensor(tok, device=dev), torch.tensor(par, device=dev),
+                                    torch.tensor(n, device=dev), tau, torch.tensor(U, device=dev))
+    ver, ids, ln = ver.cpu().numpy(), ids.cpu().numpy(), ln.cpu().numpy()
+    longest = 0
+    for b in range(Bq):
+        k = n[b]
+        rv, rids = restatement.mss_verify(logits[b, :k], q[b, :k], tok[b, :k], par[b, :k], tau, U[b])
+        assert ln[b] == len(rv)
+        np.testing.assert_array_equal(ver[b, : ln[b]], rv)
+        np.testing.assert_array_equal(ids[b, : ln[b]], rids)
+        longest = max(longest, len(rv))
+    assert longest > 2
