@@ -14,6 +14,10 @@
   checked on one (request, head) pair per request against the C restatement
   (each pair is a B=1, H=1 oracle problem; pairs run on a thread pool — the
   oracle is C behind ctypes, which releases the GIL).
+* C4 (bench.py --config c4: 65B shape, B=8, merged 3-SSM trees of 61 nodes,
+  KV 2048) on one rank of 1 or of 8 head shards — the latter is the per-rank
+  slice on the two-piece DSMEM merge: every pair's K1 output, the head-output
+  layout and the greedy verify at V=32000.
 """
 from concurrent.futures import ThreadPoolExecutor
 
@@ -245,3 +249,58 @@ def test_decode_loop_prefix_advances_early_kv(capi, restatement):
         Pe = int(Ps[steps][b])
         assert torch.equal(st.kc[b, :, :Pe], kc[b, :, :Pe])
         assert torch.equal(st.vc[b, :, :Pe], vc[b, :, :Pe])
+
+
+@pytest.mark.parametrize("world", [1, 8])
+def test_c4_bench_step_full_shape(capi, restatement, world):
+    """C4 as bench.py --config c4 builds it (65B shape: 64 heads, B=8, merged
+    3-SSM trees <1,1,3,1,1,1,1,1> of 61 nodes, KV 2048, tree rows in their own
+    tensors) for rank 0 of `world` head shards: world=1 runs all 64 heads,
+    world=8 rank 0's 8 — the per-rank slice tools/c4_slice.py times, whose 64
+    pairs take the two-piece DSMEM merge. K1 on every (request, head) pair
+    within 2e-3 of the f64 restatement; the head-output layout of the
+    (1-rank) gather; greedy verify at V=32000 bit-exact."""
+    import bench
+    from paper_2305_09781_b200.dist import gather_head_outputs, head_shard
+    from paper_2305_09781_b200.tree import TokenTree, TreeBatch
+    dev = torch.device("cuda", 0)
+    HT, Bq, D, L, V = 64, 8, 128, 2048, 32000
+    h0, h1 = head_shard(HT, world, 0)
+    Hl = h1 - h0
+    trees = bench.c4_trees(lambda s: TokenTree.merge_sequences(s, 1 << 20), 65, Bq)
+    tb = TreeBatch([t for t, _ in trees])
+    T = tb.T
+    assert T == 61
+    g = torch.Generator(device=dev).manual_seed(99)
+    q = (torch.rand(Bq, T, Hl, D, device=dev, generator=g) * 2 - 1).half()
+    kc = (torch.rand(Bq, Hl, L + T, D, device=dev, generator=g) * 2 - 1).half()
+    vc = (torch.rand(Bq, Hl, L + T, D, device=dev, generator=g) * 2 - 1).half()
+    kt = (torch.rand(Bq, T, Hl, D, device=dev, generator=g) * 2 - 1).half()
+    vt = (torch.rand(Bq, T, Hl, D, device=dev, generator=g) * 2 - 1).half()
+    logits = torch.randn(Bq, T, V, device=dev, generator=torch.Generator(device=dev).manual_seed(5))
+    par = torch.tensor(tb.parents, device=dev)
+    tok = torch.tensor(tb.tokens, device=dev)
+    nn = torch.tensor(tb.n_nodes, device=dev)
+    P = torch.full((Bq,), L, dtype=torch.int32, device=dev)
+    mask = capi.build_masks(par, nn)
+    out = torch.zeros_like(q)
+    ws = capi.tree_attention_workspace(q, kc, vc, mask, P, nn)
+    capi.tree_attention(q, kc, vc, mask, P, nn, out=out, workspace=ws, k_tree=kt, v_tree=vt)
+    full = gather_head_outputs(out, 1)
+    am, ver, ids, ln = capi.verify_greedy(logits, tok, par, nn)
+    torch.cuda.synchronize()
+    n = np.array(tb.n_nodes)
+    m = masks(restatement, np.array(tb.parents), n, (T + 63) // 64)
+    pairs = [(b, h) for b in range(Bq) for h in range(Hl)]
+    ref = oracle_pairs(restatement, q, kc, vc, m, P.cpu().numpy(), n, pairs, kt, vt)
+    err = worst_err(out, ref)
+    assert err <= TOL16, f"K1 max-abs {err:.3e} over {len(pairs)} pairs"
+    assert torch.equal(full, out), "1-rank gather layout"
+    lg = logits.cpu().numpy()
+    for b in range(Bq):
+        k = int(n[b])
+        _, rv, rids = restatement.greedy_verify(lg[b, :k], np.array(tb.tokens)[b, :k],
+                                                np.array(tb.parents)[b, :k])
+        assert int(ln[b]) == len(rv)
+        assert ver[b, : len(rv)].cpu().tolist() == list(rv)
+        assert ids[b, : len(rv)].cpu().tolist() == list(rids)
