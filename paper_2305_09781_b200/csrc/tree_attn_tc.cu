@@ -14,7 +14,10 @@
 //     stream-K (equal tile counts per CTA). A pair cut by range boundaries
 //     leaves pieces (O, m, l) that the pair's head owner merges in-kernel, in
 //     CTA order (deterministic, no atomics in any reduction), after staging
-//     them into its drained K ring with TMA.
+//     them into its drained K ring with TMA. On 2-CTA clusters a pair of two
+//     pieces (the split schedule) merges over DSMEM instead: the piece
+//     bulk-copies its (O, m, l) into the head's first freed K stage while the
+//     head runs its last tile (M=128: the two CTAs exchange d halves).
 //   * GQA: the G query heads of a KV head share one M-row Q tile (row r =
 //     node r/G of head r%G). k_tree mode: the tree rows come from their own
 //     [B][T][Hkv][D] tensors as one extra tile after the prefix tiles.
@@ -22,7 +25,7 @@
 //     TMA producer for Q and K, a TMA producer for V and the MMA issuer (the
 //     whole warp runs its loop; one elected lane issues inside the asm).
 //   * TMA (SWIZZLE_128B) streams K and V tiles [128 rows x 128 d] through
-//     3-stage rings; Q (rows >= T zero-filled by TMA) double-buffered for M=64
+//     3-stage rings, one box per tile (the maps view d as (64, half)); Q (rows >= T zero-filled by TMA) double-buffered for M=64
 //     so the next pair's Q is in smem before its first S.
 //   * S = Q K^T (SS MMA) and O += P V (TS MMA: P read from TMEM) on tcgen05
 //     (kind::f16, fp32 accumulate). M=64 (T <= 64): every product is split into
