@@ -25,8 +25,9 @@
 //     TMA producer for Q and K, a TMA producer for V and the MMA issuer (the
 //     whole warp runs its loop; one elected lane issues inside the asm).
 //   * TMA (SWIZZLE_128B) streams K and V tiles [128 rows x 128 d] through
-//     3-stage rings, one box per tile (the maps view d as (64, half)); Q (rows >= T zero-filled by TMA) double-buffered for M=64
-//     so the next pair's Q is in smem before its first S.
+//     3-stage rings, one box per tile (the maps view d as (64, half)); Q
+//     (rows >= T zero-filled by TMA) double-buffered for M=64 so the next
+//     pair's Q is in smem before its first S.
 //   * S = Q K^T (SS MMA) and O += P V (TS MMA: P read from TMEM) on tcgen05
 //     (kind::f16, fp32 accumulate). M=64 (T <= 64): every product is split into
 //     two N=64 MMAs whose accumulators land in TMEM lanes 0-15 and 16-31 of
