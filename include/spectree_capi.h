@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define ST_ABI_VERSION 4
+#define ST_ABI_VERSION 5
 
 typedef int st_status;
 
@@ -111,6 +111,13 @@ typedef struct {
      * and st_tree_prepare follow this rule, which makes "previous step's
      * commit -> masks -> early_kv K1" safe while P advances every step. */
     int early_kv;
+    /* Optional (0 = off; ABI 5): q, o and lse hold only q_rows rows per
+     * request — tree nodes [q_node0, q_node0 + q_rows), e.g. one level of a
+     * draft tree grown level by level — while the mask rows and the tree rows
+     * (k_tree, required) stay indexed by node id over T and n_nodes counts
+     * every node so far. q/o row stride q_rows, lse [B][H][q_rows]. */
+    int q_rows;
+    int q_node0;
 } st_attn_args;
 
 size_t st_tree_attention_workspace_size(const st_attn_args* a);

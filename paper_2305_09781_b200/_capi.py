@@ -44,7 +44,7 @@ class AttnArgs(C.Structure):
                 ("o", C.c_void_p), ("lse", C.c_void_p), ("scale", C.c_double),
                 ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t),
                 ("force_path", C.c_int), ("k_tree", C.c_void_p), ("v_tree", C.c_void_p),
-                ("early_kv", C.c_int)]
+                ("early_kv", C.c_int), ("q_rows", C.c_int), ("q_node0", C.c_int)]
 
 
 _lib = None
@@ -143,8 +143,12 @@ def _stream(stream=None):
 
 # ------------------------------------------------------------------ K1 ----
 def attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, lse=None, scale=None,
-              workspace=None, force_path=0, k_tree=None, v_tree=None, early_kv=False):
+              workspace=None, force_path=0, k_tree=None, v_tree=None, early_kv=False,
+              q_node0=None):
     B, T, H, D = q.shape
+    q_rows = 0
+    if q_node0 is not None:   # q holds nodes [q_node0, q_node0 + q.shape[1]) of T = mask rows
+        q_rows, T = q.shape[1], mask.shape[1]
     Hkv, Lmax = k_cache.shape[1], k_cache.shape[2]
     a = AttnArgs()
     a.dtype = DTYPES[q.dtype]
@@ -160,6 +164,8 @@ def attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, lse=None, sca
     a.k_tree = k_tree.data_ptr() if k_tree is not None else None
     a.v_tree = v_tree.data_ptr() if v_tree is not None else None
     a.early_kv = 1 if early_kv else 0
+    a.q_rows = q_rows
+    a.q_node0 = int(q_node0) if q_node0 is not None else 0
     return a
 
 
@@ -178,18 +184,19 @@ def tree_attention_path(q, k_cache, v_cache, mask, prefix_len, n_nodes, force_pa
 
 def tree_attention(q, k_cache, v_cache, mask, prefix_len, n_nodes, out=None, lse=None,
                    scale=None, workspace=None, force_path=0, stream=None, k_tree=None,
-                   v_tree=None, early_kv=False):
+                   v_tree=None, early_kv=False, q_node0=None):
     """K1 through st_tree_attention. Shapes: q [B,T,H,D]; caches [B,Hkv,Lmax,D];
     mask [B,T,W] int64 (uint64 bits); prefix_len/n_nodes [B] int32 (device);
     k_tree/v_tree (optional) [B,T,Hkv,D]: the tree rows, read instead of cache
-    rows [P, P+n)."""
+    rows [P, P+n). q_node0 (needs k_tree): q / out / lse hold only the nodes
+    [q_node0, q_node0 + q.shape[1]) of the T = mask.shape[1] tree nodes."""
     if out is None:
         out = torch.empty_like(q)
     if workspace is None:
         workspace = tree_attention_workspace(q, k_cache, v_cache, mask, prefix_len, n_nodes,
                                              force_path)
     a = attn_args(q, k_cache, v_cache, mask, prefix_len, n_nodes, out, lse, scale, workspace,
-                  force_path, k_tree, v_tree, early_kv)
+                  force_path, k_tree, v_tree, early_kv, q_node0)
     check(lib().st_tree_attention(C.byref(a), _stream(stream)))
     return out
 

@@ -51,7 +51,46 @@ struct GemmParams {
     int nm, nn, nk;        // tile counts
     int vec;               // 16-byte stores allowed (aligned C rows)
     int wmerge;            // N % 64 == 0: the W map views N as (64, N/64), one box per K block
+    // split-K (ks > 1, GEMMs with fewer output tiles than CTAs): work unit u is
+    // split u % ks of tile u / ks over K blocks [split * nkb, +nkb); each unit
+    // stores its fp32 partial tile to part[split][z][M][N], and a second kernel
+    // sums the ks partials in split order and applies the epilogue
+    int ks, nkb;
+    float* part;
 };
+
+// The work unit's tile coordinates and K-block range.
+struct Unit {
+    int mb, nb, z, split, kb0, kb1;
+};
+__device__ __forceinline__ Unit unit_of(const GemmParams& p, int u, int nm) {
+    Unit w;
+    const int t = u / p.ks;
+    w.split = u - t * p.ks;
+    w.mb = t % nm;
+    const int rest = t / nm;
+    w.nb = rest % p.nn;
+    w.z = rest / p.nn;
+    w.kb0 = w.split * p.nkb;
+    w.kb1 = min(p.nk, w.kb0 + p.nkb);
+    return w;
+}
+
+// Split-K: this unit's fp32 partial of one row's 32 columns [col0, col0+32).
+__device__ __forceinline__ void partial_chunk(const GemmParams& p, const Unit& w, int row, int col0,
+                                              const float (&v)[32]) {
+    if (row >= p.M) return;
+    float* c = p.part + (((long long)w.split * p.Z + w.z) * p.M + row) * p.N + col0;
+    if (col0 + 32 <= p.N && (p.N & 3) == 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            reinterpret_cast<float4*>(c)[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+            if (col0 + k < p.N) c[k] = v[k];
+    }
+}
 
 template <class T> struct pk;
 template <> struct pk<__half> {
@@ -136,6 +175,46 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, int z, int r
     }
 }
 
+// Split-K reduction: C = epi(sum over splits of part[split], in split order —
+// deterministic), 32 columns of one row per thread.
+template <class T, int EPI>
+__global__ void __launch_bounds__(256)
+splitk_reduce_kernel(const GemmParams p) {
+    pdl_wait();
+    pdl_trigger();
+    const int cpr = (p.N + 31) / 32;  // 32-column chunks per row
+    const long long chunks = (long long)p.Z * p.M * cpr;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < chunks;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(i % cpr);
+        const long long zr = i / cpr;
+        const int row = (int)(zr % p.M), z = (int)(zr / p.M);
+        const int col0 = c * 32;
+        float v[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] = 0.f;
+        const bool vec = col0 + 32 <= p.N && (p.N & 3) == 0;
+        for (int sp = 0; sp < p.ks; ++sp) {
+            const float* src = p.part + (((long long)sp * p.Z + z) * p.M + row) * p.N + col0;
+            if (vec) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const float4 x = __ldcs(reinterpret_cast<const float4*>(src) + k);
+                    v[4 * k] += x.x;
+                    v[4 * k + 1] += x.y;
+                    v[4 * k + 2] += x.z;
+                    v[4 * k + 3] += x.w;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 32; ++k)
+                    if (col0 + k < p.N) v[k] += src[k];
+            }
+        }
+        epilogue_chunk<T, EPI>(p, z, row, col0, v);
+    }
+}
+
 template <class T, int EPI>
 __global__ void __launch_bounds__(THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
@@ -170,15 +249,16 @@ gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CU
     const uint32_t tmem = *tmem_slot;
     pdl_wait();       // A (and C for add-to) come from the previous kernel
     pdl_trigger();
-    const int tiles = p.nm * p.nn * p.Z;
+    const int units = p.nm * p.nn * p.Z * p.ks;
 
     if (warp == 0) {
         // ============================ TMA producer ============================
         if (lane == 0) {
             uint32_t kc = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-                const int mb = t % p.nm, rest = t / p.nm, nb = rest % p.nn, z = rest / p.nn;
-                for (int kb = 0; kb < p.nk; ++kb, ++kc) {
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                const Unit w = unit_of(p, u, p.nm);
+                const int mb = w.mb, nb = w.nb, z = w.z;
+                for (int kb = w.kb0; kb < w.kb1; ++kb, ++kc) {
                     const uint32_t s = kc % STAGES;
                     mbar_wait(empty + s, ((kc / STAGES) & 1) ^ 1);
                     mbar_arrive_expect_tx(full + s, STAGE_BYTES);
@@ -200,12 +280,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CU
         constexpr uint32_t fmt = std::is_same<T, __half>::value ? 0u : 1u;
         constexpr uint32_t idesc = idesc_f16(fmt, BM, BN, 0, 1);  // A K-major, W MN-major
         uint32_t kc = 0, ac = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++ac) {
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++ac) {
+            const Unit w = unit_of(p, u, p.nm);
             const uint32_t acc = ac & 1;
             mbar_wait(acc_empty + acc, ((ac >> 1) & 1) ^ 1);
             tc_fence_after();
             const uint32_t d = tmem + acc * BN;
-            for (int kb = 0; kb < p.nk; ++kb, ++kc) {
+            for (int kb = w.kb0; kb < w.kb1; ++kb, ++kc) {
                 const uint32_t s = kc % STAGES;
                 mbar_wait(full + s, (kc / STAGES) & 1);
                 tc_fence_after();
@@ -215,7 +296,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CU
 #pragma unroll
                 for (int kk = 0; kk < BK / 16; ++kk)
                     umma_f16_ss_warp(d, ad + ((kk * 32) >> 4), bd + ((kk * 2048) >> 4), idesc,
-                                     (kb | kk) ? 1u : 0u);
+                                     (kb > w.kb0 || kk) ? 1u : 0u);
                 umma_commit_warp(empty + s);
             }
             umma_commit_warp(acc_full + acc);
@@ -225,8 +306,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CU
         const int q = warp & 3;  // TMEM lane quadrant this warp may access
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
         uint32_t ac = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++ac) {
-            const int mb = t % p.nm, rest = t / p.nm, nb = rest % p.nn, z = rest / p.nn;
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++ac) {
+            const Unit w = unit_of(p, u, p.nm);
+            const int mb = w.mb, nb = w.nb, z = w.z;
             const uint32_t acc = ac & 1;
             mbar_wait(acc_full + acc, (ac >> 1) & 1);
             tc_fence_after();
@@ -241,7 +323,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CU
                 float v[32];
 #pragma unroll
                 for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(raw[k]);
-                epilogue_chunk<T, EPI>(p, z, row, col0, v);
+                if (p.ks > 1) partial_chunk(p, w, row, col0, v);
+                else epilogue_chunk<T, EPI>(p, z, row, col0, v);
             }
             tc_fence_before();
             mbar_arrive(acc_empty + acc);
@@ -354,16 +437,17 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
     pdl_wait();
     pdl_trigger();
     const int nm2 = (p.M + 255) / 256;
-    const int tiles = nm2 * p.nn * p.Z;
+    const int units = nm2 * p.nn * p.Z * p.ks;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
     if (warp == 0) {
         // ========================= TMA producer (both CTAs) ======================
         if (lane == 0) {
             uint32_t kc = 0;
-            for (int t = cid; t < tiles; t += ncl) {
-                const int mb = t % nm2, rest = t / nm2, nb = rest % p.nn, z = rest / p.nn;
-                for (int kb = 0; kb < p.nk; ++kb, ++kc) {
+            for (int u = cid; u < units; u += ncl) {
+                const Unit w = unit_of(p, u, nm2);
+                const int mb = w.mb, nb = w.nb, z = w.z;
+                for (int kb = w.kb0; kb < w.kb1; ++kb, ++kc) {
                     const uint32_t s = kc % P_STAGES;
                     mbar_wait(empty + s, ((kc / P_STAGES) & 1) ^ 1);
                     // the leader's full barrier counts both CTAs' bytes
@@ -388,12 +472,13 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
             constexpr uint32_t fmt = std::is_same<T, __half>::value ? 0u : 1u;
             constexpr uint32_t idesc = idesc_f16(fmt, 256, BN, 0, 1);
             uint32_t kc = 0, ac = 0;
-            for (int t = cid; t < tiles; t += ncl, ++ac) {
+            for (int u = cid; u < units; u += ncl, ++ac) {
+                const Unit w = unit_of(p, u, nm2);
                 const uint32_t acc = ac & 1;
                 mbar_wait(acc_empty + acc, ((ac >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + acc * BN;
-                for (int kb = 0; kb < p.nk; ++kb, ++kc) {
+                for (int kb = w.kb0; kb < w.kb1; ++kb, ++kc) {
                     const uint32_t s = kc % P_STAGES;
                     mbar_wait(full + s, (kc / P_STAGES) & 1);
                     tc_fence_after();
@@ -403,7 +488,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
 #pragma unroll
                     for (int kk = 0; kk < BK / 16; ++kk)
                         umma2_warp(d, ad + ((kk * 32) >> 4), bd + ((kk * 2048) >> 4), idesc,
-                                   (kb | kk) ? 1u : 0u);
+                                   (kb > w.kb0 || kk) ? 1u : 0u);
                     umma2_commit_both(empty + s);
                 }
                 umma2_commit_both(acc_full + acc);
@@ -415,8 +500,9 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
         const uint32_t ae0 = leader_addr(acc_empty), ae1 = leader_addr(acc_empty + 1);
         uint32_t ac = 0;
-        for (int t = cid; t < tiles; t += ncl, ++ac) {
-            const int mb = t % nm2, rest = t / nm2, nb = rest % p.nn, z = rest / p.nn;
+        for (int u = cid; u < units; u += ncl, ++ac) {
+            const Unit w = unit_of(p, u, nm2);
+            const int mb = w.mb, nb = w.nb, z = w.z;
             const uint32_t acc = ac & 1;
             mbar_wait(acc_full + acc, (ac >> 1) & 1);
             tc_fence_after();
@@ -431,7 +517,8 @@ gemm2_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ C
                 float v[32];
 #pragma unroll
                 for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(raw[k]);
-                epilogue_chunk<T, EPI>(p, z, row, col0, v);
+                if (p.ks > 1) partial_chunk(p, w, row, col0, v);
+                else epilogue_chunk<T, EPI>(p, z, row, col0, v);
             }
             tc_fence_before();
             __syncwarp();
@@ -478,10 +565,20 @@ st_status launch(const GemmArgs& g, const CUtensorMap& ta, const CUtensorMap& tb
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
         attr = true;
     }
-    const int tiles = p.nm * p.nn * p.Z;
-    const int grid = tiles < sm_count() ? tiles : sm_count();
+    const int units = p.nm * p.nn * p.Z * p.ks;
+    const int grid = units < sm_count() ? units : sm_count();
     ST_CUDA_TRY(launch_pdl(gemm_kernel<T, EPI>, dim3(grid), dim3(THREADS), SMEM_BYTES, s, ta, tb, p));
     (void)g;
+    return ST_OK;
+}
+
+// Split-K: the reduction + epilogue pass after the partial GEMM (PDL-chained).
+template <class T, int EPI>
+st_status launch_reduce(const GemmParams& p, cudaStream_t s) {
+    const long long chunks = (long long)p.Z * p.M * ((p.N + 31) / 32);
+    const long long blocks = (chunks + 255) / 256;
+    const int grid = (int)(blocks < 8 * sm_count() ? blocks : 8 * sm_count());
+    ST_CUDA_TRY(launch_pdl(splitk_reduce_kernel<T, EPI>, dim3(grid), dim3(256), 0, s, p));
     return ST_OK;
 }
 
@@ -508,8 +605,8 @@ st_status launch_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmPa
         ST_CUDA_TRY(cudaOccupancyMaxActiveClusters(&max_clusters, gemm2_kernel<T, EPI>, &cfg));
         if (max_clusters < 1) max_clusters = 1;
     }
-    const int tiles = ((p.M + 255) / 256) * p.nn * p.Z;
-    const int clusters = tiles < max_clusters ? tiles : max_clusters;
+    const int units = ((p.M + 255) / 256) * p.nn * p.Z * p.ks;
+    const int clusters = units < max_clusters ? units : max_clusters;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * clusters);
     cfg.blockDim = dim3(THREADS);
@@ -600,16 +697,55 @@ st_status gemm_sm100(const GemmArgs& g, cudaStream_t s) {
     p.vec = (reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && ((size_t)g.ldc * cbytes) % 16 == 0 &&
             ((size_t)g.c_stride_z * cbytes) % 16 == 0;
     p.wmerge = wmerge ? 1 : 0;
+    // Split-K for GEMMs with fewer output tiles than CTA slots (the engine's
+    // drafting passes, small batches), when the caller lends fp32 scratch:
+    // pick ks minimising (waves of units) x (K blocks per unit) x (per-block
+    // time: the larger of the MMA time and the per-SM load time) + the
+    // partials' extra HBM traffic and the reduction launch.
+    p.ks = 1;
+    p.nkb = p.nk;
+    p.part = nullptr;
+    static const bool splitk_env = !(getenv("ST_GEMM_SPLITK") && atoi(getenv("ST_GEMM_SPLITK")) == 0);
+    {
+        const int slots = pair ? sm_count() / 2 : sm_count();
+        const long long tiles = (long long)(pair ? (g.M + 255) / 256 : p.nm) * p.nn * p.Z;
+        const double tau = pair ? 0.44 : 0.64;  // us per K block per CTA (pair: MMA; single: 48 KB loads)
+        const double out_bytes = 4.0 * g.Z * (double)g.M * g.N;
+        auto cost = [&](int ks) {
+            const long long units = tiles * ks;
+            const long long waves = (units + slots - 1) / slots;
+            const int nkb = (p.nk + ks - 1) / ks;
+            return waves * nkb * tau + (ks > 1 ? (ks + 1) * out_bytes / 6.0e6 + 2.0 : 0.0);
+        };
+        if (splitk_env && g.work && tiles < slots) {
+            double best = cost(1);
+            for (int ks = 2; ks <= 16 && p.nk / ks >= 4; ++ks) {
+                if ((double)ks * out_bytes > (double)g.work_bytes) break;
+                const double c = cost(ks);
+                if (c < best * 0.9) {
+                    best = c;
+                    p.ks = ks;
+                }
+            }
+        }
+        if (p.ks > 1) {
+            p.nkb = (p.nk + p.ks - 1) / p.ks;
+            p.ks = (p.nk + p.nkb - 1) / p.nkb;  // no empty splits
+            p.part = g.work;
+        }
+    }
+#define ST_GEMM_RUN(TT, E)                                                          \
+    {                                                                               \
+        const st_status r_ = pair ? launch_pair<TT, E>(ta, tb, p, s) : launch<TT, E>(g, ta, tb, p, s); \
+        if (r_ != ST_OK || p.ks == 1) return r_;                                    \
+        return launch_reduce<TT, E>(p, s);                                          \
+    }
 #define ST_GEMM_EPI(TT)                                                              \
     switch (g.epi) {                                                                 \
-        case kGemmStore: return pair ? launch_pair<TT, kGemmStore>(ta, tb, p, s)     \
-                                     : launch<TT, kGemmStore>(g, ta, tb, p, s);      \
-        case kGemmGelu: return pair ? launch_pair<TT, kGemmGelu>(ta, tb, p, s)       \
-                                    : launch<TT, kGemmGelu>(g, ta, tb, p, s);        \
-        case kGemmAddTo: return pair ? launch_pair<TT, kGemmAddTo>(ta, tb, p, s)     \
-                                     : launch<TT, kGemmAddTo>(g, ta, tb, p, s);      \
-        case kGemmStoreF32: return pair ? launch_pair<TT, kGemmStoreF32>(ta, tb, p, s) \
-                                        : launch<TT, kGemmStoreF32>(g, ta, tb, p, s); \
+        case kGemmStore: ST_GEMM_RUN(TT, kGemmStore)                                 \
+        case kGemmGelu: ST_GEMM_RUN(TT, kGemmGelu)                                   \
+        case kGemmAddTo: ST_GEMM_RUN(TT, kGemmAddTo)                                 \
+        case kGemmStoreF32: ST_GEMM_RUN(TT, kGemmStoreF32)                           \
     }
     if (g.dtype == ST_F16) {
         ST_GEMM_EPI(__half)
@@ -617,6 +753,7 @@ st_status gemm_sm100(const GemmArgs& g, cudaStream_t s) {
         ST_GEMM_EPI(__nv_bfloat16)
     }
 #undef ST_GEMM_EPI
+#undef ST_GEMM_RUN
     set_error("gemm: bad epilogue");
     return ST_ERR_INVALID_ARGUMENT;
 }

@@ -24,6 +24,8 @@ struct GemmArgs {
     int ldc;                // elements
     int M, N, K, Z;
     int epi;
+    float* work = nullptr;  // optional fp32 scratch for split-K partials (none: no split)
+    size_t work_bytes = 0;
 };
 
 bool gemm_supported(const GemmArgs& g);

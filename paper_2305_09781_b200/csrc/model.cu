@@ -252,9 +252,15 @@ layernorm_warp_kernel(const T* __restrict__ x, const T* __restrict__ g, const T*
 }
 
 // Row-major C[z] (op)= A W[z] on the tcgen05 GEMM (gemm.cu).
+// fp32 scratch lent to the GEMM for split-K partials (small-M projections:
+// the engine's drafting passes and small batches)
+constexpr size_t kSplitScratch = 64ull << 20;
+
 st_status gemm(st_model* m, const void* A, const void* W, int ldw, void* C, int ldc, int M, int N,
-               int K, int Z, long long c_stride_z, int epi, cudaStream_t s) {
+               int K, int Z, long long c_stride_z, int epi, cudaStream_t s, float* work) {
     GemmArgs g{m->dtype, A, K, W, ldw, C, c_stride_z, ldc, M, N, K, Z, epi};
+    g.work = work;
+    g.work_bytes = work ? kSplitScratch : 0;
     return gemm_sm100(g, s);
 }
 
@@ -374,7 +380,7 @@ size_t st_model_workspace_size(const st_model* m, int B, int T) {
     a.W = (T + 63) / 64;
     a.Lmax = T;
     const size_t es = st::dtype_size(m->dtype);
-    return rows * (6 * d + F) * es + st_tree_attention_workspace_size(&a) + 8 * 256;
+    return rows * (6 * d + F) * es + st_tree_attention_workspace_size(&a) + st::kSplitScratch + 9 * 256;
 }
 
 static st_status tree_forward(st_model* m, int B, int T, const int32_t* tokens,
@@ -421,6 +427,8 @@ static st_status tree_forward(st_model* m, int B, int T, const int32_t* tokens,
     a.scale = 1.0 / std::sqrt((double)Dh);
     a.workspace = ws;
     a.workspace_bytes = st_tree_attention_workspace_size(&a);
+    ws += (a.workspace_bytes + 255) & ~size_t(255);
+    float* splitk = reinterpret_cast<float*>(take(st::kSplitScratch));
     // K1's predecessor is the layer's K2 append (tree rows [P, P+n) only) or,
     // in k_tree mode, the QKV GEMM: the committed rows and the lengths are
     // stable, so K1 may stream them early
@@ -484,14 +492,14 @@ static st_status tree_forward(st_model* m, int B, int T, const int32_t* tokens,
             static_cast<char*>(vn) - static_cast<char*>(kn) == qkv_stride * (long long)es) {
             // wq|wk|wv are consecutive in the serialized order: one batched launch
             if (st_status e = st::gemm(m, h, Wp(L.wq), d, q, d, rows, d, d, 3, qkv_stride,
-                                       st::kGemmStore, s))
+                                       st::kGemmStore, s, splitk))
                 return e;
         } else {
-            if (st_status e = st::gemm(m, h, Wp(L.wq), d, q, d, rows, d, d, 1, 0, st::kGemmStore, s))
+            if (st_status e = st::gemm(m, h, Wp(L.wq), d, q, d, rows, d, d, 1, 0, st::kGemmStore, s, splitk))
                 return e;
-            if (st_status e = st::gemm(m, h, Wp(L.wk), d, kn, d, rows, d, d, 1, 0, st::kGemmStore, s))
+            if (st_status e = st::gemm(m, h, Wp(L.wk), d, kn, d, rows, d, d, 1, 0, st::kGemmStore, s, splitk))
                 return e;
-            if (st_status e = st::gemm(m, h, Wp(L.wv), d, vn, d, rows, d, d, 1, 0, st::kGemmStore, s))
+            if (st_status e = st::gemm(m, h, Wp(L.wv), d, vn, d, rows, d, d, 1, 0, st::kGemmStore, s, splitk))
                 return e;
         }
         if (!tree_qkv) {
@@ -507,20 +515,20 @@ static st_status tree_forward(st_model* m, int B, int T, const int32_t* tokens,
         a.v_tree = tree_qkv ? vn : nullptr;
         if (st_status e = st_tree_attention(&a, stream)) return e;
         // x += o W_o (residual add in the epilogue)
-        if (st_status e = st::gemm(m, o, Wp(L.wo), d, x, d, rows, d, d, 1, 0, st::kGemmAddTo, s))
+        if (st_status e = st::gemm(m, o, Wp(L.wo), d, x, d, rows, d, d, 1, 0, st::kGemmAddTo, s, splitk))
             return e;
         if (st_status e = layernorm(L.ln2_g, L.ln2_b)) return e;
         // f = gelu(h W_1) (GELU in the epilogue), then x += f W_2
-        if (st_status e = st::gemm(m, h, Wp(L.w1), F, f, F, rows, F, d, 1, 0, st::kGemmGelu, s))
+        if (st_status e = st::gemm(m, h, Wp(L.w1), F, f, F, rows, F, d, 1, 0, st::kGemmGelu, s, splitk))
             return e;
-        if (st_status e = st::gemm(m, f, Wp(L.w2), d, x, d, rows, d, F, 1, 0, st::kGemmAddTo, s))
+        if (st_status e = st::gemm(m, f, Wp(L.w2), d, x, d, rows, d, F, 1, 0, st::kGemmAddTo, s, splitk))
             return e;
     }
     if (st_status e = layernorm(m->lnf_g, m->lnf_b)) return e;
 #undef ST_M_DISPATCH
     const void* wout = m->wout_pad ? m->wout_pad : Wp(m->wout);
     return st::gemm(m, h, wout, m->ldw_out, logits, c.vocab_size, rows, c.vocab_size, d, 1, 0,
-                    st::kGemmStoreF32, s);
+                    st::kGemmStoreF32, s, splitk);
 }
 
 st_status st_model_tree_forward(st_model* m, int B, int T, const int32_t* tokens,

@@ -58,6 +58,8 @@ st_status st_tree_attention(const st_attn_args* a, void* stream) {
     if (st_status e = validate_ptrs(a)) return e;
     if (a->B == 0) return ST_OK;
     const int path = choose_path(a);
+    ST_CHECK_ARG(a->q_rows <= 0 || path == 2, ST_ERR_UNSUPPORTED,
+                 "st_tree_attention: q_rows (a node slice of Q) needs the tcgen05 path and k_tree");
     if (path == 2) {
         if (!st::tree_attention_tc_supported(a)) {
             st::set_error("st_tree_attention: tcgen05 path needs f16/bf16, D == 128, G*T <= 128");

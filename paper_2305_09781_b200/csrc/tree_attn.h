@@ -17,6 +17,8 @@ struct TcParams {
     float* partial;      // [gridDim.x][SLOT_FLOATS]: the piece a CTA's first segment leaves
     unsigned* flags;     // [gridDim.x]: 1 while that piece is published and not yet merged
     int B, T, H, W;      // H: KV heads (one (b, h) pair per request and KV head)
+    int Tq, u0;          // Q / o / lse rows per request and the node id of Q row 0
+                         // (st_attn_args.q_rows / q_node0; Tq = T, u0 = 0 when unset)
     int G, Hq;           // query heads per KV head (GQA group), query heads = G * H
     int R;               // row blocks per pair: G*T <= 128 -> 1; <= 256 -> 2 (CTAs 2s, 2s+1
                          // take the two 128-row blocks of schedule slot s)

@@ -289,7 +289,7 @@ __device__ __forceinline__ void sched_finish(const TcParams& p, Sched& s, int lo
             // the symmetric DSMEM exchange (M=128 pairs of two pieces on
             // 2-CTA clusters) wants equal halves; otherwise the head piece
             // takes extra tiles, so the other pieces are in by its last P.V
-            const bool sym = p.cluster2 && S == 2 && p.R == 1 && p.G * p.T > 64;
+            const bool sym = p.cluster2 && S == 2 && p.R == 1 && p.G * p.Tq > 64;
             s.hx = sym ? 0u : min((uint32_t)p.head_extra, (uint32_t)s.nt - S);
         }
     }
@@ -927,7 +927,9 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         // Q/S/O row r holds tree node u_r of query head g_r of the pair's
         // KV-head group (the Q box lays rows out node-major, head-minor)
         const int rr = rblk * M + r;  // row within the pair's G*T rows
-        const int u_r = rr / p.G, g_r = rr - u_r * p.G;
+        // Q row qr of request b is tree node u_r (q_rows / q_node0: a slice)
+        const int qr = rr / p.G, g_r = rr - qr * p.G;
+        const int u_r = p.u0 + qr;
         const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         const uint32_t s_half = DUAL ? half * COLS : 0;          // this half's S columns
         const uint32_t o_own = DUAL ? (half ? C::OB_COL : C::O_COL) : C::O_COL;
@@ -949,7 +951,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             mt.P = __ldg(p.prefix_len + sg.b);
 #pragma unroll
             for (int w = 0; w < MW; ++w) mt.mw[w] = 0;
-            if (u_r < p.T) {
+            if (qr < p.Tq && u_r < p.T) {
                 const uint64_t* mr = p.mask + ((long long)sg.b * p.T + u_r) * p.W;
 #pragma unroll
                 for (int w = 0; w < MW; ++w)
@@ -973,7 +975,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             // first kv row index of the tree rows: P, or (k_tree mode) the
             // start of the extra tree tile after the ceil(P/BN) prefix tiles
             const int Pt = p.tree_src ? (s.ntiles - (n + BN - 1) / BN) * BN : P;
-            const bool valid = u_r < n;
+            const bool valid = qr < p.Tq && u_r < n;
             const bool warp_live = __any_sync(0xffffffffu, valid);
             uint64_t mw[MW];
 #pragma unroll
@@ -1128,7 +1130,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             const bool head = (s.lo == 0 && !full);
             const int d0 = half * DCOLS;
             const long long orow =
-                (((long long)s.b * p.T + u_r) * p.H_out + p.head_offset + s.h * p.G + g_r) * HD + d0;
+                (((long long)s.b * p.Tq + qr) * p.H_out + p.head_offset + s.h * p.G + g_r) * HD + d0;
             const uint32_t q1 = pc - 1;
             mbar_wait(pv_done + (q1 & 1), (q1 >> 1) & 1);
             if (threadIdx.x == 0) K1_GT(3);
@@ -1236,7 +1238,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             store_row<T, DCOLS>(reinterpret_cast<T*>(p.o) + orow, ov, inv);
                         }
                         if (p.lse && half == 0)
-                            p.lse[((long long)s.b * p.Hq + s.h * p.G + g_r) * p.T + u_r] = mf * p.scale + __logf(lf);
+                            p.lse[((long long)s.b * p.Hq + s.h * p.G + g_r) * p.Tq + qr] = mf * p.scale + __logf(lf);
                     }
                     if (stamp) K1_TRACE(14, 42);
                 }
@@ -1352,7 +1354,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             }
                         }
                         if (valid && p.lse && rank == 0)
-                            p.lse[((long long)s.b * p.Hq + s.h * p.G + g_r) * p.T + u_r] = mf * p.scale + __logf(lf);
+                            p.lse[((long long)s.b * p.Hq + s.h * p.G + g_r) * p.Tq + qr] = mf * p.scale + __logf(lf);
                     }
                     if (stamp) K1_TRACE(14, 42);
                 }
@@ -1475,7 +1477,7 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                     if (threadIdx.x == 0) st_release_gpu(p.flags + blockIdx.x, 1u);
                 } else {
                     if (valid && p.lse && half == 0)
-                        p.lse[((long long)s.b * p.Hq + s.h * p.G + g_r) * p.T + u_r] = m_fin * p.scale + __logf(l_fin);
+                        p.lse[((long long)s.b * p.Hq + s.h * p.G + g_r) * p.Tq + qr] = m_fin * p.scale + __logf(l_fin);
                 }
             }
             if (threadIdx.x == 0) K1_GT(4);
@@ -1545,9 +1547,12 @@ bool tree_attention_tc_supported(const st_attn_args* a) {
     // (node, head) rows in M-row blocks (M = 64 or 128; G*T > 128: two blocks
     // of 128 on a CTA pair), so G must divide M and G*T <= 256
     const int G = a->Hkv > 0 && a->H % a->Hkv == 0 ? a->H / a->Hkv : 0;
-    const int M = (int64_t)G * a->T <= 64 ? 64 : 128;
+    const int Tq = a->q_rows > 0 ? a->q_rows : a->T;
+    const int M = (int64_t)G * Tq <= 64 ? 64 : 128;
+    const bool slice_ok = a->q_rows <= 0 ||
+                          (a->k_tree && a->q_node0 >= 0 && (int64_t)a->q_node0 + a->q_rows <= a->T);
     return (a->dtype == ST_F16 || a->dtype == ST_BF16) && a->D == HD && G >= 1 && M % G == 0 &&
-           (int64_t)G * a->T <= 256 && a->W <= 4 && a->Lmax < (1ll << 31) && al(a->q) && al(a->k_cache) &&
+           slice_ok && (int64_t)G * Tq <= 256 && a->W <= 4 && a->Lmax < (1ll << 31) && al(a->q) && al(a->k_cache) &&
            al(a->v_cache) && al(a->o) && al(a->k_tree) && al(a->v_tree) &&
            (int64_t)a->B * a->Hkv * ((a->Lmax + BN - 1) / BN) < (1ll << 31);  // 32-bit tile indices
 }
@@ -1615,10 +1620,11 @@ st_status tree_attention_tc_prepare(const st_attn_args* a, const st_peer_out* po
     {
         // D = 128 as (64, half): dims (64, H, T, 2, B), the half (stride 128 B)
         // outside the nodes, so one box lands as the two K-major atoms
-        const uint64_t dims[5] = {64, (uint64_t)a->H, (uint64_t)a->T, 2, (uint64_t)a->B};
-        const uint64_t strides[4] = {HD * 2ull, (uint64_t)a->H * HD * 2, 128, (uint64_t)a->T * a->H * HD * 2};
+        const uint64_t Tq = a->q_rows > 0 ? (uint64_t)a->q_rows : (uint64_t)a->T;
+        const uint64_t dims[5] = {64, (uint64_t)a->H, Tq, 2, (uint64_t)a->B};
+        const uint64_t strides[4] = {HD * 2ull, (uint64_t)a->H * HD * 2, 128, Tq * a->H * HD * 2};
         const int G = a->H / a->Hkv;
-        const uint32_t M = (int64_t)G * a->T <= 64 ? 64 : 128;
+        const uint32_t M = (int64_t)G * Tq <= 64 ? 64 : 128;
         const uint32_t box[5] = {64, (uint32_t)G, M / G, 2, 1};
         if (!encode(&L->tq, dt, 5, a->q, dims, strides, box)) {
             set_error("st_tree_attention: cuTensorMapEncodeTiled(q) failed");
@@ -1656,7 +1662,8 @@ st_status tree_attention_tc_prepare(const st_attn_args* a, const st_peer_out* po
             return ST_ERR_CUDA;
         }
     }
-    const int R = (int64_t)(a->H / a->Hkv) * a->T <= 128 ? 1 : 2;   // row blocks per pair
+    const int Tq = a->q_rows > 0 ? a->q_rows : a->T;                 // Q rows per request
+    const int R = (int64_t)(a->H / a->Hkv) * Tq <= 128 ? 1 : 2;      // row blocks per pair
     // ST_K1_GRID (diagnostic): fewer CTAs than SMs, e.g. to measure the HBM
     // rate K1 keeps on a subset of the SMs
     static const int grid_env = getenv("ST_K1_GRID") ? atoi(getenv("ST_K1_GRID")) : 0;
@@ -1673,6 +1680,8 @@ st_status tree_attention_tc_prepare(const st_attn_args* a, const st_peer_out* po
                                             align_up((size_t)G * SLOT_FLOATS * sizeof(float), 256));
     prm.B = a->B;
     prm.T = a->T;
+    prm.Tq = Tq;
+    prm.u0 = a->q_rows > 0 ? a->q_node0 : 0;
     prm.H = a->Hkv;
     prm.G = a->H / a->Hkv;
     prm.Hq = a->H;
@@ -1700,7 +1709,7 @@ st_status tree_attention_tc_prepare(const st_attn_args* a, const st_peer_out* po
     static const bool coop = !(getenv("ST_K1_COOP") && atoi(getenv("ST_K1_COOP")) == 0);
     L->coop = coop;
     L->grid = G;
-    L->m64 = (int64_t)prm.G * a->T <= 64;
+    L->m64 = (int64_t)prm.G * Tq <= 64;
     L->mw4 = a->W > 2;   // T > 128
     L->f16 = a->dtype == ST_F16;
     return ST_OK;

@@ -42,7 +42,7 @@ def test_python_binding_covers_exports(lib):
 
 
 def test_abi_version(lib):
-    assert lib.st_abi_version() == 4
+    assert lib.st_abi_version() == 5
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the CPU-only host behaviour")

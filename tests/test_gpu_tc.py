@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 import torch
 
-from tests.test_gpu_kernels import check_k1, make_batch, run_k1
+from tests.test_gpu_kernels import TOL, check_k1, make_batch, run_k1
 from tests.treegen import expansion_seqs, pack, width_depth_seqs
 
 pytestmark = pytest.mark.gpu
@@ -440,3 +440,54 @@ def test_tc_large_trees_two_row_blocks(capi, restatement, T, G, width, own, dtyp
     capi.tree_attention(q, kc, vc, mask, Pd, nd, out=out, lse=lse, k_tree=kt, v_tree=vt)
     torch.cuda.synchronize()
     check_k1(restatement, bt, out, dtype, lse)
+
+
+@pytest.mark.parametrize("G,T,slices,dtype", [(1, 61, [(0, 1), (1, 2), (2, 12), (12, 61)], torch.float16),
+                                              (4, 21, [(0, 1), (5, 21)], torch.bfloat16),
+                                              (1, 200, [(3, 170), (100, 200)], torch.float16)])
+def test_tc_q_node_slices(capi, restatement, G, T, slices, dtype):
+    """st_attn_args.q_rows / q_node0 (ABI 5): Q, o and lse hold only the nodes
+    [u0, u0 + rows) — one level of a draft tree grown level by level — while
+    the masks and the tree rows (k_tree) span all T nodes. Every slice vs the
+    f64 restatement of the whole tree's rows; ragged n (rows past n[b] are
+    not written)."""
+    rng = np.random.default_rng(T + G)
+    B, Hkv = 3, 2
+    w = 3
+    trees = [restatement.merge(width_depth_seqs(rng, int(rng.integers(0, 40)), 40, w, max(1, (T - 1) // w)),
+                               4096) for _ in range(B)]
+    bt = make_batch(restatement, rng, B, G * Hkv, Hkv, 128, trees=trees, T=T, P_range=(0, 400),
+                    dtype=dtype)
+    D = 128
+    dev = "cuda"
+    ref, ref_lse = restatement.tree_attention(bt["q"], bt["kc"], bt["vc"], bt["mask"], bt["P"], bt["n"],
+                                              1.0 / np.sqrt(D), want_lse=True)
+    q = torch.tensor(bt["q"], device=dev).to(dtype)
+    kc = torch.tensor(bt["kc"], device=dev).to(dtype)
+    vc = torch.tensor(bt["vc"], device=dev).to(dtype)
+    Tt = q.shape[1]
+    kt = torch.zeros(B, Tt, Hkv, D, dtype=dtype, device=dev)
+    vt = torch.zeros_like(kt)
+    for b in range(B):
+        P, n = int(bt["P"][b]), int(bt["n"][b])
+        kt[b, :n] = kc[b, :, P:P + n].transpose(0, 1)
+        vt[b, :n] = vc[b, :, P:P + n].transpose(0, 1)
+    mask = torch.tensor(bt["mask"].view(np.int64), device=dev)
+    P_t, n_t = torch.tensor(bt["P"], device=dev), torch.tensor(bt["n"], device=dev)
+    for u0, u1 in slices:
+        u1 = min(u1, Tt)
+        qs = q[:, u0:u1].contiguous()
+        out = torch.full_like(qs, 7.0)
+        lse = torch.zeros((B, G * Hkv, u1 - u0), dtype=torch.float32, device=dev)
+        capi.tree_attention(qs, kc, vc, mask, P_t, n_t, out=out, lse=lse, force_path=2, k_tree=kt,
+                            v_tree=vt, q_node0=u0)
+        torch.cuda.synchronize()
+        got, L = out.double().cpu().numpy(), lse.double().cpu().numpy()
+        for b in range(B):
+            k = int(bt["n"][b])
+            hi = min(u1, k)
+            if hi > u0:
+                assert np.abs(got[b, : hi - u0] - ref[b, u0:hi]).max() <= TOL[dtype]
+                np.testing.assert_allclose(L[b, :, : hi - u0], ref_lse[b, :, u0:hi], atol=1e-4, rtol=0)
+            if u1 > max(k, u0):   # rows past n[b] untouched
+                assert torch.all(out[b, max(k, u0) - u0:] == 7.0)
