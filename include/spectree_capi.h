@@ -114,7 +114,7 @@ typedef struct {
     /* Optional (0 = off; ABI 5): q, o and lse hold only q_rows rows per
      * request — tree nodes [q_node0, q_node0 + q_rows), e.g. one level of a
      * draft tree grown level by level — while the mask rows and the tree rows
-     * (k_tree, required) stay indexed by node id over T and n_nodes counts
+     * (k_tree; required on the tcgen05 path) stay indexed by node id over T and n_nodes counts
      * every node so far. q/o row stride q_rows, lse [B][H][q_rows]. */
     int q_rows;
     int q_node0;
@@ -307,6 +307,20 @@ st_status st_model_tree_forward_kt(st_model* m, int B, int T, const int32_t* tok
                                    void* k_cache, void* v_cache, int64_t Lmax, void* tree_qkv,
                                    float* logits, void* workspace, size_t workspace_bytes,
                                    void* stream);
+/* The k_tree pass over a SLICE of the tree: only nodes [u0, u0 + nf) of every
+ * request (e.g. one level of a tree grown level by level) go through the
+ * model — B*nf rows — attending to the committed rows and to every tree node
+ * whose K/V is already in tree_qkv (earlier slices); the slice's own K/V rows
+ * are written there (rows b*T + u), so after the last slice tree_qkv holds
+ * the whole tree as st_model_tree_forward_kt leaves it. tokens / positions /
+ * mask are the full-tree arrays ([B][T]); n_nodes counts the nodes so far.
+ * logits (optional) [B][nf][V]; workspace st_model_workspace_size(m, B, nf). */
+st_status st_model_tree_forward_slice(st_model* m, int B, int T, int u0, int nf,
+                                      const int32_t* tokens, const int32_t* positions,
+                                      const uint64_t* mask, int W, const int32_t* prefix_len,
+                                      const int32_t* n_nodes, void* k_cache, void* v_cache,
+                                      int64_t Lmax, void* tree_qkv, float* logits, void* workspace,
+                                      size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------- verification step plan ---
  * One verification step of a batch as a prepared object:

@@ -104,6 +104,8 @@ SIGNATURES = {
                                _I64, _V, _V, _V]),
     "st_model_tree_forward_kt": (_I, [_V, _I, _I, _V, _V, _V, _I, _V, _V, _V, _V, _I64, _V, _V,
                                       _V, _Z, _V]),
+    "st_model_tree_forward_slice": (_I, [_V, _I, _I, _I, _I, _V, _V, _V, _I, _V, _V, _V, _V,
+                                         _I64, _V, _V, _V, _Z, _V]),
     "st_gemm": (_I, [_I, _I, _I, _I, _I, _V, _I, _V, _I, _V, _I, _I64, _I, _V]),
 }
 
@@ -188,7 +190,7 @@ def tree_attention(q, k_cache, v_cache, mask, prefix_len, n_nodes, out=None, lse
     """K1 through st_tree_attention. Shapes: q [B,T,H,D]; caches [B,Hkv,Lmax,D];
     mask [B,T,W] int64 (uint64 bits); prefix_len/n_nodes [B] int32 (device);
     k_tree/v_tree (optional) [B,T,Hkv,D]: the tree rows, read instead of cache
-    rows [P, P+n). q_node0 (needs k_tree): q / out / lse hold only the nodes
+    rows [P, P+n). q_node0 (tcgen05 path: needs k_tree): q / out / lse hold only the nodes
     [q_node0, q_node0 + q.shape[1]) of the T = mask.shape[1] tree nodes."""
     if out is None:
         out = torch.empty_like(q)
@@ -444,6 +446,24 @@ class DeviceModel:
                                                  k_cache.shape[-2], _ptr(tree_qkv), _ptr(logits),
                                                  _ptr(self._ws), self._ws.numel(),
                                                  _stream(stream)))
+        return logits
+
+    def tree_forward_slice(self, u0, nf, tokens, positions, mask, prefix_len, n_nodes, k_cache,
+                           v_cache, tree_qkv, logits=None, stream=None):
+        """st_model_tree_forward_slice: only nodes [u0, u0 + nf) of every
+        request go through the model (one level of a tree grown level by
+        level); their K/V land in tree_qkv, earlier slices' K/V are read from
+        there. tokens / positions / mask are the full-tree arrays; n_nodes
+        counts the nodes so far. logits (optional) [B, nf, V] f32."""
+        B, T = tokens.shape
+        need = int(lib().st_model_workspace_size(self.handle, B, T))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.zeros(need, dtype=torch.uint8, device=tokens.device)
+        check(lib().st_model_tree_forward_slice(
+            self.handle, B, T, u0, nf, _ptr(tokens), _ptr(positions), _ptr(mask), mask.shape[-1],
+            _ptr(prefix_len), _ptr(n_nodes), _ptr(k_cache), _ptr(v_cache), k_cache.shape[-2],
+            _ptr(tree_qkv), _ptr(logits) if logits is not None else None, _ptr(self._ws),
+            self._ws.numel(), _stream(stream)))
         return logits
 
 

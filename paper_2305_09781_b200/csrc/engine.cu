@@ -4,11 +4,14 @@
 //
 // One step (st_engine_step, no host synchronisation, CUDA-graph capturable):
 //   draft  : the SSM (or the LLM itself) grows each request's expansion tree
-//            <e_1..e_d> level by level — one masked tree pass of the draft model
-//            over the current tree, then the e_i most likely next tokens of
-//            every frontier node become its children (top-e kernel below);
-//            one more pass over the final tree leaves the draft model's K/V of
-//            every node in its cache
+//            <e_1..e_d> level by level — one pass of the draft model over the
+//            frontier level ONLY (st_model_tree_forward_slice: the earlier
+//            levels' K/V stay in the draft tree buffer, so each node goes
+//            through the draft model once per step, not once per level), then
+//            the e_i most likely next tokens of every frontier node become its
+//            children (top-e kernel below); one more slice pass over the last
+//            level completes the tree's draft K/V, committed to the draft
+//            model's cache with the accepted ids after verification
 //   verify : one tree pass of the LLM over every request's tree -> K3 greedy
 //            walk with the engine's budget truncation and EOS cut applied on
 //            the device (engine.cpp:110-121), fused with the K2 commit of the
@@ -44,6 +47,7 @@ struct st_engine {
     uint64_t* mask;
     float *logits_llm, *logits_ssm;
     void *llm_k, *llm_v, *ssm_k, *ssm_v;
+    void* tree_draft = nullptr;    // [ssm layers][3][B*T][d]: the draft tree's Q|K|V (slice passes)
     void *ws_model, *ws_ssm, *ws_ver;
     size_t ws_model_bytes = 0, ws_ssm_bytes = 0;
     int32_t* host = nullptr;       // pinned: [B][T+1] verified | [B] len | [B] done
@@ -94,7 +98,8 @@ expand_kernel(const float* __restrict__ logits, int T, int V, int f0, int f1, in
     const int k = blockIdx.x, b = blockIdx.y, u = f0 + k;
     const bool allowed = !done[b] && P[b] + depth + 1 <= max_positions - 1;
     if (!allowed || u >= f1) return;
-    const float* row = logits + ((int64_t)b * T + u) * V;
+    // the slice pass's logits: [B][f1 - f0][V], row k of request b = node f0 + k
+    const float* row = logits + ((int64_t)b * (f1 - f0) + k) * V;
     // per-thread top-e (sorted, largest key first), then e block-wide rounds
     unsigned long long mine[kMaxE];
 #pragma unroll
@@ -224,6 +229,9 @@ st_status st_engine_create(st_model* llm, st_model* ssm, const st_engine_config*
     bytes += (c.depth > 0 ? (size_t)B * T * V * 4 : 0) + 256;        // draft logits
     bytes += 2 * (cache_elems(e->mc) * es + 256);
     if (e->ssm != e->llm) bytes += 2 * (cache_elems(e->sc) * es + 256);
+    const size_t tree_draft_bytes =
+        c.depth > 0 ? (size_t)e->sc.num_layers * 3 * B * T * e->sc.d_model * es : 0;
+    bytes += tree_draft_bytes + 256;
     bytes += e->ws_model_bytes + e->ws_ssm_bytes + st_verify_workspace_size(B, T) + 3 * 256;
     if (cudaMalloc(&e->buf, bytes) != cudaSuccess) {
         cudaGetLastError();
@@ -258,6 +266,7 @@ st_status st_engine_create(st_model* llm, st_model* ssm, const st_engine_config*
         e->ssm_k = e->llm_k;  // self-drafting: the draft passes use the LLM's own cache
         e->ssm_v = e->llm_v;
     }
+    e->tree_draft = tree_draft_bytes ? st::carve<char>(at, tree_draft_bytes) : nullptr;
     e->ws_model = st::carve<char>(at, e->ws_model_bytes);
     e->ws_ssm = e->ws_ssm_bytes ? st::carve<char>(at, e->ws_ssm_bytes) : e->ws_model;
     if (!e->ws_ssm_bytes) e->ws_ssm_bytes = e->ws_model_bytes;
@@ -351,22 +360,27 @@ st_status st_engine_step(st_engine* e, void* stream) {
     ST_LAUNCH_CHECK();
     const int d = e->cfg.depth;
     for (int i = 0; i < d; ++i) {   // draft: grow level i+1 from level i
-        if (st_status r = st_build_masks(e->par, e->n, B, T, W, e->mask, stream)) return r;
-        if (st_status r = st_model_tree_forward(e->ssm, B, T, e->tok, e->pos, e->mask, W, e->P,
-                                                e->n, e->ssm_k, e->ssm_v, e->Lmax, e->logits_ssm,
-                                                e->ws_ssm, e->ws_ssm_bytes, stream))
-            return r;
         const int f0 = i == 0 ? 0 : e->lvl_end[i - 1], f1 = e->lvl_end[i];
+        if (st_status r = st_build_masks(e->par, e->n, B, T, W, e->mask, stream)) return r;
+        // the frontier level through the draft model (earlier levels' K/V
+        // are in tree_draft from the previous slices)
+        if (st_status r = st_model_tree_forward_slice(e->ssm, B, T, f0, f1 - f0, e->tok, e->pos,
+                                                      e->mask, W, e->P, e->n, e->ssm_k, e->ssm_v,
+                                                      e->Lmax, e->tree_draft, e->logits_ssm,
+                                                      e->ws_ssm, e->ws_ssm_bytes, stream))
+            return r;
         st::expand_kernel<<<dim3(f1 - f0, B), st::kTopThreads, 0, s>>>(
             e->logits_ssm, T, V, f0, f1, e->cfg.expansion[i], i, e->mc.max_positions, e->P, e->done,
             e->tok, e->par, e->pos, e->n);
         ST_LAUNCH_CHECK();
     }
     if (st_status r = st_build_masks(e->par, e->n, B, T, W, e->mask, stream)) return r;
-    if (d > 0 && e->ssm != e->llm) {  // draft-model K/V of every node of the final tree
-        if (st_status r = st_model_tree_forward(e->ssm, B, T, e->tok, e->pos, e->mask, W, e->P,
-                                                e->n, e->ssm_k, e->ssm_v, e->Lmax, e->logits_ssm,
-                                                e->ws_ssm, e->ws_ssm_bytes, stream))
+    if (d > 0 && e->ssm != e->llm) {  // draft-model K/V of the last level (no logits needed)
+        const int f0 = e->lvl_end[d - 1], f1 = e->lvl_end[d];
+        if (st_status r = st_model_tree_forward_slice(e->ssm, B, T, f0, f1 - f0, e->tok, e->pos,
+                                                      e->mask, W, e->P, e->n, e->ssm_k, e->ssm_v,
+                                                      e->Lmax, e->tree_draft, nullptr, e->ws_ssm,
+                                                      e->ws_ssm_bytes, stream))
             return r;
     }
     // verify: the LLM over every tree, greedy walk + budget/EOS + K2 commit
@@ -382,12 +396,15 @@ st_status st_engine_step(st_engine* e, void* stream) {
             e->mc.num_layers, layer, e->P, e->Pnext, nullptr, nullptr, 0, e->llm_k, e->llm_v,
             stream))
         return r;
-    if (d > 0 && e->ssm != e->llm) {
+    if (d > 0 && e->ssm != e->llm) {  // the accepted rows' draft K/V into the draft cache
         const int sDh = e->sc.d_model / e->sc.num_heads;
-        if (st_status r = st_kv_compact(e->dtype, B, e->sc.num_heads, sDh, e->Lmax,
-                                        e->sc.num_layers,
-                                        (int64_t)B * e->sc.num_heads * e->Lmax * sDh, e->ids,
-                                        T + 1, e->len, e->P, nullptr, e->ssm_k, e->ssm_v, stream))
+        const size_t tl = (size_t)B * T * e->sc.d_model;  // one [B*T][d] slot of tree_draft
+        const size_t es = st::dtype_size(e->dtype);
+        if (st_status r = st_kv_commit_tree(
+                e->dtype, B, T, e->sc.num_heads, sDh, e->Lmax, e->sc.num_layers,
+                (int64_t)B * e->sc.num_heads * e->Lmax * sDh, e->ids, T + 1, e->len, e->P, nullptr,
+                static_cast<char*>(e->tree_draft) + tl * es, static_cast<char*>(e->tree_draft) + 2 * tl * es,
+                (int64_t)(3 * tl), e->ssm_k, e->ssm_v, stream))
             return r;
     }
     st::commit_rows_kernel<<<(B + 127) / 128, 128, 0, s>>>(e->ver, e->len, e->Pnext, B, T, e->Lseq,

@@ -66,6 +66,33 @@ __global__ void embed_kernel(const T* __restrict__ tok_emb, const T* __restrict_
         x[(int64_t)i * d + c] = from_acc<T>(to_acc<float>(te[c]) + to_acc<float>(pe[c]));
 }
 
+// The embedding rows of a tree slice: row j = b * nf + r is node u0 + r of
+// request b (full-tree token / position arrays [B][T]).
+template <class T>
+__global__ void embed_slice_kernel(const T* __restrict__ tok_emb, const T* __restrict__ pos_emb,
+                                   const int32_t* __restrict__ tokens, const int32_t* __restrict__ pos,
+                                   int Ttree, int u0, int nf, int d, T* __restrict__ x) {
+    const int j = blockIdx.x, b = j / nf, u = u0 + (j - b * nf);
+    const int32_t t = tokens[(int64_t)b * Ttree + u], p = pos[(int64_t)b * Ttree + u];
+    const T* te = tok_emb + (int64_t)t * d;
+    const T* pe = pos_emb + (int64_t)p * d;
+    for (int c = threadIdx.x; c < d; c += blockDim.x)
+        x[(int64_t)j * d + c] = from_acc<T>(to_acc<float>(te[c]) + to_acc<float>(pe[c]));
+}
+
+// Compact slice rows [B*nf][d] -> full-tree rows (b*T + u0 + r) of dst, for
+// K and V at once (16-byte vectors; d % 8 == 0).
+__global__ void scatter_slice_kernel(const uint4* __restrict__ k_src, const uint4* __restrict__ v_src,
+                                     uint4* __restrict__ k_dst, uint4* __restrict__ v_dst, int Ttree,
+                                     int u0, int nf, int row_vecs) {
+    const int j = blockIdx.x, b = j / nf, u = u0 + (j - b * nf);
+    const int64_t src = (int64_t)j * row_vecs, dst = ((int64_t)b * Ttree + u) * row_vecs;
+    for (int c = threadIdx.x; c < row_vecs; c += blockDim.x) {
+        k_dst[dst + c] = k_src[src + c];
+        v_dst[dst + c] = v_src[src + c];
+    }
+}
+
 __device__ float block_sum(float v, float* red) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -383,20 +410,26 @@ size_t st_model_workspace_size(const st_model* m, int B, int T) {
     return rows * (6 * d + F) * es + st_tree_attention_workspace_size(&a) + st::kSplitScratch + 9 * 256;
 }
 
+// nf > 0: the slice pass (st_model_tree_forward_slice) — only nodes
+// [u0, u0 + nf) of every request go through the model (rows = B * nf), their
+// K/V scattered into tree_qkv's full-tree rows before each layer's K1, which
+// reads Q for the slice and the tree rows from tree_qkv (q_rows / q_node0).
 static st_status tree_forward(st_model* m, int B, int T, const int32_t* tokens,
                               const int32_t* positions, const uint64_t* mask, int W,
                               const int32_t* prefix_len, const int32_t* n_nodes, void* k_cache,
                               void* v_cache, int64_t Lmax, void* tree_qkv, float* logits,
-                              void* workspace, size_t workspace_bytes, void* stream) {
+                              void* workspace, size_t workspace_bytes, void* stream, int u0 = 0,
+                              int nf = 0) {
     if (st_status e = st::require_device()) return e;
+    const bool slice = nf > 0;
     ST_CHECK_ARG(m && tokens && positions && mask && prefix_len && n_nodes && k_cache && v_cache &&
-                     logits && workspace,
+                     (logits || slice) && workspace && (tree_qkv || !slice),
                  ST_ERR_INVALID_ARGUMENT, "null pointer");
     ST_CHECK_ARG(B >= 1 && T >= 1 && W * 64 >= T && Lmax >= T, ST_ERR_SHAPE_MISMATCH, "bad shape");
-    ST_CHECK_ARG(workspace_bytes >= st_model_workspace_size(m, B, T), ST_ERR_INVALID_ARGUMENT,
-                 "workspace too small");
+    ST_CHECK_ARG(!slice || (u0 >= 0 && u0 + nf <= T), ST_ERR_SHAPE_MISMATCH, "bad tree slice");
+    const int Tr = slice ? nf : T;   // model rows per request
     const auto& c = m->cfg;
-    const int rows = B * T, d = c.d_model, H = c.num_heads, Dh = d / H, F = c.ffn_mult * d;
+    const int rows = B * Tr, d = c.d_model, H = c.num_heads, Dh = d / H, F = c.ffn_mult * d;
     const size_t es = st::dtype_size(m->dtype);
     cudaStream_t s = st::as_stream(stream);
     char* ws = static_cast<char*>(workspace);
@@ -425,10 +458,19 @@ static st_status tree_forward(st_model* m, int B, int T, const int32_t* tokens,
     a.prefix_len = prefix_len;
     a.n_nodes = n_nodes;
     a.scale = 1.0 / std::sqrt((double)Dh);
+    if (slice) {
+        a.q_rows = nf;
+        a.q_node0 = u0;
+    }
     a.workspace = ws;
+    a.k_tree = a.v_tree = tree_qkv;  // (the path, hence the size, depends on k_tree being set)
     a.workspace_bytes = st_tree_attention_workspace_size(&a);
     ws += (a.workspace_bytes + 255) & ~size_t(255);
     float* splitk = reinterpret_cast<float*>(take(st::kSplitScratch));
+    // exact need of this pass (a slice's K1 spans T nodes with q_rows = nf;
+    // st_model_workspace_size(m, B, T) always covers it)
+    ST_CHECK_ARG((size_t)(ws - static_cast<char*>(workspace)) <= workspace_bytes,
+                 ST_ERR_INVALID_ARGUMENT, "workspace too small");
     // K1's predecessor is the layer's K2 append (tree rows [P, P+n) only) or,
     // in k_tree mode, the QKV GEMM: the committed rows and the lengths are
     // stable, so K1 may stream them early
@@ -444,9 +486,15 @@ static st_status tree_forward(st_model* m, int B, int T, const int32_t* tokens,
         using T = __nv_bfloat16;                                             \
         __VA_ARGS__;                                                         \
     }
-    ST_M_DISPATCH(st::embed_kernel<T><<<rows, 256, 0, s>>>(st::wptr<T>(m, m->tok),
-                                                           st::wptr<T>(m, m->pos), tokens,
-                                                           positions, d, (T*)x));
+    const int Ttree = T;  // (the dispatch macro binds T to the element type)
+    if (slice) {
+        ST_M_DISPATCH(st::embed_slice_kernel<T><<<rows, 256, 0, s>>>(
+            st::wptr<T>(m, m->tok), st::wptr<T>(m, m->pos), tokens, positions, Ttree, u0, nf, d, (T*)x));
+    } else {
+        ST_M_DISPATCH(st::embed_kernel<T><<<rows, 256, 0, s>>>(st::wptr<T>(m, m->tok),
+                                                               st::wptr<T>(m, m->pos), tokens,
+                                                               positions, d, (T*)x));
+    }
     ST_LAUNCH_CHECK();
     auto aligned16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
     // LayerNorm of x into h: register-resident vector kernel when the shapes allow
@@ -482,10 +530,14 @@ static st_status tree_forward(st_model* m, int B, int T, const int32_t* tokens,
         void* vc = static_cast<char*>(v_cache) + (size_t)l * layer_elems * es;
         if (st_status e = layernorm(L.ln1_g, L.ln1_b)) return e;
         const size_t dd = (size_t)d * d;
-        if (tree_qkv) {  // k_tree mode: this layer's Q|K|V stay in the caller's buffer
-            q = static_cast<char*>(tree_qkv) + (size_t)l * 3 * rows * d * es;
-            kn = static_cast<char*>(q) + (size_t)rows * d * es;
-            vn = static_cast<char*>(kn) + (size_t)rows * d * es;
+        // tree_qkv layer l: [3][B*T][d] (Q | K | V of every tree node)
+        char* tq_l = tree_qkv ? static_cast<char*>(tree_qkv) + (size_t)l * 3 * B * T * d * es : nullptr;
+        char* tk_l = tq_l ? tq_l + (size_t)B * T * d * es : nullptr;
+        char* tv_l = tq_l ? tk_l + (size_t)B * T * d * es : nullptr;
+        if (tree_qkv && !slice) {  // k_tree mode: this layer's Q|K|V stay in the caller's buffer
+            q = tq_l;
+            kn = tk_l;
+            vn = tv_l;
         }
         const long long qkv_stride = (static_cast<char*>(kn) - static_cast<char*>(q)) / (long long)es;
         if (L.wk == L.wq + dd && L.wv == L.wk + dd &&
@@ -507,12 +559,18 @@ static st_status tree_forward(st_model* m, int B, int T, const int32_t* tokens,
                                            kc, vc, stream))
                 return e;
         }
+        if (slice) {  // the slice's K/V rows into the full-tree rows b*T + u0 + r
+            st::scatter_slice_kernel<<<rows, 128, 0, s>>>(
+                static_cast<const uint4*>(kn), static_cast<const uint4*>(vn), reinterpret_cast<uint4*>(tk_l),
+                reinterpret_cast<uint4*>(tv_l), T, u0, nf, (int)((size_t)d * es / 16));
+            ST_LAUNCH_CHECK();
+        }
         a.q = q;
         a.k_cache = kc;
         a.v_cache = vc;
         a.o = o;
-        a.k_tree = tree_qkv ? kn : nullptr;
-        a.v_tree = tree_qkv ? vn : nullptr;
+        a.k_tree = tree_qkv ? tk_l : nullptr;
+        a.v_tree = tree_qkv ? tv_l : nullptr;
         if (st_status e = st_tree_attention(&a, stream)) return e;
         // x += o W_o (residual add in the epilogue)
         if (st_status e = st::gemm(m, o, Wp(L.wo), d, x, d, rows, d, d, 1, 0, st::kGemmAddTo, s, splitk))
@@ -524,6 +582,7 @@ static st_status tree_forward(st_model* m, int B, int T, const int32_t* tokens,
         if (st_status e = st::gemm(m, f, Wp(L.w2), d, x, d, rows, d, F, 1, 0, st::kGemmAddTo, s, splitk))
             return e;
     }
+    if (!logits) return ST_OK;  // (slice pass for the tree's K/V only)
     if (st_status e = layernorm(m->lnf_g, m->lnf_b)) return e;
 #undef ST_M_DISPATCH
     const void* wout = m->wout_pad ? m->wout_pad : Wp(m->wout);
@@ -552,3 +611,15 @@ st_status st_model_tree_forward_kt(st_model* m, int B, int T, const int32_t* tok
 }
 
 }  // extern "C"
+
+st_status st_model_tree_forward_slice(st_model* m, int B, int T, int u0, int nf,
+                                      const int32_t* tokens, const int32_t* positions,
+                                      const uint64_t* mask, int W, const int32_t* prefix_len,
+                                      const int32_t* n_nodes, void* k_cache, void* v_cache,
+                                      int64_t Lmax, void* tree_qkv, float* logits, void* workspace,
+                                      size_t workspace_bytes, void* stream) {
+    ST_CHECK_ARG(tree_qkv != nullptr && nf >= 1, ST_ERR_INVALID_ARGUMENT, "null tree_qkv or empty slice");
+    ST_CHECK_ARG(m && m->cfg.d_model % 8 == 0, ST_ERR_UNSUPPORTED, "slice pass needs d_model % 8 == 0");
+    return tree_forward(m, B, T, tokens, positions, mask, W, prefix_len, n_nodes, k_cache, v_cache,
+                        Lmax, tree_qkv, logits, workspace, workspace_bytes, stream, u0, nf);
+}

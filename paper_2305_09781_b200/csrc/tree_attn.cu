@@ -58,8 +58,9 @@ st_status st_tree_attention(const st_attn_args* a, void* stream) {
     if (st_status e = validate_ptrs(a)) return e;
     if (a->B == 0) return ST_OK;
     const int path = choose_path(a);
-    ST_CHECK_ARG(a->q_rows <= 0 || path == 2, ST_ERR_UNSUPPORTED,
-                 "st_tree_attention: q_rows (a node slice of Q) needs the tcgen05 path and k_tree");
+    ST_CHECK_ARG(a->q_rows <= 0 || (a->q_node0 >= 0 && (int64_t)a->q_node0 + a->q_rows <= a->T),
+                 ST_ERR_INVALID_ARGUMENT,
+                 "st_tree_attention: q_rows slice [q_node0, q_node0 + q_rows) outside [0, T)");
     if (path == 2) {
         if (!st::tree_attention_tc_supported(a)) {
             st::set_error("st_tree_attention: tcgen05 path needs f16/bf16, D == 128, G*T <= 128");

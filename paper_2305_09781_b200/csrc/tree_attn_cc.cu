@@ -48,22 +48,24 @@ tree_attn_cc_kernel(const T* __restrict__ q, const T* __restrict__ kc, const T* 
                     const uint64_t* __restrict__ mask, const int32_t* __restrict__ prefix_len,
                     const int32_t* __restrict__ n_nodes, T* __restrict__ o, float* __restrict__ lse,
                     int B, int T_, int H, int Hkv, int D, int W, int64_t Lmax, double scale_d,
-                    const T* __restrict__ kt, const T* __restrict__ vt) {
+                    const T* __restrict__ kt, const T* __restrict__ vt, int Tq, int u0) {
     using A = typename acc_of<T>::type;
     __shared__ A qs[kWarps][32 * DPL];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t item = (int64_t)blockIdx.x * kWarps + warp;
-    if (item >= (int64_t)B * T_ * H) return;
+    if (item >= (int64_t)B * Tq * H) return;
+    // Q row r of the Tq-row slice is tree node u = u0 + r (u0 = 0, Tq = T: all nodes)
     const int h = (int)(item % H);
-    const int u = (int)((item / H) % T_);
-    const int b = (int)(item / ((int64_t)H * T_));
+    const int r = (int)((item / H) % Tq);
+    const int u = u0 + r;
+    const int b = (int)(item / ((int64_t)H * Tq));
     const int n = n_nodes[b];
     if (u >= n) return;
     const int P = prefix_len[b];
     const int hk = h / (H / Hkv);
     const A scale = (A)scale_d;
 
-    const T* qrow = q + (((int64_t)b * T_ + u) * H + h) * D;
+    const T* qrow = q + (((int64_t)b * Tq + r) * H + h) * D;
     for (int d = lane; d < 32 * DPL; d += 32) qs[warp][d] = d < D ? to_acc<A>(qrow[d]) : (A)0;
     __syncwarp();
 
@@ -119,7 +121,7 @@ tree_attn_cc_kernel(const T* __restrict__ q, const T* __restrict__ kc, const T* 
         m = m_new;
     }
 
-    T* orow = o + (((int64_t)b * T_ + u) * H + h) * D;
+    T* orow = o + (((int64_t)b * Tq + r) * H + h) * D;
     const A inv = (A)1 / l;
 #pragma unroll
     for (int i = 0; i < DPL; ++i) {
@@ -129,12 +131,13 @@ tree_attn_cc_kernel(const T* __restrict__ q, const T* __restrict__ kc, const T* 
             else orow[d] = from_acc<T>(acc[i] * inv);
         }
     }
-    if (lse && lane == 0) lse[((int64_t)b * H + h) * T_ + u] = (float)(m + log_acc(l));
+    if (lse && lane == 0) lse[((int64_t)b * H + h) * Tq + r] = (float)(m + log_acc(l));
 }
 
 template <class T>
 st_status launch_cc(const st_attn_args* a, cudaStream_t s) {
-    const int64_t items = (int64_t)a->B * a->T * a->H;
+    const int Tq = a->q_rows > 0 ? a->q_rows : a->T, u0 = a->q_rows > 0 ? a->q_node0 : 0;
+    const int64_t items = (int64_t)a->B * Tq * a->H;
     const unsigned grid = (unsigned)((items + kWarps - 1) / kWarps);
     if (grid == 0) return ST_OK;
     const int dpl = (a->D + 31) / 32;
@@ -142,7 +145,7 @@ st_status launch_cc(const st_attn_args* a, cudaStream_t s) {
     tree_attn_cc_kernel<T, N><<<grid, 32 * kWarps, 0, s>>>(                                  \
         (const T*)a->q, (const T*)a->k_cache, (const T*)a->v_cache, a->mask, a->prefix_len, \
         a->n_nodes, (T*)a->o, a->lse, a->B, a->T, a->H, a->Hkv, a->D, a->W, a->Lmax, a->scale, \
-        (const T*)a->k_tree, (const T*)a->v_tree)
+        (const T*)a->k_tree, (const T*)a->v_tree, Tq, u0)
     if (dpl <= 1) ST_CC_LAUNCH(1);
     else if (dpl <= 2) ST_CC_LAUNCH(2);
     else if (dpl <= 4) ST_CC_LAUNCH(4);

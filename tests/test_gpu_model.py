@@ -144,3 +144,53 @@ def test_tree_forward_k_tree_mode_and_commit(capi, restatement):
                 vt = qkv[layer, 2, src].view(H, Dh)
                 assert torch.equal(k2[layer, b, :, p0 + k], kt)
                 assert torch.equal(v2[layer, b, :, p0 + k], vt)
+
+
+@pytest.mark.parametrize("H,d", [(4, 512), (4, 256)])   # head dim 128 (tcgen05 K1), 64 (CUDA-core K1)
+def test_tree_forward_slices_match_whole_tree(capi, restatement, H, d):
+    """st_model_tree_forward_slice: the tree pushed through the model slice
+    by slice (each slice attends to the earlier slices' K/V in tree_qkv and
+    to itself) gives the whole-tree k_tree pass's logits and leaves the same
+    tree_qkv — the incremental drafting of the device engine. Nodes are in
+    parent-before-child order, so any contiguous slicing is valid; n_nodes
+    counts the nodes pushed so far."""
+    from tests.treegen import pack, width_depth_seqs
+    rng = np.random.default_rng(11)
+    L_, V = 2, 512
+    model = capi.DeviceModel(L_, H, d, V, 256, 4, seed=3, dtype=torch.float16)
+    trees = [restatement.merge(width_depth_seqs(rng, int(rng.integers(0, V)), V, 3, 6), 1024)
+             for _ in range(3)]
+    tok, par, dep, n = pack(trees)
+    assert all((par[b, 1:int(n[b])] < np.arange(1, int(n[b]))).all() for b in range(len(n)))
+    B, T = tok.shape
+    dev = "cuda"
+    P = torch.tensor([40, 7, 100], dtype=torch.int32, device=dev)
+    tk, pr, nd = (torch.tensor(x, device=dev) for x in (tok, par, n))
+    pos = (P[:, None] + torch.tensor(dep, device=dev)).to(torch.int32)
+    mask = capi.build_masks(pr, nd)
+    kc, vc = model.new_cache(B, 128 + T)
+    kc.uniform_(-1, 1)
+    vc.uniform_(-1, 1)
+    qkv_full = model.new_tree_qkv(B, T)
+    full = model.tree_forward(tk, pos, mask, P, nd, kc, vc, tree_qkv=qkv_full)
+    qkv = model.new_tree_qkv(B, T)
+    cuts = sorted({0, 1, 4, T // 3, T - 5, T} & set(range(T + 1)))
+    for u0, u1 in zip(cuts[:-1], cuts[1:]):
+        lg = torch.full((B, u1 - u0, V), float("nan"), dtype=torch.float32, device=dev)
+        so_far = torch.clamp(nd, max=u1).to(torch.int32)
+        model.tree_forward_slice(u0, u1 - u0, tk, pos, mask, P, so_far, kc, vc, qkv, logits=lg)
+        torch.cuda.synchronize()
+        for b in range(B):
+            hi = min(u1, int(n[b]))
+            if hi > u0:
+                err = (lg[b, :hi - u0] - full[b, u0:hi]).abs().max().item()
+                assert err < 2e-3, (u0, u1, b, err)
+    # the K/V tree rows every layer's K1 read (GEMM accumulation order may differ
+    # with the row count, e.g. split-K for small slices)
+    for b in range(B):
+        rows = slice(b * T, b * T + int(n[b]))
+        err = (qkv[:, 1:, rows].float() - qkv_full[:, 1:, rows].float()).abs().max().item()
+        assert err < 2e-3, err
+    # slice outside [0, T) is rejected
+    with pytest.raises(Exception):
+        model.tree_forward_slice(T - 1, 2, tk, pos, mask, P, nd, kc, vc, qkv)

@@ -445,12 +445,14 @@ def test_tc_large_trees_two_row_blocks(capi, restatement, T, G, width, own, dtyp
 @pytest.mark.parametrize("G,T,slices,dtype", [(1, 61, [(0, 1), (1, 2), (2, 12), (12, 61)], torch.float16),
                                               (4, 21, [(0, 1), (5, 21)], torch.bfloat16),
                                               (1, 200, [(3, 170), (100, 200)], torch.float16)])
-def test_tc_q_node_slices(capi, restatement, G, T, slices, dtype):
+@pytest.mark.parametrize("path,tree", [(2, True), (1, True), (1, False)])
+def test_tc_q_node_slices(capi, restatement, G, T, slices, dtype, path, tree):
     """st_attn_args.q_rows / q_node0 (ABI 5): Q, o and lse hold only the nodes
     [u0, u0 + rows) — one level of a draft tree grown level by level — while
     the masks and the tree rows (k_tree) span all T nodes. Every slice vs the
     f64 restatement of the whole tree's rows; ragged n (rows past n[b] are
-    not written)."""
+    not written). Both kernels: the CUDA-core path also slices with the tree
+    rows in the cache (no k_tree)."""
     rng = np.random.default_rng(T + G)
     B, Hkv = 3, 2
     w = 3
@@ -479,8 +481,8 @@ def test_tc_q_node_slices(capi, restatement, G, T, slices, dtype):
         qs = q[:, u0:u1].contiguous()
         out = torch.full_like(qs, 7.0)
         lse = torch.zeros((B, G * Hkv, u1 - u0), dtype=torch.float32, device=dev)
-        capi.tree_attention(qs, kc, vc, mask, P_t, n_t, out=out, lse=lse, force_path=2, k_tree=kt,
-                            v_tree=vt, q_node0=u0)
+        capi.tree_attention(qs, kc, vc, mask, P_t, n_t, out=out, lse=lse, force_path=path,
+                            k_tree=kt if tree else None, v_tree=vt if tree else None, q_node0=u0)
         torch.cuda.synchronize()
         got, L = out.double().cpu().numpy(), lse.double().cpu().numpy()
         for b in range(B):
