@@ -44,10 +44,10 @@ lines = [list(map(int, l.split())) for l in open(out)]
 rows = lines[-17:-1]
 cta = np.array(lines[-1], dtype=np.int64).reshape(-1, 12)
 t = np.array(rows, dtype=np.int64)
-t0 = t[0][t[0] > 0].min()
+t0 = t[0][t[0] > 0].min() if (t[0] > 0).any() else 0
 names = ["K issue", "V issue", "S issue", "PV issue", "S ready", "P done", "K full(mma)", "V full(mma)", "S loaded", "masked+max", "pv wait done", "rescaled"]
 print("tile " + " ".join(f"{x:>12s}" for x in names))
-for i in range(64):
+for i in range(64 if t0 else 0):
     print(f"{i:4d} " + " ".join(f"{(t[r][i] - t0) if t[r][i] else -1:12d}" for r in range(12)))
 print("segment epilogues (cycles rel. to first K load): PV done | (m,l) merged | O stored | end")
 for i in range(64):

@@ -35,15 +35,35 @@ def trees_of(T, seed):
 
 
 def time_k1(args_, iters, path):
-    q, kc, vc, mask, P, n, out, ws = args_
-    for _ in range(3):
+    """Device time per launch. tcgen05: `iters` launches captured in one CUDA
+    graph, alternating two KV copies (each launch streams from HBM: 268 MB+
+    per copy > L2) — eager launches through the Python wrapper are host-bound
+    at 4K (~50 us of host work per call, more than the kernel). CUDA-core
+    (milliseconds per launch): eager."""
+    q, kvs, mask, P, n, out, ws = args_
+
+    def launch(i):
+        kc, vc = kvs[i % len(kvs)]
         _capi.tree_attention(q, kc, vc, mask, P, n, out=out, workspace=ws, force_path=path)
+    for i in range(4):
+        launch(i)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(iters):
-        _capi.tree_attention(q, kc, vc, mask, P, n, out=out, workspace=ws, force_path=path)
-    e1.record()
+    if path == 2:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(iters):
+                launch(i)
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record()
+        g.replay()
+        e1.record()
+    else:
+        e0.record()
+        for i in range(iters):
+            launch(i)
+        e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) * 1e3 / iters
 
@@ -59,8 +79,9 @@ def main():
     dev = "cuda"
     Ls, Ts = [4096, 8192, 16384], [8, 16]
     Lmax = max(Ls) + max(Ts)
-    kc = torch.empty(B, HKV, Lmax, D, dtype=torch.float16, device=dev).uniform_(-1, 1)
-    vc = torch.empty(B, HKV, Lmax, D, dtype=torch.float16, device=dev).uniform_(-1, 1)
+    kvs = [(torch.empty(B, HKV, Lmax, D, dtype=torch.float16, device=dev).uniform_(-1, 1),
+            torch.empty(B, HKV, Lmax, D, dtype=torch.float16, device=dev).uniform_(-1, 1)) for _ in range(2)]
+    kc, vc = kvs[0]
     rows = []
     for T in Ts:
         tb = trees_of(T, T)
@@ -72,10 +93,10 @@ def main():
         for L in Ls:
             P = torch.full((B,), L, dtype=torch.int32, device=dev)
             ws = _capi.tree_attention_workspace(q, kc, vc, mask, P, n)
-            a = (q, kc, vc, mask, P, n, out, ws)
-            us_tc = time_k1(a, args.iters, 2)
+            us_tc = time_k1((q, kvs, mask, P, n, out, ws), 2 * args.iters, 2)
+            _capi.tree_attention(q, kc, vc, mask, P, n, out=out, workspace=ws, force_path=2)
             ref = out.clone()
-            us_cc = time_k1(a, max(2, args.iters // 5), 1)
+            us_cc = time_k1((q, [(kc, vc)], mask, P, n, out, ws), max(2, args.iters // 5), 1)
             err = (out.float() - ref.float()).abs().max().item()
             W = (T + 63) // 64
             byts = 2 * (2 * B * L * HKV * D + B * T * H * D + 2 * B * T * HKV * D + B * T * H * D) \
