@@ -144,3 +144,43 @@ def test_k4_c3_bench_shape(restatement):
         np.testing.assert_array_equal(ids[b, : ln[b]], rids)
         longest = max(longest, len(rv))
     assert longest > 2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("V,width", [(32000, 40), (4099, 36), (2048, 70)])
+def test_k4_wide_nodes(restatement, V, width):
+    """Nodes with more children than K4 prefetches test scalars for (32): the
+    later children's scalars are loaded at test time; long rejection chains
+    (drafts that the target mostly disagrees with) end in the residual
+    sample. Both the float4 (V % 4 == 0) and the scalar slice paths."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2305_09781_b200 import _capi
+    rng = np.random.default_rng(width)
+    trees = []
+    for _ in range(4):
+        root = int(rng.integers(0, V))
+        toks = rng.choice(V, size=width, replace=False)
+        seqs = [[root, int(t), int(rng.integers(0, V))] for t in toks]
+        trees.append(restatement.merge(seqs, 1024))
+    tok, par, dep, n = pack(trees)
+    Bq, T = tok.shape
+    logits = (rng.standard_normal((Bq, T, V)) * 2.0).astype(np.float32)
+    q = softmax(rng.standard_normal((Bq, T, V)).astype(np.float32) * 2.0)
+    for b in range(Bq):
+        for v in range(1, n[b]):
+            q[b, v] *= 0.2
+            q[b, v, tok[b, v]] += 0.8
+    U = rng.uniform(0, 1, (Bq, T + 1)).astype(np.float32)
+    dev = "cuda"
+    ver, ids, ln = _capi.verify_mss(torch.tensor(logits, device=dev), torch.tensor(q, device=dev),
+                                    torch.tensor(tok, device=dev), torch.tensor(par, device=dev),
+                                    torch.tensor(n, device=dev), 1.0, torch.tensor(U, device=dev))
+    ver, ids, ln = ver.cpu().numpy(), ids.cpu().numpy(), ln.cpu().numpy()
+    for b in range(Bq):
+        k = n[b]
+        rv, rids = restatement.mss_verify(logits[b, :k], q[b, :k], tok[b, :k], par[b, :k], 1.0, U[b])
+        assert ln[b] == len(rv)
+        np.testing.assert_array_equal(ver[b, : ln[b]], rv)
+        np.testing.assert_array_equal(ids[b, : ln[b]], rids)
