@@ -25,3 +25,4 @@ timeout 300 python tools/gemm_bench.py > $OUT/$TAG.gemm.txt 2>&1; echo "gemm rc=
 timeout 600 python bench.py --config c3 --steps 5 --warmup 2 > $OUT/$TAG.c3.json 2> $OUT/$TAG.c3.err; echo "c3 rc=$?"
 timeout 600 python bench.py --config c3e > $OUT/$TAG.c3e.json 2> $OUT/$TAG.c3e.err; echo "c3e rc=$?"
 timeout 300 python tools/step_modes.py > $OUT/$TAG.step_modes.txt 2>&1; echo "modes rc=$?"
+timeout 120 python tools/mss_bench.py > $OUT/$TAG.k4.txt 2>&1; echo "k4 rc=$?"
