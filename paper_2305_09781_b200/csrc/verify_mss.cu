@@ -273,7 +273,9 @@ mss_cluster_kernel(const float* __restrict__ logits, const float* __restrict__ q
             __syncwarp();
         }
     }
-    __syncthreads();
+    // (a cluster barrier, not only a CTA one: no CTA writes a peer's shared
+    // memory before every CTA of the cluster has started)
+    cl.sync();
     const float* U = uniforms + (int64_t)b * n_uniforms;
     int32_t* vrow = verified + (int64_t)b * (T + 1);
     int32_t* irow = ids + (int64_t)b * (T + 1);
