@@ -32,6 +32,7 @@ struct TcParams {
     int trace_cta;              // CTA whose per-tile pipeline is traced (ST_K1_TRACE_CTA)
     unsigned long long g_magic; // floor(2^64 / G) + 1, G = schedule slots: exact floor(x / G)
                                 // for x < 2^40 as one 64-bit high multiply
+    int o_tma;                  // `to` is valid: whole-pair last segments store o with one TMA store
     int most_aligned;           // whole pairs when 4G/5 <= pairs <= G (ST_K1_MOST=0: off)
     int cluster2;               // launched as 2-CTA clusters: split pairs of two pieces merge
                                 // over DSMEM (the piece's (O, m, l) copied into the head's
@@ -45,6 +46,7 @@ struct TcParams {
 struct TcLaunch {
     CUtensorMap tq, tk, tv, tkt, tvt;  // one box = both d halves of a tile
     CUtensorMap tk1, tv1, tkt1, tvt1;  // one d half (multicast two-row-block loads)
+    CUtensorMap to;                    // o, same view as tq (TMA-store epilogue)
     TcParams prm;
     int grid;
     bool coop, m64, mw4, f16;

@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(Cfg<M>::THREADS, 1)
 tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_v,
                     const __grid_constant__ CUtensorMap tm_kt, const __grid_constant__ CUtensorMap tm_vt,
-                    const __grid_constant__ TcParams p) {
+                    const __grid_constant__ CUtensorMap tm_o, const __grid_constant__ TcParams p) {
     using C = Cfg<M>;
     constexpr int KS = C::KSTAGES, VS = C::VSTAGES, QS = C::QSTAGES;
     constexpr int SPLIT = C::SPLIT;          // threads per query row in a warp (2 for M=64)
@@ -1400,6 +1400,19 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                 const float w_self = (m == -INFINITY) ? 0.f : ex2((m - m_fin) * c);
                 const float inv = 1.f / l_fin;
                 float* sp = p.partial + (long long)blockIdx.x * SLOT_FLOATS;
+                // TMA-store epilogue: a whole pair that is this CTA's last
+                // segment, every row of its Q box a live node — the rows are
+                // staged (normalised, as the 128-byte-swizzled rows of the Q box
+                // layout) in this segment's Q buffer, free once its last P.V is
+                // done and reloaded by no later segment, and leave with one
+                // tensor store instead of a warp's 32 row-strided stores
+                const int node0 = rblk * (M / p.G);
+                // (M=128 only: measured, GQA T=16 at 4K 52.66 -> 52.30 us; M=64's
+                // two lanes per row already write 256 contiguous bytes, and the
+                // staging barrier cost it 0.3 us at GQA T=8)
+                const bool tma_out = DUAL && p.o_tma && full && t + ntl >= t_end &&
+                                     p.u0 + min(node0 + M / p.G, p.Tq) <= n;
+                uint8_t* stage = sm_q + (segn % QS) * C::A_BYTES;
                 if (warp_live) {
                     tc_fence_after();
     #pragma unroll 1
@@ -1454,7 +1467,19 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                             }
                         }
                         if (threadIdx.x == 0) K1_TRACE(13, 42 + 2 * ch);
-                        if (p.o_peers) {  // fused all-gather: this row into every rank's buffer
+                        if (tma_out) {
+                            uint8_t* rowp = stage + (half * M + r) * 128;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                uint32_t w4[4];
+#pragma unroll
+                                for (int e = 0; e < 4; ++e)
+                                    w4[e] = pk2<T>::pack(ov[8 * j + 2 * e] * inv, ov[8 * j + 2 * e + 1] * inv);
+                                const int cx = ch * 4 + j;  // 16-byte chunk of the row, swizzled
+                                *reinterpret_cast<uint4*>(rowp + ((cx ^ (r & 7)) << 4)) =
+                                    make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                            }
+                        } else if (p.o_peers) {  // fused all-gather: this row into every rank's buffer
                             for (int k = 0; k < p.world; ++k)
                                 store_row<T, 32>(reinterpret_cast<T*>(p.o_peers[k]) + orow + ch * 32, ov, inv);
                         } else {
@@ -1463,6 +1488,15 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         if (threadIdx.x == 0) K1_TRACE(13, 43 + 2 * ch);
                     }
                     tc_fence_before();
+                }
+                if (tma_out) {
+                    fence_proxy_async_smem();  // the staged rows, visible to the tensor store
+                    named_bar_sync(1, SW * 32);
+                    if (threadIdx.x == 0) {
+                        tma_store_5d(&tm_o, stage, 0, s.h * p.G, node0, 0, s.b);
+                        bulk_commit_group();
+                        bulk_wait_group_read0();  // (the CTA's shared memory outlives the read)
+                    }
                 }
                 if (threadIdx.x == 0) K1_TRACE(14, segn);
                 mbar_arrive(o_empty);
@@ -1608,7 +1642,7 @@ st_status launch_tc(const TcLaunch& L, cudaStream_t stream) {
     const bool mc = MM == 128 && L.prm.R == 2 && clus;
     ST_CUDA_TRY(launch_pdl_ex(tree_attn_tc_kernel<TT, MM, MW>, dim3(L.grid), dim3(Cfg<MM>::THREADS),
                               Cfg<MM>::SMEM_BYTES, stream, L.coop, clus ? 2 : 1, L.tq, mc ? L.tk1 : L.tk,
-                              mc ? L.tv1 : L.tv, mc ? L.tkt1 : L.tkt, mc ? L.tvt1 : L.tvt, prm));
+                              mc ? L.tv1 : L.tv, mc ? L.tkt1 : L.tkt, mc ? L.tvt1 : L.tvt, L.to, prm));
     return ST_OK;
 }
 
@@ -1630,6 +1664,12 @@ st_status tree_attention_tc_prepare(const st_attn_args* a, const st_peer_out* po
             set_error("st_tree_attention: cuTensorMapEncodeTiled(q) failed");
             return ST_ERR_CUDA;
         }
+        // o has q's layout (no head-sharded peer output): the same view, so a
+        // staged tile leaves with one TMA store (ST_K1_OTMA=0: per-thread stores)
+        static const bool otma = !(getenv("ST_K1_OTMA") && atoi(getenv("ST_K1_OTMA")) == 0);
+        L->prm.o_tma = otma && !po && a->o && (reinterpret_cast<uintptr_t>(a->o) & 15) == 0 &&
+                       encode(&L->to, dt, 5, a->o, dims, strides, box) ? 1 : 0;
+        if (!L->prm.o_tma) L->to = L->tq;
     }
     {
         // (64, Lmax, 2, B*Hkv): one box = both d halves of a 128-row tile;
