@@ -33,6 +33,7 @@ struct TcParams {
     unsigned long long g_magic; // floor(2^64 / G) + 1, G = schedule slots: exact floor(x / G)
                                 // for x < 2^40 as one 64-bit high multiply
     int o_tma;                  // `to` is valid: whole-pair last segments store o with one TMA store
+    int pre_cap;                // producer fast start: tiles per ring before the CTA barrier (0: the ring)
     int most_aligned;           // whole pairs when 4G/5 <= pairs <= G (ST_K1_MOST=0: off)
     int cluster2;               // launched as 2-CTA clusters: split pairs of two pieces merge
                                 // over DSMEM (the piece's (O, m, l) copied into the head's

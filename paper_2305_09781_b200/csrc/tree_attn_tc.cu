@@ -570,7 +570,8 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
             uint8_t* ring = kside ? sm_k : sm_v;
             const CUtensorMap* mcache = kside ? &tm_k : &tm_v;
             const CUtensorMap* mt = kside ? &tm_kt : &tm_vt;
-            const uint32_t cap = kside ? (uint32_t)KS : (uint32_t)VS;
+            const uint32_t stages = kside ? (uint32_t)KS : (uint32_t)VS;
+            const uint32_t cap = p.pre_cap > 0 && (uint32_t)p.pre_cap < stages ? (uint32_t)p.pre_cap : stages;
             for (int j = s0.lo; j < s0.hi && pre_n < cap &&
                                 (!p.early_kv || (p.tree_src ? j < jt0 : j * BN + BN <= f0.P));
                  ++j, ++pre_n) {
@@ -1744,6 +1745,12 @@ st_status tree_attention_tc_prepare(const st_attn_args* a, const st_peer_out* po
     prm.trace_cta = getenv("ST_K1_TRACE_CTA") ? atoi(getenv("ST_K1_TRACE_CTA")) : 0;
     prm.g_magic = ~0ull / (unsigned long long)(G / R) + 1ull;  // floor(2^64 / slots) + 1
     prm.cluster2 = 0;  // set per launch (launch_tc)
+    // fast start: two tiles per ring before the CTA barrier, not the whole
+    // ring — every CTA's first burst queues less in front of the metadata and
+    // the later issues (measured: 0.2-0.5 % on every K1 shape of
+    // tools/k1_sched_ab.py, three same-box repetitions; ST_K1_PRE=0: the ring)
+    static const int pre_env = getenv("ST_K1_PRE") ? atoi(getenv("ST_K1_PRE")) : 2;
+    prm.pre_cap = pre_env;
     static const int most_env = getenv("ST_K1_MOST") ? atoi(getenv("ST_K1_MOST")) : 1;
     prm.most_aligned = most_env;
     static const bool coop = !(getenv("ST_K1_COOP") && atoi(getenv("ST_K1_COOP")) == 0);
