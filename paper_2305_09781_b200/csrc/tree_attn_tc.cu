@@ -1423,14 +1423,17 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
                         // M=64: this lane's d half of the shared O. DUAL: d half
                         // `half` of both accumulators, weighted.
                         tmem_ld_32x32b_x32(lane_addr + C::O_COL + (DUAL ? half * DCOLS : 0) + ch * 32, raw);
-                        tmem_ld_wait();
-    #pragma unroll
-                        for (int k = 0; k < 32; ++k) ov[k] = __uint_as_float(raw[k]) * wa;
-                        if constexpr (DUAL) {
-                            tmem_ld_32x32b_x32(lane_addr + C::OB_COL + half * DCOLS + ch * 32, raw);
+                        if constexpr (DUAL) {  // both accumulators' loads in flight, one wait
+                            uint32_t rawb[32];
+                            tmem_ld_32x32b_x32(lane_addr + C::OB_COL + half * DCOLS + ch * 32, rawb);
                             tmem_ld_wait();
     #pragma unroll
-                            for (int k = 0; k < 32; ++k) ov[k] += __uint_as_float(raw[k]) * wb;
+                            for (int k = 0; k < 32; ++k)
+                                ov[k] = fmaf(__uint_as_float(rawb[k]), wb, __uint_as_float(raw[k]) * wa);
+                        } else {
+                            tmem_ld_wait();
+    #pragma unroll
+                            for (int k = 0; k < 32; ++k) ov[k] = __uint_as_float(raw[k]) * wa;
                         }
                         if (!valid) continue;
                         const int dc = d0 + ch * 32;
