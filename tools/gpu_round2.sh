@@ -16,7 +16,7 @@ timeout 400 ncu --set full --clock-control none --import-source on -k regex:tree
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:greedy_argmax -s 5 -c 1 \
     -o $OUT/$TAG.k3 -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-strong \
     > /dev/null 2> $OUT/$TAG.ncu3.err; echo "k3 rc=$?"
-timeout 900 python tools/sweep_c5.py --out $OUT/$TAG.c5_sweep.json > $OUT/$TAG.c5_sweep.txt 2>&1; echo "c5 rc=$?"
+timeout 1200 python tools/sweep_c5.py --cool 2 --out $OUT/$TAG.c5_sweep.json > $OUT/$TAG.c5_sweep.txt 2>&1; echo "c5 rc=$?"
 timeout 600 python tools/sweep_gqa.py --out $OUT/$TAG.gqa_sweep.json > $OUT/$TAG.gqa_sweep.txt 2>&1; echo "gqa rc=$?"
 timeout 300 python bench.py --config c4 > $OUT/$TAG.c4.json 2> $OUT/$TAG.c4.err; echo "c4 rc=$?"
 timeout 120 python tools/c4_slice.py --out $OUT/$TAG.c4_slice.json > $OUT/$TAG.c4_slice.txt 2>&1; echo "c4 slice rc=$?"
