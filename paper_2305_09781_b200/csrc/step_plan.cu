@@ -4,6 +4,8 @@
 // programmatic dependent launch, so consecutive steps chain with no boundary
 // between them (a CUDA graph per step pays one: graph replays do not overlap),
 // and K1's tensor maps and schedule parameters are encoded once, not per call.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tree_attn.h"
 
@@ -65,7 +67,13 @@ st_status st_verify_plan_run(st_verify_plan* p, void* stream) {
         if (st_status e = st_tree_attention(&a, stream)) return e;
     }
     const int64_t layer = (int64_t)a.B * a.Hkv * a.Lmax * a.D;
-    return st_verify_greedy_compact(d.logits, a.B, a.T, d.V, d.tokens, d.parent, a.n_nodes,
+    // K1 releases its dependents once past its own griddepcontrol.wait and
+    // nothing it writes is read by the argmax (logits, node counts are step
+    // inputs): the argmax blocks stream the logits on the SMs K1's tail frees
+    // (ST_K3_EARLY=0: wait for K1 first)
+    static const bool early = !(getenv("ST_K3_EARLY") && atoi(getenv("ST_K3_EARLY")) == 0);
+    auto* compact = early && p->tc ? st::verify_greedy_compact_early : st_verify_greedy_compact;
+    return compact(d.logits, a.B, a.T, d.V, d.tokens, d.parent, a.n_nodes,
                                     d.budget, d.eos, nullptr, d.verified, d.ids, d.len,
                                     d.verify_workspace, a.dtype, a.Hkv, a.D, a.Lmax, 1, layer,
                                     a.prefix_len, d.new_prefix_len, a.k_tree, a.v_tree, 0,

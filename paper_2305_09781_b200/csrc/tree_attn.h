@@ -60,4 +60,17 @@ size_t tree_attention_tc_workspace(const st_attn_args* a);
 st_status tree_attention_tc(const st_attn_args* a, cudaStream_t s, const st_peer_out* po = nullptr);
 st_status tree_attention_tc_prepare(const st_attn_args* a, const st_peer_out* po, TcLaunch* out);
 st_status tree_attention_tc_launch(const TcLaunch& l, cudaStream_t s);
+// st_verify_greedy_compact for the step plan: the argmax streams the logits
+// before the previous kernel (K1) completes — it writes neither the logits
+// nor the node counts — and only its key stores wait (griddepcontrol)
+st_status verify_greedy_compact_early(const float* logits, int B, int T, int V, const int32_t*
+                                      tokens,
+                                   const int32_t* parent, const int32_t* n_nodes,
+                                   const int32_t* budget, int32_t eos, int32_t* argmax,
+                                   int32_t* verified, int32_t* ids, int32_t* len, void* workspace,
+                                   st_dtype dtype, int Hkv, int D, int64_t Lmax, int n_layers,
+                                   int64_t layer_stride, const int32_t* prefix_len,
+                                   int32_t* new_prefix_len, const void* k_tree,
+                                   const void* v_tree, int64_t tree_layer_stride, void* k_cache,
+                                   void* v_cache, void* stream);
 }  // namespace st

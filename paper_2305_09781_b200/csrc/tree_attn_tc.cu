@@ -963,6 +963,10 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
         Seg s_next{};
         Meta m_next{};
         if (p.early_kv) pdl_wait();  // masks and lengths below; outputs written later
+        // past this CTA's own wait (either branch above): the next kernel may be
+        // scheduled — it waits for this grid before reading anything K1 writes
+        // (the step plan's argmax streams its logits on the SMs K1's tail frees)
+        pdl_trigger();
         if (t_begin < t_end) {
             s_next = find_seg(p, cum, t_begin, t_end);
             m_next = load_meta(s_next);

@@ -231,12 +231,17 @@ struct WalkArgs {
 __global__ void __launch_bounds__(kThreads)
 greedy_argmax_kernel(const float* __restrict__ logits, int T, int V,
                      const int32_t* __restrict__ n_nodes, unsigned long long* keys,
-                     const WalkArgs wa) {
-    pdl_wait();
+                     const WalkArgs wa, int early) {
+    // early (the step plan): the kernel before this one writes neither the
+    // logits nor the node counts, so the rows stream while it drains and only
+    // the key store waits for it (every block's completion still implies the
+    // previous kernel's, as the launches after this one rely on)
+    if (!early) pdl_wait();
     pdl_trigger();  // let the next kernel get scheduled while the rows stream
     const int part = blockIdx.x, u = blockIdx.y, b = blockIdx.z;
     const int n = n_nodes[b];
     if (u >= n) {
+        if (early) pdl_wait();
         if (wa.counters && n <= 0 && u == 0 && part == 0 && threadIdx.x == 0) wa.len[b] = 0;
         return;
     }
@@ -286,6 +291,7 @@ greedy_argmax_kernel(const float* __restrict__ logits, int T, int V,
     __shared__ bool s_last;
     if (threadIdx.x == 0) {
         for (int w = 1; w < kThreads / 32; ++w) best = max(best, red[w]);
+        if (early) pdl_wait();
         keys[((int64_t)b * T + u) * kSplit + part] = best;
         if (wa.counters) {
             __threadfence();  // the key before the count
@@ -446,13 +452,13 @@ st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32
     if (T <= st::kWalkMax) {  // one launch: the last argmax block of each request walks it
         const st::WalkArgs wa{counters, tokens, parent, budget, eos, argmax, verified, ids, len};
         ST_CUDA_TRY(st::launch_pdl(st::greedy_argmax_kernel, grid, dim3(st::kThreads), 0, strm,
-                                   logits, T, V, n_nodes, keys, wa));
+                                   logits, T, V, n_nodes, keys, wa, 0));
         ST_LAUNCH_CHECK();
         return ST_OK;
     }
     const st::WalkArgs none{};
     ST_CUDA_TRY(st::launch_pdl(st::greedy_argmax_kernel, grid, dim3(st::kThreads), 0, strm, logits,
-                               T, V, n_nodes, keys, none));
+                               T, V, n_nodes, keys, none, 0));
     ST_LAUNCH_CHECK();
     ST_CUDA_TRY(st::launch_pdl(st::greedy_walk_kernel, dim3(B), dim3(32), 0, strm, T, tokens,
                                parent, n_nodes, budget, eos, argmax, keys, scratch, verified, ids,
@@ -461,7 +467,8 @@ st_status st_verify_greedy(const float* logits, int B, int T, int V, const int32
     return ST_OK;
 }
 
-st_status st_verify_greedy_compact(const float* logits, int B, int T, int V, const int32_t* tokens,
+static st_status verify_greedy_compact_impl(const float* logits, int B, int T, int V, const int32_t*
+                                            tokens,
                                    const int32_t* parent, const int32_t* n_nodes,
                                    const int32_t* budget, int32_t eos, int32_t* argmax,
                                    int32_t* verified, int32_t* ids, int32_t* len, void* workspace,
@@ -469,7 +476,7 @@ st_status st_verify_greedy_compact(const float* logits, int B, int T, int V, con
                                    int64_t layer_stride, const int32_t* prefix_len,
                                    int32_t* new_prefix_len, const void* k_tree,
                                    const void* v_tree, int64_t tree_layer_stride, void* k_cache,
-                                   void* v_cache, void* stream) {
+                                   void* v_cache, void* stream, int early) {
     if (st_status e = st::require_device()) return e;
     ST_CHECK_ARG(B >= 0 && T >= 1 && V >= 1 && Hkv >= 1 && D >= 1 && n_layers >= 1,
                  ST_ERR_SHAPE_MISMATCH, "bad shape");
@@ -496,7 +503,7 @@ st_status st_verify_greedy_compact(const float* logits, int B, int T, int V, con
     // follow as a kernel anyway, so it only lengthens the argmax tail)
     const st::WalkArgs none{};
     ST_CUDA_TRY(st::launch_pdl(st::greedy_argmax_kernel, dim3(st::kSplit, T, B), dim3(st::kThreads), 0,
-                               strm, logits, T, V, n_nodes, keys, none));
+                               strm, logits, T, V, n_nodes, keys, none, early));
     ST_LAUNCH_CHECK();
     // heads per block: about 2 KB of K+V per accepted row per block
     const int row_vecs = (int)(row_bytes / 16);
@@ -512,6 +519,21 @@ st_status st_verify_greedy_compact(const float* logits, int B, int T, int V, con
                                (const char*)k_tree, (const char*)v_tree, tree_layer_stride * es, 0));
     ST_LAUNCH_CHECK();
     return ST_OK;
+}
+
+st_status st_verify_greedy_compact(const float* logits, int B, int T, int V, const int32_t* tokens,
+                                   const int32_t* parent, const int32_t* n_nodes,
+                                   const int32_t* budget, int32_t eos, int32_t* argmax,
+                                   int32_t* verified, int32_t* ids, int32_t* len, void* workspace,
+                                   st_dtype dtype, int Hkv, int D, int64_t Lmax, int n_layers,
+                                   int64_t layer_stride, const int32_t* prefix_len,
+                                   int32_t* new_prefix_len, const void* k_tree,
+                                   const void* v_tree, int64_t tree_layer_stride, void* k_cache,
+                                   void* v_cache, void* stream) {
+    return verify_greedy_compact_impl(logits, B, T, V, tokens, parent, n_nodes, budget, eos, argmax,
+                                      verified, ids, len, workspace, dtype, Hkv, D, Lmax, n_layers,
+                                      layer_stride, prefix_len, new_prefix_len, k_tree, v_tree,
+                                      tree_layer_stride, k_cache, v_cache, stream, 0);
 }
 
 st_status st_verify_outputs(const int32_t* outputs, int B, int T, const int32_t* tokens,
@@ -555,3 +577,20 @@ st_status st_build_masks_early(const int32_t* parent, const int32_t* n_nodes, in
 }
 
 }  // extern "C"
+
+namespace st {
+st_status verify_greedy_compact_early(const float* logits, int B, int T, int V, const int32_t* tokens,
+                                   const int32_t* parent, const int32_t* n_nodes,
+                                   const int32_t* budget, int32_t eos, int32_t* argmax,
+                                   int32_t* verified, int32_t* ids, int32_t* len, void* workspace,
+                                   st_dtype dtype, int Hkv, int D, int64_t Lmax, int n_layers,
+                                   int64_t layer_stride, const int32_t* prefix_len,
+                                   int32_t* new_prefix_len, const void* k_tree,
+                                   const void* v_tree, int64_t tree_layer_stride, void* k_cache,
+                                   void* v_cache, void* stream) {
+    return verify_greedy_compact_impl(logits, B, T, V, tokens, parent, n_nodes, budget, eos, argmax,
+                                      verified, ids, len, workspace, dtype, Hkv, D, Lmax, n_layers,
+                                      layer_stride, prefix_len, new_prefix_len, k_tree, v_tree,
+                                      tree_layer_stride, k_cache, v_cache, stream, 1);
+}
+}  // namespace st
