@@ -85,7 +85,11 @@ template <int M> struct Cfg {
     // running (m, l) and their own O accumulator, merged once per segment.
     static constexpr bool DUAL = M == 128;
     static constexpr int SW = M == 64 ? 4 : 8;              // softmax warps
-    static constexpr int THREADS = (SW + 3) * 32;           // + K-TMA, V-TMA, MMA warps
+    // + K-TMA, V-TMA, MMA warps; M=128: + one idle warp, so the three form a
+    // whole warpgroup that hands registers to the two softmax warpgroups
+    // (setmaxnreg: 168 at launch -> 56 / 224; at 168 the M=128 softmax spilled)
+    static constexpr int THREADS = (SW + (M == 128 ? 4 : 3)) * 32;
+    static constexpr uint32_t REG_LOW = 56, REG_HIGH = 224;
     static constexpr int SPLIT = M == 64 ? 2 : 1;           // threads per query row in a warp
     static constexpr uint32_t A_ATOM = M * 128;             // M rows x 64 elems x 2 B
     static constexpr uint32_t A_BYTES = 2 * A_ATOM;         // Q or one P buffer
@@ -645,278 +649,284 @@ tree_attn_tc_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_const
     }
     if (threadIdx.x == 0) K1_TRACE(15, 59);
 
-    if (warp == SW) {
-        // ======================= TMA producer: Q and K =========================
-        if (lane == 0) {
-            // the KV stream is read once (R = 1): evict_first keeps Q, masks and
-            // pieces in L2. With two row blocks (R = 2) both CTAs of a slot read
-            // every tile: normal priority, so the second read finds it in L2.
-            const uint64_t pol = p.R == 1 || mc ? l2_policy_evict_first() : l2_policy_evict_normal();
-            uint32_t qc = 0, kc = 0;
-            bool waited = !p.early_kv;
-            for (uint32_t t = t_begin; t < t_end;) {
-                const bool first = t == t_begin;
-                const Seg s = fast && first ? f0.s : find_seg(p, cum, t, t_end);
-                int j = s.lo;
-                const int jt0 = p.tree_src ? s.ntiles - tree_tiles(p, s) : 1 << 30;  // first tree tile
-                if (first) {  // resume after the fast start's tiles
-                    j += (int)pre_n;
-                    kc = pre_n;
-                }
-                if (!waited) {  // early_kv: up to KS committed-prefix K tiles before the wait
-                    const int P0 = __ldg(p.prefix_len + s.b);
-                    const int bh0 = s.b * p.H + s.h;
-                    for (; j < s.hi && kc < (uint32_t)KS &&
-                           (p.tree_src ? j < jt0 : j * BN + BN <= P0);
-                         ++j, ++kc) {
-                        const uint32_t st = kc;  // first use of each stage: nothing to wait for
-                        mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
-                        load_kv_tile(sm_k + st * TILE_BYTES, k_full + st, &tm_k, &tm_kt, false, j * BN, s.h,
-                                     s.b, bh0, pol, mc, rblk);
-                    }
-                    pdl_wait();
-                    waited = true;
-                }
-                if (!(first && pre_q)) {
-                    const uint32_t qb = qc % QS;
-                    mbar_wait(q_empty + qb, ((qc / QS) & 1) ^ 1);
-                    mbar_arrive_expect_tx(q_full + qb, C::A_BYTES);
-                    // box {64 d, G heads, M/G nodes}: smem row = node * G + head;
-                    // row block rblk starts at node rblk * M / G
-                    const int node0 = rblk * (M / p.G);
-                    tma_load_5d(sm_q + qb * C::A_BYTES, &tm_q, q_full + qb, 0, s.h * p.G, node0, 0, s.b);
-                }
-                ++qc;
-                const int bh = s.b * p.H + s.h;
-                for (; j < s.hi; ++j, ++kc) {
-                    const uint32_t st = kc % KS, ph = (kc / KS) & 1;
-                    mbar_wait(k_empty + st, ph ^ 1);
-                    K1_TRACE(0, kc);
-                    if (kc == 0) K1_GT(5);
-                    mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
-                    // (tree tiles: the tree's own rows [B][T][Hkv][D], 128 nodes per tile)
-                    const bool tr = j >= jt0;
-                    load_kv_tile(sm_k + st * TILE_BYTES, k_full + st, &tm_k, &tm_kt, tr, (tr ? j - jt0 : j) * BN,
-                                 s.h, s.b, bh, pol, mc, rblk);
-                }
-                t += s.hi - s.lo;
-            }
-        }
-        // If this range ends with a pair's head, stage the pair's other pieces
-        // (published by the following CTAs early in their ranges) into the K
-        // ring as soon as the last S MMA has drained it, so the softmax warps'
-        // merge reads shared memory instead of making L2 round trips.
-        if (t_end > t_begin && dsm) {
-            // DSMEM merge of a pair's two pieces on one 2-CTA cluster.
-            //   M=64: the head (rank 0, one tile more) receives the piece's O
-            //   in the first K stage its last tiles free — stage kc % KS once
-            //   S of tile kc - KS is done (or the never-used stage kc) — so the
-            //   piece pushes it while the head still runs its last tile.
-            //   DUAL: both CTAs receive the other's half once the whole ring
-            //   has drained (symmetric exchange).
+    if (warp >= SW) {
+        // producer / MMA warpgroup (M=128: with the idle warp): registers handed
+        // to the softmax warpgroups, each role's code allocated under its limit
+        if constexpr (DUAL) reg_dealloc<C::REG_LOW>();
+        if (warp == SW) {
+            // ======================= TMA producer: Q and K =========================
             if (lane == 0) {
-                const uint32_t kc = (uint32_t)(t_end - t_begin);
-                if constexpr (!DUAL) {
-                    if ((blockIdx.x & 1u) == 0) {
-                        if (kc >= (uint32_t)KS) mbar_wait(k_empty + kc % KS, ((kc - KS) / KS) & 1);
-                        mbar_arrive_expect_tx(xchg_full, 4u * C::PIECE_BOX + 8u * M);
-                        K1_GT(11);
-                        mbar_arrive_cluster(mapa_rank(peer_ready, 1));
+                // the KV stream is read once (R = 1): evict_first keeps Q, masks and
+                // pieces in L2. With two row blocks (R = 2) both CTAs of a slot read
+                // every tile: normal priority, so the second read finds it in L2.
+                const uint64_t pol = p.R == 1 || mc ? l2_policy_evict_first() : l2_policy_evict_normal();
+                uint32_t qc = 0, kc = 0;
+                bool waited = !p.early_kv;
+                for (uint32_t t = t_begin; t < t_end;) {
+                    const bool first = t == t_begin;
+                    const Seg s = fast && first ? f0.s : find_seg(p, cum, t, t_end);
+                    int j = s.lo;
+                    const int jt0 = p.tree_src ? s.ntiles - tree_tiles(p, s) : 1 << 30;  // first tree tile
+                    if (first) {  // resume after the fast start's tiles
+                        j += (int)pre_n;
+                        kc = pre_n;
                     }
-                } else {
-                    for (uint32_t st = 0; st < (uint32_t)KS && st < kc; ++st) {
-                        const uint32_t k = kc - 1 - ((kc - 1 - st) % KS);  // last use of stage st
-                        mbar_wait(k_empty + st, (k / KS) & 1);
+                    if (!waited) {  // early_kv: up to KS committed-prefix K tiles before the wait
+                        const int P0 = __ldg(p.prefix_len + s.b);
+                        const int bh0 = s.b * p.H + s.h;
+                        for (; j < s.hi && kc < (uint32_t)KS &&
+                               (p.tree_src ? j < jt0 : j * BN + BN <= P0);
+                             ++j, ++kc) {
+                            const uint32_t st = kc;  // first use of each stage: nothing to wait for
+                            mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
+                            load_kv_tile(sm_k + st * TILE_BYTES, k_full + st, &tm_k, &tm_kt, false, j * BN, s.h,
+                                         s.b, bh0, pol, mc, rblk);
+                        }
+                        pdl_wait();
+                        waited = true;
                     }
-                    K1_GT(11);
-                    mbar_arrive_cluster(mapa_rank(peer_ready, (blockIdx.x & 1u) ^ 1u));
+                    if (!(first && pre_q)) {
+                        const uint32_t qb = qc % QS;
+                        mbar_wait(q_empty + qb, ((qc / QS) & 1) ^ 1);
+                        mbar_arrive_expect_tx(q_full + qb, C::A_BYTES);
+                        // box {64 d, G heads, M/G nodes}: smem row = node * G + head;
+                        // row block rblk starts at node rblk * M / G
+                        const int node0 = rblk * (M / p.G);
+                        tma_load_5d(sm_q + qb * C::A_BYTES, &tm_q, q_full + qb, 0, s.h * p.G, node0, 0, s.b);
+                    }
+                    ++qc;
+                    const int bh = s.b * p.H + s.h;
+                    for (; j < s.hi; ++j, ++kc) {
+                        const uint32_t st = kc % KS, ph = (kc / KS) & 1;
+                        mbar_wait(k_empty + st, ph ^ 1);
+                        K1_TRACE(0, kc);
+                        if (kc == 0) K1_GT(5);
+                        mbar_arrive_expect_tx(k_full + st, TILE_BYTES);
+                        // (tree tiles: the tree's own rows [B][T][Hkv][D], 128 nodes per tile)
+                        const bool tr = j >= jt0;
+                        load_kv_tile(sm_k + st * TILE_BYTES, k_full + st, &tm_k, &tm_kt, tr, (tr ? j - jt0 : j) * BN,
+                                     s.h, s.b, bh, pol, mc, rblk);
+                    }
+                    t += s.hi - s.lo;
                 }
             }
-        } else if (t_end > t_begin) {
-            const Seg ls = find_seg(p, cum, t_end - 1, t_end);
-            const uint32_t pend = ls.pair_start + (uint32_t)ls.ntiles;
-            if (ls.pair_start >= t_begin && pend > t_end) {
-                const uint32_t kc = (uint32_t)(t_end - t_begin);  // K tiles this CTA loaded
+            // If this range ends with a pair's head, stage the pair's other pieces
+            // (published by the following CTAs early in their ranges) into the K
+            // ring as soon as the last S MMA has drained it, so the softmax warps'
+            // merge reads shared memory instead of making L2 round trips.
+            if (t_end > t_begin && dsm) {
+                // DSMEM merge of a pair's two pieces on one 2-CTA cluster.
+                //   M=64: the head (rank 0, one tile more) receives the piece's O
+                //   in the first K stage its last tiles free — stage kc % KS once
+                //   S of tile kc - KS is done (or the never-used stage kc) — so the
+                //   piece pushes it while the head still runs its last tile.
+                //   DUAL: both CTAs receive the other's half once the whole ring
+                //   has drained (symmetric exchange).
                 if (lane == 0) {
-                    // piece list for the softmax warps; every piece's flag is
-                    // awaited (and re-armed for the next launch) before its
-                    // copy is issued into the drained K ring (the first
-                    // STAGED_PIECES pieces) or, beyond those, before the final
-                    // arrival that releases the softmax warps to read it from L2
-                    // the list and the staged pieces live in the K ring: drain it
-                    for (uint32_t st = 0; st < (uint32_t)KS && st < kc; ++st) {
-                        const uint32_t k = kc - 1 - ((kc - 1 - st) % KS);  // last use of stage st
-                        mbar_wait(k_empty + st, (k / KS) & 1);
+                    const uint32_t kc = (uint32_t)(t_end - t_begin);
+                    if constexpr (!DUAL) {
+                        if ((blockIdx.x & 1u) == 0) {
+                            if (kc >= (uint32_t)KS) mbar_wait(k_empty + kc % KS, ((kc - KS) / KS) & 1);
+                            mbar_arrive_expect_tx(xchg_full, 4u * C::PIECE_BOX + 8u * M);
+                            K1_GT(11);
+                            mbar_arrive_cluster(mapa_rank(peer_ready, 1));
+                        }
+                    } else {
+                        for (uint32_t st = 0; st < (uint32_t)KS && st < kc; ++st) {
+                            const uint32_t k = kc - 1 - ((kc - 1 - st) % KS);  // last use of stage st
+                            mbar_wait(k_empty + st, (k / KS) & 1);
+                        }
+                        K1_GT(11);
+                        mbar_arrive_cluster(mapa_rank(peer_ready, (blockIdx.x & 1u) ^ 1u));
                     }
-                    int* pieces = reinterpret_cast<int*>(smem + C::OFF_PIECES);
-                    int np = 0;
-                    for (uint32_t c2 = slot + 1; c2 < G && np < kMaxPieces; ++c2) {
-                        const uint32_t rs = range_start(c2, sched, G);
-                        if (rs >= pend) break;
-                        if (range_start(c2 + 1, sched, G) == rs) continue;  // empty range
-                        pieces[1 + np++] = (int)(c2 * (uint32_t)p.R) + rblk;  // same row block
+                }
+            } else if (t_end > t_begin) {
+                const Seg ls = find_seg(p, cum, t_end - 1, t_end);
+                const uint32_t pend = ls.pair_start + (uint32_t)ls.ntiles;
+                if (ls.pair_start >= t_begin && pend > t_end) {
+                    const uint32_t kc = (uint32_t)(t_end - t_begin);  // K tiles this CTA loaded
+                    if (lane == 0) {
+                        // piece list for the softmax warps; every piece's flag is
+                        // awaited (and re-armed for the next launch) before its
+                        // copy is issued into the drained K ring (the first
+                        // STAGED_PIECES pieces) or, beyond those, before the final
+                        // arrival that releases the softmax warps to read it from L2
+                        // the list and the staged pieces live in the K ring: drain it
+                        for (uint32_t st = 0; st < (uint32_t)KS && st < kc; ++st) {
+                            const uint32_t k = kc - 1 - ((kc - 1 - st) % KS);  // last use of stage st
+                            mbar_wait(k_empty + st, (k / KS) & 1);
+                        }
+                        int* pieces = reinterpret_cast<int*>(smem + C::OFF_PIECES);
+                        int np = 0;
+                        for (uint32_t c2 = slot + 1; c2 < G && np < kMaxPieces; ++c2) {
+                            const uint32_t rs = range_start(c2, sched, G);
+                            if (rs >= pend) break;
+                            if (range_start(c2 + 1, sched, G) == rs) continue;  // empty range
+                            pieces[1 + np++] = (int)(c2 * (uint32_t)p.R) + rblk;  // same row block
+                        }
+                        pieces[0] = np;
+                        const int ns = np < C::STAGED_PIECES ? np : C::STAGED_PIECES;
+                        mbar_expect_tx(merge_full, (uint32_t)ns * (1024u + 4u * C::PIECE_BOX));
+                        K1_GT(11);
+                        for (int i = 0; i < np; ++i) {
+                            const int c2 = pieces[1 + i];
+                            wait_flag_gpu(p.flags + c2);
+                            p.flags[c2] = 0u;
+                            if (i < ns) {
+                                fence_proxy_async_global();
+                                uint8_t* dst = sm_k + i * C::PIECE_SMEM;
+                                bulk_load(dst, p.partial + (long long)c2 * SLOT_FLOATS + 128 * HD, 1024, merge_full);
+                                bulk_load(dst + 1024, p.partial + (long long)c2 * SLOT_FLOATS, 4 * C::PIECE_BOX, merge_full);
+                            }
+                        }
+                        mbar_arrive(merge_full);
                     }
-                    pieces[0] = np;
-                    const int ns = np < C::STAGED_PIECES ? np : C::STAGED_PIECES;
-                    mbar_expect_tx(merge_full, (uint32_t)ns * (1024u + 4u * C::PIECE_BOX));
-                    K1_GT(11);
-                    for (int i = 0; i < np; ++i) {
-                        const int c2 = pieces[1 + i];
-                        wait_flag_gpu(p.flags + c2);
-                        p.flags[c2] = 0u;
-                        if (i < ns) {
-                            fence_proxy_async_global();
-                            uint8_t* dst = sm_k + i * C::PIECE_SMEM;
-                            bulk_load(dst, p.partial + (long long)c2 * SLOT_FLOATS + 128 * HD, 1024, merge_full);
-                            bulk_load(dst + 1024, p.partial + (long long)c2 * SLOT_FLOATS, 4 * C::PIECE_BOX, merge_full);
+                }
+            }
+        } else if (warp == SW + 1) {
+            // =========================== TMA producer: V ============================
+            if (lane == 0) {
+                const uint64_t pol = p.R == 1 || mc ? l2_policy_evict_first() : l2_policy_evict_normal();
+                uint32_t vc = 0;
+                bool waited = !p.early_kv;
+                for (uint32_t t = t_begin; t < t_end;) {
+                    const bool first = t == t_begin;
+                    const Seg s = fast && first ? f0.s : find_seg(p, cum, t, t_end);
+                    const int bh = s.b * p.H + s.h;
+                    int j = s.lo;
+                    const int jt0 = p.tree_src ? s.ntiles - tree_tiles(p, s) : 1 << 30;  // first tree tile
+                    if (first) {  // resume after the fast start's tiles
+                        j += (int)pre_n;
+                        vc = pre_n;
+                    }
+                    if (!waited) {  // early_kv: up to VS committed-prefix V tiles before the wait
+                        const int P0 = __ldg(p.prefix_len + s.b);
+                        for (; j < s.hi && vc < (uint32_t)VS &&
+                               (p.tree_src ? j < jt0 : j * BN + BN <= P0);
+                             ++j, ++vc) {
+                            const uint32_t st = vc;
+                            mbar_arrive_expect_tx(v_full + st, TILE_BYTES);
+                            load_kv_tile(sm_v + st * TILE_BYTES, v_full + st, &tm_v, &tm_vt, false, j * BN, s.h,
+                                         s.b, bh, pol, mc, rblk);
+                        }
+                        pdl_wait();
+                        waited = true;
+                    }
+                    for (; j < s.hi; ++j, ++vc) {
+                        const uint32_t st = vc % VS, ph = (vc / VS) & 1;
+                        mbar_wait(v_empty + st, ph ^ 1);
+                        K1_TRACE(1, vc);
+                        mbar_arrive_expect_tx(v_full + st, TILE_BYTES);
+                        const bool tr = j >= jt0;
+                        load_kv_tile(sm_v + st * TILE_BYTES, v_full + st, &tm_v, &tm_vt, tr, (tr ? j - jt0 : j) * BN,
+                                     s.h, s.b, bh, pol, mc, rblk);
+                    }
+                    t += s.hi - s.lo;
+                }
+            }
+        } else if (warp == SW + 2) {
+            // ============================ MMA issuer ==============================
+            // M=128: S = Q K^T (N=128); O_a += P[:, 0:64] V[0:64] and
+            //        O_b += P[:, 64:128] V[64:128] (N=128, K=64 each), one
+            //        accumulator per column half of the softmax.
+            // M=64 : every product is split into two N=64 MMAs whose accumulators
+            //        land in TMEM lanes 0-15 and 16-31 of each subpartition (the
+            //        interleaved M=64 layout), so all 32 softmax lanes hold data:
+            //        S kv-rows 0-63 | 64-127 and O d 0-63 | 64-127.
+            // The whole warp runs this loop (uniform control flow); MMAs and
+            // commits are issued by one elected lane inside the asm.
+            constexpr uint32_t fmt = std::is_same<T, __half>::value ? 0u : 1u;
+            constexpr uint32_t NS = BN / SPLIT, NO = HD / SPLIT;
+            constexpr uint32_t idS = idesc_f16(fmt, M, NS, 0, 0);   // Q K^T: both K-major
+            constexpr uint32_t idPV = idesc_f16(fmt, M, NO, 0, 1);  // P V: V is MN-major
+            constexpr uint32_t HI_LANES = 16u << 16;                // lane offset of the 2nd half
+            const uint32_t q_base0 = smem_u32(sm_q), k_base = smem_u32(sm_k);
+            const uint32_t v_base = smem_u32(sm_v);
+            uint32_t qc = 0, kc = 0, vc = 0, sc = 0, pc = 0, segc = 0;
+            auto issue_pv = [&](int i_local) {
+                const uint32_t pb = pc & 1;
+                mbar_wait(p_full + pb, (pc >> 1) & 1);
+                const uint32_t st = vc % VS;
+                mbar_wait(v_full + st, (vc / VS) & 1);
+                K1_TRACE(7, vc);
+                if (i_local == 0) mbar_wait(o_empty, (segc & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t vb = v_base + st * TILE_BYTES;
+                const uint64_t vd = smem_desc(vb, KV_ATOM, 1024);
+                // P of this tile sits in TMEM over its S buffer (K-major, 2 elements
+                // per column: K=16 per MMA = 8 columns). For M=64 each half-lane
+                // group holds the full P rows, matching its O accumulator's lanes.
+                const uint32_t pt = tmem + pb * C::S_COLS;
+    #pragma unroll
+                for (int kk = 0; kk < BN / 16; ++kk) {
+                    const uint32_t acc = (i_local > 0 || (kk & 3) > 0) ? 1u : 0u;
+                    if constexpr (DUAL) {  // half h's P sits at S columns [64h, 64h+32)
+                        const uint32_t h = kk >> 2;
+                        umma_f16_ts_warp(tmem + (h ? C::OB_COL : C::O_COL), pt + h * 64 + (kk & 3) * 8,
+                                         vd + ((kk * 2048) >> 4), idPV, acc);
+                    } else {
+                        const uint32_t acc = (i_local > 0 || kk > 0) ? 1u : 0u;
+                        umma_f16_ts_warp(tmem + C::O_COL, pt + kk * 8, vd + ((kk * 2048) >> 4), idPV, acc);
+                        umma_f16_ts_warp(tmem + HI_LANES + C::O_COL, pt + HI_LANES + kk * 8,
+                                         vd + ((KV_ATOM + kk * 2048) >> 4), idPV, acc);
+                    }
+                }
+                K1_TRACE(3, pc);
+                umma_commit_warp(pv_done + pb);
+                if (mc) umma_commit_warp_mc(v_empty + st, 0x3);
+                else umma_commit_warp(v_empty + st);
+                ++vc;
+                ++pc;
+            };
+            for (uint32_t t = t_begin; t < t_end;) {
+                const Seg s = find_seg(p, cum, t, t_end);
+                const int ntl = s.hi - s.lo;
+                const uint32_t qb = qc % QS;
+                mbar_wait(q_full + qb, (qc / QS) & 1);
+                ++qc;
+                const uint32_t q_base = q_base0 + qb * C::A_BYTES;
+                for (int i = 0; i < ntl; ++i) {
+                    const uint32_t st = kc % KS;
+                    mbar_wait(k_full + st, (kc / KS) & 1);
+                    K1_TRACE(6, kc);
+                    // S buffer sb last held P of tile sc-2, read by the P.V MMA
+                    // issued before this one: tcgen05 MMAs of one thread execute in
+                    // issue order, so no barrier is needed before overwriting it.
+                    const uint32_t sb = sc & 1;
+                    tc_fence_after();
+                    const uint32_t kb = k_base + st * TILE_BYTES;
+                    const uint32_t scol = sb * C::S_COLS;
+                    const uint64_t qd = smem_desc(q_base, 16, 1024), kd = smem_desc(kb, 16, 1024);
+    #pragma unroll
+                    for (int kk = 0; kk < HD / 16; ++kk) {
+                        const uint32_t off = (kk >> 2) * C::A_ATOM + (kk & 3) * 32;
+                        const uint32_t koff = (kk >> 2) * KV_ATOM + (kk & 3) * 32;
+                        const uint64_t a = qd + (off >> 4);
+                        const uint32_t acc = kk > 0 ? 1u : 0u;
+                        if constexpr (SPLIT == 1) {
+                            umma_f16_ss_warp(tmem + scol, a, kd + (koff >> 4), idS, acc);
+                        } else {  // kv rows 0-63 -> lanes 0-15, kv rows 64-127 -> lanes 16-31
+                            umma_f16_ss_warp(tmem + scol, a, kd + (koff >> 4), idS, acc);
+                            umma_f16_ss_warp(tmem + HI_LANES + scol, a,
+                                             kd + ((koff + 64 * 128) >> 4), idS, acc);
                         }
                     }
-                    mbar_arrive(merge_full);
+                    K1_TRACE(2, sc);
+                    umma_commit_warp(s_full + sb);
+                    if (mc) umma_commit_warp_mc(k_empty + st, 0x3);
+                    else umma_commit_warp(k_empty + st);
+                    if (i == ntl - 1) umma_commit_warp(q_empty + qb);
+                    ++kc;
+                    ++sc;
+                    if (i > 0) issue_pv(i - 1);
                 }
+                issue_pv(ntl - 1);
+                ++segc;
+                t += ntl;
             }
-        }
-    } else if (warp == SW + 1) {
-        // =========================== TMA producer: V ============================
-        if (lane == 0) {
-            const uint64_t pol = p.R == 1 || mc ? l2_policy_evict_first() : l2_policy_evict_normal();
-            uint32_t vc = 0;
-            bool waited = !p.early_kv;
-            for (uint32_t t = t_begin; t < t_end;) {
-                const bool first = t == t_begin;
-                const Seg s = fast && first ? f0.s : find_seg(p, cum, t, t_end);
-                const int bh = s.b * p.H + s.h;
-                int j = s.lo;
-                const int jt0 = p.tree_src ? s.ntiles - tree_tiles(p, s) : 1 << 30;  // first tree tile
-                if (first) {  // resume after the fast start's tiles
-                    j += (int)pre_n;
-                    vc = pre_n;
-                }
-                if (!waited) {  // early_kv: up to VS committed-prefix V tiles before the wait
-                    const int P0 = __ldg(p.prefix_len + s.b);
-                    for (; j < s.hi && vc < (uint32_t)VS &&
-                           (p.tree_src ? j < jt0 : j * BN + BN <= P0);
-                         ++j, ++vc) {
-                        const uint32_t st = vc;
-                        mbar_arrive_expect_tx(v_full + st, TILE_BYTES);
-                        load_kv_tile(sm_v + st * TILE_BYTES, v_full + st, &tm_v, &tm_vt, false, j * BN, s.h,
-                                     s.b, bh, pol, mc, rblk);
-                    }
-                    pdl_wait();
-                    waited = true;
-                }
-                for (; j < s.hi; ++j, ++vc) {
-                    const uint32_t st = vc % VS, ph = (vc / VS) & 1;
-                    mbar_wait(v_empty + st, ph ^ 1);
-                    K1_TRACE(1, vc);
-                    mbar_arrive_expect_tx(v_full + st, TILE_BYTES);
-                    const bool tr = j >= jt0;
-                    load_kv_tile(sm_v + st * TILE_BYTES, v_full + st, &tm_v, &tm_vt, tr, (tr ? j - jt0 : j) * BN,
-                                 s.h, s.b, bh, pol, mc, rblk);
-                }
-                t += s.hi - s.lo;
-            }
-        }
-    } else if (warp == SW + 2) {
-        // ============================ MMA issuer ==============================
-        // M=128: S = Q K^T (N=128); O_a += P[:, 0:64] V[0:64] and
-        //        O_b += P[:, 64:128] V[64:128] (N=128, K=64 each), one
-        //        accumulator per column half of the softmax.
-        // M=64 : every product is split into two N=64 MMAs whose accumulators
-        //        land in TMEM lanes 0-15 and 16-31 of each subpartition (the
-        //        interleaved M=64 layout), so all 32 softmax lanes hold data:
-        //        S kv-rows 0-63 | 64-127 and O d 0-63 | 64-127.
-        // The whole warp runs this loop (uniform control flow); MMAs and
-        // commits are issued by one elected lane inside the asm.
-        constexpr uint32_t fmt = std::is_same<T, __half>::value ? 0u : 1u;
-        constexpr uint32_t NS = BN / SPLIT, NO = HD / SPLIT;
-        constexpr uint32_t idS = idesc_f16(fmt, M, NS, 0, 0);   // Q K^T: both K-major
-        constexpr uint32_t idPV = idesc_f16(fmt, M, NO, 0, 1);  // P V: V is MN-major
-        constexpr uint32_t HI_LANES = 16u << 16;                // lane offset of the 2nd half
-        const uint32_t q_base0 = smem_u32(sm_q), k_base = smem_u32(sm_k);
-        const uint32_t v_base = smem_u32(sm_v);
-        uint32_t qc = 0, kc = 0, vc = 0, sc = 0, pc = 0, segc = 0;
-        auto issue_pv = [&](int i_local) {
-            const uint32_t pb = pc & 1;
-            mbar_wait(p_full + pb, (pc >> 1) & 1);
-            const uint32_t st = vc % VS;
-            mbar_wait(v_full + st, (vc / VS) & 1);
-            K1_TRACE(7, vc);
-            if (i_local == 0) mbar_wait(o_empty, (segc & 1) ^ 1);
-            tc_fence_after();
-            const uint32_t vb = v_base + st * TILE_BYTES;
-            const uint64_t vd = smem_desc(vb, KV_ATOM, 1024);
-            // P of this tile sits in TMEM over its S buffer (K-major, 2 elements
-            // per column: K=16 per MMA = 8 columns). For M=64 each half-lane
-            // group holds the full P rows, matching its O accumulator's lanes.
-            const uint32_t pt = tmem + pb * C::S_COLS;
-#pragma unroll
-            for (int kk = 0; kk < BN / 16; ++kk) {
-                const uint32_t acc = (i_local > 0 || (kk & 3) > 0) ? 1u : 0u;
-                if constexpr (DUAL) {  // half h's P sits at S columns [64h, 64h+32)
-                    const uint32_t h = kk >> 2;
-                    umma_f16_ts_warp(tmem + (h ? C::OB_COL : C::O_COL), pt + h * 64 + (kk & 3) * 8,
-                                     vd + ((kk * 2048) >> 4), idPV, acc);
-                } else {
-                    const uint32_t acc = (i_local > 0 || kk > 0) ? 1u : 0u;
-                    umma_f16_ts_warp(tmem + C::O_COL, pt + kk * 8, vd + ((kk * 2048) >> 4), idPV, acc);
-                    umma_f16_ts_warp(tmem + HI_LANES + C::O_COL, pt + HI_LANES + kk * 8,
-                                     vd + ((KV_ATOM + kk * 2048) >> 4), idPV, acc);
-                }
-            }
-            K1_TRACE(3, pc);
-            umma_commit_warp(pv_done + pb);
-            if (mc) umma_commit_warp_mc(v_empty + st, 0x3);
-            else umma_commit_warp(v_empty + st);
-            ++vc;
-            ++pc;
-        };
-        for (uint32_t t = t_begin; t < t_end;) {
-            const Seg s = find_seg(p, cum, t, t_end);
-            const int ntl = s.hi - s.lo;
-            const uint32_t qb = qc % QS;
-            mbar_wait(q_full + qb, (qc / QS) & 1);
-            ++qc;
-            const uint32_t q_base = q_base0 + qb * C::A_BYTES;
-            for (int i = 0; i < ntl; ++i) {
-                const uint32_t st = kc % KS;
-                mbar_wait(k_full + st, (kc / KS) & 1);
-                K1_TRACE(6, kc);
-                // S buffer sb last held P of tile sc-2, read by the P.V MMA
-                // issued before this one: tcgen05 MMAs of one thread execute in
-                // issue order, so no barrier is needed before overwriting it.
-                const uint32_t sb = sc & 1;
-                tc_fence_after();
-                const uint32_t kb = k_base + st * TILE_BYTES;
-                const uint32_t scol = sb * C::S_COLS;
-                const uint64_t qd = smem_desc(q_base, 16, 1024), kd = smem_desc(kb, 16, 1024);
-#pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * C::A_ATOM + (kk & 3) * 32;
-                    const uint32_t koff = (kk >> 2) * KV_ATOM + (kk & 3) * 32;
-                    const uint64_t a = qd + (off >> 4);
-                    const uint32_t acc = kk > 0 ? 1u : 0u;
-                    if constexpr (SPLIT == 1) {
-                        umma_f16_ss_warp(tmem + scol, a, kd + (koff >> 4), idS, acc);
-                    } else {  // kv rows 0-63 -> lanes 0-15, kv rows 64-127 -> lanes 16-31
-                        umma_f16_ss_warp(tmem + scol, a, kd + (koff >> 4), idS, acc);
-                        umma_f16_ss_warp(tmem + HI_LANES + scol, a,
-                                         kd + ((koff + 64 * 128) >> 4), idS, acc);
-                    }
-                }
-                K1_TRACE(2, sc);
-                umma_commit_warp(s_full + sb);
-                if (mc) umma_commit_warp_mc(k_empty + st, 0x3);
-                else umma_commit_warp(k_empty + st);
-                if (i == ntl - 1) umma_commit_warp(q_empty + qb);
-                ++kc;
-                ++sc;
-                if (i > 0) issue_pv(i - 1);
-            }
-            issue_pv(ntl - 1);
-            ++segc;
-            t += ntl;
-        }
+        }  // (warp SW + 3, M=128: idle — it completes the producers' warpgroup)
     } else {
+        if constexpr (DUAL) reg_alloc<C::REG_HIGH>();
         // ===================== softmax + epilogue (warps 0..SW-1) ==================
         // Thread (warp w, lane t) reads TMEM lane 32(w%4)+t and owns column half
         // `half` of its row's kv tile (S) and of d (output). M=64: row

@@ -5,7 +5,7 @@ import sys
 d = collections.defaultdict(list)
 order = []
 for line in sys.stdin:
-    if " us " not in line:
+    if " us " not in line or "]" not in line:
         continue
     v = line.split()[0]
     head = line[:line.index(" us")]
